@@ -1,0 +1,568 @@
+// FFMA (SIMT) kernels of the LoRS layer.
+//
+// These are the fp32 parity-mode path (TF32 fails the 1e-4 bar,
+// FFMA does not) plus the small utility kernels shared by both dtypes
+// (mask packing, 2:4 compression, effective weight, dbias).  The bf16 hot
+// path lives in lors_tc.cu (tcgen05/TMA/TMEM).
+//
+// Reference semantics: lors_forward / lors_backward adapters.py:359-406,
+// _sqft_grads adapters.py:303-312, merged_weight adapters.py:214-224.
+
+#include "lors_common.cuh"
+#include "lors_simt.cuh"
+
+namespace lors {
+
+// ===========================================================================
+// S1: GEMM with the effective weight rebuilt in the tile prologue.
+//
+//   FWD : out[l, m] = sum_k act[l, k] * Weff[m, k]   (act = X_t, m over R, k over C)
+//   DX  : out[l, m] = sum_k act[l, k] * Weff[k, m]   (act = dY_t, m over C, k over R)
+//
+// Weff(row, col) = select(M, W + alpha * sum_j a[row, j] b[j, col], 0).
+// The "fixed" adapter factor (a rows for FWD, b columns for DX) is staged in
+// shared memory once per block; the "streamed" one per k-tile.  W_eff lives
+// only in shared memory.
+// Block tile 128 (m) x 128 (l), BK = 8, 256 threads, 8x8 outputs per thread.
+// ===========================================================================
+namespace {
+constexpr int BM = 128, BL = 128, BK = 8, NT = 256;
+}
+
+template <typename T, bool DX>
+__global__ void __launch_bounds__(NT) simt_lors_gemm_kernel(
+    const T* __restrict__ act, const T* __restrict__ w, const uint32_t* __restrict__ bits,
+    const T* __restrict__ a, const T* __restrict__ b, const T* __restrict__ bias,
+    T* __restrict__ out, int L, int R, int C, int r, float alpha) {
+  extern __shared__ float smem[];
+  // fixed factor F[j][m] (r x BM), streamed factor S[k][j] (BK x r),
+  // act tile sA[k][l] (BK x BL), weight tile sW[k][m] (BK x BM)
+  float* sF = smem;
+  float* sS = sF + (size_t)r * BM;
+  float* sA = sS + (size_t)BK * r;
+  float* sW = sA + BK * BL;
+
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.x * BM;
+  const int l0 = blockIdx.y * BL;
+  const int M = DX ? C : R;   // output feature count
+  const int K = DX ? R : C;   // reduction length
+  const int64_t words = (C + 31) / 32;
+
+  // stage the fixed factor once: FWD F[j][m] = a[m0+m, j]; DX F[j][m] = b[j, m0+m]
+  for (int i = tid; i < r * BM; i += NT) {
+    int j, m;
+    float v = 0.f;
+    if (DX) {
+      j = i / BM; m = i % BM;
+      if (m0 + m < M) v = to_f(b[(int64_t)j * C + m0 + m]);
+    } else {
+      m = i / r; j = i % r;
+      if (m0 + m < M) v = to_f(a[(int64_t)(m0 + m) * r + j]);
+    }
+    sF[j * BM + m] = v;
+  }
+
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+  const int tx = tid % 16, ty = tid / 16;
+  // weight-tile ownership for the prologue: one m, 4 consecutive k
+  const int pm = tid % BM, pk = (tid / BM) * 4;
+
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    __syncthreads();
+    // streamed factor: FWD S[k][j] = b[j, k0+k]; DX S[k][j] = a[k0+k, j]
+    for (int i = tid; i < BK * r; i += NT) {
+      int k, j;
+      float v = 0.f;
+      if (DX) {
+        k = i / r; j = i % r;
+        if (k0 + k < K) v = to_f(a[(int64_t)(k0 + k) * r + j]);
+      } else {
+        j = i / BK; k = i % BK;
+        if (k0 + k < K) v = to_f(b[(int64_t)j * C + k0 + k]);
+      }
+      sS[k * r + j] = v;
+    }
+    // activation tile, transposed into sA[k][l]
+    for (int i = tid; i < BK * BL; i += NT) {
+      int l = i / BK, k = i % BK;
+      float v = 0.f;
+      if (l0 + l < L && k0 + k < K) v = to_f(act[(int64_t)(l0 + l) * K + k0 + k]);
+      sA[k * BL + l] = v;
+    }
+    __syncthreads();
+    // prologue: rebuild W_eff for this k-tile
+    {
+      const int gm = m0 + pm;
+      float p[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int j = 0; j < r; ++j) {
+        float f = sF[j * BM + pm];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) p[q] = fmaf(f, sS[(pk + q) * r + j], p[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int gk = k0 + pk + q;
+        float v = 0.f;
+        if (gm < M && gk < K) {
+          const int64_t row = DX ? gk : gm, col = DX ? gm : gk;
+          const T wv = w[row * C + col];
+          v = round_to<T>(weff_value(mask_at(wv, bits, words, row, col), to_f(wv), p[q], alpha));
+        }
+        sW[(pk + q) * BM + pm] = v;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      float av[8], wv[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        av[i] = sA[k * BL + ty * 4 + i];
+        av[4 + i] = sA[k * BL + 64 + ty * 4 + i];
+        wv[i] = sW[k * BM + tx * 4 + i];
+        wv[4 + i] = sW[k * BM + 64 + tx * 4 + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], wv[j], acc[i][j]);
+    }
+  }
+  // epilogue: out[l, m] (+ bias[m] for the forward)
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int l = l0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+    if (l >= L) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int m = m0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+      if (m >= M) continue;
+      float v = acc[i][j];
+      if (!DX && bias != nullptr) v += to_f(bias[m]);
+      out[(int64_t)l * M + m] = from_f<T>(v);
+    }
+  }
+}
+
+template <typename T>
+int simt_lors_gemm(bool dx, const T* act, const T* w, const uint32_t* bits, const T* a, const T* b,
+                   const T* bias, T* out, int L, int R, int C, int r, float alpha, cudaStream_t s) {
+  const int M = dx ? C : R;
+  dim3 grid((unsigned)ceil_div(M, BM), (unsigned)ceil_div(L, BL));
+  size_t smem = sizeof(float) * ((size_t)r * BM + (size_t)BK * r + BK * BL + BK * BM);
+  auto kern = dx ? simt_lors_gemm_kernel<T, true> : simt_lors_gemm_kernel<T, false>;
+  LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                "simt_lors_gemm smem attribute");
+  kern<<<grid, NT, smem, s>>>(act, w, bits, a, b, bias, out, L, R, C, r, alpha);
+  LORS_CHECK_LAUNCH("simt_lors_gemm");
+  return LORS_OK;
+}
+
+// ===========================================================================
+// S2: strided "skinny" GEMM for the rank-r products (P, Q, dA, dB):
+//   out[m*som + n*son] (= or +=) alpha * sum_k A[m*sam + k*sak] * B[n*sbn + k*sbk]
+// 64x64 tiles, BK = 16, 256 threads, 4x4 per thread; gridDim.z splits K and
+// accumulates with atomicAdd into a zeroed fp32 output.
+// ===========================================================================
+template <typename TA, typename TB, typename TO>
+__global__ void __launch_bounds__(256) simt_strided_gemm_kernel(
+    const TA* __restrict__ A, int64_t sam, int64_t sak, const TB* __restrict__ B, int64_t sbn,
+    int64_t sbk, TO* __restrict__ out, int64_t som, int64_t son, int M, int N, int K,
+    int k_per_split, float alpha, int atomic_out) {
+  __shared__ float sA[16][64 + 4];
+  __shared__ float sB[16][64 + 4];
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.x * 64, n0 = blockIdx.y * 64;
+  const int kbeg = blockIdx.z * k_per_split;
+  const int kend = min(K, kbeg + k_per_split);
+  const int tx = tid % 16, ty = tid / 16;
+  float acc[4][4] = {};
+  for (int k0 = kbeg; k0 < kend; k0 += 16) {
+    for (int i = tid; i < 16 * 64; i += 256) {
+      int m, k;
+      if (sak == 1) { k = i % 16; m = i / 16; } else { m = i % 64; k = i / 64; }
+      float v = 0.f;
+      if (m0 + m < M && k0 + k < kend) v = to_f(A[(int64_t)(m0 + m) * sam + (int64_t)(k0 + k) * sak]);
+      sA[k][m] = v;
+      int n;
+      if (sbk == 1) { k = i % 16; n = i / 16; } else { n = i % 64; k = i / 64; }
+      v = 0.f;
+      if (n0 + n < N && k0 + k < kend) v = to_f(B[(int64_t)(n0 + n) * sbn + (int64_t)(k0 + k) * sbk]);
+      sB[k][n] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { av[i] = sA[k][ty * 4 + i]; bv[i] = sB[k][tx * 4 + i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= N) continue;
+      TO* dst = out + (int64_t)m * som + (int64_t)n * son;
+      const float v = alpha * acc[i][j];
+      if (atomic_out) atomicAdd(reinterpret_cast<float*>(dst), v);
+      else *dst = from_f<TO>(v);
+    }
+  }
+}
+
+template <typename TA, typename TB, typename TO>
+int simt_strided_gemm(const TA* A, int64_t sam, int64_t sak, const TB* B, int64_t sbn, int64_t sbk,
+                      TO* out, int64_t som, int64_t son, int M, int N, int K, float alpha,
+                      bool allow_split, cudaStream_t s) {
+  const int tiles = (int)(ceil_div(M, 64) * ceil_div(N, 64));
+  int split = 1;
+  if (allow_split && sizeof(TO) == sizeof(float)) {
+    split = (int)ceil_div(296, tiles);
+    split = max(1, min(split, (int)ceil_div(K, 256)));
+  }
+  int kps = (int)(ceil_div(ceil_div(K, split), 16) * 16);
+  split = (int)ceil_div(K, kps);
+  if (split > 1) {
+    // atomic accumulation requires a zeroed fp32, densely addressed output
+    LORS_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)M * N, s), "zero split-K output");
+  }
+  dim3 grid((unsigned)ceil_div(M, 64), (unsigned)ceil_div(N, 64), (unsigned)split);
+  simt_strided_gemm_kernel<TA, TB, TO><<<grid, 256, 0, s>>>(A, sam, sak, B, sbn, sbk, out, som, son, M, N, K,
+                                                            kps, alpha, split > 1 ? 1 : 0);
+  LORS_CHECK_LAUNCH("simt_strided_gemm");
+  return LORS_OK;
+}
+
+// ===========================================================================
+// S3: masked-gradient fused kernel (north_star 3, SIMT form for fp32 mode).
+// Each block forms one G tile = (dY^T X)[64 rows of R x 64 cols of C] over
+// all L tokens in registers, masks it, parks it in shared memory and
+// contracts it immediately:  dA[n, :] += alpha G b^T,  dB[:, c] += alpha a^T G.
+// G never reaches HBM.  Oracle: _sqft_grads adapters.py:303-312.
+// ===========================================================================
+template <typename T>
+__global__ void __launch_bounds__(256) simt_masked_grad_kernel(
+    const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ w,
+    const uint32_t* __restrict__ bits, const T* __restrict__ a, const T* __restrict__ b,
+    float* __restrict__ da, float* __restrict__ db, int L, int R, int C, int r, float alpha) {
+  __shared__ float sA[16][64 + 4];
+  __shared__ float sB[16][64 + 4];
+  __shared__ float sG[64][64 + 1];
+  const int tid = threadIdx.x;
+  const int n0 = blockIdx.x * 64, c0 = blockIdx.y * 64;
+  const int tx = tid % 16, ty = tid / 16;
+  const int64_t words = (C + 31) / 32;
+  float acc[4][4] = {};
+  for (int l0 = 0; l0 < L; l0 += 16) {
+    for (int i = tid; i < 16 * 64; i += 256) {
+      const int mm = i % 64, k = i / 64;
+      float v = 0.f;
+      if (n0 + mm < R && l0 + k < L) v = to_f(dy[(int64_t)(l0 + k) * R + n0 + mm]);
+      sA[k][mm] = v;
+      v = 0.f;
+      if (c0 + mm < C && l0 + k < L) v = to_f(x[(int64_t)(l0 + k) * C + c0 + mm]);
+      sB[k][mm] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { av[i] = sA[k][ty * 4 + i]; bv[i] = sB[k][tx * 4 + i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  // mask in registers, park in shared memory
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + ty * 4 + i, c = c0 + tx * 4 + j;
+      float g = 0.f;
+      if (n < R && c < C) {
+        const T wv = w[(int64_t)n * C + c];
+        g = mask_at(wv, bits, words, n, c) ? acc[i][j] : 0.f;
+      }
+      sG[ty * 4 + i][tx * 4 + j] = g;
+    }
+  __syncthreads();
+  // dA[n, j] += alpha * sum_c G[n, c] b[j, c]
+  for (int i = tid; i < 64 * r; i += 256) {
+    const int nn = i / r, j = i % r;
+    if (n0 + nn >= R) continue;
+    float s = 0.f;
+    for (int cc = 0; cc < 64 && c0 + cc < C; ++cc) s = fmaf(sG[nn][cc], to_f(b[(int64_t)j * C + c0 + cc]), s);
+    atomicAdd(da + (int64_t)(n0 + nn) * r + j, alpha * s);
+  }
+  // dB[j, c] += alpha * sum_n a[n, j] G[n, c]
+  for (int i = tid; i < 64 * r; i += 256) {
+    const int cc = i % 64, j = i / 64;
+    if (c0 + cc >= C) continue;
+    float s = 0.f;
+    for (int nn = 0; nn < 64 && n0 + nn < R; ++nn) s = fmaf(to_f(a[(int64_t)(n0 + nn) * r + j]), sG[nn][cc], s);
+    atomicAdd(db + (int64_t)j * C + c0 + cc, alpha * s);
+  }
+}
+
+template <typename T>
+int simt_masked_grad(const T* dy, const T* x, const T* w, const uint32_t* bits, const T* a,
+                     const T* b, float* da, float* db, int L, int R, int C, int r, float alpha,
+                     cudaStream_t s) {
+  LORS_CUDA_TRY(cudaMemsetAsync(da, 0, sizeof(float) * (size_t)R * r, s), "zero dA");
+  LORS_CUDA_TRY(cudaMemsetAsync(db, 0, sizeof(float) * (size_t)r * C, s), "zero dB");
+  dim3 grid((unsigned)ceil_div(R, 64), (unsigned)ceil_div(C, 64));
+  simt_masked_grad_kernel<T><<<grid, 256, 0, s>>>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha);
+  LORS_CHECK_LAUNCH("simt_masked_grad");
+  return LORS_OK;
+}
+
+// ===========================================================================
+// utility kernels (both dtypes)
+// ===========================================================================
+
+// dbias[n] = sum_l dY_t[l, n]   (reduce_sum_rows, adapters.py:402)
+template <typename T>
+__global__ void colsum_kernel(const T* __restrict__ dy, float* __restrict__ out, int L, int R) {
+  const int n = blockIdx.x * 32 + threadIdx.x;
+  const int part = threadIdx.y;  // 8 partial sums over L
+  __shared__ float red[8][33];
+  float s = 0.f;
+  if (n < R)
+    for (int l = part; l < L; l += 8) s += to_f(dy[(int64_t)l * R + n]);
+  red[part][threadIdx.x] = s;
+  __syncthreads();
+  if (part == 0 && n < R) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[i][threadIdx.x];
+    out[n] = t;
+  }
+}
+
+template <typename T>
+int colsum(const T* dy, float* out, int L, int R, cudaStream_t s) {
+  colsum_kernel<T><<<(unsigned)ceil_div(R, 32), dim3(32, 8), 0, s>>>(dy, out, L, R);
+  LORS_CHECK_LAUNCH("colsum");
+  return LORS_OK;
+}
+
+// out[n, c] = select(M, W + alpha * (a b)[n, c], +0) -- merged_weight / merge
+template <typename T>
+__global__ void effective_weight_kernel(const T* __restrict__ w, const uint32_t* __restrict__ bits,
+                                        const T* __restrict__ a, const T* __restrict__ b,
+                                        T* __restrict__ out, int R, int C, int r, float alpha) {
+  extern __shared__ float sa[];  // 4 rows of a
+  const int n0 = blockIdx.y * 4;
+  for (int i = threadIdx.x; i < 4 * r; i += blockDim.x) {
+    const int nn = i / r;
+    sa[i] = (n0 + nn < R) ? to_f(a[(int64_t)(n0 + nn) * r + i % r]) : 0.f;
+  }
+  __syncthreads();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const int64_t words = (C + 31) / 32;
+  float p[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int j = 0; j < r; ++j) {
+    const float bv = to_f(b[(int64_t)j * C + c]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) p[q] = fmaf(sa[q * r + j], bv, p[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int n = n0 + q;
+    if (n >= R) break;
+    const T wv = w[(int64_t)n * C + c];
+    out[(int64_t)n * C + c] = from_f<T>(weff_value(mask_at(wv, bits, words, n, c), to_f(wv), p[q], alpha));
+  }
+}
+
+template <typename T>
+int effective_weight(const T* w, const uint32_t* bits, const T* a, const T* b, T* out, int R, int C,
+                     int r, float alpha, cudaStream_t s) {
+  dim3 grid((unsigned)ceil_div(C, 256), (unsigned)ceil_div(R, 4));
+  effective_weight_kernel<T><<<grid, 256, sizeof(float) * 4 * r, s>>>(w, bits, a, b, out, R, C, r, alpha);
+  LORS_CHECK_LAUNCH("effective_weight");
+  return LORS_OK;
+}
+
+// bits[n, k] : bit j = (W[n, 32k + j] != 0), one warp ballot per word
+template <typename T>
+__global__ void pack_mask_kernel(const T* __restrict__ w, uint32_t* __restrict__ bits, int R, int C) {
+  const int64_t words = (C + 31) / 32;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;  // global word
+  if (gw >= (int64_t)R * words) return;
+  const int64_t n = gw / words, k = gw % words;
+  const int lane = threadIdx.x & 31;
+  const int64_t c = k * 32 + lane;
+  const bool nz = c < C && to_f(w[n * C + c]) != 0.0f;
+  const uint32_t word = __ballot_sync(0xffffffffu, nz);
+  if (lane == 0) bits[gw] = word;
+}
+
+template <typename T>
+int pack_mask(const T* w, uint32_t* bits, int R, int C, cudaStream_t s) {
+  const int64_t words = (int64_t)R * ceil_div(C, 32);
+  pack_mask_kernel<T><<<(unsigned)ceil_div(words, 8), 256, 0, s>>>(w, bits, R, C);
+  LORS_CHECK_LAUNCH("pack_mask");
+  return LORS_OK;
+}
+
+// 2:4 compression: per group of 4 along C keep the (<= 2) nonzero positions.
+// Groups with fewer than 2 nonzeros are padded with zero-valued positions
+// (lowest unused index first); groups with more set *invalid.
+template <typename T>
+__global__ void compress24_kernel(const T* __restrict__ w, T* __restrict__ vals, uint8_t* __restrict__ meta,
+                                  int32_t* __restrict__ invalid, int R, int C) {
+  const int64_t pair = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // two groups per thread
+  const int64_t pairs_per_row = C / 8;
+  if (pair >= (int64_t)R * pairs_per_row) return;
+  const int64_t n = pair / pairs_per_row, gp = pair % pairs_per_row;
+  uint8_t byte = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t c0 = gp * 8 + h * 4;
+    int idx[2] = {-1, -1};
+    int cnt = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (to_f(w[n * C + c0 + q]) != 0.0f) {
+        if (cnt < 2) idx[cnt] = q;
+        ++cnt;
+      }
+    }
+    if (cnt > 2 && invalid != nullptr) *invalid = 1;
+    // pad with unused positions
+    for (int q = 0; q < 4 && (idx[0] < 0 || idx[1] < 0); ++q) {
+      if (q == idx[0] || q == idx[1]) continue;
+      if (idx[0] < 0) idx[0] = q;
+      else if (idx[1] < 0) idx[1] = q;
+    }
+    if (idx[0] > idx[1]) { int t = idx[0]; idx[0] = idx[1]; idx[1] = t; }
+    vals[n * (C / 2) + (c0 / 2)] = w[n * C + c0 + idx[0]];
+    vals[n * (C / 2) + (c0 / 2) + 1] = w[n * C + c0 + idx[1]];
+    byte |= (uint8_t)((idx[0] | (idx[1] << 2)) << (4 * h));
+  }
+  meta[n * (C / 8) + gp] = byte;
+}
+
+template <typename T>
+int compress24(const T* w, T* vals, uint8_t* meta, int32_t* invalid, int R, int C, cudaStream_t s) {
+  const int64_t pairs = (int64_t)R * (C / 8);
+  compress24_kernel<T><<<(unsigned)ceil_div(pairs, 256), 256, 0, s>>>(w, vals, meta, invalid, R, C);
+  LORS_CHECK_LAUNCH("compress24");
+  return LORS_OK;
+}
+
+// dW = dY_t^T X_t (optionally masked), the probe gradient of gradient-SVD init
+template <typename T>
+__global__ void __launch_bounds__(256) grad_outer_kernel(const T* __restrict__ dy, const T* __restrict__ x,
+                                                         const T* __restrict__ w, float* __restrict__ dw,
+                                                         int L, int R, int C, int masked) {
+  __shared__ float sA[16][64 + 4];
+  __shared__ float sB[16][64 + 4];
+  const int tid = threadIdx.x;
+  const int n0 = blockIdx.x * 64, c0 = blockIdx.y * 64;
+  const int tx = tid % 16, ty = tid / 16;
+  float acc[4][4] = {};
+  for (int l0 = 0; l0 < L; l0 += 16) {
+    for (int i = tid; i < 16 * 64; i += 256) {
+      const int mm = i % 64, k = i / 64;
+      sA[k][mm] = (n0 + mm < R && l0 + k < L) ? to_f(dy[(int64_t)(l0 + k) * R + n0 + mm]) : 0.f;
+      sB[k][mm] = (c0 + mm < C && l0 + k < L) ? to_f(x[(int64_t)(l0 + k) * C + c0 + mm]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(sA[k][ty * 4 + i], sB[k][tx * 4 + j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + ty * 4 + i, c = c0 + tx * 4 + j;
+      if (n >= R || c >= C) continue;
+      float g = acc[i][j];
+      if (masked && to_f(w[(int64_t)n * C + c]) == 0.0f) g = 0.f;
+      dw[(int64_t)n * C + c] = g;
+    }
+}
+
+template <typename T>
+int grad_outer(const T* dy, const T* x, const T* w, float* dw, int L, int R, int C, int masked, cudaStream_t s) {
+  dim3 grid((unsigned)ceil_div(R, 64), (unsigned)ceil_div(C, 64));
+  grad_outer_kernel<T><<<grid, 256, 0, s>>>(dy, x, w, dw, L, R, C, masked);
+  LORS_CHECK_LAUNCH("grad_outer");
+  return LORS_OK;
+}
+
+// negate in place (negative-control fault injection)
+__global__ void negate_kernel(float* p, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = -p[i];
+}
+int negate_f32(float* p, int64_t n, cudaStream_t s) {
+  negate_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(p, n);
+  LORS_CHECK_LAUNCH("negate");
+  return LORS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// explicit instantiations
+// ---------------------------------------------------------------------------
+#define LORS_INST(T)                                                                                       \
+  template int simt_lors_gemm<T>(bool, const T*, const T*, const uint32_t*, const T*, const T*, const T*, \
+                                 T*, int, int, int, int, float, cudaStream_t);                            \
+  template int simt_masked_grad<T>(const T*, const T*, const T*, const uint32_t*, const T*, const T*,     \
+                                   float*, float*, int, int, int, int, float, cudaStream_t);              \
+  template int colsum<T>(const T*, float*, int, int, cudaStream_t);                                       \
+  template int effective_weight<T>(const T*, const uint32_t*, const T*, const T*, T*, int, int, int,      \
+                                   float, cudaStream_t);                                                  \
+  template int pack_mask<T>(const T*, uint32_t*, int, int, cudaStream_t);                                 \
+  template int compress24<T>(const T*, T*, uint8_t*, int32_t*, int, int, cudaStream_t);                   \
+  template int grad_outer<T>(const T*, const T*, const T*, float*, int, int, int, int, cudaStream_t);
+
+LORS_INST(float)
+LORS_INST(__nv_bfloat16)
+
+template int simt_strided_gemm<float, float, float>(const float*, int64_t, int64_t, const float*, int64_t,
+                                                    int64_t, float*, int64_t, int64_t, int, int, int, float,
+                                                    bool, cudaStream_t);
+template int simt_strided_gemm<__nv_bfloat16, __nv_bfloat16, float>(const __nv_bfloat16*, int64_t, int64_t,
+                                                                    const __nv_bfloat16*, int64_t, int64_t,
+                                                                    float*, int64_t, int64_t, int, int, int,
+                                                                    float, bool, cudaStream_t);
+template int simt_strided_gemm<__nv_bfloat16, __nv_bfloat16, __nv_bfloat16>(
+    const __nv_bfloat16*, int64_t, int64_t, const __nv_bfloat16*, int64_t, int64_t, __nv_bfloat16*, int64_t,
+    int64_t, int, int, int, float, bool, cudaStream_t);
+template int simt_strided_gemm<__nv_bfloat16, float, float>(const __nv_bfloat16*, int64_t, int64_t, const float*,
+                                                            int64_t, int64_t, float*, int64_t, int64_t, int, int,
+                                                            int, float, bool, cudaStream_t);
+template int simt_strided_gemm<float, __nv_bfloat16, float>(const float*, int64_t, int64_t, const __nv_bfloat16*,
+                                                            int64_t, int64_t, float*, int64_t, int64_t, int, int,
+                                                            int, float, bool, cudaStream_t);
+
+}  // namespace lors

@@ -1,0 +1,189 @@
+"""torch.autograd.Function / nn.Module form of the LoRS linear.
+
+Mirrors the paper's PyTorch listing `forward_lors` / `backward_lors`
+(/root/reference/PAPER.md:481-510): `lora_A` is the reference `a` [out, r],
+`lora_B` is `b` [r, in]; backward returns
+(grad_x, None, grad_bias, grad_A, grad_B, None).  Differences by design:
+the merged weight is never materialised (the native kernels rebuild W_eff
+tiles on chip), and only X is saved for backward (the paper listing saves
+x, weight, lora_A, lora_B; the reference package saves X only,
+adapters.py:372).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+from torch import nn
+
+from . import ops
+from .errors import ArgumentError, ShapeError
+
+
+@dataclass
+class LoRSParams:
+    alpha: float = 2.0            # scaling_factor (adapters.py:69)
+    grad_mode: str = "ste"        # "ste" = lors (adapters.py:376-406); "masked" = sqft_gc (:303-312)
+    mask_bits: Optional[torch.Tensor] = None
+    save_p: bool = False          # keep P = X b^T (rL elements, dense-LoRA footprint)
+    fault_da_sign: bool = False   # negative control (adapters.py:57-60)
+
+
+class LoRSFunction(torch.autograd.Function):
+    """y = x (W + alpha a b . M)^T + bias over x [..., in]."""
+
+    @staticmethod
+    def forward(ctx, x, weight, bias, lora_A, lora_B, params: LoRSParams):
+        out_f, in_f = weight.shape
+        if x.shape[-1] != in_f:
+            raise ShapeError(f"layer expects {in_f} input features, got {x.shape[-1]}")
+        dt = weight.dtype
+        shape = x.shape
+        x2 = x.reshape(-1, in_f)
+        if x2.dtype != dt:
+            x2 = x2.to(dt)
+        x2 = x2.contiguous()
+        a = lora_A.detach().to(dt).contiguous()
+        b = lora_B.detach().to(dt).contiguous()
+        bias_c = None if bias is None else bias.detach().to(dt).contiguous()
+        y, p = ops.lors_fwd(x2, weight, a, b, params.alpha, bias_c, params.mask_bits, emit_p=params.save_p)
+        if params.save_p:
+            ctx.save_for_backward(x2, p)
+        else:
+            ctx.save_for_backward(x2)
+        # adapter read at backward time (reference b2, adapters.py:387-394)
+        ctx.lors = (weight, lora_A, lora_B, bias is not None, params, shape, x.dtype)
+        return y.view(*shape[:-1], out_f)
+
+    @staticmethod
+    def backward(ctx, grad_y):
+        weight, lora_A, lora_B, has_bias, params, x_shape, x_dtype = ctx.lors
+        saved = ctx.saved_tensors
+        x2 = saved[0]
+        p = saved[1] if len(saved) > 1 else None
+        out_f, in_f = weight.shape
+        dt = weight.dtype
+        dy = grad_y.reshape(-1, out_f)
+        if dy.dtype != dt:
+            dy = dy.to(dt)
+        dy = dy.contiguous()
+        a = lora_A.detach().to(dt).contiguous()
+        b = lora_B.detach().to(dt).contiguous()
+        need_dx = ctx.needs_input_grad[0]
+        dx, da, db, dbias = ops.lors_bwd(x2, weight, a, b, dy, params.alpha, p=p, mask_bits=params.mask_bits,
+                                         grad_mode=params.grad_mode, need_dx=need_dx, with_bias=has_bias,
+                                         fault_da_sign=params.fault_da_sign)
+        grad_x = dx.view(x_shape).to(x_dtype) if need_dx else None
+        grad_bias = dbias.to(dt) if has_bias and ctx.needs_input_grad[2] else None
+        grad_a = da.to(lora_A.dtype) if ctx.needs_input_grad[3] else None
+        grad_b = db.to(lora_B.dtype) if ctx.needs_input_grad[4] else None
+        return grad_x, None, grad_bias, grad_a, grad_b, None
+
+
+class LoRSLinear(nn.Module):
+    """Sparsity-preserving LoRA linear: frozen pruned `weight`, trainable `a`, `b`.
+
+    Constructor follows the reference contract (make_layer / AdaptedLayer,
+    adapters.py:114-176): `weight` (the pruned base; zeros are the mask),
+    `rank` (zero-initialised a and b, as make_layer) or explicit `a`/`b`,
+    `alpha=2.0`, `bias=None`, `name`.  state_dict: `weight` (frozen buffer),
+    `a`, `b` (fp32 master parameters), `bias`, and `mask` (packed bits) when
+    mask_mode == "bits".  The compute dtype is weight.dtype (float32 = FFMA
+    parity mode, bfloat16 = tcgen05 mode).
+    """
+
+    def __init__(self, weight: torch.Tensor, rank: Optional[int] = None, a: Optional[torch.Tensor] = None,
+                 b: Optional[torch.Tensor] = None, alpha: float = 2.0, bias: Optional[torch.Tensor] = None,
+                 name: str = "", grad_mode: str = "ste", mask_mode: str = "from_w", save_p: bool = False,
+                 param_dtype: torch.dtype = torch.float32):
+        super().__init__()
+        if weight.dim() != 2:
+            raise ShapeError("weight must be 2-D [out, in]")
+        R, C = weight.shape
+        if (a is None) != (b is None):
+            raise ArgumentError("give both a and b, or neither")
+        if a is None:
+            if rank is None:
+                raise ArgumentError("need rank or a/b")
+            a = torch.zeros(R, rank, dtype=param_dtype, device=weight.device)
+            b = torch.zeros(rank, C, dtype=param_dtype, device=weight.device)
+        if a.shape[1] != b.shape[0]:
+            raise ShapeError(f"adapter rank mismatch: a is {a.shape[0]}x{a.shape[1]}, b is {b.shape[0]}x{b.shape[1]}")
+        r = a.shape[1]
+        if r < 1 or r > min(R, C):
+            raise ArgumentError(f"rank {r} must satisfy 1 <= r <= min({R}, {C})")
+        if a.shape[0] != R:
+            raise ShapeError(f"adapter a has {a.shape[0]} rows, base has {R}")
+        if b.shape[1] != C:
+            raise ShapeError(f"adapter b has {b.shape[1]} cols, base has {C}")
+        if not alpha > 0:
+            raise ArgumentError(f"alpha must be positive, got {alpha}")
+        if grad_mode not in ("ste", "masked"):
+            raise ArgumentError(f"grad_mode must be 'ste' or 'masked', got {grad_mode!r}")
+        if mask_mode not in ("from_w", "bits"):
+            raise ArgumentError(f"mask_mode must be 'from_w' or 'bits', got {mask_mode!r}")
+        w = weight.detach()
+        w = torch.where(w == 0, torch.zeros_like(w), w).contiguous()  # -0.0 -> +0.0 (prune.py:47)
+        self.register_buffer("weight", w)
+        self.a = nn.Parameter(a.detach().clone())
+        self.b = nn.Parameter(b.detach().clone())
+        self.bias = None if bias is None else nn.Parameter(bias.detach().clone().reshape(R))
+        if mask_mode == "bits":
+            self.register_buffer("mask", ops.pack_mask(w))
+        else:
+            self.mask = None
+        self.alpha = float(alpha)
+        self.name = name
+        self.grad_mode = grad_mode
+        self.save_p = save_p
+        self.fault_da_sign = False
+
+    @property
+    def in_features(self) -> int:
+        return self.weight.shape[1]
+
+    @property
+    def out_features(self) -> int:
+        return self.weight.shape[0]
+
+    @property
+    def rank(self) -> int:
+        return self.a.shape[1]
+
+    def params(self) -> LoRSParams:
+        return LoRSParams(alpha=self.alpha, grad_mode=self.grad_mode, mask_bits=self.mask,
+                          save_p=self.save_p, fault_da_sign=self.fault_da_sign)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        return LoRSFunction.apply(x, self.weight, self.bias, self.a, self.b, self.params())
+
+    @torch.no_grad()
+    def effective_weight(self) -> torch.Tensor:
+        """W_eff through the kernels' prologue function (bit-exact +0 where M = 0)."""
+        dt = self.weight.dtype
+        return ops.effective_weight(self.weight, self.a.to(dt).contiguous(), self.b.to(dt).contiguous(),
+                                    self.alpha, self.mask)
+
+    @torch.no_grad()
+    def merge(self) -> torch.Tensor:
+        """merge() (adapters.py:709-727): the finalised sparse weight."""
+        return self.effective_weight()
+
+    def extra_repr(self) -> str:
+        return (f"in={self.in_features}, out={self.out_features}, r={self.rank}, alpha={self.alpha}, "
+                f"grad_mode={self.grad_mode}, dtype={self.weight.dtype}")
+
+    @staticmethod
+    def init_normal(a_std: float, b_std: float, R: int, C: int, r: int, generator=None, device="cuda"):
+        """BASELINE config-1 init in reference names: b ~ N(0, b_std^2) (north_star A),
+        a ~ N(0, a_std^2) (north_star B); SURVEY C2."""
+        a = torch.randn(R, r, generator=generator, device=device) * a_std
+        b = torch.randn(r, C, generator=generator, device=device) * b_std
+        return a, b
+
+
+def default_b_std(r: int) -> float:
+    return 1.0 / math.sqrt(r)

@@ -1,0 +1,186 @@
+"""Torch-tensor wrappers over the C ABI (torch layout: tokens are rows).
+
+PyTorch is plumbing here: it owns device memory and the current stream; the
+work happens in the native library.  Every function validates shapes with
+the reference's messages (adapters.py:227-238) and raises ShapeError /
+ArgumentError; nothing falls back to torch math.
+"""
+
+from __future__ import annotations
+
+import ctypes as ct
+from typing import Optional
+
+import torch
+
+from . import _native as N
+from .errors import ArgumentError, ShapeError
+
+_DTYPES = {torch.float32: N.DTYPE_F32, torch.bfloat16: N.DTYPE_BF16}
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    if dt not in _DTYPES:
+        raise ArgumentError(f"unsupported dtype {dt}; expected float32 or bfloat16")
+    return _DTYPES[dt]
+
+
+def _p(t: Optional[torch.Tensor]):
+    return None if t is None else ct.c_void_p(t.data_ptr())
+
+
+def _stream() -> ct.c_void_p:
+    return ct.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _need(t: torch.Tensor, name: str, shape, dtype=None):
+    if tuple(t.shape) != tuple(shape):
+        raise ShapeError(f"{name} must be {'x'.join(map(str, shape))}, got {'x'.join(map(str, t.shape))}")
+    if dtype is not None and t.dtype != dtype:
+        raise ArgumentError(f"{name} has dtype {t.dtype}, expected {dtype}")
+    if not t.is_cuda:
+        raise ArgumentError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if not t.is_contiguous():
+        raise ArgumentError(f"{name} must be contiguous")
+
+
+def _check_layer(x_t, w, a, b):
+    if w.dim() != 2 or a.dim() != 2 or b.dim() != 2 or x_t.dim() != 2:
+        raise ShapeError("x_t, w, a, b must be 2-D")
+    R, C = w.shape
+    if a.shape[1] != b.shape[0]:
+        raise ShapeError(f"adapter rank mismatch: a is {a.shape[0]}x{a.shape[1]}, b is {b.shape[0]}x{b.shape[1]}")
+    if a.shape[0] != R:
+        raise ShapeError(f"adapter a has {a.shape[0]} rows, base has {R}")
+    if b.shape[1] != C:
+        raise ShapeError(f"adapter b has {b.shape[1]} cols, base has {C}")
+    if x_t.shape[1] != C:
+        raise ShapeError(f"layer expects {C} input rows, got {x_t.shape[1]}x{x_t.shape[0]}")
+    return x_t.shape[0], R, C, a.shape[1]
+
+
+def lors_fwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tensor, alpha: float = 2.0,
+             bias: Optional[torch.Tensor] = None, mask_bits: Optional[torch.Tensor] = None,
+             emit_p: bool = False, sparse24=None):
+    """Y_t [L, R] = X_t . W_eff^T (+ bias); optionally P = X_t b^T [L, r]."""
+    L, R, C, r = _check_layer(x_t, w, a, b)
+    dt = w.dtype
+    code = dtype_code(dt)
+    for t, nm, sh in ((x_t, "x", (L, C)), (w, "w", (R, C)), (a, "a", (R, r)), (b, "b", (r, C))):
+        _need(t, nm, sh, dt)
+    if bias is not None:
+        _need(bias, "bias", (R,), dt)
+    y = torch.empty((L, R), dtype=dt, device=w.device)
+    p = torch.empty((L, r), dtype=dt, device=w.device) if emit_p else None
+    args = N.FwdArgs()
+    args.L, args.R, args.C, args.r = L, R, C, r
+    args.dtype = code
+    args.mask_mode = N.MASK_BITS if mask_bits is not None else N.MASK_FROM_W
+    args.flags = (N.FLAG_EMIT_P if emit_p else 0) | (N.FLAG_SPARSE24 if sparse24 is not None else 0)
+    args.alpha = float(alpha)
+    args.x, args.w, args.a, args.b = _p(x_t), _p(w), _p(a), _p(b)
+    args.mask_bits = _p(mask_bits)
+    if sparse24 is not None:
+        vals, meta = sparse24
+        args.w24, args.meta24 = _p(vals), _p(meta)
+    args.bias, args.y, args.p = _p(bias), _p(y), _p(p)
+    lib = N.load()
+    ws_bytes = lib.lors_fwd_workspace(ct.byref(args))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=w.device) if ws_bytes else None
+    args.workspace, args.workspace_bytes = _p(ws), ws_bytes
+    N.check(lib.lors_fwd(ct.byref(args), _stream()))
+    return y, p
+
+
+def lors_bwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tensor, dy_t: torch.Tensor,
+             alpha: float = 2.0, p: Optional[torch.Tensor] = None, mask_bits: Optional[torch.Tensor] = None,
+             grad_mode: str = "ste", need_dx: bool = True, with_bias: bool = False,
+             fault_da_sign: bool = False):
+    """(dX_t [L, C] | None, dA [R, r] fp32, dB [r, C] fp32, dbias [R] fp32 | None)."""
+    L, R, C, r = _check_layer(x_t, w, a, b)
+    dt = w.dtype
+    code = dtype_code(dt)
+    if tuple(dy_t.shape) != (L, R):
+        raise ShapeError(f"gradient must be {R}x{L}, got {dy_t.shape[1]}x{dy_t.shape[0]}")
+    for t, nm, sh in ((x_t, "x", (L, C)), (w, "w", (R, C)), (a, "a", (R, r)), (b, "b", (r, C)),
+                      (dy_t, "dy", (L, R))):
+        _need(t, nm, sh, dt)
+    if p is not None:
+        _need(p, "p", (L, r), dt)
+    if grad_mode not in ("ste", "masked"):
+        raise ArgumentError(f"grad_mode must be 'ste' or 'masked', got {grad_mode!r}")
+    dev = w.device
+    dx = torch.empty((L, C), dtype=dt, device=dev) if need_dx else None
+    da = torch.empty((R, r), dtype=torch.float32, device=dev)
+    db = torch.empty((r, C), dtype=torch.float32, device=dev)
+    dbias = torch.empty((R,), dtype=torch.float32, device=dev) if with_bias else None
+    args = N.BwdArgs()
+    args.L, args.R, args.C, args.r = L, R, C, r
+    args.dtype = code
+    args.mask_mode = N.MASK_BITS if mask_bits is not None else N.MASK_FROM_W
+    args.grad_mode = N.GRAD_STE if grad_mode == "ste" else N.GRAD_MASKED
+    args.flags = (0 if need_dx else N.FLAG_NO_DX) | (N.FLAG_FAULT_DA_SIGN if fault_da_sign else 0)
+    args.alpha = float(alpha)
+    args.x, args.w, args.mask_bits, args.a, args.b = _p(x_t), _p(w), _p(mask_bits), _p(a), _p(b)
+    args.dy, args.p, args.dx, args.da, args.db, args.dbias = _p(dy_t), _p(p), _p(dx), _p(da), _p(db), _p(dbias)
+    lib = N.load()
+    ws_bytes = lib.lors_bwd_workspace(ct.byref(args))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev) if ws_bytes else None
+    args.workspace, args.workspace_bytes = _p(ws), ws_bytes
+    N.check(lib.lors_bwd(ct.byref(args), _stream()))
+    return dx, da, db, dbias
+
+
+def effective_weight(w: torch.Tensor, a: torch.Tensor, b: torch.Tensor, alpha: float = 2.0,
+                     mask_bits: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """W_eff = select(M, W + alpha a b, +0) [R, C] (merged_weight, adapters.py:214-224)."""
+    R, C = w.shape
+    r = a.shape[1]
+    _check_layer(torch.empty((0, C), device="meta"), w, a, b)
+    for t, nm, sh in ((w, "w", (R, C)), (a, "a", (R, r)), (b, "b", (r, C))):
+        _need(t, nm, sh, w.dtype)
+    out = torch.empty_like(w)
+    N.check(N.load().lors_effective_weight(R, C, r, dtype_code(w.dtype),
+                                           N.MASK_BITS if mask_bits is not None else N.MASK_FROM_W,
+                                           float(alpha), _p(w), _p(mask_bits), _p(a), _p(b), _p(out),
+                                           _stream()))
+    return out
+
+
+def pack_mask(w: torch.Tensor) -> torch.Tensor:
+    """Packed mask [R, ceil(C/32)] (int32 storage of uint32 words), bit j of
+    word k = (W[:, 32k+j] != 0)."""
+    R, C = w.shape
+    _need(w, "w", (R, C))
+    bits = torch.empty((R, (C + 31) // 32), dtype=torch.int32, device=w.device)
+    N.check(N.load().lors_pack_mask(R, C, dtype_code(w.dtype), _p(w), _p(bits), _stream()))
+    return bits
+
+
+def compress_24(w: torch.Tensor):
+    """(values [R, C/2], meta [R, C/8] uint8, valid) for a 2:4 pruned W."""
+    R, C = w.shape
+    _need(w, "w", (R, C))
+    vals = torch.empty((R, C // 2), dtype=w.dtype, device=w.device)
+    meta = torch.empty((R, C // 8), dtype=torch.uint8, device=w.device)
+    flag = torch.zeros((1,), dtype=torch.int32, device=w.device)
+    N.check(N.load().lors_compress_24(R, C, dtype_code(w.dtype), _p(w), _p(vals), _p(meta), _p(flag),
+                                      _stream()))
+    return vals, meta, flag
+
+
+def grad_outer(dy_t: torch.Tensor, x_t: torch.Tensor, w: Optional[torch.Tensor] = None,
+               masked: bool = False) -> torch.Tensor:
+    """dW [R, C] fp32 = dY_t^T X_t, optionally (.) (W != 0) (initialization.py:209-211)."""
+    L, R = dy_t.shape
+    C = x_t.shape[1]
+    _need(dy_t, "dy", (L, R))
+    _need(x_t, "x", (L, C), dy_t.dtype)
+    if masked:
+        if w is None:
+            raise ArgumentError("masked grad_outer needs w")
+        _need(w, "w", (R, C), dy_t.dtype)
+    dw = torch.empty((R, C), dtype=torch.float32, device=dy_t.device)
+    N.check(N.load().lors_grad_outer(L, R, C, dtype_code(dy_t.dtype), int(masked), _p(dy_t), _p(x_t),
+                                     _p(w), _p(dw), _stream()))
+    return dw

@@ -1,0 +1,321 @@
+"""GPU parity: the native kernels vs the reference (golden fixtures) and the oracle.
+
+Patterned on the reference's own suites (pkg/tests/test_adapters.py,
+test_acceptance.py criteria 1-3, 5): forward/backward against the defining
+expressions, masked-forward bitwise identity between lors and sqft_gc,
+single-use contexts, shape validation, merge preserving the mask, and the
+fault-injection negative control.  Tolerances (north_star): fp32 rel-L2 <= 1e-4,
+bf16 rel-L2 <= 2e-2 (oracle fed the bf16-rounded inputs).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import lors_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = os.path.join(HERE, "golden")
+TOL = {torch.float32: 1e-4, torch.bfloat16: 2e-2}
+
+
+def _manifest():
+    with open(os.path.join(GOLD, "manifest.json")) as f:
+        return json.load(f)
+
+
+CASES = _manifest()["cases"]
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2501_08582_b200 as P
+    from paper_2501_08582_b200 import _native
+    _native.check(_native.load().lors_device_check())
+    return P
+
+
+def _dev(a, dt):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dt).cuda().contiguous()
+
+
+def _rel(got, ref):
+    return orc.rel_l2(got.double().cpu().numpy(), ref)
+
+
+def _bits_zero(t):
+    it = {torch.float32: torch.int32, torch.bfloat16: torch.int16}[t.dtype]
+    return bool((t.view(it) == 0).all())
+
+
+# ---------------------------------------------------------------------------
+# reference-produced fixtures
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("case", CASES, ids=[c["key"] for c in CASES])
+def test_golden_lors_step(P, case, dt):
+    from paper_2501_08582_b200 import ops
+    d = dict(np.load(os.path.join(GOLD, f"lors_{case['key']}.npz")))
+    if dt == torch.float32 or case["bf16_inputs"]:
+        ref = d  # reference outputs on exactly these inputs
+        y_ref, dx_ref, da_ref, db_ref = d["y"].T, d["dx"].T, d["da"], d["db"]
+        mda, mdb = d["m_da"], d["m_db"]
+    else:  # oracle on the bf16-rounded inputs
+        q = {k: torch.from_numpy(d[k]).to(dt).double().numpy() for k in ("w", "a", "b", "x", "dy")}
+        bias = None if "bias" not in d else torch.from_numpy(d["bias"]).to(dt).double().numpy()
+        y_ref, dx_ref, da_ref, db_ref, _ = orc.lors_step_torch_layout(q["w"], q["a"], q["b"], q["x"].T,
+                                                                      q["dy"].T, 2.0, bias)
+        m = orc.sqft_gc_backward(q["w"], q["a"], q["b"], q["x"], q["dy"])
+        mda, mdb = m.da, m.db
+        ref = dict(d, bias=bias) if bias is not None else d
+    w, a, b = _dev(d["w"], dt), _dev(d["a"], dt), _dev(d["b"], dt)
+    x_t, dy_t = _dev(d["x"].T, dt), _dev(d["dy"].T, dt)
+    bias = _dev(ref["bias"], dt) if "bias" in d else None
+    y, _ = ops.lors_fwd(x_t, w, a, b, 2.0, bias)
+    dx, da, db, dbias = ops.lors_bwd(x_t, w, a, b, dy_t, 2.0, with_bias=bias is not None)
+    tol = TOL[dt]
+    assert _rel(y, y_ref) <= tol
+    assert _rel(dx, dx_ref) <= tol
+    assert _rel(da, da_ref) <= tol
+    assert _rel(db, db_ref) <= tol
+    if bias is not None:
+        assert _rel(dbias, d["dbias"]) <= tol
+    _, mda_g, mdb_g, _ = ops.lors_bwd(x_t, w, a, b, dy_t, 2.0, grad_mode="masked", need_dx=False)
+    assert _rel(mda_g, mda) <= tol
+    assert _rel(mdb_g, mdb) <= tol
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("case", CASES, ids=[c["key"] for c in CASES])
+def test_golden_merge_preserves_mask_bitexact(P, case, dt):
+    from paper_2501_08582_b200 import ops
+    d = dict(np.load(os.path.join(GOLD, f"lors_{case['key']}.npz")))
+    w, a, b = _dev(d["w"], dt), _dev(d["a"], dt), _dev(d["b"], dt)
+    weff = ops.effective_weight(w, a, b, 2.0)
+    assert _bits_zero(weff[w == 0])
+    if dt == torch.float32:
+        assert _rel(weff, d["merged"]) <= 1e-6
+    bits = ops.pack_mask(w)
+    weff2 = ops.effective_weight(w, a, b, 2.0, mask_bits=bits)
+    assert torch.equal(weff.view(torch.uint8), weff2.view(torch.uint8))
+
+
+# ---------------------------------------------------------------------------
+# reference-API mirror (test_adapters.py patterns)
+# ---------------------------------------------------------------------------
+
+def random_layer(P, seed, variant, R, C, r, alpha=2.0, zero_frac=0.5, bias=False, dt=torch.float32):
+    rng = np.random.default_rng(seed)
+    w = rng.normal(size=(R, C))
+    flat = np.argsort(np.abs(w), axis=None)
+    w.reshape(-1)[flat[: int(zero_frac * R * C)]] = 0.0
+    base = P.SparseWeight(_dev(w, dt))
+    layer = P.make_layer(base, rank=r, variant=variant, alpha=alpha,
+                         bias=_dev(rng.normal(size=(R,)), dt) if bias else None)
+    layer.adapter.a = _dev(rng.normal(size=(R, r)), torch.float32)
+    layer.adapter.b = _dev(rng.normal(size=(r, C)), torch.float32)
+    return layer, w
+
+
+def test_forward_matches_defining_expression(P):
+    for i, variant in enumerate(P.VARIANTS):
+        layer, w = random_layer(P, 100 + i, variant, R=6, C=8, r=2, bias=(i % 2 == 0))
+        x = np.random.default_rng(7 + i).normal(size=(8, 5))
+        y, _ = P.variant_forward(layer, _dev(x, torch.float32))
+        a, b = layer.adapter.a.double().cpu().numpy(), layer.adapter.b.double().cpu().numpy()
+        want = orc.lors_forward(w, a, b, x, 2.0,
+                                None if layer.bias is None else layer.bias.double().cpu().numpy())
+        assert _rel(y, want) <= 1e-6
+
+
+def test_masked_forwards_bitwise_identical(P):
+    for seed in range(5):
+        outs = []
+        x = _dev(np.random.default_rng(seed).normal(size=(7, 3)), torch.float32)
+        for variant in P.VARIANTS:
+            layer, _ = random_layer(P, seed, variant, R=5, C=7, r=2)
+            y, _ = P.variant_forward(layer, x)
+            outs.append(y.contiguous())
+        assert torch.equal(outs[0], outs[1])
+
+
+def test_context_is_single_use(P):
+    layer, _ = random_layer(P, 21, "lors", R=4, C=4, r=1)
+    x = _dev(np.random.default_rng(21).normal(size=(4, 3)), torch.float32)
+    g = torch.ones(4, 3, device="cuda")
+    _, ctx = P.variant_forward(layer, x)
+    P.variant_backward(layer, g, ctx)
+    with pytest.raises(P.GraphError):
+        P.variant_backward(layer, g, ctx)
+
+
+def test_shape_and_argument_validation(P):
+    layer, _ = random_layer(P, 22, "sqft_gc", R=4, C=5, r=1)
+    with pytest.raises(P.ShapeError):
+        P.variant_forward(layer, torch.ones(4, 3, device="cuda"))
+    _, ctx = P.variant_forward(layer, torch.ones(5, 3, device="cuda"))
+    with pytest.raises(P.ShapeError):
+        P.variant_backward(layer, torch.ones(4, 2, device="cuda"), ctx)
+    z = lambda *s: torch.zeros(*s, device="cuda")  # noqa: E731
+    with pytest.raises(P.ShapeError):
+        P.AdapterPair(z(4, 2), z(3, 5))
+    with pytest.raises(P.ArgumentError):
+        P.AdapterPair(z(4, 5), z(5, 4))
+    with pytest.raises(P.ArgumentError):
+        P.AdapterPair(z(4, 2), z(2, 5), alpha=0.0)
+    base = P.SparseWeight(torch.ones(4, 6, device="cuda"))
+    with pytest.raises(P.ArgumentError):
+        P.AdaptedLayer(base, P.AdapterPair(z(4, 2), z(2, 6)), "nope")
+    with pytest.raises(P.ShapeError):
+        P.AdaptedLayer(base, P.AdapterPair(z(5, 2), z(2, 6)), "lors")
+    with pytest.raises(P.ShapeError):
+        P.make_layer(base, rank=2, variant="lors", bias=torch.ones(3, device="cuda"))
+
+
+def test_lors_grads_against_oracle_and_ste_surrogate(P):
+    """dA/dB are the STE surrogate's gradients; dX the masked function's (test_adapters.py:138-187)."""
+    layer, w = random_layer(P, 200, "lors", R=5, C=6, r=2, bias=True)
+    rng = np.random.default_rng(50)
+    x0, g = rng.normal(size=(6, 4)), rng.normal(size=(5, 4))
+    _, ctx = P.variant_forward(layer, _dev(x0, torch.float32))
+    grads = P.variant_backward(layer, _dev(g, torch.float32), ctx)
+    a, b = layer.adapter.a.double().cpu().numpy(), layer.adapter.b.double().cpu().numpy()
+    ref = orc.lors_backward(w, a, b, x0, g, 2.0, with_bias=True)
+    for got, want in ((grads.da, ref.da), (grads.db, ref.db), (grads.dx, ref.dx), (grads.dbias, ref.dbias)):
+        assert _rel(got, want) <= 1e-5
+    # STE: the unmasked surrogate's gradient wrt a is alpha * g (b x)^T
+    assert _rel(grads.da, 2.0 * g @ (b @ x0).T) <= 1e-5
+
+
+def test_fault_injection_is_caught(P):
+    layer, w = random_layer(P, 31, "lors", R=16, C=24, r=4)
+    rng = np.random.default_rng(31)
+    x0, g = rng.normal(size=(24, 8)), rng.normal(size=(16, 8))
+    a, b = layer.adapter.a.double().cpu().numpy(), layer.adapter.b.double().cpu().numpy()
+    ref = orc.lors_backward(w, a, b, x0, g)
+    P.FAULT_INJECTION["lors_backward_sign_flip"] = True
+    try:
+        _, ctx = P.variant_forward(layer, _dev(x0, torch.float32))
+        bad = P.variant_backward(layer, _dev(g, torch.float32), ctx)
+    finally:
+        P.FAULT_INJECTION["lors_backward_sign_flip"] = False
+    assert _rel(bad.da, ref.da) > 1.0  # parity harness trips
+    assert _rel(bad.db, ref.db) <= 1e-5
+
+
+def test_merge_inside_mask_after_updates(P):
+    layer, w = random_layer(P, 41, "lors", R=32, C=48, r=4)
+    merged = P.merge(layer).values
+    assert _bits_zero(merged[torch.from_numpy(w == 0).cuda()])
+    layer.base.values[0, 0] = 0.0 if w[0, 0] != 0 else layer.base.values[0, 0]
+    merged2 = P.merge(layer).values  # uses the mask captured at construction
+    assert torch.count_nonzero(merged2) >= torch.count_nonzero(merged) - 1
+
+
+def test_empty_batch(P):
+    from paper_2501_08582_b200 import ops
+    w = torch.randn(64, 32, device="cuda")
+    a, b = torch.randn(64, 4, device="cuda"), torch.randn(4, 32, device="cuda")
+    x = torch.empty(0, 32, device="cuda")
+    y, _ = ops.lors_fwd(x, w, a, b)
+    assert y.shape == (0, 64)
+    dx, da, db, _ = ops.lors_bwd(x, w, a, b, torch.empty(0, 64, device="cuda"))
+    assert dx.shape == (0, 32) and float(da.abs().sum()) == 0.0 and float(db.abs().sum()) == 0.0
+
+
+# ---------------------------------------------------------------------------
+# utilities: pack_mask, compress_24, grad_outer vs the oracle
+# ---------------------------------------------------------------------------
+
+def test_pack_mask_and_compress24(P):
+    from paper_2501_08582_b200 import ops, prune
+    rng = np.random.default_rng(3)
+    w = orc.prune_two_four(rng.normal(size=(48, 96)))
+    wd = _dev(w, torch.bfloat16)
+    bits = ops.pack_mask(wd).cpu().numpy().view(np.uint32)
+    np.testing.assert_array_equal(bits, orc.pack_mask(w))
+    vals, meta, flag = ops.compress_24(wd)
+    assert int(flag.item()) == 0
+    m = meta.cpu().numpy()
+    v = vals.float().cpu().numpy()
+    for n in range(48):
+        for g in range(96 // 4):
+            nib = (int(m[n, g // 2]) >> (4 * (g % 2))) & 0xF
+            i0, i1 = nib & 3, nib >> 2
+            assert i0 < i1
+            dense = np.zeros(4)
+            dense[i0], dense[i1] = v[n, 2 * g], v[n, 2 * g + 1]
+            np.testing.assert_array_equal(dense, torch.from_numpy(w[n, 4 * g:4 * g + 4]).bfloat16().float().numpy())
+    bad = _dev(rng.normal(size=(8, 16)), torch.bfloat16)
+    assert int(ops.compress_24(bad)[2].item()) == 1
+    assert prune.two_four_valid(wd)
+
+
+@pytest.mark.parametrize("masked", [False, True])
+def test_grad_outer(P, masked):
+    from paper_2501_08582_b200 import ops
+    rng = np.random.default_rng(5)
+    L, R, C = 40, 24, 36
+    w = orc.prune_rowwise(rng.normal(size=(R, C)), 0.5)
+    dy, x = rng.normal(size=(L, R)), rng.normal(size=(L, C))
+    dw = ops.grad_outer(_dev(dy, torch.float32), _dev(x, torch.float32), _dev(w, torch.float32), masked)
+    want = dy.T @ x
+    if masked:
+        want = want * (w != 0)
+    assert _rel(dw, want) <= 1e-5
+
+
+# ---------------------------------------------------------------------------
+# full BASELINE sizes
+# ---------------------------------------------------------------------------
+
+def _cfg_tensors(R, C, L, r, dt, pattern, seed=0):
+    from paper_2501_08582_b200 import prune
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    w = torch.randn(R, C, device="cuda", generator=g) * 0.02
+    w = prune.prune_two_four(w) if pattern == "two_four" else prune.prune_rowwise(w, 0.5)
+    a = torch.randn(R, r, device="cuda", generator=g) * 1e-3   # north_star B ~ N(0, 1e-3^2)
+    b = torch.randn(r, C, device="cuda", generator=g) / r ** 0.5  # north_star A ~ N(0, 1/r)
+    x = torch.randn(L, C, device="cuda", generator=g)
+    dy = torch.randn(L, R, device="cuda", generator=g)
+    return [t.to(dt).contiguous() for t in (w, a, b, x, dy)]
+
+
+def test_config1_fp32_full_size_vs_oracle(P):
+    """BASELINE config 1 at full size: fp32 mode within rel-L2 1e-4 of the f64 reference path."""
+    from paper_2501_08582_b200 import ops
+    w, a, b, x, dy = _cfg_tensors(4096, 4096, 2048, 16, torch.float32, "rowwise")
+    y, _ = ops.lors_fwd(x, w, a, b, 2.0)
+    dx, da, db, _ = ops.lors_bwd(x, w, a, b, dy, 2.0)
+    weff = ops.effective_weight(w, a, b, 2.0)
+    assert _bits_zero(weff[w == 0])
+    ref = orc.lors_step_torch_layout(*[t.double().cpu().numpy() for t in (w, a, b, x, dy)], alpha=2.0)
+    for got, want in zip((y, dx, da, db), ref[:4]):
+        assert _rel(got, want) <= 1e-4
+
+
+def test_config2_bf16_full_size_properties(P):
+    """BASELINE config 2 size (11008x4096, L=8192, r=64, 2:4) in bf16 against a torch
+    fp32 reference of the same op (kept for this floating-point kernel), plus linearity."""
+    from paper_2501_08582_b200 import ops
+    w, a, b, x, dy = _cfg_tensors(11008, 4096, 8192, 64, torch.bfloat16, "two_four")
+    y, _ = ops.lors_fwd(x, w, a, b, 2.0)
+    dx, da, db, _ = ops.lors_bwd(x, w, a, b, dy, 2.0)
+    wf, af, bf, xf, dyf = (t.float() for t in (w, a, b, x, dy))
+    weff = torch.where(wf != 0, wf + 2.0 * (af @ bf), torch.zeros_like(wf))
+    assert (_rel(y, (xf @ weff.t()).double().cpu().numpy()) <= 2e-2)
+    assert (_rel(dx, (dyf @ weff).double().cpu().numpy()) <= 2e-2)
+    p = xf @ bf.t()
+    assert _rel(da, (2.0 * dyf.t() @ p).double().cpu().numpy()) <= 2e-2
+    assert _rel(db, (2.0 * (dyf @ af).t() @ xf).double().cpu().numpy()) <= 2e-2
+    # linearity in X (size-independent property)
+    y1, _ = ops.lors_fwd(x[:4096].contiguous(), w, a, b, 2.0)
+    assert torch.equal(y1, y[:4096])

@@ -1,0 +1,96 @@
+"""Host-side logic that runs without a GPU: pruning producers (bitwise vs the
+reference fixtures), the cost model, module/adapter validation."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2501_08582_b200 as P
+from oracle import lors_oracle as orc
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def test_prune_producers_bitwise_vs_reference_fixtures():
+    d = dict(np.load(os.path.join(GOLD, "prune_kats.npz")))
+    for i in range(4):
+        w = torch.from_numpy(d[f"p{i}_w"])
+        np.testing.assert_array_equal(P.prune_rowwise(w, 0.5).numpy(), d[f"p{i}_rowwise"])
+        if f"p{i}_two_four" in d:
+            got = P.prune_two_four(w)
+            np.testing.assert_array_equal(got.numpy(), d[f"p{i}_two_four"])
+            assert P.two_four_valid(got)
+    np.testing.assert_array_equal(P.prune_magnitude(torch.tensor([[1.0, -4.0], [2.0, 3.0]]), 0.5).numpy(),
+                                  d["kat_magnitude"])
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_prune_rowwise_matches_oracle_with_ties(seed):
+    rng = np.random.default_rng(seed)
+    w = rng.normal(size=(7, 12))
+    w[:, 3] = w[:, 2]
+    w[2] = 0.5
+    np.testing.assert_array_equal(P.prune_rowwise(torch.from_numpy(w), 0.5).numpy(), orc.prune_rowwise(w, 0.5))
+    np.testing.assert_array_equal(P.prune_two_four(torch.from_numpy(w)).numpy(), orc.prune_two_four(w))
+
+
+def test_sparse_weight_normalises_negative_zero_and_validates():
+    sw = P.SparseWeight(torch.tensor([[-0.0, 1.0, 0.0, 2.0]]), pattern="two_four")
+    assert torch.signbit(sw.values).tolist() == [[False, False, False, False]]
+    with pytest.raises(P.ArgumentError):
+        P.SparseWeight(torch.ones(1, 4), pattern="two_four")
+    with pytest.raises(P.ArgumentError):
+        P.SparseWeight(torch.ones(1, 4), pattern="weird")
+
+
+def test_cost_model_matches_oracle_and_kat():
+    assert (P.predict_cost("lors", 4, 4, 4, 1).macs_forward, P.predict_cost("lors", 4, 4, 4, 1).macs_backward,
+            P.predict_cost("lors", 4, 4, 4, 1).saved_elements) == (96, 160, 16)
+    rng = np.random.default_rng(11)
+    for _ in range(50):
+        R, C, L, r = (int(v) for v in rng.integers(1, 50, size=4))
+        for variant in ("lors", "sqft_gc", "sqft", "lora"):
+            p = P.predict_cost(variant, R, C, L, r)
+            assert (p.macs_forward, p.macs_backward, p.saved_elements) == orc.predict_cost(variant, R, C, L, r)
+    with pytest.raises(P.ArgumentError):
+        P.predict_cost("nope", 1, 1, 1, 1)
+    # cfg2 = 1520.87 GFLOP per fwd+bwd step
+    assert abs(P.predict_cost("lors", 11008, 4096, 8192, 64).flops / 1e9 - 1520.87) < 0.01
+    assert abs(P.predict_cost("lors", 4096, 4096, 2048, 16).flops / 1e9 - 139.65) < 0.01
+
+
+def test_cost_model_fault_injection():
+    P.FAULT_INJECTION["cost_model_off_by_one"] = True
+    try:
+        assert P.predict_cost("lors", 4, 4, 4, 1).macs_backward == 161
+    finally:
+        P.FAULT_INJECTION["cost_model_off_by_one"] = False
+
+
+def test_module_constructor_validation_cpu():
+    w = torch.randn(8, 6)
+    with pytest.raises(P.ArgumentError):
+        P.LoRSLinear(w)
+    with pytest.raises(P.ArgumentError):
+        P.LoRSLinear(w, rank=7)
+    with pytest.raises(P.ShapeError):
+        P.LoRSLinear(w, a=torch.zeros(8, 2), b=torch.zeros(3, 6))
+    with pytest.raises(P.ArgumentError):
+        P.LoRSLinear(w, rank=2, alpha=0.0)
+    with pytest.raises(P.ArgumentError):
+        P.LoRSLinear(w, rank=2, grad_mode="other")
+    m = P.LoRSLinear(w, rank=2, bias=torch.zeros(8))
+    assert sorted(m.state_dict().keys()) == ["a", "b", "bias", "weight"]
+    assert not m.weight.requires_grad and m.a.requires_grad and m.b.requires_grad
+    assert float(m.a.abs().sum()) == 0.0 and float(m.b.abs().sum()) == 0.0  # make_layer zero init
+
+
+def test_adapter_pair_validation_cpu():
+    with pytest.raises(P.ShapeError):
+        P.AdapterPair(torch.zeros(4, 2), torch.zeros(3, 5))
+    with pytest.raises(P.ArgumentError):
+        P.AdapterPair(torch.zeros(4, 5), torch.zeros(5, 4))
+    with pytest.raises(P.ArgumentError):
+        P.AdapterPair(torch.zeros(4, 2), torch.zeros(2, 5), alpha=-1.0)
