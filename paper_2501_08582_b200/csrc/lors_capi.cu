@@ -92,8 +92,9 @@ int lors_fwd(const lors_fwd_args* A, void* stream) {
   if (A == nullptr) return fail(LORS_ERR_ARGUMENT, "null args");
   int st = check_common(A->L, A->R, A->C, A->r, A->dtype, A->mask_mode, A->alpha, A->mask_bits);
   if (st) return st;
-  if (!A->x || !A->w || !A->a || !A->b || !A->y) return fail(LORS_ERR_ARGUMENT, "null tensor pointer");
-  if ((A->flags & LORS_FLAG_EMIT_P) && !A->p) return fail(LORS_ERR_ARGUMENT, "EMIT_P needs p");
+  if (!A->w || !A->a || !A->b) return fail(LORS_ERR_ARGUMENT, "null tensor pointer");
+  if (A->L > 0 && (!A->x || !A->y)) return fail(LORS_ERR_ARGUMENT, "null tensor pointer");
+  if (A->L > 0 && (A->flags & LORS_FLAG_EMIT_P) && !A->p) return fail(LORS_ERR_ARGUMENT, "EMIT_P needs p");
   if ((st = require_sm100())) return st;
   if (A->L == 0) return LORS_OK;
   cudaStream_t s = (cudaStream_t)stream;
@@ -117,9 +118,9 @@ int lors_bwd(const lors_bwd_args* A, void* stream) {
   if (st) return st;
   if (A->grad_mode != LORS_GRAD_STE && A->grad_mode != LORS_GRAD_MASKED)
     return fail(LORS_ERR_ARGUMENT, "unknown grad_mode");
-  if (!A->x || !A->w || !A->a || !A->b || !A->dy || !A->da || !A->db)
-    return fail(LORS_ERR_ARGUMENT, "null tensor pointer");
-  if (!(A->flags & LORS_FLAG_NO_DX) && !A->dx) return fail(LORS_ERR_ARGUMENT, "dx is null");
+  if (!A->w || !A->a || !A->b || !A->da || !A->db) return fail(LORS_ERR_ARGUMENT, "null tensor pointer");
+  if (A->L > 0 && (!A->x || !A->dy)) return fail(LORS_ERR_ARGUMENT, "null tensor pointer");
+  if (A->L > 0 && !(A->flags & LORS_FLAG_NO_DX) && !A->dx) return fail(LORS_ERR_ARGUMENT, "dx is null");
   if (A->workspace_bytes < lors_bwd_workspace(A) || (A->workspace == nullptr && lors_bwd_workspace(A) > 0))
     return fail(LORS_ERR_ARGUMENT, "workspace too small: need " + std::to_string(lors_bwd_workspace(A)) + " bytes");
   if ((st = require_sm100())) return st;
