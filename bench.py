@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark of the LoRS masked-LoRA linear hot path (fwd+bwd) on B200.
+
+Workload (BASELINE.json configs[1], the single-GPU configuration the metric is
+quoted on): one LoRS MLP projection, W 11008 x 4096 bf16 ~ N(0, 0.02^2) with
+2:4 magnitude sparsity, rank r = 64 (a ~ N(0, 1e-3^2), b ~ N(0, 1/r); SURVEY
+C2), alpha = 2.0, X = 8192 tokens x 4096 ~ N(0,1), dY ~ N(0,1), seeded
+synthetic data.  One step = forward (Y) + backward (dX, dA, dB) of the layer;
+with N > 1 GPUs every rank runs its own 8192 tokens (weak scaling) and the
+adapter gradients dA/dB are averaged with one NCCL all-reduce per step (the
+only exchange the path has).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+                    [--config cfg2|cfg1]
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+float64 numpy port in oracle/, the reference itself is Python and cannot
+travel to the GPU box) on a bounded token sample of the same layer.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fine-tune tokens/s (fwd+bwd) at 1/2/4/8 B200 vs roofline; peak HBM GB"
+CONFIGS = {
+    # name: (R, C, L, r, pattern, dtype)
+    "cfg2": dict(R=11008, C=4096, L=8192, r=64, pattern="two_four", dtype="bf16",
+                 desc="LoRS MLP projection 11008x4096, 2:4, r=64, 8192 tokens/GPU (BASELINE configs[1])"),
+    "cfg1": dict(R=4096, C=4096, L=2048, r=16, pattern="rowwise", dtype="f32",
+                 desc="LoRS linear 4096x4096, 50% per-row, r=16, 2048 tokens (BASELINE configs[0], fp32 parity mode)"),
+}
+FALLBACK_PEAKS = dict(bf16_tflops=1590.0, hbm_gbs=6650.0)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return FALLBACK_PEAKS, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle port (float64 numpy)
+# ---------------------------------------------------------------------------
+def cpu_inputs(cfg, L_sample, seed=0):
+    import numpy as np
+    from oracle import lors_oracle as orc
+    rng = np.random.default_rng(seed)
+    R, C, r = cfg["R"], cfg["C"], cfg["r"]
+    w = rng.normal(0, 0.02, size=(R, C))
+    w = orc.prune_two_four(w) if cfg["pattern"] == "two_four" else orc.prune_rowwise(w, 0.5)
+    a = rng.normal(0, 1e-3, size=(R, r))
+    b = rng.normal(0, 1 / np.sqrt(r), size=(r, C))
+    x = rng.normal(size=(C, L_sample))
+    dy = rng.normal(size=(R, L_sample))
+    return w, a, b, x, dy
+
+
+def cpu_step(w, a, b, x, dy):
+    from oracle import lors_oracle as orc
+    orc.lors_forward(w, a, b, x, 2.0)
+    orc.lors_backward(w, a, b, x, dy, 2.0)
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(cfg, L_sample=1024, reps=3):
+    """Time the float64 port of lors_forward+lors_backward on a token sample."""
+    w, a, b, x, dy = cpu_inputs(cfg, L_sample)
+    cpu_step(w, a, b, x, dy)  # warm
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        cpu_step(w, a, b, x, dy)
+        ts.append(time.perf_counter() - t0)
+    med = statistics.median(ts)
+    return {"value": L_sample / med, "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
+            "sample": f"{L_sample} tokens of the {cfg['R']}x{cfg['C']} r={cfg['r']} layer, float64 numpy "
+                      f"(OpenBLAS threads = {cpu_cores()}), median of {reps} fwd+bwd; full step holds "
+                      f"{cfg['L']} tokens",
+            "s_per_sample_step": med}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    L_sample = 1024
+    w, a, b, x, dy = cpu_inputs(cfg, L_sample)
+    for _ in range(max(args.warmup, 1)):
+        cpu_step(w, a, b, x, dy)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cpu_step(w, a, b, x, dy)
+        ts.append(time.perf_counter() - t0)
+    tot = sum(ts)
+    value = L_sample * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "sample_tokens_per_step": L_sample},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
+                         "sample": f"{L_sample} tokens per step of the {cfg['R']}x{cfg['C']} r={cfg['r']} layer, "
+                                   "oracle/lors_oracle.py float64 numpy (reference algorithm, adapters.py:359-406)"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# native arm
+# ---------------------------------------------------------------------------
+def run_native(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_08582_b200 import _native, adapters, ops, prune
+    from paper_2501_08582_b200.module import LoRSLinear
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _native.check(_native.load().lors_device_check())
+
+    R, C, L, r = cfg["R"], cfg["C"], cfg["L"], cfg["r"]
+    dt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+    g = torch.Generator(device=dev).manual_seed(1234)          # replicated W, a, b
+    w = torch.randn(R, C, device=dev, generator=g) * 0.02
+    w = (prune.prune_two_four(w) if cfg["pattern"] == "two_four" else prune.prune_rowwise(w, 0.5)).to(dt)
+    a32 = torch.randn(R, r, device=dev, generator=g) * 1e-3
+    b32 = torch.randn(r, C, device=dev, generator=g) / r ** 0.5
+    gx = torch.Generator(device=dev).manual_seed(99 + rank)    # per-rank token shard
+    x = torch.randn(L, C, device=dev, generator=gx).to(dt)
+    dy = torch.randn(L, R, device=dev, generator=gx).to(dt)
+    a, b = a32.to(dt), b32.to(dt)
+    grad_bucket = torch.empty(R * r + r * C, device=dev, dtype=torch.float32)
+
+    stream = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(times=None):
+        e0, e1, e2 = (ev(), ev(), ev()) if times is not None else (None, None, None)
+        if e0: e0.record(stream)
+        ops.lors_fwd(x, w, a, b, 2.0)
+        if e1: e1.record(stream)
+        dxo, da, db, _ = ops.lors_bwd(x, w, a, b, dy, 2.0)
+        if e2: e2.record(stream)
+        if world > 1:
+            grad_bucket[: R * r].copy_(da.view(-1))
+            grad_bucket[R * r:].copy_(db.view(-1))
+            dist.all_reduce(grad_bucket, op=dist.ReduceOp.AVG)
+        if times is not None:
+            times.append((e0, e1, e2))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    _native.reset_launch_count()
+    t_start, t_end = ev(), ev()
+    times = []
+    t_start.record(stream)
+    for _ in range(args.steps):
+        step(times)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    launches = _native.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = t_start.elapsed_time(t_end) / args.steps
+    fwd_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1, _ in times)
+    bwd_ms = statistics.mean(e1.elapsed_time(e2) for _, e1, e2 in times)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+
+    # per-kernel split inside the backward (dX GEMM vs rank-r products), timed live
+    ebx0, ebx1 = ev(), ev()
+    ebx0.record(stream)
+    for _ in range(3):
+        ops.lors_bwd(x, w, a, b, dy, 2.0, need_dx=False)
+    ebx1.record(stream)
+    torch.cuda.synchronize()
+    rank_r_ms = ebx0.elapsed_time(ebx1) / 3
+    dx_ms = max(bwd_ms - rank_r_ms, 1e-6)
+
+    # ---------------- end-to-end through the public module API (host buffers)
+    layer = LoRSLinear(w, a=a32, b=b32, alpha=2.0).to(dev)
+    hx = x.cpu().pin_memory()
+    hdy = dy.cpu().pin_memory()
+    hda = torch.empty(R, r, dtype=torch.float32).pin_memory()
+    hdb = torch.empty(r, C, dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        xd = hx.to(dev, non_blocking=True).requires_grad_(True)
+        dyd = hdy.to(dev, non_blocking=True)
+        layer.a.grad = None
+        layer.b.grad = None
+        y = layer(xd)
+        y.backward(dyd)
+        if world > 1:
+            grad_bucket[: R * r].copy_(layer.a.grad.view(-1))
+            grad_bucket[R * r:].copy_(layer.b.grad.view(-1))
+            dist.all_reduce(grad_bucket, op=dist.ReduceOp.AVG)
+        hda.copy_(layer.a.grad, non_blocking=True)
+        hdb.copy_(layer.b.grad, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.reset_peak_memory_stats(dev)
+    e0, e1 = ev(), ev()
+    e2e_steps = max(3, min(args.steps, 10))
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    peak_gb = torch.cuda.max_memory_allocated(dev) / 1e9
+    if world > 1:
+        tt = torch.tensor([e2e_ms, peak_gb], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms, peak_gb = float(tt[0]), float(tt[1])
+
+    if rank == 0:
+        pk, pk_kind = peaks()
+        cost = adapters.predict_cost("lors", R, C, L, r)
+        fwd_flops = 2 * cost.macs_forward                       # one K1 launch (RCL + rRC + RC)
+        dx_flops = 2 * (R * C * L + r * R * C + R * C)          # one K3 launch (dX GEMM + its recompute)
+        # dominant kernel = the larger of K1 (fwd) and K3 (dX)
+        if dx_ms >= fwd_ms:
+            dom, dom_ms, dom_flops = "tc_lors_gemm<dx> (K3, dX = dY W_eff)", dx_ms, dx_flops
+        else:
+            dom, dom_ms, dom_flops = "tc_lors_gemm<fwd> (K1, Y = X W_eff^T)", fwd_ms, fwd_flops
+        peak_tf = float(pk.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])) if dt == torch.bfloat16 else None
+        achieved = dom_flops / (dom_ms * 1e-3) / 1e12
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic_latest.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                tr = json.load(f)
+            key = "dx" if "dx" in dom else "fwd"
+            traffic = tr.get(key, {}).get("dram_bytes_per_launch")
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                    "frac": (achieved / peak_tf) if peak_tf else None, "traffic": traffic,
+                    "kernel": dom, "peak_kind": pk_kind + (" bf16 burst" if peak_tf else ""),
+                    "algorithmic_flops_per_launch": dom_flops, "ms_per_launch": dom_ms}
+        step_flops = cost.flops
+        tokens = L * world
+        line = {
+            "metric": METRIC, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
+            "config": {"workload": cfg["desc"], "tokens_per_gpu": L, "R": R, "C": C, "rank": r, "alpha": 2.0,
+                       "sparsity": cfg["pattern"], "forward": "dense-masked tcgen05 (W_eff rebuilt on chip)",
+                       "adapter_grads": "ste (lors)", "parallelism": f"dp{world}",
+                       "l2": "inputs larger than L2 (W 90 MB + X 64 MB + dY 180 MB per step, 126 MB L2)"},
+            "peak_hbm_gb": peak_gb,
+            "step_breakdown_ms": {"fwd": fwd_ms, "bwd": bwd_ms, "bwd_dx_gemm": dx_ms, "bwd_rank_r": rank_r_ms},
+            "algorithmic_tflops": step_flops / (ms * 1e-3) / 1e12,
+            "roofline": roofline,
+            "gpu_launches": launches,
+            "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": x.numel() * x.element_size() + dy.numel() * dy.element_size(),
+                    "d2h_bytes_per_step": (R * r + r * C) * 4,
+                    "ms_per_step": e2e_ms, "api": "LoRSLinear.forward + backward (autograd), pinned host X/dY in, "
+                                                  "dA/dB out"},
+            "clocks": clk,
+        }
+        if world == 1 and not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("native", "reference"), default="native")
+    ap.add_argument("--config", choices=tuple(CONFIGS), default="cfg2")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline sample")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_native(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
