@@ -22,6 +22,12 @@
 #include "lors_tc.cuh"
 #include "ptx_sm100.cuh"
 
+#ifdef LORS_DEBUG_HANG
+extern "C" int lors_debug_hang_info(unsigned int* out) {
+  return (int)cudaMemcpyFromSymbol(out, lors::ptx::g_lors_hang, sizeof(unsigned int) * 64);
+}
+#endif
+
 namespace lors {
 using bf16 = __nv_bfloat16;
 using namespace ptx;
@@ -269,88 +275,118 @@ static int skinny(int rp, const bf16* A, const bf16* B, void* out, int M, int N,
 }
 
 // ===========================================================================
-// K1 / K3: GEMM with W_eff rebuilt in the prologue.
+// K1 / K3: GEMM with W_eff rebuilt in the prologue, on CTA pairs.
 //
 //   out[l, m] = sum_k act[l, k] * Weff'(m, k)
 //   FWD (DX=false): act = X_t [L, C], m over R, k over C, Weff'(m,k) = Weff[m,k]
 //   DX  (DX=true) : act = dY_t [L, R], m over C, k over R, Weff'(m,k) = Weff[k,m]
 //
-// CTA tile: 128 output features (TMEM lanes) x 256 tokens (TMEM columns),
-// k-step 64.  Per k-step:
-//   TMA   : W tile, act tile [256 x 64] (SW128), streamed adapter factor
-//   MMA   : recompute D_re[128 x 64] = F . S^T (K = r) into TMEM (2 buffers)
-//   xform : 8 warps read D_re (tcgen05.ld), add W, select on the mask, round
-//           to bf16, store the K-major SW128 W_eff tile (2 buffers)
-//   MMA   : D[128 x 256] += W_eff . act^T (4 x K16)
+// A cluster of two CTAs computes a 256 (features) x 256 (tokens) tile with
+// tcgen05 cta_group::2: CTA c owns features m0 + 128c .. +127 (its TMEM lanes,
+// its W / W_eff tiles) and stages tokens l0 + 128c .. +127 of the activation
+// tile; the pair MMA (M = 256, N = 256, K = 16) reads both halves, so each SM
+// streams half of the activation tile from L2.  Per 64-wide k-step:
+//   TMA   : W tile (own rows), activation half, streamed adapter-factor half
+//   MMA   : recompute D_re[256 x 64] = F . S^T (K = r) into TMEM (2 buffers)
+//   xform : 8 warps per CTA read D_re (tcgen05.ld), add W, select on the mask,
+//           round to bf16 and store the K-major SW128 W_eff tile (2 buffers)
+//   MMA   : D[256 x 256] += W_eff . act^T (4 x K16), leader CTA issues
 // The recompute of step i is issued before the main MMA of step i-1, so the
 // transform of step i overlaps the tensor-core work of step i-1.
-// warps 0-7: transform + epilogue, warp 8: TMA producer, warp 9: MMA issuer.
+// warps 0-7: transform + epilogue, warp 8: TMA producer, warp 9: MMA issuer
+// (leader CTA) and TMEM owner.
 // ===========================================================================
+struct alignas(16) Bar16 {
+  uint64_t b;
+  uint64_t pad;
+};
+
 namespace rg {
-constexpr int BM = 128, BN = 256, BK = 64, THREADS = 320, XFORM_THREADS = 256;
-constexpr uint32_t ACT_BYTES = BN * BK * 2;   // 32 KB
-constexpr uint32_t W_BYTES = BM * BK * 2;     // 16 KB
-constexpr uint32_t WEFF_BYTES = BM * BK * 2;  // 16 KB
+constexpr int BM = 128, BN = 256, BK = 64;
+constexpr int THREADS = 384, XFORM_THREADS = 256;
+constexpr int NE = 4;   // early ring: W tile + streamed adapter-factor half (recompute, transform)
+constexpr int NA = 4;   // activation ring (main MMA)
+constexpr int NW = 3;   // W_eff buffers
+constexpr int NRE = 4;  // TMEM recompute buffers
+constexpr int D = 3;    // recompute lookahead (steps)
+constexpr uint32_t ACT_BYTES = (BN / 2) * BK * 2;   // 16 KB: this CTA's token half
+constexpr uint32_t W_BYTES = BM * BK * 2;           // 16 KB
+constexpr uint32_t WEFF_BYTES = BM * BK * 2;        // 16 KB
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t RE_COL = 256;              // recompute buffers at TMEM cols 256 / 320
+constexpr uint32_t RE_COL = 256;                    // recompute buffers at TMEM cols 256 + 64 b
 template <int RP>
-constexpr int stages() { return 3; }
-template <int RP>
-constexpr uint32_t sf_bytes() { return 64 * RP * 2; }   // streamed factor tile (64 k x RP)
+constexpr uint32_t sf_bytes() { return 32 * RP * 2; }   // streamed factor half (32 k x RP)
 template <int RP>
 constexpr uint32_t ff_bytes() { return 128 * RP * 2; }  // fixed factor tile (128 m x RP)
 template <int RP>
-constexpr uint32_t stage_bytes() { return W_BYTES + ACT_BYTES + sf_bytes<RP>(); }
+constexpr uint32_t early_bytes() { return W_BYTES + sf_bytes<RP>(); }
 template <int RP>
 constexpr size_t smem_bytes() {
-  return 1024 + stages<RP>() * stage_bytes<RP>() + 2 * WEFF_BYTES + ff_bytes<RP>() + 256;
+  return 1024 + NE * early_bytes<RP>() + NA * ACT_BYTES + NW * WEFF_BYTES + ff_bytes<RP>() + 1024;
 }
 }  // namespace rg
 
-template <bool DX, int RP>
-__global__ void __launch_bounds__(rg::THREADS, 1)
+template <bool DX, int RP, bool BITS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
     tc_lors_gemm_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmF,
                         const __grid_constant__ CUtensorMap tmOut, const bf16* __restrict__ bias,
                         const uint32_t* __restrict__ bits, int words_per_row, int Mout, int Kred, float alpha) {
   using namespace rg;
-  constexpr int S = stages<RP>();
-  constexpr uint32_t SF = sf_bytes<RP>(), FF = ff_bytes<RP>(), STG = stage_bytes<RP>();
+  constexpr uint32_t SF = sf_bytes<RP>(), FF = ff_bytes<RP>(), EB = early_bytes<RP>();
   constexpr uint32_t SWR = RP * 2;  // swizzle span of the K-major rank-r tiles
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // stage s: [W | act | streamed factor]
-  uint8_t* stage0 = smem;
-  uint8_t* weff = smem + S * STG;           // 2 buffers
-  uint8_t* ffac = weff + 2 * WEFF_BYTES;    // fixed factor
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ffac + FF);
-  uint64_t* full = bars;                    // [S]   TMA -> MMA / xform
-  uint64_t* empty = full + S;               // [S]   main MMA -> TMA
-  uint64_t* refull = empty + S;             // [2]   recompute MMA -> xform
-  uint64_t* reempty = refull + 2;           // [2]   xform -> MMA
-  uint64_t* wready = reempty + 2;           // [2]   xform -> main MMA
-  uint64_t* wempty = wready + 2;            // [2]   main MMA -> xform
-  uint64_t* ffull = wempty + 2;             // fixed factor landed
-  uint64_t* accf = ffull + 1;               // accumulator complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  uint8_t* early = smem;                     // [NE] W tile | streamed factor half
+  uint8_t* actb = early + NE * EB;           // [NA] activation halves
+  uint8_t* weff = actb + NA * ACT_BYTES;     // [NW]
+  uint8_t* ffac = weff + NW * WEFF_BYTES;    // fixed factor
+  // mbarriers, one per 16 bytes
+  Bar16* bars = reinterpret_cast<Bar16*>(ffac + FF);
+  Bar16* e_full = bars;                 // [NE] local: W + factor half landed
+  Bar16* e_empty = e_full + NE;         // [NE] local: recompute commit + 8 transform warps done
+  Bar16* a_full = e_empty + NE;         // [NA] local: activation half landed
+  Bar16* a_empty = a_full + NA;         // [NA] local: pair MMA done with it
+  Bar16* refull = a_empty + NA;         // [NRE] local: recompute landed in TMEM
+  Bar16* reempty = refull + NRE;        // [NRE] leader: 16 warps read it
+  Bar16* wready = reempty + NRE;        // [NW] leader: 16 warps wrote their W_eff halves
+  Bar16* wempty = wready + NW;          // [NW] local: pair MMA done with the buffer
+  Bar16* p_early = wempty + NW;         // [NE] leader: peer's early stage landed (relayed)
+  Bar16* p_act = p_early + NE;          // [NA] leader: peer's activation half landed (relayed)
+  uint64_t* ffull = &(p_act + NA)->b;   // local: own fixed factor landed
+  uint64_t* pffull = &(p_act + NA + 1)->b;  // leader: peer's fixed factor landed (relayed)
+  uint64_t* accf = &(p_act + NA + 2)->b;    // local: accumulator complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_act + NA + 3);
 
   const int warp = warp_id(), lane = lane_id();
-  const int m0 = blockIdx.x * BM;
-  const int l0 = blockIdx.y * BN;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int m0 = (blockIdx.x >> 1) * (2 * BM) + rank * BM;   // this CTA's features
+  const int l0 = blockIdx.y * BN;                             // the pair's tokens
+  const int lh = l0 + rank * (BN / 2);                        // this CTA's token half
   const int nk = (Kred + BK - 1) / BK;
 
   if (warp == 8 && lane == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int i = 0; i < NE; ++i) {
+      mbar_init(&e_full[i].b, 1);
+      mbar_init(&e_empty[i].b, 9);
+      mbar_init(&p_early[i].b, 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&refull[b], 1);
-      mbar_init(&reempty[b], 8);
-      mbar_init(&wready[b], 8);
-      mbar_init(&wempty[b], 1);
+    for (int i = 0; i < NA; ++i) {
+      mbar_init(&a_full[i].b, 1);
+      mbar_init(&a_empty[i].b, 1);
+      mbar_init(&p_act[i].b, 1);
+    }
+    for (int i = 0; i < NRE; ++i) {
+      mbar_init(&refull[i].b, 1);
+      mbar_init(&reempty[i].b, 16);
+    }
+    for (int i = 0; i < NW; ++i) {
+      mbar_init(&wready[i].b, 16);
+      mbar_init(&wempty[i].b, 1);
     }
     mbar_init(ffull, 1);
+    mbar_init(pffull, 1);
     mbar_init(accf, 1);
     fence_barrier_init();
     tma_prefetch_desc(&tmAct);
@@ -359,51 +395,93 @@ __global__ void __launch_bounds__(rg::THREADS, 1)
     tma_prefetch_desc(&tmF);
     tma_prefetch_desc(&tmOut);
   }
-  if (warp == 9) tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == 9) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // Every TMA completes on a barrier of the CTA that issued it; the leader
+  // learns about the peer's stages through relayed remote arrives, and the
+  // transform warps of both CTAs arrive remotely on the leader's reempty /
+  // wready.  Remote arrives address the leader through mapa.
+  const uint32_t reempty_l = mapa_shared(smem_u32(reempty), 0);
+  const uint32_t wready_l = mapa_shared(smem_u32(wready), 0);
+  const uint32_t p_early_l = mapa_shared(smem_u32(p_early), 0);
+  const uint32_t p_act_l = mapa_shared(smem_u32(p_act), 0);
+  const uint32_t pffull_l = mapa_shared(smem_u32(pffull), 0);
 
   if (warp == 8) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ early-ring producer (both CTAs)
     if (lane == 0) {
       mbar_arrive_expect_tx(ffull, FF);
-      if (DX) {  // b [r, C] as MN-major A of the recompute: two 64-wide atoms
+      if (DX) {  // b [r, C] as MN-major A of the recompute: two 64-wide atoms of this CTA's columns
         tma_load_2d(ffac, &tmF, ffull, m0, 0);
         tma_load_2d(ffac + FF / 2, &tmF, ffull, m0 + 64, 0);
-      } else {   // a [R, r] K-major
+      } else {   // a [R, r] K-major, this CTA's rows
         tma_load_2d(ffac, &tmF, ffull, 0, m0);
       }
       for (int i = 0; i < nk; ++i) {
-        const int s = i % S;
-        const uint32_t ph = (i / S) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], STG);
-        uint8_t* st = stage0 + s * STG;
+        const int e = i % NE;
+        mbar_wait(&e_empty[e].b, ((i / NE) & 1) ^ 1);
+        uint8_t* st = early + e * EB;
         const int k0 = i * BK;
-        if (DX) tma_load_2d(st, &tmW, &full[s], m0, k0);   // W[k0:k0+64, m0:m0+128], no swizzle
-        else tma_load_2d(st, &tmW, &full[s], k0, m0);      // W[m0:m0+128, k0:k0+64], SW128
-        tma_load_2d(st + W_BYTES, &tmAct, &full[s], k0, l0);
-        if (DX) tma_load_2d(st + W_BYTES + ACT_BYTES, &tmS, &full[s], 0, k0);  // a[k0:k0+64, :] K-major
-        else tma_load_2d(st + W_BYTES + ACT_BYTES, &tmS, &full[s], k0, 0);     // b[:, k0:k0+64] MN-major
+        mbar_arrive_expect_tx(&e_full[e].b, EB);
+        if (DX) {  // W[k0:k0+64, m0:m0+128] as two SW128 boxes of 64 columns
+          tma_load_2d(st, &tmW, &e_full[e].b, m0, k0);
+          tma_load_2d(st + W_BYTES / 2, &tmW, &e_full[e].b, m0 + 64, k0);
+          tma_load_2d(st + W_BYTES, &tmS, &e_full[e].b, 0, k0 + 32 * rank);   // a rows, K-major
+        } else {   // W[m0:m0+128, k0:k0+64], SW128
+          tma_load_2d(st, &tmW, &e_full[e].b, k0, m0);
+          tma_load_2d(st + W_BYTES, &tmS, &e_full[e].b, k0 + 32 * rank, 0);   // b cols, MN-major
+        }
+      }
+    }
+  } else if (warp == 10) {
+    // ------------------------------------------------------------ activation-ring producer (both CTAs)
+    if (lane == 0) {
+      for (int i = 0; i < nk; ++i) {
+        const int a = i % NA;
+        mbar_wait(&a_empty[a].b, ((i / NA) & 1) ^ 1);
+        mbar_arrive_expect_tx(&a_full[a].b, ACT_BYTES);
+        tma_load_2d(actb + a * ACT_BYTES, &tmAct, &a_full[a].b, i * BK, lh);
+      }
+    }
+  } else if (warp == 11) {
+    // ------------------------------------------------------------ activation relay (peer CTA)
+    if (!leader && lane == 0) {
+      for (int i = 0; i < nk; ++i) {
+        const int a = i % NA;
+        mbar_wait(&a_full[a].b, (i / NA) & 1);
+        mbar_arrive_cluster(p_act_l + a * 16);
       }
     }
   } else if (warp == 9) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc_re = make_idesc_bf16(128, 64, DX, !DX);
-      constexpr uint32_t idesc_main = make_idesc_bf16(128, 256, false, false);
+    if (!leader) {
+      // ---------------------------------------------------------- early relay (peer CTA)
+      if (lane == 0) {
+        mbar_wait(ffull, 0);
+        mbar_arrive_cluster(pffull_l);
+        for (int i = 0; i < nk; ++i) {
+          const int e = i % NE;
+          mbar_wait(&e_full[e].b, (i / NE) & 1);
+          mbar_arrive_cluster(p_early_l + e * 16);
+        }
+      }
+    } else if (lane == 0) {
+      // ---------------------------------------------------------- MMA issuer (leader CTA)
+      constexpr uint32_t idesc_re = make_idesc_bf16(256, 64, DX, !DX);
+      constexpr uint32_t idesc_main = make_idesc_bf16(256, 256, false, false);
       mbar_wait(ffull, 0);
+      mbar_wait_cluster(pffull, 0);
       const uint32_t ff_base = smem_u32(ffac);
-      for (int i = 0; i <= nk; ++i) {
-        if (i < nk) {
-          const int s = i % S;
-          const int rb = i & 1;
-          mbar_wait(&full[s], (i / S) & 1);
-          mbar_wait(&reempty[rb], ((i >> 1) & 1) ^ 1);
+      for (int j = 0; j < nk + D; ++j) {
+        if (j < nk) {  // recompute for step j, D steps ahead of its main MMA
+          const int e = j % NE, rb = j % NRE;
+          mbar_wait(&e_full[e].b, (j / NE) & 1);
+          mbar_wait_cluster(&p_early[e].b, (j / NE) & 1);
+          mbar_wait_cluster(&reempty[rb].b, ((j / NRE) & 1) ^ 1);
           tc_fence_after();
-          const uint32_t sf_base = smem_u32(stage0 + s * STG + W_BYTES + ACT_BYTES);
+          const uint32_t sf_base = smem_u32(early + e * EB + W_BYTES);
 #pragma unroll
           for (int kk = 0; kk < RP / 16; ++kk) {
             uint64_t ad, bd;
@@ -412,30 +490,32 @@ __global__ void __launch_bounds__(rg::THREADS, 1)
               bd = make_sdesc(sf_base + kk * 32, 16, 8 * SWR, sw_layout(SWR));       // a rows, K-major
             } else {
               ad = make_sdesc(ff_base + kk * 32, 16, 8 * SWR, sw_layout(SWR));       // a rows, K-major
-              bd = make_sdesc(sf_base + kk * 2048, 0, 1024, SW_128);                 // b cols, MN-major
+              bd = make_sdesc(sf_base + kk * 16 * 64, 0, 8 * 64, SW_64);             // b cols, MN-major (32 wide)
             }
-            mma_bf16(tmem + RE_COL + rb * 64, ad, bd, idesc_re, kk > 0 ? 1u : 0u);
+            mma_bf16_pair(tmem + RE_COL + rb * 64, ad, bd, idesc_re, kk > 0 ? 1u : 0u);
           }
-          mma_commit(&refull[rb]);
+          mma_commit_pair(&refull[rb].b, 0x3);
+          mma_commit_pair(&e_empty[e].b, 0x3);
         }
-        if (i >= 1) {
-          const int j = i - 1;
-          const int s = j % S;
-          const int wb = j & 1;
-          mbar_wait(&wready[wb], (j >> 1) & 1);
+        const int jm = j - D;
+        if (jm >= 0) {  // main MMA for step jm
+          const int a = jm % NA, wb = jm % NW;
+          mbar_wait(&a_full[a].b, (jm / NA) & 1);
+          mbar_wait_cluster(&p_act[a].b, (jm / NA) & 1);
+          mbar_wait_cluster(&wready[wb].b, (jm / NW) & 1);
           tc_fence_after();
           const uint32_t a_base = smem_u32(weff + wb * WEFF_BYTES);
-          const uint32_t b_base = smem_u32(stage0 + s * STG + W_BYTES);
+          const uint32_t b_base = smem_u32(actb + a * ACT_BYTES);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            mma_bf16(tmem, make_sdesc(a_base + kk * 32, 16, 1024, SW_128), make_sdesc(b_base + kk * 32, 16, 1024, SW_128),
-                     idesc_main, (j > 0 || kk > 0) ? 1u : 0u);
+            mma_bf16_pair(tmem, make_sdesc(a_base + kk * 32, 16, 1024, SW_128),
+                          make_sdesc(b_base + kk * 32, 16, 1024, SW_128), idesc_main, (jm > 0 || kk > 0) ? 1u : 0u);
           }
-          mma_commit(&empty[s]);
-          mma_commit(&wempty[wb]);
+          mma_commit_pair(&a_empty[a].b, 0x3);
+          mma_commit_pair(&wempty[wb].b, 0x3);
         }
       }
-      mma_commit(accf);
+      mma_commit_pair(accf, 0x3);
     }
   } else {
     // ------------------------------------------------------------ transform warps 0..7
@@ -444,81 +524,117 @@ __global__ void __launch_bounds__(rg::THREADS, 1)
     const int t = q * 32 + lane;   // feature row inside the tile (TMEM lane)
     const int gm = m0 + t;         // global output feature
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    const uint32_t alpha2 = pack_bf16x2(alpha, alpha);
     for (int i = 0; i < nk; ++i) {
-      const int s = i % S;
-      const int rb = i & 1;
-      // 1. rank-r product of this k-step, 32 columns for this thread's row
-      mbar_wait(&refull[rb], (i >> 1) & 1);
+      const int e = i % NE, rb = i % NRE, wb = i % NW;
+      // 1. rank-r product of this k-step (TMEM -> registers), then release the buffer
+      mbar_wait(&refull[rb].b, (i / NRE) & 1);
       tc_fence_after();
       uint32_t p[32];
-      tmem_ld_x32(tmem + lane_addr + RE_COL + rb * 64 + h * 32, p);
+      const uint32_t re_col = RE_COL + rb * 64 + h * 32;
+      if (!DX) {
+        tmem_ld_x32(tmem + lane_addr + re_col, p);
+      } else {  // fragment layout matching ldmatrix.trans, two 16-lane groups
+        uint32_t (&p0)[16] = *reinterpret_cast<uint32_t(*)[16]>(&p[0]);
+        uint32_t (&p1)[16] = *reinterpret_cast<uint32_t(*)[16]>(&p[16]);
+        tmem_ld_16x256b_x4(tmem + lane_addr + re_col, p0);
+        tmem_ld_16x256b_x4(tmem + lane_addr + (16u << 16) + re_col, p1);
+      }
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&reempty[rb]);
-      // 2. W values (TMA landed) and the destination buffer free
-      mbar_wait(&full[s], (i / S) & 1);
-      mbar_wait(&wempty[rb], ((i >> 1) & 1) ^ 1);
-      const uint8_t* wt = stage0 + s * STG;
-      uint8_t* dst = weff + rb * WEFF_BYTES + t * 128;
-      const int kbase = i * BK + h * 32;
-      uint32_t mword = 0xFFFFFFFFu;
-      if (bits != nullptr) {
-        if (!DX) {
-          mword = (gm < Mout) ? __ldg(bits + (int64_t)gm * words_per_row + (kbase >> 5)) : 0u;
-        }
-      }
+      if (lane == 0) mbar_arrive_cluster(reempty_l + rb * 16);
+      // 2. W tile landed, destination buffer drained by the MMA of step i - NW
+      mbar_wait(&e_full[e].b, (i / NE) & 1);
+      mbar_wait(&wempty[wb].b, ((i / NW) & 1) ^ 1);
+      const uint32_t wt = smem_u32(early + e * EB);
+      const uint32_t dst = smem_u32(weff + wb * WEFF_BYTES);
+      if (!DX) {
+        // thread = W row; 4 chunks of 8 k-values, same swizzled position in and out
+        uint32_t mword = 0;
+        if (BITS) mword = (gm < Mout) ? __ldg(bits + (int64_t)gm * words_per_row + ((i * BK + h * 32) >> 5)) : 0u;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {  // 4 chunks of 8 k-values
-        float wv[8];
-        if (!DX) {
-          const uint4 raw = *reinterpret_cast<const uint4*>(wt + t * 128 + (((h * 4 + c) ^ (t & 7)) << 4));
-          const bf16* e = reinterpret_cast<const bf16*>(&raw);
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t off = (uint32_t)t * 128 + ((((uint32_t)h * 4 + c) ^ ((uint32_t)t & 7)) << 4);
+          uint4 raw;
+          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
+                       : "r"(wt + off));
+          const uint32_t wv[4] = {raw.x, raw.y, raw.z, raw.w};
+          uint32_t o[4];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) wv[u] = __bfloat162float(e[u]);
-        } else {
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            wv[u] = __bfloat162float(*reinterpret_cast<const bf16*>(wt + (h * 32 + c * 8 + u) * 256 + t * 2));
-        }
-        uint32_t pk[4];
-#pragma unroll
-        for (int u = 0; u < 8; u += 2) {
-          float o[2];
-#pragma unroll
-          for (int e2 = 0; e2 < 2; ++e2) {
-            const int kk = c * 8 + u + e2;  // 0..31 within this thread's half
-            bool keep;
-            if (bits == nullptr) {
-              keep = wv[u + e2] != 0.0f;
-            } else if (!DX) {
-              keep = (mword >> kk) & 1u;
-            } else {
-              const int64_t krow = kbase + kk;
-              keep = (gm < Mout && krow < Kred)
-                         ? ((__ldg(bits + krow * words_per_row + (gm >> 5)) >> (gm & 31)) & 1u)
-                         : false;
-            }
-            o[e2] = keep ? fmaf(alpha, __uint_as_float(p[kk]), wv[u + e2]) : 0.0f;
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t keep = BITS ? bits2_to_mask((mword >> (c * 8 + 2 * u)) & 3u) : nonzero_mask_bf16x2(wv[u]);
+            o[u] = weff_pair(wv[u], __uint_as_float(p[c * 8 + 2 * u]), __uint_as_float(p[c * 8 + 2 * u + 1]), alpha2,
+                             keep);
           }
-          pk[u / 2] = pack_bf16x2(o[0], o[1]);
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + off), "r"(o[0]), "r"(o[1]), "r"(o[2]),
+                       "r"(o[3])
+                       : "memory");
         }
-        *reinterpret_cast<uint4*>(dst + (((h * 4 + c) ^ (t & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      } else {
+        // W tile [64 k][128 c] as two SW128 boxes of 64 c.  ldmatrix.trans hands
+        // thread l the pair (k = 32h + 8j + 2(l%4) + {0,1}, c = 32q + 16g + 8s + l/4),
+        // the positions p[16g + 4j + 2s + {0,1}] hold; results go to the K-major
+        // W_eff^T tile (row c) as 32-bit pairs.
+        const int mi = lane >> 3, rr = lane & 7;
+        uint32_t bword[8];
+        if (BITS) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e2 = 0; e2 < 2; ++e2) {
+              const int64_t kr = (int64_t)i * BK + h * 32 + 8 * j + 2 * (lane & 3) + e2;
+              bword[j * 2 + e2] = kr < Kred ? __ldg(bits + kr * words_per_row + ((m0 + q * 32) >> 5)) : 0u;
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+#pragma unroll
+          for (int jp = 0; jp < 2; ++jp) {
+            uint32_t wv[4];
+            {
+              const int sa = mi & 1, ja = 2 * jp + (mi >> 1);
+              const uint32_t k = h * 32 + 8 * ja + rr;
+              const uint32_t c = q * 32 + 16 * g + 8 * sa;
+              ldsm_x4_trans(wt + (c >> 6) * 8192 + k * 128 + ((((c & 63) >> 3) ^ (k & 7)) << 4), wv);
+            }
+#pragma unroll
+            for (int mm = 0; mm < 4; ++mm) {
+              const int sm = mm & 1, j = 2 * jp + (mm >> 1);
+              const uint32_t ct = q * 32 + 16 * g + 8 * sm + (lane >> 2);
+              const uint32_t k = h * 32 + 8 * j + 2 * (lane & 3);
+              uint32_t keep;
+              if (BITS) {
+                const uint32_t cb = ct & 31;
+                keep = bits2_to_mask(((bword[j * 2] >> cb) & 1u) | (((bword[j * 2 + 1] >> cb) & 1u) << 1));
+              } else {
+                keep = nonzero_mask_bf16x2(wv[mm]);
+              }
+              const uint32_t o = weff_pair(wv[mm], __uint_as_float(p[16 * g + 4 * j + 2 * sm]),
+                                           __uint_as_float(p[16 * g + 4 * j + 2 * sm + 1]), alpha2, keep);
+              sts32(dst + ct * 128 + ((((k >> 3)) ^ (ct & 7)) << 4) + (k & 7) * 2, o);
+            }
+          }
+        }
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&wready[rb]);
+      if (lane == 0) {
+        mbar_arrive(&e_empty[e].b);                  // done reading the W tile
+        mbar_arrive_cluster(wready_l + wb * 16);     // W_eff half ready for the pair MMA
+      }
     }
     // ------------------------------------------------------------ epilogue
     mbar_wait(accf, 0);
     tc_fence_after();
-    // stage [256 tokens][128 features] bf16 (256 B rows) in the drained pipeline buffers
+    // stage [256 tokens][128 features] bf16 (256 B rows) in the drained ring buffers
     uint8_t* stg = smem;
     float bv = 0.f;
     if (!DX && bias != nullptr && gm < Mout) bv = __bfloat162float(bias[gm]);
 #pragma unroll 1
     for (int c0 = 0; c0 < 128; c0 += 32) {
-      const int col = h * 128 + c0;  // token offset inside the tile
+      const int col = h * 128 + c0;  // token offset inside the pair tile
       uint32_t v[32];
       tmem_ld_x32(tmem + lane_addr + col, v);
       tmem_ld_wait();
@@ -536,8 +652,8 @@ __global__ void __launch_bounds__(rg::THREADS, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == 9) tmem_dealloc<TMEM_COLS>(tmem);
+  cluster_sync();
+  if (warp == 9) tmem_dealloc_pair<TMEM_COLS>(tmem);
 }
 
 template <bool DX, int RP>
@@ -548,23 +664,23 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
   const int Mout = DX ? C : R, Kred = DX ? R : C;
   CUtensorMap tAct, tW, tS, tF, tOut;
   int st;
-  if ((st = make_map(&tAct, act, Kred, L, 64, BN, 128, "activation"))) return st;
-  if (DX) st = make_map(&tW, w, C, R, 128, 64, 0, "W (dX)");
+  if ((st = make_map(&tAct, act, Kred, L, 64, BN / 2, 128, "activation"))) return st;
+  if (DX) st = make_map(&tW, w, C, R, 64, 64, 128, "W (dX)");
   else st = make_map(&tW, w, C, R, 64, 128, 128, "W (fwd)");
   if (st) return st;
   if (DX) {
-    if ((st = make_map(&tS, a, r, R, RP, 64, RP * 2, "a (streamed)"))) return st;
+    if ((st = make_map(&tS, a, r, R, RP, 32, RP * 2, "a (streamed half)"))) return st;
     if ((st = make_map(&tF, b, C, r, 64, RP, 128, "b (fixed)"))) return st;
   } else {
-    if ((st = make_map(&tS, b, C, r, 64, RP, 128, "b (streamed)"))) return st;
+    if ((st = make_map(&tS, b, C, r, 32, RP, 64, "b (streamed half)"))) return st;
     if ((st = make_map(&tF, a, r, R, RP, 128, RP * 2, "a (fixed)"))) return st;
   }
   if ((st = make_map(&tOut, out, Mout, L, 128, BN, 0, "output"))) return st;
-  auto kern = tc_lors_gemm_kernel<DX, RP>;
+  auto kern = bits ? tc_lors_gemm_kernel<DX, RP, true> : tc_lors_gemm_kernel<DX, RP, false>;
   const size_t smem = smem_bytes<RP>();
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "lors_gemm smem attribute");
-  dim3 grid((unsigned)ceil_div(Mout, BM), (unsigned)ceil_div(L, BN));
+  dim3 grid((unsigned)(2 * ceil_div(Mout, 2 * BM)), (unsigned)ceil_div(L, BN));
   kern<<<grid, THREADS, smem, s>>>(tAct, tW, tS, tF, tOut, bias, bits, (int)ceil_div(C, 32), Mout, Kred, alpha);
   LORS_CHECK_LAUNCH(DX ? "tc_lors_gemm<dx>" : "tc_lors_gemm<fwd>");
   return LORS_OK;

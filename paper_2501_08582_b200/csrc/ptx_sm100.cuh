@@ -45,16 +45,58 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#ifdef LORS_DEBUG_HANG
+// debug builds: a wait that exceeds 1 s records (block, warp, barrier offset,
+// parity) into g_lors_hang and gives up, so the host can read where it hung.
+__device__ unsigned int g_lors_hang[64];
+#endif
 // Wait for the phase with the given parity to complete.  A watchdog traps
-// after ~2^31 polls so a protocol bug surfaces as a launch error, never as a
-// hung GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+// after ~10 s so a protocol bug surfaces as a launch error, never as a hung GPU.
+template <bool CLUSTER>
+__device__ __forceinline__ void mbar_wait_impl(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
+  auto probe = [&]() { return CLUSTER ? mbar_try_wait_cluster(addr, parity) : mbar_try_wait(addr, parity); };
+  if (probe()) return;
+  const uint64_t t0 = globaltimer_ns();
   uint32_t spins = 0;
-  while (!mbar_try_wait(addr, parity)) {
-    if (++spins == 0x80000000u) __trap();
+  while (!probe()) {
+    if ((++spins & 1023u) == 0) {
+#ifdef LORS_DEBUG_HANG
+      if (globaltimer_ns() - t0 > 1000000000ull) {
+        unsigned slot = atomicAdd(&g_lors_hang[0], 1u);
+        if (slot < 15) {
+          g_lors_hang[1 + slot * 4 + 0] = blockIdx.x | (blockIdx.y << 16);
+          g_lors_hang[1 + slot * 4 + 1] = threadIdx.x;
+          g_lors_hang[1 + slot * 4 + 2] = addr;
+          g_lors_hang[1 + slot * 4 + 3] = parity;
+        }
+        return;
+      }
+#else
+      if (globaltimer_ns() - t0 > 10000000000ull) __trap();
+#endif
+    }
   }
 }
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_wait_impl<false>(bar, parity); }
+// wait on a barrier that receives arrives from the peer CTA (cluster-scope acquire)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) { mbar_wait_impl<true>(bar, parity); }
 
 // ---------------------------------------------------------------------------
 // fences
@@ -146,6 +188,18 @@ __device__ __forceinline__ void tmem_ld_x32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
 }
+// 16 lanes x 256 bits, 4 repetitions along columns (32 columns):
+//   v[4j+0..1] = lane (l/4),   columns 8j + 2(l%4) + {0,1}
+//   v[4j+2..3] = lane (l/4)+8, same columns          (l = laneid)
+// -- the same fragment positions ldmatrix.trans delivers, which lets a warp
+// pair TMEM values with transposed shared-memory tiles element for element.
+__device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
@@ -177,6 +231,113 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(uint32_t M, uint32_t N, b
 // swizzle byte width -> UMMA layout code
 __host__ __device__ constexpr uint32_t sw_layout(uint32_t bytes) {
   return bytes == 128 ? SW_128 : bytes == 64 ? SW_64 : bytes == 32 ? SW_32 : SW_NONE;
+}
+
+// ---------------------------------------------------------------------------
+// CTA pairs (cluster of 2, tcgen05 cta_group::2)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// Remote arrive with the default (.release.cta) semantics, as CUTLASS's
+// ClusterBarrier does: an explicit .release.cluster compiles to
+// MEMBAR.ALL.GPU + ERRBAR, which profiled as ~30% of the transform's stalls.
+// Shared-memory producers order their writes with fence.proxy.async first.
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA load into this CTA's shared memory, completion bytes counted on an
+// mbarrier that may live in the peer CTA of the pair (the MMA leader).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cluster_addr, int32_t c0,
+                                                 int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster_addr), "r"(c0), "r"(c1)
+      : "memory");
+}
+template <uint32_t NCOLS>
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem) {  // same warp id in both CTAs
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(NCOLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <uint32_t NCOLS>
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS) : "memory");
+}
+// pair MMA (issued by the leader CTA): M = 256 split over both CTAs' TMEM lanes,
+// A rows and B columns each split between the two CTAs' shared memory.
+__device__ __forceinline__ void mma_bf16_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// commit the leader's pair MMAs to the mbarrier at the same offset in every CTA of `mask`
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// shared-memory fragments
+// ---------------------------------------------------------------------------
+// four 8x8 b16 matrices, transposed: thread l gets, per matrix i, the pair
+// (stored rows 2(l%4), 2(l%4)+1 ; stored column l/4) packed low/high.
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t saddr, uint32_t (&v)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(saddr));
+}
+__device__ __forceinline__ void sts32(uint32_t saddr, uint32_t v) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// packed bf16x2 helpers for the W_eff transform
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ uint32_t fma_bf16x2(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+// 0xFFFF in each half where the bf16 value is nonzero (+-0 -> 0)
+__device__ __forceinline__ uint32_t nonzero_mask_bf16x2(uint32_t w) {
+  uint32_t r;
+  asm("set.ne.u32.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(w), "r"(0u));
+  return r;
+}
+// two mask bits (bit0 -> low half, bit1 -> high half) to a per-half mask
+__device__ __forceinline__ uint32_t bits2_to_mask(uint32_t two) {
+  return ((two & 1u) * 0xFFFFu) | ((two >> 1) * 0xFFFF0000u);
+}
+// W_eff pair = select(M, W + alpha * P, +0): one cvt, one bf16x2 fma, one and.
+__device__ __forceinline__ uint32_t weff_pair(uint32_t w2, float p_lo, float p_hi, uint32_t alpha2, uint32_t keep) {
+  return fma_bf16x2(alpha2, cvt_bf16x2(p_lo, p_hi), w2) & keep;
 }
 
 // ---------------------------------------------------------------------------

@@ -24,3 +24,8 @@ for (L, R, C, r) in [(256, 128, 64, 16), (512, 384, 256, 64), (300, 264, 136, 32
     P = xf @ bf.t(); Q = dyf @ af
     print(f"L={L} R={R} C={C} r={r}: y {rel(y, xf @ weff.t()):.2e}  P {rel(p, P):.2e}  dx {rel(dx, dyf @ weff):.2e}  "
           f"dA {rel(da, 2 * dyf.t() @ P):.2e}  dB {rel(db, 2 * Q.t() @ xf):.2e}", flush=True)
+    bits = ops.pack_mask(w)
+    yb, _ = ops.lors_fwd(x, w, a, b, 2.0, mask_bits=bits)
+    dxb, dab, dbb, _ = ops.lors_bwd(x, w, a, b, dy, 2.0, mask_bits=bits)
+    torch.cuda.synchronize()
+    print("   bits-mode identical:", torch.equal(y, yb), torch.equal(dx, dxb), torch.equal(da, dab), flush=True)
