@@ -304,16 +304,15 @@ struct alignas(16) Bar16 {
 namespace rg {
 constexpr int BM = 128, BN = 256, BK = 64;
 constexpr int THREADS = 384, XFORM_THREADS = 256;
-constexpr int NE = 4;   // early ring: W tile + streamed adapter-factor half (recompute, transform)
-constexpr int NA = 4;   // activation ring (main MMA)
-constexpr int NW = 3;   // W_eff buffers
-constexpr int NRE = 4;  // TMEM recompute buffers
+constexpr int NE = 4;   // early ring (W tile + streamed adapter-factor half) = TMEM recompute buffers
+constexpr int NA = 4;   // activation ring = W_eff buffers
 constexpr int D = 3;    // recompute lookahead (steps)
+constexpr int GROUP_T = 8;  // raster: token tiles per group (clusters of a wave share W and activation tiles)
 constexpr uint32_t ACT_BYTES = (BN / 2) * BK * 2;   // 16 KB: this CTA's token half
 constexpr uint32_t W_BYTES = BM * BK * 2;           // 16 KB
 constexpr uint32_t WEFF_BYTES = BM * BK * 2;        // 16 KB
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t RE_COL = 256;                    // recompute buffers at TMEM cols 256 + 64 b
+constexpr uint32_t RE_COL = 256;                    // recompute buffers at TMEM cols 256 + 64 e
 template <int RP>
 constexpr uint32_t sf_bytes() { return 32 * RP * 2; }   // streamed factor half (32 k x RP)
 template <int RP>
@@ -322,7 +321,7 @@ template <int RP>
 constexpr uint32_t early_bytes() { return W_BYTES + sf_bytes<RP>(); }
 template <int RP>
 constexpr size_t smem_bytes() {
-  return 1024 + NE * early_bytes<RP>() + NA * ACT_BYTES + NW * WEFF_BYTES + ff_bytes<RP>() + 1024;
+  return 1024 + NE * early_bytes<RP>() + NA * ACT_BYTES + NA * WEFF_BYTES + ff_bytes<RP>() + 1024;
 }
 }  // namespace rg
 
@@ -339,56 +338,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* early = smem;                     // [NE] W tile | streamed factor half
   uint8_t* actb = early + NE * EB;           // [NA] activation halves
-  uint8_t* weff = actb + NA * ACT_BYTES;     // [NW]
-  uint8_t* ffac = weff + NW * WEFF_BYTES;    // fixed factor
-  // mbarriers, one per 16 bytes
+  uint8_t* weff = actb + NA * ACT_BYTES;     // [NA] W_eff tiles
+  uint8_t* ffac = weff + NA * WEFF_BYTES;    // fixed factor
+  // mbarriers, one per 16 bytes.  rready / mready are the merged "may issue"
+  // barriers of the leader: count 18 = own producer (with its TMA bytes) +
+  // the peer's relayed landing + 16 transform warps of both CTAs.  In the
+  // peer they only track the peer's own TMA landing (count 1).
   Bar16* bars = reinterpret_cast<Bar16*>(ffac + FF);
-  Bar16* e_full = bars;                 // [NE] local: W + factor half landed
-  Bar16* e_empty = e_full + NE;         // [NE] local: recompute commit + 8 transform warps done
-  Bar16* a_full = e_empty + NE;         // [NA] local: activation half landed
-  Bar16* a_empty = a_full + NA;         // [NA] local: pair MMA done with it
-  Bar16* refull = a_empty + NA;         // [NRE] local: recompute landed in TMEM
-  Bar16* reempty = refull + NRE;        // [NRE] leader: 16 warps read it
-  Bar16* wready = reempty + NRE;        // [NW] leader: 16 warps wrote their W_eff halves
-  Bar16* wempty = wready + NW;          // [NW] local: pair MMA done with the buffer
-  Bar16* p_early = wempty + NW;         // [NE] leader: peer's early stage landed (relayed)
-  Bar16* p_act = p_early + NE;          // [NA] leader: peer's activation half landed (relayed)
-  uint64_t* ffull = &(p_act + NA)->b;   // local: own fixed factor landed
-  uint64_t* pffull = &(p_act + NA + 1)->b;  // leader: peer's fixed factor landed (relayed)
-  uint64_t* accf = &(p_act + NA + 2)->b;    // local: accumulator complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_act + NA + 3);
+  Bar16* rready = bars;                 // [NE] recompute(j) may issue / W+factor landed
+  Bar16* e_empty = rready + NE;         // [NE] local: recompute commit + 8 transform warps done
+  Bar16* mready = e_empty + NE;         // [NA] main(j) may issue / activation landed
+  Bar16* a_empty = mready + NA;         // [NA] local: pair MMA done with the activation half
+  Bar16* refull = a_empty + NA;         // [NE] local: recompute landed in TMEM
+  Bar16* wempty = refull + NE;          // [NA] local: pair MMA done with the W_eff buffer
+  uint64_t* ffull = &(wempty + NA)->b;      // local: own fixed factor landed
+  uint64_t* pffull = &(wempty + NA + 1)->b; // leader: peer's fixed factor landed (relayed)
+  uint64_t* accf = &(wempty + NA + 2)->b;   // local: accumulator complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + NA + 3);
 
   const int warp = warp_id(), lane = lane_id();
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
-  const int m0 = (blockIdx.x >> 1) * (2 * BM) + rank * BM;   // this CTA's features
-  const int l0 = blockIdx.y * BN;                             // the pair's tokens
-  const int lh = l0 + rank * (BN / 2);                        // this CTA's token half
+  // grouped raster over (token tile, feature pair): GROUP_T token tiles x all
+  // feature pairs per group, token tile fastest, so the ~74 clusters of a wave
+  // read ~9 W panels and <= 8 activation panels and both stay L2-resident.
+  int tt, fp;
+  {
+    const int n_t = (int)gridDim.y;  // token tiles
+    const int n_f = (int)(gridDim.x >> 1);
+    const int cid = (int)blockIdx.y * n_f + (int)(blockIdx.x >> 1);
+    const int per_group = GROUP_T * n_f;
+    const int g = cid / per_group, idx = cid % per_group;
+    const int gt = min(GROUP_T, n_t - g * GROUP_T);
+    fp = idx / gt;
+    tt = g * GROUP_T + idx % gt;
+  }
+  const int m0 = fp * (2 * BM) + rank * BM;   // this CTA's features
+  const int l0 = tt * BN;                       // the pair's tokens
+  const int lh = l0 + rank * (BN / 2);          // this CTA's token half
   const int nk = (Kred + BK - 1) / BK;
 
   if (warp == 8 && lane == 0) {
+    const uint32_t merged = leader ? 18u : 1u;
     for (int i = 0; i < NE; ++i) {
-      mbar_init(&e_full[i].b, 1);
+      mbar_init(&rready[i].b, merged);
       mbar_init(&e_empty[i].b, 9);
-      mbar_init(&p_early[i].b, 1);
+      mbar_init(&refull[i].b, 1);
     }
     for (int i = 0; i < NA; ++i) {
-      mbar_init(&a_full[i].b, 1);
+      mbar_init(&mready[i].b, merged);
       mbar_init(&a_empty[i].b, 1);
-      mbar_init(&p_act[i].b, 1);
-    }
-    for (int i = 0; i < NRE; ++i) {
-      mbar_init(&refull[i].b, 1);
-      mbar_init(&reempty[i].b, 16);
-    }
-    for (int i = 0; i < NW; ++i) {
-      mbar_init(&wready[i].b, 16);
       mbar_init(&wempty[i].b, 1);
     }
     mbar_init(ffull, 1);
     mbar_init(pffull, 1);
     mbar_init(accf, 1);
     fence_barrier_init();
+    // first use of every recompute buffer: nobody has read it yet
+    if (leader)
+      for (int i = 0; i < NE; ++i) mbar_arrive_count(&rready[i].b, 16);
     tma_prefetch_desc(&tmAct);
     tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmS);
@@ -400,14 +408,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // Every TMA completes on a barrier of the CTA that issued it; the leader
-  // learns about the peer's stages through relayed remote arrives, and the
-  // transform warps of both CTAs arrive remotely on the leader's reempty /
-  // wready.  Remote arrives address the leader through mapa.
-  const uint32_t reempty_l = mapa_shared(smem_u32(reempty), 0);
-  const uint32_t wready_l = mapa_shared(smem_u32(wready), 0);
-  const uint32_t p_early_l = mapa_shared(smem_u32(p_early), 0);
-  const uint32_t p_act_l = mapa_shared(smem_u32(p_act), 0);
+  // Every TMA completes on a barrier of the CTA that issued it; the peer
+  // relays its landings to the leader, and the transform warps of both CTAs
+  // arrive on the leader's merged barriers.  Remote arrives go through mapa.
+  const uint32_t rready_l = mapa_shared(smem_u32(rready), 0);
+  const uint32_t mready_l = mapa_shared(smem_u32(mready), 0);
   const uint32_t pffull_l = mapa_shared(smem_u32(pffull), 0);
 
   if (warp == 8) {
@@ -425,14 +430,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
         mbar_wait(&e_empty[e].b, ((i / NE) & 1) ^ 1);
         uint8_t* st = early + e * EB;
         const int k0 = i * BK;
-        mbar_arrive_expect_tx(&e_full[e].b, EB);
+        mbar_arrive_expect_tx(&rready[e].b, EB);
         if (DX) {  // W[k0:k0+64, m0:m0+128] as two SW128 boxes of 64 columns
-          tma_load_2d(st, &tmW, &e_full[e].b, m0, k0);
-          tma_load_2d(st + W_BYTES / 2, &tmW, &e_full[e].b, m0 + 64, k0);
-          tma_load_2d(st + W_BYTES, &tmS, &e_full[e].b, 0, k0 + 32 * rank);   // a rows, K-major
+          tma_load_2d(st, &tmW, &rready[e].b, m0, k0);
+          tma_load_2d(st + W_BYTES / 2, &tmW, &rready[e].b, m0 + 64, k0);
+          tma_load_2d(st + W_BYTES, &tmS, &rready[e].b, 0, k0 + 32 * rank);   // a rows, K-major
         } else {   // W[m0:m0+128, k0:k0+64], SW128
-          tma_load_2d(st, &tmW, &e_full[e].b, k0, m0);
-          tma_load_2d(st + W_BYTES, &tmS, &e_full[e].b, k0 + 32 * rank, 0);   // b cols, MN-major
+          tma_load_2d(st, &tmW, &rready[e].b, k0, m0);
+          tma_load_2d(st + W_BYTES, &tmS, &rready[e].b, k0 + 32 * rank, 0);   // b cols, MN-major
         }
       }
     }
@@ -442,8 +447,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
       for (int i = 0; i < nk; ++i) {
         const int a = i % NA;
         mbar_wait(&a_empty[a].b, ((i / NA) & 1) ^ 1);
-        mbar_arrive_expect_tx(&a_full[a].b, ACT_BYTES);
-        tma_load_2d(actb + a * ACT_BYTES, &tmAct, &a_full[a].b, i * BK, lh);
+        mbar_arrive_expect_tx(&mready[a].b, ACT_BYTES);
+        tma_load_2d(actb + a * ACT_BYTES, &tmAct, &mready[a].b, i * BK, lh);
       }
     }
   } else if (warp == 11) {
@@ -451,8 +456,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
     if (!leader && lane == 0) {
       for (int i = 0; i < nk; ++i) {
         const int a = i % NA;
-        mbar_wait(&a_full[a].b, (i / NA) & 1);
-        mbar_arrive_cluster(p_act_l + a * 16);
+        mbar_wait(&mready[a].b, (i / NA) & 1);
+        mbar_arrive_cluster(mready_l + a * 16);
       }
     }
   } else if (warp == 9) {
@@ -463,59 +468,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
         mbar_arrive_cluster(pffull_l);
         for (int i = 0; i < nk; ++i) {
           const int e = i % NE;
-          mbar_wait(&e_full[e].b, (i / NE) & 1);
-          mbar_arrive_cluster(p_early_l + e * 16);
+          mbar_wait(&rready[e].b, (i / NE) & 1);
+          mbar_arrive_cluster(rready_l + e * 16);
         }
       }
-    } else if (lane == 0) {
-      // ---------------------------------------------------------- MMA issuer (leader CTA)
+    } else {
+      // ---------------------------------------------------------- MMA issuer (leader CTA, converged warp)
       constexpr uint32_t idesc_re = make_idesc_bf16(256, 64, DX, !DX);
       constexpr uint32_t idesc_main = make_idesc_bf16(256, 256, false, false);
+      // descriptor bases; a descriptor's start-address field is addr >> 4, so
+      // byte offsets inside shared memory are added as (offset >> 4)
+      const uint64_t ff_desc = DX ? make_sdesc(smem_u32(ffac), FF / 2, 1024, SW_128)
+                                  : make_sdesc(smem_u32(ffac), 16, 8 * SWR, sw_layout(SWR));
+      const uint64_t sf_desc = DX ? make_sdesc(smem_u32(early + W_BYTES), 16, 8 * SWR, sw_layout(SWR))
+                                  : make_sdesc(smem_u32(early + W_BYTES), 0, 8 * 64, SW_64);
+      const uint64_t weff_desc = make_sdesc(smem_u32(weff), 16, 1024, SW_128);
+      const uint64_t act_desc = make_sdesc(smem_u32(actb), 16, 1024, SW_128);
+      constexpr uint32_t FF_KSTEP = DX ? 2048 >> 4 : 32 >> 4;   // per K16 of the recompute
+      constexpr uint32_t SF_KSTEP = DX ? 32 >> 4 : 1024 >> 4;
       mbar_wait(ffull, 0);
-      mbar_wait_cluster(pffull, 0);
-      const uint32_t ff_base = smem_u32(ffac);
+      mbar_wait(pffull, 0);
       for (int j = 0; j < nk + D; ++j) {
         if (j < nk) {  // recompute for step j, D steps ahead of its main MMA
-          const int e = j % NE, rb = j % NRE;
-          mbar_wait(&e_full[e].b, (j / NE) & 1);
-          mbar_wait_cluster(&p_early[e].b, (j / NE) & 1);
-          mbar_wait_cluster(&reempty[rb].b, ((j / NRE) & 1) ^ 1);
+          const int e = j % NE;
+          mbar_wait(&rready[e].b, (j / NE) & 1);
           tc_fence_after();
-          const uint32_t sf_base = smem_u32(early + e * EB + W_BYTES);
+          if (elect_one()) {
+            const uint64_t sfd = sf_desc + (uint64_t)(e * (EB >> 4));
 #pragma unroll
-          for (int kk = 0; kk < RP / 16; ++kk) {
-            uint64_t ad, bd;
-            if (DX) {
-              ad = make_sdesc(ff_base + kk * 2048, FF / 2, 1024, SW_128);            // b^T, MN-major
-              bd = make_sdesc(sf_base + kk * 32, 16, 8 * SWR, sw_layout(SWR));       // a rows, K-major
-            } else {
-              ad = make_sdesc(ff_base + kk * 32, 16, 8 * SWR, sw_layout(SWR));       // a rows, K-major
-              bd = make_sdesc(sf_base + kk * 16 * 64, 0, 8 * 64, SW_64);             // b cols, MN-major (32 wide)
-            }
-            mma_bf16_pair(tmem + RE_COL + rb * 64, ad, bd, idesc_re, kk > 0 ? 1u : 0u);
+            for (int kk = 0; kk < RP / 16; ++kk)
+              mma_bf16_pair(tmem + RE_COL + e * 64, ff_desc + kk * FF_KSTEP, sfd + kk * SF_KSTEP, idesc_re,
+                            kk > 0 ? 1u : 0u);
+            mma_commit_pair(&refull[e].b, 0x3);
+            mma_commit_pair(&e_empty[e].b, 0x3);
           }
-          mma_commit_pair(&refull[rb].b, 0x3);
-          mma_commit_pair(&e_empty[e].b, 0x3);
+          __syncwarp();
         }
         const int jm = j - D;
         if (jm >= 0) {  // main MMA for step jm
-          const int a = jm % NA, wb = jm % NW;
-          mbar_wait(&a_full[a].b, (jm / NA) & 1);
-          mbar_wait_cluster(&p_act[a].b, (jm / NA) & 1);
-          mbar_wait_cluster(&wready[wb].b, (jm / NW) & 1);
+          const int a = jm % NA;
+          mbar_wait(&mready[a].b, (jm / NA) & 1);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(weff + wb * WEFF_BYTES);
-          const uint32_t b_base = smem_u32(actb + a * ACT_BYTES);
+          if (elect_one()) {
+            const uint64_t ad = weff_desc + (uint64_t)(a * (WEFF_BYTES >> 4));
+            const uint64_t bd = act_desc + (uint64_t)(a * (ACT_BYTES >> 4));
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            mma_bf16_pair(tmem, make_sdesc(a_base + kk * 32, 16, 1024, SW_128),
-                          make_sdesc(b_base + kk * 32, 16, 1024, SW_128), idesc_main, (jm > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < BK / 16; ++kk)
+              mma_bf16_pair(tmem, ad + kk * 2, bd + kk * 2, idesc_main, (jm > 0 || kk > 0) ? 1u : 0u);
+            mma_commit_pair(&a_empty[a].b, 0x3);
+            mma_commit_pair(&wempty[a].b, 0x3);
           }
-          mma_commit_pair(&a_empty[a].b, 0x3);
-          mma_commit_pair(&wempty[wb].b, 0x3);
+          __syncwarp();
         }
       }
-      mma_commit_pair(accf, 0x3);
+      if (elect_one()) mma_commit_pair(accf, 0x3);
+      __syncwarp();
     }
   } else {
     // ------------------------------------------------------------ transform warps 0..7
@@ -526,9 +533,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const uint32_t alpha2 = pack_bf16x2(alpha, alpha);
     for (int i = 0; i < nk; ++i) {
-      const int e = i % NE, rb = i % NRE, wb = i % NW;
+      const int e = i % NE, rb = e, wb = i % NA;
       // 1. rank-r product of this k-step (TMEM -> registers), then release the buffer
-      mbar_wait(&refull[rb].b, (i / NRE) & 1);
+      mbar_wait(&refull[rb].b, (i / NE) & 1);
       tc_fence_after();
       uint32_t p[32];
       const uint32_t re_col = RE_COL + rb * 64 + h * 32;
@@ -543,10 +550,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(reempty_l + rb * 16);
+      if (lane == 0) mbar_arrive_cluster(rready_l + rb * 16);  // RE buffer free for step i + NE
       // 2. W tile landed, destination buffer drained by the MMA of step i - NW
-      mbar_wait(&e_full[e].b, (i / NE) & 1);
-      mbar_wait(&wempty[wb].b, ((i / NW) & 1) ^ 1);
+      mbar_wait(&rready[e].b, (i / NE) & 1);
+      mbar_wait(&wempty[wb].b, ((i / NA) & 1) ^ 1);
       const uint32_t wt = smem_u32(early + e * EB);
       const uint32_t dst = smem_u32(weff + wb * WEFF_BYTES);
       if (!DX) {
@@ -622,7 +629,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&e_empty[e].b);                  // done reading the W tile
-        mbar_arrive_cluster(wready_l + wb * 16);     // W_eff half ready for the pair MMA
+        mbar_arrive_cluster(mready_l + wb * 16);     // W_eff half ready for the pair MMA
       }
     }
     // ------------------------------------------------------------ epilogue
