@@ -56,57 +56,61 @@ def peaks():
 # clocks sampler (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Samples NVML (SM clock + clock-event reasons) from the main thread while
+    the already-enqueued timed region runs on the GPU (no helper thread)."""
 
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
-        self.lines = []
-        self.thread = None
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def start(self):
+    def __init__(self, torch_device):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self.nvml = None
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            idx = torch_device.index or 0
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                idx = int(vis.split(",")[idx])
+            h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.nvml = (nv, h)
+        except Exception as exc:  # noqa: BLE001
+            print(f"[bench] NVML unavailable: {exc}", file=sys.stderr)
+
+    def sample_until(self, event, min_samples=3):
+        """Poll every ~2 ms until `event` (recorded after the timed region) completes."""
+        if self.nvml is None:
             return
-        self.thread = threading.Thread(target=self._read, daemon=True)
-        self.thread.start()
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
-    def stop(self):
-        if self.proc is None:
-            return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        if self.thread:
-            self.thread.join(timeout=2)
-        sm, mx, reasons = [], None, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
+        nv, h = self.nvml
+        while True:
+            done = event.query()
             try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[2:6]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        if not sm:
+                self.samples.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for name, attr in self.REASONS:
+                    if mask & getattr(nv, attr, 0):
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            if done and len(self.samples) >= min_samples:
+                return
+            if done:
+                return
+            time.sleep(0.002)
+
+    def result(self):
+        if not self.samples:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "source": "NVML, sampled while the timed region ran"}
 
 
 # ---------------------------------------------------------------------------
@@ -234,14 +238,14 @@ def run_native(args, cfg):
         if times is not None:
             times.append((e0, e1, e2))
 
+    print('[bench] warmup', file=sys.stderr, flush=True)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks = ClockSampler(dev)
     _native.reset_launch_count()
     t_start, t_end = ev(), ev()
     times = []
@@ -249,12 +253,13 @@ def run_native(args, cfg):
     for _ in range(args.steps):
         step(times)
     t_end.record(stream)
+    clocks.sample_until(t_end)
     torch.cuda.synchronize()
     launches = _native.launch_count()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clk = clocks.stop()
+    clk = clocks.result()
     ms = t_start.elapsed_time(t_end) / args.steps
     fwd_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1, _ in times)
     bwd_ms = statistics.mean(e1.elapsed_time(e2) for _, e1, e2 in times)
@@ -273,6 +278,7 @@ def run_native(args, cfg):
     rank_r_ms = ebx0.elapsed_time(ebx1) / 3
     dx_ms = max(bwd_ms - rank_r_ms, 1e-6)
 
+    print('[bench] e2e', file=sys.stderr, flush=True)
     # ---------------- end-to-end through the public module API (host buffers)
     layer = LoRSLinear(w, a=a32, b=b32, alpha=2.0).to(dev)
     hx = x.cpu().pin_memory()
@@ -280,9 +286,26 @@ def run_native(args, cfg):
     hda = torch.empty(R, r, dtype=torch.float32).pin_memory()
     hdb = torch.empty(r, C, dtype=torch.float32).pin_memory()
 
+    copy_stream = torch.cuda.Stream(device=dev)
+    staged = {}
+
+    def prefetch():
+        # H2D of the next step's batch on a side stream (as a training loop's
+        # data prefetch would); the consumer waits on its event
+        with torch.cuda.stream(copy_stream):
+            xd = hx.to(dev, non_blocking=True)
+            dyd = hdy.to(dev, non_blocking=True)
+            evt = torch.cuda.Event()
+            evt.record(copy_stream)
+        staged["next"] = (xd, dyd, evt)
+
     def e2e_step():
-        xd = hx.to(dev, non_blocking=True).requires_grad_(True)
-        dyd = hdy.to(dev, non_blocking=True)
+        xd, dyd, evt = staged.pop("next")
+        stream.wait_event(evt)
+        xd.record_stream(stream)
+        dyd.record_stream(stream)
+        prefetch()
+        xd.requires_grad_(True)
         layer.a.grad = None
         layer.b.grad = None
         y = layer(xd)
@@ -294,6 +317,7 @@ def run_native(args, cfg):
         hda.copy_(layer.a.grad, non_blocking=True)
         hdb.copy_(layer.b.grad, non_blocking=True)
 
+    prefetch()
     for _ in range(2):
         e2e_step()
     torch.cuda.synchronize()
@@ -308,6 +332,7 @@ def run_native(args, cfg):
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    staged.clear()
     peak_gb = torch.cuda.max_memory_allocated(dev) / 1e9
     if world > 1:
         tt = torch.tensor([e2e_ms, peak_gb], device=dev)
@@ -355,8 +380,9 @@ def run_native(args, cfg):
             "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": x.numel() * x.element_size() + dy.numel() * dy.element_size(),
                     "d2h_bytes_per_step": (R * r + r * C) * 4,
-                    "ms_per_step": e2e_ms, "api": "LoRSLinear.forward + backward (autograd), pinned host X/dY in, "
-                                                  "dA/dB out"},
+                    "ms_per_step": e2e_ms, "api": "LoRSLinear.forward + backward (autograd); pinned host X/dY "
+                                                  "copied in every step (next batch prefetched on a copy stream), "
+                                                  "dA/dB copied out every step"},
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu:
