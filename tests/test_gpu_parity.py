@@ -319,3 +319,45 @@ def test_config2_bf16_full_size_properties(P):
     # linearity in X (size-independent property)
     y1, _ = ops.lors_fwd(x[:4096].contiguous(), w, a, b, 2.0)
     assert torch.equal(y1, y[:4096])
+
+
+# ---------------------------------------------------------------------------
+# gradient-SVD adapter init on the GPU (initialization.py:171-232)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("masked", [False, True])
+def test_init_gradient_svd_two_layer_probe(P, masked):
+    from paper_2501_08582_b200.init import init_gradient_svd
+    rng = np.random.default_rng(9)
+    C0, H, O, L, r = 48, 40, 24, 64, 4
+    w1 = orc.prune_rowwise(rng.normal(size=(H, C0)), 0.5)
+    w2 = orc.prune_rowwise(rng.normal(size=(O, H)), 0.5)
+    x = rng.normal(size=(L, C0))
+    g = rng.normal(size=(L, O))
+    l1 = P.LoRSLinear(_dev(w1, torch.float32), rank=r)
+    l2 = P.LoRSLinear(_dev(w2, torch.float32), rank=r)
+    with torch.no_grad():
+        l1.a.normal_()
+        l2.a.normal_()   # init must zero a before probing
+    xd, gd = _dev(x, torch.float32), _dev(g, torch.float32)
+
+    def probe():
+        y = l2(torch.relu(l1(xd)))
+        (y * gd).sum().backward()
+
+    diag = []
+    init_gradient_svd([l1, l2], probe, masked_gradient=masked, diagnostics=diag)
+    # oracle: a = 0 so W_eff = W
+    y1 = x @ w1.T
+    h = np.maximum(y1, 0)
+    dy2 = g
+    dy1 = (dy2 @ w2) * (y1 > 0)
+    for layer, dy, xin, w in ((l1, dy1, x, w1), (l2, dy2, h, w2)):
+        dw = dy.T @ xin
+        if masked:
+            dw = dw * (w != 0)
+        want = orc.fit_rank_r_rows(dw, r)
+        np.testing.assert_allclose(layer.b.double().cpu().numpy(), want, atol=2e-3)
+        assert float(layer.a.abs().sum()) == 0.0
+    for d in diag:
+        assert abs(d["projection_residual"] - d["singular_tail"]) <= 1e-3 * max(1.0, d["grad_norm"])

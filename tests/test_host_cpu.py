@@ -94,3 +94,15 @@ def test_adapter_pair_validation_cpu():
         P.AdapterPair(torch.zeros(4, 5), torch.zeros(5, 4))
     with pytest.raises(P.ArgumentError):
         P.AdapterPair(torch.zeros(4, 2), torch.zeros(2, 5), alpha=-1.0)
+
+
+def test_fit_rank_r_rows_matches_reference_svd_fixtures():
+    """GPU init's SVD step (run here on CPU tensors) vs the reference's Jacobi SVD."""
+    from paper_2501_08582_b200.init import fit_rank_r_rows, singular_tail
+    d = dict(np.load(os.path.join(GOLD, "svd_init.npz")))
+    for i, r in enumerate((3, 4, 5)):
+        dw = torch.from_numpy(d[f"s{i}_dw"])
+        for lim in (2048, 1):   # exact SVD path and the eigh (large-layer) path
+            b = fit_rank_r_rows(dw, r, exact_limit=lim)
+            np.testing.assert_allclose(b.double().numpy(), d[f"s{i}_b"], atol=2e-5)
+        assert abs(singular_tail(dw, r) - float(d[f"s{i}_tail"])) < 1e-9
