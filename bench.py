@@ -277,6 +277,18 @@ def run_native(args, cfg):
     torch.cuda.synchronize()
     rank_r_ms = ebx0.elapsed_time(ebx1) / 3
     dx_ms = max(bwd_ms - rank_r_ms, 1e-6)
+    sp_ms = None
+    if cfg["pattern"] == "two_four" and dt == torch.bfloat16:
+        # the 2:4 sparse-tensor-core forward (north_star 4), timed beside the dense-masked one
+        for _ in range(2):
+            ops.lors_fwd(x, w, a, b, 2.0, sparse24=True)
+        es0, es1 = ev(), ev()
+        es0.record(stream)
+        for _ in range(5):
+            ops.lors_fwd(x, w, a, b, 2.0, sparse24=True)
+        es1.record(stream)
+        torch.cuda.synchronize()
+        sp_ms = es0.elapsed_time(es1) / 5
 
     print('[bench] e2e', file=sys.stderr, flush=True)
     # ---------------- end-to-end through the public module API (host buffers)
@@ -373,7 +385,8 @@ def run_native(args, cfg):
                        "adapter_grads": "ste (lors)", "parallelism": f"dp{world}",
                        "l2": "inputs larger than L2 (W 90 MB + X 64 MB + dY 180 MB per step, 126 MB L2)"},
             "peak_hbm_gb": peak_gb,
-            "step_breakdown_ms": {"fwd": fwd_ms, "bwd": bwd_ms, "bwd_dx_gemm": dx_ms, "bwd_rank_r": rank_r_ms},
+            "step_breakdown_ms": {"fwd": fwd_ms, "bwd": bwd_ms, "bwd_dx_gemm": dx_ms, "bwd_rank_r": rank_r_ms,
+                                  "fwd_sparse24_tc": sp_ms},
             "algorithmic_tflops": step_flops / (ms * 1e-3) / 1e12,
             "roofline": roofline,
             "gpu_launches": launches,

@@ -66,7 +66,9 @@ typedef enum { LORS_MASK_FROM_W = 0, LORS_MASK_BITS = 1 } lors_mask_mode_t;
 typedef enum { LORS_GRAD_STE = 0, LORS_GRAD_MASKED = 1 } lors_grad_mode_t;
 
 #define LORS_FLAG_EMIT_P (1u << 0)   /* forward also writes P = X_t b^T [L, r] */
-#define LORS_FLAG_SPARSE24 (1u << 1) /* forward uses 2:4 sparse tensor cores   */
+#define LORS_FLAG_SPARSE24 (1u << 1) /* forward on 2:4 sparse tensor cores: each
+                                        masked W_eff tile is compressed on chip
+                                        (W must be 2:4 along C; bf16; C % 64 == 0) */
 #define LORS_FLAG_NO_DX (1u << 2)    /* backward skips dX (first layer)        */
 #define LORS_FLAG_FAULT_DA_SIGN (1u << 30) /* negative control: flip dA sign,
                                               mirrors FAULT_INJECTION
@@ -82,8 +84,8 @@ typedef struct lors_fwd_args {
   const void* x;     /* [L, C]                                         */
   const void* w;     /* [R, C] frozen pruned weight                    */
   const uint32_t* mask_bits; /* [R, ceil(C/32)] when mask_mode == BITS */
-  const void* w24;   /* [R, C/2] compressed kept values (SPARSE24)     */
-  const uint8_t* meta24; /* [R, C/8] 2:4 metadata (SPARSE24)           */
+  const void* w24;   /* reserved (pre-compressed 2:4 values); unused:   */
+  const uint8_t* meta24; /* the kernel compresses W_eff tiles on chip   */
   const void* a;     /* [R, r]                                         */
   const void* b;     /* [r, C]                                         */
   const void* bias;  /* [R] or NULL                                    */

@@ -304,13 +304,36 @@ struct alignas(16) Bar16 {
 namespace rg {
 constexpr int BM = 128, BN = 256, BK = 64;
 constexpr int THREADS = 384, XFORM_THREADS = 256;
-constexpr int NE = 4;   // early ring (W tile + streamed adapter-factor half) = TMEM recompute buffers
+// early ring (W tile + streamed adapter-factor half) = TMEM recompute buffers;
+// the 2:4 variant gives one recompute buffer to the sparse-metadata columns
+template <bool SP>
+constexpr int ne() { return SP ? 3 : 4; }
 constexpr int NA = 4;   // activation ring = W_eff buffers
-constexpr int D = 3;    // recompute lookahead (steps)
+template <bool SP>
+constexpr int lookahead() { return SP ? 2 : 3; }  // recompute lookahead (steps)
+// 2:4 index nibble (idx0 | idx1 << 2, idx0 < idx1) for each 4-bit keep mask;
+// groups with fewer than two kept entries are padded with zero-valued slots,
+// masks with more than two are not 2:4 (prune.py:72-77) and never reach here.
+constexpr uint64_t nibble_lut() {
+  uint64_t lut = 0;
+  for (int m = 0; m < 16; ++m) {
+    int idx[2] = {-1, -1}, n = 0;
+    for (int i = 0; i < 4; ++i)
+      if (((m >> i) & 1) && n < 2) idx[n++] = i;
+    for (int i = 0; i < 4 && n < 2; ++i)
+      if (i != idx[0]) idx[n++] = i;
+    if (idx[0] > idx[1]) { int tmp = idx[0]; idx[0] = idx[1]; idx[1] = tmp; }
+    lut |= (uint64_t)(idx[0] | (idx[1] << 2)) << (4 * m);
+  }
+  return lut;
+}
+constexpr uint64_t kNibbleLut = nibble_lut();
+constexpr uint32_t E_COL = 448;  // 2:4 metadata: W_eff buffer b, MMA h at column 448 + 8 b + 4 h
 constexpr int GROUP_T = 8;  // raster: token tiles per group (clusters of a wave share W and activation tiles)
 constexpr uint32_t ACT_BYTES = (BN / 2) * BK * 2;   // 16 KB: this CTA's token half
 constexpr uint32_t W_BYTES = BM * BK * 2;           // 16 KB
-constexpr uint32_t WEFF_BYTES = BM * BK * 2;        // 16 KB
+template <bool SP>
+constexpr uint32_t weff_bytes() { return SP ? BM * BK : BM * BK * 2; }  // 2:4 keeps half (compressed)
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t RE_COL = 256;                    // recompute buffers at TMEM cols 256 + 64 e
 template <int RP>
@@ -319,19 +342,22 @@ template <int RP>
 constexpr uint32_t ff_bytes() { return 128 * RP * 2; }  // fixed factor tile (128 m x RP)
 template <int RP>
 constexpr uint32_t early_bytes() { return W_BYTES + sf_bytes<RP>(); }
-template <int RP>
+template <int RP, bool SP>
 constexpr size_t smem_bytes() {
-  return 1024 + NE * early_bytes<RP>() + NA * ACT_BYTES + NA * WEFF_BYTES + ff_bytes<RP>() + 1024;
+  return 1024 + ne<SP>() * early_bytes<RP>() + NA * ACT_BYTES + NA * weff_bytes<SP>() + ff_bytes<RP>() + 1024;
 }
 }  // namespace rg
 
-template <bool DX, int RP, bool BITS>
+template <bool DX, int RP, bool BITS, bool SP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
     tc_lors_gemm_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmF,
                         const __grid_constant__ CUtensorMap tmOut, const bf16* __restrict__ bias,
                         const uint32_t* __restrict__ bits, int words_per_row, int Mout, int Kred, float alpha) {
   using namespace rg;
+  static_assert(!(SP && DX), "2:4 sparse tensor cores apply to the forward only (SURVEY C6)");
+  constexpr int NE = ne<SP>(), D = lookahead<SP>();
+  constexpr uint32_t WEFF_BYTES = weff_bytes<SP>();
   constexpr uint32_t SF = sf_bytes<RP>(), FF = ff_bytes<RP>(), EB = early_bytes<RP>();
   constexpr uint32_t SWR = RP * 2;  // swizzle span of the K-major rank-r tiles
   extern __shared__ uint8_t smem_raw[];
@@ -476,13 +502,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
       // ---------------------------------------------------------- MMA issuer (leader CTA, converged warp)
       constexpr uint32_t idesc_re = make_idesc_bf16(256, 64, DX, !DX);
       constexpr uint32_t idesc_main = make_idesc_bf16(256, 256, false, false);
+      constexpr uint32_t idesc_sp = make_idesc_bf16(256, 256, false, false, true);
       // descriptor bases; a descriptor's start-address field is addr >> 4, so
       // byte offsets inside shared memory are added as (offset >> 4)
       const uint64_t ff_desc = DX ? make_sdesc(smem_u32(ffac), FF / 2, 1024, SW_128)
                                   : make_sdesc(smem_u32(ffac), 16, 8 * SWR, sw_layout(SWR));
       const uint64_t sf_desc = DX ? make_sdesc(smem_u32(early + W_BYTES), 16, 8 * SWR, sw_layout(SWR))
                                   : make_sdesc(smem_u32(early + W_BYTES), 0, 8 * 64, SW_64);
-      const uint64_t weff_desc = make_sdesc(smem_u32(weff), 16, 1024, SW_128);
+      const uint64_t weff_desc = SP ? make_sdesc(smem_u32(weff), 16, 512, SW_64)    // compressed, 64 B rows
+                                    : make_sdesc(smem_u32(weff), 16, 1024, SW_128);
       const uint64_t act_desc = make_sdesc(smem_u32(actb), 16, 1024, SW_128);
       constexpr uint32_t FF_KSTEP = DX ? 2048 >> 4 : 32 >> 4;   // per K16 of the recompute
       constexpr uint32_t SF_KSTEP = DX ? 32 >> 4 : 1024 >> 4;
@@ -512,9 +540,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
           if (elect_one()) {
             const uint64_t ad = weff_desc + (uint64_t)(a * (WEFF_BYTES >> 4));
             const uint64_t bd = act_desc + (uint64_t)(a * (ACT_BYTES >> 4));
+            if (SP) {
+              // two K = 32 sparse MMAs: compressed A advances 32 B, B 64 B, metadata one column each
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk)
-              mma_bf16_pair(tmem, ad + kk * 2, bd + kk * 2, idesc_main, (jm > 0 || kk > 0) ? 1u : 0u);
+              for (int hh = 0; hh < 2; ++hh)
+                mma_bf16_pair_sp(tmem, ad + hh * 2, bd + hh * 4, tmem + E_COL + a * 8 + hh * 4, idesc_sp,
+                                 (jm > 0 || hh > 0) ? 1u : 0u);
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk)
+                mma_bf16_pair(tmem, ad + kk * 2, bd + kk * 2, idesc_main, (jm > 0 || kk > 0) ? 1u : 0u);
+            }
             mma_commit_pair(&a_empty[a].b, 0x3);
             mma_commit_pair(&wempty[a].b, 0x3);
           }
@@ -559,6 +595,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
       if (!DX) {
         // thread = W row; 4 chunks of 8 k-values, same swizzled position in and out
         uint32_t mword = 0;
+        uint32_t comp[8], meta = 0;  // 2:4: compressed pairs and index nibbles of this half
         if (BITS) mword = (gm < Mout) ? __ldg(bits + (int64_t)gm * words_per_row + ((i * BK + h * 32) >> 5)) : 0u;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -568,16 +605,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
                        : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
                        : "r"(wt + off));
           const uint32_t wv[4] = {raw.x, raw.y, raw.z, raw.w};
-          uint32_t o[4];
+          uint32_t o[4], keepm[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const uint32_t keep = BITS ? bits2_to_mask((mword >> (c * 8 + 2 * u)) & 3u) : nonzero_mask_bf16x2(wv[u]);
+            keepm[u] = keep;
             o[u] = weff_pair(wv[u], __uint_as_float(p[c * 8 + 2 * u]), __uint_as_float(p[c * 8 + 2 * u + 1]), alpha2,
                              keep);
           }
-          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + off), "r"(o[0]), "r"(o[1]), "r"(o[2]),
-                       "r"(o[3])
-                       : "memory");
+          if (SP) {
+            // compress each group of 4 to its two kept values (select on the mask,
+            // so padded slots of sparser groups carry +0) and a 4-bit index nibble
+#pragma unroll
+            for (int gi = 0; gi < 2; ++gi) {
+              const uint32_t k0 = keepm[2 * gi], k1 = keepm[2 * gi + 1];
+              const uint32_t m = (k0 & 1u) | ((k0 >> 15) & 2u) | ((k1 & 1u) << 2) | ((k1 >> 13) & 8u);
+              const uint32_t nib = (uint32_t)(kNibbleLut >> (4 * m)) & 0xFu;
+              const uint32_t sel = 0x1010u + (nib & 3u) * 0x22u + (nib >> 2) * 0x2200u;
+              comp[c * 2 + gi] = prmt(o[2 * gi], o[2 * gi + 1], sel);
+              meta |= nib << (4 * (c * 2 + gi));
+            }
+          } else {
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + off), "r"(o[0]), "r"(o[1]), "r"(o[2]),
+                         "r"(o[3])
+                         : "memory");
+          }
+        }
+        if (SP) {
+          // compressed K-major SW64 tile: row t, bytes [32h, 32h + 32)
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const uint32_t off = (uint32_t)t * 64 + (((uint32_t)(2 * h + cc) ^ (((uint32_t)t >> 1) & 3u)) << 4);
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + off), "r"(comp[4 * cc]),
+                         "r"(comp[4 * cc + 1]), "r"(comp[4 * cc + 2]), "r"(comp[4 * cc + 3])
+                         : "memory");
+          }
+          // metadata in the tcgen05 sparse layout: lane L = a + 8b + 16c holds, for the
+          // MMA's k-half b, rows (L & ~8) in bits 0-15 and (L | 8) in bits 16-31
+          const uint32_t pm = __shfl_xor_sync(0xffffffffu, meta, 8);
+          const uint32_t word = (lane & 8) ? ((pm >> 16) | (meta & 0xFFFF0000u)) : ((meta & 0xFFFFu) | (pm << 16));
+          tmem_st_x1(tmem + lane_addr + E_COL + wb * 8 + h * 4, word);
+          tmem_st_wait();
+          tc_fence_before();
         }
       } else {
         // W tile [64 k][128 c] as two SW128 boxes of 64 c.  ldmatrix.trans hands
@@ -663,7 +732,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
   if (warp == 9) tmem_dealloc_pair<TMEM_COLS>(tmem);
 }
 
-template <bool DX, int RP>
+template <bool DX, int RP, bool SP>
 static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const bf16* b, const bf16* bias,
                             const uint32_t* bits, bf16* out, int L, int R, int C, int r, float alpha,
                             cudaStream_t s) {
@@ -683,8 +752,8 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
     if ((st = make_map(&tF, a, r, R, RP, 128, RP * 2, "a (fixed)"))) return st;
   }
   if ((st = make_map(&tOut, out, Mout, L, 128, BN, 0, "output"))) return st;
-  auto kern = bits ? tc_lors_gemm_kernel<DX, RP, true> : tc_lors_gemm_kernel<DX, RP, false>;
-  const size_t smem = smem_bytes<RP>();
+  auto kern = bits ? tc_lors_gemm_kernel<DX, RP, true, SP> : tc_lors_gemm_kernel<DX, RP, false, SP>;
+  const size_t smem = smem_bytes<RP, SP>();
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "lors_gemm smem attribute");
   dim3 grid((unsigned)(2 * ceil_div(Mout, 2 * BM)), (unsigned)ceil_div(L, BN));
@@ -693,13 +762,13 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
   return LORS_OK;
 }
 
-template <bool DX>
+template <bool DX, bool SP = false>
 static int lors_gemm(int rp, const bf16* act, const bf16* w, const bf16* a, const bf16* b, const bf16* bias,
                      const uint32_t* bits, bf16* out, int L, int R, int C, int r, float alpha, cudaStream_t s) {
   switch (rp) {
-    case 16: return launch_lors_gemm<DX, 16>(act, w, a, b, bias, bits, out, L, R, C, r, alpha, s);
-    case 32: return launch_lors_gemm<DX, 32>(act, w, a, b, bias, bits, out, L, R, C, r, alpha, s);
-    default: return launch_lors_gemm<DX, 64>(act, w, a, b, bias, bits, out, L, R, C, r, alpha, s);
+    case 16: return launch_lors_gemm<DX, 16, SP>(act, w, a, b, bias, bits, out, L, R, C, r, alpha, s);
+    case 32: return launch_lors_gemm<DX, 32, SP>(act, w, a, b, bias, bits, out, L, R, C, r, alpha, s);
+    default: return launch_lors_gemm<DX, 64, SP>(act, w, a, b, bias, bits, out, L, R, C, r, alpha, s);
   }
 }
 
@@ -726,7 +795,15 @@ int tc_fwd(const lors_fwd_args* A, cudaStream_t s) {
     return st;
   }
   const int rp = (int)pad_rank(r);
-  st = lors_gemm<false>(rp, x, w, a, b, (const bf16*)A->bias, bits, (bf16*)A->y, L, R, C, r, A->alpha, s);
+  if (A->flags & LORS_FLAG_SPARSE24) {
+    if (C % 64 != 0) {
+      set_error("2:4 sparse forward needs C % 64 == 0");
+      return LORS_ERR_SHAPE;
+    }
+    st = lors_gemm<false, true>(rp, x, w, a, b, (const bf16*)A->bias, bits, (bf16*)A->y, L, R, C, r, A->alpha, s);
+  } else {
+    st = lors_gemm<false>(rp, x, w, a, b, (const bf16*)A->bias, bits, (bf16*)A->y, L, R, C, r, A->alpha, s);
+  }
   if (st) return st;
   if (A->flags & LORS_FLAG_EMIT_P)  // P = X_t b^T: A = X_t K-major, B = b [r, C] K-major
     st = skinny<false, false, 0>(rp, x, b, A->p, L, r, C, r, 1.0f, false, s);

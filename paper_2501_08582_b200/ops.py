@@ -61,8 +61,12 @@ def _check_layer(x_t, w, a, b):
 
 def lors_fwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tensor, alpha: float = 2.0,
              bias: Optional[torch.Tensor] = None, mask_bits: Optional[torch.Tensor] = None,
-             emit_p: bool = False, sparse24=None):
-    """Y_t [L, R] = X_t . W_eff^T (+ bias); optionally P = X_t b^T [L, r]."""
+             emit_p: bool = False, sparse24: bool = False):
+    """Y_t [L, R] = X_t . W_eff^T (+ bias); optionally P = X_t b^T [L, r].
+
+    sparse24=True runs the forward on 2:4 sparse tensor cores: the kernel
+    compresses each masked W_eff tile on chip (W must satisfy 2:4 along C,
+    prune.py:72-77; bf16 only)."""
     L, R, C, r = _check_layer(x_t, w, a, b)
     dt = w.dtype
     code = dtype_code(dt)
@@ -76,13 +80,10 @@ def lors_fwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
     args.L, args.R, args.C, args.r = L, R, C, r
     args.dtype = code
     args.mask_mode = N.MASK_BITS if mask_bits is not None else N.MASK_FROM_W
-    args.flags = (N.FLAG_EMIT_P if emit_p else 0) | (N.FLAG_SPARSE24 if sparse24 is not None else 0)
+    args.flags = (N.FLAG_EMIT_P if emit_p else 0) | (N.FLAG_SPARSE24 if sparse24 else 0)
     args.alpha = float(alpha)
     args.x, args.w, args.a, args.b = _p(x_t), _p(w), _p(a), _p(b)
     args.mask_bits = _p(mask_bits)
-    if sparse24 is not None:
-        vals, meta = sparse24
-        args.w24, args.meta24 = _p(vals), _p(meta)
     args.bias, args.y, args.p = _p(bias), _p(y), _p(p)
     lib = N.load()
     ws_bytes = lib.lors_fwd_workspace(ct.byref(args))

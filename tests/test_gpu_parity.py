@@ -361,3 +361,26 @@ def test_init_gradient_svd_two_layer_probe(P, masked):
         assert float(layer.a.abs().sum()) == 0.0
     for d in diag:
         assert abs(d["projection_residual"] - d["singular_tail"]) <= 1e-3 * max(1.0, d["grad_norm"])
+
+
+# ---------------------------------------------------------------------------
+# 2:4 sparse-tensor-core forward (north_star 4)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("shape", [(256, 256, 64, 16), (300, 264, 192, 32), (512, 384, 256, 64)])
+def test_sparse24_forward_matches_dense_and_oracle(P, shape):
+    from paper_2501_08582_b200 import ops, prune
+    L, R, C, r = shape
+    g = torch.Generator(device="cuda").manual_seed(L + R)
+    w = prune.prune_two_four(torch.randn(R, C, device="cuda", generator=g) * 0.02)
+    w[: R // 4] = torch.where(torch.rand(R // 4, C, device="cuda", generator=g) < 0.3,
+                              torch.zeros_like(w[: R // 4]), w[: R // 4])   # sparser groups: padding path
+    a = torch.randn(R, r, device="cuda", generator=g) * 0.05
+    b = torch.randn(r, C, device="cuda", generator=g) / r ** 0.5
+    x = torch.randn(L, C, device="cuda", generator=g)
+    w, a, b, x = (t.to(torch.bfloat16).contiguous() for t in (w, a, b, x))
+    ys, _ = ops.lors_fwd(x, w, a, b, 2.0, sparse24=True)
+    yd, _ = ops.lors_fwd(x, w, a, b, 2.0)
+    ref = orc.lors_forward(*(t.double().cpu().numpy() for t in (w, a, b)), x.double().cpu().numpy().T, 2.0)
+    assert _rel(ys, ref.T) <= 2e-2
+    assert _rel(ys, yd.double().cpu().numpy()) <= 1e-3
