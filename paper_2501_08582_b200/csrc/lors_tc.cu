@@ -773,6 +773,272 @@ static int lors_gemm(int rp, const bf16* act, const bf16* w, const bf16* a, cons
 }
 
 // ===========================================================================
+// K5: masked-G fused adapter gradient (north_star 3; oracle _sqft_grads,
+// adapters.py:303-312).
+//
+// One CTA owns G[128 rows of R x 256 cols of C] = sum_l dY_t[l, R] X_t[l, C]:
+//   mainloop : tcgen05 M=128 N=256 over all L tokens (A = dY_t tile, B = X_t
+//              tile, both MN-major via TMA), fp32 accumulator in TMEM;
+//   mask     : 4 epilogue warps read G rows from TMEM, select on W != 0 (or the
+//              packed bits), round to bf16 and park G.M as a K-major SW128 tile
+//              in shared memory -- G never reaches HBM;
+//   contract : dA_part[128 x r]  = (G.M) . b[:, C-tile]^T   (M=128, K=256)
+//              dB_part^T[256 x r] = (G.M)^T . a[R-tile]      (2 x M=128, K=128)
+//              with the same shared-memory bytes read K-major and MN-major;
+//   reduce   : alpha * partials added into dA / dB with red.global.add.v4.f32.
+// warps: 0 TMA producer, 1 MMA issuer + TMEM owner, 2..5 mask / reduce.
+// ===========================================================================
+namespace mg {
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 3, THREADS = 192;
+constexpr uint32_t A_BYTES = BM * BK * 2;   // 16 KB  dY tile [64 tokens][128 R]  (2 MN atoms)
+constexpr uint32_t B_BYTES = BN * BK * 2;   // 32 KB  X tile  [64 tokens][256 C]  (4 MN atoms)
+constexpr uint32_t GM_BYTES = BM * BN * 2;  // 64 KB  masked G tile, 4 K-atoms of [128 R][64 C]
+constexpr uint32_t G_COL = 0, DA_COL = 256, DB_COL = 320;
+template <int RP>
+constexpr uint32_t bt_bytes() { return RP * BN * 2; }   // b[:, C-tile] as 4 K-atoms of [RP][64 C]
+template <int RP>
+constexpr uint32_t at_bytes() { return BM * RP * 2; }   // a[R-tile, :] MN-major [128 R][RP]
+template <int RP>
+constexpr size_t smem_bytes() { return 1024 + STAGES * (A_BYTES + B_BYTES) + bt_bytes<RP>() + at_bytes<RP>() + 256; }
+}  // namespace mg
+
+template <int RP, bool BITS>
+__global__ void __launch_bounds__(mg::THREADS, 1)
+    tc_masked_grad_kernel(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmX,
+                          const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmA,
+                          const bf16* __restrict__ w, const uint32_t* __restrict__ bits, int words_per_row,
+                          float* __restrict__ da, float* __restrict__ db, int L, int R, int C, int r, float alpha) {
+  using namespace mg;
+  constexpr uint32_t BT = bt_bytes<RP>(), AT = at_bytes<RP>();
+  constexpr uint32_t SWR = RP * 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                          // [STAGES] dY tiles
+  uint8_t* sB = sA + STAGES * A_BYTES;         // [STAGES] X tiles
+  uint8_t* sBt = sB + STAGES * B_BYTES;        // b tile (dA contraction, B operand)
+  uint8_t* sAt = sBt + BT;                     // a tile (dB contraction, B operand)
+  uint8_t* sGM = smem;                         // masked G (reuses the drained pipeline)
+  Bar16* bars = reinterpret_cast<Bar16*>(sAt + AT);
+  Bar16* full = bars;                          // [STAGES]
+  Bar16* empty = full + STAGES;                // [STAGES]
+  uint64_t* gfull = &(empty + STAGES)->b;      // G accumulated
+  uint64_t* abfull = &(empty + STAGES + 1)->b; // a / b tiles landed
+  uint64_t* gmready = &(empty + STAGES + 2)->b;  // 4 mask warps parked G.M
+  uint64_t* cfull = &(empty + STAGES + 3)->b;  // contractions done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + STAGES + 4);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int m0 = blockIdx.x * BM;   // R rows
+  const int c0 = blockIdx.y * BN;   // C cols
+  const int nk = (L + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s].b, 1);
+      mbar_init(&empty[s].b, 1);
+    }
+    mbar_init(gfull, 1);
+    mbar_init(abfull, 1);
+    mbar_init(gmready, 4);
+    mbar_init(cfull, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tmDY);
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmA);
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(abfull, BT + AT);
+      for (int q = 0; q < 4; ++q) tma_load_2d(sBt + q * (RP * 128), &tmB, abfull, c0 + 64 * q, 0);
+      tma_load_2d(sAt, &tmA, abfull, 0, m0);
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % STAGES;
+        mbar_wait(&empty[s].b, ((i / STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s].b, A_BYTES + B_BYTES);
+        const int l0 = i * BK;
+        uint8_t* a = sA + s * A_BYTES;
+        uint8_t* b = sB + s * B_BYTES;
+        tma_load_2d(a, &tmDY, &full[s].b, m0, l0);
+        tma_load_2d(a + A_BYTES / 2, &tmDY, &full[s].b, m0 + 64, l0);
+        for (int q = 0; q < 4; ++q) tma_load_2d(b + q * (B_BYTES / 4), &tmX, &full[s].b, c0 + 64 * q, l0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_g = make_idesc_bf16(128, 256, true, true);
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % STAGES;
+        mbar_wait(&full[s].b, (i / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t a_base = smem_u32(sA + s * A_BYTES), b_base = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk)
+          mma_bf16(tmem + G_COL, make_sdesc(a_base + kk * 2048, A_BYTES / 2, 1024, SW_128),
+                   make_sdesc(b_base + kk * 2048, B_BYTES / 4, 1024, SW_128), idesc_g, (i > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&empty[s].b);
+      }
+      mma_commit(gfull);
+      // contractions once the mask warps parked G.M
+      mbar_wait(gmready, 0);
+      mbar_wait(abfull, 0);
+      tc_fence_after();
+      const uint32_t gm = smem_u32(sGM), bt = smem_u32(sBt), at = smem_u32(sAt);
+      constexpr uint32_t idesc_da = make_idesc_bf16(128, RP, false, false);   // G.M K-major, b K-major
+      constexpr uint32_t idesc_db = make_idesc_bf16(128, RP, true, true);     // (G.M)^T MN-major, a MN-major
+#pragma unroll
+      for (int kk = 0; kk < BN / 16; ++kk) {   // K = 256 columns of C, 4 per 64-wide atom
+        const uint32_t q = kk >> 2, o = (kk & 3) * 32;
+        mma_bf16(tmem + DA_COL, make_sdesc(gm + q * 16384 + o, 16, 1024, SW_128),
+                 make_sdesc(bt + q * (RP * 128) + o, 16, 1024, SW_128), idesc_da, kk > 0 ? 1u : 0u);
+      }
+#pragma unroll
+      for (int hc = 0; hc < 2; ++hc) {         // C halves of 128 (M), K = 128 rows of R
+#pragma unroll
+        for (int kk = 0; kk < BM / 16; ++kk) {
+          mma_bf16(tmem + DB_COL + hc * 64, make_sdesc(gm + hc * 32768 + kk * 2048, 16384, 1024, SW_128),
+                   make_sdesc(at + kk * 16 * SWR, 0, 8 * SWR, sw_layout(SWR)), idesc_db, kk > 0 ? 1u : 0u);
+        }
+      }
+      mma_commit(cfull);
+    }
+  } else {
+    // ---------------------------------------------------------------- mask / reduce warps 2..5
+    const int q = warp & 3;
+    const int t = q * 32 + lane;             // TMEM lane = G row inside the tile
+    const int gm_row = m0 + t;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    mbar_wait(gfull, 0);
+    tc_fence_after();
+    const uint32_t gmb = smem_u32(sGM);
+#pragma unroll 1
+    for (int cb = 0; cb < BN; cb += 32) {
+      uint32_t v[32];
+      tmem_ld_x32(tmem + lane_addr + G_COL + cb, v);
+      tmem_ld_wait();
+      uint32_t keepw = 0;   // keep bits for columns cb .. cb+31
+      const int gc = c0 + cb;
+      if (gm_row < R) {
+        if (BITS) {
+          keepw = __ldg(bits + (int64_t)gm_row * words_per_row + (gc >> 5));
+          if (gc + 32 > C) keepw &= (C - gc) >= 32 ? 0xFFFFFFFFu : ((1u << max(C - gc, 0)) - 1u);
+        } else {
+          const bf16* wr = w + (int64_t)gm_row * C + gc;
+#pragma unroll
+          for (int u = 0; u < 32; u += 8) {
+            if (gc + u + 8 <= C) {
+              const uint4 raw = *reinterpret_cast<const uint4*>(wr + u);
+              const uint32_t ww[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const uint32_t nz = nonzero_mask_bf16x2(ww[e]);
+                keepw |= ((nz & 1u) | ((nz >> 15) & 2u)) << (u + 2 * e);
+              }
+            }
+          }
+        }
+      }
+      uint32_t pk[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const float g0 = ((keepw >> (2 * e)) & 1u) ? __uint_as_float(v[2 * e]) : 0.0f;
+        const float g1 = ((keepw >> (2 * e + 1)) & 1u) ? __uint_as_float(v[2 * e + 1]) : 0.0f;
+        pk[e] = pack_bf16x2(g0, g1);
+      }
+      // K-major SW128 atom cb/64 [128 rows][64 cols]: row t, chunks (cb%64)/8 .. +3
+      const uint32_t atom = gmb + (cb >> 6) * 16384 + t * 128;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const uint32_t chunk = ((((cb & 63) >> 3) + cc) ^ (t & 7)) << 4;
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(atom + chunk), "r"(pk[4 * cc]),
+                     "r"(pk[4 * cc + 1]), "r"(pk[4 * cc + 2]), "r"(pk[4 * cc + 3])
+                     : "memory");
+      }
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(gmready);
+    // reduce the partials
+    mbar_wait(cfull, 0);
+    tc_fence_after();
+    {
+      uint32_t v[32];
+#pragma unroll
+      for (int half = 0; half < RP / 32 + (RP < 32 ? 1 : 0); ++half) {
+        if (half * 32 >= RP) break;
+        tmem_ld_x32(tmem + lane_addr + DA_COL + half * 32, v);
+        tmem_ld_wait();
+        if (gm_row < R) {
+          float* dst = da + (int64_t)gm_row * r + half * 32;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            if (half * 32 + j < r)
+              red_add_v4(dst + j, alpha * __uint_as_float(v[j]), alpha * __uint_as_float(v[j + 1]),
+                         alpha * __uint_as_float(v[j + 2]), alpha * __uint_as_float(v[j + 3]));
+        }
+      }
+#pragma unroll
+      for (int hc = 0; hc < 2; ++hc) {
+        const int gc = c0 + hc * 128 + t;   // dB^T row = C index
+#pragma unroll
+        for (int half = 0; half * 32 < RP; ++half) {
+          tmem_ld_x32(tmem + lane_addr + DB_COL + hc * 64 + half * 32, v);
+          tmem_ld_wait();
+          if (gc < C) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (half * 32 + j < r) atomicAdd(db + (int64_t)(half * 32 + j) * C + gc, alpha * __uint_as_float(v[j]));
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+template <int RP>
+static int launch_masked_grad(const bf16* dy, const bf16* x, const bf16* w, const uint32_t* bits, const bf16* a,
+                              const bf16* b, float* da, float* db, int L, int R, int C, int r, float alpha,
+                              cudaStream_t s) {
+  using namespace mg;
+  CUtensorMap tDY, tX, tB, tA;
+  int st;
+  if ((st = make_map(&tDY, dy, R, L, 64, 64, 128, "dY (MN)"))) return st;
+  if ((st = make_map(&tX, x, C, L, 64, 64, 128, "X (MN)"))) return st;
+  if ((st = make_map(&tB, b, C, r, 64, RP, 128, "b tile (K-major, K = C)"))) return st;
+  if ((st = make_map(&tA, a, r, R, RP, 128, RP * 2, "a tile (MN-major)"))) return st;
+  LORS_CUDA_TRY(cudaMemsetAsync(da, 0, sizeof(float) * (size_t)R * r, s), "zero dA");
+  LORS_CUDA_TRY(cudaMemsetAsync(db, 0, sizeof(float) * (size_t)r * C, s), "zero dB");
+  auto kern = bits ? tc_masked_grad_kernel<RP, true> : tc_masked_grad_kernel<RP, false>;
+  const size_t smem = smem_bytes<RP>();
+  LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                "masked_grad smem attribute");
+  dim3 grid((unsigned)ceil_div(R, BM), (unsigned)ceil_div(C, BN));
+  kern<<<grid, THREADS, smem, s>>>(tDY, tX, tB, tA, w, bits, (int)ceil_div(C, 32), da, db, L, R, C, r, alpha);
+  LORS_CHECK_LAUNCH("tc_masked_grad");
+  return LORS_OK;
+}
+
+static int masked_grad_tc(int rp, const bf16* dy, const bf16* x, const bf16* w, const uint32_t* bits, const bf16* a,
+                          const bf16* b, float* da, float* db, int L, int R, int C, int r, float alpha,
+                          cudaStream_t s) {
+  switch (rp) {
+    case 16: return launch_masked_grad<16>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s);
+    case 32: return launch_masked_grad<32>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s);
+    default: return launch_masked_grad<64>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s);
+  }
+}
+
+// ===========================================================================
 // dispatch
 // ===========================================================================
 bool tc_shape_ok(int64_t R, int64_t C, int64_t r) {
@@ -852,7 +1118,8 @@ int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {
       if (st) return st;
     }
   } else {
-    st = simt_masked_grad<bf16>(dy, x, w, bits, a, b, A->da, A->db, L, R, C, r, A->alpha, s);
+    st = tc ? masked_grad_tc(rp, dy, x, w, bits, a, b, A->da, A->db, L, R, C, r, A->alpha, s)
+            : simt_masked_grad<bf16>(dy, x, w, bits, a, b, A->da, A->db, L, R, C, r, A->alpha, s);
     if (st) return st;
   }
   if (A->dbias) {

@@ -357,7 +357,7 @@ def test_init_gradient_svd_two_layer_probe(P, masked):
         if masked:
             dw = dw * (w != 0)
         want = orc.fit_rank_r_rows(dw, r)
-        np.testing.assert_allclose(layer.b.double().cpu().numpy(), want, atol=2e-3)
+        np.testing.assert_allclose(layer.b.detach().double().cpu().numpy(), want, atol=2e-3)
         assert float(layer.a.abs().sum()) == 0.0
     for d in diag:
         assert abs(d["projection_residual"] - d["singular_tail"]) <= 1e-3 * max(1.0, d["grad_norm"])
@@ -384,3 +384,21 @@ def test_sparse24_forward_matches_dense_and_oracle(P, shape):
     ref = orc.lors_forward(*(t.double().cpu().numpy() for t in (w, a, b)), x.double().cpu().numpy().T, 2.0)
     assert _rel(ys, ref.T) <= 2e-2
     assert _rel(ys, yd.double().cpu().numpy()) <= 1e-3
+
+
+def test_masked_grad_tensor_core_path_vs_oracle(P):
+    """The tcgen05 masked-G kernel (aligned shapes) against sqft_gc_backward, incl. ragged R/C/L."""
+    from paper_2501_08582_b200 import ops
+    for (L, R, C, r) in [(200, 136, 264, 16), (320, 256, 512, 64), (64, 128, 256, 32)]:
+        rng = np.random.default_rng(L + R + C)
+        w = orc.prune_rowwise(rng.normal(0, 0.02, size=(R, C)), 0.5)
+        a, b = rng.normal(0, 0.05, size=(R, r)), rng.normal(0, 1 / np.sqrt(r), size=(r, C))
+        x, dy = rng.normal(size=(L, C)), rng.normal(size=(L, R))
+        q = [torch.from_numpy(v).to(torch.bfloat16) for v in (w, a, b, x, dy)]
+        ref = orc.sqft_gc_backward(*(t.double().numpy() for t in q[:3]), q[3].double().numpy().T,
+                                   q[4].double().numpy().T)
+        wd, ad, bd, xd, dyd = (t.cuda().contiguous() for t in q)
+        for bits in (None, ops.pack_mask(wd)):
+            _, da, db, _ = ops.lors_bwd(xd, wd, ad, bd, dyd, 2.0, grad_mode="masked", need_dx=False, mask_bits=bits)
+            assert _rel(da, ref.da) <= 2e-2
+            assert _rel(db, ref.db) <= 2e-2

@@ -30,3 +30,10 @@ flops = 2 * ((R*C*L + r*R*C + R*C) + (R*C*L + 2*r*R*L + 2*r*C*L + r*R*C + R*C))
 print(f"step {tot:.0f} us, {L/tot*1e6/1e6:.2f} M tok/s, algorithmic {flops/tot/1e6:.0f} TF/s")
 fs = t(lambda: ops.lors_fwd(x, w, a, b, 2.0, sparse24=True))
 print(f"sparse-TC fwd {fs:.0f} us ({gflop_main/fs*1e3:.0f} TF/s dense-equivalent) vs dense-masked {fw:.0f} us")
+bm = t(lambda: ops.lors_bwd(x, w, a, b, dy, 2.0, grad_mode="masked", need_dx=False), n=3)
+print(f"masked-G fused grads (no dX) {bm:.0f} us ({2*R*C*L/bm/1e6:.0f} TF/s on the G GEMM)")
+dxm, dam, dbm, _ = ops.lors_bwd(x, w, a, b, dy, 2.0, grad_mode="masked", need_dx=False)
+wf, af, bf, xf, dyf = (tt.float() for tt in (w, a, b, x, dy))
+G = (dyf.t() @ xf) * (wf != 0)
+def rel(u, v): return float((u.float() - v).norm() / v.norm())
+print(f"masked-G parity at cfg2: dA {rel(dam, 2 * G @ bf.t()):.2e}  dB {rel(dbm, 2 * af.t() @ G):.2e}")
