@@ -351,6 +351,46 @@ def run_native(args, cfg):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms, peak_gb = float(tt[0]), float(tt[1])
 
+    # ---------------- memory / speed comparators (north_star: peak memory <= plain
+    # dense LoRA; bytes not allocated relative to an SQFT-style path that
+    # materialises W_eff), same layer and inputs, one fwd+bwd each
+    from paper_2501_08582_b200.comparators import DenseLoRAFunction, SQFTFunction, peak_bytes_of_step
+    xg = x.detach().clone().requires_grad_(True)
+    a_p = layer.a
+    b_p = layer.b
+
+    def run_lors():
+        y = layer(xg)
+        y.backward(dy)
+
+    def run_lora():
+        y = DenseLoRAFunction.apply(xg, w, a_p, b_p, 2.0)
+        y.backward(dy)
+
+    def run_sqft():
+        y = SQFTFunction.apply(xg, w, a_p, b_p, 2.0)
+        y.backward(dy)
+
+    memory, comp_speed = {}, {}
+    for name, fn in (("lors", run_lors), ("dense_lora", run_lora), ("sqft_materialised", run_sqft)):
+        xg.grad = None
+        layer.a.grad = None
+        layer.b.grad = None
+        fn()
+        memory[name + "_step_peak_gb"] = peak_bytes_of_step(fn) / 1e9
+        c0_, c1_ = ev(), ev()
+        c0_.record(stream)
+        for _ in range(3):
+            fn()
+        c1_.record(stream)
+        torch.cuda.synchronize()
+        comp_speed[name + "_tokens_per_s"] = L / (c0_.elapsed_time(c1_) / 3 * 1e-3)
+    memory["bytes_not_allocated_vs_sqft_gb"] = memory["sqft_materialised_step_peak_gb"] - memory["lors_step_peak_gb"]
+    memory["lors_le_dense_lora"] = memory["lors_step_peak_gb"] <= memory["dense_lora_step_peak_gb"]
+    memory["note"] = ("extra device bytes allocated during one fwd+bwd above the resident inputs "
+                      "(W, a, b, X, dY); comparators are plain torch/cuBLAS (adapters.py:245-312 semantics)")
+    del xg
+
     if rank == 0:
         pk, pk_kind = peaks()
         cost = adapters.predict_cost("lors", R, C, L, r)
@@ -385,6 +425,8 @@ def run_native(args, cfg):
                        "adapter_grads": "ste (lors)", "parallelism": f"dp{world}",
                        "l2": "inputs larger than L2 (W 90 MB + X 64 MB + dY 180 MB per step, 126 MB L2)"},
             "peak_hbm_gb": peak_gb,
+            "memory": memory,
+            "comparators_tokens_per_s": comp_speed,
             "step_breakdown_ms": {"fwd": fwd_ms, "bwd": bwd_ms, "bwd_dx_gemm": dx_ms, "bwd_rank_r": rank_r_ms,
                                   "fwd_sparse24_tc": sp_ms},
             "algorithmic_tflops": step_flops / (ms * 1e-3) / 1e12,

@@ -30,8 +30,9 @@ for i in range(min(n, 15)):
 wf = w.float(); weff = torch.where(wf != 0, wf + 2 * a.float() @ b.float(), torch.zeros_like(wf))
 ref = dy.float() @ weff if dx else x.float() @ weff.t()
 print("rel err", float((out.float() - ref).norm() / ref.norm()))
-names = ["e_full", "p_early(relay)", "reempty", "a_full", "p_act(relay)", "wready"]
-tot = info[46] * 256
-print("MMA thread of cluster 0: total cycles", tot, "steps", info[47])
-for i, n in enumerate(names):
-    print(f"  wait {n:16s} {info[40+i]*256:>12d} cycles  ({info[40+i]*256/max(tot,1)*100:5.1f}%)")
+tot = info[46] * 16
+print("cluster 0: main issuer total cycles", tot, "k-steps", info[47], "cycles/step", tot / max(info[47], 1))
+names = {40: "main: accempty", 41: "main: mready", 42: "recompute: ffready", 43: "recompute: rready",
+         48: "xform warp0: W landed (rready)", 49: "xform warp0: wempty", 50: "xform warp0: refull"}
+for k, n in names.items():
+    print(f"  wait {n:32s} {info[k]*16:>10d} cycles ({info[k]*16/max(tot,1)*100:5.1f}%)")
