@@ -303,17 +303,14 @@ struct alignas(16) Bar16 {
 
 namespace rg {
 constexpr int BM = 128, BN = 256, BK = 64;
-constexpr int XFORM_WARPS = 8, EPI_WARPS = 4;
-constexpr int THREADS = 32 * (XFORM_WARPS + EPI_WARPS + 4);   // + early producer, MMA/relay, act producer, relay
-constexpr int W_EARLY = 8, W_MMA = 9, W_ACT = 10, W_RELAY = 11, W_EPI0 = 12;
-constexpr int NE = 4;     // early ring (W tile + streamed adapter-factor half)
-constexpr int NRE = 2;    // TMEM recompute buffers
-constexpr int NAR = 6;    // activation ring
-constexpr int NW = 3;     // W_eff buffers (TMEM for the dense path, smem for 2:4)
-constexpr int D = 1;      // recompute lookahead (k-steps, crosses tile boundaries)
-// TMEM columns: accumulator [0,256), recompute [256,384), fixed factor [384,416),
-// W_eff [416,512) (dense) or 2:4 metadata at 416 + 8 b + 4 h
-constexpr uint32_t RE_COL = 256, FF_COL = 384, WEFF_COL = 416, E_COL = 416, TMEM_COLS = 512;
+constexpr int THREADS = 384, XFORM_THREADS = 256;
+// early ring (W tile + streamed adapter-factor half) = TMEM recompute buffers;
+// the 2:4 variant gives one recompute buffer to the sparse-metadata columns
+template <bool SP>
+constexpr int ne() { return SP ? 3 : 4; }
+constexpr int NA = 4;   // activation ring = W_eff buffers
+template <bool SP>
+constexpr int lookahead() { return SP ? 2 : 3; }  // recompute lookahead (steps)
 // 2:4 index nibble (idx0 | idx1 << 2, idx0 < idx1) for each 4-bit keep mask;
 // groups with fewer than two kept entries are padded with zero-valued slots,
 // masks with more than two are not 2:4 (prune.py:72-77) and never reach here.
@@ -331,131 +328,132 @@ constexpr uint64_t nibble_lut() {
   return lut;
 }
 constexpr uint64_t kNibbleLut = nibble_lut();
+constexpr uint32_t E_COL = 448;  // 2:4 metadata: W_eff buffer b, MMA h at column 448 + 8 b + 4 h
 constexpr int GROUP_T = 8;  // raster: token tiles per group (clusters of a wave share W and activation tiles)
 constexpr uint32_t ACT_BYTES = (BN / 2) * BK * 2;   // 16 KB: this CTA's token half
 constexpr uint32_t W_BYTES = BM * BK * 2;           // 16 KB
-constexpr uint32_t SPW_BYTES = BM * BK;             // 8 KB: compressed 2:4 W_eff tile
-constexpr uint32_t STG_BYTES = 32 * BM * 2;         // epilogue staging chunk [32 tokens][128 features] bf16
+template <bool SP>
+constexpr uint32_t weff_bytes() { return SP ? BM * BK : BM * BK * 2; }  // 2:4 keeps half (compressed)
+constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t RE_COL = 256;                    // recompute buffers at TMEM cols 256 + 64 e
 template <int RP>
 constexpr uint32_t sf_bytes() { return 32 * RP * 2; }   // streamed factor half (32 k x RP)
+template <int RP>
+constexpr uint32_t ff_bytes() { return 128 * RP * 2; }  // fixed factor tile (128 m x RP)
 template <int RP>
 constexpr uint32_t early_bytes() { return W_BYTES + sf_bytes<RP>(); }
 template <int RP, bool SP>
 constexpr size_t smem_bytes() {
-  return 1024 + NE * early_bytes<RP>() + NAR * ACT_BYTES + (SP ? NW * SPW_BYTES : 0) + 2 * STG_BYTES + 1024;
-}
-
-// grouped raster: GROUP_T token tiles x all feature pairs per group, token
-// tile fastest, so concurrently running clusters share W and activation panels.
-__device__ __forceinline__ void tile_coords(int tile, int n_t, int n_f, int& tt, int& fp) {
-  const int per_group = GROUP_T * n_f;
-  const int g = tile / per_group, idx = tile % per_group;
-  const int gt = min(GROUP_T, n_t - g * GROUP_T);
-  fp = idx / gt;
-  tt = g * GROUP_T + idx % gt;
+  return 1024 + ne<SP>() * early_bytes<RP>() + NA * ACT_BYTES + NA * weff_bytes<SP>() + ff_bytes<RP>() + 1024;
 }
 }  // namespace rg
 
-// Persistent cluster kernel: gridDim.x / 2 clusters loop over the tiles
-// cid, cid + nclusters, ...; every role walks one global k-step sequence over
-// its tiles, so rings, the recompute lookahead and the prefetch of the next
-// tile's operands all run across tile boundaries.  Both MMAs take their A
-// operand from TMEM (W_eff written by the transform with tcgen05.st, the fixed
-// adapter factor written once per tile), which keeps shared-memory traffic to
-// the TMA-staged W / activation / factor tiles and their B-operand reads.
 template <bool DX, int RP, bool BITS, bool SP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
     tc_lors_gemm_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmW,
-                        const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmOut,
-                        const bf16* __restrict__ fac, const bf16* __restrict__ bias,
-                        const uint32_t* __restrict__ bits, int words_per_row, int Mout, int Kred, int L, int r,
-                        float alpha, int n_t, int n_f) {
+                        const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmF,
+                        const __grid_constant__ CUtensorMap tmOut, const bf16* __restrict__ bias,
+                        const uint32_t* __restrict__ bits, int words_per_row, int Mout, int Kred, float alpha) {
   using namespace rg;
   static_assert(!(SP && DX), "2:4 sparse tensor cores apply to the forward only (SURVEY C6)");
-  constexpr uint32_t SF = sf_bytes<RP>(), EB = early_bytes<RP>();
+  constexpr int NE = ne<SP>(), D = lookahead<SP>();
+  constexpr uint32_t WEFF_BYTES = weff_bytes<SP>();
+  constexpr uint32_t SF = sf_bytes<RP>(), FF = ff_bytes<RP>(), EB = early_bytes<RP>();
+  constexpr uint32_t SWR = RP * 2;  // swizzle span of the K-major rank-r tiles
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* early = smem;                      // [NE] W tile | streamed factor half
-  uint8_t* actb = early + NE * EB;            // [NAR] activation halves
-  uint8_t* spw = actb + NAR * ACT_BYTES;      // [NW] compressed 2:4 W_eff (SP only)
-  uint8_t* stg = spw + (SP ? NW * SPW_BYTES : 0);  // [2] epilogue staging chunks
+  uint8_t* early = smem;                     // [NE] W tile | streamed factor half
+  uint8_t* actb = early + NE * EB;           // [NA] activation halves
+  uint8_t* weff = actb + NA * ACT_BYTES;     // [NA] W_eff tiles
+  uint8_t* ffac = weff + NA * WEFF_BYTES;    // fixed factor
   // mbarriers, one per 16 bytes.  rready / mready are the merged "may issue"
   // barriers of the leader: count 18 = own producer (with its TMA bytes) +
-  // the peer's relayed landing + 16 transform warps of both CTAs (for rready:
-  // the recompute buffer this step reuses was read; for mready: the W_eff
-  // halves are written).  In the peer they only track its own TMA landing.
-  Bar16* bars = reinterpret_cast<Bar16*>(stg + 2 * STG_BYTES);
-  Bar16* rready = bars;                 // [NE]
+  // the peer's relayed landing + 16 transform warps of both CTAs.  In the
+  // peer they only track the peer's own TMA landing (count 1).
+  Bar16* bars = reinterpret_cast<Bar16*>(ffac + FF);
+  Bar16* rready = bars;                 // [NE] recompute(j) may issue / W+factor landed
   Bar16* e_empty = rready + NE;         // [NE] local: recompute commit + 8 transform warps done
-  Bar16* mready = e_empty + NE;         // [NAR]
-  Bar16* a_empty = mready + NAR;        // [NAR] local: pair MMA done with the activation half
-  Bar16* refull = a_empty + NAR;        // [NRE] local: recompute landed in TMEM
-  Bar16* wempty = refull + NRE;         // [NW] local: pair MMA done with the W_eff buffer
-  Bar16* ffready = wempty + NW;         // leader: 16 transform warps wrote the tile's fixed factor
-  Bar16* ffempty = ffready + 1;         // local: last recompute of the tile done with it
-  Bar16* accf = ffempty + 1;            // local: accumulator of the tile complete
-  Bar16* accempty = accf + 1;           // leader: 8 epilogue warps drained the accumulator
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 1);
+  Bar16* mready = e_empty + NE;         // [NA] main(j) may issue / activation landed
+  Bar16* a_empty = mready + NA;         // [NA] local: pair MMA done with the activation half
+  Bar16* refull = a_empty + NA;         // [NE] local: recompute landed in TMEM
+  Bar16* wempty = refull + NE;          // [NA] local: pair MMA done with the W_eff buffer
+  uint64_t* ffull = &(wempty + NA)->b;      // local: own fixed factor landed
+  uint64_t* pffull = &(wempty + NA + 1)->b; // leader: peer's fixed factor landed (relayed)
+  uint64_t* accf = &(wempty + NA + 2)->b;   // local: accumulator complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + NA + 3);
 
   const int warp = warp_id(), lane = lane_id();
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
-  const int cid = (int)(blockIdx.x >> 1), ncl = (int)(gridDim.x >> 1);
-  const int n_tiles = n_t * n_f;
-  const int my_tiles = cid < n_tiles ? (n_tiles - 1 - cid) / ncl + 1 : 0;
+  // grouped raster over (token tile, feature pair): GROUP_T token tiles x all
+  // feature pairs per group, token tile fastest, so the ~74 clusters of a wave
+  // read ~9 W panels and <= 8 activation panels and both stay L2-resident.
+  int tt, fp;
+  {
+    const int n_t = (int)gridDim.y;  // token tiles
+    const int n_f = (int)(gridDim.x >> 1);
+    const int cid = (int)blockIdx.y * n_f + (int)(blockIdx.x >> 1);
+    const int per_group = GROUP_T * n_f;
+    const int g = cid / per_group, idx = cid % per_group;
+    const int gt = min(GROUP_T, n_t - g * GROUP_T);
+    fp = idx / gt;
+    tt = g * GROUP_T + idx % gt;
+  }
+  const int m0 = fp * (2 * BM) + rank * BM;   // this CTA's features
+  const int l0 = tt * BN;                       // the pair's tokens
+  const int lh = l0 + rank * (BN / 2);          // this CTA's token half
   const int nk = (Kred + BK - 1) / BK;
-  const int total = my_tiles * nk;       // global k-steps of this cluster
-  auto tile_of = [&](int k, int& m0, int& l0) {
-    int tt, fp;
-    tile_coords(cid + k * ncl, n_t, n_f, tt, fp);
-    m0 = fp * (2 * BM) + (int)rank * BM;   // this CTA's features
-    l0 = tt * BN;                           // the pair's tokens
-  };
 
-  if (warp == W_EARLY && lane == 0) {
+  if (warp == 8 && lane == 0) {
     const uint32_t merged = leader ? 18u : 1u;
     for (int i = 0; i < NE; ++i) {
       mbar_init(&rready[i].b, merged);
       mbar_init(&e_empty[i].b, 9);
+      mbar_init(&refull[i].b, 1);
     }
-    for (int i = 0; i < NAR; ++i) {
+    for (int i = 0; i < NA; ++i) {
       mbar_init(&mready[i].b, merged);
       mbar_init(&a_empty[i].b, 1);
+      mbar_init(&wempty[i].b, 1);
     }
-    for (int i = 0; i < NRE; ++i) mbar_init(&refull[i].b, 1);
-    for (int i = 0; i < NW; ++i) mbar_init(&wempty[i].b, 1);
-    mbar_init(&ffready->b, 16);
-    mbar_init(&ffempty->b, 1);
-    mbar_init(&accf->b, 1);
-    mbar_init(&accempty->b, 8);
+    mbar_init(ffull, 1);
+    mbar_init(pffull, 1);
+    mbar_init(accf, 1);
     fence_barrier_init();
-    // steps 0 .. NRE-1 use each recompute buffer for the first time: nobody has read it
+    // first use of every recompute buffer: nobody has read it yet
     if (leader)
-      for (int i = 0; i < NRE; ++i) mbar_arrive_count(&rready[i].b, 16);
+      for (int i = 0; i < NE; ++i) mbar_arrive_count(&rready[i].b, 16);
     tma_prefetch_desc(&tmAct);
     tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmS);
+    tma_prefetch_desc(&tmF);
     tma_prefetch_desc(&tmOut);
   }
-  if (warp == W_MMA) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+  if (warp == 9) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // Every TMA completes on a barrier of the CTA that issued it; the peer
+  // relays its landings to the leader, and the transform warps of both CTAs
+  // arrive on the leader's merged barriers.  Remote arrives go through mapa.
   const uint32_t rready_l = mapa_shared(smem_u32(rready), 0);
   const uint32_t mready_l = mapa_shared(smem_u32(mready), 0);
-  const uint32_t ffready_l = mapa_shared(smem_u32(ffready), 0);
-  const uint32_t accempty_l = mapa_shared(smem_u32(accempty), 0);
+  const uint32_t pffull_l = mapa_shared(smem_u32(pffull), 0);
 
-  if (warp == W_EARLY) {
+  if (warp == 8) {
     // ------------------------------------------------------------ early-ring producer (both CTAs)
     if (lane == 0) {
-      for (int g = 0; g < total; ++g) {
-        const int k = g / nk, i = g % nk;
-        int m0, l0;
-        tile_of(k, m0, l0);
-        const int e = g % NE;
-        mbar_wait(&e_empty[e].b, ((g / NE) & 1) ^ 1);
+      mbar_arrive_expect_tx(ffull, FF);
+      if (DX) {  // b [r, C] as MN-major A of the recompute: two 64-wide atoms of this CTA's columns
+        tma_load_2d(ffac, &tmF, ffull, m0, 0);
+        tma_load_2d(ffac + FF / 2, &tmF, ffull, m0 + 64, 0);
+      } else {   // a [R, r] K-major, this CTA's rows
+        tma_load_2d(ffac, &tmF, ffull, 0, m0);
+      }
+      for (int i = 0; i < nk; ++i) {
+        const int e = i % NE;
+        mbar_wait(&e_empty[e].b, ((i / NE) & 1) ^ 1);
         uint8_t* st = early + e * EB;
         const int k0 = i * BK;
         mbar_arrive_expect_tx(&rready[e].b, EB);
@@ -469,415 +467,269 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
         }
       }
     }
-  } else if (warp == W_ACT) {
+  } else if (warp == 10) {
     // ------------------------------------------------------------ activation-ring producer (both CTAs)
     if (lane == 0) {
-      for (int g = 0; g < total; ++g) {
-        const int k = g / nk, i = g % nk;
-        int m0, l0;
-        tile_of(k, m0, l0);
-        const int a = g % NAR;
-        mbar_wait(&a_empty[a].b, ((g / NAR) & 1) ^ 1);
+      for (int i = 0; i < nk; ++i) {
+        const int a = i % NA;
+        mbar_wait(&a_empty[a].b, ((i / NA) & 1) ^ 1);
         mbar_arrive_expect_tx(&mready[a].b, ACT_BYTES);
-        tma_load_2d(actb + a * ACT_BYTES, &tmAct, &mready[a].b, i * BK, l0 + (int)rank * (BN / 2));
+        tma_load_2d(actb + a * ACT_BYTES, &tmAct, &mready[a].b, i * BK, lh);
       }
     }
-  } else if (warp == W_RELAY) {
-    if (!leader) {
-      // ---------------------------------------------------------- activation relay (peer CTA)
-      if (lane == 0) {
-        int a = 0;
-        uint32_t ph = 0;
-        for (int g = 0; g < total; ++g) {
-          mbar_wait(&mready[a].b, ph);
-          mbar_arrive_cluster(mready_l + a * 16);
-          if (++a == NAR) { a = 0; ph ^= 1; }
-        }
-      }
-    } else {
-      // ---------------------------------------------------------- main-MMA issuer (leader CTA)
-      // Its own warp (and commit stream) so the recompute stream, issued by
-      // warp W_MMA, never waits behind it; all ring indices are incremental.
-      constexpr uint32_t idesc_main = make_idesc_bf16(256, 256, false, false);
-      constexpr uint32_t idesc_sp = make_idesc_bf16(256, 256, false, false, true);
-      const uint64_t spw_desc = make_sdesc(smem_u32(spw), 16, 512, SW_64);   // compressed, 64 B rows
-      const uint64_t act_desc0 = make_sdesc(smem_u32(actb), 16, 1024, SW_128);
-      int a = 0, wb = 0, im = 0;
-      uint32_t pha = 0, phacc = 1;
-      uint64_t act_desc = act_desc0;
-#ifdef LORS_DEBUG_HANG
-      unsigned long long t_acc = 0, t_m = 0;
-      const unsigned long long t_0 = clock64();
-#endif
-      for (int gm = 0; gm < total; ++gm) {
-        if (im == 0) {
-#ifdef LORS_DEBUG_HANG
-          const unsigned long long c0 = clock64();
-#endif
-          mbar_wait(&accempty->b, phacc);   // epilogue drained the previous tile's accumulator
-#ifdef LORS_DEBUG_HANG
-          t_acc += clock64() - c0;
-#endif
-          phacc ^= 1;
-        }
-#ifdef LORS_DEBUG_HANG
-        const unsigned long long c1 = clock64();
-#endif
-        mbar_wait(&mready[a].b, pha);
-#ifdef LORS_DEBUG_HANG
-        t_m += clock64() - c1;
-#endif
-        tc_fence_after();
-        if (elect_one()) {
-          if (SP) {
-            // two K = 32 sparse MMAs: compressed A advances 32 B, B 64 B, metadata one column each
-            const uint64_t ad = spw_desc + (uint64_t)(wb * (SPW_BYTES >> 4));
-            mma_bf16_pair_sp(tmem, ad, act_desc, tmem + E_COL + wb * 8, idesc_sp, im > 0 ? 1u : 0u);
-            mma_bf16_pair_sp(tmem, ad + 2, act_desc + 4, tmem + E_COL + wb * 8 + 4, idesc_sp, 1u);
-          } else {
-            const uint32_t aw = tmem + WEFF_COL + wb * 32;
-            mma_bf16_pair_ts(tmem, aw, act_desc, idesc_main, im > 0 ? 1u : 0u);
-            mma_bf16_pair_ts(tmem, aw + 8, act_desc + 2, idesc_main, 1u);
-            mma_bf16_pair_ts(tmem, aw + 16, act_desc + 4, idesc_main, 1u);
-            mma_bf16_pair_ts(tmem, aw + 24, act_desc + 6, idesc_main, 1u);
-          }
-          mma_commit_pair(&a_empty[a].b, 0x3);
-          mma_commit_pair(&wempty[wb].b, 0x3);
-          if (im == nk - 1) mma_commit_pair(&accf->b, 0x3);
-        }
-        __syncwarp();
-#ifdef LORS_DEBUG_HANG
-        if (gm == total - 1 && blockIdx.x == 0 && lane == 0) {
-          g_lors_hang[40] = (unsigned)(t_acc >> 4);
-          g_lors_hang[41] = (unsigned)(t_m >> 4);
-          g_lors_hang[46] = (unsigned)((clock64() - t_0) >> 4);
-          g_lors_hang[47] = total;
-        }
-#endif
-        if (++im == nk) im = 0;
-        if (++wb == NW) wb = 0;
-        act_desc += ACT_BYTES >> 4;
-        if (++a == NAR) { a = 0; pha ^= 1; act_desc = act_desc0; }
+  } else if (warp == 11) {
+    // ------------------------------------------------------------ activation relay (peer CTA)
+    if (!leader && lane == 0) {
+      for (int i = 0; i < nk; ++i) {
+        const int a = i % NA;
+        mbar_wait(&mready[a].b, (i / NA) & 1);
+        mbar_arrive_cluster(mready_l + a * 16);
       }
     }
-  } else if (warp == W_MMA) {
+  } else if (warp == 9) {
     if (!leader) {
       // ---------------------------------------------------------- early relay (peer CTA)
       if (lane == 0) {
-        int e = 0;
-        uint32_t ph = 0;
-        for (int g = 0; g < total; ++g) {
-          mbar_wait(&rready[e].b, ph);
+        mbar_wait(ffull, 0);
+        mbar_arrive_cluster(pffull_l);
+        for (int i = 0; i < nk; ++i) {
+          const int e = i % NE;
+          mbar_wait(&rready[e].b, (i / NE) & 1);
           mbar_arrive_cluster(rready_l + e * 16);
-          if (++e == NE) { e = 0; ph ^= 1; }
         }
       }
     } else {
-      // ---------------------------------------------------------- recompute issuer (leader CTA)
-      constexpr uint32_t idesc_re = make_idesc_bf16(256, 64, false, !DX);
-      constexpr uint32_t SWR = RP * 2;
-      const uint64_t sf_desc0 = DX ? make_sdesc(smem_u32(early + W_BYTES), 16, 8 * SWR, sw_layout(SWR))
-                                   : make_sdesc(smem_u32(early + W_BYTES), 0, 8 * 64, SW_64);
+      // ---------------------------------------------------------- MMA issuer (leader CTA, converged warp)
+      constexpr uint32_t idesc_re = make_idesc_bf16(256, 64, DX, !DX);
+      constexpr uint32_t idesc_main = make_idesc_bf16(256, 256, false, false);
+      constexpr uint32_t idesc_sp = make_idesc_bf16(256, 256, false, false, true);
+      // descriptor bases; a descriptor's start-address field is addr >> 4, so
+      // byte offsets inside shared memory are added as (offset >> 4)
+      const uint64_t ff_desc = DX ? make_sdesc(smem_u32(ffac), FF / 2, 1024, SW_128)
+                                  : make_sdesc(smem_u32(ffac), 16, 8 * SWR, sw_layout(SWR));
+      const uint64_t sf_desc = DX ? make_sdesc(smem_u32(early + W_BYTES), 16, 8 * SWR, sw_layout(SWR))
+                                  : make_sdesc(smem_u32(early + W_BYTES), 0, 8 * 64, SW_64);
+      const uint64_t weff_desc = SP ? make_sdesc(smem_u32(weff), 16, 512, SW_64)    // compressed, 64 B rows
+                                    : make_sdesc(smem_u32(weff), 16, 1024, SW_128);
+      const uint64_t act_desc = make_sdesc(smem_u32(actb), 16, 1024, SW_128);
+      constexpr uint32_t FF_KSTEP = DX ? 2048 >> 4 : 32 >> 4;   // per K16 of the recompute
       constexpr uint32_t SF_KSTEP = DX ? 32 >> 4 : 1024 >> 4;
-      int e = 0, rb = 0, i = 0;
-      uint32_t phe = 0, phf = 0;
-      uint64_t sf_desc = sf_desc0;
-#ifdef LORS_DEBUG_HANG
-      unsigned long long t_ff = 0, t_r = 0;
-#endif
-      for (int g = 0; g < total; ++g) {
-        if (i == 0) {
-#ifdef LORS_DEBUG_HANG
-          const unsigned long long c0 = clock64();
-#endif
-          mbar_wait(&ffready->b, phf);
-#ifdef LORS_DEBUG_HANG
-          t_ff += clock64() - c0;
-#endif
-          phf ^= 1u;
-        }
-#ifdef LORS_DEBUG_HANG
-        const unsigned long long c1 = clock64();
-#endif
-        mbar_wait(&rready[e].b, phe);
-#ifdef LORS_DEBUG_HANG
-        t_r += clock64() - c1;
-        if (g == total - 1 && blockIdx.x == 0 && lane == 0) {
-          g_lors_hang[42] = (unsigned)(t_ff >> 4);
-          g_lors_hang[43] = (unsigned)(t_r >> 4);
-        }
-#endif
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t d = tmem + RE_COL + rb * 64, f = tmem + FF_COL;
+      mbar_wait(ffull, 0);
+      mbar_wait(pffull, 0);
+      for (int j = 0; j < nk + D; ++j) {
+        if (j < nk) {  // recompute for step j, D steps ahead of its main MMA
+          const int e = j % NE;
+          mbar_wait(&rready[e].b, (j / NE) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t sfd = sf_desc + (uint64_t)(e * (EB >> 4));
 #pragma unroll
-          for (int kk = 0; kk < RP / 16; ++kk)
-            mma_bf16_pair_ts(d, f + kk * 8, sf_desc + kk * SF_KSTEP, idesc_re, kk > 0 ? 1u : 0u);
-          mma_commit_pair(&refull[rb].b, 0x3);
-          mma_commit_pair(&e_empty[e].b, 0x3);
-          if (i == nk - 1) mma_commit_pair(&ffempty->b, 0x3);
-        }
-        __syncwarp();
-        rb ^= 1;
-        sf_desc += EB >> 4;
-        if (++e == NE) { e = 0; phe ^= 1; sf_desc = sf_desc0; }
-        if (++i == nk) i = 0;
-      }
-    }
-  } else if (warp >= W_EPI0) {
-    // ------------------------------------------------------------ epilogue warps 12..15
-    // TMEM -> registers -> bf16 -> [32 tokens][128 features] staging chunk -> TMA
-    // store, two chunks in flight; the accumulator is released to the MMA as
-    // soon as its last chunk is in registers.
-    const int q = warp & 3;
-    const int t = q * 32 + lane;
-    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    const bool issuer = (warp == W_EPI0 && lane == 0);
-    for (int k = 0; k < my_tiles; ++k) {
-      int m0, l0;
-      tile_of(k, m0, l0);
-      const int gm = m0 + t;
-      float bv = 0.f;
-      if (!DX && bias != nullptr && gm < Mout) bv = __bfloat162float(bias[gm]);
-      mbar_wait(&accf->b, k & 1);
-      tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_x32(tmem + lane_addr + c * 32, v);
-        tmem_ld_wait();
-        if (c == BN / 32 - 1) {  // last read of this tile's accumulator: release it
-          tc_fence_before();
+            for (int kk = 0; kk < RP / 16; ++kk)
+              mma_bf16_pair(tmem + RE_COL + e * 64, ff_desc + kk * FF_KSTEP, sfd + kk * SF_KSTEP, idesc_re,
+                            kk > 0 ? 1u : 0u);
+            mma_commit_pair(&refull[e].b, 0x3);
+            mma_commit_pair(&e_empty[e].b, 0x3);
+          }
           __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(accempty_l);
         }
-        uint8_t* buf = stg + (c & 1) * STG_BYTES;
-        if (issuer) tma_store_wait_read1();   // the store that last used `buf` has read it
-        named_bar_sync(2, 32 * EPI_WARPS);
+        const int jm = j - D;
+        if (jm >= 0) {  // main MMA for step jm
+          const int a = jm % NA;
+          mbar_wait(&mready[a].b, (jm / NA) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t ad = weff_desc + (uint64_t)(a * (WEFF_BYTES >> 4));
+            const uint64_t bd = act_desc + (uint64_t)(a * (ACT_BYTES >> 4));
+            if (SP) {
+              // two K = 32 sparse MMAs: compressed A advances 32 B, B 64 B, metadata one column each
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          *reinterpret_cast<bf16*>(buf + j * (BM * 2) + t * 2) = __float2bfloat16_rn(__uint_as_float(v[j]) + bv);
-        fence_proxy_async_smem();
-        named_bar_sync(2, 32 * EPI_WARPS);
-        if (issuer) {
-          tma_store_2d(&tmOut, buf, m0, l0 + c * 32);
-          tma_store_commit();
+              for (int hh = 0; hh < 2; ++hh)
+                mma_bf16_pair_sp(tmem, ad + hh * 2, bd + hh * 4, tmem + E_COL + a * 8 + hh * 4, idesc_sp,
+                                 (jm > 0 || hh > 0) ? 1u : 0u);
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk)
+                mma_bf16_pair(tmem, ad + kk * 2, bd + kk * 2, idesc_main, (jm > 0 || kk > 0) ? 1u : 0u);
+            }
+            mma_commit_pair(&a_empty[a].b, 0x3);
+            mma_commit_pair(&wempty[a].b, 0x3);
+          }
+          __syncwarp();
         }
       }
+      if (elect_one()) mma_commit_pair(accf, 0x3);
+      __syncwarp();
     }
-    if (issuer) tma_store_wait_all();
   } else {
     // ------------------------------------------------------------ transform warps 0..7
     const int q = warp & 3;        // TMEM lane quarter
     const int h = warp >> 2;       // column half of the 64-wide k-step
     const int t = q * 32 + lane;   // feature row inside the tile (TMEM lane)
+    const int gm = m0 + t;         // global output feature
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const uint32_t alpha2 = pack_bf16x2(alpha, alpha);
-    // The tile's fixed adapter factor as the recompute's A operand in TMEM:
-    // row t holds F[t, 0..r) (fwd: a[m0 + t, :]; dX: b[:, m0 + t]), this warp
-    // half writes k in [h RP/2, (h+1) RP/2).  Single-buffered: tile k+1's
-    // factor is fetched into registers while tile k runs and stored right
-    // after the tile's last recompute has landed.
-    auto load_factor = [&](int k, uint32_t (&v)[RP / 4]) {
-      int m0, l0;
-      tile_of(k, m0, l0);
-      const int gmr = m0 + t;
-#pragma unroll
-      for (int c = 0; c < RP / 4; ++c) {
-        const int j0 = h * (RP / 2) + 2 * c;
-        float f0 = 0.f, f1 = 0.f;
-        if (gmr < Mout) {
-          if (DX) {
-            if (j0 < r) f0 = __bfloat162float(fac[(int64_t)j0 * Mout + gmr]);
-            if (j0 + 1 < r) f1 = __bfloat162float(fac[(int64_t)(j0 + 1) * Mout + gmr]);
-          } else {
-            if (j0 < r) f0 = __bfloat162float(fac[(int64_t)gmr * r + j0]);
-            if (j0 + 1 < r) f1 = __bfloat162float(fac[(int64_t)gmr * r + j0 + 1]);
-          }
-        }
-        v[c] = pack_bf16x2(f0, f1);
+    for (int i = 0; i < nk; ++i) {
+      const int e = i % NE, rb = e, wb = i % NA;
+      // 1. rank-r product of this k-step (TMEM -> registers), then release the buffer
+      mbar_wait(&refull[rb].b, (i / NE) & 1);
+      tc_fence_after();
+      uint32_t p[32];
+      const uint32_t re_col = RE_COL + rb * 64 + h * 32;
+      if (!DX) {
+        tmem_ld_x32(tmem + lane_addr + re_col, p);
+      } else {  // fragment layout matching ldmatrix.trans, two 16-lane groups
+        uint32_t (&p0)[16] = *reinterpret_cast<uint32_t(*)[16]>(&p[0]);
+        uint32_t (&p1)[16] = *reinterpret_cast<uint32_t(*)[16]>(&p[16]);
+        tmem_ld_16x256b_x4(tmem + lane_addr + re_col, p0);
+        tmem_ld_16x256b_x4(tmem + lane_addr + (16u << 16) + re_col, p1);
       }
-    };
-    auto store_factor = [&](const uint32_t (&v)[RP / 4]) {
-      tmem_st_32x32b<RP / 4>(tmem + lane_addr + FF_COL + h * (RP / 4), v);
-      tmem_st_wait();
+      tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(ffready_l);
-    };
-    uint32_t fnext[RP / 4];
-    if (my_tiles > 0) {
-      load_factor(0, fnext);
-      store_factor(fnext);
-    }
-    for (int k = 0; k < my_tiles; ++k) {
-      if (k + 1 < my_tiles) load_factor(k + 1, fnext);
-      int m0, l0;
-      tile_of(k, m0, l0);
-      const int gm = m0 + t;       // global output feature
-      for (int i = 0; i < nk; ++i) {
-        const int g = k * nk + i;
-        const int e = g % NE, rb = g % NRE, wb = g % NW, a = g % NAR;
-        // 1. rank-r product of this k-step (TMEM -> registers), then release the buffer
-#ifdef LORS_DEBUG_HANG
-        const unsigned long long cr0 = clock64();
-#endif
-        mbar_wait(&refull[rb].b, (g / NRE) & 1);
-#ifdef LORS_DEBUG_HANG
-        if (blockIdx.x == 0 && warp == 0 && lane == 0) atomicAdd(&g_lors_hang[50], (unsigned)((clock64() - cr0) >> 4));
-#endif
-        tc_fence_after();
-        uint32_t p[32];
-        const uint32_t re_col = RE_COL + rb * 64 + h * 32;
-        if (!DX) {
-          tmem_ld_x32(tmem + lane_addr + re_col, p);
-        } else {  // fragment layout matching ldmatrix.trans, two 16-lane groups
-          uint32_t (&p0)[16] = *reinterpret_cast<uint32_t(*)[16]>(&p[0]);
-          uint32_t (&p1)[16] = *reinterpret_cast<uint32_t(*)[16]>(&p[16]);
-          tmem_ld_16x256b_x4(tmem + lane_addr + re_col, p0);
-          tmem_ld_16x256b_x4(tmem + lane_addr + (16u << 16) + re_col, p1);
-        }
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        // recompute buffer rb is free again: it is next used by step g + NRE
-        if (lane == 0) mbar_arrive_cluster(rready_l + ((g + NRE) % NE) * 16);
-        if (i == nk - 1 && k + 1 < my_tiles) {
-          // the tile's last recompute has landed: hand the factor buffer to tile k+1
-          mbar_wait(&ffempty->b, k & 1);
-          store_factor(fnext);
-        }
-        // 2. W tile landed, destination buffer drained by the MMA of step g - NW
-#ifdef LORS_DEBUG_HANG
-        const unsigned long long cw0 = clock64();
-#endif
-        mbar_wait(&rready[e].b, (g / NE) & 1);
-#ifdef LORS_DEBUG_HANG
-        const unsigned long long cw1 = clock64();
-#endif
-        mbar_wait(&wempty[wb].b, ((g / NW) & 1) ^ 1);
-#ifdef LORS_DEBUG_HANG
-        if (blockIdx.x == 0 && warp == 0 && lane == 0) {
-          atomicAdd(&g_lors_hang[48], (unsigned)((cw1 - cw0) >> 4));
-          atomicAdd(&g_lors_hang[49], (unsigned)((clock64() - cw1) >> 4));
-        }
-#endif
-        const uint32_t wt = smem_u32(early + e * EB);
-        if (!DX) {
-          // thread = W row; 4 chunks of 8 k-values
-          uint32_t mword = 0;
-          uint32_t comp[8], meta = 0;  // 2:4: compressed pairs and index nibbles of this half
-          uint32_t outw[16];           // dense: W_eff pairs of this half for tcgen05.st
-          if (BITS) mword = (gm < Mout) ? __ldg(bits + (int64_t)gm * words_per_row + ((i * BK + h * 32) >> 5)) : 0u;
+      if (lane == 0) mbar_arrive_cluster(rready_l + rb * 16);  // RE buffer free for step i + NE
+      // 2. W tile landed, destination buffer drained by the MMA of step i - NW
+      mbar_wait(&rready[e].b, (i / NE) & 1);
+      mbar_wait(&wempty[wb].b, ((i / NA) & 1) ^ 1);
+      const uint32_t wt = smem_u32(early + e * EB);
+      const uint32_t dst = smem_u32(weff + wb * WEFF_BYTES);
+      if (!DX) {
+        // thread = W row; 4 chunks of 8 k-values, same swizzled position in and out
+        uint32_t mword = 0;
+        uint32_t comp[8], meta = 0;  // 2:4: compressed pairs and index nibbles of this half
+        if (BITS) mword = (gm < Mout) ? __ldg(bits + (int64_t)gm * words_per_row + ((i * BK + h * 32) >> 5)) : 0u;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const uint32_t off = (uint32_t)t * 128 + ((((uint32_t)h * 4 + c) ^ ((uint32_t)t & 7)) << 4);
-            uint4 raw;
-            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
-                         : "r"(wt + off));
-            const uint32_t wv[4] = {raw.x, raw.y, raw.z, raw.w};
-            uint32_t o[4], keepm[4];
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t off = (uint32_t)t * 128 + ((((uint32_t)h * 4 + c) ^ ((uint32_t)t & 7)) << 4);
+          uint4 raw;
+          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
+                       : "r"(wt + off));
+          const uint32_t wv[4] = {raw.x, raw.y, raw.z, raw.w};
+          uint32_t o[4], keepm[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const uint32_t keep = BITS ? bits2_to_mask((mword >> (c * 8 + 2 * u)) & 3u) : nonzero_mask_bf16x2(wv[u]);
-              keepm[u] = keep;
-              o[u] = weff_pair(wv[u], __uint_as_float(p[c * 8 + 2 * u]), __uint_as_float(p[c * 8 + 2 * u + 1]),
-                               alpha2, keep);
-              outw[c * 4 + u] = o[u];
-            }
-            if (SP) {
-              // compress each group of 4 to its two kept values (select on the mask,
-              // so padded slots of sparser groups carry +0) and a 4-bit index nibble
-#pragma unroll
-              for (int gi = 0; gi < 2; ++gi) {
-                const uint32_t k0 = keepm[2 * gi], k1 = keepm[2 * gi + 1];
-                const uint32_t m = (k0 & 1u) | ((k0 >> 15) & 2u) | ((k1 & 1u) << 2) | ((k1 >> 13) & 8u);
-                const uint32_t nib = (uint32_t)(kNibbleLut >> (4 * m)) & 0xFu;
-                const uint32_t sel = 0x1010u + (nib & 3u) * 0x22u + (nib >> 2) * 0x2200u;
-                comp[c * 2 + gi] = prmt(o[2 * gi], o[2 * gi + 1], sel);
-                meta |= nib << (4 * (c * 2 + gi));
-              }
-            }
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t keep = BITS ? bits2_to_mask((mword >> (c * 8 + 2 * u)) & 3u) : nonzero_mask_bf16x2(wv[u]);
+            keepm[u] = keep;
+            o[u] = weff_pair(wv[u], __uint_as_float(p[c * 8 + 2 * u]), __uint_as_float(p[c * 8 + 2 * u + 1]), alpha2,
+                             keep);
           }
           if (SP) {
-            // compressed K-major SW64 tile: row t, bytes [32h, 32h + 32)
-            const uint32_t dst = smem_u32(spw + wb * SPW_BYTES);
+            // compress each group of 4 to its two kept values (select on the mask,
+            // so padded slots of sparser groups carry +0) and a 4-bit index nibble
 #pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-              const uint32_t off = (uint32_t)t * 64 + (((uint32_t)(2 * h + cc) ^ (((uint32_t)t >> 1) & 3u)) << 4);
-              asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + off), "r"(comp[4 * cc]),
-                           "r"(comp[4 * cc + 1]), "r"(comp[4 * cc + 2]), "r"(comp[4 * cc + 3])
-                           : "memory");
+            for (int gi = 0; gi < 2; ++gi) {
+              const uint32_t k0 = keepm[2 * gi], k1 = keepm[2 * gi + 1];
+              const uint32_t m = (k0 & 1u) | ((k0 >> 15) & 2u) | ((k1 & 1u) << 2) | ((k1 >> 13) & 8u);
+              const uint32_t nib = (uint32_t)(kNibbleLut >> (4 * m)) & 0xFu;
+              const uint32_t sel = 0x1010u + (nib & 3u) * 0x22u + (nib >> 2) * 0x2200u;
+              comp[c * 2 + gi] = prmt(o[2 * gi], o[2 * gi + 1], sel);
+              meta |= nib << (4 * (c * 2 + gi));
             }
-            // metadata in the tcgen05 sparse layout: lane L = a + 8b + 16c holds, for the
-            // MMA's k-half b, rows (L & ~8) in bits 0-15 and (L | 8) in bits 16-31
-            const uint32_t pm = __shfl_xor_sync(0xffffffffu, meta, 8);
-            const uint32_t word = (lane & 8) ? ((pm >> 16) | (meta & 0xFFFF0000u)) : ((meta & 0xFFFFu) | (pm << 16));
-            tmem_st_x1(tmem + lane_addr + E_COL + wb * 8 + h * 4, word);
-            fence_proxy_async_smem();
           } else {
-            // W_eff row t, k in [32h, 32h+32): 16 packed columns of the A operand in TMEM
-            tmem_st_32x32b<16>(tmem + lane_addr + WEFF_COL + wb * 32 + h * 16, outw);
-          }
-        } else {
-          // W tile [64 k][128 c] as two SW128 boxes of 64 c.  ldmatrix.trans hands
-          // thread l the pair (k = 32h + 8j + 2(l%4) + {0,1}, c = 32q + 16g + 8s + l/4),
-          // the positions p[16g + 4j + 2s + {0,1}] hold and, as packed W_eff^T pairs,
-          // exactly the (lane, column) slots tcgen05.st.16x128b writes.
-          const int mi = lane >> 3, rr = lane & 7;
-          uint32_t bword[8];
-          if (BITS) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-              for (int e2 = 0; e2 < 2; ++e2) {
-                const int64_t kr = (int64_t)i * BK + h * 32 + 8 * j + 2 * (lane & 3) + e2;
-                bword[j * 2 + e2] = kr < Kred ? __ldg(bits + kr * words_per_row + ((m0 + q * 32) >> 5)) : 0u;
-              }
-          }
-#pragma unroll
-          for (int g16 = 0; g16 < 2; ++g16) {
-            uint32_t outv[8];
-#pragma unroll
-            for (int jp = 0; jp < 2; ++jp) {
-              uint32_t wv[4];
-              {
-                const int sa = mi & 1, ja = 2 * jp + (mi >> 1);
-                const uint32_t k = h * 32 + 8 * ja + rr;
-                const uint32_t c = q * 32 + 16 * g16 + 8 * sa;
-                ldsm_x4_trans(wt + (c >> 6) * 8192 + k * 128 + ((((c & 63) >> 3) ^ (k & 7)) << 4), wv);
-              }
-#pragma unroll
-              for (int mm = 0; mm < 4; ++mm) {
-                const int sm = mm & 1, j = 2 * jp + (mm >> 1);
-                uint32_t keep;
-                if (BITS) {
-                  const uint32_t cb = (q * 32 + 16 * g16 + 8 * sm + (lane >> 2)) & 31;
-                  keep = bits2_to_mask(((bword[j * 2] >> cb) & 1u) | (((bword[j * 2 + 1] >> cb) & 1u) << 1));
-                } else {
-                  keep = nonzero_mask_bf16x2(wv[mm]);
-                }
-                outv[2 * j + sm] = weff_pair(wv[mm], __uint_as_float(p[16 * g16 + 4 * j + 2 * sm]),
-                                             __uint_as_float(p[16 * g16 + 4 * j + 2 * sm + 1]), alpha2, keep);
-              }
-            }
-            tmem_st_16x128b_x4(tmem + lane_addr + ((uint32_t)(16 * g16) << 16) + WEFF_COL + wb * 32 + h * 16, outv);
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + off), "r"(o[0]), "r"(o[1]), "r"(o[2]),
+                         "r"(o[3])
+                         : "memory");
           }
         }
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&e_empty[e].b);                  // done reading the W tile
-          mbar_arrive_cluster(mready_l + a * 16);      // W_eff half ready for the pair MMA
+        if (SP) {
+          // compressed K-major SW64 tile: row t, bytes [32h, 32h + 32)
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const uint32_t off = (uint32_t)t * 64 + (((uint32_t)(2 * h + cc) ^ (((uint32_t)t >> 1) & 3u)) << 4);
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + off), "r"(comp[4 * cc]),
+                         "r"(comp[4 * cc + 1]), "r"(comp[4 * cc + 2]), "r"(comp[4 * cc + 3])
+                         : "memory");
+          }
+          // metadata in the tcgen05 sparse layout: lane L = a + 8b + 16c holds, for the
+          // MMA's k-half b, rows (L & ~8) in bits 0-15 and (L | 8) in bits 16-31
+          const uint32_t pm = __shfl_xor_sync(0xffffffffu, meta, 8);
+          const uint32_t word = (lane & 8) ? ((pm >> 16) | (meta & 0xFFFF0000u)) : ((meta & 0xFFFFu) | (pm << 16));
+          tmem_st_x1(tmem + lane_addr + E_COL + wb * 8 + h * 4, word);
+          tmem_st_wait();
+          tc_fence_before();
+        }
+      } else {
+        // W tile [64 k][128 c] as two SW128 boxes of 64 c.  ldmatrix.trans hands
+        // thread l the pair (k = 32h + 8j + 2(l%4) + {0,1}, c = 32q + 16g + 8s + l/4),
+        // the positions p[16g + 4j + 2s + {0,1}] hold; results go to the K-major
+        // W_eff^T tile (row c) as 32-bit pairs.
+        const int mi = lane >> 3, rr = lane & 7;
+        uint32_t bword[8];
+        if (BITS) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e2 = 0; e2 < 2; ++e2) {
+              const int64_t kr = (int64_t)i * BK + h * 32 + 8 * j + 2 * (lane & 3) + e2;
+              bword[j * 2 + e2] = kr < Kred ? __ldg(bits + kr * words_per_row + ((m0 + q * 32) >> 5)) : 0u;
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+#pragma unroll
+          for (int jp = 0; jp < 2; ++jp) {
+            uint32_t wv[4];
+            {
+              const int sa = mi & 1, ja = 2 * jp + (mi >> 1);
+              const uint32_t k = h * 32 + 8 * ja + rr;
+              const uint32_t c = q * 32 + 16 * g + 8 * sa;
+              ldsm_x4_trans(wt + (c >> 6) * 8192 + k * 128 + ((((c & 63) >> 3) ^ (k & 7)) << 4), wv);
+            }
+#pragma unroll
+            for (int mm = 0; mm < 4; ++mm) {
+              const int sm = mm & 1, j = 2 * jp + (mm >> 1);
+              const uint32_t ct = q * 32 + 16 * g + 8 * sm + (lane >> 2);
+              const uint32_t k = h * 32 + 8 * j + 2 * (lane & 3);
+              uint32_t keep;
+              if (BITS) {
+                const uint32_t cb = ct & 31;
+                keep = bits2_to_mask(((bword[j * 2] >> cb) & 1u) | (((bword[j * 2 + 1] >> cb) & 1u) << 1));
+              } else {
+                keep = nonzero_mask_bf16x2(wv[mm]);
+              }
+              const uint32_t o = weff_pair(wv[mm], __uint_as_float(p[16 * g + 4 * j + 2 * sm]),
+                                           __uint_as_float(p[16 * g + 4 * j + 2 * sm + 1]), alpha2, keep);
+              sts32(dst + ct * 128 + ((((k >> 3)) ^ (ct & 7)) << 4) + (k & 7) * 2, o);
+            }
+          }
         }
       }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&e_empty[e].b);                  // done reading the W tile
+        mbar_arrive_cluster(mready_l + wb * 16);     // W_eff half ready for the pair MMA
+      }
+    }
+    // ------------------------------------------------------------ epilogue
+    mbar_wait(accf, 0);
+    tc_fence_after();
+    // stage [256 tokens][128 features] bf16 (256 B rows) in the drained ring buffers
+    uint8_t* stg = smem;
+    float bv = 0.f;
+    if (!DX && bias != nullptr && gm < Mout) bv = __bfloat162float(bias[gm]);
+#pragma unroll 1
+    for (int c0 = 0; c0 < 128; c0 += 32) {
+      const int col = h * 128 + c0;  // token offset inside the pair tile
+      uint32_t v[32];
+      tmem_ld_x32(tmem + lane_addr + col, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        *reinterpret_cast<bf16*>(stg + (col + j) * 256 + t * 2) = __float2bfloat16_rn(__uint_as_float(v[j]) + bv);
+      }
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, XFORM_THREADS);
+    if (warp == 0 && lane == 0) {
+      tma_store_2d(&tmOut, stg, m0, l0);
+      tma_store_commit();
+      tma_store_wait_all();
     }
   }
   tc_fence_before();
   cluster_sync();
-  if (warp == W_MMA) tmem_dealloc_pair<TMEM_COLS>(tmem);
+  if (warp == 9) tmem_dealloc_pair<TMEM_COLS>(tmem);
 }
 
 template <bool DX, int RP, bool SP>
@@ -886,7 +738,7 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
                             cudaStream_t s) {
   using namespace rg;
   const int Mout = DX ? C : R, Kred = DX ? R : C;
-  CUtensorMap tAct, tW, tS, tOut;
+  CUtensorMap tAct, tW, tS, tF, tOut;
   int st;
   if ((st = make_map(&tAct, act, Kred, L, 64, BN / 2, 128, "activation"))) return st;
   if (DX) st = make_map(&tW, w, C, R, 64, 64, 128, "W (dX)");
@@ -894,23 +746,18 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
   if (st) return st;
   if (DX) {
     if ((st = make_map(&tS, a, r, R, RP, 32, RP * 2, "a (streamed half)"))) return st;
+    if ((st = make_map(&tF, b, C, r, 64, RP, 128, "b (fixed)"))) return st;
   } else {
     if ((st = make_map(&tS, b, C, r, 32, RP, 64, "b (streamed half)"))) return st;
+    if ((st = make_map(&tF, a, r, R, RP, 128, RP * 2, "a (fixed)"))) return st;
   }
-  if ((st = make_map(&tOut, out, Mout, L, BM, 32, 0, "output chunk"))) return st;
+  if ((st = make_map(&tOut, out, Mout, L, 128, BN, 0, "output"))) return st;
   auto kern = bits ? tc_lors_gemm_kernel<DX, RP, true, SP> : tc_lors_gemm_kernel<DX, RP, false, SP>;
   const size_t smem = smem_bytes<RP, SP>();
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "lors_gemm smem attribute");
-  const int n_f = (int)ceil_div(Mout, 2 * BM), n_t = (int)ceil_div(L, BN);
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int clusters = std::max(1, std::min(n_f * n_t, sms / 2));
-  // fixed factor source: a [R, r] (fwd rows) or b [r, C] (dX columns)
-  const bf16* fac = DX ? b : a;
-  kern<<<dim3(2 * clusters), THREADS, smem, s>>>(tAct, tW, tS, tOut, fac, bias, bits, (int)ceil_div(C, 32), Mout,
-                                                 Kred, L, r, alpha, n_t, n_f);
+  dim3 grid((unsigned)(2 * ceil_div(Mout, 2 * BM)), (unsigned)ceil_div(L, BN));
+  kern<<<grid, THREADS, smem, s>>>(tAct, tW, tS, tF, tOut, bias, bits, (int)ceil_div(C, 32), Mout, Kred, alpha);
   LORS_CHECK_LAUNCH(DX ? "tc_lors_gemm<dx>" : "tc_lors_gemm<fwd>");
   return LORS_OK;
 }
