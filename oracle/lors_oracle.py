@@ -221,6 +221,64 @@ def projection_residual(dw, b):
 
 
 # ---------------------------------------------------------------------------
+# the reference's own training task (train.py) -- loss-curve oracle
+# ---------------------------------------------------------------------------
+
+def adaptive_update(p, g, m, v, step, lr, beta1=0.9, beta2=0.999, eps=1e-8):
+    """OptimState "adaptive" with bias correction, in place (train.py:139-154)."""
+    m[:] = beta1 * m + (1.0 - beta1) * g
+    v[:] = beta2 * v + (1.0 - beta2) * g * g
+    m_hat = m / (1.0 - beta1 ** step)
+    v_hat = v / (1.0 - beta2 ** step)
+    p[:] = p - lr * m_hat / (np.sqrt(v_hat) + eps)
+
+
+def toy_finetune(bases, a_list, b_list, x_t, t_t, batches, lr, alpha=ALPHA_DEFAULT, optimizer="adaptive"):
+    """Loss per step of the reference's finetune loop on a ToyModel of lors
+    layers with ReLU between them and the regression head
+    (train.py:53-79 forward_loss, :196-207 _run_step, :255-277 finetune).
+
+    x_t [N, C] and t_t [N, R_last] are the dataset in torch layout, batches is
+    [steps, batch] column indices; a_list / b_list are updated in place.
+    Loss = 0.5 * sum((Y - T)^2) / batch, so dY = (Y - T) / batch.
+    """
+    a_list = [np.array(a, dtype=np.float64) for a in a_list]      # copies: updated in place below
+    b_list = [np.array(b, dtype=np.float64) for b in b_list]
+    bases = [np.asarray(w, dtype=np.float64) for w in bases]
+    mom = [(np.zeros_like(a), np.zeros_like(a), np.zeros_like(b), np.zeros_like(b))
+           for a, b in zip(a_list, b_list)]
+    losses = []
+    for step, idx in enumerate(batches, start=1):
+        x = np.ascontiguousarray(np.asarray(x_t, dtype=np.float64)[idx].T)   # C x L
+        t = np.ascontiguousarray(np.asarray(t_t, dtype=np.float64)[idx].T)
+        acts, pre = [x], []
+        for i, w in enumerate(bases):
+            z = lors_forward(w, a_list[i], b_list[i], acts[-1], alpha)
+            pre.append(z)
+            if i < len(bases) - 1:
+                acts.append(np.maximum(z, 0.0))
+        diff = pre[-1] - t
+        n = x.shape[1]
+        losses.append(0.5 * float(np.sum(diff * diff)) / n)
+        dy = diff / n
+        grads = [None] * len(bases)
+        for i in range(len(bases) - 1, -1, -1):
+            g = lors_backward(bases[i], a_list[i], b_list[i], acts[i], dy, alpha)
+            grads[i] = g
+            if i > 0:
+                dy = g.dx * (pre[i - 1] > 0.0)
+        for i, g in enumerate(grads):
+            if optimizer == "sgd":                     # train.py:145-147
+                a_list[i][:] = a_list[i] - lr * g.da
+                b_list[i][:] = b_list[i] - lr * g.db
+                continue
+            ma, va, mb, vb = mom[i]
+            adaptive_update(a_list[i], g.da, ma, va, step, lr)
+            adaptive_update(b_list[i], g.db, mb, vb, step, lr)
+    return np.array(losses), a_list, b_list
+
+
+# ---------------------------------------------------------------------------
 # torch-layout helpers for the parity harness
 # ---------------------------------------------------------------------------
 
