@@ -30,6 +30,7 @@ class LoRSParams:
     mask_bits: Optional[torch.Tensor] = None
     save_p: bool = False          # keep P = X b^T (rL elements, dense-LoRA footprint)
     fault_da_sign: bool = False   # negative control (adapters.py:57-60)
+    sparse24: bool = False        # forward on 2:4 sparse tensor cores (north_star 4)
 
 
 class LoRSFunction(torch.autograd.Function):
@@ -49,7 +50,8 @@ class LoRSFunction(torch.autograd.Function):
         a = lora_A.detach().to(dt).contiguous()
         b = lora_B.detach().to(dt).contiguous()
         bias_c = None if bias is None else bias.detach().to(dt).contiguous()
-        y, p = ops.lors_fwd(x2, weight, a, b, params.alpha, bias_c, params.mask_bits, emit_p=params.save_p)
+        y, p = ops.lors_fwd(x2, weight, a, b, params.alpha, bias_c, params.mask_bits, emit_p=params.save_p,
+                            sparse24=params.sparse24)
         if params.save_p:
             ctx.save_for_backward(x2, p)
         else:
@@ -98,7 +100,7 @@ class LoRSLinear(nn.Module):
     def __init__(self, weight: torch.Tensor, rank: Optional[int] = None, a: Optional[torch.Tensor] = None,
                  b: Optional[torch.Tensor] = None, alpha: float = 2.0, bias: Optional[torch.Tensor] = None,
                  name: str = "", grad_mode: str = "ste", mask_mode: str = "from_w", save_p: bool = False,
-                 param_dtype: torch.dtype = torch.float32):
+                 param_dtype: torch.dtype = torch.float32, sparse24: bool = False):
         super().__init__()
         if weight.dim() != 2:
             raise ShapeError("weight must be 2-D [out, in]")
@@ -127,6 +129,11 @@ class LoRSLinear(nn.Module):
             raise ArgumentError(f"mask_mode must be 'from_w' or 'bits', got {mask_mode!r}")
         w = weight.detach()
         w = torch.where(w == 0, torch.zeros_like(w), w).contiguous()  # -0.0 -> +0.0 (prune.py:47)
+        if sparse24:
+            from .prune import two_four_valid
+            if w.dtype != torch.bfloat16 or C % 64 or not two_four_valid(w):
+                raise ArgumentError("sparse24 needs a bf16 weight that is 2:4 along the input axis, in % 64 == 0")
+        self.sparse24 = sparse24
         self.register_buffer("weight", w)
         self.a = nn.Parameter(a.detach().clone())
         self.b = nn.Parameter(b.detach().clone())
@@ -155,7 +162,7 @@ class LoRSLinear(nn.Module):
 
     def params(self) -> LoRSParams:
         return LoRSParams(alpha=self.alpha, grad_mode=self.grad_mode, mask_bits=self.mask,
-                          save_p=self.save_p, fault_da_sign=self.fault_da_sign)
+                          save_p=self.save_p, fault_da_sign=self.fault_da_sign, sparse24=self.sparse24)
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         return LoRSFunction.apply(x, self.weight, self.bias, self.a, self.b, self.params())

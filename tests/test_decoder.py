@@ -1,0 +1,221 @@
+"""LLaMA-shaped LoRS decoder and its data-parallel trainer.
+
+CPU: the model-level cost figures of SURVEY 8 d3 / BASELINE.md, the decoder's
+structure with the test-only torch projection, and the world-size-2 gloo
+trainer (DDP step == single-process step on the concatenated batch).
+GPU: the native decoder against the torch and float64-oracle projections, the
+2:4 sparse-tensor-core forward inside the model, mask preservation through
+training, and a model-level loss curve.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2501_08582_b200 import decoder as dec
+from paper_2501_08582_b200.trainer import Trainer, synthetic_tokens
+
+
+# --------------------------------------------------------------------------- cost KATs
+
+@pytest.mark.parametrize("name,adapters_m,gflop_tok,roof_spec", [
+    ("llama2-7b", 39.98, 27.64, 81418),
+    ("llama3-8b", 167.77, 33.01, 86431),
+    ("llama2-13b", 250.35, 59.09, 38081),
+])
+def test_model_cost_matches_survey(name, adapters_m, gflop_tok, roof_spec):
+    cfg = dec.preset(name)
+    assert abs(dec.adapter_param_count(cfg) / 1e6 - adapters_m) < 0.01
+    assert abs(dec.flops_per_token(cfg)["total"] / 1e9 - gflop_tok) < 0.01
+    assert abs(dec.roofline_tokens_per_s(cfg, 2250.0, 4500.0) - roof_spec) / roof_spec < 2e-3
+
+
+def test_cfg3_cost_breakdown():
+    f = dec.flops_per_token(dec.preset("llama2-7b"))
+    assert abs(f["linear"] / 1e9 - 26.06) < 0.01
+    assert abs(f["attention"] / 1e9 - 0.94) < 0.01
+    assert abs(f["head"] / 1e9 - 0.52) < 0.01
+    assert abs(f["recompute"] / 1e9 - 0.11) < 0.01
+
+
+# --------------------------------------------------------------------------- CPU structure
+
+def _tiny(**kw):
+    return dec.preset("tiny", **kw)
+
+
+def test_tiny_decoder_structure_cpu():
+    from ref_linear import torch_factory
+    cfg = _tiny(dtype=torch.float32)
+    m = dec.LoRSDecoder(cfg, device="cpu", linear_factory=torch_factory)
+    names = sorted(n for n, _ in m.named_parameters())
+    assert len(names) == 2 * 7 * cfg.n_layers and all(n.endswith((".a", ".b")) for n in names)
+    assert sum(p.numel() for p in m.parameters()) == dec.adapter_param_count(cfg)
+    for proj in m.projections():
+        w = proj.weight
+        assert float((w == 0).float().mean()) == pytest.approx(0.5, abs=1e-6)   # per-row 50%
+    tok = synthetic_tokens(cfg.vocab, cfg.batch, cfg.seq, step=0, device="cpu")
+    loss = m.loss(tok)
+    assert abs(float(loss.detach()) - np.log(cfg.vocab)) < 1.0
+    loss.backward()
+    assert all(p.grad is not None for p in m.parameters())
+
+
+def test_two_four_preset_prunes_two_of_four_cpu():
+    from ref_linear import torch_factory
+    from paper_2501_08582_b200.prune import two_four_valid
+    m = dec.LoRSDecoder(_tiny(dtype=torch.float32, sparsity="two_four"), device="cpu", linear_factory=torch_factory)
+    for proj in m.projections():
+        assert two_four_valid(proj.weight)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _ddp_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from ref_linear import torch_factory
+        cfg = _tiny(dtype=torch.float32, n_layers=1, seq=32)
+        torch.manual_seed(0)
+        m = dec.LoRSDecoder(cfg, device="cpu", linear_factory=torch_factory, seed=0)
+        with torch.no_grad():
+            for p in m.parameters():
+                p.normal_(0, 0.05)
+        tr = Trainer(m, lr=1e-2, overlap=True, bucket_bytes=4096)
+        for step in range(2):
+            tr.step(synthetic_tokens(cfg.vocab, cfg.batch, cfg.seq, step=step, rank=rank, device="cpu"))
+        q.put((rank, {n: p.detach().numpy().copy() for n, p in m.named_parameters()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_trainer_ddp_world2_equals_single_process():
+    """Two gloo ranks with overlapped bucketed all-reduce end with exactly the adapters
+    one process gets from the two ranks' batches concatenated (the mean loss over
+    equal-size shards has the averaged gradient)."""
+    from ref_linear import torch_factory
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ddp_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = _tiny(dtype=torch.float32, n_layers=1, seq=32)
+    torch.manual_seed(0)
+    m = dec.LoRSDecoder(cfg, device="cpu", linear_factory=torch_factory, seed=0)
+    with torch.no_grad():
+        for p in m.parameters():
+            p.normal_(0, 0.05)
+    tr = Trainer(m, lr=1e-2)
+    for step in range(2):
+        tok = torch.cat([synthetic_tokens(cfg.vocab, cfg.batch, cfg.seq, step=step, rank=r, device="cpu")
+                         for r in range(world)])
+        tr.step(tok)
+    for n, p in m.named_parameters():
+        for r in range(world):
+            np.testing.assert_allclose(res[r][n], p.detach().numpy(), rtol=1e-5, atol=1e-6)
+    for n in res[0]:
+        np.testing.assert_array_equal(res[0][n], res[1][n])
+
+
+# --------------------------------------------------------------------------- GPU
+
+def _native_and_ref(cfg, ref_factory, ref_dtype, ref_device, seed=0):
+    m = dec.LoRSDecoder(cfg, device="cuda", seed=seed)
+    ref = dec.LoRSDecoder(dec.replace(cfg, dtype=ref_dtype), device=ref_device, linear_factory=ref_factory,
+                          seed=seed)
+    ref.load_state_dict(m.state_dict())
+    return m, ref
+
+
+def _grads(model):
+    return {n: p.grad.detach().double().cpu() for n, p in model.named_parameters()}
+
+
+def _rel(a, b):
+    return float((a - b).norm() / b.norm())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-4), (torch.bfloat16, 2e-2)])
+def test_native_decoder_matches_torch_reference(dtype, tol):
+    from ref_linear import torch_factory
+    cfg = _tiny(dtype=dtype)
+    m, ref = _native_and_ref(cfg, torch_factory, torch.float32, "cuda")
+    tok = synthetic_tokens(cfg.vocab, cfg.batch, cfg.seq, step=0, device="cuda")
+    l1 = m.loss(tok)
+    l1.backward()
+    l2 = ref.loss(tok)
+    l2.backward()
+    assert abs(float(l1.detach()) - float(l2.detach())) / float(l2.detach()) < tol
+    g1, g2 = _grads(m), _grads(ref)
+    worst = max(_rel(g1[n], g2[n]) for n in g2)
+    assert worst < (5 * tol if dtype == torch.bfloat16 else tol), worst
+
+
+@pytest.mark.gpu
+def test_native_decoder_sparse24_forward_matches_dense_masked():
+    cfg = _tiny(sparsity="two_four", dim=256, ffn=512)
+    m = dec.LoRSDecoder(cfg, device="cuda", seed=1)
+    dense = dec.LoRSDecoder(cfg, device="cuda", seed=1,
+                            linear_factory=dec.lors_factory(cfg, seed=1, sparse24_forward=False))
+    dense.load_state_dict(m.state_dict())
+    assert all(p.sparse24 for p in m.projections()) and not any(p.sparse24 for p in dense.projections())
+    tok = synthetic_tokens(cfg.vocab, cfg.batch, cfg.seq, step=0, device="cuda")
+    with torch.no_grad():
+        a, b = m(tok[:, :-1]).float(), dense(tok[:, :-1]).float()
+    assert _rel(a.cpu().double(), b.cpu().double()) < 1e-2
+
+
+@pytest.mark.gpu
+def test_decoder_training_preserves_masks_bit_exactly():
+    from paper_2501_08582_b200 import ops
+    cfg = _tiny()
+    m = dec.LoRSDecoder(cfg, device="cuda")
+    tr = Trainer(m, lr=1e-2)
+    for step in range(3):
+        tr.step(synthetic_tokens(cfg.vocab, cfg.batch, cfg.seq, step=step, device="cuda"))
+    for proj in m.projections():
+        weff = proj.effective_weight()
+        assert torch.all(weff[proj.weight == 0].view(torch.int16) == 0)
+        assert torch.count_nonzero(weff) <= torch.count_nonzero(proj.weight)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-4), (torch.bfloat16, 1e-2)])
+def test_decoder_loss_curve_vs_float64_oracle(dtype, tol):
+    """a reduced LLaMA-shaped decoder trained 30 steps through the native
+    kernels tracks the same decoder whose projections call the float64 oracle on the
+    CPU (test-only shim) within 1% (bf16) / 1e-4 (fp32)."""
+    from ref_linear import oracle_factory
+    cfg = _tiny(dtype=dtype, n_layers=2, seq=64)
+    m, ref = _native_and_ref(cfg, oracle_factory, torch.float64, "cpu")
+    t1, t2 = Trainer(m, lr=1e-3), Trainer(ref, lr=1e-3)
+    l1, l2 = [], []
+    tok = synthetic_tokens(cfg.vocab, cfg.batch, cfg.seq, step=0, device="cpu")   # fit one batch
+    for step in range(30):
+        l1.append(float(t1.step(tok.cuda())))
+        l2.append(float(t2.step(tok)))
+    l1, l2 = np.array(l1), np.array(l2)
+    rel = np.abs(l1 - l2) / l2
+    print(f"{dtype}: decoder loss {l2[0]:.4f} -> {l2[-1]:.4f}; max rel deviation {rel.max():.2e}")
+    assert l2[-1] < l2[0] - 1.0
+    assert rel.max() <= tol
