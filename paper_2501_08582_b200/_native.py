@@ -14,6 +14,8 @@ import threading
 from .errors import ArgumentError, DeviceError, ShapeError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_native", "liblors_b200.so")
+# tools/ kernel experiments load alternative builds of the same sources
+LIB_PATH = os.environ.get("LORS_B200_LIB", LIB_PATH)
 
 LORS_OK, LORS_ERR_SHAPE, LORS_ERR_ARGUMENT, LORS_ERR_DEVICE, LORS_ERR_CUDA = range(5)
 DTYPE_F32, DTYPE_BF16 = 0, 1

@@ -303,11 +303,15 @@ struct alignas(16) Bar16 {
 
 namespace rg {
 constexpr int BM = 128, BN = 256, BK = 64;
-constexpr int THREADS = 384, XFORM_THREADS = 256;
-// early ring (W tile + streamed adapter-factor half) = TMEM recompute buffers;
-// the 2:4 variant gives one recompute buffer to the sparse-metadata columns
+constexpr int THREADS = 416, XFORM_THREADS = 256;
+// factor ring (streamed adapter-factor half) = TMEM recompute buffers; the 2:4
+// variant gives one recompute buffer to the sparse-metadata columns.  The W
+// ring is separate: the recompute of step j needs only its factor slice, W(j)
+// is first read by the transform, D steps later, so W loads are not exposed.
 template <bool SP>
 constexpr int ne() { return SP ? 3 : 4; }
+template <bool SP>
+constexpr int nw() { return SP ? 6 : 4; }  // W ring
 constexpr int NA = 4;   // activation ring = W_eff buffers
 template <bool SP>
 constexpr int lookahead() { return SP ? 2 : 3; }  // recompute lookahead (steps)
@@ -340,11 +344,10 @@ template <int RP>
 constexpr uint32_t sf_bytes() { return 32 * RP * 2; }   // streamed factor half (32 k x RP)
 template <int RP>
 constexpr uint32_t ff_bytes() { return 128 * RP * 2; }  // fixed factor tile (128 m x RP)
-template <int RP>
-constexpr uint32_t early_bytes() { return W_BYTES + sf_bytes<RP>(); }
 template <int RP, bool SP>
 constexpr size_t smem_bytes() {
-  return 1024 + ne<SP>() * early_bytes<RP>() + NA * ACT_BYTES + NA * weff_bytes<SP>() + ff_bytes<RP>() + 1024;
+  return 1024 + ne<SP>() * sf_bytes<RP>() + nw<SP>() * W_BYTES + NA * ACT_BYTES + NA * weff_bytes<SP>() +
+         ff_bytes<RP>() + 1024;
 }
 }  // namespace rg
 
@@ -356,14 +359,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
                         const uint32_t* __restrict__ bits, int words_per_row, int Mout, int Kred, float alpha) {
   using namespace rg;
   static_assert(!(SP && DX), "2:4 sparse tensor cores apply to the forward only (SURVEY C6)");
-  constexpr int NE = ne<SP>(), D = lookahead<SP>();
+  constexpr int NE = ne<SP>(), NW = nw<SP>(), D = lookahead<SP>();
   constexpr uint32_t WEFF_BYTES = weff_bytes<SP>();
-  constexpr uint32_t SF = sf_bytes<RP>(), FF = ff_bytes<RP>(), EB = early_bytes<RP>();
+  constexpr uint32_t SF = sf_bytes<RP>(), FF = ff_bytes<RP>();
   constexpr uint32_t SWR = RP * 2;  // swizzle span of the K-major rank-r tiles
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* early = smem;                     // [NE] W tile | streamed factor half
-  uint8_t* actb = early + NE * EB;           // [NA] activation halves
+  uint8_t* sfr = smem;                       // [NE] streamed factor halves
+  uint8_t* wring = sfr + NE * SF;            // [NW] W tiles
+  uint8_t* actb = wring + NW * W_BYTES;      // [NA] activation halves
   uint8_t* weff = actb + NA * ACT_BYTES;     // [NA] W_eff tiles
   uint8_t* ffac = weff + NA * WEFF_BYTES;    // fixed factor
   // mbarriers, one per 16 bytes.  rready / mready are the merged "may issue"
@@ -371,8 +375,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
   // the peer's relayed landing + 16 transform warps of both CTAs.  In the
   // peer they only track the peer's own TMA landing (count 1).
   Bar16* bars = reinterpret_cast<Bar16*>(ffac + FF);
-  Bar16* rready = bars;                 // [NE] recompute(j) may issue / W+factor landed
-  Bar16* e_empty = rready + NE;         // [NE] local: recompute commit + 8 transform warps done
+  Bar16* rready = bars;                 // [NE] recompute(j) may issue / factor landed
+  Bar16* e_empty = rready + NE;         // [NE] local: recompute committed (factor slot free)
   Bar16* mready = e_empty + NE;         // [NA] main(j) may issue / activation landed
   Bar16* a_empty = mready + NA;         // [NA] local: pair MMA done with the activation half
   Bar16* refull = a_empty + NA;         // [NE] local: recompute landed in TMEM
@@ -380,7 +384,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
   uint64_t* ffull = &(wempty + NA)->b;      // local: own fixed factor landed
   uint64_t* pffull = &(wempty + NA + 1)->b; // leader: peer's fixed factor landed (relayed)
   uint64_t* accf = &(wempty + NA + 2)->b;   // local: accumulator complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + NA + 3);
+  Bar16* wfull = wempty + NA + 3;       // [NW] local: W tile landed
+  Bar16* wfree = wfull + NW;            // [NW] local: 8 transform warps done reading the W tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wfree + NW);
 
   const int warp = warp_id(), lane = lane_id();
   const uint32_t rank = cluster_ctarank();
@@ -408,13 +414,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
     const uint32_t merged = leader ? 18u : 1u;
     for (int i = 0; i < NE; ++i) {
       mbar_init(&rready[i].b, merged);
-      mbar_init(&e_empty[i].b, 9);
+      mbar_init(&e_empty[i].b, 1);
       mbar_init(&refull[i].b, 1);
     }
     for (int i = 0; i < NA; ++i) {
       mbar_init(&mready[i].b, merged);
       mbar_init(&a_empty[i].b, 1);
       mbar_init(&wempty[i].b, 1);
+    }
+    for (int i = 0; i < NW; ++i) {
+      mbar_init(&wfull[i].b, 1);
+      mbar_init(&wfree[i].b, 8);
     }
     mbar_init(ffull, 1);
     mbar_init(pffull, 1);
@@ -454,17 +464,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
       for (int i = 0; i < nk; ++i) {
         const int e = i % NE;
         mbar_wait(&e_empty[e].b, ((i / NE) & 1) ^ 1);
-        uint8_t* st = early + e * EB;
+        uint8_t* st = sfr + e * SF;
         const int k0 = i * BK;
-        mbar_arrive_expect_tx(&rready[e].b, EB);
+        mbar_arrive_expect_tx(&rready[e].b, SF);
+        if (DX) tma_load_2d(st, &tmS, &rready[e].b, 0, k0 + 32 * rank);   // a rows, K-major
+        else tma_load_2d(st, &tmS, &rready[e].b, k0 + 32 * rank, 0);      // b cols, MN-major
+      }
+    }
+  } else if (warp == 12) {
+    // ------------------------------------------------------------ W-ring producer (both CTAs)
+    if (lane == 0) {
+      for (int i = 0; i < nk; ++i) {
+        const int wi = i % NW;
+        mbar_wait(&wfree[wi].b, ((i / NW) & 1) ^ 1);
+        uint8_t* st = wring + wi * W_BYTES;
+        const int k0 = i * BK;
+#ifdef LORS_EXP_NO_W_TMA
+        mbar_arrive(&wfull[wi].b);
+#else
+        mbar_arrive_expect_tx(&wfull[wi].b, W_BYTES);
         if (DX) {  // W[k0:k0+64, m0:m0+128] as two SW128 boxes of 64 columns
-          tma_load_2d(st, &tmW, &rready[e].b, m0, k0);
-          tma_load_2d(st + W_BYTES / 2, &tmW, &rready[e].b, m0 + 64, k0);
-          tma_load_2d(st + W_BYTES, &tmS, &rready[e].b, 0, k0 + 32 * rank);   // a rows, K-major
+          tma_load_2d(st, &tmW, &wfull[wi].b, m0, k0);
+          tma_load_2d(st + W_BYTES / 2, &tmW, &wfull[wi].b, m0 + 64, k0);
         } else {   // W[m0:m0+128, k0:k0+64], SW128
-          tma_load_2d(st, &tmW, &rready[e].b, k0, m0);
-          tma_load_2d(st + W_BYTES, &tmS, &rready[e].b, k0 + 32 * rank, 0);   // b cols, MN-major
+          tma_load_2d(st, &tmW, &wfull[wi].b, k0, m0);
         }
+#endif
       }
     }
   } else if (warp == 10) {
@@ -473,8 +498,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
       for (int i = 0; i < nk; ++i) {
         const int a = i % NA;
         mbar_wait(&a_empty[a].b, ((i / NA) & 1) ^ 1);
+#ifdef LORS_EXP_NO_ACT_TMA
+        mbar_arrive(&mready[a].b);
+#else
         mbar_arrive_expect_tx(&mready[a].b, ACT_BYTES);
         tma_load_2d(actb + a * ACT_BYTES, &tmAct, &mready[a].b, i * BK, lh);
+#endif
       }
     }
   } else if (warp == 11) {
@@ -507,8 +536,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
       // byte offsets inside shared memory are added as (offset >> 4)
       const uint64_t ff_desc = DX ? make_sdesc(smem_u32(ffac), FF / 2, 1024, SW_128)
                                   : make_sdesc(smem_u32(ffac), 16, 8 * SWR, sw_layout(SWR));
-      const uint64_t sf_desc = DX ? make_sdesc(smem_u32(early + W_BYTES), 16, 8 * SWR, sw_layout(SWR))
-                                  : make_sdesc(smem_u32(early + W_BYTES), 0, 8 * 64, SW_64);
+      const uint64_t sf_desc = DX ? make_sdesc(smem_u32(sfr), 16, 8 * SWR, sw_layout(SWR))
+                                  : make_sdesc(smem_u32(sfr), 0, 8 * 64, SW_64);
       const uint64_t weff_desc = SP ? make_sdesc(smem_u32(weff), 16, 512, SW_64)    // compressed, 64 B rows
                                     : make_sdesc(smem_u32(weff), 16, 1024, SW_128);
       const uint64_t act_desc = make_sdesc(smem_u32(actb), 16, 1024, SW_128);
@@ -522,11 +551,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
           mbar_wait(&rready[e].b, (j / NE) & 1);
           tc_fence_after();
           if (elect_one()) {
-            const uint64_t sfd = sf_desc + (uint64_t)(e * (EB >> 4));
+            const uint64_t sfd = sf_desc + (uint64_t)(e * (SF >> 4));
+#ifndef LORS_EXP_NO_RECOMPUTE
 #pragma unroll
             for (int kk = 0; kk < RP / 16; ++kk)
               mma_bf16_pair(tmem + RE_COL + e * 64, ff_desc + kk * FF_KSTEP, sfd + kk * SF_KSTEP, idesc_re,
                             kk > 0 ? 1u : 0u);
+#endif
             mma_commit_pair(&refull[e].b, 0x3);
             mma_commit_pair(&e_empty[e].b, 0x3);
           }
@@ -568,12 +599,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
     const int gm = m0 + t;         // global output feature
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const uint32_t alpha2 = pack_bf16x2(alpha, alpha);
-    for (int i = 0; i < nk; ++i) {
-      const int e = i % NE, rb = e, wb = i % NA;
+    // Per k-step: issue the TMEM load of the rank-r product and all W loads,
+    // release the recompute buffer, then transform and store.  (Pipelining the
+    // loads of step i + 1 under step i measured no faster.)
+    auto issue = [&](const int i, uint32_t (&p)[32], uint32_t (&wv)[16]) {
       // 1. rank-r product of this k-step (TMEM -> registers), then release the buffer
+      const int rb = i % NE;
       mbar_wait(&refull[rb].b, (i / NE) & 1);
       tc_fence_after();
-      uint32_t p[32];
       const uint32_t re_col = RE_COL + rb * 64 + h * 32;
       if (!DX) {
         tmem_ld_x32(tmem + lane_addr + re_col, p);
@@ -583,16 +616,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
         tmem_ld_16x256b_x4(tmem + lane_addr + re_col, p0);
         tmem_ld_16x256b_x4(tmem + lane_addr + (16u << 16) + re_col, p1);
       }
+      // 2. W tile landed: all of this thread's W loads are issued before any
+      //    result is needed, so their latency overlaps the TMEM load's
+      const int wi = i % NW;
+      mbar_wait(&wfull[wi].b, (i / NW) & 1);
+      const uint32_t wt = smem_u32(wring + wi * W_BYTES);
+      if (!DX) {
+        // thread = W row t; chunks 4h .. 4h+3 of 8 k-values (SW128)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          lds128(wt + (uint32_t)t * 128 + ((((uint32_t)h * 4 + c) ^ ((uint32_t)t & 7)) << 4),
+                 *reinterpret_cast<uint32_t(*)[4]>(&wv[4 * c]));
+      } else {
+        // W tile [64 k][128 c] as two SW128 boxes of 64 c; ldmatrix.trans
+        const int mi = lane >> 3, rr = lane & 7;
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+          for (int jp = 0; jp < 2; ++jp) {
+            const int sa = mi & 1, ja = 2 * jp + (mi >> 1);
+            const uint32_t k = h * 32 + 8 * ja + rr;
+            const uint32_t c = q * 32 + 16 * g + 8 * sa;
+            ldsm_x4_trans(wt + (c >> 6) * 8192 + k * 128 + ((((c & 63) >> 3) ^ (k & 7)) << 4),
+                          *reinterpret_cast<uint32_t(*)[4]>(&wv[4 * (2 * g + jp)]));
+          }
+      }
+    };
+    auto release = [&](const int i) {
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(rready_l + rb * 16);  // RE buffer free for step i + NE
-      // 2. W tile landed, destination buffer drained by the MMA of step i - NW
-      mbar_wait(&rready[e].b, (i / NE) & 1);
+      if (lane == 0) mbar_arrive_cluster(rready_l + (i % NE) * 16);  // RE buffer free for step i + NE
+    };
+    auto finish = [&](const int i, uint32_t (&p)[32], uint32_t (&wv)[16]) {
+      const int wb = i % NA, wi = i % NW;
+      // 3. destination buffer drained by the MMA of step i - NA
       mbar_wait(&wempty[wb].b, ((i / NA) & 1) ^ 1);
-      const uint32_t wt = smem_u32(early + e * EB);
       const uint32_t dst = smem_u32(weff + wb * WEFF_BYTES);
-      if (!DX) {
+#ifdef LORS_EXP_EARLY_ARRIVE
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mready_l + wb * 16);  // timing experiment only (races)
+#endif
+#ifdef LORS_EXP_NO_XFORM
+      constexpr bool XF = false;  // timing experiment: W_eff buffers left as they are
+#else
+      constexpr bool XF = true;
+#endif
+      if (XF && !DX) {
         // thread = W row; 4 chunks of 8 k-values, same swizzled position in and out
         uint32_t mword = 0;
         uint32_t comp[8], meta = 0;  // 2:4: compressed pairs and index nibbles of this half
@@ -600,17 +670,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const uint32_t off = (uint32_t)t * 128 + ((((uint32_t)h * 4 + c) ^ ((uint32_t)t & 7)) << 4);
-          uint4 raw;
-          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                       : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
-                       : "r"(wt + off));
-          const uint32_t wv[4] = {raw.x, raw.y, raw.z, raw.w};
           uint32_t o[4], keepm[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const uint32_t keep = BITS ? bits2_to_mask((mword >> (c * 8 + 2 * u)) & 3u) : nonzero_mask_bf16x2(wv[u]);
+            const uint32_t w2 = wv[4 * c + u];
+            const uint32_t keep = BITS ? bits2_to_mask((mword >> (c * 8 + 2 * u)) & 3u) : nonzero_mask_bf16x2(w2);
             keepm[u] = keep;
-            o[u] = weff_pair(wv[u], __uint_as_float(p[c * 8 + 2 * u]), __uint_as_float(p[c * 8 + 2 * u + 1]), alpha2,
+            o[u] = weff_pair(w2, __uint_as_float(p[c * 8 + 2 * u]), __uint_as_float(p[c * 8 + 2 * u + 1]), alpha2,
                              keep);
           }
           if (SP) {
@@ -626,6 +692,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
               meta |= nib << (4 * (c * 2 + gi));
             }
           } else {
+#ifdef LORS_EXP_XF_NO_ST
+            if ((o[0] ^ o[1] ^ o[2] ^ o[3]) == 0x12345679u)
+#endif
             asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + off), "r"(o[0]), "r"(o[1]), "r"(o[2]),
                          "r"(o[3])
                          : "memory");
@@ -648,12 +717,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
           tmem_st_wait();
           tc_fence_before();
         }
-      } else {
-        // W tile [64 k][128 c] as two SW128 boxes of 64 c.  ldmatrix.trans hands
-        // thread l the pair (k = 32h + 8j + 2(l%4) + {0,1}, c = 32q + 16g + 8s + l/4),
-        // the positions p[16g + 4j + 2s + {0,1}] hold; results go to the K-major
-        // W_eff^T tile (row c) as 32-bit pairs.
-        const int mi = lane >> 3, rr = lane & 7;
+      } else if (XF && DX) {
+        // ldmatrix.trans handed thread l the pair (k = 32h + 8j + 2(l%4) + {0,1},
+        // c = 32q + 16g + 8s + l/4), the positions p[16g + 4j + 2s + {0,1}] hold;
+        // results go to the K-major W_eff^T tile (row c) as 32-bit pairs.
         uint32_t bword[8];
         if (BITS) {
 #pragma unroll
@@ -668,13 +735,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
         for (int g = 0; g < 2; ++g) {
 #pragma unroll
           for (int jp = 0; jp < 2; ++jp) {
-            uint32_t wv[4];
-            {
-              const int sa = mi & 1, ja = 2 * jp + (mi >> 1);
-              const uint32_t k = h * 32 + 8 * ja + rr;
-              const uint32_t c = q * 32 + 16 * g + 8 * sa;
-              ldsm_x4_trans(wt + (c >> 6) * 8192 + k * 128 + ((((c & 63) >> 3) ^ (k & 7)) << 4), wv);
-            }
+            const uint32_t* wq = &wv[4 * (2 * g + jp)];
 #pragma unroll
             for (int mm = 0; mm < 4; ++mm) {
               const int sm = mm & 1, j = 2 * jp + (mm >> 1);
@@ -685,21 +746,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
                 const uint32_t cb = ct & 31;
                 keep = bits2_to_mask(((bword[j * 2] >> cb) & 1u) | (((bword[j * 2 + 1] >> cb) & 1u) << 1));
               } else {
-                keep = nonzero_mask_bf16x2(wv[mm]);
+                keep = nonzero_mask_bf16x2(wq[mm]);
               }
-              const uint32_t o = weff_pair(wv[mm], __uint_as_float(p[16 * g + 4 * j + 2 * sm]),
+              const uint32_t o = weff_pair(wq[mm], __uint_as_float(p[16 * g + 4 * j + 2 * sm]),
                                            __uint_as_float(p[16 * g + 4 * j + 2 * sm + 1]), alpha2, keep);
               sts32(dst + ct * 128 + ((((k >> 3)) ^ (ct & 7)) << 4) + (k & 7) * 2, o);
             }
           }
         }
       }
+#ifndef LORS_EXP_NO_FENCE
       fence_proxy_async_smem();
+#endif
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&e_empty[e].b);                  // done reading the W tile
+        mbar_arrive(&wfree[wi].b);                   // done reading the W tile
+#ifndef LORS_EXP_EARLY_ARRIVE
         mbar_arrive_cluster(mready_l + wb * 16);     // W_eff half ready for the pair MMA
+#endif
       }
+    };
+    for (int i = 0; i < nk; ++i) {
+      uint32_t p[32], wv[16];
+      issue(i, p, wv);
+      release(i);
+      finish(i, p, wv);
     }
     // ------------------------------------------------------------ epilogue
     mbar_wait(accf, 0);

@@ -384,6 +384,9 @@ __device__ __forceinline__ void ldsm_x4_trans(uint32_t saddr, uint32_t (&v)[4]) 
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
                : "r"(saddr));
 }
+__device__ __forceinline__ void lds128(uint32_t saddr, uint32_t (&v)[4]) {
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(saddr));
+}
 __device__ __forceinline__ void sts32(uint32_t saddr, uint32_t v) {
   asm volatile("st.shared.b32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
 }
