@@ -40,7 +40,11 @@ CONFIGS = {
     "cfg1": dict(R=4096, C=4096, L=2048, r=16, pattern="rowwise", dtype="f32",
                  desc="LoRS linear 4096x4096, 50% per-row, r=16, 2048 tokens (BASELINE configs[0], fp32 parity mode)"),
 }
+# Model-level workloads (BASELINE configs 3-5): a fine-tuning step of the LLaMA-shaped
+# decoder whose 7 projections per layer are LoRS linears (decoder.py / trainer.py).
+DECODER_CONFIGS = {"cfg3": "llama2-7b", "cfg4": "llama3-8b", "cfg5": "llama2-13b", "tiny": "tiny"}
 FALLBACK_PEAKS = dict(bf16_tflops=1590.0, hbm_gbs=6650.0)
+SPEC_PEAKS = dict(dense_tflops=2250.0, sparse_tflops=4500.0, hbm_gbs=8000.0)  # north_star's roofline
 
 
 def peaks():
@@ -160,9 +164,47 @@ def cpu_baseline(cfg, L_sample=1024, reps=3):
             "s_per_sample_step": med}
 
 
+def decoder_cpu_baseline(dcfg, L_sample=256):
+    """Reference CPU LoRS-linear time for one decoder token, extrapolated: each
+    distinct projection shape timed once with the float64 port on an L_sample-token sample,
+    summed over the 7 projections x layers; attention, norms and the LM head excluded."""
+    import collections
+    shapes = collections.Counter(dcfg.shapes().values())
+    per_token_s = 0.0
+    detail = {}
+    for (R, C), count in shapes.items():
+        cfg = dict(R=R, C=C, r=dcfg.rank, pattern=dcfg.sparsity)
+        w, a, b, x, dy = cpu_inputs(cfg, L_sample)
+        cpu_step(w, a, b, x, dy)
+        t0 = time.perf_counter()
+        cpu_step(w, a, b, x, dy)
+        dt = time.perf_counter() - t0
+        per_token_s += count * dcfg.n_layers * dt / L_sample
+        detail[f"{R}x{C}"] = dt
+    return {"value": 1.0 / per_token_s, "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
+            "sample": f"each distinct projection shape once on {L_sample} tokens (float64 numpy port, OpenBLAS "
+                      f"threads = {cpu_cores()}), summed x 7 projections x {dcfg.n_layers} layers; reference CPU "
+                      "LoRS-linear time, extrapolated, attention / norms / LM head excluded",
+            "s_per_shape_sample": detail}
+
+
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
+        return 0
+    if args.config in DECODER_CONFIGS:
+        from paper_2501_08582_b200 import decoder as D
+        dcfg = D.preset(DECODER_CONFIGS[args.config])
+        cb = decoder_cpu_baseline(dcfg)
+        line = {
+            "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": 1, "warmup": 1, "ms_per_step": 1e3 * dcfg.tokens_per_step() / cb["value"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {DECODER_CONFIGS[args.config]} decoder, LoRS linears only"},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
         return 0
     L_sample = 1024
     w, a, b, x, dy = cpu_inputs(cfg, L_sample)
@@ -448,16 +490,170 @@ def run_native(args, cfg):
     return 0
 
 
+def run_decoder(args):
+    """Fine-tuning step of a LLaMA-shaped LoRS decoder (BASELINE configs 3-5): forward, next-token
+    CE, backward through the LoRS kernels, NCCL all-reduce of the adapter gradients (N > 1),
+    AdamW on a/b.  Weak scaling: every rank runs batch x seq tokens of its own."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_08582_b200 import _native, decoder as D
+    from paper_2501_08582_b200.trainer import Trainer, synthetic_tokens
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _native.check(_native.load().lors_device_check())
+    name = DECODER_CONFIGS[args.config]
+    dcfg = D.preset(name)
+    T = dcfg.tokens_per_step()
+    stream = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def build(kind):
+        if kind == "lors":
+            fac = D.lors_factory(dcfg, seed=0, sparse24_forward=args.sparse24)
+        else:
+            from paper_2501_08582_b200.comparators import comparator_factory
+            fac = comparator_factory(kind, dcfg, seed=0)
+        model = D.LoRSDecoder(dcfg, device=dev, seed=0, linear_factory=fac)
+        return model, Trainer(model, lr=2e-5)
+
+    def measure(kind, steps, warmup, sample_clocks=False):
+        model, trainer = build(kind)
+        toks = [synthetic_tokens(dcfg.vocab, dcfg.batch, dcfg.seq, s, rank=rank, device=dev)
+                for s in range(steps + warmup)]
+        for s in range(warmup):
+            trainer.step(toks[s])
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats(dev)
+        clocks = ClockSampler(dev) if sample_clocks else None
+        _native.reset_launch_count()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for s in range(steps):
+            loss = trainer.step(toks[warmup + s])
+        e1.record(stream)
+        if clocks:
+            clocks.sample_until(e1)
+        torch.cuda.synchronize()
+        launches = _native.launch_count()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        peak = torch.cuda.max_memory_allocated(dev) / 1e9
+        out = {"ms": ms, "peak_gb": peak, "launches": launches, "loss": float(loss),
+               "clocks": clocks.result() if clocks else None}
+        # end to end through the public API: host token ids copied in, loss copied out, every step
+        hbuf = [t.cpu().pin_memory() for t in toks[:min(steps, 5)]]
+        hloss = torch.empty((), dtype=torch.float32).pin_memory()
+        torch.cuda.synchronize()
+        f0, f1 = ev(), ev()
+        f0.record(stream)
+        for s in range(len(hbuf)):
+            l = trainer.step(hbuf[s].to(dev, non_blocking=True))
+            hloss.copy_(l, non_blocking=True)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        out["e2e_ms"] = f0.elapsed_time(f1) / len(hbuf)
+        out["h2d"] = hbuf[0].numel() * hbuf[0].element_size()
+        del trainer, model, toks
+        torch.cuda.empty_cache()
+        return out
+
+    print(f"[bench] {name}: building + warmup", file=sys.stderr, flush=True)
+    r = measure("lors", args.steps, args.warmup, sample_clocks=True)
+    vals = torch.tensor([r["ms"], r["e2e_ms"], r["peak_gb"]], device=dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms, e2e_ms, peak_gb = (float(v) for v in vals)
+    memory = {"lors_peak_gb": peak_gb}
+    comp_speed = {}
+    if args.compare:
+        for kind in ("dense_lora", "sqft"):
+            print(f"[bench] comparator {kind}", file=sys.stderr, flush=True)
+            try:
+                c = measure(kind, max(2, min(args.steps, 5)), 2)
+                memory[kind + "_peak_gb"] = c["peak_gb"]
+                comp_speed[kind + "_tokens_per_s"] = world * T / (c["ms"] * 1e-3)
+            except torch.cuda.OutOfMemoryError as exc:  # report, do not die
+                memory[kind + "_peak_gb"] = f"OOM: {str(exc).splitlines()[0]}"
+                torch.cuda.empty_cache()
+        if isinstance(memory.get("sqft_peak_gb"), float):
+            memory["bytes_not_allocated_vs_sqft_gb"] = memory["sqft_peak_gb"] - peak_gb
+        if isinstance(memory.get("dense_lora_peak_gb"), float):
+            memory["lors_le_dense_lora"] = peak_gb <= memory["dense_lora_peak_gb"]
+    if rank == 0:
+        pk, pk_kind = peaks()
+        f = D.flops_per_token(dcfg)
+        per_gpu = T / (ms * 1e-3)
+        sustained = float(pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])))
+        achieved = f["total"] * per_gpu / 1e12
+        spec_roof = D.roofline_tokens_per_s(dcfg, SPEC_PEAKS["dense_tflops"], SPEC_PEAKS["sparse_tflops"])
+        line = {
+            "metric": METRIC, "value": world * per_gpu, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {name}-shaped decoder fine-tuning step (random init, "
+                                   "uniform token ids)", "layers": dcfg.n_layers, "dim": dcfg.dim,
+                       "ffn": dcfg.ffn, "heads": dcfg.n_heads, "kv_heads": dcfg.n_kv_heads, "vocab": dcfg.vocab,
+                       "rank": dcfg.rank, "sparsity": dcfg.sparsity if dcfg.sparsity == "two_four"
+                       else f"{dcfg.ratio:.0%} per-row magnitude", "seq": dcfg.seq, "batch_per_gpu": dcfg.batch,
+                       "global_batch": dcfg.batch * world, "parallelism": f"dp{world}",
+                       "forward": "2:4 sparse tensor cores" if args.sparse24 and dcfg.sparsity == "two_four"
+                       else "dense-masked tcgen05 (W_eff rebuilt on chip)",
+                       "l2": "weights and activations far larger than L2"},
+            "peak_hbm_gb": peak_gb,
+            "memory": memory,
+            "comparators_tokens_per_s": comp_speed,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
+                         "frac": achieved / sustained, "traffic": None,
+                         "kernel": "whole fine-tuning step (model FLOPs / step time)",
+                         "peak_kind": pk_kind + " bf16 sustained",
+                         "flops_per_token": f, "spec_roofline_tokens_per_s_per_gpu": spec_roof,
+                         "frac_of_spec_roofline": per_gpu / spec_roof},
+            "gpu_launches": r["launches"],
+            "e2e": {"value": world * T / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": r["h2d"],
+                    "d2h_bytes_per_step": 4, "ms_per_step": e2e_ms,
+                    "api": "Trainer.step (LoRSDecoder.loss + backward + all-reduce + AdamW); host token ids "
+                           "copied in and the loss copied out every step"},
+            "clocks": r["clocks"],
+            "loss": r["loss"],
+        }
+        if world == 1 and not args.no_cpu:
+            line["cpu_baseline"] = decoder_cpu_baseline(dcfg)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("native", "reference"), default="native")
-    ap.add_argument("--config", choices=tuple(CONFIGS), default="cfg2")
+    ap.add_argument("--config", choices=tuple(CONFIGS) + tuple(DECODER_CONFIGS), default="cfg2")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline sample")
+    ap.add_argument("--compare", action="store_true",
+                    help="decoder configs: also run the dense-LoRA and SQFT-style decoders (peak HBM, tokens/s)")
+    ap.add_argument("--sparse24", action="store_true",
+                    help="decoder configs with 2:4 masks: forward on the sparse tensor cores")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.config in DECODER_CONFIGS:
+        if args.impl == "reference":
+            return run_reference(args, None)
+        return run_decoder(args)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)

@@ -70,3 +70,51 @@ def peak_bytes_of_step(fn, *tensors) -> int:
     fn(*tensors)
     torch.cuda.synchronize()
     return torch.cuda.max_memory_allocated() - base
+
+
+class _ComparatorLinear(torch.nn.Module):
+    """Frozen weight buffer + fp32 adapter masters a [R, r], b [r, C] (the LoRSLinear
+    parameter layout), forward through one of the comparator Functions above."""
+
+    FN = None
+
+    def __init__(self, weight: torch.Tensor, a: torch.Tensor, b: torch.Tensor, alpha: float = 2.0, name: str = ""):
+        super().__init__()
+        self.register_buffer("weight", weight.detach())
+        self.a = torch.nn.Parameter(a.detach().float().clone())
+        self.b = torch.nn.Parameter(b.detach().float().clone())
+        self.alpha = float(alpha)
+        self.name = name
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        R, C = self.weight.shape
+        y = self.FN.apply(x.reshape(-1, C), self.weight, self.a, self.b, self.alpha)
+        return y.view(*x.shape[:-1], R)
+
+
+class DenseLoRALinear(_ComparatorLinear):
+    FN = DenseLoRAFunction
+
+
+class SQFTLinear(_ComparatorLinear):
+    FN = SQFTFunction
+
+
+def comparator_factory(kind: str, cfg, a_std: float = 1e-3, seed: int = 0):
+    """Decoder linear_factory for the memory comparators: kind "dense_lora" or "sqft".
+    Same seeded adapters as decoder.lors_factory, so the three decoders differ only
+    in the adapter linear."""
+    import math
+
+    cls = {"dense_lora": DenseLoRALinear, "sqft": SQFTLinear}[kind]
+    counter = [0]
+
+    def make(weight, rank, name):
+        g = torch.Generator(device=weight.device).manual_seed(seed * 1000003 + counter[0])
+        counter[0] += 1
+        R, C = weight.shape
+        a = torch.randn(R, rank, generator=g, device=weight.device) * a_std
+        b = torch.randn(rank, C, generator=g, device=weight.device) / math.sqrt(rank)
+        return cls(weight, a, b, alpha=cfg.alpha, name=name)
+
+    return make
