@@ -83,6 +83,33 @@ static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
   return LORS_OK;
 }
 
+static int num_sms() {
+  static int n[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (n[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev] = v > 1 ? v : 148;
+  }
+  return n[dev];
+}
+
+// fp32 -> bf16 of the split-K rank-r side products (P and Q in one launch)
+__global__ void f32_to_bf16_pair_kernel(const float4* __restrict__ a32, __nv_bfloat16* __restrict__ a16, int64_t na4,
+                                        const float4* __restrict__ b32, __nv_bfloat16* __restrict__ b16, int64_t nb4) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const float4* src = i < na4 ? a32 : b32;
+  __nv_bfloat16* dst = i < na4 ? a16 : b16;
+  const int64_t j = i < na4 ? i : i - na4;
+  if (i >= na4 + nb4) return;
+  const float4 v = src[j];
+  uint2 o;
+  o.x = ptx::pack_bf16x2(v.x, v.y);
+  o.y = ptx::pack_bf16x2(v.z, v.w);
+  reinterpret_cast<uint2*>(dst)[j] = o;
+}
+
 static inline uint32_t pad_rank(int r) { return r <= 16 ? 16 : r <= 32 ? 32 : 64; }
 
 // ===========================================================================
@@ -196,7 +223,14 @@ __global__ void __launch_bounds__(sk::THREADS, 1)
       tmem_ld_x16(taddr + c0, v);
       tmem_ld_wait();
       if (m < M) {
-        if (OUT == 0) {
+        if (OUT == 0 && atomic_out) {  // split-K partial: fp32 sums, converted to bf16 afterwards
+          float* o = reinterpret_cast<float*>(out) + (int64_t)m * ldo + c0;
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+            if (c0 + h * 4 + 4 <= N)
+              red_add_v4(o + h * 4, __uint_as_float(v[h * 4]), __uint_as_float(v[h * 4 + 1]),
+                         __uint_as_float(v[h * 4 + 2]), __uint_as_float(v[h * 4 + 3]));
+        } else if (OUT == 0) {
           bf16* o = reinterpret_cast<bf16*>(out) + (int64_t)m * ldo + c0;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -235,7 +269,7 @@ __global__ void __launch_bounds__(sk::THREADS, 1)
 //   B: K-major [N, K] or MN-major [K, N]
 template <int BN, bool A_MN, bool B_MN, int OUT>
 static int launch_skinny(const bf16* A, const bf16* B, void* out, int M, int N, int K, int ldo, float alpha,
-                         bool allow_split, cudaStream_t s) {
+                         bool allow_split, cudaStream_t s, float* acc32 = nullptr) {
   CUtensorMap tA, tB;
   int st;
   if (A_MN) st = make_map(&tA, A, M, K, 64, 64, 128, "skinny A (MN)");
@@ -246,19 +280,25 @@ static int launch_skinny(const bf16* A, const bf16* B, void* out, int M, int N, 
   if (st) return st;
   const int mt = (int)ceil_div(M, sk::BM);
   const int kblocks = (int)ceil_div(K, sk::BK);
+  // split K so that the CTAs fill one wave at two resident per SM (never a
+  // second, mostly empty wave); OUT 0 splits only into a caller-zeroed fp32
+  // accumulator (acc32)
   int split = 1;
-  if (allow_split && OUT != 0) split = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(148, mt), kblocks / 4));
+  const bool can_split = allow_split && (OUT != 0 || acc32 != nullptr);
+  if (can_split) split = (int)std::max<int64_t>(1, std::min<int64_t>((2 * num_sms()) / mt, kblocks / 4));
   const int kps = (int)ceil_div(kblocks, split) * sk::BK;
   split = (int)ceil_div(K, kps);
-  if (split > 1) {
+  if (split > 1 && OUT != 0) {
     const size_t elems = OUT == 2 ? (size_t)N * ldo : (size_t)M * ldo;
     LORS_CUDA_TRY(cudaMemsetAsync(out, 0, elems * sizeof(float), s), "zero split-K output");
   }
+  if (OUT == 0 && acc32 != nullptr) out = acc32;  // fp32 sums; the caller converts to bf16
   auto kern = tc_skinny_kernel<BN, A_MN, B_MN, OUT>;
   const size_t smem = sk::smem_bytes<BN>();
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "skinny smem attribute");
-  kern<<<dim3(mt, split), sk::THREADS, smem, s>>>(tA, tB, out, M, N, K, kps, ldo, alpha, split > 1 ? 1 : 0);
+  const int atomic_out = (split > 1 || (OUT == 0 && acc32 != nullptr)) ? 1 : 0;
+  kern<<<dim3(mt, split), sk::THREADS, smem, s>>>(tA, tB, out, M, N, K, kps, ldo, alpha, atomic_out);
   LORS_CHECK_LAUNCH("tc_skinny");
   return LORS_OK;
 }
@@ -266,11 +306,11 @@ static int launch_skinny(const bf16* A, const bf16* B, void* out, int M, int N, 
 // dispatch on the padded rank
 template <bool A_MN, bool B_MN, int OUT>
 static int skinny(int rp, const bf16* A, const bf16* B, void* out, int M, int N, int K, int ldo, float alpha,
-                  bool allow_split, cudaStream_t s) {
+                  bool allow_split, cudaStream_t s, float* acc32 = nullptr) {
   switch (rp) {
-    case 16: return launch_skinny<16, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s);
-    case 32: return launch_skinny<32, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s);
-    default: return launch_skinny<64, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s);
+    case 16: return launch_skinny<16, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32);
+    case 32: return launch_skinny<32, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32);
+    default: return launch_skinny<64, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32);
   }
 }
 
@@ -1117,7 +1157,10 @@ bool tc_shape_ok(int64_t R, int64_t C, int64_t r) {
 }
 
 size_t tc_fwd_workspace(const lors_fwd_args*) { return 0; }
-size_t tc_bwd_workspace(const lors_bwd_args*) { return 0; }
+// beyond the capi's two bf16 P / Q slots: their fp32 split-K accumulators
+size_t tc_bwd_workspace(const lors_bwd_args* a) {
+  return 2 * (((size_t)a->L * (size_t)a->r * sizeof(float) + 255) / 256 * 256);
+}
 
 int tc_fwd(const lors_fwd_args* A, cudaStream_t s) {
   const int L = (int)A->L, R = (int)A->R, C = (int)A->C, r = (int)A->r;
@@ -1165,12 +1208,25 @@ int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {
     bf16* P = (bf16*)A->p;
     bf16* Q = (bf16*)((char*)A->workspace + slot);
     if (tc) {
-      if (P == nullptr) {  // P = X_t b^T
+      // P = X_t b^T and Q = dY_t a are split over their reductions (C, R) into fp32
+      // accumulators so that L / 128 token tiles still fill the SMs, then rounded to bf16
+      float* P32 = (float*)((char*)A->workspace + 2 * slot);
+      float* Q32 = (float*)((char*)A->workspace + 3 * slot);
+      const bool need_p = P == nullptr;
+      LORS_CUDA_TRY(cudaMemsetAsync(need_p ? (void*)P32 : (void*)Q32, 0, (need_p ? 2 : 1) * slot, s),
+                    "zero rank-r accumulators");
+      if (need_p) {  // P = X_t b^T
         P = (bf16*)A->workspace;
-        if ((st = skinny<false, false, 0>(rp, x, b, P, L, r, C, r, 1.0f, false, s))) return st;
+        if ((st = skinny<false, false, 0>(rp, x, b, P, L, r, C, r, 1.0f, true, s, P32))) return st;
       }
       // Q = dY_t a: A = dY_t K-major [L, R], B = a [R, r] MN-major
-      if ((st = skinny<false, true, 0>(rp, dy, a, Q, L, r, R, r, 1.0f, false, s))) return st;
+      if ((st = skinny<false, true, 0>(rp, dy, a, Q, L, r, R, r, 1.0f, true, s, Q32))) return st;
+      {
+        const int64_t na4 = need_p ? (int64_t)L * r / 4 : 0, nb4 = (int64_t)L * r / 4;
+        f32_to_bf16_pair_kernel<<<(unsigned)ceil_div(na4 + nb4, 256), 256, 0, s>>>(
+            (const float4*)P32, P, na4, (const float4*)Q32, Q, nb4);
+        LORS_CHECK_LAUNCH("rank-r fp32 -> bf16");
+      }
       // dA = alpha dY_t^T P: A = dY_t as MN-major [L, R] (m = R), B = P [L, r] MN-major
       if ((st = skinny<true, true, 1>(rp, dy, P, A->da, R, r, L, r, A->alpha, true, s))) return st;
       // dB^T = alpha X_t^T Q: A = X_t MN-major (m = C), B = Q MN-major; stored transposed into dB [r, C]
