@@ -84,8 +84,10 @@ typedef struct lors_fwd_args {
   const void* x;     /* [L, C]                                         */
   const void* w;     /* [R, C] frozen pruned weight                    */
   const uint32_t* mask_bits; /* [R, ceil(C/32)] when mask_mode == BITS */
-  const void* w24;   /* reserved (pre-compressed 2:4 values); unused:   */
-  const uint8_t* meta24; /* the kernel compresses W_eff tiles on chip   */
+  const void* w24;   /* reserved (pre-compressed 2:4 values), unused   */
+  const uint8_t* meta24; /* SPARSE24 only, optional: [R, C/8] index     */
+                     /* nibbles of W from lors_compress_24 (built once; */
+                     /* NULL = derived on chip from every W tile)       */
   const void* a;     /* [R, r]                                         */
   const void* b;     /* [r, C]                                         */
   const void* bias;  /* [R] or NULL                                    */

@@ -22,6 +22,22 @@
 #include "lors_tc.cuh"
 #include "ptx_sm100.cuh"
 
+#ifdef LORS_EXP_CLOCK
+// timing experiment: per-CTA (clock64, globaltimer) at start and end of the LoRS GEMM
+__device__ unsigned long long g_lors_clk[4096 * 4];
+__device__ unsigned int g_lors_clk_n;
+extern "C" int lors_exp_clock_read(unsigned long long* out, unsigned int* n) {
+  cudaMemcpyFromSymbol(n, g_lors_clk_n, sizeof(unsigned int));
+  unsigned int z = 0;
+  cudaMemcpyToSymbol(g_lors_clk_n, &z, sizeof(unsigned int));
+  return (int)cudaMemcpyFromSymbol(out, g_lors_clk, sizeof(unsigned long long) * 4096 * 4);
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 #ifdef LORS_DEBUG_HANG
 extern "C" int lors_debug_hang_info(unsigned int* out) {
   return (int)cudaMemcpyFromSymbol(out, lors::ptx::g_lors_hang, sizeof(unsigned int) * 64);
@@ -343,7 +359,15 @@ struct alignas(16) Bar16 {
 
 namespace rg {
 constexpr int BM = 128, BN = 256, BK = 64;
-constexpr int THREADS = 416, XFORM_THREADS = 256;
+// warps 0 .. XW-1: transform + epilogue.  The 2:4 forward runs two groups of 8
+// taking alternate k-steps, so one step's transform may span two (twice as
+// fast) sparse MMA steps; the dense kernels measured faster with one group.
+// Then the roles: factor-ring producer, MMA issuer / relay, activation
+// producer, activation relay, W-ring producer.
+template <bool SP>
+constexpr int xw() { return SP ? 16 : 8; }
+template <bool SP>
+constexpr int threads() { return 32 * (xw<SP>() + 5); }
 // factor ring (streamed adapter-factor half) = TMEM recompute buffers; the 2:4
 // variant gives one recompute buffer to the sparse-metadata columns.  The W
 // ring is separate: the recompute of step j needs only its factor slice, W(j)
@@ -392,13 +416,16 @@ constexpr size_t smem_bytes() {
 }  // namespace rg
 
 template <bool DX, int RP, bool BITS, bool SP>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1)
     tc_lors_gemm_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmF,
                         const __grid_constant__ CUtensorMap tmOut, const bf16* __restrict__ bias,
-                        const uint32_t* __restrict__ bits, int words_per_row, int Mout, int Kred, float alpha) {
+                        const uint32_t* __restrict__ bits, const uint8_t* __restrict__ meta24, int words_per_row,
+                        int Mout, int Kred, float alpha) {
   using namespace rg;
   static_assert(!(SP && DX), "2:4 sparse tensor cores apply to the forward only (SURVEY C6)");
+  constexpr int XW = xw<SP>(), XFORM_THREADS = 32 * XW;
+  constexpr int W_SF = XW, W_MMA = XW + 1, W_ACT = XW + 2, W_RELAY = XW + 3, W_WLOAD = XW + 4;
   constexpr int NE = ne<SP>(), NW = nw<SP>(), D = lookahead<SP>();
   constexpr uint32_t WEFF_BYTES = weff_bytes<SP>();
   constexpr uint32_t SF = sf_bytes<RP>(), FF = ff_bytes<RP>();
@@ -419,8 +446,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
   Bar16* e_empty = rready + NE;         // [NE] local: recompute committed (factor slot free)
   Bar16* mready = e_empty + NE;         // [NA] main(j) may issue / activation landed
   Bar16* a_empty = mready + NA;         // [NA] local: pair MMA done with the activation half
-  Bar16* refull = a_empty + NA;         // [NE] local: recompute landed in TMEM
-  Bar16* wempty = refull + NE;          // [NA] local: pair MMA done with the W_eff buffer
+  // [2][NE] local: recompute landed in TMEM, one set per transform group so that
+  // with an odd NE (buffers alternate between the groups) no waiter runs two
+  // phases ahead of a barrier
+  Bar16* refull = a_empty + NA;
+  Bar16* wempty = refull + 2 * NE;      // [NA] local: pair MMA done with the W_eff buffer
   uint64_t* ffull = &(wempty + NA)->b;      // local: own fixed factor landed
   uint64_t* pffull = &(wempty + NA + 1)->b; // leader: peer's fixed factor landed (relayed)
   uint64_t* accf = &(wempty + NA + 2)->b;   // local: accumulator complete
@@ -431,6 +461,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
   const int warp = warp_id(), lane = lane_id();
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
+#ifdef LORS_EXP_CLOCK
+  const unsigned long long clk0 = clock64(), gt0 = gtimer();
+#endif
   // grouped raster over (token tile, feature pair): GROUP_T token tiles x all
   // feature pairs per group, token tile fastest, so the ~74 clusters of a wave
   // read ~9 W panels and <= 8 activation panels and both stay L2-resident.
@@ -450,12 +483,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
   const int lh = l0 + rank * (BN / 2);          // this CTA's token half
   const int nk = (Kred + BK - 1) / BK;
 
-  if (warp == 8 && lane == 0) {
+  if (warp == W_SF && lane == 0) {
     const uint32_t merged = leader ? 18u : 1u;
     for (int i = 0; i < NE; ++i) {
       mbar_init(&rready[i].b, merged);
       mbar_init(&e_empty[i].b, 1);
       mbar_init(&refull[i].b, 1);
+      mbar_init(&refull[NE + i].b, 1);
     }
     for (int i = 0; i < NA; ++i) {
       mbar_init(&mready[i].b, merged);
@@ -479,7 +513,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
     tma_prefetch_desc(&tmF);
     tma_prefetch_desc(&tmOut);
   }
-  if (warp == 9) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+  if (warp == W_MMA) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
@@ -491,7 +525,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
   const uint32_t mready_l = mapa_shared(smem_u32(mready), 0);
   const uint32_t pffull_l = mapa_shared(smem_u32(pffull), 0);
 
-  if (warp == 8) {
+  if (warp == W_SF) {
     // ------------------------------------------------------------ early-ring producer (both CTAs)
     if (lane == 0) {
       mbar_arrive_expect_tx(ffull, FF);
@@ -511,7 +545,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
         else tma_load_2d(st, &tmS, &rready[e].b, k0 + 32 * rank, 0);      // b cols, MN-major
       }
     }
-  } else if (warp == 12) {
+  } else if (warp == W_WLOAD) {
     // ------------------------------------------------------------ W-ring producer (both CTAs)
     if (lane == 0) {
       for (int i = 0; i < nk; ++i) {
@@ -532,7 +566,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
 #endif
       }
     }
-  } else if (warp == 10) {
+  } else if (warp == W_ACT) {
     // ------------------------------------------------------------ activation-ring producer (both CTAs)
     if (lane == 0) {
       for (int i = 0; i < nk; ++i) {
@@ -546,7 +580,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
 #endif
       }
     }
-  } else if (warp == 11) {
+  } else if (warp == W_RELAY) {
     // ------------------------------------------------------------ activation relay (peer CTA)
     if (!leader && lane == 0) {
       for (int i = 0; i < nk; ++i) {
@@ -555,7 +589,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
         mbar_arrive_cluster(mready_l + a * 16);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == W_MMA) {
     if (!leader) {
       // ---------------------------------------------------------- early relay (peer CTA)
       if (lane == 0) {
@@ -598,7 +632,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
               mma_bf16_pair(tmem + RE_COL + e * 64, ff_desc + kk * FF_KSTEP, sfd + kk * SF_KSTEP, idesc_re,
                             kk > 0 ? 1u : 0u);
 #endif
-            mma_commit_pair(&refull[e].b, 0x3);
+            mma_commit_pair(&refull[(j & 1) * NE + e].b, 0x3);
             mma_commit_pair(&e_empty[e].b, 0x3);
           }
           __syncwarp();
@@ -634,7 +668,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
   } else {
     // ------------------------------------------------------------ transform warps 0..7
     const int q = warp & 3;        // TMEM lane quarter
-    const int h = warp >> 2;       // column half of the 64-wide k-step
+    const int h = (warp >> 2) & 1; // column half of the 64-wide k-step
+    const int grp = warp >> 3;     // group: k-step parity this warp transforms (SP), else 0
     const int t = q * 32 + lane;   // feature row inside the tile (TMEM lane)
     const int gm = m0 + t;         // global output feature
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
@@ -642,10 +677,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
     // Per k-step: issue the TMEM load of the rank-r product and all W loads,
     // release the recompute buffer, then transform and store.  (Pipelining the
     // loads of step i + 1 under step i measured no faster.)
-    auto issue = [&](const int i, uint32_t (&p)[32], uint32_t (&wv)[16]) {
+    auto issue = [&](const int i, uint32_t (&p)[32], uint32_t (&wv)[16], uint32_t& mw) {
+      // 0. 2:4 with precomputed metadata: this row's 8 index nibbles of the half
+      //    (lors_compress_24 layout [R, C/8]); the load overlaps everything below
+      if (SP && meta24 != nullptr)
+        mw = gm < Mout ? __ldg(reinterpret_cast<const uint32_t*>(meta24 + (int64_t)gm * (Kred / 8) + i * 8 + h * 4))
+                       : 0x44444444u;
       // 1. rank-r product of this k-step (TMEM -> registers), then release the buffer
       const int rb = i % NE;
-      mbar_wait(&refull[rb].b, (i / NE) & 1);
+      constexpr int RE_PERIOD = (NE % 2) ? 2 * NE : NE;   // steps between a group's uses of one buffer
+      mbar_wait(&refull[(i & 1) * NE + rb].b, (i / RE_PERIOD) & 1);
       tc_fence_after();
       const uint32_t re_col = RE_COL + rb * 64 + h * 32;
       if (!DX) {
@@ -688,7 +729,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(rready_l + (i % NE) * 16);  // RE buffer free for step i + NE
     };
-    auto finish = [&](const int i, uint32_t (&p)[32], uint32_t (&wv)[16]) {
+    auto finish = [&](const int i, uint32_t (&p)[32], uint32_t (&wv)[16], uint32_t mw) {
       const int wb = i % NA, wi = i % NW;
       // 3. destination buffer drained by the MMA of step i - NA
       mbar_wait(&wempty[wb].b, ((i / NA) & 1) ^ 1);
@@ -702,7 +743,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
 #else
       constexpr bool XF = true;
 #endif
-      if (XF && !DX) {
+      if (XF && SP && meta24 != nullptr) {
+        // 2:4 with precomputed index nibbles: select the two kept positions of each
+        // group of 4 first (W and the rounded rank-r product alike), then form
+        // select(W != 0, W + alpha P, +0) on the kept pair only -- bit-identical to
+        // transforming all four and compressing afterwards, half the arithmetic
+        uint32_t comp[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          const uint32_t nib = (mw >> (4 * g)) & 0xFu;
+          const uint32_t sel = 0x1010u + (nib & 3u) * 0x22u + (nib >> 2) * 0x2200u;
+          const uint32_t wsel = prmt(wv[2 * g], wv[2 * g + 1], sel);
+          const uint32_t psel = prmt(cvt_bf16x2(__uint_as_float(p[4 * g]), __uint_as_float(p[4 * g + 1])),
+                                     cvt_bf16x2(__uint_as_float(p[4 * g + 2]), __uint_as_float(p[4 * g + 3])), sel);
+          comp[g] = fma_bf16x2(alpha2, psel, wsel) & nonzero_mask_bf16x2(wsel);
+        }
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const uint32_t off = (uint32_t)t * 64 + (((uint32_t)(2 * h + cc) ^ (((uint32_t)t >> 1) & 3u)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + off), "r"(comp[4 * cc]),
+                       "r"(comp[4 * cc + 1]), "r"(comp[4 * cc + 2]), "r"(comp[4 * cc + 3])
+                       : "memory");
+        }
+#ifdef LORS_EXP_SP_CONST_META
+        const uint32_t pm = 0x44444444u;
+        mw = 0x44444444u;
+#else
+        const uint32_t pm = __shfl_xor_sync(0xffffffffu, mw, 8);
+#endif
+        const uint32_t word = (lane & 8) ? ((pm >> 16) | (mw & 0xFFFF0000u)) : ((mw & 0xFFFFu) | (pm << 16));
+        tmem_st_x1(tmem + lane_addr + E_COL + wb * 8 + h * 4, word);
+        tmem_st_wait();
+        tc_fence_before();
+      } else if (XF && !DX) {
         // thread = W row; 4 chunks of 8 k-values, same swizzled position in and out
         uint32_t mword = 0;
         uint32_t comp[8], meta = 0;  // 2:4: compressed pairs and index nibbles of this half
@@ -806,11 +879,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
 #endif
       }
     };
-    for (int i = 0; i < nk; ++i) {
-      uint32_t p[32], wv[16];
-      issue(i, p, wv);
+    for (int i = grp; i < nk; i += XW / 8) {
+      uint32_t p[32], wv[16], mw = 0;
+      issue(i, p, wv, mw);
       release(i);
-      finish(i, p, wv);
+      finish(i, p, wv, mw);
     }
     // ------------------------------------------------------------ epilogue
     mbar_wait(accf, 0);
@@ -820,8 +893,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
     float bv = 0.f;
     if (!DX && bias != nullptr && gm < Mout) bv = __bfloat162float(bias[gm]);
 #pragma unroll 1
-    for (int c0 = 0; c0 < 128; c0 += 32) {
-      const int col = h * 128 + c0;  // token offset inside the pair tile
+    for (int c0 = 0; c0 < 256 / (XW / 4); c0 += 32) {
+      const int col = (warp >> 2) * (256 / (XW / 4)) + c0;  // token offset inside the pair tile
       uint32_t v[32];
       tmem_ld_x32(tmem + lane_addr + col, v);
       tmem_ld_wait();
@@ -840,13 +913,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::THREADS, 1)
   }
   tc_fence_before();
   cluster_sync();
-  if (warp == 9) tmem_dealloc_pair<TMEM_COLS>(tmem);
+  if (warp == W_MMA) tmem_dealloc_pair<TMEM_COLS>(tmem);
+#ifdef LORS_EXP_CLOCK
+  if (threadIdx.x == 0) {
+    const unsigned int slot = atomicAdd(&g_lors_clk_n, 1u);
+    if (slot < 4096) {
+      g_lors_clk[slot * 4 + 0] = clk0;
+      g_lors_clk[slot * 4 + 1] = clock64();
+      g_lors_clk[slot * 4 + 2] = gt0;
+      g_lors_clk[slot * 4 + 3] = gtimer();
+    }
+  }
+#endif
 }
 
 template <bool DX, int RP, bool SP>
 static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const bf16* b, const bf16* bias,
-                            const uint32_t* bits, bf16* out, int L, int R, int C, int r, float alpha,
-                            cudaStream_t s) {
+                            const uint32_t* bits, const uint8_t* meta24, bf16* out, int L, int R, int C, int r,
+                            float alpha, cudaStream_t s) {
   using namespace rg;
   const int Mout = DX ? C : R, Kred = DX ? R : C;
   CUtensorMap tAct, tW, tS, tF, tOut;
@@ -868,18 +952,20 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "lors_gemm smem attribute");
   dim3 grid((unsigned)(2 * ceil_div(Mout, 2 * BM)), (unsigned)ceil_div(L, BN));
-  kern<<<grid, THREADS, smem, s>>>(tAct, tW, tS, tF, tOut, bias, bits, (int)ceil_div(C, 32), Mout, Kred, alpha);
+  kern<<<grid, threads<SP>(), smem, s>>>(tAct, tW, tS, tF, tOut, bias, bits, SP ? meta24 : nullptr, (int)ceil_div(C, 32),
+                                   Mout, Kred, alpha);
   LORS_CHECK_LAUNCH(DX ? "tc_lors_gemm<dx>" : "tc_lors_gemm<fwd>");
   return LORS_OK;
 }
 
 template <bool DX, bool SP = false>
 static int lors_gemm(int rp, const bf16* act, const bf16* w, const bf16* a, const bf16* b, const bf16* bias,
-                     const uint32_t* bits, bf16* out, int L, int R, int C, int r, float alpha, cudaStream_t s) {
+                     const uint32_t* bits, bf16* out, int L, int R, int C, int r, float alpha, cudaStream_t s,
+                     const uint8_t* meta24 = nullptr) {
   switch (rp) {
-    case 16: return launch_lors_gemm<DX, 16, SP>(act, w, a, b, bias, bits, out, L, R, C, r, alpha, s);
-    case 32: return launch_lors_gemm<DX, 32, SP>(act, w, a, b, bias, bits, out, L, R, C, r, alpha, s);
-    default: return launch_lors_gemm<DX, 64, SP>(act, w, a, b, bias, bits, out, L, R, C, r, alpha, s);
+    case 16: return launch_lors_gemm<DX, 16, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s);
+    case 32: return launch_lors_gemm<DX, 32, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s);
+    default: return launch_lors_gemm<DX, 64, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s);
   }
 }
 
@@ -1180,7 +1266,8 @@ int tc_fwd(const lors_fwd_args* A, cudaStream_t s) {
       set_error("2:4 sparse forward needs C % 64 == 0");
       return LORS_ERR_SHAPE;
     }
-    st = lors_gemm<false, true>(rp, x, w, a, b, (const bf16*)A->bias, bits, (bf16*)A->y, L, R, C, r, A->alpha, s);
+    st = lors_gemm<false, true>(rp, x, w, a, b, (const bf16*)A->bias, bits, (bf16*)A->y, L, R, C, r, A->alpha, s,
+                                A->meta24);
   } else {
     st = lors_gemm<false>(rp, x, w, a, b, (const bf16*)A->bias, bits, (bf16*)A->y, L, R, C, r, A->alpha, s);
   }

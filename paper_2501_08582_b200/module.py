@@ -31,6 +31,7 @@ class LoRSParams:
     save_p: bool = False          # keep P = X b^T (rL elements, dense-LoRA footprint)
     fault_da_sign: bool = False   # negative control (adapters.py:57-60)
     sparse24: bool = False        # forward on 2:4 sparse tensor cores (north_star 4)
+    meta24: Optional[torch.Tensor] = None  # kept-position metadata of the frozen 2:4 weight
 
 
 class LoRSFunction(torch.autograd.Function):
@@ -51,7 +52,7 @@ class LoRSFunction(torch.autograd.Function):
         b = lora_B.detach().to(dt).contiguous()
         bias_c = None if bias is None else bias.detach().to(dt).contiguous()
         y, p = ops.lors_fwd(x2, weight, a, b, params.alpha, bias_c, params.mask_bits, emit_p=params.save_p,
-                            sparse24=params.sparse24)
+                            sparse24=params.sparse24, meta24=params.meta24 if params.sparse24 else None)
         if params.save_p:
             ctx.save_for_backward(x2, p)
         else:
@@ -135,6 +136,9 @@ class LoRSLinear(nn.Module):
                 raise ArgumentError("sparse24 needs a bf16 weight that is 2:4 along the input axis, in % 64 == 0")
         self.sparse24 = sparse24
         self.register_buffer("weight", w)
+        # 2:4 index nibbles of the frozen weight ([R, C/8] u8, 1/16 of W's bytes),
+        # built once here (lors_compress_24) and read by the sparse forward
+        self.register_buffer("meta24", ops.compress_24(w)[1] if sparse24 else None, persistent=False)
         self.a = nn.Parameter(a.detach().clone())
         self.b = nn.Parameter(b.detach().clone())
         self.bias = None if bias is None else nn.Parameter(bias.detach().clone().reshape(R))
@@ -162,7 +166,8 @@ class LoRSLinear(nn.Module):
 
     def params(self) -> LoRSParams:
         return LoRSParams(alpha=self.alpha, grad_mode=self.grad_mode, mask_bits=self.mask,
-                          save_p=self.save_p, fault_da_sign=self.fault_da_sign, sparse24=self.sparse24)
+                          save_p=self.save_p, fault_da_sign=self.fault_da_sign, sparse24=self.sparse24,
+                          meta24=self.meta24)
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         return LoRSFunction.apply(x, self.weight, self.bias, self.a, self.b, self.params())

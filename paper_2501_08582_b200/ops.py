@@ -61,12 +61,14 @@ def _check_layer(x_t, w, a, b):
 
 def lors_fwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tensor, alpha: float = 2.0,
              bias: Optional[torch.Tensor] = None, mask_bits: Optional[torch.Tensor] = None,
-             emit_p: bool = False, sparse24: bool = False):
+             emit_p: bool = False, sparse24: bool = False, meta24: Optional[torch.Tensor] = None):
     """Y_t [L, R] = X_t . W_eff^T (+ bias); optionally P = X_t b^T [L, r].
 
     sparse24=True runs the forward on 2:4 sparse tensor cores: the kernel
     compresses each masked W_eff tile on chip (W must satisfy 2:4 along C,
-    prune.py:72-77; bf16 only)."""
+    prune.py:72-77; bf16 only).  `meta24` ([R, C/8] uint8, the metadata of
+    `compress_24(w)`, computed once per frozen weight) lets the kernel read the
+    kept positions instead of deriving them from every W tile."""
     L, R, C, r = _check_layer(x_t, w, a, b)
     dt = w.dtype
     code = dtype_code(dt)
@@ -74,6 +76,10 @@ def lors_fwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
         _need(t, nm, sh, dt)
     if bias is not None:
         _need(bias, "bias", (R,), dt)
+    if meta24 is not None:
+        if not sparse24:
+            raise ArgumentError("meta24 is only used by the 2:4 sparse forward (sparse24=True)")
+        _need(meta24, "meta24", (R, C // 8), torch.uint8)
     y = torch.empty((L, R), dtype=dt, device=w.device)
     p = torch.empty((L, r), dtype=dt, device=w.device) if emit_p else None
     args = N.FwdArgs()
@@ -84,6 +90,7 @@ def lors_fwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
     args.alpha = float(alpha)
     args.x, args.w, args.a, args.b = _p(x_t), _p(w), _p(a), _p(b)
     args.mask_bits = _p(mask_bits)
+    args.meta24 = _p(meta24)
     args.bias, args.y, args.p = _p(bias), _p(y), _p(p)
     lib = N.load()
     ws_bytes = lib.lors_fwd_workspace(ct.byref(args))

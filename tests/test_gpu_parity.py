@@ -384,6 +384,11 @@ def test_sparse24_forward_matches_dense_and_oracle(P, shape):
     ref = orc.lors_forward(*(t.double().cpu().numpy() for t in (w, a, b)), x.double().cpu().numpy().T, 2.0)
     assert _rel(ys, ref.T) <= 2e-2
     assert _rel(ys, yd.double().cpu().numpy()) <= 1e-3
+    # precomputed kept-position metadata (lors_compress_24): same tiles, same bits
+    _, meta, flag = ops.compress_24(w)
+    assert int(flag.item()) == 0
+    ym, _ = ops.lors_fwd(x, w, a, b, 2.0, sparse24=True, meta24=meta)
+    assert torch.equal(ym.view(torch.int16), ys.view(torch.int16))
 
 
 def test_masked_grad_tensor_core_path_vs_oracle(P):

@@ -38,7 +38,8 @@ def fmt(name, res):
     return f"{name} {us:.0f} us @{mhz:.0f} MHz {pw:.0f} W"
 fw = t(lambda: ops.lors_fwd(x, w, a, b, 2.0))
 dxo = t(lambda: ops.lors_bwd(x, w, a, b, dy, 2.0))
-fs = t(lambda: ops.lors_fwd(x, w, a, b, 2.0, sparse24=True))
+meta = ops.compress_24(w)[1]
+fs = t(lambda: ops.lors_fwd(x, w, a, b, 2.0, sparse24=True, meta24=meta))
 mm = t(lambda: x @ w.t())
 name = os.path.basename(os.path.dirname(os.environ.get("LORS_B200_LIB", "default/x")))
 print(f"[{name}] " + " | ".join([fmt("fwd", fw), fmt("bwd", dxo), fmt("fwd24", fs), fmt("cuBLAS", mm)]), flush=True)

@@ -28,7 +28,8 @@ print(f"fwd {fw:.0f} us ({gflop_main/fw*1e3:.0f} TF/s main), bwd {bw:.0f} us, bw
 tot = fw + bw
 flops = 2 * ((R*C*L + r*R*C + R*C) + (R*C*L + 2*r*R*L + 2*r*C*L + r*R*C + R*C))
 print(f"step {tot:.0f} us, {L/tot*1e6/1e6:.2f} M tok/s, algorithmic {flops/tot/1e6:.0f} TF/s")
-fs = t(lambda: ops.lors_fwd(x, w, a, b, 2.0, sparse24=True))
+meta = ops.compress_24(w)[1]
+fs = t(lambda: ops.lors_fwd(x, w, a, b, 2.0, sparse24=True, meta24=meta))
 print(f"sparse-TC fwd {fs:.0f} us ({gflop_main/fs*1e3:.0f} TF/s dense-equivalent) vs dense-masked {fw:.0f} us")
 bm = t(lambda: ops.lors_bwd(x, w, a, b, dy, 2.0, grad_mode="masked", need_dx=False), n=3)
 print(f"masked-G fused grads (no dX) {bm:.0f} us ({2*R*C*L/bm/1e6:.0f} TF/s on the G GEMM)")
