@@ -365,20 +365,30 @@ constexpr int BM = 128, BN = 256, BK = 64;
 // Then the roles: factor-ring producer, MMA issuer / relay, activation
 // producer, activation relay, W-ring producer.
 template <bool SP>
-constexpr int xw() { return SP ? 16 : 8; }
+constexpr int xw() { return 16; }
 template <bool SP>
 constexpr int threads() { return 32 * (xw<SP>() + 5); }
-// factor ring (streamed adapter-factor half) = TMEM recompute buffers; the 2:4
-// variant gives one recompute buffer to the sparse-metadata columns.  The W
+// Token tile of a CTA pair.  The dense kernels take 256 + N2 tokens per W_eff
+// tile -- one N = 256 MMA and one N = N2 MMA per k-step into two accumulators
+// -- so each on-chip W_eff tile (its rank-r recompute, transform and W load)
+// serves 1.5x the tokens; TMEM is then acc 256 + N2 columns plus NE = 2
+// recompute buffers of 64.  The 2:4 kernel keeps 256 tokens: its TMEM holds
+// the sparse metadata next to three recompute buffers.
+template <bool SP>
+constexpr int n2() { return SP ? 0 : 128; }
+template <bool SP>
+constexpr int bnt() { return 256 + n2<SP>(); }            // tokens per pair tile
+// factor ring (streamed adapter-factor half) = TMEM recompute buffers.  The W
 // ring is separate: the recompute of step j needs only its factor slice, W(j)
 // is first read by the transform, D steps later, so W loads are not exposed.
 template <bool SP>
-constexpr int ne() { return SP ? 3 : 4; }
+constexpr int ne() { return SP ? 3 : (512 - 256 - n2<SP>()) / 64; }
 template <bool SP>
 constexpr int nw() { return SP ? 6 : 4; }  // W ring
-constexpr int NA = 4;   // activation ring = W_eff buffers
 template <bool SP>
-constexpr int lookahead() { return SP ? 2 : 3; }  // recompute lookahead (steps)
+constexpr int na() { return SP ? 4 : 3; }  // activation ring = W_eff buffers
+template <bool SP>
+constexpr int lookahead() { return ne<SP>() - 1; }  // recompute lookahead (steps)
 // 2:4 index nibble (idx0 | idx1 << 2, idx0 < idx1) for each 4-bit keep mask;
 // groups with fewer than two kept entries are padded with zero-valued slots,
 // masks with more than two are not 2:4 (prune.py:72-77) and never reach here.
@@ -398,26 +408,29 @@ constexpr uint64_t nibble_lut() {
 constexpr uint64_t kNibbleLut = nibble_lut();
 constexpr uint32_t E_COL = 448;  // 2:4 metadata: W_eff buffer b, MMA h at column 448 + 8 b + 4 h
 constexpr int GROUP_T = 8;  // raster: token tiles per group (clusters of a wave share W and activation tiles)
-constexpr uint32_t ACT_BYTES = (BN / 2) * BK * 2;   // 16 KB: this CTA's token half
+template <bool SP>
+constexpr uint32_t act_bytes() { return (bnt<SP>() / 2) * BK * 2; }   // this CTA's tokens: 24 KB / 16 KB
 constexpr uint32_t W_BYTES = BM * BK * 2;           // 16 KB
 template <bool SP>
 constexpr uint32_t weff_bytes() { return SP ? BM * BK : BM * BK * 2; }  // 2:4 keeps half (compressed)
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t RE_COL = 256;                    // recompute buffers at TMEM cols 256 + 64 e
+template <bool SP>
+constexpr uint32_t re_col() { return 256 + n2<SP>(); }  // recompute buffers at TMEM cols re_col + 64 e
 template <int RP>
 constexpr uint32_t sf_bytes() { return 32 * RP * 2; }   // streamed factor half (32 k x RP)
 template <int RP>
 constexpr uint32_t ff_bytes() { return 128 * RP * 2; }  // fixed factor tile (128 m x RP)
 template <int RP, bool SP>
 constexpr size_t smem_bytes() {
-  return 1024 + ne<SP>() * sf_bytes<RP>() + nw<SP>() * W_BYTES + NA * ACT_BYTES + NA * weff_bytes<SP>() +
-         ff_bytes<RP>() + 1024;
+  return 1024 + ne<SP>() * sf_bytes<RP>() + nw<SP>() * W_BYTES + na<SP>() * act_bytes<SP>() +
+         na<SP>() * weff_bytes<SP>() + ff_bytes<RP>() + 1024;
 }
 }  // namespace rg
 
 template <bool DX, int RP, bool BITS, bool SP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1)
-    tc_lors_gemm_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmW,
+    tc_lors_gemm_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmAct2,
+                        const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmF,
                         const __grid_constant__ CUtensorMap tmOut, const bf16* __restrict__ bias,
                         const uint32_t* __restrict__ bits, const uint8_t* __restrict__ meta24, int words_per_row,
@@ -426,8 +439,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   static_assert(!(SP && DX), "2:4 sparse tensor cores apply to the forward only (SURVEY C6)");
   constexpr int XW = xw<SP>(), XFORM_THREADS = 32 * XW;
   constexpr int W_SF = XW, W_MMA = XW + 1, W_ACT = XW + 2, W_RELAY = XW + 3, W_WLOAD = XW + 4;
-  constexpr int NE = ne<SP>(), NW = nw<SP>(), D = lookahead<SP>();
+  constexpr int NE = ne<SP>(), NW = nw<SP>(), NA = na<SP>(), D = lookahead<SP>();
+  constexpr int NGRP = XW / 8;          // transform groups (alternate k-steps)
+  constexpr int N2 = n2<SP>(), BNT = bnt<SP>();
+  constexpr uint32_t ACT_BYTES = act_bytes<SP>(), ACT1_BYTES = 128 * BK * 2;
+  constexpr uint32_t RE_COL = re_col<SP>();
   constexpr uint32_t WEFF_BYTES = weff_bytes<SP>();
+  // a ring used by the transform groups round robin: the period (in k-steps)
+  // between two uses of one slot by the same group, so phase parities of the
+  // per-group barrier sets stay sequential for odd ring sizes
+  constexpr int RE_PERIOD = (NE % NGRP) ? NGRP * NE : NE;
+  constexpr int W_PERIOD = (NW % NGRP) ? NGRP * NW : NW;
+  constexpr int A_PERIOD = (NA % NGRP) ? NGRP * NA : NA;
   constexpr uint32_t SF = sf_bytes<RP>(), FF = ff_bytes<RP>();
   constexpr uint32_t SWR = RP * 2;  // swizzle span of the K-major rank-r tiles
   extern __shared__ uint8_t smem_raw[];
@@ -450,12 +473,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   // with an odd NE (buffers alternate between the groups) no waiter runs two
   // phases ahead of a barrier
   Bar16* refull = a_empty + NA;
-  Bar16* wempty = refull + 2 * NE;      // [NA] local: pair MMA done with the W_eff buffer
-  uint64_t* ffull = &(wempty + NA)->b;      // local: own fixed factor landed
-  uint64_t* pffull = &(wempty + NA + 1)->b; // leader: peer's fixed factor landed (relayed)
-  uint64_t* accf = &(wempty + NA + 2)->b;   // local: accumulator complete
-  Bar16* wfull = wempty + NA + 3;       // [NW] local: W tile landed
-  Bar16* wfree = wfull + NW;            // [NW] local: 8 transform warps done reading the W tile
+  // [2][NA] local: pair MMA done with the W_eff buffer, set = group of the next writer
+  Bar16* wempty = refull + 2 * NE;
+  uint64_t* ffull = &(wempty + 2 * NA)->b;      // local: own fixed factor landed
+  uint64_t* pffull = &(wempty + 2 * NA + 1)->b; // leader: peer's fixed factor landed (relayed)
+  uint64_t* accf = &(wempty + 2 * NA + 2)->b;   // local: accumulator complete
+  Bar16* wfull = wempty + 2 * NA + 3;   // [2][NW] local: W tile landed, set = group of the reader
+  Bar16* wfree = wfull + 2 * NW;        // [NW] local: 8 transform warps done reading the W tile
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wfree + NW);
 
   const int warp = warp_id(), lane = lane_id();
@@ -479,8 +503,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     tt = g * GROUP_T + idx % gt;
   }
   const int m0 = fp * (2 * BM) + rank * BM;   // this CTA's features
-  const int l0 = tt * BN;                       // the pair's tokens
-  const int lh = l0 + rank * (BN / 2);          // this CTA's token half
+  const int l0 = tt * BNT;                      // the pair's tokens
+  // this CTA's rows of the two MMAs' B operands: tokens l0 + 128 rank .. +127
+  // (N = 256 MMA) and l0 + 256 + (N2 / 2) rank .. (N = N2 MMA)
+  const int lh = l0 + rank * 128, lh2 = l0 + 256 + rank * (N2 / 2);
   const int nk = (Kred + BK - 1) / BK;
 
   if (warp == W_SF && lane == 0) {
@@ -495,9 +521,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       mbar_init(&mready[i].b, merged);
       mbar_init(&a_empty[i].b, 1);
       mbar_init(&wempty[i].b, 1);
+      mbar_init(&wempty[NA + i].b, 1);
     }
     for (int i = 0; i < NW; ++i) {
       mbar_init(&wfull[i].b, 1);
+      mbar_init(&wfull[NW + i].b, 1);
       mbar_init(&wfree[i].b, 8);
     }
     mbar_init(ffull, 1);
@@ -508,6 +536,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     if (leader)
       for (int i = 0; i < NE; ++i) mbar_arrive_count(&rready[i].b, 16);
     tma_prefetch_desc(&tmAct);
+    if (N2) tma_prefetch_desc(&tmAct2);
     tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmS);
     tma_prefetch_desc(&tmF);
@@ -553,15 +582,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         mbar_wait(&wfree[wi].b, ((i / NW) & 1) ^ 1);
         uint8_t* st = wring + wi * W_BYTES;
         const int k0 = i * BK;
+        uint64_t* wf = &wfull[(i % NGRP) * NW + wi].b;   // the set of the group that reads step i
 #ifdef LORS_EXP_NO_W_TMA
-        mbar_arrive(&wfull[wi].b);
+        mbar_arrive(wf);
 #else
-        mbar_arrive_expect_tx(&wfull[wi].b, W_BYTES);
+        mbar_arrive_expect_tx(wf, W_BYTES);
         if (DX) {  // W[k0:k0+64, m0:m0+128] as two SW128 boxes of 64 columns
-          tma_load_2d(st, &tmW, &wfull[wi].b, m0, k0);
-          tma_load_2d(st + W_BYTES / 2, &tmW, &wfull[wi].b, m0 + 64, k0);
+          tma_load_2d(st, &tmW, wf, m0, k0);
+          tma_load_2d(st + W_BYTES / 2, &tmW, wf, m0 + 64, k0);
         } else {   // W[m0:m0+128, k0:k0+64], SW128
-          tma_load_2d(st, &tmW, &wfull[wi].b, k0, m0);
+          tma_load_2d(st, &tmW, wf, k0, m0);
         }
 #endif
       }
@@ -577,6 +607,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 #else
         mbar_arrive_expect_tx(&mready[a].b, ACT_BYTES);
         tma_load_2d(actb + a * ACT_BYTES, &tmAct, &mready[a].b, i * BK, lh);
+        if (N2) tma_load_2d(actb + a * ACT_BYTES + ACT1_BYTES, &tmAct2, &mready[a].b, i * BK, lh2);
 #endif
       }
     }
@@ -605,6 +636,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       // ---------------------------------------------------------- MMA issuer (leader CTA, converged warp)
       constexpr uint32_t idesc_re = make_idesc_bf16(256, 64, DX, !DX);
       constexpr uint32_t idesc_main = make_idesc_bf16(256, 256, false, false);
+      constexpr uint32_t idesc_n2 = make_idesc_bf16(256, N2 ? N2 : 256, false, false);
       constexpr uint32_t idesc_sp = make_idesc_bf16(256, 256, false, false, true);
       // descriptor bases; a descriptor's start-address field is addr >> 4, so
       // byte offsets inside shared memory are added as (offset >> 4)
@@ -632,7 +664,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
               mma_bf16_pair(tmem + RE_COL + e * 64, ff_desc + kk * FF_KSTEP, sfd + kk * SF_KSTEP, idesc_re,
                             kk > 0 ? 1u : 0u);
 #endif
-            mma_commit_pair(&refull[(j & 1) * NE + e].b, 0x3);
+            mma_commit_pair(&refull[(j % NGRP) * NE + e].b, 0x3);
             mma_commit_pair(&e_empty[e].b, 0x3);
           }
           __syncwarp();
@@ -655,9 +687,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 #pragma unroll
               for (int kk = 0; kk < BK / 16; ++kk)
                 mma_bf16_pair(tmem, ad + kk * 2, bd + kk * 2, idesc_main, (jm > 0 || kk > 0) ? 1u : 0u);
+              if (N2) {  // tokens 256 .. 256 + N2 into the second accumulator
+                const uint64_t bd2 = bd + (ACT1_BYTES >> 4);
+#pragma unroll
+                for (int kk = 0; kk < BK / 16; ++kk)
+                  mma_bf16_pair(tmem + 256, ad + kk * 2, bd2 + kk * 2, idesc_n2, (jm > 0 || kk > 0) ? 1u : 0u);
+              }
             }
             mma_commit_pair(&a_empty[a].b, 0x3);
-            mma_commit_pair(&wempty[a].b, 0x3);
+            mma_commit_pair(&wempty[((jm + NA) % NGRP) * NA + a].b, 0x3);   // next writer's group
           }
           __syncwarp();
         }
@@ -685,8 +723,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
                        : 0x44444444u;
       // 1. rank-r product of this k-step (TMEM -> registers), then release the buffer
       const int rb = i % NE;
-      constexpr int RE_PERIOD = (NE % 2) ? 2 * NE : NE;   // steps between a group's uses of one buffer
-      mbar_wait(&refull[(i & 1) * NE + rb].b, (i / RE_PERIOD) & 1);
+      mbar_wait(&refull[(i % NGRP) * NE + rb].b, (i / RE_PERIOD) & 1);
       tc_fence_after();
       const uint32_t re_col = RE_COL + rb * 64 + h * 32;
       if (!DX) {
@@ -700,7 +737,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       // 2. W tile landed: all of this thread's W loads are issued before any
       //    result is needed, so their latency overlaps the TMEM load's
       const int wi = i % NW;
-      mbar_wait(&wfull[wi].b, (i / NW) & 1);
+      mbar_wait(&wfull[(i % NGRP) * NW + wi].b, (i / W_PERIOD) & 1);
       const uint32_t wt = smem_u32(wring + wi * W_BYTES);
       if (!DX) {
         // thread = W row t; chunks 4h .. 4h+3 of 8 k-values (SW128)
@@ -732,7 +769,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     auto finish = [&](const int i, uint32_t (&p)[32], uint32_t (&wv)[16], uint32_t mw) {
       const int wb = i % NA, wi = i % NW;
       // 3. destination buffer drained by the MMA of step i - NA
-      mbar_wait(&wempty[wb].b, ((i / NA) & 1) ^ 1);
+      // waits for the commit of main(i - NA), the previous user of this buffer
+      if (i >= NA) mbar_wait(&wempty[(i % NGRP) * NA + wb].b, ((i - NA) / A_PERIOD) & 1);
       const uint32_t dst = smem_u32(weff + wb * WEFF_BYTES);
 #ifdef LORS_EXP_EARLY_ARRIVE
       __syncwarp();
@@ -879,7 +917,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 #endif
       }
     };
-    for (int i = grp; i < nk; i += XW / 8) {
+    for (int i = grp; i < nk; i += NGRP) {
       uint32_t p[32], wv[16], mw = 0;
       issue(i, p, wv, mw);
       release(i);
@@ -888,13 +926,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     // ------------------------------------------------------------ epilogue
     mbar_wait(accf, 0);
     tc_fence_after();
-    // stage [256 tokens][128 features] bf16 (256 B rows) in the drained ring buffers
+    // stage [BNT tokens][128 features] bf16 (256 B rows) in the drained ring buffers
     uint8_t* stg = smem;
     float bv = 0.f;
     if (!DX && bias != nullptr && gm < Mout) bv = __bfloat162float(bias[gm]);
 #pragma unroll 1
-    for (int c0 = 0; c0 < 256 / (XW / 4); c0 += 32) {
-      const int col = (warp >> 2) * (256 / (XW / 4)) + c0;  // token offset inside the pair tile
+    for (int c0 = 0; c0 < BNT / (XW / 4); c0 += 32) {
+      const int col = (warp >> 2) * (BNT / (XW / 4)) + c0;  // token offset inside the pair tile
       uint32_t v[32];
       tmem_ld_x32(tmem + lane_addr + col, v);
       tmem_ld_wait();
@@ -906,7 +944,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     fence_proxy_async_smem();
     named_bar_sync(1, XFORM_THREADS);
     if (warp == 0 && lane == 0) {
-      tma_store_2d(&tmOut, stg, m0, l0);
+      for (int c = 0; c < BNT / 128; ++c) tma_store_2d(&tmOut, stg + c * 128 * 256, m0, l0 + 128 * c);
       tma_store_commit();
       tma_store_wait_all();
     }
@@ -933,9 +971,11 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
                             float alpha, cudaStream_t s) {
   using namespace rg;
   const int Mout = DX ? C : R, Kred = DX ? R : C;
-  CUtensorMap tAct, tW, tS, tF, tOut;
+  constexpr int N2 = n2<SP>(), BNT = bnt<SP>();
+  CUtensorMap tAct, tAct2, tW, tS, tF, tOut;
   int st;
-  if ((st = make_map(&tAct, act, Kred, L, 64, BN / 2, 128, "activation"))) return st;
+  if ((st = make_map(&tAct, act, Kred, L, 64, 128, 128, "activation"))) return st;
+  if ((st = make_map(&tAct2, act, Kred, L, 64, N2 ? N2 / 2 : 128, 128, "activation (second MMA)"))) return st;
   if (DX) st = make_map(&tW, w, C, R, 64, 64, 128, "W (dX)");
   else st = make_map(&tW, w, C, R, 64, 128, 128, "W (fwd)");
   if (st) return st;
@@ -946,13 +986,13 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
     if ((st = make_map(&tS, b, C, r, 32, RP, 64, "b (streamed half)"))) return st;
     if ((st = make_map(&tF, a, r, R, RP, 128, RP * 2, "a (fixed)"))) return st;
   }
-  if ((st = make_map(&tOut, out, Mout, L, 128, BN, 0, "output"))) return st;
+  if ((st = make_map(&tOut, out, Mout, L, 128, 128, 0, "output"))) return st;
   auto kern = bits ? tc_lors_gemm_kernel<DX, RP, true, SP> : tc_lors_gemm_kernel<DX, RP, false, SP>;
   const size_t smem = smem_bytes<RP, SP>();
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "lors_gemm smem attribute");
-  dim3 grid((unsigned)(2 * ceil_div(Mout, 2 * BM)), (unsigned)ceil_div(L, BN));
-  kern<<<grid, threads<SP>(), smem, s>>>(tAct, tW, tS, tF, tOut, bias, bits, SP ? meta24 : nullptr, (int)ceil_div(C, 32),
+  dim3 grid((unsigned)(2 * ceil_div(Mout, 2 * BM)), (unsigned)ceil_div(L, BNT));
+  kern<<<grid, threads<SP>(), smem, s>>>(tAct, tAct2, tW, tS, tF, tOut, bias, bits, SP ? meta24 : nullptr, (int)ceil_div(C, 32),
                                    Mout, Kred, alpha);
   LORS_CHECK_LAUNCH(DX ? "tc_lors_gemm<dx>" : "tc_lors_gemm<fwd>");
   return LORS_OK;
