@@ -364,8 +364,14 @@ constexpr int BM = 128, BN = 256, BK = 64;
 // fast) sparse MMA steps; the dense kernels measured faster with one group.
 // Then the roles: factor-ring producer, MMA issuer / relay, activation
 // producer, activation relay, W-ring producer.
+#ifndef LORS_XW_DENSE
+#define LORS_XW_DENSE 8
+#endif
+#ifndef LORS_N2
+#define LORS_N2 128
+#endif
 template <bool SP>
-constexpr int xw() { return 16; }
+constexpr int xw() { return SP ? 16 : LORS_XW_DENSE; }
 template <bool SP>
 constexpr int threads() { return 32 * (xw<SP>() + 5); }
 // Token tile of a CTA pair.  The dense kernels take 256 + N2 tokens per W_eff
@@ -375,7 +381,7 @@ constexpr int threads() { return 32 * (xw<SP>() + 5); }
 // recompute buffers of 64.  The 2:4 kernel keeps 256 tokens: its TMEM holds
 // the sparse metadata next to three recompute buffers.
 template <bool SP>
-constexpr int n2() { return SP ? 0 : 128; }
+constexpr int n2() { return SP ? 0 : LORS_N2; }
 template <bool SP>
 constexpr int bnt() { return 256 + n2<SP>(); }            // tokens per pair tile
 // factor ring (streamed adapter-factor half) = TMEM recompute buffers.  The W
