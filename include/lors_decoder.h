@@ -1,0 +1,27 @@
+/* Decoder-side helpers of the B200 LoRS library (not the drop-in boundary of
+ * the LoRS path -- that is lors_b200.h).  They serve the LLaMA-shaped decoder
+ * that benchmarks the path at BASELINE configs 3-5.  Same status
+ * codes and error string (lors_last_error) as lors_b200.h.
+ */
+#ifndef LORS_DECODER_H_
+#define LORS_DECODER_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Rotary position embedding (rotate-half convention), bf16, fused with the
+ * head transpose that attention wants:
+ *   layout 0:  x [B, S, H, hd] -> y [B, H, S, hd]   (forward: projection output -> attention input)
+ *   layout 1:  x [B, H, S, hd] -> y [B, S, H, hd]   (backward: attention grad -> projection grad)
+ * y = x * cos + rotate_half(x) * (inverse ? -sin : sin), cos / sin [S, hd] (bf16), computed in fp32 and
+ * rounded once.  hd must be a multiple of 8 (16-byte accesses). */
+int lors_rope(const void* x, void* y, const void* cos_t, const void* sin_t, int64_t B, int64_t S, int64_t H,
+              int64_t hd, int32_t layout, int32_t inverse, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -33,6 +33,8 @@ EXPORTED_SYMBOLS = (
     "lors_last_error", "lors_abi_version", "lors_device_check",
     "lors_launch_count", "lors_reset_launch_count",
 )
+# include/lors_decoder.h: decoder-side helpers (not the LoRS drop-in boundary)
+DECODER_SYMBOLS = ("lors_rope",)
 
 _vp = ct.c_void_p
 
@@ -96,6 +98,9 @@ def load(path: str = LIB_PATH) -> ct.CDLL:
         lib.lors_last_error.restype = ct.c_char_p
         lib.lors_abi_version.restype = ct.c_int
         lib.lors_device_check.restype = ct.c_int
+        lib.lors_rope.argtypes = [_vp, _vp, _vp, _vp, ct.c_int64, ct.c_int64, ct.c_int64, ct.c_int64, ct.c_int32,
+                                  ct.c_int32, _vp]
+        lib.lors_rope.restype = ct.c_int
         lib.lors_launch_count.restype = ct.c_uint64
         lib.lors_reset_launch_count.restype = None
         _lib = lib

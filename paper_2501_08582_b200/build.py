@@ -19,7 +19,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_native")
 LIB = os.path.join(OUT_DIR, "liblors_b200.so")
-SOURCES = ["lors_capi.cu", "lors_simt.cu", "lors_tc.cu"]
+SOURCES = ["lors_capi.cu", "lors_simt.cu", "lors_tc.cu", "lors_decoder.cu"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [
@@ -45,6 +45,7 @@ def _stale(target: str, deps: list[str]) -> bool:
 def _headers() -> list[str]:
     hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     hs.append(os.path.join(ROOT, "include", "lors_b200.h"))
+    hs.append(os.path.join(ROOT, "include", "lors_decoder.h"))
     return hs
 
 

@@ -1,0 +1,94 @@
+// Decoder-side helpers (include/lors_decoder.h): fused RoPE + head transpose.
+// Memory-bound elementwise work: one thread per 8 consecutive elements of a
+// head's first half (16-byte loads and stores of both halves), so a warp reads
+// and writes 512 contiguous bytes.
+#include "../../include/lors_decoder.h"
+#include "lors_common.cuh"
+
+namespace lors {
+
+__device__ __forceinline__ void unpack8(const uint4 v, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 v;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return v;
+}
+
+template <int LAYOUT>
+__global__ void rope_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                            const __nv_bfloat16* __restrict__ cs, const __nv_bfloat16* __restrict__ sn, int64_t B,
+                            int64_t S, int64_t H, int hd, float sgn) {
+  const int half = hd / 2, per_head = half / 8;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = B * S * H * per_head;
+  if (idx >= total) return;
+  const int c = (int)(idx % per_head) * 8;
+  int64_t rest = idx / per_head;
+  // LAYOUT 0 walks the input [B, S, H] order, LAYOUT 1 the input [B, H, S] order
+  int64_t b, s, h;
+  if (LAYOUT == 0) {
+    h = rest % H; rest /= H; s = rest % S; b = rest / S;
+  } else {
+    s = rest % S; rest /= S; h = rest % H; b = rest / H;
+  }
+  const int64_t bsh = ((b * S + s) * H + h) * hd;   // [B, S, H, hd]
+  const int64_t bhs = ((b * H + h) * S + s) * hd;   // [B, H, S, hd]
+  const int64_t in = LAYOUT == 0 ? bsh : bhs, out = LAYOUT == 0 ? bhs : bsh;
+  float x1[8], x2[8], c1[8], c2[8], s1[8], s2[8], o1[8], o2[8];
+  unpack8(*reinterpret_cast<const uint4*>(x + in + c), x1);
+  unpack8(*reinterpret_cast<const uint4*>(x + in + half + c), x2);
+  unpack8(__ldg(reinterpret_cast<const uint4*>(cs + s * hd + c)), c1);
+  unpack8(__ldg(reinterpret_cast<const uint4*>(cs + s * hd + half + c)), c2);
+  unpack8(__ldg(reinterpret_cast<const uint4*>(sn + s * hd + c)), s1);
+  unpack8(__ldg(reinterpret_cast<const uint4*>(sn + s * hd + half + c)), s2);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    // rotate_half(x) = (-x2, x1)
+    o1[i] = fmaf(x1[i], c1[i], -sgn * x2[i] * s1[i]);
+    o2[i] = fmaf(x2[i], c2[i], sgn * x1[i] * s2[i]);
+  }
+  *reinterpret_cast<uint4*>(y + out + c) = pack8(o1);
+  *reinterpret_cast<uint4*>(y + out + half + c) = pack8(o2);
+}
+
+}  // namespace lors
+
+extern "C" int lors_rope(const void* x, void* y, const void* cos_t, const void* sin_t, int64_t B, int64_t S,
+                         int64_t H, int64_t hd, int32_t layout, int32_t inverse, void* stream) {
+  using namespace lors;
+  if (!x || !y || !cos_t || !sin_t) {
+    set_error("lors_rope: null pointer");
+    return LORS_ERR_ARGUMENT;
+  }
+  if (B < 0 || S < 0 || H < 0 || hd <= 0 || hd % 16 != 0) {
+    set_error("lors_rope: head dim must be a positive multiple of 16 (two 8-element halves)");
+    return LORS_ERR_SHAPE;
+  }
+  if (layout != 0 && layout != 1) {
+    set_error("lors_rope: layout must be 0 ([B,S,H,hd] -> [B,H,S,hd]) or 1 (the reverse)");
+    return LORS_ERR_ARGUMENT;
+  }
+  const int64_t total = B * S * H * (hd / 16);
+  if (total == 0) return LORS_OK;
+  const cudaStream_t s = (cudaStream_t)stream;
+  const unsigned grid = (unsigned)ceil_div(total, 256);
+  const float sgn = inverse ? -1.0f : 1.0f;
+  auto xp = (const __nv_bfloat16*)x;
+  auto yp = (__nv_bfloat16*)y;
+  auto cp = (const __nv_bfloat16*)cos_t;
+  auto sp = (const __nv_bfloat16*)sin_t;
+  if (layout == 0) rope_kernel<0><<<grid, 256, 0, s>>>(xp, yp, cp, sp, B, S, H, (int)hd, sgn);
+  else rope_kernel<1><<<grid, 256, 0, s>>>(xp, yp, cp, sp, B, S, H, (int)hd, sgn);
+  LORS_CHECK_LAUNCH("rope");
+  return LORS_OK;
+}

@@ -25,6 +25,7 @@ import torch
 import torch.nn.functional as F
 from torch import nn
 
+from . import ops
 from .errors import ArgumentError
 from .module import LoRSLinear
 from .prune import prune_rowwise, prune_two_four
@@ -156,6 +157,30 @@ def apply_rope(x, cos, sin):
     return x * cos + _rotate_half(x) * sin
 
 
+class RopeFunction(torch.autograd.Function):
+    """Fused RoPE + head transpose on the GPU (ops.rope, one kernel each way):
+    x [B, S, H, hd] (the projection output viewed per head) -> [B, H, S, hd]."""
+
+    @staticmethod
+    def forward(ctx, x, cos, sin):
+        ctx.save_for_backward(cos, sin)
+        return ops.rope(x, cos, sin, layout=0)
+
+    @staticmethod
+    def backward(ctx, gy):
+        cos, sin = ctx.saved_tensors
+        return ops.rope(gy, cos, sin, layout=1, inverse=True), None, None
+
+
+def rope_heads(x_bshd, cos, sin):
+    """[B, S, H, hd] -> RoPE'd [B, H, S, hd].  CUDA bf16: the native fused kernel
+    (fails loudly without the library); elsewhere (CPU reference decoders in the
+    tests): the plain torch formula."""
+    if x_bshd.is_cuda and x_bshd.dtype == torch.bfloat16 and x_bshd.shape[-1] % 16 == 0:
+        return RopeFunction.apply(x_bshd, cos, sin)
+    return apply_rope(x_bshd.transpose(1, 2), cos, sin)
+
+
 class DecoderLayer(nn.Module):
     def __init__(self, cfg: DecoderConfig, linears: Dict[str, nn.Module], device):
         super().__init__()
@@ -168,10 +193,9 @@ class DecoderLayer(nn.Module):
         cfg, p = self.cfg, self.proj
         B, S, _ = h.shape
         x = self.attn_norm(h)
-        q = p["q"](x).view(B, S, cfg.n_heads, cfg.head_dim).transpose(1, 2)
-        k = p["k"](x).view(B, S, cfg.n_kv_heads, cfg.head_dim).transpose(1, 2)
+        q = rope_heads(p["q"](x).view(B, S, cfg.n_heads, cfg.head_dim), cos, sin)
+        k = rope_heads(p["k"](x).view(B, S, cfg.n_kv_heads, cfg.head_dim), cos, sin)
         v = p["v"](x).view(B, S, cfg.n_kv_heads, cfg.head_dim).transpose(1, 2)
-        q, k = apply_rope(q, cos, sin), apply_rope(k, cos, sin)
         att = F.scaled_dot_product_attention(q, k, v, is_causal=True,
                                              enable_gqa=cfg.n_kv_heads != cfg.n_heads)
         h = h + p["o"](att.transpose(1, 2).reshape(B, S, cfg.dim))

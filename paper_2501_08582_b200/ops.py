@@ -192,3 +192,25 @@ def grad_outer(dy_t: torch.Tensor, x_t: torch.Tensor, w: Optional[torch.Tensor] 
     N.check(N.load().lors_grad_outer(L, R, C, dtype_code(dy_t.dtype), int(masked), _p(dy_t), _p(x_t),
                                      _p(w), _p(dw), _stream()))
     return dw
+
+
+def rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor, layout: int = 0, inverse: bool = False):
+    """Fused RoPE (rotate-half) + head transpose, bf16 (include/lors_decoder.h).
+    layout 0: x [B, S, H, hd] -> [B, H, S, hd]; layout 1: x [B, H, S, hd] -> [B, S, H, hd].
+    inverse=True rotates by -theta (the backward)."""
+    if x.dtype != torch.bfloat16 or cos.dtype != torch.bfloat16 or sin.dtype != torch.bfloat16:
+        raise ArgumentError("rope: bf16 tensors expected")
+    if x.dim() != 4:
+        raise ShapeError(f"rope: x must be 4-D, got {tuple(x.shape)}")
+    x = x.contiguous()
+    if layout == 0:
+        B, S, H, hd = x.shape
+        y = torch.empty((B, H, S, hd), dtype=x.dtype, device=x.device)
+    else:
+        B, H, S, hd = x.shape
+        y = torch.empty((B, S, H, hd), dtype=x.dtype, device=x.device)
+    if cos.shape[0] < S or cos.shape[1] != hd or sin.shape != cos.shape:
+        raise ShapeError(f"rope: tables {tuple(cos.shape)} do not cover [S={S}, hd={hd}]")
+    cos, sin = cos.contiguous(), sin.contiguous()
+    N.check(N.load().lors_rope(_p(x), _p(y), _p(cos), _p(sin), B, S, H, hd, layout, int(inverse), _stream()))
+    return y

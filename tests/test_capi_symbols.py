@@ -13,6 +13,7 @@ from paper_2501_08582_b200 import _native as N
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "lors_b200.h")
+HEADERS = [os.path.join(ROOT, "include", h) for h in sorted(os.listdir(os.path.join(ROOT, "include"))) if h.endswith(".h")]
 
 
 @pytest.fixture(scope="module")
@@ -23,14 +24,18 @@ def lib():
     return N.load()
 
 
-def _declared_functions():
-    src = open(HEADER).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(lors_[a-z_0-9]+)\s*\(", src, flags=re.M)))
+def _declared_functions(headers=None):
+    names = set()
+    for h in headers or HEADERS:
+        src = open(h).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names |= set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(lors_[a-z_0-9]+)\s*\(", src, flags=re.M))
+    return sorted(names)
 
 
 def test_header_declares_expected_symbols():
-    assert _declared_functions() == sorted(N.EXPORTED_SYMBOLS)
+    assert _declared_functions([HEADER]) == sorted(N.EXPORTED_SYMBOLS)
+    assert _declared_functions() == sorted(N.EXPORTED_SYMBOLS + N.DECODER_SYMBOLS)
 
 
 def test_library_exports_every_declared_symbol(lib):

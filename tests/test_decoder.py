@@ -219,3 +219,23 @@ def test_decoder_loss_curve_vs_float64_oracle(dtype, tol):
     print(f"{dtype}: decoder loss {l2[0]:.4f} -> {l2[-1]:.4f}; max rel deviation {rel.max():.2e}")
     assert l2[-1] < l2[0] - 1.0
     assert rel.max() <= tol
+
+
+@pytest.mark.gpu
+def test_fused_rope_matches_torch_formula():
+    """ops.rope / RopeFunction (fused RoPE + head transpose) against the torch
+    rotate-half formula in fp32, forward and backward, GQA head counts."""
+    cfg = dec.preset("tiny", dtype=torch.bfloat16, seq=64)
+    cos, sin = dec.rope_tables(cfg, "cuda")
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for H in (4, 2):
+        x = torch.randn(2, 64, H, cfg.head_dim, device="cuda", generator=g).bfloat16().requires_grad_(True)
+        gy = torch.randn(2, H, 64, cfg.head_dim, device="cuda", generator=g).bfloat16()
+        y = dec.rope_heads(x, cos, sin)
+        y.backward(gy)
+        xr = x.detach().float().requires_grad_(True)
+        yr = dec.apply_rope(xr.transpose(1, 2), cos.float(), sin.float())
+        yr.backward(gy.float())
+        assert y.shape == (2, H, 64, cfg.head_dim) and y.is_contiguous()
+        assert float((y.float() - yr).norm() / yr.norm()) < 5e-3
+        assert float((x.grad.float() - xr.grad).norm() / xr.grad.norm()) < 5e-3

@@ -6,7 +6,7 @@ cd "$(dirname "$0")/.."
 OUT=paper_2501_08582_b200/_native/exp/$1
 mkdir -p "$OUT"
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC,-O3 -Iinclude $2"
-for s in lors_capi lors_simt lors_tc; do
+for s in lors_capi lors_simt lors_tc lors_decoder; do
   nvcc $F -c paper_2501_08582_b200/csrc/$s.cu -o $OUT/$s.o &
 done
 wait
