@@ -24,13 +24,13 @@
 
 #ifdef LORS_EXP_CLOCK
 // timing experiment: per-CTA (clock64, globaltimer) at start and end of the LoRS GEMM
-__device__ unsigned long long g_lors_clk[4096 * 4];
+__device__ unsigned long long g_lors_clk[4096 * 8];
 __device__ unsigned int g_lors_clk_n;
 extern "C" int lors_exp_clock_read(unsigned long long* out, unsigned int* n) {
   cudaMemcpyFromSymbol(n, g_lors_clk_n, sizeof(unsigned int));
   unsigned int z = 0;
   cudaMemcpyToSymbol(g_lors_clk_n, &z, sizeof(unsigned int));
-  return (int)cudaMemcpyFromSymbol(out, g_lors_clk, sizeof(unsigned long long) * 4096 * 4);
+  return (int)cudaMemcpyFromSymbol(out, g_lors_clk, sizeof(unsigned long long) * 4096 * 8);
 }
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -493,6 +493,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   const bool leader = rank == 0;
 #ifdef LORS_EXP_CLOCK
   const unsigned long long clk0 = clock64(), gt0 = gtimer();
+  __shared__ unsigned long long t_ev[4];  // first main MMA issued, accumulator done, staged, stored
 #endif
   // grouped raster over (token tile, feature pair): GROUP_T token tiles x all
   // feature pairs per group, token tile fastest, so the ~74 clusters of a wave
@@ -676,6 +677,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           __syncwarp();
         }
         const int jm = j - D;
+#ifdef LORS_EXP_CLOCK
+        if (jm == 0 && lane == 0) t_ev[0] = gtimer();
+#endif
         if (jm >= 0) {  // main MMA for step jm
           const int a = jm % NA;
           mbar_wait(&mready[a].b, (jm / NA) & 1);
@@ -932,27 +936,77 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     // ------------------------------------------------------------ epilogue
     mbar_wait(accf, 0);
     tc_fence_after();
-    // stage [BNT tokens][128 features] bf16 (256 B rows) in the drained ring buffers
+#ifdef LORS_EXP_CLOCK
+    if (warp == 0 && lane == 0) t_ev[1] = gtimer();
+#endif
+    // Per 128-token chunk: the accumulator is read in the MMA fragment layout
+    // (tcgen05.ld.16x256b: a thread holds two adjacent tokens of a feature),
+    // rounded to bf16 pairs and written transposed by stmatrix.trans into
+    // [token][64 features] SW128 blocks (one 16 KB block per chunk and feature
+    // half, bank-conflict free); the chunk's two TMA stores are issued while the
+    // next chunk is staged.  Warp (q, hh): features 32q .. 32q+31, tokens hh*64 ..
+    // of each chunk (XW / 4 token slices of 128 / (XW / 4)).
     uint8_t* stg = smem;
-    float bv = 0.f;
-    if (!DX && bias != nullptr && gm < Mout) bv = __bfloat162float(bias[gm]);
-#pragma unroll 1
-    for (int c0 = 0; c0 < BNT / (XW / 4); c0 += 32) {
-      const int col = (warp >> 2) * (BNT / (XW / 4)) + c0;  // token offset inside the pair tile
-      uint32_t v[32];
-      tmem_ld_x32(tmem + lane_addr + col, v);
-      tmem_ld_wait();
+    constexpr int TSL = 128 / (XW / 4);              // tokens of a chunk per warp (64 or 32)
+    const int hh = warp >> 2;
+    float bvals[2][2];                               // bias of features (16 g + l/4) and (+8)
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        *reinterpret_cast<bf16*>(stg + (col + j) * 256 + t * 2) = __float2bfloat16_rn(__uint_as_float(v[j]) + bv);
+    for (int g16 = 0; g16 < 2; ++g16)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int f = m0 + q * 32 + 16 * g16 + 8 * e + (lane >> 2);
+        bvals[g16][e] = (!DX && bias != nullptr && f < Mout) ? __bfloat162float(bias[f]) : 0.f;
+      }
+#pragma unroll 1
+    for (int c = 0; c < BNT / 128; ++c) {
+#pragma unroll 1
+      for (int tb = 0; tb < TSL; tb += 32) {
+        const int tok = hh * TSL + tb;                // token offset inside the chunk
+        uint32_t v[2][16];
+#pragma unroll
+        for (int g16 = 0; g16 < 2; ++g16)
+          tmem_ld_16x256b_x4(tmem + ((uint32_t)(q * 32 + 16 * g16) << 16) + (uint32_t)(c * 128 + tok), v[g16]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int g16 = 0; g16 < 2; ++g16) {
+          // features F = 32q + 16 g16 (+8 for the second row block); 64-feature half of the staging
+          const int F = q * 32 + 16 * g16, fh = F >> 6;
+          uint8_t* blk = stg + (size_t)((c * 2 + fh) * 16384);
+#pragma unroll
+          for (int bp = 0; bp < 2; ++bp) {           // token blocks 2bp, 2bp+1 (8 tokens each)
+            uint32_t m[4];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int bb = 2 * bp + u;
+              m[2 * u] = pack_bf16x2(__uint_as_float(v[g16][4 * bb]) + bvals[g16][0],
+                                     __uint_as_float(v[g16][4 * bb + 1]) + bvals[g16][0]);
+              m[2 * u + 1] = pack_bf16x2(__uint_as_float(v[g16][4 * bb + 2]) + bvals[g16][1],
+                                         __uint_as_float(v[g16][4 * bb + 3]) + bvals[g16][1]);
+            }
+            // matrix mi = lane / 8: token block 2bp + (mi >> 1), feature block F + 8 (mi & 1);
+            // this lane addresses stored row (token) lane % 8 of it
+            const int mi = lane >> 3, tr = tok + 8 * (2 * bp + (mi >> 1)) + (lane & 7);
+            const int fu = ((F & 63) >> 3) + (mi & 1);   // 16-byte unit of the 128-byte row
+            stsm_x4_trans(smem_u32(blk + tr * 128 + ((fu ^ (tr & 7)) << 4)), m[0], m[1], m[2], m[3]);
+          }
+        }
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, XFORM_THREADS);
+      if (warp == 0 && lane == 0) {
+#ifdef LORS_EXP_CLOCK
+        if (c == 0) t_ev[2] = gtimer();
+#endif
+        tma_store_2d(&tmOut, stg + (c * 2) * 16384, m0, l0 + 128 * c);
+        tma_store_2d(&tmOut, stg + (c * 2 + 1) * 16384, m0 + 64, l0 + 128 * c);
+        tma_store_commit();
       }
     }
-    fence_proxy_async_smem();
-    named_bar_sync(1, XFORM_THREADS);
     if (warp == 0 && lane == 0) {
-      for (int c = 0; c < BNT / 128; ++c) tma_store_2d(&tmOut, stg + c * 128 * 256, m0, l0 + 128 * c);
-      tma_store_commit();
       tma_store_wait_all();
+#ifdef LORS_EXP_CLOCK
+      t_ev[3] = gtimer();
+#endif
     }
   }
   tc_fence_before();
@@ -962,10 +1016,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   if (threadIdx.x == 0) {
     const unsigned int slot = atomicAdd(&g_lors_clk_n, 1u);
     if (slot < 4096) {
-      g_lors_clk[slot * 4 + 0] = clk0;
-      g_lors_clk[slot * 4 + 1] = clock64();
-      g_lors_clk[slot * 4 + 2] = gt0;
-      g_lors_clk[slot * 4 + 3] = gtimer();
+      g_lors_clk[slot * 8 + 0] = clk0;
+      g_lors_clk[slot * 8 + 1] = clock64();
+      g_lors_clk[slot * 8 + 2] = gt0;
+      g_lors_clk[slot * 8 + 3] = gtimer();
+      for (int e = 0; e < 4; ++e) g_lors_clk[slot * 8 + 4 + e] = leader || e > 0 ? t_ev[e] : 0ull;
     }
   }
 #endif
@@ -992,7 +1047,7 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
     if ((st = make_map(&tS, b, C, r, 32, RP, 64, "b (streamed half)"))) return st;
     if ((st = make_map(&tF, a, r, R, RP, 128, RP * 2, "a (fixed)"))) return st;
   }
-  if ((st = make_map(&tOut, out, Mout, L, 128, 128, 0, "output"))) return st;
+  if ((st = make_map(&tOut, out, Mout, L, 64, 128, 128, "output"))) return st;  // [128 tokens][64 features] SW128
   auto kern = bits ? tc_lors_gemm_kernel<DX, RP, true, SP> : tc_lors_gemm_kernel<DX, RP, false, SP>;
   const size_t smem = smem_bytes<RP, SP>();
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),

@@ -387,6 +387,13 @@ __device__ __forceinline__ void ldsm_x4_trans(uint32_t saddr, uint32_t (&v)[4]) 
 __device__ __forceinline__ void lds128(uint32_t saddr, uint32_t (&v)[4]) {
   asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(saddr));
 }
+// four 8x8 bf16 matrices, each thread's register = (row lane/4, cols 2(lane%4), +1) of its
+// matrix, stored transposed; lanes 8i .. 8i+7 give the row addresses of matrix i
+__device__ __forceinline__ void stsm_x4_trans(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(a), "r"(b),
+               "r"(c), "r"(d)
+               : "memory");
+}
 __device__ __forceinline__ void sts32(uint32_t saddr, uint32_t v) {
   asm volatile("st.shared.b32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
 }
