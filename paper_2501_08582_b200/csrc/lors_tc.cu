@@ -516,43 +516,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   const int lh = l0 + rank * 128, lh2 = l0 + 256 + rank * (N2 / 2);
   const int nk = (Kred + BK - 1) / BK;
 
-  if (warp == W_SF && lane == 0) {
+  if (warp == W_SF) {
+    // lane-parallel barrier initialisation over the flat Bar16 array (layout above):
+    // rready / mready count the merged arrivals in the leader, wfree the 8
+    // transform warps, everything else one arrival
+    constexpr int NBARS = 4 * NE + 4 * NA + 3 + 3 * NW;
     const uint32_t merged = leader ? 18u : 1u;
-    for (int i = 0; i < NE; ++i) {
-      mbar_init(&rready[i].b, merged);
-      mbar_init(&e_empty[i].b, 1);
-      mbar_init(&refull[i].b, 1);
-      mbar_init(&refull[NE + i].b, 1);
+    for (int k = lane; k < NBARS; k += 32) {
+      uint32_t cnt = 1;
+      if (k < NE || (k >= 2 * NE && k < 2 * NE + NA)) cnt = merged;
+      if (k >= NBARS - NW) cnt = 8;
+      mbar_init(&bars[k].b, cnt);
     }
-    for (int i = 0; i < NA; ++i) {
-      mbar_init(&mready[i].b, merged);
-      mbar_init(&a_empty[i].b, 1);
-      mbar_init(&wempty[i].b, 1);
-      mbar_init(&wempty[NA + i].b, 1);
-    }
-    for (int i = 0; i < NW; ++i) {
-      mbar_init(&wfull[i].b, 1);
-      mbar_init(&wfull[NW + i].b, 1);
-      mbar_init(&wfree[i].b, 8);
-    }
-    mbar_init(ffull, 1);
-    mbar_init(pffull, 1);
-    mbar_init(accf, 1);
     fence_barrier_init();
+    __syncwarp();
     // first use of every recompute buffer: nobody has read it yet
-    if (leader)
-      for (int i = 0; i < NE; ++i) mbar_arrive_count(&rready[i].b, 16);
-    tma_prefetch_desc(&tmAct);
-    if (N2) tma_prefetch_desc(&tmAct2);
-    tma_prefetch_desc(&tmW);
-    tma_prefetch_desc(&tmS);
-    tma_prefetch_desc(&tmF);
-    tma_prefetch_desc(&tmOut);
+    if (leader && lane < NE) mbar_arrive_count(&rready[lane].b, 16);
+    if (lane == 0) {
+      tma_prefetch_desc(&tmAct);
+      if (N2) tma_prefetch_desc(&tmAct2);
+      tma_prefetch_desc(&tmW);
+      tma_prefetch_desc(&tmS);
+      tma_prefetch_desc(&tmF);
+      tma_prefetch_desc(&tmOut);
+    }
   }
   if (warp == W_MMA) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
   tc_fence_before();
-  cluster_sync();
+  // Local barrier only: the producers start their TMA loads (which complete on
+  // this CTA's own barriers) at once; every role that touches the peer CTA
+  // (remote arrives, pair MMAs, multicast commits) waits on the cluster
+  // barrier first, so the peer's barrier initialisation overlaps the loads.
+  __syncthreads();
   tc_fence_after();
+  cluster_arrive();
+#ifdef LORS_EXP_CLOCK_PRO
+  if (threadIdx.x == 0) t_ev[0] = gtimer();
+#endif
   const uint32_t tmem = *tmem_slot;
   // Every TMA completes on a barrier of the CTA that issued it; the peer
   // relays its landings to the leader, and the transform warps of both CTAs
@@ -562,7 +562,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   const uint32_t pffull_l = mapa_shared(smem_u32(pffull), 0);
 
   if (warp == W_SF) {
-    // ------------------------------------------------------------ early-ring producer (both CTAs)
+    // ------------------------------------------------------------ factor-ring producer (both CTAs)
     if (lane == 0) {
       mbar_arrive_expect_tx(ffull, FF);
       if (DX) {  // b [r, C] as MN-major A of the recompute: two 64-wide atoms of this CTA's columns
@@ -581,6 +581,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         else tma_load_2d(st, &tmS, &rready[e].b, k0 + 32 * rank, 0);      // b cols, MN-major
       }
     }
+    cluster_wait();
   } else if (warp == W_WLOAD) {
     // ------------------------------------------------------------ W-ring producer (both CTAs)
     if (lane == 0) {
@@ -603,6 +604,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 #endif
       }
     }
+    cluster_wait();
   } else if (warp == W_ACT) {
     // ------------------------------------------------------------ activation-ring producer (both CTAs)
     if (lane == 0) {
@@ -618,7 +620,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 #endif
       }
     }
+    cluster_wait();
   } else if (warp == W_RELAY) {
+    cluster_wait();
     // ------------------------------------------------------------ activation relay (peer CTA)
     if (!leader && lane == 0) {
       for (int i = 0; i < nk; ++i) {
@@ -628,6 +632,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       }
     }
   } else if (warp == W_MMA) {
+    cluster_wait();
     if (!leader) {
       // ---------------------------------------------------------- early relay (peer CTA)
       if (lane == 0) {
@@ -677,8 +682,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           __syncwarp();
         }
         const int jm = j - D;
-#ifdef LORS_EXP_CLOCK
+#if defined(LORS_EXP_CLOCK) && !defined(LORS_EXP_CLOCK_PRO)
         if (jm == 0 && lane == 0) t_ev[0] = gtimer();
+#endif
+#ifdef LORS_EXP_CLOCK_PRO
+        if (jm == 0 && lane == 0) t_ev[3] = gtimer();
+        if (j == 0 && lane == 0) t_ev[1] = gtimer();
 #endif
         if (jm >= 0) {  // main MMA for step jm
           const int a = jm % NA;
@@ -715,6 +724,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     }
   } else {
     // ------------------------------------------------------------ transform warps 0..7
+    cluster_wait();
     const int q = warp & 3;        // TMEM lane quarter
     const int h = (warp >> 2) & 1; // column half of the 64-wide k-step
     const int grp = warp >> 3;     // group: k-step parity this warp transforms (SP), else 0
@@ -920,6 +930,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       fence_proxy_async_smem();
 #endif
       __syncwarp();
+#ifdef LORS_EXP_CLOCK_PRO
+      if (i == 0 && warp == 0 && lane == 0) t_ev[2] = gtimer();
+#endif
       if (lane == 0) {
         mbar_arrive(&wfree[wi].b);                   // done reading the W tile
 #ifndef LORS_EXP_EARLY_ARRIVE
@@ -936,7 +949,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     // ------------------------------------------------------------ epilogue
     mbar_wait(accf, 0);
     tc_fence_after();
-#ifdef LORS_EXP_CLOCK
+#if defined(LORS_EXP_CLOCK) && !defined(LORS_EXP_CLOCK_PRO)
     if (warp == 0 && lane == 0) t_ev[1] = gtimer();
 #endif
     // Per 128-token chunk: the accumulator is read in the MMA fragment layout
@@ -994,7 +1007,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       fence_proxy_async_smem();
       named_bar_sync(1, XFORM_THREADS);
       if (warp == 0 && lane == 0) {
-#ifdef LORS_EXP_CLOCK
+#if defined(LORS_EXP_CLOCK) && !defined(LORS_EXP_CLOCK_PRO)
         if (c == 0) t_ev[2] = gtimer();
 #endif
         tma_store_2d(&tmOut, stg + (c * 2) * 16384, m0, l0 + 128 * c);
@@ -1004,7 +1017,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     }
     if (warp == 0 && lane == 0) {
       tma_store_wait_all();
-#ifdef LORS_EXP_CLOCK
+#if defined(LORS_EXP_CLOCK) && !defined(LORS_EXP_CLOCK_PRO)
       t_ev[3] = gtimer();
 #endif
     }
@@ -1020,7 +1033,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       g_lors_clk[slot * 8 + 1] = clock64();
       g_lors_clk[slot * 8 + 2] = gt0;
       g_lors_clk[slot * 8 + 3] = gtimer();
+#ifdef LORS_EXP_CLOCK_PRO
+      for (int e = 0; e < 4; ++e) g_lors_clk[slot * 8 + 4 + e] = leader ? t_ev[e] : 0ull;
+#else
       for (int e = 0; e < 4; ++e) g_lors_clk[slot * 8 + 4 + e] = leader || e > 0 ? t_ev[e] : 0ull;
+#endif
     }
   }
 #endif
