@@ -342,29 +342,35 @@ def run_native(args, cfg):
     hdb = torch.empty(r, C, dtype=torch.float32).pin_memory()
 
     copy_stream = torch.cuda.Stream(device=dev)
-    staged = {}
+    # two preallocated device batches: step k computes on slot k % 2 while the
+    # copy stream fills slot (k + 1) % 2 (a training loop's data prefetch)
+    slots = [(torch.empty_like(x), torch.empty_like(dy)) for _ in range(2)]
+    filled = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
+    for ev_ in consumed:
+        ev_.record(stream)
+    state = {"k": 0}
 
-    def prefetch():
-        # H2D of the next step's batch on a side stream (as a training loop's
-        # data prefetch would); the consumer waits on its event
+    def prefetch(k):
+        xs, dys = slots[k % 2]
         with torch.cuda.stream(copy_stream):
-            xd = hx.to(dev, non_blocking=True)
-            dyd = hdy.to(dev, non_blocking=True)
-            evt = torch.cuda.Event()
-            evt.record(copy_stream)
-        staged["next"] = (xd, dyd, evt)
+            copy_stream.wait_event(consumed[k % 2])
+            xs.copy_(hx, non_blocking=True)
+            dys.copy_(hdy, non_blocking=True)
+            filled[k % 2].record(copy_stream)
 
     def e2e_step():
-        xd, dyd, evt = staged.pop("next")
-        stream.wait_event(evt)
-        xd.record_stream(stream)
-        dyd.record_stream(stream)
-        prefetch()
-        xd.requires_grad_(True)
+        k = state["k"]
+        state["k"] = k + 1
+        xs, dys = slots[k % 2]
+        stream.wait_event(filled[k % 2])
+        prefetch(k + 1)
+        xd = xs.detach().requires_grad_(True)
         layer.a.grad = None
         layer.b.grad = None
         y = layer(xd)
-        y.backward(dyd)
+        y.backward(dys)
+        consumed[k % 2].record(stream)
         if world > 1:
             grad_bucket[: R * r].copy_(layer.a.grad.view(-1))
             grad_bucket[R * r:].copy_(layer.b.grad.view(-1))
@@ -372,7 +378,7 @@ def run_native(args, cfg):
         hda.copy_(layer.a.grad, non_blocking=True)
         hdb.copy_(layer.b.grad, non_blocking=True)
 
-    prefetch()
+    prefetch(0)
     for _ in range(2):
         e2e_step()
     torch.cuda.synchronize()
@@ -387,7 +393,6 @@ def run_native(args, cfg):
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    staged.clear()
     peak_gb = torch.cuda.max_memory_allocated(dev) / 1e9
     if world > 1:
         tt = torch.tensor([e2e_ms, peak_gb], device=dev)
