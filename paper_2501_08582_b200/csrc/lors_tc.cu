@@ -16,6 +16,8 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "lors_simt.cuh"
@@ -1070,6 +1072,17 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "lors_gemm smem attribute");
   dim3 grid((unsigned)(2 * ceil_div(Mout, 2 * BM)), (unsigned)ceil_div(L, BNT));
+  if (getenv("LORS_VERBOSE")) {  // diagnostics: how many clusters of this kernel fit on the GPU at once
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(threads<SP>());
+    cfg.dynamicSmemBytes = smem_bytes<RP, SP>();
+    int v = -1;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&v, (void*)kern, &cfg);
+    fprintf(stderr, "[lors] tc_lors_gemm<dx=%d,r=%d,sp=%d>: grid %u x %u, max active clusters %d (%s)\n", (int)DX,
+            RP, (int)SP, grid.x, grid.y, v, cudaGetErrorString(e));
+    (void)cudaGetLastError();
+  }
   kern<<<grid, threads<SP>(), smem, s>>>(tAct, tAct2, tW, tS, tF, tOut, bias, bits, SP ? meta24 : nullptr, (int)ceil_div(C, 32),
                                    Mout, Kred, alpha);
   LORS_CHECK_LAUNCH(DX ? "tc_lors_gemm<dx>" : "tc_lors_gemm<fwd>");
