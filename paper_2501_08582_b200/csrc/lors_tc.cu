@@ -372,6 +372,14 @@ constexpr int BM = 128, BN = 256, BK = 64;
 #ifndef LORS_N2
 #define LORS_N2 128
 #endif
+#ifndef LORS_PERSIST
+#define LORS_PERSIST 1
+#endif
+// Persistent dense kernels: one CTA pair per SM pair walks its tiles; the
+// producers and the recompute run ahead into the next tile while the
+// epilogue drains the accumulator through the (then idle) W_eff ring.
+template <bool SP>
+constexpr bool persist() { return !SP && LORS_PERSIST; }
 template <bool SP>
 constexpr int xw() { return SP ? 16 : LORS_XW_DENSE; }
 template <bool SP>
@@ -442,13 +450,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
                         const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmF,
                         const __grid_constant__ CUtensorMap tmOut, const bf16* __restrict__ bias,
                         const uint32_t* __restrict__ bits, const uint8_t* __restrict__ meta24, int words_per_row,
-                        int Mout, int Kred, float alpha) {
+                        int Mout, int Kred, int n_t, int n_f, float alpha) {
   using namespace rg;
   static_assert(!(SP && DX), "2:4 sparse tensor cores apply to the forward only (SURVEY C6)");
   constexpr int XW = xw<SP>(), XFORM_THREADS = 32 * XW;
   constexpr int W_SF = XW, W_MMA = XW + 1, W_ACT = XW + 2, W_RELAY = XW + 3, W_WLOAD = XW + 4;
   constexpr int NE = ne<SP>(), NW = nw<SP>(), NA = na<SP>(), D = lookahead<SP>();
   constexpr int NGRP = XW / 8;          // transform groups (alternate k-steps)
+  constexpr bool PERSIST = persist<SP>();
+  static_assert(!PERSIST || NGRP == 1, "persistent schedule assumes one transform group");
   constexpr int N2 = n2<SP>(), BNT = bnt<SP>();
   constexpr uint32_t ACT_BYTES = act_bytes<SP>(), ACT1_BYTES = 128 * BK * 2;
   constexpr uint32_t RE_COL = re_col<SP>();
@@ -488,7 +498,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   uint64_t* accf = &(wempty + 2 * NA + 2)->b;   // local: accumulator complete
   Bar16* wfull = wempty + 2 * NA + 3;   // [2][NW] local: W tile landed, set = group of the reader
   Bar16* wfree = wfull + 2 * NW;        // [NW] local: 8 transform warps done reading the W tile
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wfree + NW);
+  uint64_t* ff_empty = &(wfree + NW)->b;      // local (PERSIST): the tile's last recompute committed
+  uint64_t* acc_empty = &(wfree + NW + 1)->b; // leader (PERSIST): 16 transform warps drained the accumulator
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wfree + NW + 2);
 
   const int warp = warp_id(), lane = lane_id();
   const uint32_t rank = cluster_ctarank();
@@ -500,34 +512,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   // grouped raster over (token tile, feature pair): GROUP_T token tiles x all
   // feature pairs per group, token tile fastest, so the ~74 clusters of a wave
   // read ~9 W panels and <= 8 activation panels and both stay L2-resident.
-  int tt, fp;
-  {
-    const int n_t = (int)gridDim.y;  // token tiles
-    const int n_f = (int)(gridDim.x >> 1);
-    const int cid = (int)blockIdx.y * n_f + (int)(blockIdx.x >> 1);
+  // Tile n of this cluster: non-persistent = the cluster's own tile; persistent =
+  // tiles cl, cl + n_cl, ... of the same raster (static schedule).
+  const int cl = (int)(blockIdx.x >> 1), n_cl = (int)(gridDim.x >> 1);
+  const int n_tiles = n_t * n_f;
+  const int my_tiles = PERSIST ? (n_tiles > cl ? (n_tiles - cl + n_cl - 1) / n_cl : 0) : 1;
+  auto coords = [&](int n, int& m0_, int& l0_) {
+    const int cid = PERSIST ? cl + n * n_cl : (int)blockIdx.y * n_f + cl;
     const int per_group = GROUP_T * n_f;
-    const int g = cid / per_group, idx = cid % per_group;
-    const int gt = min(GROUP_T, n_t - g * GROUP_T);
-    fp = idx / gt;
-    tt = g * GROUP_T + idx % gt;
-  }
-  const int m0 = fp * (2 * BM) + rank * BM;   // this CTA's features
-  const int l0 = tt * BNT;                      // the pair's tokens
+    const int grp_ = cid / per_group, idx = cid % per_group;
+    const int gt = min(GROUP_T, n_t - grp_ * GROUP_T);
+    const int fp = idx / gt, tt = grp_ * GROUP_T + idx % gt;
+    m0_ = fp * (2 * BM) + rank * BM;   // this CTA's features
+    l0_ = tt * BNT;                    // the pair's tokens
+  };
+  int m0, l0;
+  coords(0, m0, l0);
   // this CTA's rows of the two MMAs' B operands: tokens l0 + 128 rank .. +127
   // (N = 256 MMA) and l0 + 256 + (N2 / 2) rank .. (N = N2 MMA)
-  const int lh = l0 + rank * 128, lh2 = l0 + 256 + rank * (N2 / 2);
   const int nk = (Kred + BK - 1) / BK;
 
   if (warp == W_SF) {
     // lane-parallel barrier initialisation over the flat Bar16 array (layout above):
     // rready / mready count the merged arrivals in the leader, wfree the 8
     // transform warps, everything else one arrival
-    constexpr int NBARS = 4 * NE + 4 * NA + 3 + 3 * NW;
+    constexpr int NBARS = 4 * NE + 4 * NA + 3 + 3 * NW + 2;
     const uint32_t merged = leader ? 18u : 1u;
     for (int k = lane; k < NBARS; k += 32) {
       uint32_t cnt = 1;
       if (k < NE || (k >= 2 * NE && k < 2 * NE + NA)) cnt = merged;
-      if (k >= NBARS - NW) cnt = 8;
+      if (k >= NBARS - 2 - NW && k < NBARS - 2) cnt = 8;   // wfree
+      if (k == NBARS - 1) cnt = 16;                       // acc_empty
       mbar_init(&bars[k].b, cnt);
     }
     fence_barrier_init();
@@ -562,10 +577,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   const uint32_t rready_l = mapa_shared(smem_u32(rready), 0);
   const uint32_t mready_l = mapa_shared(smem_u32(mready), 0);
   const uint32_t pffull_l = mapa_shared(smem_u32(pffull), 0);
+  const uint32_t acc_empty_l = mapa_shared(smem_u32(acc_empty), 0);
 
   if (warp == W_SF) {
     // ------------------------------------------------------------ factor-ring producer (both CTAs)
     if (lane == 0) {
+      for (int n = 0, g = 0; n < my_tiles; ++n) {
+      if (PERSIST && n > 0) {
+        coords(n, m0, l0);
+        mbar_wait(ff_empty, (n - 1) & 1);   // every recompute of the previous tile committed
+      }
       mbar_arrive_expect_tx(ffull, FF);
       if (DX) {  // b [r, C] as MN-major A of the recompute: two 64-wide atoms of this CTA's columns
         tma_load_2d(ffac, &tmF, ffull, m0, 0);
@@ -573,26 +594,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       } else {   // a [R, r] K-major, this CTA's rows
         tma_load_2d(ffac, &tmF, ffull, 0, m0);
       }
-      for (int i = 0; i < nk; ++i) {
-        const int e = i % NE;
-        mbar_wait(&e_empty[e].b, ((i / NE) & 1) ^ 1);
+      for (int i = 0; i < nk; ++i, ++g) {
+        const int e = g % NE;
+        mbar_wait(&e_empty[e].b, ((g / NE) & 1) ^ 1);
         uint8_t* st = sfr + e * SF;
         const int k0 = i * BK;
         mbar_arrive_expect_tx(&rready[e].b, SF);
         if (DX) tma_load_2d(st, &tmS, &rready[e].b, 0, k0 + 32 * rank);   // a rows, K-major
         else tma_load_2d(st, &tmS, &rready[e].b, k0 + 32 * rank, 0);      // b cols, MN-major
       }
+      }
     }
     cluster_wait();
   } else if (warp == W_WLOAD) {
     // ------------------------------------------------------------ W-ring producer (both CTAs)
     if (lane == 0) {
-      for (int i = 0; i < nk; ++i) {
-        const int wi = i % NW;
-        mbar_wait(&wfree[wi].b, ((i / NW) & 1) ^ 1);
+      for (int n = 0, g = 0; n < my_tiles; ++n) {
+      if (n > 0) coords(n, m0, l0);
+      for (int i = 0; i < nk; ++i, ++g) {
+        const int wi = g % NW;
+        mbar_wait(&wfree[wi].b, ((g / NW) & 1) ^ 1);
         uint8_t* st = wring + wi * W_BYTES;
         const int k0 = i * BK;
-        uint64_t* wf = &wfull[(i % NGRP) * NW + wi].b;   // the set of the group that reads step i
+        uint64_t* wf = &wfull[(g % NGRP) * NW + wi].b;   // the set of the group that reads step g
 #ifdef LORS_EXP_NO_W_TMA
         mbar_arrive(wf);
 #else
@@ -605,14 +629,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         }
 #endif
       }
+      }
     }
     cluster_wait();
   } else if (warp == W_ACT) {
     // ------------------------------------------------------------ activation-ring producer (both CTAs)
     if (lane == 0) {
-      for (int i = 0; i < nk; ++i) {
-        const int a = i % NA;
-        mbar_wait(&a_empty[a].b, ((i / NA) & 1) ^ 1);
+      for (int n = 0, g = 0; n < my_tiles; ++n) {
+      if (n > 0) coords(n, m0, l0);
+      const int lh = l0 + rank * 128, lh2 = l0 + 256 + rank * (N2 / 2);
+      for (int i = 0; i < nk; ++i, ++g) {
+        const int a = g % NA;
+        mbar_wait(&a_empty[a].b, ((g / NA) & 1) ^ 1);
 #ifdef LORS_EXP_NO_ACT_TMA
         mbar_arrive(&mready[a].b);
 #else
@@ -621,15 +649,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         if (N2) tma_load_2d(actb + a * ACT_BYTES + ACT1_BYTES, &tmAct2, &mready[a].b, i * BK, lh2);
 #endif
       }
+      }
     }
     cluster_wait();
   } else if (warp == W_RELAY) {
     cluster_wait();
     // ------------------------------------------------------------ activation relay (peer CTA)
     if (!leader && lane == 0) {
-      for (int i = 0; i < nk; ++i) {
-        const int a = i % NA;
-        mbar_wait(&mready[a].b, (i / NA) & 1);
+      const int total = my_tiles * nk;
+      for (int g = 0; g < total; ++g) {
+        const int a = g % NA;
+        mbar_wait(&mready[a].b, (g / NA) & 1);
         mbar_arrive_cluster(mready_l + a * 16);
       }
     }
@@ -638,12 +668,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     if (!leader) {
       // ---------------------------------------------------------- early relay (peer CTA)
       if (lane == 0) {
-        mbar_wait(ffull, 0);
-        mbar_arrive_cluster(pffull_l);
-        for (int i = 0; i < nk; ++i) {
-          const int e = i % NE;
-          mbar_wait(&rready[e].b, (i / NE) & 1);
-          mbar_arrive_cluster(rready_l + e * 16);
+        for (int n = 0, g = 0; n < my_tiles; ++n) {
+          mbar_wait(ffull, n & 1);
+          mbar_arrive_cluster(pffull_l);
+          for (int i = 0; i < nk; ++i, ++g) {
+            const int e = g % NE;
+            mbar_wait(&rready[e].b, (g / NE) & 1);
+            mbar_arrive_cluster(rready_l + e * 16);
+          }
         }
       }
     } else {
@@ -663,66 +695,88 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       const uint64_t act_desc = make_sdesc(smem_u32(actb), 16, 1024, SW_128);
       constexpr uint32_t FF_KSTEP = DX ? 2048 >> 4 : 32 >> 4;   // per K16 of the recompute
       constexpr uint32_t SF_KSTEP = DX ? 32 >> 4 : 1024 >> 4;
-      mbar_wait(ffull, 0);
-      mbar_wait(pffull, 0);
-      for (int j = 0; j < nk + D; ++j) {
-        if (j < nk) {  // recompute for step j, D steps ahead of its main MMA
-          const int e = j % NE;
-          mbar_wait(&rready[e].b, (j / NE) & 1);
-          tc_fence_after();
-          if (elect_one()) {
-            const uint64_t sfd = sf_desc + (uint64_t)(e * (SF >> 4));
+      auto do_rec = [&](const int j, const int rk, const int rn) {
+        if (rk == 0) {  // this tile's fixed factor, both CTAs
+          mbar_wait(ffull, rn & 1);
+          mbar_wait(pffull, rn & 1);
+        }
+        const int e = j % NE;
+        mbar_wait(&rready[e].b, (j / NE) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t sfd = sf_desc + (uint64_t)(e * (SF >> 4));
 #ifndef LORS_EXP_NO_RECOMPUTE
 #pragma unroll
-            for (int kk = 0; kk < RP / 16; ++kk)
-              mma_bf16_pair(tmem + RE_COL + e * 64, ff_desc + kk * FF_KSTEP, sfd + kk * SF_KSTEP, idesc_re,
-                            kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < RP / 16; ++kk)
+            mma_bf16_pair(tmem + RE_COL + e * 64, ff_desc + kk * FF_KSTEP, sfd + kk * SF_KSTEP, idesc_re,
+                          kk > 0 ? 1u : 0u);
 #endif
-            mma_commit_pair(&refull[(j % NGRP) * NE + e].b, 0x3);
-            mma_commit_pair(&e_empty[e].b, 0x3);
-          }
-          __syncwarp();
+          mma_commit_pair(&refull[(j % NGRP) * NE + e].b, 0x3);
+          mma_commit_pair(&e_empty[e].b, 0x3);
+          if (PERSIST && rk == nk - 1) mma_commit_pair(ff_empty, 0x3);   // fixed factor may be replaced
         }
-        const int jm = j - D;
-#if defined(LORS_EXP_CLOCK) && !defined(LORS_EXP_CLOCK_PRO)
-        if (jm == 0 && lane == 0) t_ev[0] = gtimer();
-#endif
-#ifdef LORS_EXP_CLOCK_PRO
-        if (jm == 0 && lane == 0) t_ev[3] = gtimer();
-        if (j == 0 && lane == 0) t_ev[1] = gtimer();
-#endif
-        if (jm >= 0) {  // main MMA for step jm
-          const int a = jm % NA;
-          mbar_wait(&mready[a].b, (jm / NA) & 1);
-          tc_fence_after();
-          if (elect_one()) {
-            const uint64_t ad = weff_desc + (uint64_t)(a * (WEFF_BYTES >> 4));
-            const uint64_t bd = act_desc + (uint64_t)(a * (ACT_BYTES >> 4));
-            if (SP) {
-              // two K = 32 sparse MMAs: compressed A advances 32 B, B 64 B, metadata one column each
+        __syncwarp();
+      };
+      auto do_main = [&](const int jm, const int mk, const int mn) {
+        if (PERSIST && mk == 0 && mn > 0) mbar_wait(acc_empty, (mn - 1) & 1);  // previous tile drained
+        const int a = jm % NA;
+        mbar_wait(&mready[a].b, (jm / NA) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t ad = weff_desc + (uint64_t)(a * (WEFF_BYTES >> 4));
+          const uint64_t bd = act_desc + (uint64_t)(a * (ACT_BYTES >> 4));
+          if (SP) {
+            // two K = 32 sparse MMAs: compressed A advances 32 B, B 64 B, metadata one column each
 #pragma unroll
-              for (int hh = 0; hh < 2; ++hh)
-                mma_bf16_pair_sp(tmem, ad + hh * 2, bd + hh * 4, tmem + E_COL + a * 8 + hh * 4, idesc_sp,
-                                 (jm > 0 || hh > 0) ? 1u : 0u);
-            } else {
+            for (int hh = 0; hh < 2; ++hh)
+              mma_bf16_pair_sp(tmem, ad + hh * 2, bd + hh * 4, tmem + E_COL + a * 8 + hh * 4, idesc_sp,
+                               (mk > 0 || hh > 0) ? 1u : 0u);
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              mma_bf16_pair(tmem, ad + kk * 2, bd + kk * 2, idesc_main, (mk > 0 || kk > 0) ? 1u : 0u);
+            if (N2) {  // tokens 256 .. 256 + N2 into the second accumulator
+              const uint64_t bd2 = bd + (ACT1_BYTES >> 4);
 #pragma unroll
               for (int kk = 0; kk < BK / 16; ++kk)
-                mma_bf16_pair(tmem, ad + kk * 2, bd + kk * 2, idesc_main, (jm > 0 || kk > 0) ? 1u : 0u);
-              if (N2) {  // tokens 256 .. 256 + N2 into the second accumulator
-                const uint64_t bd2 = bd + (ACT1_BYTES >> 4);
-#pragma unroll
-                for (int kk = 0; kk < BK / 16; ++kk)
-                  mma_bf16_pair(tmem + 256, ad + kk * 2, bd2 + kk * 2, idesc_n2, (jm > 0 || kk > 0) ? 1u : 0u);
-              }
+                mma_bf16_pair(tmem + 256, ad + kk * 2, bd2 + kk * 2, idesc_n2, (mk > 0 || kk > 0) ? 1u : 0u);
             }
-            mma_commit_pair(&a_empty[a].b, 0x3);
-            mma_commit_pair(&wempty[((jm + NA) % NGRP) * NA + a].b, 0x3);   // next writer's group
           }
-          __syncwarp();
+          mma_commit_pair(&a_empty[a].b, 0x3);
+          mma_commit_pair(&wempty[((jm + NA) % NGRP) * NA + a].b, 0x3);   // next writer's group
+          if (mk == nk - 1) mma_commit_pair(accf, 0x3);
+        }
+        __syncwarp();
+      };
+      // Flat schedule over this CTA pair's tiles: the recompute of step j runs D
+      // steps ahead of its main MMA and into the next tile.  At a tile boundary
+      // the previous tile's last main MMA goes first (the new tile's recompute
+      // waits for its fixed factor); incremental counters, no division by nk.
+      const int total = my_tiles * nk;
+      int rk = 0, rn = 0, mk = 0, mn = 0;
+      for (int j = 0; j < total + D; ++j) {
+        const bool has_rec = j < total, has_main = j >= D;
+        const bool flip = has_rec && rk == 0 && j > 0;
+#if defined(LORS_EXP_CLOCK) && !defined(LORS_EXP_CLOCK_PRO)
+        if (j == D && lane == 0) t_ev[0] = gtimer();
+#endif
+#ifdef LORS_EXP_CLOCK_PRO
+        if (j == D && lane == 0) t_ev[3] = gtimer();
+        if (j == 0 && lane == 0) t_ev[1] = gtimer();
+#endif
+        if (flip && has_main) {
+          do_main(j - D, mk, mn);
+          if (++mk == nk) { mk = 0; ++mn; }
+        }
+        if (has_rec) {
+          do_rec(j, rk, rn);
+          if (++rk == nk) { rk = 0; ++rn; }
+        }
+        if (!flip && has_main) {
+          do_main(j - D, mk, mn);
+          if (++mk == nk) { mk = 0; ++mn; }
         }
       }
-      if (elect_one()) mma_commit_pair(accf, 0x3);
-      __syncwarp();
     }
   } else {
     // ------------------------------------------------------------ transform warps 0..7
@@ -731,17 +785,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     const int h = (warp >> 2) & 1; // column half of the 64-wide k-step
     const int grp = warp >> 3;     // group: k-step parity this warp transforms (SP), else 0
     const int t = q * 32 + lane;   // feature row inside the tile (TMEM lane)
-    const int gm = m0 + t;         // global output feature
+    int gm = m0 + t;               // global output feature (per tile)
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const uint32_t alpha2 = pack_bf16x2(alpha, alpha);
     // Per k-step: issue the TMEM load of the rank-r product and all W loads,
     // release the recompute buffer, then transform and store.  (Pipelining the
     // loads of step i + 1 under step i measured no faster.)
-    auto issue = [&](const int i, uint32_t (&p)[32], uint32_t (&wv)[16], uint32_t& mw) {
+    auto issue = [&](const int i, const int kq, uint32_t (&p)[32], uint32_t (&wv)[16], uint32_t& mw) {
       // 0. 2:4 with precomputed metadata: this row's 8 index nibbles of the half
       //    (lors_compress_24 layout [R, C/8]); the load overlaps everything below
       if (SP && meta24 != nullptr)
-        mw = gm < Mout ? __ldg(reinterpret_cast<const uint32_t*>(meta24 + (int64_t)gm * (Kred / 8) + i * 8 + h * 4))
+        mw = gm < Mout ? __ldg(reinterpret_cast<const uint32_t*>(meta24 + (int64_t)gm * (Kred / 8) + kq * 8 + h * 4))
                        : 0x44444444u;
       // 1. rank-r product of this k-step (TMEM -> registers), then release the buffer
       const int rb = i % NE;
@@ -788,7 +842,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(rready_l + (i % NE) * 16);  // RE buffer free for step i + NE
     };
-    auto finish = [&](const int i, uint32_t (&p)[32], uint32_t (&wv)[16], uint32_t mw) {
+    auto finish = [&](const int i, const int kq, uint32_t (&p)[32], uint32_t (&wv)[16], uint32_t mw) {
       const int wb = i % NA, wi = i % NW;
       // 3. destination buffer drained by the MMA of step i - NA
       // waits for the commit of main(i - NA), the previous user of this buffer
@@ -839,7 +893,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         // thread = W row; 4 chunks of 8 k-values, same swizzled position in and out
         uint32_t mword = 0;
         uint32_t comp[8], meta = 0;  // 2:4: compressed pairs and index nibbles of this half
-        if (BITS) mword = (gm < Mout) ? __ldg(bits + (int64_t)gm * words_per_row + ((i * BK + h * 32) >> 5)) : 0u;
+        if (BITS) mword = (gm < Mout) ? __ldg(bits + (int64_t)gm * words_per_row + ((kq * BK + h * 32) >> 5)) : 0u;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const uint32_t off = (uint32_t)t * 128 + ((((uint32_t)h * 4 + c) ^ ((uint32_t)t & 7)) << 4);
@@ -900,7 +954,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           for (int j = 0; j < 4; ++j)
 #pragma unroll
             for (int e2 = 0; e2 < 2; ++e2) {
-              const int64_t kr = (int64_t)i * BK + h * 32 + 8 * j + 2 * (lane & 3) + e2;
+              const int64_t kr = (int64_t)kq * BK + h * 32 + 8 * j + 2 * (lane & 3) + e2;
               bword[j * 2 + e2] = kr < Kred ? __ldg(bits + kr * words_per_row + ((m0 + q * 32) >> 5)) : 0u;
             }
         }
@@ -942,11 +996,103 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 #endif
       }
     };
+    // Accumulator -> bf16 -> transposed staging: the accumulator is read in the MMA
+    // fragment layout (tcgen05.ld.16x256b: a thread holds two adjacent tokens of a
+    // feature), rounded to bf16 pairs (+bias) and written by stmatrix.trans into a
+    // [128 tokens][64 features] SW128 block (bank-conflict free).  Warp (q, hh):
+    // features 32q .. 32q+31 (feature half q >> 1), tokens hh*TSL .. of chunk c.
+    constexpr int TSL = 128 / (XW / 4);              // tokens of a chunk per warp (64 or 32)
+    const int hh = warp >> 2;
+    auto stage_chunk = [&](const int c, uint8_t* blk, const float (&bvals)[2][2]) {
+#pragma unroll 1
+      for (int tb = 0; tb < TSL; tb += 32) {
+        const int tok = hh * TSL + tb;                // token offset inside the chunk
+        uint32_t v[2][16];
+#pragma unroll
+        for (int g16 = 0; g16 < 2; ++g16)
+          tmem_ld_16x256b_x4(tmem + ((uint32_t)(q * 32 + 16 * g16) << 16) + (uint32_t)(c * 128 + tok), v[g16]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int g16 = 0; g16 < 2; ++g16) {
+          const int F = q * 32 + 16 * g16;
+#pragma unroll
+          for (int bp = 0; bp < 2; ++bp) {           // token blocks 2bp, 2bp+1 (8 tokens each)
+            uint32_t m[4];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int bb = 2 * bp + u;
+              m[2 * u] = pack_bf16x2(__uint_as_float(v[g16][4 * bb]) + bvals[g16][0],
+                                     __uint_as_float(v[g16][4 * bb + 1]) + bvals[g16][0]);
+              m[2 * u + 1] = pack_bf16x2(__uint_as_float(v[g16][4 * bb + 2]) + bvals[g16][1],
+                                         __uint_as_float(v[g16][4 * bb + 3]) + bvals[g16][1]);
+            }
+            // matrix mi = lane / 8: token block 2bp + (mi >> 1), feature block F + 8 (mi & 1);
+            // this lane addresses stored row (token) lane % 8 of it
+            const int mi = lane >> 3, tr = tok + 8 * (2 * bp + (mi >> 1)) + (lane & 7);
+            const int fu = ((F & 63) >> 3) + (mi & 1);   // 16-byte unit of the 128-byte row
+            stsm_x4_trans(smem_u32(blk + tr * 128 + ((fu ^ (tr & 7)) << 4)), m[0], m[1], m[2], m[3]);
+          }
+        }
+      }
+    };
+    auto bias_of = [&](float (&bvals)[2][2]) {     // bias of features (16 g + l/4) and (+8)
+#pragma unroll
+      for (int g16 = 0; g16 < 2; ++g16)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int f = m0 + q * 32 + 16 * g16 + 8 * e + (lane >> 2);
+          bvals[g16][e] = (!DX && bias != nullptr && f < Mout) ? __bfloat162float(bias[f]) : 0.f;
+        }
+    };
+    if constexpr (PERSIST) {
+      for (int n = 0, g = 0; n < my_tiles; ++n) {
+        if (n > 0) {
+          coords(n, m0, l0);
+          gm = m0 + t;
+        }
+        for (int kq = 0; kq < nk; ++kq, ++g) {
+          uint32_t p[32], wv[16], mw = 0;
+          issue(g, kq, p, wv, mw);
+          release(g);
+          finish(g, kq, p, wv, mw);
+        }
+        // -------------------------------------------------------- epilogue of tile n
+        // Staged through the W_eff ring, idle until this tile's successor is
+        // transformed: six [128 tokens][64 features] blocks in two batches of three;
+        // the accumulator is handed back to the MMA issuer after the last TMEM read.
+        mbar_wait(accf, n & 1);
+        tc_fence_after();
+        float bvals[2][2];
+        bias_of(bvals);
+#pragma unroll 1
+        for (int batch = 0; batch < 2; ++batch) {
+#pragma unroll 1
+          for (int c = 0; c < BNT / 128; ++c) {
+            const int b = 2 * c + (q >> 1);            // block (chunk c, feature half q >> 1)
+            if (b / 3 == batch) stage_chunk(c, weff + (b % 3) * WEFF_BYTES, bvals);
+          }
+          if (batch == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(acc_empty_l);
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(1, XFORM_THREADS);
+          if (warp == 0 && lane == 0) {
+            for (int b = 3 * batch; b < 3 * batch + 3; ++b)
+              tma_store_2d(&tmOut, weff + (b % 3) * WEFF_BYTES, m0 + 64 * (b & 1), l0 + 128 * (b >> 1));
+            tma_store_commit();
+            tma_store_wait_all();                      // the blocks are rewritten next
+          }
+          named_bar_sync(1, XFORM_THREADS);
+        }
+      }
+    } else {
     for (int i = grp; i < nk; i += NGRP) {
       uint32_t p[32], wv[16], mw = 0;
-      issue(i, p, wv, mw);
+      issue(i, i, p, wv, mw);
       release(i);
-      finish(i, p, wv, mw);
+      finish(i, i, p, wv, mw);
     }
     // ------------------------------------------------------------ epilogue
     mbar_wait(accf, 0);
@@ -1023,6 +1169,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       t_ev[3] = gtimer();
 #endif
     }
+    }
   }
   tc_fence_before();
   cluster_sync();
@@ -1071,7 +1218,23 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
   const size_t smem = smem_bytes<RP, SP>();
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "lors_gemm smem attribute");
-  dim3 grid((unsigned)(2 * ceil_div(Mout, 2 * BM)), (unsigned)ceil_div(L, BNT));
+  const int n_f = (int)ceil_div(Mout, 2 * BM), n_t = (int)ceil_div(L, BNT);
+  dim3 grid((unsigned)(2 * n_f), (unsigned)n_t);
+  if (persist<SP>()) {  // one CTA pair per co-resident cluster slot, tiles walked in the raster order
+    static int max_clusters[2][3] = {};
+    int& mc = max_clusters[DX][RP == 16 ? 0 : RP == 32 ? 1 : 2];
+    if (mc == 0) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(2 * (unsigned)(num_sms() / 2));
+      cfg.blockDim = dim3(threads<SP>());
+      cfg.dynamicSmemBytes = smem;
+      int v = 0;
+      if (cudaOccupancyMaxActiveClusters(&v, (void*)kern, &cfg) != cudaSuccess || v <= 0) v = num_sms() / 2;
+      (void)cudaGetLastError();
+      mc = v;
+    }
+    grid = dim3((unsigned)(2 * std::min(n_f * n_t, mc)));
+  }
   if (getenv("LORS_VERBOSE")) {  // diagnostics: how many clusters of this kernel fit on the GPU at once
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
@@ -1083,8 +1246,8 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
             RP, (int)SP, grid.x, grid.y, v, cudaGetErrorString(e));
     (void)cudaGetLastError();
   }
-  kern<<<grid, threads<SP>(), smem, s>>>(tAct, tAct2, tW, tS, tF, tOut, bias, bits, SP ? meta24 : nullptr, (int)ceil_div(C, 32),
-                                   Mout, Kred, alpha);
+  kern<<<grid, threads<SP>(), smem, s>>>(tAct, tAct2, tW, tS, tF, tOut, bias, bits, SP ? meta24 : nullptr,
+                                         (int)ceil_div(C, 32), Mout, Kred, n_t, n_f, alpha);
   LORS_CHECK_LAUNCH(DX ? "tc_lors_gemm<dx>" : "tc_lors_gemm<fwd>");
   return LORS_OK;
 }
