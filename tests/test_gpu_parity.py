@@ -407,3 +407,26 @@ def test_masked_grad_tensor_core_path_vs_oracle(P):
             _, da, db, _ = ops.lors_bwd(xd, wd, ad, bd, dyd, 2.0, grad_mode="masked", need_dx=False, mask_bits=bits)
             assert _rel(da, ref.da) <= 2e-2
             assert _rel(db, ref.db) <= 2e-2
+
+
+@pytest.mark.gpu
+def test_backward_reads_adapter_at_backward_time(P):
+    """The backward reuses the forward's bf16 adapter copies only while the fp32
+    masters are unmodified; an in-place change between forward and backward is
+    read at backward time (reference b2, adapters.py:387-394)."""
+    from paper_2501_08582_b200 import ops
+    from paper_2501_08582_b200.module import LoRSLinear
+    g = torch.Generator(device="cuda").manual_seed(11)
+    w = torch.randn(256, 128, device="cuda", generator=g) * 0.02
+    w = torch.where(w.abs() < 0.01, torch.zeros_like(w), w).bfloat16()
+    layer = LoRSLinear(w, a=torch.randn(256, 16, device="cuda", generator=g) * 0.05,
+                       b=torch.randn(16, 128, device="cuda", generator=g) * 0.2)
+    x = torch.randn(64, 128, device="cuda", generator=g).bfloat16().requires_grad_(True)
+    dy = torch.randn(64, 256, device="cuda", generator=g).bfloat16()
+    y = layer(x)
+    with torch.no_grad():
+        layer.a.mul_(3.0)                       # modified between forward and backward
+    y.backward(dy)
+    _, da, db, _ = ops.lors_bwd(x.detach(), w, layer.a.detach().bfloat16(), layer.b.detach().bfloat16(), dy, 2.0)
+    assert torch.equal(layer.b.grad, db)       # dB = alpha a^T dY X uses the updated a
+    assert torch.equal(layer.a.grad, da)
