@@ -70,6 +70,10 @@ typedef enum { LORS_GRAD_STE = 0, LORS_GRAD_MASKED = 1 } lors_grad_mode_t;
                                         masked W_eff tile is compressed on chip
                                         (W must be 2:4 along C; bf16; C % 64 == 0) */
 #define LORS_FLAG_NO_DX (1u << 2)    /* backward skips dX (first layer)        */
+#define LORS_FLAG_DX_ONLY (1u << 3)  /* backward computes dX only (da, db,     */
+                                     /* dbias may be NULL; no workspace) -- the */
+                                     /* caller runs the rank-r part separately, */
+                                     /* e.g. on a second stream, with NO_DX     */
 #define LORS_FLAG_FAULT_DA_SIGN (1u << 30) /* negative control: flip dA sign,
                                               mirrors FAULT_INJECTION
                                               "lors_backward_sign_flip"

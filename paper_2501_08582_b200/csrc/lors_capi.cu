@@ -82,7 +82,7 @@ size_t lors_fwd_workspace(const lors_fwd_args* a) {
 }
 
 size_t lors_bwd_workspace(const lors_bwd_args* a) {
-  if (a == nullptr) return 0;
+  if (a == nullptr || (a->flags & LORS_FLAG_DX_ONLY)) return 0;
   // P (when not supplied) and Q, fp32-sized slots, 256-byte aligned
   const size_t slot = ((size_t)a->L * (size_t)a->r * sizeof(float) + 255) / 256 * 256;
   return 2 * slot + tc_bwd_workspace(a);
@@ -118,7 +118,10 @@ int lors_bwd(const lors_bwd_args* A, void* stream) {
   if (st) return st;
   if (A->grad_mode != LORS_GRAD_STE && A->grad_mode != LORS_GRAD_MASKED)
     return fail(LORS_ERR_ARGUMENT, "unknown grad_mode");
-  if (!A->w || !A->a || !A->b || !A->da || !A->db) return fail(LORS_ERR_ARGUMENT, "null tensor pointer");
+  const bool dx_only = (A->flags & LORS_FLAG_DX_ONLY) != 0;
+  if (dx_only && (A->flags & LORS_FLAG_NO_DX)) return fail(LORS_ERR_ARGUMENT, "DX_ONLY and NO_DX together");
+  if (!A->w || !A->a || !A->b || (!dx_only && (!A->da || !A->db)))
+    return fail(LORS_ERR_ARGUMENT, "null tensor pointer");
   if (A->L > 0 && (!A->x || !A->dy)) return fail(LORS_ERR_ARGUMENT, "null tensor pointer");
   if (A->L > 0 && !(A->flags & LORS_FLAG_NO_DX) && !A->dx) return fail(LORS_ERR_ARGUMENT, "dx is null");
   if (A->workspace_bytes < lors_bwd_workspace(A) || (A->workspace == nullptr && lors_bwd_workspace(A) > 0))
@@ -127,6 +130,7 @@ int lors_bwd(const lors_bwd_args* A, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const int L = (int)A->L, R = (int)A->R, C = (int)A->C, r = (int)A->r;
   if (L == 0) {
+    if (dx_only) return LORS_OK;
     LORS_CUDA_TRY(cudaMemsetAsync(A->da, 0, sizeof(float) * R * r, s), "zero dA");
     LORS_CUDA_TRY(cudaMemsetAsync(A->db, 0, sizeof(float) * r * C, s), "zero dB");
     if (A->dbias) LORS_CUDA_TRY(cudaMemsetAsync(A->dbias, 0, sizeof(float) * R, s), "zero dbias");
@@ -140,6 +144,7 @@ int lors_bwd(const lors_bwd_args* A, void* stream) {
       st = simt_lors_gemm<float>(true, dy, w, bits, a, b, nullptr, (float*)A->dx, L, R, C, r, A->alpha, s);
       if (st) return st;
     }
+    if (dx_only) return LORS_OK;
     if (A->grad_mode == LORS_GRAD_STE) {
       const size_t slot = ((size_t)L * r * sizeof(float) + 255) / 256 * 256;
       float* P = (float*)A->p;

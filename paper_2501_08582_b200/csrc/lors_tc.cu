@@ -1584,6 +1584,7 @@ int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {
             : simt_lors_gemm<bf16>(true, dy, w, bits, a, b, nullptr, (bf16*)A->dx, L, R, C, r, A->alpha, s);
     if (st) return st;
   }
+  if (A->flags & LORS_FLAG_DX_ONLY) return LORS_OK;
   if (A->grad_mode == LORS_GRAD_STE) {
     const size_t slot = ((size_t)L * r * sizeof(float) + 255) / 256 * 256;
     bf16* P = (bf16*)A->p;

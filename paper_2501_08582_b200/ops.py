@@ -100,11 +100,51 @@ def lors_fwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
     return y, p
 
 
+_SIDE_STREAMS = {}
+
+
+def _side_stream(dev: torch.device) -> torch.cuda.Stream:
+    s = _SIDE_STREAMS.get(dev.index)
+    if s is None:
+        s = torch.cuda.Stream(device=dev)
+        _SIDE_STREAMS[dev.index] = s
+    return s
+
+
 def lors_bwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tensor, dy_t: torch.Tensor,
              alpha: float = 2.0, p: Optional[torch.Tensor] = None, mask_bits: Optional[torch.Tensor] = None,
              grad_mode: str = "ste", need_dx: bool = True, with_bias: bool = False,
-             fault_da_sign: bool = False):
-    """(dX_t [L, C] | None, dA [R, r] fp32, dB [r, C] fp32, dbias [R] fp32 | None)."""
+             fault_da_sign: bool = False, overlap: bool = True):
+    """(dX_t [L, C] | None, dA [R, r] fp32, dB [r, C] fp32, dbias [R] fp32 | None).
+
+    overlap=True (bf16 tensor-core shapes): the dX GEMM is enqueued on the
+    current stream and the rank-r products (P, Q, dA, dB) on a side stream, two
+    C-ABI calls (LORS_FLAG_DX_ONLY / LORS_FLAG_NO_DX); the HBM-bound rank-r
+    kernels then fill the SMs the persistent dX kernel leaves idle in its last
+    round.  The current stream waits for both before returning."""
+    R_, C_ = w.shape
+    r_ = a.shape[1] if a.dim() == 2 else 0
+    if (overlap and need_dx and w.is_cuda and w.dtype == torch.bfloat16 and R_ % 8 == 0 and C_ % 8 == 0
+            and r_ % 8 == 0 and 0 < r_ <= 64 and x_t.dim() == 2 and x_t.shape[0] > 0):
+        dev = w.device
+        main = torch.cuda.current_stream(dev)
+        side = _side_stream(dev)
+        side.wait_stream(main)
+        dx = _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, True, False, fault_da_sign,
+                            dx_only=True)[0]
+        with torch.cuda.stream(side):
+            _, da, db, dbias = _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, False,
+                                              with_bias, fault_da_sign)
+        for t in (x_t, w, a, b, dy_t, p, mask_bits, da, db, dbias):
+            if t is not None:
+                t.record_stream(side)
+        main.wait_stream(side)
+        return dx, da, db, dbias
+    return _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, with_bias, fault_da_sign)
+
+
+def _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, with_bias, fault_da_sign,
+                   dx_only: bool = False):
     L, R, C, r = _check_layer(x_t, w, a, b)
     dt = w.dtype
     code = dtype_code(dt)
@@ -119,15 +159,16 @@ def lors_bwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
         raise ArgumentError(f"grad_mode must be 'ste' or 'masked', got {grad_mode!r}")
     dev = w.device
     dx = torch.empty((L, C), dtype=dt, device=dev) if need_dx else None
-    da = torch.empty((R, r), dtype=torch.float32, device=dev)
-    db = torch.empty((r, C), dtype=torch.float32, device=dev)
-    dbias = torch.empty((R,), dtype=torch.float32, device=dev) if with_bias else None
+    da = None if dx_only else torch.empty((R, r), dtype=torch.float32, device=dev)
+    db = None if dx_only else torch.empty((r, C), dtype=torch.float32, device=dev)
+    dbias = torch.empty((R,), dtype=torch.float32, device=dev) if with_bias and not dx_only else None
     args = N.BwdArgs()
     args.L, args.R, args.C, args.r = L, R, C, r
     args.dtype = code
     args.mask_mode = N.MASK_BITS if mask_bits is not None else N.MASK_FROM_W
     args.grad_mode = N.GRAD_STE if grad_mode == "ste" else N.GRAD_MASKED
-    args.flags = (0 if need_dx else N.FLAG_NO_DX) | (N.FLAG_FAULT_DA_SIGN if fault_da_sign else 0)
+    args.flags = ((0 if need_dx else N.FLAG_NO_DX) | (N.FLAG_DX_ONLY if dx_only else 0)
+                  | (N.FLAG_FAULT_DA_SIGN if fault_da_sign and not dx_only else 0))
     args.alpha = float(alpha)
     args.x, args.w, args.mask_bits, args.a, args.b = _p(x_t), _p(w), _p(mask_bits), _p(a), _p(b)
     args.dy, args.p, args.dx, args.da, args.db, args.dbias = _p(dy_t), _p(p), _p(dx), _p(da), _p(db), _p(dbias)
