@@ -111,3 +111,18 @@ def test_c_side_validation_without_gpu(lib):
     assert lib.lors_fwd(ct.byref(a), None) == N.LORS_ERR_ARGUMENT
     a.alpha, a.R = 2.0, 0
     assert lib.lors_fwd(ct.byref(a), None) == N.LORS_ERR_SHAPE
+
+
+def test_bwd_flag_validation_without_gpu(lib):
+    """DX_ONLY (dX alone, no workspace) and NO_DX are exclusive; DX_ONLY needs no dA/dB."""
+    b = N.BwdArgs()
+    b.L, b.R, b.C, b.r = 8, 16, 16, 4
+    b.dtype, b.alpha, b.grad_mode = N.DTYPE_BF16, 2.0, N.GRAD_STE
+    b.flags = N.FLAG_DX_ONLY | N.FLAG_NO_DX
+    b.w = b.a = b.b = b.x = b.dy = b.dx = ct.c_void_p(16)
+    assert lib.lors_bwd(ct.byref(b), None) == N.LORS_ERR_ARGUMENT
+    b.flags = N.FLAG_DX_ONLY
+    assert lib.lors_bwd_workspace(ct.byref(b)) == 0
+    b.flags = 0
+    assert lib.lors_bwd_workspace(ct.byref(b)) > 0
+    assert lib.lors_bwd(ct.byref(b), None) == N.LORS_ERR_ARGUMENT      # dA / dB missing without DX_ONLY

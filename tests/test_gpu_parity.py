@@ -430,3 +430,25 @@ def test_backward_reads_adapter_at_backward_time(P):
     _, da, db, _ = ops.lors_bwd(x.detach(), w, layer.a.detach().bfloat16(), layer.b.detach().bfloat16(), dy, 2.0)
     assert torch.equal(layer.b.grad, db)       # dB = alpha a^T dY X uses the updated a
     assert torch.equal(layer.a.grad, da)
+
+
+@pytest.mark.gpu
+def test_overlapped_backward_equals_single_call(P):
+    """ops.lors_bwd's two-stream split (LORS_FLAG_DX_ONLY + NO_DX) gives the same results
+    as one C-ABI call computing everything on one stream: dX and dbias bit-identical,
+    dA / dB to fp32 summation order (their split-K partial sums are atomic reductions)."""
+    from paper_2501_08582_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(21)
+    L, R, C, r = 1000, 512, 384, 24
+    w = torch.randn(R, C, device="cuda", generator=g) * 0.02
+    w = torch.where(w.abs() < 0.012, torch.zeros_like(w), w).bfloat16()
+    a = (torch.randn(R, r, device="cuda", generator=g) * 0.05).bfloat16()
+    b = (torch.randn(r, C, device="cuda", generator=g) * 0.2).bfloat16()
+    x = torch.randn(L, C, device="cuda", generator=g).bfloat16()
+    dy = torch.randn(L, R, device="cuda", generator=g).bfloat16()
+    one = ops.lors_bwd(x, w, a, b, dy, 2.0, with_bias=True, overlap=False)
+    two = ops.lors_bwd(x, w, a, b, dy, 2.0, with_bias=True, overlap=True)
+    torch.cuda.synchronize()
+    assert torch.equal(one[0], two[0]) and torch.equal(one[3], two[3])
+    for u, v in zip(one[1:3], two[1:3]):
+        assert float((u - v).norm() / u.norm()) < 1e-5
