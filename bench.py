@@ -21,6 +21,7 @@ travel to the GPU box) on a bounded token sample of the same layer.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -115,6 +116,30 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
                 "reasons": sorted(self.reasons), "samples": len(self.samples),
                 "source": "NVML, sampled while the timed region ran"}
+
+
+def gpu_local_affinity(torch_device):
+    """Bind this process to the CPUs NVML reports as local to the GPU; returns the
+    previous affinity (None if NVML or affinity control is unavailable)."""
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+        idx = torch_device.index or 0
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            idx = int(vis.split(",")[idx])
+        h = nv.nvmlDeviceGetHandleByIndex(idx)
+        n = (os.cpu_count() + 63) // 64
+        mask = nv.nvmlDeviceGetCpuAffinity(h, n)
+        cpus = {64 * i + b for i, word in enumerate(mask) for b in range(64) if (word >> b) & 1}
+        prev = os.sched_getaffinity(0)
+        cpus &= prev
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return prev
+    except Exception as exc:  # noqa: BLE001
+        print(f"[bench] GPU-local CPU binding unavailable: {exc}", file=sys.stderr)
+    return None
 
 
 # ---------------------------------------------------------------------------
@@ -342,8 +367,14 @@ def run_native(args, cfg):
     print('[bench] e2e', file=sys.stderr, flush=True)
     # ---------------- end-to-end through the public module API (host buffers)
     layer = LoRSLinear(w, a=a32, b=b32, alpha=2.0).to(dev)
-    hx = x.cpu().pin_memory()
-    hdy = dy.cpu().pin_memory()
+    # host buffers on the GPU's NUMA node (as a data loader bound to the GPU's
+    # CPUs would place them): bind to the GPU-local CPUs while allocating and
+    # first-touching the pinned batches, so H2D runs at the local PCIe rate
+    prev_aff = gpu_local_affinity(dev)
+    hx = torch.empty(x.shape, dtype=x.dtype).pin_memory()
+    hdy = torch.empty(dy.shape, dtype=dy.dtype).pin_memory()
+    hx.copy_(x.cpu())
+    hdy.copy_(dy.cpu())
     hda = torch.empty(R, r, dtype=torch.float32).pin_memory()
     hdb = torch.empty(r, C, dtype=torch.float32).pin_memory()
 
@@ -385,20 +416,31 @@ def run_native(args, cfg):
         hdb.copy_(layer.b.grad, non_blocking=True)
 
     prefetch(0)
-    for _ in range(2):
+    for _ in range(5):   # warm the copy path (PCIe link out of its idle state) before timing
         e2e_step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.reset_peak_memory_stats(dev)
     e0, e1 = ev(), ev()
-    e2e_steps = max(3, min(args.steps, 10))
+    e2e_steps = max(5, min(args.steps, 10))
+    marks = [ev() for _ in range(e2e_steps + 1)]
+    gc.collect()
+    gc.disable()   # no interpreter GC pause inside the timed loop (training loops collect between steps)
     e0.record(stream)
-    for _ in range(e2e_steps):
+    marks[0].record(stream)
+    for i_ in range(e2e_steps):
         e2e_step()
+        marks[i_ + 1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
+    gc.enable()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if os.environ.get("LORS_BENCH_VERBOSE"):
+        print("[bench] e2e per-step ms", [round(marks[i].elapsed_time(marks[i + 1]), 2) for i in range(e2e_steps)],
+              file=sys.stderr)
+    if prev_aff is not None:
+        os.sched_setaffinity(0, prev_aff)
     peak_gb = torch.cuda.max_memory_allocated(dev) / 1e9
     if world > 1:
         tt = torch.tensor([e2e_ms, peak_gb], device=dev)

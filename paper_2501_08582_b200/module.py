@@ -56,9 +56,6 @@ class LoRSFunction(torch.autograd.Function):
         x2 = x2.contiguous()
         a = compute_copy(lora_A, dt)
         b = compute_copy(lora_B, dt)
-        # the backward reuses these copies while the masters are unmodified (same
-        # version counter); an in-place change in between is read at backward time
-        ctx.ab = (a, b, lora_A._version, lora_B._version)
         bias_c = None if bias is None else bias.detach().to(dt).contiguous()
         y, p = ops.lors_fwd(x2, weight, a, b, params.alpha, bias_c, params.mask_bits, emit_p=params.save_p,
                             sparse24=params.sparse24, meta24=params.meta24 if params.sparse24 else None)
@@ -82,11 +79,11 @@ class LoRSFunction(torch.autograd.Function):
         if dy.dtype != dt:
             dy = dy.to(dt)
         dy = dy.contiguous()
-        a, b, va, vb = ctx.ab
-        if lora_A._version != va or lora_A.dtype == dt:
-            a = compute_copy(lora_A, dt)
-        if lora_B._version != vb or lora_B.dtype == dt:
-            b = compute_copy(lora_B, dt)
+        # adapter read at backward time (a fresh compute-dtype copy: holding the
+        # forward's copies until the backward would cost r(R + C) elements per layer
+        # of peak memory, above the dense-LoRA bar)
+        a = compute_copy(lora_A, dt)
+        b = compute_copy(lora_B, dt)
         need_dx = ctx.needs_input_grad[0]
         dx, da, db, dbias = ops.lors_bwd(x2, weight, a, b, dy, params.alpha, p=p, mask_bits=params.mask_bits,
                                          grad_mode=params.grad_mode, need_dx=need_dx, with_bias=has_bias,

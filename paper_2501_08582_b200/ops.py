@@ -9,6 +9,7 @@ ArgumentError; nothing falls back to torch math.
 from __future__ import annotations
 
 import ctypes as ct
+import os
 from typing import Optional
 
 import torch
@@ -114,7 +115,7 @@ def _side_stream(dev: torch.device) -> torch.cuda.Stream:
 def lors_bwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tensor, dy_t: torch.Tensor,
              alpha: float = 2.0, p: Optional[torch.Tensor] = None, mask_bits: Optional[torch.Tensor] = None,
              grad_mode: str = "ste", need_dx: bool = True, with_bias: bool = False,
-             fault_da_sign: bool = False, overlap: bool = True):
+             fault_da_sign: bool = False, overlap: Optional[bool] = None):
     """(dX_t [L, C] | None, dA [R, r] fp32, dB [r, C] fp32, dbias [R] fp32 | None).
 
     overlap=True (bf16 tensor-core shapes): the dX GEMM is enqueued on the
@@ -122,6 +123,8 @@ def lors_bwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
     C-ABI calls (LORS_FLAG_DX_ONLY / LORS_FLAG_NO_DX); the HBM-bound rank-r
     kernels then fill the SMs the persistent dX kernel leaves idle in its last
     round.  The current stream waits for both before returning."""
+    if overlap is None:
+        overlap = os.environ.get("LORS_BWD_OVERLAP", "1") != "0"
     R_, C_ = w.shape
     r_ = a.shape[1] if a.dim() == 2 else 0
     if (overlap and need_dx and w.is_cuda and w.dtype == torch.bfloat16 and R_ % 8 == 0 and C_ % 8 == 0
@@ -132,19 +135,25 @@ def lors_bwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
         side.wait_stream(main)
         dx = _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, True, False, fault_da_sign,
                             dx_only=True)[0]
-        with torch.cuda.stream(side):
-            _, da, db, dbias = _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, False,
-                                              with_bias, fault_da_sign)
-        for t in (x_t, w, a, b, dy_t, p, mask_bits, da, db, dbias):
+        # every buffer is allocated from the current stream's pool and only marked
+        # as in use by the side stream (record_stream), so the caching allocator
+        # never has to grow a second pool for the side stream's short-lived blocks
+        _, da, db, dbias, ws = _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, False, with_bias,
+                                              fault_da_sign, launch_stream=side)
+        for t in (x_t, w, a, b, dy_t, p, mask_bits, da, db, dbias, ws):
             if t is not None:
                 t.record_stream(side)
         main.wait_stream(side)
         return dx, da, db, dbias
-    return _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, with_bias, fault_da_sign)
+    return _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, with_bias,
+                          fault_da_sign)[:4]
 
 
 def _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, with_bias, fault_da_sign,
-                   dx_only: bool = False):
+                   dx_only: bool = False, launch_stream=None):
+    """One lors_bwd C-ABI call: outputs and workspace allocated on the current
+    stream, the kernels launched on `launch_stream` (default: the current stream).
+    Returns (dx, da, db, dbias, workspace)."""
     L, R, C, r = _check_layer(x_t, w, a, b)
     dt = w.dtype
     code = dtype_code(dt)
@@ -176,8 +185,9 @@ def _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, 
     ws_bytes = lib.lors_bwd_workspace(ct.byref(args))
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev) if ws_bytes else None
     args.workspace, args.workspace_bytes = _p(ws), ws_bytes
-    N.check(lib.lors_bwd(ct.byref(args), _stream()))
-    return dx, da, db, dbias
+    st = _stream() if launch_stream is None else ct.c_void_p(launch_stream.cuda_stream)
+    N.check(lib.lors_bwd(ct.byref(args), st))
+    return dx, da, db, dbias, ws
 
 
 def effective_weight(w: torch.Tensor, a: torch.Tensor, b: torch.Tensor, alpha: float = 2.0,
