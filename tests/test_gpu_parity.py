@@ -452,3 +452,39 @@ def test_overlapped_backward_equals_single_call(P):
     assert torch.equal(one[0], two[0]) and torch.equal(one[3], two[3])
     for u, v in zip(one[1:3], two[1:3]):
         assert float((u - v).norm() / u.norm()) < 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("r,mask_mode,with_bias", [(16, "from_w", True), (24, "bits", False), (40, "from_w", False),
+                                                   (64, "bits", True)])
+def test_persistent_multi_tile_shapes(P, r, mask_mode, with_bias):
+    """Shapes with more pair tiles than co-resident CTA pairs (several tiles per
+    persistent CTA pair), ragged token count, every padded-rank variant, packed-bit
+    and from-W masks, bias: forward / dX / dA / dB against a torch fp32 reference,
+    masked W_eff entries bit-exact +0, and the token-split property."""
+    from paper_2501_08582_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(100 + r)
+    L, R, C = 3001, 4352, 1280                      # 17 feature pairs x 8 token tiles = 136 pair tiles
+    w = torch.randn(R, C, device="cuda", generator=g) * 0.02
+    w = torch.where(w.abs() < 0.015, torch.zeros_like(w), w).bfloat16()
+    a = (torch.randn(R, r, device="cuda", generator=g) * 0.05).bfloat16()
+    b = (torch.randn(r, C, device="cuda", generator=g) * 0.3).bfloat16()
+    x = torch.randn(L, C, device="cuda", generator=g).bfloat16()
+    dy = torch.randn(L, R, device="cuda", generator=g).bfloat16()
+    bias = (torch.randn(R, device="cuda", generator=g) * 0.1).bfloat16() if with_bias else None
+    bits = ops.pack_mask(w) if mask_mode == "bits" else None
+    y, _ = ops.lors_fwd(x, w, a, b, 2.0, bias, bits)
+    dx, da, db, dbias = ops.lors_bwd(x, w, a, b, dy, 2.0, mask_bits=bits, with_bias=with_bias)
+    wf, af, bf, xf, dyf = (t.float() for t in (w, a, b, x, dy))
+    weff = torch.where(wf != 0, wf + 2.0 * (af @ bf), torch.zeros_like(wf))
+    yref = xf @ weff.t() + (bias.float() if with_bias else 0.0)
+    assert _rel(y, yref.double().cpu().numpy()) <= 2e-2
+    assert _rel(dx, (dyf @ weff).double().cpu().numpy()) <= 2e-2
+    assert _rel(da, (2.0 * dyf.t() @ (xf @ bf.t())).double().cpu().numpy()) <= 2e-2
+    assert _rel(db, (2.0 * (dyf @ af).t() @ xf).double().cpu().numpy()) <= 2e-2
+    if with_bias:
+        assert _rel(dbias, dyf.sum(0).double().cpu().numpy()) <= 1e-3
+    we = ops.effective_weight(w, a, b, 2.0, bits)
+    assert bool((we[w == 0].view(torch.int16) == 0).all())
+    y2, _ = ops.lors_fwd(x[1000:].contiguous(), w, a, b, 2.0, bias, bits)
+    assert torch.equal(y2, y[1000:])
