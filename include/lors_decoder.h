@@ -21,6 +21,13 @@ extern "C" {
 int lors_rope(const void* x, void* y, const void* cos_t, const void* sin_t, int64_t B, int64_t S, int64_t H,
               int64_t hd, int32_t layout, int32_t inverse, void* stream);
 
+/* SwiGLU of the decoder MLP, bf16, n elements (n % 8 == 0, 16-byte aligned):
+ *   forward  h = silu(g) * u
+ *   backward dg = dh * u * silu'(g),  du = dh * silu(g)     (silu'(g) = s (1 + g (1 - s)), s = sigmoid(g))
+ * computed in fp32 and rounded once per output. */
+int lors_swiglu(const void* g, const void* u, void* h, int64_t n, void* stream);
+int lors_swiglu_bwd(const void* dh, const void* g, const void* u, void* dg, void* du, int64_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

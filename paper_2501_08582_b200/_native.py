@@ -35,7 +35,7 @@ EXPORTED_SYMBOLS = (
     "lors_launch_count", "lors_reset_launch_count",
 )
 # include/lors_decoder.h: decoder-side helpers (not the LoRS drop-in boundary)
-DECODER_SYMBOLS = ("lors_rope",)
+DECODER_SYMBOLS = ("lors_rope", "lors_swiglu", "lors_swiglu_bwd")
 
 _vp = ct.c_void_p
 
@@ -102,6 +102,10 @@ def load(path: str = LIB_PATH) -> ct.CDLL:
         lib.lors_rope.argtypes = [_vp, _vp, _vp, _vp, ct.c_int64, ct.c_int64, ct.c_int64, ct.c_int64, ct.c_int32,
                                   ct.c_int32, _vp]
         lib.lors_rope.restype = ct.c_int
+        lib.lors_swiglu.argtypes = [_vp, _vp, _vp, ct.c_int64, _vp]
+        lib.lors_swiglu.restype = ct.c_int
+        lib.lors_swiglu_bwd.argtypes = [_vp, _vp, _vp, _vp, _vp, ct.c_int64, _vp]
+        lib.lors_swiglu_bwd.restype = ct.c_int
         lib.lors_launch_count.restype = ct.c_uint64
         lib.lors_reset_launch_count.restype = None
         _lib = lib

@@ -61,7 +61,76 @@ __global__ void rope_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* 
   *reinterpret_cast<uint4*>(y + out + half + c) = pack8(o2);
 }
 
+__global__ void swiglu_kernel(const uint4* __restrict__ g, const uint4* __restrict__ u, uint4* __restrict__ h,
+                              int64_t n8) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n8) return;
+  float gf[8], uf[8], o[8];
+  unpack8(g[i], gf);
+  unpack8(u[i], uf);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) o[k] = gf[k] / (1.0f + __expf(-gf[k])) * uf[k];
+  h[i] = pack8(o);
+}
+
+__global__ void swiglu_bwd_kernel(const uint4* __restrict__ dh, const uint4* __restrict__ g,
+                                  const uint4* __restrict__ u, uint4* __restrict__ dg, uint4* __restrict__ du,
+                                  int64_t n8) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n8) return;
+  float d[8], gf[8], uf[8], og[8], ou[8];
+  unpack8(dh[i], d);
+  unpack8(g[i], gf);
+  unpack8(u[i], uf);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float s = 1.0f / (1.0f + __expf(-gf[k]));
+    const float silu = gf[k] * s;
+    og[k] = d[k] * uf[k] * (s * (1.0f + gf[k] * (1.0f - s)));
+    ou[k] = d[k] * silu;
+  }
+  dg[i] = pack8(og);
+  du[i] = pack8(ou);
+}
+
 }  // namespace lors
+
+extern "C" int lors_swiglu(const void* g, const void* u, void* h, int64_t n, void* stream) {
+  using namespace lors;
+  if (!g || !u || !h) {
+    set_error("lors_swiglu: null pointer");
+    return LORS_ERR_ARGUMENT;
+  }
+  if (n < 0 || n % 8 != 0) {
+    set_error("lors_swiglu: element count must be a non-negative multiple of 8");
+    return LORS_ERR_SHAPE;
+  }
+  if (n == 0) return LORS_OK;
+  const int64_t n8 = n / 8;
+  swiglu_kernel<<<(unsigned)ceil_div(n8, 256), 256, 0, (cudaStream_t)stream>>>((const uint4*)g, (const uint4*)u,
+                                                                              (uint4*)h, n8);
+  LORS_CHECK_LAUNCH("swiglu");
+  return LORS_OK;
+}
+
+extern "C" int lors_swiglu_bwd(const void* dh, const void* g, const void* u, void* dg, void* du, int64_t n,
+                               void* stream) {
+  using namespace lors;
+  if (!dh || !g || !u || !dg || !du) {
+    set_error("lors_swiglu_bwd: null pointer");
+    return LORS_ERR_ARGUMENT;
+  }
+  if (n < 0 || n % 8 != 0) {
+    set_error("lors_swiglu_bwd: element count must be a non-negative multiple of 8");
+    return LORS_ERR_SHAPE;
+  }
+  if (n == 0) return LORS_OK;
+  const int64_t n8 = n / 8;
+  swiglu_bwd_kernel<<<(unsigned)ceil_div(n8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)dh, (const uint4*)g, (const uint4*)u, (uint4*)dg, (uint4*)du, n8);
+  LORS_CHECK_LAUNCH("swiglu_bwd");
+  return LORS_OK;
+}
 
 extern "C" int lors_rope(const void* x, void* y, const void* cos_t, const void* sin_t, int64_t B, int64_t S,
                          int64_t H, int64_t hd, int32_t layout, int32_t inverse, void* stream) {

@@ -172,6 +172,28 @@ class RopeFunction(torch.autograd.Function):
         return ops.rope(gy, cos, sin, layout=1, inverse=True), None, None
 
 
+class SwiGLUFunction(torch.autograd.Function):
+    """silu(g) * u in one kernel each way (ops.swiglu / swiglu_bwd); saves g and u only."""
+
+    @staticmethod
+    def forward(ctx, g, u):
+        ctx.save_for_backward(g, u)
+        return ops.swiglu(g, u)
+
+    @staticmethod
+    def backward(ctx, dh):
+        g, u = ctx.saved_tensors
+        return ops.swiglu_bwd(dh, g, u)
+
+
+def swiglu(g, u):
+    """silu(g) * u: the fused native kernel for CUDA bf16 (multiple of 8 elements),
+    the torch formula elsewhere (CPU reference decoders in the tests)."""
+    if g.is_cuda and g.dtype == torch.bfloat16 and g.numel() % 8 == 0:
+        return SwiGLUFunction.apply(g, u)
+    return F.silu(g) * u
+
+
 def rope_heads(x_bshd, cos, sin):
     """[B, S, H, hd] -> RoPE'd [B, H, S, hd].  CUDA bf16: the native fused kernel
     (fails loudly without the library); elsewhere (CPU reference decoders in the
@@ -200,7 +222,7 @@ class DecoderLayer(nn.Module):
                                              enable_gqa=cfg.n_kv_heads != cfg.n_heads)
         h = h + p["o"](att.transpose(1, 2).reshape(B, S, cfg.dim))
         x = self.mlp_norm(h)
-        return h + p["down"](F.silu(p["gate"](x)) * p["up"](x))
+        return h + p["down"](swiglu(p["gate"](x), p["up"](x)))
 
 
 def lors_factory(cfg: DecoderConfig, a_std: float = 1e-3, b_std: Optional[float] = None,

@@ -265,3 +265,21 @@ def rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor, layout: int = 0,
     cos, sin = cos.contiguous(), sin.contiguous()
     N.check(N.load().lors_rope(_p(x), _p(y), _p(cos), _p(sin), B, S, H, hd, layout, int(inverse), _stream()))
     return y
+
+
+def swiglu(g: torch.Tensor, u: torch.Tensor) -> torch.Tensor:
+    """h = silu(g) * u, bf16, one kernel (include/lors_decoder.h)."""
+    if g.shape != u.shape or g.dtype != torch.bfloat16 or u.dtype != torch.bfloat16:
+        raise ShapeError("swiglu: g and u must be bf16 tensors of one shape")
+    g, u = g.contiguous(), u.contiguous()
+    h = torch.empty_like(g)
+    N.check(N.load().lors_swiglu(_p(g), _p(u), _p(h), g.numel(), _stream()))
+    return h
+
+
+def swiglu_bwd(dh: torch.Tensor, g: torch.Tensor, u: torch.Tensor):
+    """(dg, du) of h = silu(g) * u, bf16, one kernel."""
+    dh, g, u = dh.contiguous(), g.contiguous(), u.contiguous()
+    dg, du = torch.empty_like(g), torch.empty_like(u)
+    N.check(N.load().lors_swiglu_bwd(_p(dh), _p(g), _p(u), _p(dg), _p(du), g.numel(), _stream()))
+    return dg, du

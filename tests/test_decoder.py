@@ -239,3 +239,19 @@ def test_fused_rope_matches_torch_formula():
         assert y.shape == (2, H, 64, cfg.head_dim) and y.is_contiguous()
         assert float((y.float() - yr).norm() / yr.norm()) < 5e-3
         assert float((x.grad.float() - xr.grad).norm() / xr.grad.norm()) < 5e-3
+
+
+@pytest.mark.gpu
+def test_fused_swiglu_matches_torch():
+    """ops.swiglu / SwiGLUFunction against silu(g) * u in fp32, forward and backward."""
+    g0 = torch.Generator(device="cuda").manual_seed(5)
+    gate = (torch.randn(3, 100, 88, device="cuda", generator=g0) * 2).bfloat16().requires_grad_(True)
+    up = torch.randn(3, 100, 88, device="cuda", generator=g0).bfloat16().requires_grad_(True)
+    dh = torch.randn(3, 100, 88, device="cuda", generator=g0).bfloat16()
+    h = dec.swiglu(gate, up)
+    h.backward(dh)
+    gr, ur = gate.detach().float().requires_grad_(True), up.detach().float().requires_grad_(True)
+    hr = torch.nn.functional.silu(gr) * ur
+    hr.backward(dh.float())
+    rel = lambda a, b: float((a.float() - b).norm() / b.norm())  # noqa: E731
+    assert rel(h, hr) < 5e-3 and rel(gate.grad, gr.grad) < 5e-3 and rel(up.grad, ur.grad) < 5e-3
