@@ -28,6 +28,14 @@ int lors_rope(const void* x, void* y, const void* cos_t, const void* sin_t, int6
 int lors_swiglu(const void* g, const void* u, void* h, int64_t n, void* stream);
 int lors_swiglu_bwd(const void* dh, const void* g, const void* u, void* dg, void* du, int64_t n, void* stream);
 
+/* Fused AdamW over the flat fp32 adapter masters (torch.optim.AdamW semantics, decoupled weight decay,
+ * bias-corrected moments), one launch for every adapter of the model; also refreshes the bf16 compute
+ * copies (`shadow`, may be NULL) the LoRS kernels read, so no per-call casts remain:
+ *   p *= 1 - lr wd;  m = b1 m + (1 - b1) g;  v = b2 v + (1 - b2) g^2;
+ *   p -= lr / (1 - b1^t) * m / (sqrt(v) / sqrt(1 - b2^t) + eps);  shadow = bf16(p) */
+int lors_adamw(float* p, const float* g, float* m, float* v, void* shadow, int64_t n, float lr, float beta1,
+               float beta2, float eps, float weight_decay, int64_t step, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

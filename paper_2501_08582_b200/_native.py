@@ -35,7 +35,7 @@ EXPORTED_SYMBOLS = (
     "lors_launch_count", "lors_reset_launch_count",
 )
 # include/lors_decoder.h: decoder-side helpers (not the LoRS drop-in boundary)
-DECODER_SYMBOLS = ("lors_rope", "lors_swiglu", "lors_swiglu_bwd")
+DECODER_SYMBOLS = ("lors_rope", "lors_swiglu", "lors_swiglu_bwd", "lors_adamw")
 
 _vp = ct.c_void_p
 
@@ -106,6 +106,9 @@ def load(path: str = LIB_PATH) -> ct.CDLL:
         lib.lors_swiglu.restype = ct.c_int
         lib.lors_swiglu_bwd.argtypes = [_vp, _vp, _vp, _vp, _vp, ct.c_int64, _vp]
         lib.lors_swiglu_bwd.restype = ct.c_int
+        lib.lors_adamw.argtypes = [_vp, _vp, _vp, _vp, _vp, ct.c_int64, ct.c_float, ct.c_float, ct.c_float,
+                                   ct.c_float, ct.c_float, ct.c_int64, _vp]
+        lib.lors_adamw.restype = ct.c_int
         lib.lors_launch_count.restype = ct.c_uint64
         lib.lors_reset_launch_count.restype = None
         _lib = lib

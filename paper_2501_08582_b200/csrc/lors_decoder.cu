@@ -5,6 +5,8 @@
 #include "../../include/lors_decoder.h"
 #include "lors_common.cuh"
 
+#include <cmath>
+
 namespace lors {
 
 __device__ __forceinline__ void unpack8(const uint4 v, float (&f)[8]) {
@@ -93,7 +95,43 @@ __global__ void swiglu_bwd_kernel(const uint4* __restrict__ dh, const uint4* __r
   du[i] = pack8(ou);
 }
 
+__global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                             float* __restrict__ v, __nv_bfloat16* __restrict__ shadow, int64_t n, float decay,
+                             float b1, float b2, float step_size, float inv_sqrt_bc2, float eps) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float gi = g[i];
+  const float mi = fmaf(b1, m[i], (1.0f - b1) * gi);
+  const float vi = fmaf(b2, v[i], (1.0f - b2) * gi * gi);
+  const float pi = p[i] * decay - step_size * mi / (sqrtf(vi) * inv_sqrt_bc2 + eps);
+  m[i] = mi;
+  v[i] = vi;
+  p[i] = pi;
+  if (shadow != nullptr) shadow[i] = __float2bfloat16_rn(pi);
+}
+
 }  // namespace lors
+
+extern "C" int lors_adamw(float* p, const float* g, float* m, float* v, void* shadow, int64_t n, float lr,
+                          float beta1, float beta2, float eps, float weight_decay, int64_t step, void* stream) {
+  using namespace lors;
+  if (!p || !g || !m || !v) {
+    set_error("lors_adamw: null pointer");
+    return LORS_ERR_ARGUMENT;
+  }
+  if (n < 0 || step < 1 || !(lr >= 0.0f) || !(beta1 >= 0.0f && beta1 < 1.0f) || !(beta2 >= 0.0f && beta2 < 1.0f)) {
+    set_error("lors_adamw: invalid hyper-parameters (n >= 0, step >= 1, lr >= 0, 0 <= beta < 1)");
+    return LORS_ERR_ARGUMENT;
+  }
+  if (n == 0) return LORS_OK;
+  const double bc1 = 1.0 - std::pow((double)beta1, (double)step);
+  const double bc2 = 1.0 - std::pow((double)beta2, (double)step);
+  adamw_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      p, g, m, v, (__nv_bfloat16*)shadow, n, 1.0f - lr * weight_decay, beta1, beta2, (float)(lr / bc1),
+      (float)(1.0 / std::sqrt(bc2)), eps);
+  LORS_CHECK_LAUNCH("adamw");
+  return LORS_OK;
+}
 
 extern "C" int lors_swiglu(const void* g, const void* u, void* h, int64_t n, void* stream) {
   using namespace lors;

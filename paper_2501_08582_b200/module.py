@@ -35,7 +35,13 @@ class LoRSParams:
 
 
 def compute_copy(t: torch.Tensor, dt: torch.dtype) -> torch.Tensor:
-    """`t` (an fp32 adapter master) in the compute dtype, contiguous."""
+    """`t` (an fp32 adapter master) in the compute dtype, contiguous.  When the
+    fused optimizer (trainer.FlatAdamW) maintains a compute copy next to the
+    master and the master is unchanged since (same version counter), that copy
+    is returned instead of casting."""
+    sh = getattr(t, "_lors_shadow", None)
+    if sh is not None and sh.dtype == dt and getattr(t, "_lors_shadow_version", None) == t._version:
+        return sh
     src = t.detach()
     return src if src.dtype == dt and src.is_contiguous() else src.to(dt).contiguous()
 

@@ -29,10 +29,73 @@ def synthetic_tokens(vocab: int, batch: int, seq: int, step: int, rank: int = 0,
     return torch.randint(0, vocab, (batch, seq + 1), generator=g).to(device)
 
 
+class FlatAdamW:
+    """AdamW over all adapters in one launch (lors_adamw, include/lors_decoder.h).
+
+    The fp32 adapter masters become views into one flat buffer (as a DDP bucket
+    view would), the moments live in two more, and the same kernel writes the
+    bf16 compute copies the LoRS kernels read (`_lors_shadow` views, see
+    module.compute_copy), so a step casts no adapter.  Semantics of
+    torch.optim.AdamW (decoupled weight decay, bias-corrected moments)."""
+
+    def __init__(self, params: Sequence[nn.Parameter], lr: float, betas=(0.9, 0.999), eps: float = 1e-8,
+                 weight_decay: float = 0.0, shadow_dtype=torch.bfloat16):
+        from . import _native as N
+        self.N = N
+        self.params = list(params)
+        dev = self.params[0].device
+        if not all(p.is_cuda and p.dtype == torch.float32 and p.device == dev for p in self.params):
+            raise ArgumentError("FlatAdamW needs fp32 CUDA parameters on one device")
+        self.lr, (self.b1, self.b2), self.eps, self.wd = float(lr), betas, float(eps), float(weight_decay)
+        n = sum(p.numel() for p in self.params)
+        self.n = n
+        self.P = torch.empty(n, dtype=torch.float32, device=dev)
+        self.G = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.M = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.V = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.S = torch.empty(n, dtype=shadow_dtype, device=dev) if shadow_dtype is not None else None
+        off = 0
+        with torch.no_grad():
+            for p in self.params:
+                k = p.numel()
+                self.P[off:off + k].copy_(p.detach().reshape(-1))
+                p.data = self.P[off:off + k].view_as(p)
+                if self.S is not None:
+                    p._lors_shadow = self.S[off:off + k].view_as(p)
+                off += k
+            if self.S is not None:
+                self.S.copy_(self.P)
+        self._mark()
+        self.steps = 0
+
+    def _mark(self) -> None:
+        for p in self.params:
+            p._lors_shadow_version = p._version
+
+    def step(self) -> None:
+        grads = [p.grad.reshape(-1) if p.grad is not None else torch.zeros(p.numel(), device=self.P.device)
+                 for p in self.params]
+        torch.cat(grads, out=self.G)
+        if self.S is not None and any(p._version != p._lors_shadow_version for p in self.params):
+            self.S.copy_(self.P)             # a master was changed elsewhere: resync the compute copies
+        self.steps += 1
+        N = self.N
+        N.check(N.load().lors_adamw(self.P.data_ptr(), self.G.data_ptr(), self.M.data_ptr(), self.V.data_ptr(),
+                                    None if self.S is None else self.S.data_ptr(), self.n, self.lr, self.b1,
+                                    self.b2, self.eps, self.wd, self.steps,
+                                    torch.cuda.current_stream(self.P.device).cuda_stream))
+        self._mark()
+
+    def zero_grad(self, set_to_none: bool = True) -> None:
+        for p in self.params:
+            p.grad = None
+
+
 class Trainer:
     def __init__(self, model: nn.Module, lr: float = 2e-5, betas=(0.9, 0.999), eps: float = 1e-8,
                  weight_decay: float = 0.0, process_group=None, overlap: bool = True,
-                 bucket_bytes: int = 64 << 20, params: Optional[Sequence[nn.Parameter]] = None):
+                 bucket_bytes: int = 64 << 20, params: Optional[Sequence[nn.Parameter]] = None,
+                 optimizer: str = "auto"):
         self.model = model
         self.params = list(params) if params is not None else [p for p in model.parameters() if p.requires_grad]
         if not self.params:
@@ -42,9 +105,14 @@ class Trainer:
         if self.world > 1:
             broadcast_adapters(self.params, process_group=process_group)
             self.reducer = AdapterGradReducer(self.params, process_group, bucket_bytes, overlap=overlap)
-        fused = all(p.is_cuda for p in self.params)
-        self.opt = torch.optim.AdamW(self.params, lr=lr, betas=betas, eps=eps, weight_decay=weight_decay,
-                                     fused=fused)
+        cuda32 = all(p.is_cuda and p.dtype == torch.float32 for p in self.params)
+        if optimizer not in ("auto", "native", "torch"):
+            raise ArgumentError(f"optimizer must be auto, native or torch, got {optimizer!r}")
+        if optimizer == "native" or (optimizer == "auto" and cuda32):
+            self.opt = FlatAdamW(self.params, lr=lr, betas=betas, eps=eps, weight_decay=weight_decay)
+        else:
+            self.opt = torch.optim.AdamW(self.params, lr=lr, betas=betas, eps=eps, weight_decay=weight_decay,
+                                         fused=all(p.is_cuda for p in self.params))
         self.steps = 0
 
     def step(self, tokens: torch.Tensor) -> torch.Tensor:

@@ -255,3 +255,34 @@ def test_fused_swiglu_matches_torch():
     hr.backward(dh.float())
     rel = lambda a, b: float((a.float() - b).norm() / b.norm())  # noqa: E731
     assert rel(h, hr) < 5e-3 and rel(gate.grad, gr.grad) < 5e-3 and rel(up.grad, ur.grad) < 5e-3
+
+
+@pytest.mark.gpu
+def test_flat_adamw_matches_torch_adamw():
+    """trainer.FlatAdamW (one fused launch, bf16 compute copies refreshed in place)
+    against torch.optim.AdamW on identical parameters and gradients for several
+    steps (decoupled weight decay, bias correction); the compute copies equal the
+    rounded masters and are what compute_copy returns."""
+    from paper_2501_08582_b200.module import compute_copy
+    from paper_2501_08582_b200.trainer import FlatAdamW
+    g = torch.Generator(device="cuda").manual_seed(9)
+    shapes = [(64, 16), (16, 48), (300, 8), (8, 300), (7,)]
+    p1 = [torch.nn.Parameter(torch.randn(s, device="cuda", generator=g)) for s in shapes]
+    p2 = [torch.nn.Parameter(p.detach().clone()) for p in p1]
+    o1 = FlatAdamW(p1, lr=3e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.05)
+    o2 = torch.optim.AdamW(p2, lr=3e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.05)
+    for step in range(6):
+        for a, b in zip(p1, p2):
+            gr = torch.randn(a.shape, device="cuda", generator=g) * (10.0 ** (step % 3 - 2))
+            a.grad, b.grad = gr.clone(), gr.clone()
+        o1.step()
+        o2.step()
+        o1.zero_grad()
+        o2.zero_grad()
+        for a, b in zip(p1, p2):
+            assert torch.allclose(a, b, rtol=1e-5, atol=1e-7)
+            assert compute_copy(a, torch.bfloat16) is a._lors_shadow
+            assert torch.equal(compute_copy(a, torch.bfloat16), a.detach().bfloat16())
+    with torch.no_grad():                              # an outside in-place change: the cast path takes over
+        p1[0].mul_(2.0)
+    assert torch.equal(compute_copy(p1[0], torch.bfloat16), p1[0].detach().bfloat16())
