@@ -396,9 +396,15 @@ def run_native(args, cfg):
             dys.copy_(hdy, non_blocking=True)
             filled[k % 2].record(copy_stream)
 
+    done = [torch.cuda.Event() for _ in range(2)]
+
     def e2e_step():
         k = state["k"]
         state["k"] = k + 1
+        # bounded run-ahead, as a training loop reading its results has: the host waits
+        # for step k - 2's copy-out before enqueuing step k (the GPU stays a step ahead)
+        if k >= 2:
+            done[k % 2].synchronize()
         xs, dys = slots[k % 2]
         stream.wait_event(filled[k % 2])
         prefetch(k + 1)
@@ -414,6 +420,7 @@ def run_native(args, cfg):
             dist.all_reduce(grad_bucket, op=dist.ReduceOp.AVG)
         hda.copy_(layer.a.grad, non_blocking=True)
         hdb.copy_(layer.b.grad, non_blocking=True)
+        done[k % 2].record(stream)
 
     prefetch(0)
     for _ in range(5):   # warm the copy path (PCIe link out of its idle state) before timing
@@ -429,8 +436,11 @@ def run_native(args, cfg):
     gc.disable()   # no interpreter GC pause inside the timed loop (training loops collect between steps)
     e0.record(stream)
     marks[0].record(stream)
+    host_ms = []
     for i_ in range(e2e_steps):
+        th = time.perf_counter()
         e2e_step()
+        host_ms.append(1e3 * (time.perf_counter() - th))
         marks[i_ + 1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -438,7 +448,7 @@ def run_native(args, cfg):
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     if os.environ.get("LORS_BENCH_VERBOSE"):
         print("[bench] e2e per-step ms", [round(marks[i].elapsed_time(marks[i + 1]), 2) for i in range(e2e_steps)],
-              file=sys.stderr)
+              "host ms", [round(v, 2) for v in host_ms], file=sys.stderr)
     if prev_aff is not None:
         os.sched_setaffinity(0, prev_aff)
     peak_gb = torch.cuda.max_memory_allocated(dev) / 1e9
@@ -593,8 +603,12 @@ def run_decoder(args):
         _native.reset_launch_count()
         e0, e1 = ev(), ev()
         e0.record(stream)
+        done = [torch.cuda.Event() for _ in range(2)]
         for s in range(steps):
+            if s >= 2:   # bounded run-ahead: the host waits for step s - 2 (as a loop logging its loss would)
+                done[s % 2].synchronize()
             loss = trainer.step(toks[warmup + s])
+            done[s % 2].record(stream)
         e1.record(stream)
         if clocks:
             clocks.sample_until(e1)

@@ -620,6 +620,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 #ifdef LORS_EXP_NO_W_TMA
         mbar_arrive(wf);
 #else
+#ifdef LORS_EXP_HALF_W
+        if (i & 1) { mbar_arrive(wf); continue; }   // timing experiment: half the W bytes (a compressed stream)
+#endif
         mbar_arrive_expect_tx(wf, W_BYTES);
         if (DX) {  // W[k0:k0+64, m0:m0+128] as two SW128 boxes of 64 columns
           tma_load_2d(st, &tmW, wf, m0, k0);

@@ -104,10 +104,11 @@ def lors_fwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
 _SIDE_STREAMS = {}
 
 
-def _side_stream(dev: torch.device) -> torch.cuda.Stream:
+def _side_stream(dev: torch.device):
+    """(side stream, fork event, join event) for `dev`, created once and reused."""
     s = _SIDE_STREAMS.get(dev.index)
     if s is None:
-        s = torch.cuda.Stream(device=dev)
+        s = (torch.cuda.Stream(device=dev), torch.cuda.Event(), torch.cuda.Event())
         _SIDE_STREAMS[dev.index] = s
     return s
 
@@ -131,8 +132,9 @@ def lors_bwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
             and r_ % 8 == 0 and 0 < r_ <= 64 and x_t.dim() == 2 and x_t.shape[0] > 0):
         dev = w.device
         main = torch.cuda.current_stream(dev)
-        side = _side_stream(dev)
-        side.wait_stream(main)
+        side, fork, join = _side_stream(dev)
+        fork.record(main)
+        side.wait_event(fork)
         dx = _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, True, False, fault_da_sign,
                             dx_only=True)[0]
         # every buffer is allocated from the current stream's pool and only marked
@@ -143,7 +145,8 @@ def lors_bwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
         for t in (x_t, w, a, b, dy_t, p, mask_bits, da, db, dbias, ws):
             if t is not None:
                 t.record_stream(side)
-        main.wait_stream(side)
+        join.record(side)
+        main.wait_event(join)
         return dx, da, db, dbias
     return _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, with_bias,
                           fault_da_sign)[:4]
