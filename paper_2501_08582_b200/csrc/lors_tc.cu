@@ -8,8 +8,18 @@
 //        adds W, applies M = (W != 0) (or the packed bits) with a select,
 //        rounds to bf16 and writes the swizzled operand tile to shared memory,
 //        which the main MMA consumes.  W_eff never touches HBM.
+//        Dense kernels: 256 features x 384 tokens per CTA pair (two accumulators),
+//        persistent over the tile raster; the 2:4 kernel (tcgen05.mma.sp) keeps
+//        256-token tiles, one per launch.  DESIGN.md section 3 has the pipeline.
 //   K4 tc_skinny            the rank-r products P = X b^T, Q = dY a,
-//        dA = alpha dY^T P, dB = alpha Q^T X (adapters.py:396-399), N = r.
+//        dA = alpha dY^T P, dB = alpha Q^T X (adapters.py:396-399), N = r,
+//        split-K into fp32 accumulators.
+//   K5 tc_masked_grad       G = (dY^T X) . M in TMEM, contracted into dA / dB
+//        (the sqft_gc comparator's masked gradient, adapters.py:303-312).
+//
+// Timing-experiment switches (tools/exp_variants.sh, never set in the product
+// build): LORS_EXP_NO_RECOMPUTE / _NO_XFORM / _NO_W_TMA / _NO_ACT_TMA skip one
+// pipeline stage; LORS_EXP_CLOCK / _CLOCK_PRO record an in-kernel timeline.
 //
 // Shapes that the TMA path cannot address (rows not 16-byte multiples, or
 // r > 64) run the FFMA kernels of lors_simt.cu instead.
@@ -620,9 +630,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 #ifdef LORS_EXP_NO_W_TMA
         mbar_arrive(wf);
 #else
-#ifdef LORS_EXP_HALF_W
-        if (i & 1) { mbar_arrive(wf); continue; }   // timing experiment: half the W bytes (a compressed stream)
-#endif
         mbar_arrive_expect_tx(wf, W_BYTES);
         if (DX) {  // W[k0:k0+64, m0:m0+128] as two SW128 boxes of 64 columns
           tma_load_2d(st, &tmW, wf, m0, k0);
@@ -851,10 +858,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       // waits for the commit of main(i - NA), the previous user of this buffer
       if (i >= NA) mbar_wait(&wempty[(i % NGRP) * NA + wb].b, ((i - NA) / A_PERIOD) & 1);
       const uint32_t dst = smem_u32(weff + wb * WEFF_BYTES);
-#ifdef LORS_EXP_EARLY_ARRIVE
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(mready_l + wb * 16);  // timing experiment only (races)
-#endif
 #ifdef LORS_EXP_NO_XFORM
       constexpr bool XF = false;  // timing experiment: W_eff buffers left as they are
 #else
@@ -882,12 +885,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
                        "r"(comp[4 * cc + 1]), "r"(comp[4 * cc + 2]), "r"(comp[4 * cc + 3])
                        : "memory");
         }
-#ifdef LORS_EXP_SP_CONST_META
-        const uint32_t pm = 0x44444444u;
-        mw = 0x44444444u;
-#else
         const uint32_t pm = __shfl_xor_sync(0xffffffffu, mw, 8);
-#endif
         const uint32_t word = (lane & 8) ? ((pm >> 16) | (mw & 0xFFFF0000u)) : ((mw & 0xFFFFu) | (pm << 16));
         tmem_st_x1(tmem + lane_addr + E_COL + wb * 8 + h * 4, word);
         tmem_st_wait();
@@ -922,9 +920,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
               meta |= nib << (4 * (c * 2 + gi));
             }
           } else {
-#ifdef LORS_EXP_XF_NO_ST
-            if ((o[0] ^ o[1] ^ o[2] ^ o[3]) == 0x12345679u)
-#endif
             asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + off), "r"(o[0]), "r"(o[1]), "r"(o[2]),
                          "r"(o[3])
                          : "memory");
@@ -985,18 +980,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           }
         }
       }
-#ifndef LORS_EXP_NO_FENCE
       fence_proxy_async_smem();
-#endif
       __syncwarp();
 #ifdef LORS_EXP_CLOCK_PRO
       if (i == 0 && warp == 0 && lane == 0) t_ev[2] = gtimer();
 #endif
       if (lane == 0) {
         mbar_arrive(&wfree[wi].b);                   // done reading the W tile
-#ifndef LORS_EXP_EARLY_ARRIVE
         mbar_arrive_cluster(mready_l + wb * 16);     // W_eff half ready for the pair MMA
-#endif
       }
     };
     // Accumulator -> bf16 -> transposed staging: the accumulator is read in the MMA
