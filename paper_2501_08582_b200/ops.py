@@ -105,10 +105,15 @@ _SIDE_STREAMS = {}
 
 
 def _side_stream(dev: torch.device):
-    """(side stream, fork event, join event) for `dev`, created once and reused."""
+    """(high-priority stream for dX, normal stream for the rank-r part, fork event,
+    two join events) for `dev`, created once and reused.  The priority makes the
+    persistent dX kernel's CTAs win the SMs when both are ready; the rank-r
+    kernels fill whatever it leaves idle."""
     s = _SIDE_STREAMS.get(dev.index)
     if s is None:
-        s = (torch.cuda.Stream(device=dev), torch.cuda.Event(), torch.cuda.Event())
+        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
+        s = (torch.cuda.Stream(device=dev, priority=hi), torch.cuda.Stream(device=dev),
+             torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event())
         _SIDE_STREAMS[dev.index] = s
     return s
 
@@ -132,20 +137,21 @@ def lors_bwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
             and r_ % 8 == 0 and 0 < r_ <= 64 and x_t.dim() == 2 and x_t.shape[0] > 0):
         dev = w.device
         main = torch.cuda.current_stream(dev)
-        side, fork, join = _side_stream(dev)
+        hi, side, fork, join_hi, join = _side_stream(dev)
         fork.record(main)
+        hi.wait_event(fork)
         side.wait_event(fork)
         dx = _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, True, False, fault_da_sign,
-                            dx_only=True)[0]
-        # every buffer is allocated from the current stream's pool and only marked
-        # as in use by the side stream (record_stream), so the caching allocator
-        # never has to grow a second pool for the side stream's short-lived blocks
+                            dx_only=True, launch_stream=hi)[0]
+        # Every buffer comes from the current stream's pool, and the current stream
+        # waits for both side streams before this call returns, so any later reuse
+        # of these blocks is ordered after the side work: no record_stream (whose
+        # deferred frees made the caching allocator grow with cudaMalloc stalls).
         _, da, db, dbias, ws = _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, False, with_bias,
                                               fault_da_sign, launch_stream=side)
-        for t in (x_t, w, a, b, dy_t, p, mask_bits, da, db, dbias, ws):
-            if t is not None:
-                t.record_stream(side)
+        join_hi.record(hi)
         join.record(side)
+        main.wait_event(join_hi)
         main.wait_event(join)
         return dx, da, db, dbias
     return _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, with_bias,
