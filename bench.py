@@ -511,7 +511,7 @@ def run_native(args, cfg):
         achieved = dom_flops / (dom_ms * 1e-3) / 1e12
         traffic = None
         tp = os.path.join(ROOT, "profiles", "traffic_latest.json")
-        if os.path.exists(tp):
+        if os.path.exists(tp) and dt == torch.bfloat16:   # the ncu capture is of the bf16 tensor-core kernels
             with open(tp) as f:
                 tr = json.load(f)
             key = "dx" if "dx" in dom else "fwd"

@@ -433,7 +433,10 @@ constexpr uint64_t nibble_lut() {
 }
 constexpr uint64_t kNibbleLut = nibble_lut();
 constexpr uint32_t E_COL = 448;  // 2:4 metadata: W_eff buffer b, MMA h at column 448 + 8 b + 4 h
-constexpr int GROUP_T = 8;  // raster: token tiles per group (clusters of a wave share W and activation tiles)
+#ifndef LORS_GROUP_T
+#define LORS_GROUP_T 8
+#endif
+constexpr int GROUP_T = LORS_GROUP_T;  // raster: token tiles per group (clusters of a wave share W and activation tiles)
 template <bool SP>
 constexpr uint32_t act_bytes() { return (bnt<SP>() / 2) * BK * 2; }   // this CTA's tokens: 24 KB / 16 KB
 constexpr uint32_t W_BYTES = BM * BK * 2;           // 16 KB
