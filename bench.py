@@ -607,7 +607,7 @@ def run_decoder(args):
             from paper_2501_08582_b200.comparators import comparator_factory
             fac = comparator_factory(kind, dcfg, seed=0)
         model = D.LoRSDecoder(dcfg, device=dev, seed=0, linear_factory=fac)
-        return model, Trainer(model, lr=2e-5)
+        return model, Trainer(model, lr=2e-5, optimizer=args.optimizer if kind == "lors" else "auto")
 
     def measure(kind, steps, warmup, sample_clocks=False):
         model, trainer = build(kind)
@@ -736,6 +736,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline sample")
     ap.add_argument("--compare", action="store_true",
                     help="decoder configs: also run the dense-LoRA and SQFT-style decoders (peak HBM, tokens/s)")
+    ap.add_argument("--optimizer", choices=("native", "p2p", "torch"), default="native",
+                    help="decoder configs: fused flat AdamW after an NCCL all-reduce (native), the fused "
+                         "peer-memory reduce + AdamW kernel over symmetric memory (p2p), or torch AdamW")
     ap.add_argument("--sparse24", action="store_true",
                     help="decoder configs with 2:4 masks: forward on the sparse tensor cores")
     args = ap.parse_args()

@@ -36,6 +36,18 @@ int lors_swiglu_bwd(const void* dh, const void* g, const void* u, void* dg, void
 int lors_adamw(float* p, const float* g, float* m, float* v, void* shadow, int64_t n, float lr, float beta1,
                float beta2, float eps, float weight_decay, int64_t step, void* stream);
 
+/* Fused gradient collective + AdamW over NVLink peer memory: every rank owns the shard
+ * [rank n / world, (rank + 1) n / world) of the flat adapter buffers (n a multiple of 4 * world).  For each
+ * element of its shard it sums the gradient over all ranks' gradient buffers (peer loads), divides by world,
+ * applies the AdamW update of lors_adamw to its master copy with its optimizer-state shard (m, v hold n /
+ * world elements), and stores the new value -- and its bf16 compute copy -- into every rank's parameter
+ * (and shadow) buffer (peer stores).  `grads`, `params`, `shadows` are device arrays of `world` peer
+ * pointers (symmetric-memory buffer_ptrs_dev); the caller brackets the call with symmetric-memory barriers.
+ * One reduce-scatter, one optimizer step and one all-gather in a single kernel. */
+int lors_adamw_p2p(const void* grads, const void* params, const void* shadows, float* m_shard, float* v_shard,
+                   int64_t n, int32_t rank, int32_t world, float lr, float beta1, float beta2, float eps,
+                   float weight_decay, int64_t step, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

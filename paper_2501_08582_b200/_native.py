@@ -35,7 +35,7 @@ EXPORTED_SYMBOLS = (
     "lors_launch_count", "lors_reset_launch_count",
 )
 # include/lors_decoder.h: decoder-side helpers (not the LoRS drop-in boundary)
-DECODER_SYMBOLS = ("lors_rope", "lors_swiglu", "lors_swiglu_bwd", "lors_adamw")
+DECODER_SYMBOLS = ("lors_rope", "lors_swiglu", "lors_swiglu_bwd", "lors_adamw", "lors_adamw_p2p")
 
 _vp = ct.c_void_p
 
@@ -109,6 +109,9 @@ def load(path: str = LIB_PATH) -> ct.CDLL:
         lib.lors_adamw.argtypes = [_vp, _vp, _vp, _vp, _vp, ct.c_int64, ct.c_float, ct.c_float, ct.c_float,
                                    ct.c_float, ct.c_float, ct.c_int64, _vp]
         lib.lors_adamw.restype = ct.c_int
+        lib.lors_adamw_p2p.argtypes = [_vp, _vp, _vp, _vp, _vp, ct.c_int64, ct.c_int32, ct.c_int32, ct.c_float,
+                                       ct.c_float, ct.c_float, ct.c_float, ct.c_float, ct.c_int64, _vp]
+        lib.lors_adamw_p2p.restype = ct.c_int
         lib.lors_launch_count.restype = ct.c_uint64
         lib.lors_reset_launch_count.restype = None
         _lib = lib

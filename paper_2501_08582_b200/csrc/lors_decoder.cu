@@ -110,7 +110,72 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
   if (shadow != nullptr) shadow[i] = __float2bfloat16_rn(pi);
 }
 
+// Peer-memory AdamW over one shard: 4 elements per thread (16-byte peer loads and stores).
+// The rank's own master copy is read through params[rank] (all copies are identical).
+__global__ void adamw_p2p_kernel(const float* const* __restrict__ grads, float* const* __restrict__ params,
+                                 __nv_bfloat16* const* __restrict__ shadows, float* __restrict__ m,
+                                 float* __restrict__ v, int64_t lo, int64_t shard4, int rank, int world, float decay,
+                                 float b1, float b2, float step_size, float inv_sqrt_bc2, float eps, float inv_world) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // float4 index inside the shard
+  if (q >= shard4) return;
+  const int64_t e = lo + 4 * q;                                         // element index in the flat buffer
+  float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int p = 0; p < world; ++p) {                                     // reduce over the ranks (NVLink loads)
+    const float4 x = *reinterpret_cast<const float4*>(grads[p] + e);
+    g.x += x.x; g.y += x.y; g.z += x.z; g.w += x.w;
+  }
+  const float4 p0 = *reinterpret_cast<const float4*>(params[rank] + e);
+  float4 mm = reinterpret_cast<float4*>(m)[q], vv = reinterpret_cast<float4*>(v)[q];
+  float gi[4] = {g.x * inv_world, g.y * inv_world, g.z * inv_world, g.w * inv_world};
+  float pi[4] = {p0.x, p0.y, p0.z, p0.w}, mi[4] = {mm.x, mm.y, mm.z, mm.w}, vi[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    mi[k] = fmaf(b1, mi[k], (1.0f - b1) * gi[k]);
+    vi[k] = fmaf(b2, vi[k], (1.0f - b2) * gi[k] * gi[k]);
+    pi[k] = pi[k] * decay - step_size * mi[k] / (sqrtf(vi[k]) * inv_sqrt_bc2 + eps);
+  }
+  reinterpret_cast<float4*>(m)[q] = make_float4(mi[0], mi[1], mi[2], mi[3]);
+  reinterpret_cast<float4*>(v)[q] = make_float4(vi[0], vi[1], vi[2], vi[3]);
+  const float4 pn = make_float4(pi[0], pi[1], pi[2], pi[3]);
+  __nv_bfloat162 s01 = __floats2bfloat162_rn(pi[0], pi[1]), s23 = __floats2bfloat162_rn(pi[2], pi[3]);
+  uint2 sb;
+  sb.x = *reinterpret_cast<uint32_t*>(&s01);
+  sb.y = *reinterpret_cast<uint32_t*>(&s23);
+  for (int p = 0; p < world; ++p) {                                     // all-gather (NVLink stores)
+    *reinterpret_cast<float4*>(params[p] + e) = pn;
+    if (shadows != nullptr) *reinterpret_cast<uint2*>(shadows[p] + e) = sb;
+  }
+}
+
 }  // namespace lors
+
+extern "C" int lors_adamw_p2p(const void* grads, const void* params, const void* shadows, float* m_shard,
+                              float* v_shard, int64_t n, int32_t rank, int32_t world, float lr, float beta1,
+                              float beta2, float eps, float weight_decay, int64_t step, void* stream) {
+  using namespace lors;
+  if (!grads || !params || !m_shard || !v_shard) {
+    set_error("lors_adamw_p2p: null pointer");
+    return LORS_ERR_ARGUMENT;
+  }
+  if (world < 1 || world > 64 || rank < 0 || rank >= world || n < 0 || n % (4 * (int64_t)world) != 0) {
+    set_error("lors_adamw_p2p: need 1 <= world <= 64, 0 <= rank < world, n a multiple of 4 * world");
+    return LORS_ERR_ARGUMENT;
+  }
+  if (step < 1 || !(lr >= 0.0f) || !(beta1 >= 0.0f && beta1 < 1.0f) || !(beta2 >= 0.0f && beta2 < 1.0f)) {
+    set_error("lors_adamw_p2p: invalid hyper-parameters");
+    return LORS_ERR_ARGUMENT;
+  }
+  const int64_t shard = n / world, shard4 = shard / 4;
+  if (shard4 == 0) return LORS_OK;
+  const double bc1 = 1.0 - std::pow((double)beta1, (double)step);
+  const double bc2 = 1.0 - std::pow((double)beta2, (double)step);
+  adamw_p2p_kernel<<<(unsigned)ceil_div(shard4, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const float* const*)grads, (float* const*)params, (__nv_bfloat16* const*)shadows, m_shard, v_shard,
+      (int64_t)rank * shard, shard4, rank, world, 1.0f - lr * weight_decay, beta1, beta2, (float)(lr / bc1),
+      (float)(1.0 / std::sqrt(bc2)), eps, 1.0f / (float)world);
+  LORS_CHECK_LAUNCH("adamw_p2p");
+  return LORS_OK;
+}
 
 extern "C" int lors_adamw(float* p, const float* g, float* m, float* v, void* shadow, int64_t n, float lr,
                           float beta1, float beta2, float eps, float weight_decay, int64_t step, void* stream) {

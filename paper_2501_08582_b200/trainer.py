@@ -102,13 +102,18 @@ class Trainer:
             raise ArgumentError("model has no trainable adapter parameters")
         self.world = dist.get_world_size(process_group) if dist.is_initialized() else 1
         self.reducer = None
+        if optimizer not in ("auto", "native", "torch", "p2p"):
+            raise ArgumentError(f"optimizer must be auto, native, torch or p2p, got {optimizer!r}")
         if self.world > 1:
             broadcast_adapters(self.params, process_group=process_group)
-            self.reducer = AdapterGradReducer(self.params, process_group, bucket_bytes, overlap=overlap)
+            if optimizer != "p2p":    # p2p reduces the gradients inside its optimizer kernel
+                self.reducer = AdapterGradReducer(self.params, process_group, bucket_bytes, overlap=overlap)
         cuda32 = all(p.is_cuda and p.dtype == torch.float32 for p in self.params)
-        if optimizer not in ("auto", "native", "torch"):
-            raise ArgumentError(f"optimizer must be auto, native or torch, got {optimizer!r}")
-        if optimizer == "native" or (optimizer == "auto" and cuda32):
+        if optimizer == "p2p":
+            from .collective import SymmetricAdamW
+            self.opt = SymmetricAdamW(self.params, process_group, lr=lr, betas=betas, eps=eps,
+                                      weight_decay=weight_decay)
+        elif optimizer == "native" or (optimizer == "auto" and cuda32):
             self.opt = FlatAdamW(self.params, lr=lr, betas=betas, eps=eps, weight_decay=weight_decay)
         else:
             self.opt = torch.optim.AdamW(self.params, lr=lr, betas=betas, eps=eps, weight_decay=weight_decay,
