@@ -82,7 +82,8 @@ size_t lors_fwd_workspace(const lors_fwd_args* a) {
 }
 
 size_t lors_bwd_workspace(const lors_bwd_args* a) {
-  if (a == nullptr || (a->flags & LORS_FLAG_DX_ONLY)) return 0;
+  if (a == nullptr) return 0;
+  if (a->flags & LORS_FLAG_DX_ONLY) return tc_bwd_workspace(a);
   // P (when not supplied) and Q, fp32-sized slots, 256-byte aligned
   const size_t slot = ((size_t)a->L * (size_t)a->r * sizeof(float) + 255) / 256 * 256;
   return 2 * slot + tc_bwd_workspace(a);

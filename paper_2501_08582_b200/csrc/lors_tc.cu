@@ -463,7 +463,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
                         const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmF,
                         const __grid_constant__ CUtensorMap tmOut, const bf16* __restrict__ bias,
                         const uint32_t* __restrict__ bits, const uint8_t* __restrict__ meta24, int words_per_row,
-                        int Mout, int Kred, int n_t, int n_f, float alpha) {
+                        int Mout, int Kred, int n_t, int n_f, int split, float* __restrict__ partials,
+                        unsigned int* __restrict__ counters, float alpha) {
   using namespace rg;
   static_assert(!(SP && DX), "2:4 sparse tensor cores apply to the forward only (SURVEY C6)");
   constexpr int XW = xw<SP>(), XFORM_THREADS = 32 * XW;
@@ -527,23 +528,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   // read ~9 W panels and <= 8 activation panels and both stay L2-resident.
   // Tile n of this cluster: non-persistent = the cluster's own tile; persistent =
   // tiles cl, cl + n_cl, ... of the same raster (static schedule).
+  //
+  // Work units (persistent): the first n_tiles - tail tiles whole, then each of
+  // the last `tail` tiles split into `split` k-ranges, so the last round of a
+  // GEMM whose tile count is not a multiple of the co-resident clusters is
+  // spread over idle clusters instead of leaving them waiting (a stream-K
+  // style tail).  Split parts add fp32 partial accumulators through global
+  // memory; the last part to finish writes the tile.
+  const int nk = (Kred + BK - 1) / BK;
   const int cl = (int)(blockIdx.x >> 1), n_cl = (int)(gridDim.x >> 1);
   const int n_tiles = n_t * n_f;
-  const int my_tiles = PERSIST ? (n_tiles > cl ? (n_tiles - cl + n_cl - 1) / n_cl : 0) : 1;
-  auto coords = [&](int n, int& m0_, int& l0_) {
-    const int cid = PERSIST ? cl + n * n_cl : (int)blockIdx.y * n_f + cl;
+  const int tail = (PERSIST && split > 1) ? (n_tiles > n_cl ? n_tiles % n_cl : n_tiles) : 0;
+  const int n_full = n_tiles - tail;
+  const int n_units = n_full + tail * split;
+  const int my_units = PERSIST ? (n_units > cl ? (n_units - cl + n_cl - 1) / n_cl : 0) : 1;
+  // unit n of this cluster: features m0, tokens l0, k-steps [kb, ke), tail tile index ut (-1 =
+  // whole tile) and part
+  auto unit = [&](int n, int& m0_, int& l0_, int& kb_, int& ke_, int& ut_, int& part_) {
+    const int uid = PERSIST ? cl + n * n_cl : (int)blockIdx.y * n_f + cl;
+    int cid = uid;
+    ut_ = -1;
+    part_ = 0;
+    if (uid >= n_full) {
+      ut_ = (uid - n_full) / split;
+      part_ = (uid - n_full) - ut_ * split;
+      cid = n_full + ut_;
+    }
     const int per_group = GROUP_T * n_f;
     const int grp_ = cid / per_group, idx = cid % per_group;
     const int gt = min(GROUP_T, n_t - grp_ * GROUP_T);
     const int fp = idx / gt, tt = grp_ * GROUP_T + idx % gt;
     m0_ = fp * (2 * BM) + rank * BM;   // this CTA's features
     l0_ = tt * BNT;                    // the pair's tokens
+    kb_ = ut_ < 0 ? 0 : part_ * nk / split;
+    ke_ = ut_ < 0 ? nk : (part_ + 1) * nk / split;
   };
-  int m0, l0;
-  coords(0, m0, l0);
+  int m0, l0, kb0, ke0, ut0, pt0;
+  unit(0, m0, l0, kb0, ke0, ut0, pt0);
   // this CTA's rows of the two MMAs' B operands: tokens l0 + 128 rank .. +127
   // (N = 256 MMA) and l0 + 256 + (N2 / 2) rank .. (N = N2 MMA)
-  const int nk = (Kred + BK - 1) / BK;
 
   if (warp == W_SF) {
     // lane-parallel barrier initialisation over the flat Bar16 array (layout above):
@@ -595,11 +618,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   if (warp == W_SF) {
     // ------------------------------------------------------------ factor-ring producer (both CTAs)
     if (lane == 0) {
-      for (int n = 0, g = 0; n < my_tiles; ++n) {
-      if (PERSIST && n > 0) {
-        coords(n, m0, l0);
-        mbar_wait(ff_empty, (n - 1) & 1);   // every recompute of the previous tile committed
-      }
+      for (int n = 0, g = 0; n < my_units; ++n) {
+      int kb, ke, ut, part;
+      unit(n, m0, l0, kb, ke, ut, part);
+      if (PERSIST && n > 0) mbar_wait(ff_empty, (n - 1) & 1);   // every recompute of the previous unit committed
       mbar_arrive_expect_tx(ffull, FF);
       if (DX) {  // b [r, C] as MN-major A of the recompute: two 64-wide atoms of this CTA's columns
         tma_load_2d(ffac, &tmF, ffull, m0, 0);
@@ -607,7 +629,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       } else {   // a [R, r] K-major, this CTA's rows
         tma_load_2d(ffac, &tmF, ffull, 0, m0);
       }
-      for (int i = 0; i < nk; ++i, ++g) {
+      for (int i = kb; i < ke; ++i, ++g) {
         const int e = g % NE;
         mbar_wait(&e_empty[e].b, ((g / NE) & 1) ^ 1);
         uint8_t* st = sfr + e * SF;
@@ -622,9 +644,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   } else if (warp == W_WLOAD) {
     // ------------------------------------------------------------ W-ring producer (both CTAs)
     if (lane == 0) {
-      for (int n = 0, g = 0; n < my_tiles; ++n) {
-      if (n > 0) coords(n, m0, l0);
-      for (int i = 0; i < nk; ++i, ++g) {
+      for (int n = 0, g = 0; n < my_units; ++n) {
+      int kb, ke, ut, part;
+      unit(n, m0, l0, kb, ke, ut, part);
+      for (int i = kb; i < ke; ++i, ++g) {
         const int wi = g % NW;
         mbar_wait(&wfree[wi].b, ((g / NW) & 1) ^ 1);
         uint8_t* st = wring + wi * W_BYTES;
@@ -648,10 +671,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   } else if (warp == W_ACT) {
     // ------------------------------------------------------------ activation-ring producer (both CTAs)
     if (lane == 0) {
-      for (int n = 0, g = 0; n < my_tiles; ++n) {
-      if (n > 0) coords(n, m0, l0);
+      for (int n = 0, g = 0; n < my_units; ++n) {
+      int kb, ke, ut, part;
+      unit(n, m0, l0, kb, ke, ut, part);
       const int lh = l0 + rank * 128, lh2 = l0 + 256 + rank * (N2 / 2);
-      for (int i = 0; i < nk; ++i, ++g) {
+      for (int i = kb; i < ke; ++i, ++g) {
         const int a = g % NA;
         mbar_wait(&a_empty[a].b, ((g / NA) & 1) ^ 1);
 #ifdef LORS_EXP_NO_ACT_TMA
@@ -669,7 +693,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     cluster_wait();
     // ------------------------------------------------------------ activation relay (peer CTA)
     if (!leader && lane == 0) {
-      const int total = my_tiles * nk;
+      int total = 0;
+      for (int n = 0; n < my_units; ++n) {
+        int m_, l_, kb, ke, ut, part;
+        unit(n, m_, l_, kb, ke, ut, part);
+        total += ke - kb;
+      }
       for (int g = 0; g < total; ++g) {
         const int a = g % NA;
         mbar_wait(&mready[a].b, (g / NA) & 1);
@@ -681,10 +710,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     if (!leader) {
       // ---------------------------------------------------------- early relay (peer CTA)
       if (lane == 0) {
-        for (int n = 0, g = 0; n < my_tiles; ++n) {
+        for (int n = 0, g = 0; n < my_units; ++n) {
+          int m_, l_, kb, ke, ut, part;
+          unit(n, m_, l_, kb, ke, ut, part);
           mbar_wait(ffull, n & 1);
           mbar_arrive_cluster(pffull_l);
-          for (int i = 0; i < nk; ++i, ++g) {
+          for (int i = kb; i < ke; ++i, ++g) {
             const int e = g % NE;
             mbar_wait(&rready[e].b, (g / NE) & 1);
             mbar_arrive_cluster(rready_l + e * 16);
@@ -708,7 +739,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       const uint64_t act_desc = make_sdesc(smem_u32(actb), 16, 1024, SW_128);
       constexpr uint32_t FF_KSTEP = DX ? 2048 >> 4 : 32 >> 4;   // per K16 of the recompute
       constexpr uint32_t SF_KSTEP = DX ? 32 >> 4 : 1024 >> 4;
-      auto do_rec = [&](const int j, const int rk, const int rn) {
+      auto do_rec = [&](const int j, const int rk, const int rn, const int rlen) {
         if (rk == 0) {  // this tile's fixed factor, both CTAs
           mbar_wait(ffull, rn & 1);
           mbar_wait(pffull, rn & 1);
@@ -726,11 +757,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 #endif
           mma_commit_pair(&refull[(j % NGRP) * NE + e].b, 0x3);
           mma_commit_pair(&e_empty[e].b, 0x3);
-          if (PERSIST && rk == nk - 1) mma_commit_pair(ff_empty, 0x3);   // fixed factor may be replaced
+          if (PERSIST && rk == rlen - 1) mma_commit_pair(ff_empty, 0x3);   // fixed factor may be replaced
         }
         __syncwarp();
       };
-      auto do_main = [&](const int jm, const int mk, const int mn) {
+      auto do_main = [&](const int jm, const int mk, const int mn, const int mlen) {
         if (PERSIST && mk == 0 && mn > 0) mbar_wait(acc_empty, (mn - 1) & 1);  // previous tile drained
         const int a = jm % NA;
         mbar_wait(&mready[a].b, (jm / NA) & 1);
@@ -757,7 +788,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           }
           mma_commit_pair(&a_empty[a].b, 0x3);
           mma_commit_pair(&wempty[((jm + NA) % NGRP) * NA + a].b, 0x3);   // next writer's group
-          if (mk == nk - 1) mma_commit_pair(accf, 0x3);
+          if (mk == mlen - 1) mma_commit_pair(accf, 0x3);
         }
         __syncwarp();
       };
@@ -765,8 +796,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       // steps ahead of its main MMA and into the next tile.  At a tile boundary
       // the previous tile's last main MMA goes first (the new tile's recompute
       // waits for its fixed factor); incremental counters, no division by nk.
-      const int total = my_tiles * nk;
+      auto unit_len = [&](int n) {
+        int m_, l_, kb, ke, ut, part;
+        unit(n, m_, l_, kb, ke, ut, part);
+        return ke - kb;
+      };
+      int total = 0;
+      for (int n = 0; n < my_units; ++n) total += unit_len(n);
       int rk = 0, rn = 0, mk = 0, mn = 0;
+      int rlen = my_units > 0 ? unit_len(0) : 1, mlen = rlen;
       for (int j = 0; j < total + D; ++j) {
         const bool has_rec = j < total, has_main = j >= D;
         const bool flip = has_rec && rk == 0 && j > 0;
@@ -778,16 +816,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         if (j == 0 && lane == 0) t_ev[1] = gtimer();
 #endif
         if (flip && has_main) {
-          do_main(j - D, mk, mn);
-          if (++mk == nk) { mk = 0; ++mn; }
+          do_main(j - D, mk, mn, mlen);
+          if (++mk == mlen) { mk = 0; if (++mn < my_units) mlen = unit_len(mn); }
         }
         if (has_rec) {
-          do_rec(j, rk, rn);
-          if (++rk == nk) { rk = 0; ++rn; }
+          do_rec(j, rk, rn, rlen);
+          if (++rk == rlen) { rk = 0; if (++rn < my_units) rlen = unit_len(rn); }
         }
         if (!flip && has_main) {
-          do_main(j - D, mk, mn);
-          if (++mk == nk) { mk = 0; ++mn; }
+          do_main(j - D, mk, mn, mlen);
+          if (++mk == mlen) { mk = 0; if (++mn < my_units) mlen = unit_len(mn); }
         }
       }
     }
@@ -1000,7 +1038,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     // features 32q .. 32q+31 (feature half q >> 1), tokens hh*TSL .. of chunk c.
     constexpr int TSL = 128 / (XW / 4);              // tokens of a chunk per warp (64 or 32)
     const int hh = warp >> 2;
-    auto stage_chunk = [&](const int c, uint8_t* blk, const float (&bvals)[2][2]) {
+    // split-K partials: fragment f = (chunk, 32-token slice, 16-lane group) of this thread,
+    // 16 floats at ((f * XFORM_THREADS + tid) * 16) of the part's slot -- coalesced, and
+    // read back by the same thread of the CTA that finishes the tile
+    constexpr int PSLOT = 128 * BNT;                 // floats per CTA and part
+    const int tid_x = (int)threadIdx.x;
+    auto frag_off = [&](int c, int tb, int g16) {
+      return ((int64_t)((c * (TSL / 32) + tb / 32) * 2 + g16) * XFORM_THREADS + tid_x) * 16;
+    };
+    auto stage_chunk = [&](const int c, uint8_t* blk, const float (&bvals)[2][2], const float* const* adds,
+                           const int n_adds) {
 #pragma unroll 1
       for (int tb = 0; tb < TSL; tb += 32) {
         const int tok = hh * TSL + tb;                // token offset inside the chunk
@@ -1009,6 +1056,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         for (int g16 = 0; g16 < 2; ++g16)
           tmem_ld_16x256b_x4(tmem + ((uint32_t)(q * 32 + 16 * g16) << 16) + (uint32_t)(c * 128 + tok), v[g16]);
         tmem_ld_wait();
+        // a split tile: the sum of all its parts' partials in part order (run-to-run
+        // deterministic whichever part finished last), replacing the accumulator
+        for (int ai = 0; ai < n_adds; ++ai) {
+#pragma unroll
+          for (int g16 = 0; g16 < 2; ++g16) {
+            const float4* src = reinterpret_cast<const float4*>(adds[ai] + frag_off(c, tb, g16));
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float4 x = __ldcg(src + u);
+              const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                v[g16][4 * u + e] = __float_as_uint(ai == 0 ? xs[e] : __uint_as_float(v[g16][4 * u + e]) + xs[e]);
+            }
+          }
+        }
 #pragma unroll
         for (int g16 = 0; g16 < 2; ++g16) {
           const int F = q * 32 + 16 * g16;
@@ -1042,23 +1105,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         }
     };
     if constexpr (PERSIST) {
-      for (int n = 0, g = 0; n < my_tiles; ++n) {
-        if (n > 0) {
-          coords(n, m0, l0);
-          gm = m0 + t;
-        }
-        for (int kq = 0; kq < nk; ++kq, ++g) {
+      __shared__ int last_flag;
+      for (int n = 0, g = 0; n < my_units; ++n) {
+        int kb, ke, ut, part;
+        unit(n, m0, l0, kb, ke, ut, part);
+        gm = m0 + t;
+        for (int kq = kb; kq < ke; ++kq, ++g) {
           uint32_t p[32], wv[16], mw = 0;
           issue(g, kq, p, wv, mw);
           release(g);
           finish(g, kq, p, wv, mw);
         }
-        // -------------------------------------------------------- epilogue of tile n
-        // Staged through the W_eff ring, idle until this tile's successor is
-        // transformed: six [128 tokens][64 features] blocks in two batches of three;
-        // the accumulator is handed back to the MMA issuer after the last TMEM read.
+        // -------------------------------------------------------- epilogue of unit n
         mbar_wait(accf, n & 1);
         tc_fence_after();
+        const float* adds[4];
+        int n_adds = 0;
+        if (ut >= 0) {
+          // part of a split tile: publish this part's fp32 accumulator, then the last
+          // part to arrive (per CTA of the pair) adds the others and writes the tile
+          float* mine = partials + ((int64_t)(ut * split + part) * 2 + rank) * PSLOT;
+#pragma unroll 1
+          for (int c = 0; c < BNT / 128; ++c)
+#pragma unroll 1
+            for (int tb = 0; tb < TSL; tb += 32) {
+              uint32_t v[2][16];
+              const int tok = hh * TSL + tb;
+#pragma unroll
+              for (int g16 = 0; g16 < 2; ++g16)
+                tmem_ld_16x256b_x4(tmem + ((uint32_t)(q * 32 + 16 * g16) << 16) + (uint32_t)(c * 128 + tok), v[g16]);
+              tmem_ld_wait();
+#pragma unroll
+              for (int g16 = 0; g16 < 2; ++g16) {
+                float4* dst = reinterpret_cast<float4*>(mine + frag_off(c, tb, g16));
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                  __stcg(dst + u, make_float4(__uint_as_float(v[g16][4 * u]), __uint_as_float(v[g16][4 * u + 1]),
+                                              __uint_as_float(v[g16][4 * u + 2]), __uint_as_float(v[g16][4 * u + 3])));
+              }
+            }
+          __threadfence();
+          named_bar_sync(1, XFORM_THREADS);
+          if (threadIdx.x == 0) {
+            const unsigned int old = atomicAdd(&counters[ut * 2 + rank], 1u);
+            last_flag = old == (unsigned int)(split - 1);
+            if (last_flag) counters[ut * 2 + rank] = 0u;   // reusable without a memset
+          }
+          named_bar_sync(1, XFORM_THREADS);
+          if (!last_flag) {                                  // done: hand the accumulator back
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(acc_empty_l);
+            continue;
+          }
+          __threadfence();
+          for (int p2 = 0; p2 < split; ++p2) adds[n_adds++] = partials + ((int64_t)(ut * split + p2) * 2 + rank) * PSLOT;
+        }
+        // Staged through the W_eff ring, idle until this unit's successor is
+        // transformed: six [128 tokens][64 features] blocks in two batches of three;
+        // the accumulator is handed back to the MMA issuer after the last TMEM read.
         float bvals[2][2];
         bias_of(bvals);
 #pragma unroll 1
@@ -1066,7 +1171,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 #pragma unroll 1
           for (int c = 0; c < BNT / 128; ++c) {
             const int b = 2 * c + (q >> 1);            // block (chunk c, feature half q >> 1)
-            if (b / 3 == batch) stage_chunk(c, weff + (b % 3) * WEFF_BYTES, bvals);
+            if (b / 3 == batch) stage_chunk(c, weff + (b % 3) * WEFF_BYTES, bvals, adds, n_adds);
           }
           if (batch == 1) {
             tc_fence_before();
@@ -1189,10 +1294,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 #endif
 }
 
+// Co-resident clusters of the persistent kernel (cached per kernel once it is known;
+// 74 while no device answers, e.g. a workspace query on a host without a GPU).
+template <bool DX, int RP, bool SP>
+static int persistent_clusters() {
+  using namespace rg;
+  static int max_clusters = 0;
+  if (max_clusters > 0) return max_clusters;
+  auto kern = tc_lors_gemm_kernel<DX, RP, false, SP>;
+  const size_t smem = smem_bytes<RP, SP>();
+  int v = 0;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * (unsigned)(num_sms() / 2));
+    cfg.blockDim = dim3(threads<SP>());
+    cfg.dynamicSmemBytes = smem;
+    if (cudaOccupancyMaxActiveClusters(&v, (void*)kern, &cfg) != cudaSuccess) v = 0;
+  }
+  (void)cudaGetLastError();
+  if (v <= 0) return 74;
+  max_clusters = v;
+  return v;
+}
+
+// Tail split of the persistent walk: the n_tiles % clusters tiles of the last wave
+// are cut along K into `split` units (parts), so that the last wave is as long as
+// a part instead of a tile.  Parts publish fp32 partials; the last to finish adds.
+struct TailSplit {
+  int split = 1, tail = 0, clusters = 0;
+  size_t bytes = 0;        // workspace: tail * 2 counters, then tail * split * 2 partial slots
+  size_t counter_bytes = 0;
+};
+
+template <bool DX, int RP, bool SP>
+static TailSplit plan_tail_split(int L, int R, int C) {
+  using namespace rg;
+  TailSplit p;
+  if (!persist<SP>() || getenv("LORS_NO_TAIL_SPLIT")) return p;
+  constexpr int BNT = bnt<SP>();
+  const int Mout = DX ? C : R, Kred = DX ? R : C;
+  const int n_tiles = (int)(ceil_div(Mout, 2 * BM) * ceil_div(L, BNT)), nk = (int)ceil_div(Kred, BK);
+  const int mc = persistent_clusters<DX, RP, SP>();
+  p.clusters = mc;
+  const int tail = n_tiles > mc ? n_tiles % mc : n_tiles;
+  if (tail == 0 || 2 * tail > mc) return p;
+  // a part costs a fixed ~K = 64 k-steps' worth (partials out, the last part's
+  // dependent reads, the extra epilogue, and power the idle tail would have left
+  // to the busy SMs): measured a loss at K <= 4096 and +6..9% at K >= 11008
+  // (tools/exp_split.py), hence parts of at least 64 k-steps
+  int split = std::min(std::min(4, mc / tail), nk / 64);
+  if (split < 2) return p;
+  p.split = split;
+  p.tail = tail;
+  p.counter_bytes = ((size_t)tail * 2 * sizeof(unsigned int) + 255) / 256 * 256;
+  p.bytes = p.counter_bytes + (size_t)tail * split * 2 * 128 * BNT * sizeof(float);
+  return p;
+}
+
 template <bool DX, int RP, bool SP>
 static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const bf16* b, const bf16* bias,
                             const uint32_t* bits, const uint8_t* meta24, bf16* out, int L, int R, int C, int r,
-                            float alpha, cudaStream_t s) {
+                            float alpha, cudaStream_t s, void* ws, size_t ws_bytes) {
   using namespace rg;
   const int Mout = DX ? C : R, Kred = DX ? R : C;
   constexpr int N2 = n2<SP>(), BNT = bnt<SP>();
@@ -1217,20 +1379,21 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
                 "lors_gemm smem attribute");
   const int n_f = (int)ceil_div(Mout, 2 * BM), n_t = (int)ceil_div(L, BNT);
   dim3 grid((unsigned)(2 * n_f), (unsigned)n_t);
+  int split = 1;
+  float* partials = nullptr;
+  unsigned int* counters = nullptr;
   if (persist<SP>()) {  // one CTA pair per co-resident cluster slot, tiles walked in the raster order
-    static int max_clusters[2][3] = {};
-    int& mc = max_clusters[DX][RP == 16 ? 0 : RP == 32 ? 1 : 2];
-    if (mc == 0) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(2 * (unsigned)(num_sms() / 2));
-      cfg.blockDim = dim3(threads<SP>());
-      cfg.dynamicSmemBytes = smem;
-      int v = 0;
-      if (cudaOccupancyMaxActiveClusters(&v, (void*)kern, &cfg) != cudaSuccess || v <= 0) v = num_sms() / 2;
-      (void)cudaGetLastError();
-      mc = v;
+    const int mc = persistent_clusters<DX, RP, SP>();
+    int units = n_f * n_t;
+    const TailSplit ts = plan_tail_split<DX, RP, SP>(L, R, C);
+    if (ts.split > 1 && ts.clusters == mc && ws != nullptr && ws_bytes >= ts.bytes) {
+      split = ts.split;
+      counters = (unsigned int*)ws;
+      partials = (float*)((char*)ws + ts.counter_bytes);
+      units += ts.tail * (split - 1);
+      LORS_CUDA_TRY(cudaMemsetAsync(counters, 0, ts.counter_bytes, s), "zero tail-split counters");
     }
-    grid = dim3((unsigned)(2 * std::min(n_f * n_t, mc)));
+    grid = dim3((unsigned)(2 * std::min(units, mc)));
   }
   if (getenv("LORS_VERBOSE")) {  // diagnostics: how many clusters of this kernel fit on the GPU at once
     cudaLaunchConfig_t cfg = {};
@@ -1244,7 +1407,8 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
     (void)cudaGetLastError();
   }
   kern<<<grid, threads<SP>(), smem, s>>>(tAct, tAct2, tW, tS, tF, tOut, bias, bits, SP ? meta24 : nullptr,
-                                         (int)ceil_div(C, 32), Mout, Kred, n_t, n_f, alpha);
+                                         (int)ceil_div(C, 32), Mout, Kred, n_t, n_f, split, partials, counters,
+                                         alpha);
   LORS_CHECK_LAUNCH(DX ? "tc_lors_gemm<dx>" : "tc_lors_gemm<fwd>");
   return LORS_OK;
 }
@@ -1252,11 +1416,24 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
 template <bool DX, bool SP = false>
 static int lors_gemm(int rp, const bf16* act, const bf16* w, const bf16* a, const bf16* b, const bf16* bias,
                      const uint32_t* bits, bf16* out, int L, int R, int C, int r, float alpha, cudaStream_t s,
-                     const uint8_t* meta24 = nullptr) {
+                     void* ws, size_t ws_bytes, const uint8_t* meta24 = nullptr) {
   switch (rp) {
-    case 16: return launch_lors_gemm<DX, 16, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s);
-    case 32: return launch_lors_gemm<DX, 32, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s);
-    default: return launch_lors_gemm<DX, 64, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s);
+    case 16:
+      return launch_lors_gemm<DX, 16, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s, ws, ws_bytes);
+    case 32:
+      return launch_lors_gemm<DX, 32, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s, ws, ws_bytes);
+    default:
+      return launch_lors_gemm<DX, 64, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s, ws, ws_bytes);
+  }
+}
+
+// workspace of one lors_gemm (the tail split's counters and partials; 0 without a split)
+template <bool DX>
+static size_t lors_gemm_workspace(int rp, int L, int R, int C) {
+  switch (rp) {
+    case 16: return plan_tail_split<DX, 16, false>(L, R, C).bytes;
+    case 32: return plan_tail_split<DX, 32, false>(L, R, C).bytes;
+    default: return plan_tail_split<DX, 64, false>(L, R, C).bytes;
   }
 }
 
@@ -1533,10 +1710,22 @@ bool tc_shape_ok(int64_t R, int64_t C, int64_t r) {
   return R % 8 == 0 && C % 8 == 0 && r % 8 == 0 && r <= 64;
 }
 
-size_t tc_fwd_workspace(const lors_fwd_args*) { return 0; }
-// beyond the capi's two bf16 P / Q slots: their fp32 split-K accumulators
+// the forward's tail-split workspace (0 when the walk has no tail to split)
+size_t tc_fwd_workspace(const lors_fwd_args* a) {
+  if (a->dtype != LORS_DTYPE_BF16 || (a->flags & LORS_FLAG_SPARSE24) || a->L <= 0 || !tc_shape_ok(a->R, a->C, a->r))
+    return 0;
+  return lors_gemm_workspace<false>((int)pad_rank(a->r), (int)a->L, (int)a->R, (int)a->C);
+}
+static size_t dx_workspace(const lors_bwd_args* a) {
+  if (a->dtype != LORS_DTYPE_BF16 || (a->flags & LORS_FLAG_NO_DX) || a->L <= 0 || !tc_shape_ok(a->R, a->C, a->r))
+    return 0;
+  return lors_gemm_workspace<true>((int)pad_rank(a->r), (int)a->L, (int)a->R, (int)a->C);
+}
+// DX_ONLY: the dX GEMM's tail split alone; otherwise, beyond the capi's two bf16
+// P / Q slots: their fp32 split-K accumulators, then the dX tail split
 size_t tc_bwd_workspace(const lors_bwd_args* a) {
-  return 2 * (((size_t)a->L * (size_t)a->r * sizeof(float) + 255) / 256 * 256);
+  if (a->flags & LORS_FLAG_DX_ONLY) return dx_workspace(a);
+  return 2 * (((size_t)a->L * (size_t)a->r * sizeof(float) + 255) / 256 * 256) + dx_workspace(a);
 }
 
 int tc_fwd(const lors_fwd_args* A, cudaStream_t s) {
@@ -1558,9 +1747,10 @@ int tc_fwd(const lors_fwd_args* A, cudaStream_t s) {
       return LORS_ERR_SHAPE;
     }
     st = lors_gemm<false, true>(rp, x, w, a, b, (const bf16*)A->bias, bits, (bf16*)A->y, L, R, C, r, A->alpha, s,
-                                A->meta24);
+                                nullptr, 0, A->meta24);
   } else {
-    st = lors_gemm<false>(rp, x, w, a, b, (const bf16*)A->bias, bits, (bf16*)A->y, L, R, C, r, A->alpha, s);
+    st = lors_gemm<false>(rp, x, w, a, b, (const bf16*)A->bias, bits, (bf16*)A->y, L, R, C, r, A->alpha, s,
+                          A->workspace, A->workspace_bytes);
   }
   if (st) return st;
   if (A->flags & LORS_FLAG_EMIT_P)  // P = X_t b^T: A = X_t K-major, B = b [r, C] K-major
@@ -1577,7 +1767,11 @@ int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {
   const int rp = (int)pad_rank(r);
   int st;
   if (!(A->flags & LORS_FLAG_NO_DX)) {
-    st = tc ? lors_gemm<true>(rp, dy, w, a, b, nullptr, bits, (bf16*)A->dx, L, R, C, r, A->alpha, s)
+    // the dX tail split's workspace: all of it (DX_ONLY) or after the four rank-r slots
+    const size_t off = (A->flags & LORS_FLAG_DX_ONLY) ? 0 : 4 * (((size_t)L * r * sizeof(float) + 255) / 256 * 256);
+    const size_t dxw = dx_workspace(A);
+    void* ws = dxw && A->workspace && A->workspace_bytes >= off + dxw ? (char*)A->workspace + off : nullptr;
+    st = tc ? lors_gemm<true>(rp, dy, w, a, b, nullptr, bits, (bf16*)A->dx, L, R, C, r, A->alpha, s, ws, dxw)
             : simt_lors_gemm<bf16>(true, dy, w, bits, a, b, nullptr, (bf16*)A->dx, L, R, C, r, A->alpha, s);
     if (st) return st;
   }

@@ -316,9 +316,11 @@ def test_config2_bf16_full_size_properties(P):
     p = xf @ bf.t()
     assert _rel(da, (2.0 * dyf.t() @ p).double().cpu().numpy()) <= 2e-2
     assert _rel(db, (2.0 * (dyf @ af).t() @ xf).double().cpu().numpy()) <= 2e-2
-    # linearity in X (size-independent property)
-    y1, _ = ops.lors_fwd(x[:4096].contiguous(), w, a, b, 2.0)
-    assert torch.equal(y1, y[:4096])
+    # token-split property (size-independent), bit-exact with the tail split off
+    with _env("LORS_NO_TAIL_SPLIT", "1"):
+        y0, _ = ops.lors_fwd(x, w, a, b, 2.0)
+        y1, _ = ops.lors_fwd(x[:4096].contiguous(), w, a, b, 2.0)
+    assert torch.equal(y1, y0[:4096])
 
 
 # ---------------------------------------------------------------------------
@@ -486,5 +488,66 @@ def test_persistent_multi_tile_shapes(P, r, mask_mode, with_bias):
         assert _rel(dbias, dyf.sum(0).double().cpu().numpy()) <= 1e-3
     we = ops.effective_weight(w, a, b, 2.0, bits)
     assert bool((we[w == 0].view(torch.int16) == 0).all())
-    y2, _ = ops.lors_fwd(x[1000:].contiguous(), w, a, b, 2.0, bias, bits)
-    assert torch.equal(y2, y[1000:])
+    # token-split property (batch invariance) holds with the tail split off: a split
+    # tile sums its K parts in a different order than one continuous accumulation
+    with _env("LORS_NO_TAIL_SPLIT", "1"):
+        y1, _ = ops.lors_fwd(x, w, a, b, 2.0, bias, bits)
+        y2, _ = ops.lors_fwd(x[1000:].contiguous(), w, a, b, 2.0, bias, bits)
+    assert torch.equal(y2, y1[1000:])
+    assert _rel(y, y1.double().cpu().numpy()) <= 1e-2
+
+
+class _env:
+    def __init__(self, k, v):
+        self.k, self.v = k, v
+
+    def __enter__(self):
+        self.old = os.environ.get(self.k)
+        os.environ[self.k] = self.v
+
+    def __exit__(self, *exc):
+        if self.old is None:
+            os.environ.pop(self.k, None)
+        else:
+            os.environ[self.k] = self.old
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("L,R,C,r", [(1024, 1024, 16384, 16),     # fwd: 16 tiles, each split in 4 along K
+                                     (512, 2048, 12288, 16),      # fwd: 16 tiles, split in 3 (192 k-steps)
+                                     (4096, 4096, 11008, 64),     # fwd: 256 tiles, a 34-tile tail split in 2
+                                     (2048, 11008, 8192, 32),     # dX: 256 tiles, tail split in 2 (K = 11008)
+                                     (777, 512, 8192, 8)])        # fwd: 8 ragged tiles split in 2
+def test_tail_split_parity_and_determinism(P, L, R, C, r):
+    """Persistent walk with the last wave's tiles cut along K (fp32 partials summed
+    by the last part to finish): forward and dX against a torch fp32 reference and
+    against the unsplit walk, bit-identical from run to run."""
+    from paper_2501_08582_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(L + r)
+    w = torch.randn(R, C, device="cuda", generator=g) * 0.02
+    w = torch.where(w.abs() < 0.015, torch.zeros_like(w), w).bfloat16()
+    a = (torch.randn(R, r, device="cuda", generator=g) * 0.05).bfloat16()
+    b = (torch.randn(r, C, device="cuda", generator=g) * 0.3).bfloat16()
+    x = torch.randn(L, C, device="cuda", generator=g).bfloat16()
+    dy = torch.randn(L, R, device="cuda", generator=g).bfloat16()
+    bias = (torch.randn(R, device="cuda", generator=g) * 0.1).bfloat16()
+    wf, af, bf, xf, dyf = (t.float() for t in (w, a, b, x, dy))
+    weff = torch.where(wf != 0, wf + 2.0 * (af @ bf), torch.zeros_like(wf))
+    yref = (xf @ weff.t() + bias.float()).double().cpu().numpy()
+    dxref = (dyf @ weff).double().cpu().numpy()
+    outs = []
+    for _ in range(3):
+        y, _ = ops.lors_fwd(x, w, a, b, 2.0, bias)
+        dx = ops.lors_bwd(x, w, a, b, dy, 2.0, with_bias=True, overlap=False)[0]
+        outs.append((y, dx))
+    with _env("LORS_NO_TAIL_SPLIT", "1"):
+        y0, _ = ops.lors_fwd(x, w, a, b, 2.0, bias)
+        dx0 = ops.lors_bwd(x, w, a, b, dy, 2.0, with_bias=True, overlap=False)[0]
+    torch.cuda.synchronize()
+    for y, dx in outs[1:]:
+        assert torch.equal(y, outs[0][0]) and torch.equal(dx, outs[0][1])
+    y, dx = outs[0]
+    assert _rel(y, yref) <= 2e-2 and _rel(dx, dxref) <= 2e-2
+    # the split changes only the fp32 summation order: bf16 outputs within one ulp-ish
+    assert float((y.float() - y0.float()).abs().max()) <= 2 ** -6 * float(y0.float().abs().max())
+    assert float((dx.float() - dx0.float()).abs().max()) <= 2 ** -6 * float(dx0.float().abs().max())
