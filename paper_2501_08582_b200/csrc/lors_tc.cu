@@ -26,6 +26,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -339,6 +340,254 @@ static int skinny(int rp, const bf16* A, const bf16* B, void* out, int M, int N,
     case 16: return launch_skinny<16, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32);
     case 32: return launch_skinny<32, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32);
     default: return launch_skinny<64, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32);
+  }
+}
+
+// ===========================================================================
+// K4b: Q and dA from one pass over dY (lors_backward at_dy and da, adapters.py:397-398)
+//
+//   Q[l, :]  = sum_R dY_t[l, R] a[R, :]          (fp32, red.add; rounded to bf16 after)
+//   dA[R, :] = alpha sum_l dY_t[l, R] P[l, :]    (fp32, red.add)
+//
+// Every [128 tokens x 128 R] block of dY_t is staged once (two SW128 boxes) and
+// feeds two MMAs: read K-major it is the A operand of Q (M = tokens, K = R), read
+// MN-major it is the A operand of dA (M = R, K = tokens).  A CTA owns Tr R tiles
+// (their a slices stay resident in shared memory, their dA accumulators in TMEM)
+// and a run of token tiles (the P slice of the current one double-buffered, its Q
+// accumulator double-buffered so that the flush overlaps the next tile).
+// warps: 0 TMA producer, 1 MMA issuer + TMEM owner, 2..5 flush.
+// ===========================================================================
+namespace qd {
+constexpr int THREADS = 192, MAX_STAGES = 8;
+constexpr uint32_t BLK_BYTES = 128 * 128 * 2;   // dY block, two [128 tokens][64 R] boxes
+constexpr uint32_t A_REGION = 98304;            // at most this much of resident a slices (Tr x [128 R][BN])
+constexpr size_t SMEM_MAX = 232448;
+template <int BN>
+constexpr int tr_max() { return (int)(A_REGION / (128 * BN * 2)); }   // 24 / 12 / 6
+template <int BN>
+constexpr uint32_t slice_bytes() { return 128 * BN * 2; }
+// the dY ring takes what the resident a slices leave (3 .. 8 blocks)
+template <int BN>
+constexpr int stages(int tr) {
+  const int s = (int)((SMEM_MAX - 1024 - 512 - (size_t)(tr + 2) * slice_bytes<BN>()) / BLK_BYTES);
+  return s < MAX_STAGES ? s : MAX_STAGES;
+}
+template <int BN>
+constexpr size_t smem_bytes(int tr) { return 1024 + (size_t)(tr + 2) * slice_bytes<BN>() + stages<BN>(tr) * BLK_BYTES + 512; }
+}  // namespace qd
+
+template <int BN>
+__global__ void __launch_bounds__(qd::THREADS, 1)
+    tc_q_da_kernel(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmA,
+                   const __grid_constant__ CUtensorMap tmP, float* __restrict__ q32, float* __restrict__ da, int L,
+                   int R, int r, int tr, int tpg, int n_rg, float alpha, int dbg) {
+  using namespace qd;
+  constexpr uint32_t SL = slice_bytes<BN>();
+  constexpr uint32_t SWB = BN * 2;               // swizzle span of the a / P slices (MN-major B)
+  const int STAGES = stages<BN>(tr);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;                            // [tr] a slices
+  uint8_t* sp = sa + tr * SL;                    // [2] P slices
+  uint8_t* sdy = sp + 2 * SL;                    // [STAGES] dY blocks
+  uint64_t* full = reinterpret_cast<uint64_t*>(sdy + STAGES * BLK_BYTES);
+  uint64_t* empty = full + MAX_STAGES;
+  uint64_t* pfull = empty + MAX_STAGES;          // [2]
+  uint64_t* pempty = pfull + 2;                  // [2]
+  uint64_t* qfull = pempty + 2;                  // [2]
+  uint64_t* qempty = qfull + 2;                  // [2]
+  uint64_t* afull = qempty + 2;
+  uint64_t* dafull = afull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dafull + 1);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int n_rt = (R + 127) / 128, n_tt = (L + 127) / 128;
+  const int rg = (int)blockIdx.x % n_rg, tg = (int)blockIdx.x / n_rg;
+  const int r0 = rg * tr * 128, t0 = tg * tpg * 128;
+  const int trc = min(tr, n_rt - rg * tr);       // R tiles of this CTA
+  const int ntc = min(tpg, n_tt - tg * tpg);     // token tiles of this CTA
+  // TMEM columns: Q accumulators 0 / BN, dA accumulator of R tile j at (2 + j) BN
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&pfull[b], 1);
+      mbar_init(&pempty[b], 1);
+      mbar_init(&qfull[b], 1);
+      mbar_init(&qempty[b], 4);
+    }
+    mbar_init(afull, 1);
+    mbar_init(dafull, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tmDY);
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmP);
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (trc <= 0 || ntc <= 0) {                    // (the planner never launches empty CTAs)
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<512>(tmem);
+    return;
+  }
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(afull, (uint32_t)trc * SL);
+      for (int j = 0; j < trc; ++j) tma_load_2d(sa + j * SL, &tmA, afull, 0, r0 + 128 * j);
+      for (int ti = 0, i = 0; ti < ntc; ++ti) {
+        const int pb = ti & 1, tok = t0 + 128 * ti;
+        mbar_wait(&pempty[pb], ((ti >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&pfull[pb], SL);
+        tma_load_2d(sp + pb * SL, &tmP, &pfull[pb], 0, tok);
+        for (int j = 0; j < trc; ++j, ++i) {
+          const int s = i % STAGES;
+          mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], BLK_BYTES);
+          uint8_t* blk = sdy + s * BLK_BYTES;
+          tma_load_2d(blk, &tmDY, &full[s], r0 + 128 * j, tok);
+          tma_load_2d(blk + BLK_BYTES / 2, &tmDY, &full[s], r0 + 128 * j + 64, tok);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idq = make_idesc_bf16(128, BN, false, true);   // Q : A = dY (K = R)
+      constexpr uint32_t ida = make_idesc_bf16(128, BN, true, true);    // dA: A = dY^T (K = tokens)
+      mbar_wait(afull, 0);
+      for (int ti = 0, i = 0; ti < ntc; ++ti) {
+        const int pb = ti & 1;
+        mbar_wait(&pfull[pb], (ti >> 1) & 1);
+        mbar_wait(&qempty[pb], ((ti >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t p_base = smem_u32(sp + pb * SL);
+        for (int j = 0; j < trc; ++j, ++i) {
+          const int s = i % STAGES;
+          mbar_wait(&full[s], (i / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t blk = smem_u32(sdy + s * BLK_BYTES), a_base = smem_u32(sa + j * SL);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {   // Q += dY[128 tok x 128 R] . a[128 R x BN]
+            const uint64_t ad = make_sdesc(blk + (kk >> 2) * (BLK_BYTES / 2) + (kk & 3) * 32, 16, 1024, SW_128);
+            const uint64_t bd = make_sdesc(a_base + kk * 16 * SWB, 0, 8 * SWB, sw_layout(SWB));
+            mma_bf16(tmem + pb * BN, ad, bd, idq, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {   // dA_j += dY^T[128 R x 128 tok] . P[128 tok x BN]
+            const uint64_t ad = make_sdesc(blk + kk * 2048, BLK_BYTES / 2, 1024, SW_128);
+            const uint64_t bd = make_sdesc(p_base + kk * 16 * SWB, 0, 8 * SWB, sw_layout(SWB));
+            mma_bf16(tmem + (2 + j) * BN, ad, bd, ida, (ti > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&qfull[pb]);
+        mma_commit(&pempty[pb]);
+      }
+      mma_commit(dafull);
+    }
+  } else {
+    const int q = warp % 4;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    const int row = q * 32 + lane;
+    for (int ti = 0; ti < ntc; ++ti) {            // flush Q of token tile ti
+      const int pb = ti & 1;
+      mbar_wait(&qfull[pb], (ti >> 1) & 1);
+      tc_fence_after();
+      const int tok = t0 + 128 * ti + row;
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld_x16(lane_base + pb * BN + c0, v);
+        tmem_ld_wait();
+        if (tok < L && !(dbg & 1)) {
+          float* o = q32 + (int64_t)tok * r + c0;
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+            if (c0 + h * 4 + 4 <= r)
+              red_add_v4(o + h * 4, __uint_as_float(v[h * 4]), __uint_as_float(v[h * 4 + 1]),
+                         __uint_as_float(v[h * 4 + 2]), __uint_as_float(v[h * 4 + 3]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&qempty[pb]);
+    }
+    mbar_wait(dafull, 0);
+    tc_fence_after();
+    for (int j = 0; j < trc; ++j) {               // flush dA of the CTA's R tiles
+      const int gr = r0 + 128 * j + row;
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld_x16(lane_base + (2 + j) * BN + c0, v);
+        tmem_ld_wait();
+        if (gr < R && !(dbg & 2)) {
+          float* o = da + (int64_t)gr * r + c0;
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+            if (c0 + h * 4 + 4 <= r)
+              red_add_v4(o + h * 4, alpha * __uint_as_float(v[h * 4]), alpha * __uint_as_float(v[h * 4 + 1]),
+                         alpha * __uint_as_float(v[h * 4 + 2]), alpha * __uint_as_float(v[h * 4 + 3]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// Grid of the Q / dA pass: Tr R tiles x tpg token tiles per CTA, one CTA per SM,
+// chosen to minimise the blocks of the busiest CTA (fewer CTAs on ties: fewer
+// partial sums through the atomics).
+template <int BN>
+static int launch_q_da(const bf16* dy, const bf16* a, const bf16* p, float* q32, float* da, int L, int R, int r,
+                       float alpha, cudaStream_t s) {
+  CUtensorMap tDY, tA, tP;
+  int st;
+  if ((st = make_map(&tDY, dy, R, L, 64, 128, 128, "dY (Q / dA pass)"))) return st;
+  if ((st = make_map(&tA, a, r, R, BN, 128, BN * 2, "a slices (Q / dA pass)"))) return st;
+  if ((st = make_map(&tP, p, r, L, BN, 128, BN * 2, "P slices (Q / dA pass)"))) return st;
+  const int n_rt = (int)ceil_div(R, 128), n_tt = (int)ceil_div(L, 128), nsm = num_sms();
+  // R groups ~ sqrt(SMs x R tiles / token tiles): balances the Q partials (one per R
+  // group and token) against the dA partials (one per token group and R row), the
+  // two atomic streams; measured within ~5% of the best forced Tr (tools/exp_qda_sweep.py)
+  const int trm = std::min(qd::tr_max<BN>(), n_rt);
+  const int n_rg0 = std::max(1, (int)std::lround(std::sqrt((double)nsm * n_rt / n_tt)));
+  int best_tr = std::max(1, std::min(trm, (int)ceil_div(n_rt, n_rg0)));
+  if (const char* force = getenv("LORS_QDA_TR")) best_tr = std::max(1, std::min(atoi(force), trm));  // experiments
+  while ((int)ceil_div(n_rt, best_tr) > nsm && best_tr < trm) ++best_tr;   // q_da_fits() holds
+  const int best_tpg = (int)ceil_div(n_tt, std::min(n_tt, std::max(1, nsm / (int)ceil_div(n_rt, best_tr))));
+  const int n_rg = (int)ceil_div(n_rt, best_tr);
+  const int ctas = n_rg * (int)ceil_div(n_tt, best_tpg);
+  auto kern = tc_q_da_kernel<BN>;
+  const size_t smem = qd::smem_bytes<BN>(best_tr);
+  LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                "q_da smem attribute");
+  static const int dbg = getenv("LORS_QDA_DBG") ? atoi(getenv("LORS_QDA_DBG")) : 0;
+  kern<<<ctas, qd::THREADS, smem, s>>>(tDY, tA, tP, q32, da, L, R, r, best_tr, best_tpg, n_rg, alpha, dbg);
+  LORS_CHECK_LAUNCH("tc_q_da");
+  return LORS_OK;
+}
+
+// whether one wave of CTAs covers R at the largest Tr (else the separate skinny GEMMs run)
+static bool q_da_fits(int rp, int R) {
+  const int trm = rp == 16 ? qd::tr_max<16>() : rp == 32 ? qd::tr_max<32>() : qd::tr_max<64>();
+  return ceil_div(R, 128) <= (int64_t)num_sms() * trm;
+}
+
+static int q_da(int rp, const bf16* dy, const bf16* a, const bf16* p, float* q32, float* da, int L, int R, int r,
+                float alpha, cudaStream_t s) {
+  switch (rp) {
+    case 16: return launch_q_da<16>(dy, a, p, q32, da, L, R, r, alpha, s);
+    case 32: return launch_q_da<32>(dy, a, p, q32, da, L, R, r, alpha, s);
+    default: return launch_q_da<64>(dy, a, p, q32, da, L, R, r, alpha, s);
   }
 }
 
@@ -1792,6 +2041,24 @@ int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {
         P = (bf16*)A->workspace;
         if ((st = skinny<false, false, 0>(rp, x, b, P, L, r, C, r, 1.0f, true, s, P32))) return st;
       }
+      static const bool fused_q_da = getenv("LORS_NO_QDA_PASS") == nullptr;
+      if (fused_q_da && q_da_fits(rp, R)) {
+        // P rounded first; then Q and dA from one pass over dY (K4b), Q rounded; dB
+        LORS_CUDA_TRY(cudaMemsetAsync(A->da, 0, sizeof(float) * (size_t)R * r, s), "zero dA");
+        if (need_p) {
+          const int64_t na4 = (int64_t)L * r / 4;
+          f32_to_bf16_pair_kernel<<<(unsigned)ceil_div(na4, 256), 256, 0, s>>>((const float4*)P32, P, na4, nullptr,
+                                                                               nullptr, 0);
+          LORS_CHECK_LAUNCH("P fp32 -> bf16");
+        }
+        if ((st = q_da(rp, dy, a, P, Q32, A->da, L, R, r, A->alpha, s))) return st;
+        const int64_t nb4 = (int64_t)L * r / 4;
+        f32_to_bf16_pair_kernel<<<(unsigned)ceil_div(nb4, 256), 256, 0, s>>>(nullptr, nullptr, 0,
+                                                                             (const float4*)Q32, Q, nb4);
+        LORS_CHECK_LAUNCH("Q fp32 -> bf16");
+        if ((st = skinny<true, true, 2>(rp, x, Q, A->db, C, r, L, C, A->alpha, true, s))) return st;
+        goto rank_r_done;
+      }
       // Q = dY_t a: A = dY_t K-major [L, R], B = a [R, r] MN-major
       if ((st = skinny<false, true, 0>(rp, dy, a, Q, L, r, R, r, 1.0f, true, s, Q32))) return st;
       {
@@ -1804,6 +2071,7 @@ int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {
       if ((st = skinny<true, true, 1>(rp, dy, P, A->da, R, r, L, r, A->alpha, true, s))) return st;
       // dB^T = alpha X_t^T Q: A = X_t MN-major (m = C), B = Q MN-major; stored transposed into dB [r, C]
       if ((st = skinny<true, true, 2>(rp, x, Q, A->db, C, r, L, C, A->alpha, true, s))) return st;
+    rank_r_done:;
     } else {
       if (P == nullptr) {
         P = (bf16*)A->workspace;

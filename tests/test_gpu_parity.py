@@ -551,3 +551,37 @@ def test_tail_split_parity_and_determinism(P, L, R, C, r):
     # the split changes only the fp32 summation order: bf16 outputs within one ulp-ish
     assert float((y.float() - y0.float()).abs().max()) <= 2 ** -6 * float(y0.float().abs().max())
     assert float((dx.float() - dx0.float()).abs().max()) <= 2 ** -6 * float(dx0.float().abs().max())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("L,R,C,r", [(1000, 3000, 512, 24), (4096, 11008, 1024, 64), (300, 256, 256, 16)])
+def test_q_da_pass_partitions(P, L, R, C, r):
+    """The one-pass Q / dA kernel (K4b) under different R-group sizes (ragged tokens
+    and rows, one to many groups): dA / dB against a torch fp32 reference of
+    lors_backward's da / db (adapters.py:396-399)."""
+    from paper_2501_08582_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(L + R + r)
+    w = (torch.randn(R, C, device="cuda", generator=g) * 0.02).bfloat16()
+    a = (torch.randn(R, r, device="cuda", generator=g) * 0.05).bfloat16()
+    b = (torch.randn(r, C, device="cuda", generator=g) * 0.3).bfloat16()
+    x = torch.randn(L, C, device="cuda", generator=g).bfloat16()
+    dy = torch.randn(L, R, device="cuda", generator=g).bfloat16()
+    af, bf, xf, dyf = (t.float() for t in (a, b, x, dy))
+    p = (xf @ bf.t()).bfloat16().float()          # P rounded to bf16 as the kernel path does
+    q = (dyf @ af).bfloat16().float()
+    da_ref = (2.0 * dyf.t() @ p).double().cpu().numpy()
+    db_ref = (2.0 * q.t() @ xf).double().cpu().numpy()
+    for tr in (None, "1", "2", "5", "24"):
+        with _env("LORS_QDA_TR", tr) if tr else _nullenv():
+            _, da, db, _ = ops.lors_bwd(x, w, a, b, dy, 2.0, need_dx=False, overlap=False)
+        torch.cuda.synchronize()
+        assert _rel(da, da_ref) <= 1e-3, tr
+        assert _rel(db, db_ref) <= 1e-2, tr
+
+
+class _nullenv:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
