@@ -91,17 +91,17 @@ static CUtensorMapSwizzle to_swizzle(uint32_t bytes) {
 
 // 2-D bf16 tensor [outer, inner] row-major (row stride = inner elements).
 static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
-                    uint32_t box_outer, uint32_t swizzle_bytes, const char* what) {
+                    uint32_t box_outer, uint32_t swizzle_bytes, const char* what, bool f32 = false) {
   PFN_encodeTiled_t fn = encode_fn();
   if (fn == nullptr) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return LORS_ERR_CUDA;
   }
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {inner * sizeof(bf16)};
+  cuuint64_t strides[1] = {inner * (f32 ? sizeof(float) : sizeof(bf16))};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+  CUresult r = fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, to_swizzle(swizzle_bytes), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -354,33 +354,49 @@ static int skinny(int rp, const bf16* A, const bf16* B, void* out, int M, int N,
 // MN-major it is the A operand of dA (M = R, K = tokens).  A CTA owns Tr R tiles
 // (their a slices stay resident in shared memory, their dA accumulators in TMEM)
 // and a run of token tiles (the P slice of the current one double-buffered, its Q
-// accumulator double-buffered so that the flush overlaps the next tile).
+// accumulator double-buffered so that the flush overlaps the next tile).  Partial
+// Q / dA tiles leave through a swizzled fp32 staging box and a TMA bulk reduce-add
+// (one instruction per tile instead of a red.add per thread and row).
 // warps: 0 TMA producer, 1 MMA issuer + TMEM owner, 2..5 flush.
 // ===========================================================================
 namespace qd {
-constexpr int THREADS = 192, MAX_STAGES = 8;
+constexpr int THREADS = 192, MAX_STAGES = 8, MIN_STAGES = 3;
 constexpr uint32_t BLK_BYTES = 128 * 128 * 2;   // dY block, two [128 tokens][64 R] boxes
-constexpr uint32_t A_REGION = 98304;            // at most this much of resident a slices (Tr x [128 R][BN])
 constexpr size_t SMEM_MAX = 232448;
 template <int BN>
-constexpr int tr_max() { return (int)(A_REGION / (128 * BN * 2)); }   // 24 / 12 / 6
+constexpr int tr_tmem() { return 512 / BN - 2; }                      // 30 / 14 / 6 (TMEM columns)
 template <int BN>
 constexpr uint32_t slice_bytes() { return 128 * BN * 2; }
-// the dY ring takes what the resident a slices leave (3 .. 8 blocks)
+// fp32 staging of one [128 rows][BN] accumulator for the TMA reduce-add: SW128
+// boxes of [128 rows][32 floats] (one for BN <= 32)
+template <int BN>
+constexpr uint32_t stage_out_bytes() { return BN <= 32 ? 16384 : 32768; }
+template <int BN>
+constexpr size_t fixed_bytes(int tr) {
+  return 1024 + (size_t)(tr + 2) * slice_bytes<BN>() + stage_out_bytes<BN>() + 512;
+}
+// the dY ring takes what the resident a slices, P and the staging leave
 template <int BN>
 constexpr int stages(int tr) {
-  const int s = (int)((SMEM_MAX - 1024 - 512 - (size_t)(tr + 2) * slice_bytes<BN>()) / BLK_BYTES);
+  const int s = (int)((SMEM_MAX - fixed_bytes<BN>(tr)) / BLK_BYTES);
   return s < MAX_STAGES ? s : MAX_STAGES;
 }
 template <int BN>
-constexpr size_t smem_bytes(int tr) { return 1024 + (size_t)(tr + 2) * slice_bytes<BN>() + stages<BN>(tr) * BLK_BYTES + 512; }
+constexpr int tr_max() {   // TMEM- and shared-memory-bound (keeps MIN_STAGES blocks in flight)
+  int t = tr_tmem<BN>();
+  while (t > 1 && stages<BN>(t) < MIN_STAGES) --t;
+  return t;
+}
+template <int BN>
+constexpr size_t smem_bytes(int tr) { return fixed_bytes<BN>(tr) + stages<BN>(tr) * BLK_BYTES; }
 }  // namespace qd
 
 template <int BN>
 __global__ void __launch_bounds__(qd::THREADS, 1)
     tc_q_da_kernel(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmA,
-                   const __grid_constant__ CUtensorMap tmP, float* __restrict__ q32, float* __restrict__ da, int L,
-                   int R, int r, int tr, int tpg, int n_rg, float alpha, int dbg) {
+                   const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
+                   const __grid_constant__ CUtensorMap tmDA, int L, int R, int r, int tr, int tpg, int n_rg,
+                   float alpha, int dbg) {
   using namespace qd;
   constexpr uint32_t SL = slice_bytes<BN>();
   constexpr uint32_t SWB = BN * 2;               // swizzle span of the a / P slices (MN-major B)
@@ -389,7 +405,8 @@ __global__ void __launch_bounds__(qd::THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;                            // [tr] a slices
   uint8_t* sp = sa + tr * SL;                    // [2] P slices
-  uint8_t* sdy = sp + 2 * SL;                    // [STAGES] dY blocks
+  uint8_t* sout = sp + 2 * SL;                   // fp32 staging of a Q / dA tile (SW128 boxes)
+  uint8_t* sdy = sout + stage_out_bytes<BN>();   // [STAGES] dY blocks
   uint64_t* full = reinterpret_cast<uint64_t*>(sdy + STAGES * BLK_BYTES);
   uint64_t* empty = full + MAX_STAGES;
   uint64_t* pfull = empty + MAX_STAGES;          // [2]
@@ -492,60 +509,68 @@ __global__ void __launch_bounds__(qd::THREADS, 1)
       mma_commit(dafull);
     }
   } else {
+    // Flush: each thread owns one accumulator row (TMEM lane); the row's floats go
+    // to the SW128 staging boxes (chunk j of row t at chunk j ^ (t & 7): the eight
+    // rows of a bank group land in different banks), then one thread adds the
+    // whole tile into global memory with a TMA bulk reduce (full-line L2 atomics,
+    // rows / columns outside the tensor skipped by the tensor map).
     const int q = warp % 4;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     const int row = q * 32 + lane;
-    for (int ti = 0; ti < ntc; ++ti) {            // flush Q of token tile ti
+    const bool issuer = warp == 2 && lane == 0;
+    auto stage = [&](const uint32_t col, const float scale) {
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld_x16(lane_base + col + c0, v);
+        tmem_ld_wait();
+        uint8_t* box = sout + (c0 >> 5) * 16384 + row * 128;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = ((c0 & 31) >> 2) + u;
+          float4 f = make_float4(scale * __uint_as_float(v[4 * u]), scale * __uint_as_float(v[4 * u + 1]),
+                                 scale * __uint_as_float(v[4 * u + 2]), scale * __uint_as_float(v[4 * u + 3]));
+          *reinterpret_cast<float4*>(box + ((j ^ (row & 7)) << 4)) = f;
+        }
+      }
+      fence_proxy_async_smem();
+    };
+    auto reduce_out = [&](const CUtensorMap* m, int row0) {   // after the staging barrier
+      if (issuer) {
+        tma_reduce_add_2d(m, sout, 0, row0);
+        if (BN > 32) tma_reduce_add_2d(m, sout + 16384, 32, row0);
+        tma_store_commit();
+        tma_store_wait_all();                     // staging reusable (smem read done)
+      }
+    };
+    for (int ti = 0; ti < ntc; ++ti) {            // Q of token tile ti
       const int pb = ti & 1;
       mbar_wait(&qfull[pb], (ti >> 1) & 1);
       tc_fence_after();
-      const int tok = t0 + 128 * ti + row;
-#pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld_x16(lane_base + pb * BN + c0, v);
-        tmem_ld_wait();
-        if (tok < L && !(dbg & 1)) {
-          float* o = q32 + (int64_t)tok * r + c0;
-#pragma unroll
-          for (int h = 0; h < 4; ++h)
-            if (c0 + h * 4 + 4 <= r)
-              red_add_v4(o + h * 4, __uint_as_float(v[h * 4]), __uint_as_float(v[h * 4 + 1]),
-                         __uint_as_float(v[h * 4 + 2]), __uint_as_float(v[h * 4 + 3]));
-        }
-      }
+      stage(pb * BN, 1.0f);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&qempty[pb]);
+      if (lane == 0) mbar_arrive(&qempty[pb]);    // accumulator read: MMA may reuse it
+      named_bar_sync(1, 128);
+      if (!(dbg & 1)) reduce_out(&tmQ, t0 + 128 * ti);
+      named_bar_sync(1, 128);
     }
     mbar_wait(dafull, 0);
     tc_fence_after();
-    for (int j = 0; j < trc; ++j) {               // flush dA of the CTA's R tiles
-      const int gr = r0 + 128 * j + row;
-#pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld_x16(lane_base + (2 + j) * BN + c0, v);
-        tmem_ld_wait();
-        if (gr < R && !(dbg & 2)) {
-          float* o = da + (int64_t)gr * r + c0;
-#pragma unroll
-          for (int h = 0; h < 4; ++h)
-            if (c0 + h * 4 + 4 <= r)
-              red_add_v4(o + h * 4, alpha * __uint_as_float(v[h * 4]), alpha * __uint_as_float(v[h * 4 + 1]),
-                         alpha * __uint_as_float(v[h * 4 + 2]), alpha * __uint_as_float(v[h * 4 + 3]));
-        }
-      }
+    for (int j = 0; j < trc; ++j) {               // dA of the CTA's R tiles
+      stage((2 + j) * BN, alpha);
+      named_bar_sync(1, 128);
+      if (!(dbg & 2)) reduce_out(&tmDA, r0 + 128 * j);
+      named_bar_sync(1, 128);
     }
+    if (issuer) tma_store_wait_done();            // the reductions landed in global memory
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
-// Grid of the Q / dA pass: Tr R tiles x tpg token tiles per CTA, one CTA per SM,
-// chosen to minimise the blocks of the busiest CTA (fewer CTAs on ties: fewer
-// partial sums through the atomics).
+// Grid of the Q / dA pass: Tr R tiles x tpg token tiles per CTA, one CTA per SM.
 template <int BN>
 static int launch_q_da(const bf16* dy, const bf16* a, const bf16* p, float* q32, float* da, int L, int R, int r,
                        float alpha, cudaStream_t s) {
@@ -554,14 +579,23 @@ static int launch_q_da(const bf16* dy, const bf16* a, const bf16* p, float* q32,
   if ((st = make_map(&tDY, dy, R, L, 64, 128, 128, "dY (Q / dA pass)"))) return st;
   if ((st = make_map(&tA, a, r, R, BN, 128, BN * 2, "a slices (Q / dA pass)"))) return st;
   if ((st = make_map(&tP, p, r, L, BN, 128, BN * 2, "P slices (Q / dA pass)"))) return st;
+  CUtensorMap tQ, tDA;   // fp32 outputs, reduce-added in [128 rows][32 floats] SW128 boxes
+  if ((st = make_map(&tQ, q32, r, L, 32, 128, 128, "Q fp32 (Q / dA pass)", true))) return st;
+  if ((st = make_map(&tDA, da, r, R, 32, 128, 128, "dA fp32 (Q / dA pass)", true))) return st;
   const int n_rt = (int)ceil_div(R, 128), n_tt = (int)ceil_div(L, 128), nsm = num_sms();
-  // R groups ~ sqrt(SMs x R tiles / token tiles): balances the Q partials (one per R
-  // group and token) against the dA partials (one per token group and R row), the
-  // two atomic streams; measured within ~5% of the best forced Tr (tools/exp_qda_sweep.py)
+  // Tr minimising the blocks of the busiest CTA (the main loop streams ~27 GB/s per
+  // SM whatever the rank; the TMA reductions of the partials are cheap); ties go to
+  // the smallest Tr >= 2 (longer token runs per CTA, a shorter dA flush at the end).
+  // Forced Tr: LORS_QDA_TR (experiments, tools/exp_qda_sweep.py).
   const int trm = std::min(qd::tr_max<BN>(), n_rt);
-  const int n_rg0 = std::max(1, (int)std::lround(std::sqrt((double)nsm * n_rt / n_tt)));
-  int best_tr = std::max(1, std::min(trm, (int)ceil_div(n_rt, n_rg0)));
-  if (const char* force = getenv("LORS_QDA_TR")) best_tr = std::max(1, std::min(atoi(force), trm));  // experiments
+  int best_tr = trm, best_work = INT32_MAX;
+  for (int tr = trm; tr >= 1; --tr) {
+    const int n_rg = (int)ceil_div(n_rt, tr);
+    if (n_rg > nsm) break;
+    const int tpg = (int)ceil_div(n_tt, std::min(n_tt, std::max(1, nsm / n_rg)));
+    if (tr * tpg < best_work || (tr * tpg == best_work && tr >= 2)) best_tr = tr, best_work = tr * tpg;
+  }
+  if (const char* force = getenv("LORS_QDA_TR")) best_tr = std::max(1, std::min(atoi(force), trm));
   while ((int)ceil_div(n_rt, best_tr) > nsm && best_tr < trm) ++best_tr;   // q_da_fits() holds
   const int best_tpg = (int)ceil_div(n_tt, std::min(n_tt, std::max(1, nsm / (int)ceil_div(n_rt, best_tr))));
   const int n_rg = (int)ceil_div(n_rt, best_tr);
@@ -571,7 +605,7 @@ static int launch_q_da(const bf16* dy, const bf16* a, const bf16* p, float* q32,
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "q_da smem attribute");
   static const int dbg = getenv("LORS_QDA_DBG") ? atoi(getenv("LORS_QDA_DBG")) : 0;
-  kern<<<ctas, qd::THREADS, smem, s>>>(tDY, tA, tP, q32, da, L, R, r, best_tr, best_tpg, n_rg, alpha, dbg);
+  kern<<<ctas, qd::THREADS, smem, s>>>(tDY, tA, tP, tQ, tDA, L, R, r, best_tr, best_tpg, n_rg, alpha, dbg);
   LORS_CHECK_LAUNCH("tc_q_da");
   return LORS_OK;
 }
