@@ -1341,19 +1341,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         tmem_ld_wait();
         // a split tile: the sum of all its parts' partials in part order (run-to-run
         // deterministic whichever part finished last), replacing the accumulator
-        for (int ai = 0; ai < n_adds; ++ai) {
+        // (two parts: all 16 loads issued before the first add, one L2 round trip)
+        if (n_adds == 2) {
+          float4 x0[2][4], x1[2][4];
 #pragma unroll
-          for (int g16 = 0; g16 < 2; ++g16) {
-            const float4* src = reinterpret_cast<const float4*>(adds[ai] + frag_off(c, tb, g16));
+          for (int g16 = 0; g16 < 2; ++g16)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const float4 x = __ldcg(src + u);
-              const float xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                v[g16][4 * u + e] = __float_as_uint(ai == 0 ? xs[e] : __uint_as_float(v[g16][4 * u + e]) + xs[e]);
+              x0[g16][u] = __ldcg(reinterpret_cast<const float4*>(adds[0] + frag_off(c, tb, g16)) + u);
+              x1[g16][u] = __ldcg(reinterpret_cast<const float4*>(adds[1] + frag_off(c, tb, g16)) + u);
             }
-          }
+#pragma unroll
+          for (int g16 = 0; g16 < 2; ++g16)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              v[g16][4 * u] = __float_as_uint(x0[g16][u].x + x1[g16][u].x);
+              v[g16][4 * u + 1] = __float_as_uint(x0[g16][u].y + x1[g16][u].y);
+              v[g16][4 * u + 2] = __float_as_uint(x0[g16][u].z + x1[g16][u].z);
+              v[g16][4 * u + 3] = __float_as_uint(x0[g16][u].w + x1[g16][u].w);
+            }
         }
 #pragma unroll
         for (int g16 = 0; g16 < 2; ++g16) {
@@ -1402,7 +1408,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         // -------------------------------------------------------- epilogue of unit n
         mbar_wait(accf, n & 1);
         tc_fence_after();
-        const float* adds[4];
+        const float* adds[2];
         int n_adds = 0;
         if (ut >= 0) {
           // part of a split tile: publish this part's fp32 accumulator, then the last
@@ -1621,11 +1627,13 @@ static TailSplit plan_tail_split(int L, int R, int C) {
   p.clusters = mc;
   const int tail = n_tiles > mc ? n_tiles % mc : n_tiles;
   if (tail == 0 || 2 * tail > mc) return p;
-  // a part costs a fixed ~K = 64 k-steps' worth (partials out, the last part's
-  // dependent reads, the extra epilogue, and power the idle tail would have left
-  // to the busy SMs): measured a loss at K <= 4096 and +6..9% at K >= 11008
-  // (tools/exp_split.py), hence parts of at least 64 k-steps
-  int split = std::min(std::min(4, mc / tail), nk / 64);
+  // two parts when the tail fits twice and each part keeps enough k-steps to cover
+  // its fixed cost (partials out, the last part's reads, the extra epilogue, and the
+  // power the idle tail would have left to the busy SMs): measured a loss with 32
+  // k-steps per part (K = 4096) and +6..14% with >= 86 (K >= 11008), tools/exp_split.py;
+  // LORS_SPLIT_MIN_KSTEPS for experiments
+  static const int min_ksteps = getenv("LORS_SPLIT_MIN_KSTEPS") ? atoi(getenv("LORS_SPLIT_MIN_KSTEPS")) : 64;
+  const int split = (2 * tail <= mc && nk >= 2 * min_ksteps) ? 2 : 1;
   if (split < 2) return p;
   p.split = split;
   p.tail = tail;

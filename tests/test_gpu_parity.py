@@ -513,11 +513,12 @@ class _env:
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("L,R,C,r", [(1024, 1024, 16384, 16),     # fwd: 16 tiles, each split in 4 along K
-                                     (512, 2048, 12288, 16),      # fwd: 16 tiles, split in 3 (192 k-steps)
-                                     (4096, 4096, 11008, 64),     # fwd: 256 tiles, a 34-tile tail split in 2
-                                     (2048, 11008, 8192, 32),     # dX: 256 tiles, tail split in 2 (K = 11008)
-                                     (777, 512, 8192, 8)])        # fwd: 8 ragged tiles split in 2
+@pytest.mark.parametrize("L,R,C,r", [(1024, 1024, 16384, 16),     # fwd: 16 tiles, each split in 2 along K
+                                     (512, 2048, 12288, 16),      # fwd: 16 tiles split
+                                     (4096, 4096, 11008, 64),     # fwd: 176 tiles, a 28-tile tail split
+                                     (2048, 11008, 8192, 32),     # dX: 176 tiles, tail split (K = 11008)
+                                     (4096, 4096, 4096, 16),      # 176 tiles at K = 4096 (64 k-steps)
+                                     (777, 512, 8192, 8)])        # fwd: 8 ragged tiles split
 def test_tail_split_parity_and_determinism(P, L, R, C, r):
     """Persistent walk with the last wave's tiles cut along K (fp32 partials summed
     by the last part to finish): forward and dX against a torch fp32 reference and
