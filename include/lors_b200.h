@@ -71,9 +71,10 @@ typedef enum { LORS_GRAD_STE = 0, LORS_GRAD_MASKED = 1 } lors_grad_mode_t;
                                         (W must be 2:4 along C; bf16; C % 64 == 0) */
 #define LORS_FLAG_NO_DX (1u << 2)    /* backward skips dX (first layer)        */
 #define LORS_FLAG_DX_ONLY (1u << 3)  /* backward computes dX only (da, db,     */
-                                     /* dbias may be NULL; no workspace) -- the */
-                                     /* caller runs the rank-r part separately, */
-                                     /* e.g. on a second stream, with NO_DX     */
+                                     /* dbias may be NULL; workspace only for   */
+                                     /* the dX GEMM's tail split) -- the caller */
+                                     /* runs the rank-r part separately, e.g.   */
+                                     /* on a second stream, with NO_DX          */
 #define LORS_FLAG_FAULT_DA_SIGN (1u << 30) /* negative control: flip dA sign,
                                               mirrors FAULT_INJECTION
                                               "lors_backward_sign_flip"
@@ -126,6 +127,9 @@ typedef struct lors_bwd_args {
 /* Forward: Y_t = X_t . W_eff^T (+ bias), W_eff = select(M, W + alpha a b, +0)
  * built tile by tile on chip and never written to HBM. */
 int lors_fwd(const lors_fwd_args* args, void* stream);
+/* Bytes of device workspace lors_fwd can use (0 = none): fp32 partials and
+ * counters of the persistent walk's tail split along K.  A call given less
+ * (or NULL) runs without the split; results differ only in fp32 summation order. */
 size_t lors_fwd_workspace(const lors_fwd_args* args);
 
 /* Backward: dX_t = dY_t . W_eff (recomputed tiles); STE: dA = alpha dY^T P,
