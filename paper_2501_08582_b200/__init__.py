@@ -12,6 +12,6 @@ from .adapters import (
     counted_saved, lors_backward, lors_forward, make_layer, mask_matrix, merge, merged_weight, predict_cost,
     sqft_gc_backward, sqft_gc_forward, variant_backward, variant_forward,
 )
-from .module import LoRSFunction, LoRSLinear, LoRSParams
+from .module import LoRSFunction, LoRSGroupFunction, LoRSLinear, LoRSParams, lors_group
 
 __version__ = "0.1.0"

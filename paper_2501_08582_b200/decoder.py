@@ -27,7 +27,7 @@ from torch import nn
 
 from . import ops
 from .errors import ArgumentError
-from .module import LoRSLinear
+from .module import LoRSLinear, groupable, lors_group
 from .prune import prune_rowwise, prune_two_four
 
 PROJECTIONS = ("q", "k", "v", "o", "gate", "up", "down")
@@ -215,14 +215,19 @@ class DecoderLayer(nn.Module):
         cfg, p = self.cfg, self.proj
         B, S, _ = h.shape
         x = self.attn_norm(h)
-        q = rope_heads(p["q"](x).view(B, S, cfg.n_heads, cfg.head_dim), cos, sin)
-        k = rope_heads(p["k"](x).view(B, S, cfg.n_kv_heads, cfg.head_dim), cos, sin)
-        v = p["v"](x).view(B, S, cfg.n_kv_heads, cfg.head_dim).transpose(1, 2)
+        qkv = [p["q"], p["k"], p["v"]]
+        # projections of one input as one node: concurrent GEMMs, one summed dX
+        qo, ko, vo = lors_group(qkv, x) if groupable(qkv) else (m(x) for m in qkv)
+        q = rope_heads(qo.view(B, S, cfg.n_heads, cfg.head_dim), cos, sin)
+        k = rope_heads(ko.view(B, S, cfg.n_kv_heads, cfg.head_dim), cos, sin)
+        v = vo.view(B, S, cfg.n_kv_heads, cfg.head_dim).transpose(1, 2)
         att = F.scaled_dot_product_attention(q, k, v, is_causal=True,
                                              enable_gqa=cfg.n_kv_heads != cfg.n_heads)
         h = h + p["o"](att.transpose(1, 2).reshape(B, S, cfg.dim))
         x = self.mlp_norm(h)
-        return h + p["down"](swiglu(p["gate"](x), p["up"](x)))
+        gu = [p["gate"], p["up"]]
+        g, u = lors_group(gu, x) if groupable(gu) else (m(x) for m in gu)
+        return h + p["down"](swiglu(g, u))
 
 
 def lors_factory(cfg: DecoderConfig, a_std: float = 1e-3, b_std: Optional[float] = None,

@@ -13,6 +13,7 @@ adapters.py:372).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -99,6 +100,127 @@ class LoRSFunction(torch.autograd.Function):
         grad_a = da.to(lora_A.dtype) if ctx.needs_input_grad[3] else None
         grad_b = db.to(lora_B.dtype) if ctx.needs_input_grad[4] else None
         return grad_x, None, grad_bias, grad_a, grad_b, None
+
+
+class LoRSGroupFunction(torch.autograd.Function):
+    """Several LoRS projections of one input (q / k / v, gate / up) as one autograd
+    node.  Forward: the GEMMs run on concurrent high-priority streams, so the CTA
+    pairs a GEMM leaves idle in its last, partial round start the next GEMM's tiles
+    (a persistent kernel's pairs exit as their static tile lists end, lowest pair
+    index = most tiles first).  Backward: the dX GEMMs run the same way, the
+    rank-r products of every projection on a normal-priority stream, and the
+    input gradient is their sum (one add per extra projection, in projection order).
+    Per projection the arithmetic is LoRSFunction's (lors_forward / lors_backward,
+    adapters.py:359-406)."""
+
+    @staticmethod
+    def forward(ctx, x, params_list, *tensors):
+        n = len(params_list)
+        weights, biases, As, Bs = tensors[0::4], tensors[1::4], tensors[2::4], tensors[3::4]
+        in_f = weights[0].shape[1]
+        dt = weights[0].dtype
+        if x.shape[-1] != in_f:
+            raise ShapeError(f"layer expects {in_f} input features, got {x.shape[-1]}")
+        shape = x.shape
+        x2 = x.reshape(-1, in_f)
+        if x2.dtype != dt:
+            x2 = x2.to(dt)
+        x2 = x2.contiguous()
+        dev = x2.device
+        # every main-stream producer (casts, compute copies) is enqueued before the fork
+        ab = [(compute_copy(As[i], dt), compute_copy(Bs[i], dt)) for i in range(n)]
+        bc = [None if biases[i] is None else biases[i].detach().to(dt).contiguous() for i in range(n)]
+        main = torch.cuda.current_stream(dev)
+        streams, _ = ops.group_streams(dev, n)
+        fork = torch.cuda.Event()
+        fork.record(main)
+        keep, outs = [], []
+        for i, prm in enumerate(params_list):
+            streams[i].wait_event(fork)
+            y, _ = ops.lors_fwd(x2, weights[i], ab[i][0], ab[i][1], prm.alpha, bc[i], prm.mask_bits,
+                                sparse24=prm.sparse24, meta24=prm.meta24 if prm.sparse24 else None,
+                                launch_stream=streams[i], keep=keep)
+            outs.append(y.view(*shape[:-1], weights[i].shape[0]))
+        for i in range(n):
+            ev = torch.cuda.Event()
+            ev.record(streams[i])
+            main.wait_event(ev)
+        # keep / ab / bc were allocated on the main stream and are released after the
+        # joins are enqueued there, so no later main-stream reuse can overtake the GEMMs
+        ctx.save_for_backward(x2)
+        ctx.lors = (weights, As, Bs, tuple(b is not None for b in biases), params_list, shape, x.dtype)
+        return tuple(outs)
+
+    @staticmethod
+    def backward(ctx, *grads):
+        weights, As, Bs, has_bias, params_list, x_shape, x_dtype = ctx.lors
+        (x2,) = ctx.saved_tensors
+        n = len(params_list)
+        dt = weights[0].dtype
+        dev = x2.device
+        dys = []
+        for i, g in enumerate(grads):
+            dy = g.reshape(-1, weights[i].shape[0])
+            dys.append((dy if dy.dtype == dt else dy.to(dt)).contiguous())
+        ab = [(compute_copy(As[i], dt), compute_copy(Bs[i], dt)) for i in range(n)]   # read at backward time
+        need_dx = ctx.needs_input_grad[0]
+        main = torch.cuda.current_stream(dev)
+        streams, side = ops.group_streams(dev, n)
+        fork = torch.cuda.Event()
+        fork.record(main)
+        side.wait_event(fork)
+        dxs, res, keep = [], [], []
+        for i, prm in enumerate(params_list):
+            if need_dx:
+                streams[i].wait_event(fork)
+                dx, _, _, _, ws = ops._lors_bwd_call(x2, weights[i], ab[i][0], ab[i][1], dys[i], prm.alpha, None,
+                                                     prm.mask_bits, prm.grad_mode, True, False, False,
+                                                     dx_only=True, launch_stream=streams[i])
+                dxs.append(dx)
+                keep.append(ws)
+            _, da, db, dbias, ws = ops._lors_bwd_call(x2, weights[i], ab[i][0], ab[i][1], dys[i], prm.alpha, None,
+                                                      prm.mask_bits, prm.grad_mode, False, has_bias[i],
+                                                      prm.fault_da_sign, launch_stream=side)
+            res.append((da, db, dbias))
+            keep.append(ws)
+        for st in (streams if need_dx else []) + [side]:
+            ev = torch.cuda.Event()
+            ev.record(st)
+            main.wait_event(ev)
+        grad_x = None
+        if need_dx:
+            dx = dxs[0]
+            for d in dxs[1:]:
+                dx.add_(d)
+            grad_x = dx.view(x_shape).to(x_dtype)
+        out = [grad_x, None]
+        for i in range(n):
+            da, db, dbias = res[i]
+            k = 2 + 4 * i
+            out += [None,
+                    dbias.to(dt) if has_bias[i] and ctx.needs_input_grad[k + 1] else None,
+                    da.to(As[i].dtype) if ctx.needs_input_grad[k + 2] else None,
+                    db.to(Bs[i].dtype) if ctx.needs_input_grad[k + 3] else None]
+        return tuple(out)
+
+
+def groupable(layers) -> bool:
+    """Whether `layers` can run as one LoRSGroupFunction node: LoRSLinear projections
+    of the same input on a CUDA device in bf16 (the tensor-core path), without the
+    options that change the saved set (save_p)."""
+    if len(layers) < 2 or os.environ.get("LORS_GROUP", "1") == "0":
+        return False
+    w0 = getattr(layers[0], "weight", None)
+    return all(isinstance(m, LoRSLinear) and m.weight.is_cuda and m.weight.dtype == torch.bfloat16
+               and m.weight.shape[1] == w0.shape[1] and not m.save_p for m in layers)
+
+
+def lors_group(layers, x: torch.Tensor):
+    """Outputs of several LoRS projections of the same `x` (see LoRSGroupFunction)."""
+    tensors = []
+    for m in layers:
+        tensors += [m.weight, m.bias, m.a, m.b]
+    return LoRSGroupFunction.apply(x, tuple(m.params() for m in layers), *tensors)
 
 
 class LoRSLinear(nn.Module):

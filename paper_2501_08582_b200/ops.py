@@ -62,8 +62,14 @@ def _check_layer(x_t, w, a, b):
 
 def lors_fwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tensor, alpha: float = 2.0,
              bias: Optional[torch.Tensor] = None, mask_bits: Optional[torch.Tensor] = None,
-             emit_p: bool = False, sparse24: bool = False, meta24: Optional[torch.Tensor] = None):
+             emit_p: bool = False, sparse24: bool = False, meta24: Optional[torch.Tensor] = None,
+             launch_stream=None, keep: Optional[list] = None):
     """Y_t [L, R] = X_t . W_eff^T (+ bias); optionally P = X_t b^T [L, r].
+
+    Outputs and workspace come from the current stream's pool; `launch_stream`
+    (default: the current stream) runs the kernels, in which case the caller must
+    make the current stream wait for it before the outputs are used or freed and
+    keep the workspace (appended to `keep`) alive until then.
 
     sparse24=True runs the forward on 2:4 sparse tensor cores: the kernel
     compresses each masked W_eff tile on chip (W must satisfy 2:4 along C,
@@ -97,8 +103,25 @@ def lors_fwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
     ws_bytes = lib.lors_fwd_workspace(ct.byref(args))
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=w.device) if ws_bytes else None
     args.workspace, args.workspace_bytes = _p(ws), ws_bytes
-    N.check(lib.lors_fwd(ct.byref(args), _stream()))
+    if keep is not None and ws is not None:
+        keep.append(ws)
+    st = _stream() if launch_stream is None else ct.c_void_p(launch_stream.cuda_stream)
+    N.check(lib.lors_fwd(ct.byref(args), st))
     return y, p
+
+
+_GROUP_STREAMS = {}
+
+
+def group_streams(dev: torch.device, n: int):
+    """n high-priority streams (one per concurrent LoRS GEMM) and one normal-priority
+    stream for the rank-r products, created once per device and reused."""
+    pool = _GROUP_STREAMS.get(dev.index)
+    if pool is None or len(pool[0]) < n:
+        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
+        pool = ([torch.cuda.Stream(device=dev, priority=hi) for _ in range(max(n, 3))], torch.cuda.Stream(device=dev))
+        _GROUP_STREAMS[dev.index] = pool
+    return pool[0][:n], pool[1]
 
 
 _SIDE_STREAMS = {}

@@ -586,3 +586,48 @@ class _nullenv:
 
     def __exit__(self, *exc):
         return False
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("with_bias", [False, True])
+def test_group_node_matches_separate_layers(P, with_bias):
+    """LoRSGroupFunction (projections of one input on concurrent streams, one summed
+    dX) against the same LoRSLinear layers called one by one: outputs bit-identical,
+    adapter / bias / input gradients equal up to fp32 / bf16 summation order."""
+    from paper_2501_08582_b200 import LoRSLinear, lors_group
+    g = torch.Generator(device="cuda").manual_seed(5)
+    C, L = 1024, 1500
+    layers = []
+    for R, r in ((1024, 16), (512, 16), (2048, 24)):
+        w = torch.randn(R, C, device="cuda", generator=g) * 0.02
+        w = torch.where(w.abs() < 0.013, torch.zeros_like(w), w).bfloat16()
+        a = torch.randn(R, r, device="cuda", generator=g) * 0.05
+        b = torch.randn(r, C, device="cuda", generator=g) * 0.2
+        bias = torch.randn(R, device="cuda", generator=g) * 0.1 if with_bias else None
+        layers.append(LoRSLinear(w, a=a, b=b, alpha=2.0, bias=bias))
+    x = torch.randn(3, L // 3, C, device="cuda", generator=g).bfloat16()
+    dys = [torch.randn(3, L // 3, m.out_features, device="cuda", generator=g).bfloat16() for m in layers]
+
+    def run(grouped):
+        for m in layers:
+            m.zero_grad(set_to_none=True)
+        xg = x.clone().requires_grad_(True)
+        outs = lors_group(layers, xg) if grouped else [m(xg) for m in layers]
+        torch.autograd.backward(list(outs), dys)
+        torch.cuda.synchronize()
+        grads = [(m.a.grad.clone(), m.b.grad.clone(), None if m.bias is None else m.bias.grad.clone())
+                 for m in layers]
+        return [o.detach().clone() for o in outs], xg.grad.clone(), grads
+
+    o1, gx1, gr1 = run(False)
+    o2, gx2, gr2 = run(True)
+    for u, v in zip(o1, o2):
+        assert torch.equal(u, v)
+    assert float((gx1.float() - gx2.float()).norm() / gx1.float().norm()) < 5e-3
+    # (P = X b^T and Q = dY a are split-K sums in fp32 rounded to bf16: their
+    # atomics' order can flip a rounding, ~1e-5..1e-4 of dA / dB between any two runs)
+    for (a1, b1, c1), (a2, b2, c2) in zip(gr1, gr2):
+        assert float((a1 - a2).norm() / a1.norm()) < 1e-3
+        assert float((b1 - b2).norm() / b1.norm()) < 1e-3
+        if c1 is not None:
+            assert float((c1.float() - c2.float()).norm() / c1.float().norm()) < 1e-2
