@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(qd::THREADS, 1)
     tc_q_da_kernel(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                    const __grid_constant__ CUtensorMap tmDA, int L, int R, int r, int tr, int tpg, int n_rg,
-                   float alpha, int dbg) {
+                   float alpha) {
   using namespace qd;
   constexpr uint32_t SL = slice_bytes<BN>();
   constexpr uint32_t SWB = BN * 2;               // swizzle span of the a / P slices (MN-major B)
@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(qd::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&qempty[pb]);    // accumulator read: MMA may reuse it
       named_bar_sync(1, 128);
-      if (!(dbg & 1)) reduce_out(&tmQ, t0 + 128 * ti);
+      reduce_out(&tmQ, t0 + 128 * ti);
       named_bar_sync(1, 128);
     }
     mbar_wait(dafull, 0);
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(qd::THREADS, 1)
     for (int j = 0; j < trc; ++j) {               // dA of the CTA's R tiles
       stage((2 + j) * BN, alpha);
       named_bar_sync(1, 128);
-      if (!(dbg & 2)) reduce_out(&tmDA, r0 + 128 * j);
+      reduce_out(&tmDA, r0 + 128 * j);
       named_bar_sync(1, 128);
     }
     if (issuer) tma_store_wait_done();            // the reductions landed in global memory
@@ -604,8 +604,7 @@ static int launch_q_da(const bf16* dy, const bf16* a, const bf16* p, float* q32,
   const size_t smem = qd::smem_bytes<BN>(best_tr);
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "q_da smem attribute");
-  static const int dbg = getenv("LORS_QDA_DBG") ? atoi(getenv("LORS_QDA_DBG")) : 0;
-  kern<<<ctas, qd::THREADS, smem, s>>>(tDY, tA, tP, tQ, tDA, L, R, r, best_tr, best_tpg, n_rg, alpha, dbg);
+  kern<<<ctas, qd::THREADS, smem, s>>>(tDY, tA, tP, tQ, tDA, L, R, r, best_tr, best_tpg, n_rg, alpha);
   LORS_CHECK_LAUNCH("tc_q_da");
   return LORS_OK;
 }

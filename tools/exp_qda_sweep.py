@@ -32,15 +32,10 @@ if len(sys.argv) > 1:
 else:
     sweep = [("8192 11008 4096 64", (1, 2, 3, 4, 5, 6, 0)), ("4096 4096 4096 16", (2, 4, 8, 12, 16, 24, 0)),
              ("4096 11008 4096 16", (4, 8, 12, 16, 24, 0))]
-    if os.environ.get("DBG_SWEEP"):
-        sweep = [("8192 11008 4096 64", (5,)), ("4096 4096 4096 16", (2,))]
     for shape, trs in sweep:
         print(shape, flush=True)
         for tr in trs:
-            for dbg in (("0", "1", "2", "3") if os.environ.get("DBG_SWEEP") else ("0",)):
-                env = dict(os.environ)
-                env["LORS_QDA_DBG"] = dbg
-                if tr:
-                    env["LORS_QDA_TR"] = str(tr)
-                print("dbg", dbg, end=" ", flush=True)
-                subprocess.run([sys.executable, __file__] + shape.split(), env=env)
+            env = dict(os.environ)
+            if tr:
+                env["LORS_QDA_TR"] = str(tr)
+            subprocess.run([sys.executable, __file__] + shape.split(), env=env)
