@@ -28,6 +28,19 @@ int lors_rope(const void* x, void* y, const void* cos_t, const void* sin_t, int6
 int lors_swiglu(const void* g, const void* u, void* h, int64_t n, void* stream);
 int lors_swiglu_bwd(const void* dh, const void* g, const void* u, void* dg, void* du, int64_t n, void* stream);
 
+/* Residual add fused with the RMSNorm that follows it (pre-norm decoder), bf16 rows of D elements
+ * (D % 8 == 0, D <= 8192), gamma [D] bf16, fp32 arithmetic:
+ *   forward   hn = bf16(h + o)            (o may be NULL: hn = h and `hn` may be NULL)
+ *             rstd = 1 / sqrt(mean(hn^2) + eps)   (fp32 [rows], saved for the backward)
+ *             x = bf16(hn rstd gamma)
+ *   backward  dh = bf16(dhn + rstd (dx gamma) - hn rstd^3 sum(dx gamma hn) / D)   (dhn may be NULL)
+ *             -- the gradient of both h and o; the residual path's gradient and the norm's meet in
+ *             one rounding, without a separate add kernel. */
+int lors_add_rmsnorm(const void* h, const void* o, const void* gamma, void* hn, void* x, float* rstd,
+                     int64_t rows, int64_t D, float eps, void* stream);
+int lors_add_rmsnorm_bwd(const void* dhn, const void* dx, const void* hn, const void* gamma, const float* rstd,
+                         void* dh, int64_t rows, int64_t D, void* stream);
+
 /* Fused AdamW over the flat fp32 adapter masters (torch.optim.AdamW semantics, decoupled weight decay,
  * bias-corrected moments), one launch for every adapter of the model; also refreshes the bf16 compute
  * copies (`shadow`, may be NULL) the LoRS kernels read, so no per-call casts remain:

@@ -35,7 +35,8 @@ EXPORTED_SYMBOLS = (
     "lors_launch_count", "lors_reset_launch_count",
 )
 # include/lors_decoder.h: decoder-side helpers (not the LoRS drop-in boundary)
-DECODER_SYMBOLS = ("lors_rope", "lors_swiglu", "lors_swiglu_bwd", "lors_adamw", "lors_adamw_p2p")
+DECODER_SYMBOLS = ("lors_rope", "lors_swiglu", "lors_swiglu_bwd", "lors_add_rmsnorm", "lors_add_rmsnorm_bwd",
+                   "lors_adamw", "lors_adamw_p2p")
 
 _vp = ct.c_void_p
 
@@ -106,6 +107,10 @@ def load(path: str = LIB_PATH) -> ct.CDLL:
         lib.lors_swiglu.restype = ct.c_int
         lib.lors_swiglu_bwd.argtypes = [_vp, _vp, _vp, _vp, _vp, ct.c_int64, _vp]
         lib.lors_swiglu_bwd.restype = ct.c_int
+        lib.lors_add_rmsnorm.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, ct.c_int64, ct.c_int64, ct.c_float, _vp]
+        lib.lors_add_rmsnorm.restype = ct.c_int
+        lib.lors_add_rmsnorm_bwd.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, ct.c_int64, ct.c_int64, _vp]
+        lib.lors_add_rmsnorm_bwd.restype = ct.c_int
         lib.lors_adamw.argtypes = [_vp, _vp, _vp, _vp, _vp, ct.c_int64, ct.c_float, ct.c_float, ct.c_float,
                                    ct.c_float, ct.c_float, ct.c_int64, _vp]
         lib.lors_adamw.restype = ct.c_int

@@ -198,6 +198,174 @@ extern "C" int lors_adamw(float* p, const float* g, float* m, float* v, void* sh
   return LORS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// residual add + RMSNorm: one CTA of 256 threads per row, each thread NV 16-byte
+// vectors of the row held in registers between the two passes
+// ---------------------------------------------------------------------------
+namespace lors {
+namespace {
+constexpr int NORM_THREADS = 256;
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();                       // red[] reusable
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < NORM_THREADS / 32; ++i) t += red[i];
+  return t;
+}
+}  // namespace
+
+template <int NV, bool ADD>
+__global__ void __launch_bounds__(NORM_THREADS) add_rmsnorm_kernel(const uint4* __restrict__ h, const uint4* __restrict__ o,
+                                                                   const uint4* __restrict__ gamma,
+                                                                   uint4* __restrict__ hn, uint4* __restrict__ x,
+                                                                   float* __restrict__ rstd, int d8, float eps) {
+  __shared__ float red[NORM_THREADS / 32];
+  const int64_t base = (int64_t)blockIdx.x * d8;
+  float f[NV][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int v = threadIdx.x + k * NORM_THREADS;
+    if (v < d8) {
+      unpack8(h[base + v], f[k]);
+      if (ADD) {
+        float g[8];
+        unpack8(o[base + v], g);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[k][e] += g[e];
+        const uint4 r = pack8(f[k]);     // the residual stream is bf16: round, then normalise that
+        if (hn) hn[base + v] = r;
+        unpack8(r, f[k]);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ss += f[k][e] * f[k][e];
+    }
+  }
+  const float rs = rsqrtf(block_sum(ss, red) / (float)(d8 * 8) + eps);
+  if (threadIdx.x == 0) rstd[blockIdx.x] = rs;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int v = threadIdx.x + k * NORM_THREADS;
+    if (v < d8) {
+      float g[8];
+      unpack8(gamma[v], g);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) f[k][e] = f[k][e] * rs * g[e];
+      x[base + v] = pack8(f[k]);
+    }
+  }
+}
+
+template <int NV>
+__global__ void __launch_bounds__(NORM_THREADS) add_rmsnorm_bwd_kernel(const uint4* __restrict__ dhn,
+                                                                       const uint4* __restrict__ dx,
+                                                                       const uint4* __restrict__ hn,
+                                                                       const uint4* __restrict__ gamma,
+                                                                       const float* __restrict__ rstd,
+                                                                       uint4* __restrict__ dh, int d8) {
+  __shared__ float red[NORM_THREADS / 32];
+  const int64_t base = (int64_t)blockIdx.x * d8;
+  float dg[NV][8], hv[NV][8];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int v = threadIdx.x + k * NORM_THREADS;
+    if (v < d8) {
+      float g[8];
+      unpack8(dx[base + v], dg[k]);
+      unpack8(gamma[v], g);
+      unpack8(hn[base + v], hv[k]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        dg[k][e] *= g[e];
+        s += dg[k][e] * hv[k][e];
+      }
+    }
+  }
+  const float r = rstd[blockIdx.x];
+  const float c = r * r * r * block_sum(s, red) / (float)(d8 * 8);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int v = threadIdx.x + k * NORM_THREADS;
+    if (v < d8) {
+      float out[8];
+      if (dhn) unpack8(dhn[base + v], out);
+      else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) out[e] = 0.f;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) out[e] += r * dg[k][e] - c * hv[k][e];
+      dh[base + v] = pack8(out);
+    }
+  }
+}
+}  // namespace lors
+
+extern "C" int lors_add_rmsnorm(const void* h, const void* o, const void* gamma, void* hn, void* x, float* rstd,
+                                int64_t rows, int64_t D, float eps, void* stream) {
+  using namespace lors;
+  if (!h || !gamma || !x || !rstd || (o && !hn)) {
+    set_error("lors_add_rmsnorm: null pointer");
+    return LORS_ERR_ARGUMENT;
+  }
+  if (rows < 0 || D <= 0 || D % 8 != 0 || D > 8192 || rows > INT32_MAX) {
+    set_error("lors_add_rmsnorm: need D % 8 == 0, 0 < D <= 8192");
+    return LORS_ERR_SHAPE;
+  }
+  if (rows == 0) return LORS_OK;
+  const int d8 = (int)(D / 8);
+  const int nv = (d8 + NORM_THREADS - 1) / NORM_THREADS;
+  cudaStream_t s = (cudaStream_t)stream;
+  auto go = [&](auto kern) {
+    kern<<<(unsigned)rows, NORM_THREADS, 0, s>>>((const uint4*)h, (const uint4*)o, (const uint4*)gamma, (uint4*)hn,
+                                                 (uint4*)x, rstd, d8, eps);
+  };
+  if (o) {
+    if (nv <= 1) go(add_rmsnorm_kernel<1, true>);
+    else if (nv <= 2) go(add_rmsnorm_kernel<2, true>);
+    else go(add_rmsnorm_kernel<4, true>);
+  } else {
+    if (nv <= 1) go(add_rmsnorm_kernel<1, false>);
+    else if (nv <= 2) go(add_rmsnorm_kernel<2, false>);
+    else go(add_rmsnorm_kernel<4, false>);
+  }
+  LORS_CHECK_LAUNCH("add_rmsnorm");
+  return LORS_OK;
+}
+
+extern "C" int lors_add_rmsnorm_bwd(const void* dhn, const void* dx, const void* hn, const void* gamma,
+                                    const float* rstd, void* dh, int64_t rows, int64_t D, void* stream) {
+  using namespace lors;
+  if (!dx || !hn || !gamma || !rstd || !dh) {
+    set_error("lors_add_rmsnorm_bwd: null pointer");
+    return LORS_ERR_ARGUMENT;
+  }
+  if (rows < 0 || D <= 0 || D % 8 != 0 || D > 8192 || rows > INT32_MAX) {
+    set_error("lors_add_rmsnorm_bwd: need D % 8 == 0, 0 < D <= 8192");
+    return LORS_ERR_SHAPE;
+  }
+  if (rows == 0) return LORS_OK;
+  const int d8 = (int)(D / 8);
+  const int nv = (d8 + NORM_THREADS - 1) / NORM_THREADS;
+  cudaStream_t s = (cudaStream_t)stream;
+  auto go = [&](auto kern) {
+    kern<<<(unsigned)rows, NORM_THREADS, 0, s>>>((const uint4*)dhn, (const uint4*)dx, (const uint4*)hn,
+                                                 (const uint4*)gamma, rstd, (uint4*)dh, d8);
+  };
+  if (nv <= 1) go(add_rmsnorm_bwd_kernel<1>);
+  else if (nv <= 2) go(add_rmsnorm_bwd_kernel<2>);
+  else go(add_rmsnorm_bwd_kernel<4>);
+  LORS_CHECK_LAUNCH("add_rmsnorm_bwd");
+  return LORS_OK;
+}
+
 extern "C" int lors_swiglu(const void* g, const void* u, void* h, int64_t n, void* stream) {
   using namespace lors;
   if (!g || !u || !h) {

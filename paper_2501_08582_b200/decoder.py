@@ -18,6 +18,7 @@ decoders differ only in the adapter linear.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, replace
 from typing import Callable, Dict, Optional
 
@@ -194,6 +195,31 @@ def swiglu(g, u):
     return F.silu(g) * u
 
 
+class AddRMSNormFunction(torch.autograd.Function):
+    """hn = h + o and x = RMSNorm(hn) * gamma (gamma frozen) in one kernel (ops.add_rmsnorm); the
+    backward adds the residual gradient and the norm's in one kernel too, and hands that one
+    gradient to both h and o (the add's backward is the identity).  Saves hn and rstd."""
+
+    @staticmethod
+    def forward(ctx, h, o, gamma, eps):
+        hn, x, rstd = ops.add_rmsnorm(h, o, gamma, eps)
+        ctx.save_for_backward(hn, gamma, rstd)
+        return hn, x
+
+    @staticmethod
+    def backward(ctx, dhn, dx):
+        hn, gamma, rstd = ctx.saved_tensors
+        dh = ops.add_rmsnorm_bwd(dhn, dx, hn, gamma, rstd)
+        return dh, dh, None, None
+
+
+def fused_norms(h: torch.Tensor) -> bool:
+    """Whether the decoder runs the fused residual-add + RMSNorm kernels: CUDA bf16 rows whose width
+    the kernel takes (LORS_FUSED_NORM=0 turns them off for A/B runs)."""
+    return (h.is_cuda and h.dtype == torch.bfloat16 and h.shape[-1] % 8 == 0 and h.shape[-1] <= 8192
+            and os.environ.get("LORS_FUSED_NORM", "1") != "0")
+
+
 def rope_heads(x_bshd, cos, sin):
     """[B, S, H, hd] -> RoPE'd [B, H, S, hd].  CUDA bf16: the native fused kernel
     (fails loudly without the library); elsewhere (CPU reference decoders in the
@@ -211,10 +237,10 @@ class DecoderLayer(nn.Module):
         self.mlp_norm = RMSNorm(cfg.dim, cfg.eps, cfg.dtype, device)
         self.proj = nn.ModuleDict(linears)
 
-    def forward(self, h, cos, sin):
+    def attention(self, x, cos, sin):
+        """The attention branch of normalised input x [B, S, dim] (before the residual add)."""
         cfg, p = self.cfg, self.proj
-        B, S, _ = h.shape
-        x = self.attn_norm(h)
+        B, S, _ = x.shape
         qkv = [p["q"], p["k"], p["v"]]
         # projections of one input as one node: concurrent GEMMs, one summed dX
         qo, ko, vo = lors_group(qkv, x) if groupable(qkv) else (m(x) for m in qkv)
@@ -223,11 +249,23 @@ class DecoderLayer(nn.Module):
         v = vo.view(B, S, cfg.n_kv_heads, cfg.head_dim).transpose(1, 2)
         att = F.scaled_dot_product_attention(q, k, v, is_causal=True,
                                              enable_gqa=cfg.n_kv_heads != cfg.n_heads)
-        h = h + p["o"](att.transpose(1, 2).reshape(B, S, cfg.dim))
-        x = self.mlp_norm(h)
+        return p["o"](att.transpose(1, 2).reshape(B, S, cfg.dim))
+
+    def mlp(self, x):
+        p = self.proj
         gu = [p["gate"], p["up"]]
         g, u = lors_group(gu, x) if groupable(gu) else (m(x) for m in gu)
-        return h + p["down"](swiglu(g, u))
+        return p["down"](swiglu(g, u))
+
+    def forward(self, h, cos, sin):
+        h = h + self.attention(self.attn_norm(h), cos, sin)
+        return h + self.mlp(self.mlp_norm(h))
+
+    def forward_fused(self, h, x, cos, sin, next_norm: "RMSNorm"):
+        """(h_next, next_norm(h_next)) from the residual h and x = attn_norm(h): both residual adds
+        run inside the fused add + RMSNorm kernels (the second one with the next block's norm)."""
+        h, x = AddRMSNormFunction.apply(h, self.attention(x, cos, sin), self.mlp_norm.weight, self.mlp_norm.eps)
+        return AddRMSNormFunction.apply(h, self.mlp(x), next_norm.weight, next_norm.eps)
 
 
 def lors_factory(cfg: DecoderConfig, a_std: float = 1e-3, b_std: Optional[float] = None,
@@ -290,6 +328,12 @@ class LoRSDecoder(nn.Module):
             raise ArgumentError(f"sequence length {S} exceeds the RoPE table ({self.cfg.seq})")
         cos, sin = self.rope_cos[:S], self.rope_sin[:S]
         h = F.embedding(tokens, self.embed)
+        if fused_norms(h):
+            x = self.layers[0].attn_norm(h)
+            for i, layer in enumerate(self.layers):
+                nxt = self.layers[i + 1].attn_norm if i + 1 < len(self.layers) else self.norm
+                h, x = layer.forward_fused(h, x, cos, sin, nxt)
+            return F.linear(x, self.head)
         for layer in self.layers:
             h = layer(h, cos, sin)
         return F.linear(self.norm(h), self.head)

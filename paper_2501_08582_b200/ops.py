@@ -309,6 +309,37 @@ def swiglu(g: torch.Tensor, u: torch.Tensor) -> torch.Tensor:
     return h
 
 
+def add_rmsnorm(h: torch.Tensor, o: Optional[torch.Tensor], gamma: torch.Tensor, eps: float):
+    """(hn = h + o, x = rmsnorm(hn) * gamma, rstd) over the last axis, bf16 in / out, fp32 rstd
+    (include/lors_decoder.h).  o=None normalises h itself (hn is h)."""
+    D = h.shape[-1]
+    if h.dtype != torch.bfloat16 or gamma.dtype != torch.bfloat16 or (o is not None and o.dtype != torch.bfloat16):
+        raise ArgumentError("add_rmsnorm: bf16 tensors expected")
+    if gamma.shape != (D,) or (o is not None and o.shape != h.shape):
+        raise ShapeError("add_rmsnorm: o must match h and gamma must be [D]")
+    h = h.contiguous()
+    o = None if o is None else o.contiguous()
+    rows = h.numel() // D
+    hn = torch.empty_like(h) if o is not None else h
+    x = torch.empty_like(h)
+    rstd = torch.empty(h.shape[:-1], dtype=torch.float32, device=h.device)
+    N.check(N.load().lors_add_rmsnorm(_p(h), _p(o), _p(gamma.contiguous()), _p(hn) if o is not None else None, _p(x),
+                                      _p(rstd), rows, D, float(eps), _stream()))
+    return hn, x, rstd
+
+
+def add_rmsnorm_bwd(dhn: Optional[torch.Tensor], dx: torch.Tensor, hn: torch.Tensor, gamma: torch.Tensor,
+                    rstd: torch.Tensor) -> torch.Tensor:
+    """Gradient of h (and o) for add_rmsnorm: dhn + the norm's backward, one rounding."""
+    D = hn.shape[-1]
+    dx, hn = dx.contiguous(), hn.contiguous()
+    dhn = None if dhn is None else dhn.contiguous()
+    dh = torch.empty_like(hn)
+    N.check(N.load().lors_add_rmsnorm_bwd(_p(dhn), _p(dx), _p(hn), _p(gamma.contiguous()), _p(rstd), _p(dh),
+                                          hn.numel() // D, D, _stream()))
+    return dh
+
+
 def swiglu_bwd(dh: torch.Tensor, g: torch.Tensor, u: torch.Tensor):
     """(dg, du) of h = silu(g) * u, bf16, one kernel."""
     dh, g, u = dh.contiguous(), g.contiguous(), u.contiguous()

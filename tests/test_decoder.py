@@ -16,6 +16,7 @@ import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
+import torch.nn.functional as F
 
 from paper_2501_08582_b200 import decoder as dec
 from paper_2501_08582_b200.trainer import Trainer, synthetic_tokens
@@ -286,3 +287,28 @@ def test_flat_adamw_matches_torch_adamw():
     with torch.no_grad():                              # an outside in-place change: the cast path takes over
         p1[0].mul_(2.0)
     assert torch.equal(compute_copy(p1[0], torch.bfloat16), p1[0].detach().bfloat16())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("D,rows", [(4096, 700), (256, 33), (5120, 64), (2056, 5)])
+def test_fused_add_rmsnorm_matches_torch(D, rows):
+    """lors_add_rmsnorm / _bwd against the torch formula (h + o, F.rms_norm) in fp32: forward outputs
+    and the gradient that reaches h and o (residual + norm paths)."""
+    from paper_2501_08582_b200.decoder import AddRMSNormFunction
+    g = torch.Generator(device="cuda").manual_seed(D + rows)
+    h = torch.randn(rows, D, device="cuda", generator=g).bfloat16().requires_grad_(True)
+    o = torch.randn(rows, D, device="cuda", generator=g).bfloat16().requires_grad_(True)
+    gamma = (1 + 0.1 * torch.randn(D, device="cuda", generator=g)).bfloat16()
+    dhn = torch.randn(rows, D, device="cuda", generator=g).bfloat16()
+    dx = torch.randn(rows, D, device="cuda", generator=g).bfloat16()
+    hn, x = AddRMSNormFunction.apply(h, o, gamma, 1e-5)
+    torch.autograd.backward([hn, x], [dhn, dx])
+    hf, of = h.detach().float(), o.detach().float()
+    hnr = (hf + of).bfloat16().float().requires_grad_(True)
+    xr = F.rms_norm(hnr, (D,), gamma.float(), 1e-5)
+    (hnr * dhn.float()).sum().add((xr * dx.float()).sum()).backward()
+    assert torch.equal(hn, (hf + of).bfloat16())
+    assert float((x.float() - xr).norm() / xr.norm()) < 5e-3
+    ref = hnr.grad
+    for got in (h.grad, o.grad):
+        assert float((got.float() - ref).norm() / ref.norm()) < 5e-3
