@@ -75,6 +75,10 @@ typedef enum { LORS_GRAD_STE = 0, LORS_GRAD_MASKED = 1 } lors_grad_mode_t;
                                      /* the dX GEMM's tail split) -- the caller */
                                      /* runs the rank-r part separately, e.g.   */
                                      /* on a second stream, with NO_DX          */
+#define LORS_FLAG_ZEROED (1u << 4)   /* backward: dA and dB are zero on entry   */
+                                     /* (one fill of a joint buffer by the      */
+                                     /* caller replaces the library's two       */
+                                     /* zeroing launches); ignored elsewhere    */
 #define LORS_FLAG_FAULT_DA_SIGN (1u << 30) /* negative control: flip dA sign,
                                               mirrors FAULT_INJECTION
                                               "lors_backward_sign_flip"

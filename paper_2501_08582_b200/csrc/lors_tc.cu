@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(sk::THREADS, 1)
 //   B: K-major [N, K] or MN-major [K, N]
 template <int BN, bool A_MN, bool B_MN, int OUT>
 static int launch_skinny(const bf16* A, const bf16* B, void* out, int M, int N, int K, int ldo, float alpha,
-                         bool allow_split, cudaStream_t s, float* acc32 = nullptr) {
+                         bool allow_split, cudaStream_t s, float* acc32 = nullptr, bool zeroed = false) {
   CUtensorMap tA, tB;
   int st;
   if (A_MN) st = make_map(&tA, A, M, K, 64, 64, 128, "skinny A (MN)");
@@ -317,7 +317,7 @@ static int launch_skinny(const bf16* A, const bf16* B, void* out, int M, int N, 
   if (can_split) split = (int)std::max<int64_t>(1, std::min<int64_t>((2 * num_sms()) / mt, kblocks / 4));
   const int kps = (int)ceil_div(kblocks, split) * sk::BK;
   split = (int)ceil_div(K, kps);
-  if (split > 1 && OUT != 0) {
+  if (split > 1 && OUT != 0 && !zeroed) {
     const size_t elems = OUT == 2 ? (size_t)N * ldo : (size_t)M * ldo;
     LORS_CUDA_TRY(cudaMemsetAsync(out, 0, elems * sizeof(float), s), "zero split-K output");
   }
@@ -335,11 +335,11 @@ static int launch_skinny(const bf16* A, const bf16* B, void* out, int M, int N, 
 // dispatch on the padded rank
 template <bool A_MN, bool B_MN, int OUT>
 static int skinny(int rp, const bf16* A, const bf16* B, void* out, int M, int N, int K, int ldo, float alpha,
-                  bool allow_split, cudaStream_t s, float* acc32 = nullptr) {
+                  bool allow_split, cudaStream_t s, float* acc32 = nullptr, bool zeroed = false) {
   switch (rp) {
-    case 16: return launch_skinny<16, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32);
-    case 32: return launch_skinny<32, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32);
-    default: return launch_skinny<64, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32);
+    case 16: return launch_skinny<16, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32, zeroed);
+    case 32: return launch_skinny<32, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32, zeroed);
+    default: return launch_skinny<64, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32, zeroed);
   }
 }
 
@@ -2076,6 +2076,7 @@ int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {
       float* P32 = (float*)((char*)A->workspace + 2 * slot);
       float* Q32 = (float*)((char*)A->workspace + 3 * slot);
       const bool need_p = P == nullptr;
+      const bool zeroed = (A->flags & LORS_FLAG_ZEROED) != 0;   // caller-zeroed dA and dB
       LORS_CUDA_TRY(cudaMemsetAsync(need_p ? (void*)P32 : (void*)Q32, 0, (need_p ? 2 : 1) * slot, s),
                     "zero rank-r accumulators");
       if (need_p) {  // P = X_t b^T
@@ -2085,7 +2086,7 @@ int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {
       static const bool fused_q_da = getenv("LORS_NO_QDA_PASS") == nullptr;
       if (fused_q_da && q_da_fits(rp, R)) {
         // P rounded first; then Q and dA from one pass over dY (K4b), Q rounded; dB
-        LORS_CUDA_TRY(cudaMemsetAsync(A->da, 0, sizeof(float) * (size_t)R * r, s), "zero dA");
+        if (!zeroed) LORS_CUDA_TRY(cudaMemsetAsync(A->da, 0, sizeof(float) * (size_t)R * r, s), "zero dA");
         if (need_p) {
           const int64_t na4 = (int64_t)L * r / 4;
           f32_to_bf16_pair_kernel<<<(unsigned)ceil_div(na4, 256), 256, 0, s>>>((const float4*)P32, P, na4, nullptr,
@@ -2097,7 +2098,7 @@ int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {
         f32_to_bf16_pair_kernel<<<(unsigned)ceil_div(nb4, 256), 256, 0, s>>>(nullptr, nullptr, 0,
                                                                              (const float4*)Q32, Q, nb4);
         LORS_CHECK_LAUNCH("Q fp32 -> bf16");
-        if ((st = skinny<true, true, 2>(rp, x, Q, A->db, C, r, L, C, A->alpha, true, s))) return st;
+        if ((st = skinny<true, true, 2>(rp, x, Q, A->db, C, r, L, C, A->alpha, true, s, nullptr, zeroed))) return st;
         goto rank_r_done;
       }
       // Q = dY_t a: A = dY_t K-major [L, R], B = a [R, r] MN-major

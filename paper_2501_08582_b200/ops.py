@@ -200,8 +200,14 @@ def _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, 
         raise ArgumentError(f"grad_mode must be 'ste' or 'masked', got {grad_mode!r}")
     dev = w.device
     dx = torch.empty((L, C), dtype=dt, device=dev) if need_dx else None
-    da = None if dx_only else torch.empty((R, r), dtype=torch.float32, device=dev)
-    db = None if dx_only else torch.empty((r, C), dtype=torch.float32, device=dev)
+    # tensor-core STE path: dA and dB carved out of one zero-filled buffer -- one fill
+    # kernel instead of the library's two memsets (the buffer is what the grads keep)
+    zeroed = (not dx_only and dt == torch.bfloat16 and grad_mode == "ste" and L > 0 and R % 8 == 0
+              and C % 8 == 0 and r % 8 == 0 and r <= 64)
+    if zeroed:
+        da_b, db_b = (R * r * 4 + 255) // 256 * 256, (r * C * 4 + 255) // 256 * 256
+    da = None if dx_only or zeroed else torch.empty((R, r), dtype=torch.float32, device=dev)
+    db = None if dx_only or zeroed else torch.empty((r, C), dtype=torch.float32, device=dev)
     dbias = torch.empty((R,), dtype=torch.float32, device=dev) if with_bias and not dx_only else None
     args = N.BwdArgs()
     args.L, args.R, args.C, args.r = L, R, C, r
@@ -212,10 +218,15 @@ def _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, 
                   | (N.FLAG_FAULT_DA_SIGN if fault_da_sign and not dx_only else 0))
     args.alpha = float(alpha)
     args.x, args.w, args.mask_bits, args.a, args.b = _p(x_t), _p(w), _p(mask_bits), _p(a), _p(b)
-    args.dy, args.p, args.dx, args.da, args.db, args.dbias = _p(dy_t), _p(p), _p(dx), _p(da), _p(db), _p(dbias)
     lib = N.load()
     ws_bytes = lib.lors_bwd_workspace(ct.byref(args))
+    if zeroed:
+        buf = torch.zeros(da_b + db_b, dtype=torch.uint8, device=dev)
+        da = buf[:R * r * 4].view(torch.float32).view(R, r)
+        db = buf[da_b:da_b + r * C * 4].view(torch.float32).view(r, C)
+        args.flags |= N.FLAG_ZEROED
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev) if ws_bytes else None
+    args.dy, args.p, args.dx, args.da, args.db, args.dbias = _p(dy_t), _p(p), _p(dx), _p(da), _p(db), _p(dbias)
     args.workspace, args.workspace_bytes = _p(ws), ws_bytes
     st = _stream() if launch_stream is None else ct.c_void_p(launch_stream.cuda_stream)
     N.check(lib.lors_bwd(ct.byref(args), st))
