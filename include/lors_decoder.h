@@ -12,10 +12,11 @@
 extern "C" {
 #endif
 
-/* Rotary position embedding (rotate-half convention), bf16, fused with the
- * head transpose that attention wants:
+/* Rotary position embedding (rotate-half convention), bf16, optionally fused with
+ * a head transpose:
  *   layout 0:  x [B, S, H, hd] -> y [B, H, S, hd]   (forward: projection output -> attention input)
  *   layout 1:  x [B, H, S, hd] -> y [B, S, H, hd]   (backward: attention grad -> projection grad)
+ *   layout 2:  x [B, S, H, hd] -> y [B, S, H, hd]   (no transpose: attention reads strided heads)
  * y = x * cos + rotate_half(x) * (inverse ? -sin : sin), cos / sin [S, hd] (bf16), computed in fp32 and
  * rounded once.  hd must be a multiple of 8 (16-byte accesses). */
 int lors_rope(const void* x, void* y, const void* cos_t, const void* sin_t, int64_t B, int64_t S, int64_t H,

@@ -36,16 +36,16 @@ __global__ void rope_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* 
   if (idx >= total) return;
   const int c = (int)(idx % per_head) * 8;
   int64_t rest = idx / per_head;
-  // LAYOUT 0 walks the input [B, S, H] order, LAYOUT 1 the input [B, H, S] order
+  // LAYOUT 0 / 2 walk the input [B, S, H] order, LAYOUT 1 the input [B, H, S] order
   int64_t b, s, h;
-  if (LAYOUT == 0) {
+  if (LAYOUT != 1) {
     h = rest % H; rest /= H; s = rest % S; b = rest / S;
   } else {
     s = rest % S; rest /= S; h = rest % H; b = rest / H;
   }
   const int64_t bsh = ((b * S + s) * H + h) * hd;   // [B, S, H, hd]
   const int64_t bhs = ((b * H + h) * S + s) * hd;   // [B, H, S, hd]
-  const int64_t in = LAYOUT == 0 ? bsh : bhs, out = LAYOUT == 0 ? bhs : bsh;
+  const int64_t in = LAYOUT == 1 ? bhs : bsh, out = LAYOUT == 0 ? bhs : bsh;   // 2: [B, S, H, hd] in place order
   float x1[8], x2[8], c1[8], c2[8], s1[8], s2[8], o1[8], o2[8];
   unpack8(*reinterpret_cast<const uint4*>(x + in + c), x1);
   unpack8(*reinterpret_cast<const uint4*>(x + in + half + c), x2);
@@ -414,8 +414,8 @@ extern "C" int lors_rope(const void* x, void* y, const void* cos_t, const void* 
     set_error("lors_rope: head dim must be a positive multiple of 16 (two 8-element halves)");
     return LORS_ERR_SHAPE;
   }
-  if (layout != 0 && layout != 1) {
-    set_error("lors_rope: layout must be 0 ([B,S,H,hd] -> [B,H,S,hd]) or 1 (the reverse)");
+  if (layout != 0 && layout != 1 && layout != 2) {
+    set_error("lors_rope: layout must be 0 ([B,S,H,hd] -> [B,H,S,hd]), 1 (the reverse) or 2 (no transpose)");
     return LORS_ERR_ARGUMENT;
   }
   const int64_t total = B * S * H * (hd / 16);
@@ -428,7 +428,8 @@ extern "C" int lors_rope(const void* x, void* y, const void* cos_t, const void* 
   auto cp = (const __nv_bfloat16*)cos_t;
   auto sp = (const __nv_bfloat16*)sin_t;
   if (layout == 0) rope_kernel<0><<<grid, 256, 0, s>>>(xp, yp, cp, sp, B, S, H, (int)hd, sgn);
-  else rope_kernel<1><<<grid, 256, 0, s>>>(xp, yp, cp, sp, B, S, H, (int)hd, sgn);
+  else if (layout == 1) rope_kernel<1><<<grid, 256, 0, s>>>(xp, yp, cp, sp, B, S, H, (int)hd, sgn);
+  else rope_kernel<2><<<grid, 256, 0, s>>>(xp, yp, cp, sp, B, S, H, (int)hd, sgn);
   LORS_CHECK_LAUNCH("rope");
   return LORS_OK;
 }

@@ -159,18 +159,21 @@ def apply_rope(x, cos, sin):
 
 
 class RopeFunction(torch.autograd.Function):
-    """Fused RoPE + head transpose on the GPU (ops.rope, one kernel each way):
-    x [B, S, H, hd] (the projection output viewed per head) -> [B, H, S, hd]."""
+    """Fused RoPE on the GPU (ops.rope, one kernel each way): x [B, S, H, hd] (the projection output
+    viewed per head) -> the rotated heads as a [B, H, S, hd] view of a [B, S, H, hd] buffer.  Attention
+    reads q / k / v with those strides (v is the same kind of view of its projection output), writes its
+    output the same way, so neither the heads nor the attention output need a transpose copy."""
 
     @staticmethod
     def forward(ctx, x, cos, sin):
         ctx.save_for_backward(cos, sin)
-        return ops.rope(x, cos, sin, layout=0)
+        return ops.rope(x, cos, sin, layout=2).transpose(1, 2)
 
     @staticmethod
     def backward(ctx, gy):
         cos, sin = ctx.saved_tensors
-        return ops.rope(gy, cos, sin, layout=1, inverse=True), None, None
+        g = gy.transpose(1, 2)             # [B, S, H, hd]; contiguous when attention's grad kept the strides
+        return ops.rope(g, cos, sin, layout=2, inverse=True), None, None
 
 
 class SwiGLUFunction(torch.autograd.Function):

@@ -290,7 +290,8 @@ def grad_outer(dy_t: torch.Tensor, x_t: torch.Tensor, w: Optional[torch.Tensor] 
 
 def rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor, layout: int = 0, inverse: bool = False):
     """Fused RoPE (rotate-half) + head transpose, bf16 (include/lors_decoder.h).
-    layout 0: x [B, S, H, hd] -> [B, H, S, hd]; layout 1: x [B, H, S, hd] -> [B, S, H, hd].
+    layout 0: x [B, S, H, hd] -> [B, H, S, hd]; layout 1: x [B, H, S, hd] -> [B, S, H, hd];
+    layout 2: x [B, S, H, hd] -> [B, S, H, hd] (no transpose).
     inverse=True rotates by -theta (the backward)."""
     if x.dtype != torch.bfloat16 or cos.dtype != torch.bfloat16 or sin.dtype != torch.bfloat16:
         raise ArgumentError("rope: bf16 tensors expected")
@@ -300,6 +301,9 @@ def rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor, layout: int = 0,
     if layout == 0:
         B, S, H, hd = x.shape
         y = torch.empty((B, H, S, hd), dtype=x.dtype, device=x.device)
+    elif layout == 2:
+        B, S, H, hd = x.shape
+        y = torch.empty_like(x)
     else:
         B, H, S, hd = x.shape
         y = torch.empty((B, S, H, hd), dtype=x.dtype, device=x.device)

@@ -237,9 +237,15 @@ def test_fused_rope_matches_torch_formula():
         xr = x.detach().float().requires_grad_(True)
         yr = dec.apply_rope(xr.transpose(1, 2), cos.float(), sin.float())
         yr.backward(gy.float())
-        assert y.shape == (2, H, 64, cfg.head_dim) and y.is_contiguous()
+        assert y.shape == (2, H, 64, cfg.head_dim) and y.transpose(1, 2).is_contiguous()   # heads as strides
         assert float((y.float() - yr).norm() / yr.norm()) < 5e-3
         assert float((x.grad.float() - xr.grad).norm() / xr.grad.norm()) < 5e-3
+        # the transposing layouts of the same kernel
+        from paper_2501_08582_b200 import ops
+        y0 = ops.rope(x.detach(), cos, sin, layout=0)
+        assert y0.is_contiguous() and torch.equal(y0, y.detach().contiguous())
+        y1 = ops.rope(y0, cos, sin, layout=1, inverse=True)
+        assert float((y1.float() - x.detach().float()).norm() / x.detach().float().norm()) < 1e-2
 
 
 @pytest.mark.gpu
