@@ -42,6 +42,16 @@ int lors_add_rmsnorm(const void* h, const void* o, const void* gamma, void* hn, 
 int lors_add_rmsnorm_bwd(const void* dhn, const void* dx, const void* hn, const void* gamma, const float* rstd,
                          void* dh, int64_t rows, int64_t D, void* stream);
 
+/* Next-token cross-entropy over bf16 logits [N, V] (V % 8 == 0) with int64 targets [N], fp32 arithmetic:
+ *   forward   lse = logsumexp(logits[n, :]) (one online max / sum pass), loss_rows[n] = lse[n] - logits[n, t_n]
+ *   backward  dlogits[n, j] = bf16((exp(logits[n, j] - lse[n]) - [j == t_n]) * grad_out[0] / N)
+ * grad_out is a device fp32 scalar (the gradient of the mean loss, read on the device: no host sync);
+ * dlogits may alias logits (the backward then overwrites them in place). */
+int lors_cross_entropy(const void* logits, const int64_t* targets, float* loss_rows, float* lse, int64_t N,
+                       int64_t V, void* stream);
+int lors_cross_entropy_bwd(const void* logits, const int64_t* targets, const float* lse, const float* grad_out,
+                           void* dlogits, int64_t N, int64_t V, void* stream);
+
 /* Fused AdamW over the flat fp32 adapter masters (torch.optim.AdamW semantics, decoupled weight decay,
  * bias-corrected moments), one launch for every adapter of the model; also refreshes the bf16 compute
  * copies (`shadow`, may be NULL) the LoRS kernels read, so no per-call casts remain:

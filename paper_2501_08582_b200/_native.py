@@ -37,7 +37,7 @@ EXPORTED_SYMBOLS = (
 )
 # include/lors_decoder.h: decoder-side helpers (not the LoRS drop-in boundary)
 DECODER_SYMBOLS = ("lors_rope", "lors_swiglu", "lors_swiglu_bwd", "lors_add_rmsnorm", "lors_add_rmsnorm_bwd",
-                   "lors_adamw", "lors_adamw_p2p")
+                   "lors_cross_entropy", "lors_cross_entropy_bwd", "lors_adamw", "lors_adamw_p2p")
 
 _vp = ct.c_void_p
 
@@ -112,6 +112,10 @@ def load(path: str = LIB_PATH) -> ct.CDLL:
         lib.lors_add_rmsnorm.restype = ct.c_int
         lib.lors_add_rmsnorm_bwd.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, ct.c_int64, ct.c_int64, _vp]
         lib.lors_add_rmsnorm_bwd.restype = ct.c_int
+        lib.lors_cross_entropy.argtypes = [_vp, _vp, _vp, _vp, ct.c_int64, ct.c_int64, _vp]
+        lib.lors_cross_entropy.restype = ct.c_int
+        lib.lors_cross_entropy_bwd.argtypes = [_vp, _vp, _vp, _vp, _vp, ct.c_int64, ct.c_int64, _vp]
+        lib.lors_cross_entropy_bwd.restype = ct.c_int
         lib.lors_adamw.argtypes = [_vp, _vp, _vp, _vp, _vp, ct.c_int64, ct.c_float, ct.c_float, ct.c_float,
                                    ct.c_float, ct.c_float, ct.c_int64, _vp]
         lib.lors_adamw.restype = ct.c_int

@@ -308,6 +308,114 @@ __global__ void __launch_bounds__(NORM_THREADS) add_rmsnorm_bwd_kernel(const uin
 }
 }  // namespace lors
 
+// ---------------------------------------------------------------------------
+// cross-entropy: one CTA of 256 threads per row, 16-byte vectors, online max / sum
+// ---------------------------------------------------------------------------
+namespace lors {
+namespace {
+constexpr int CE_THREADS = 256;
+}  // namespace
+
+__global__ void __launch_bounds__(CE_THREADS) ce_fwd_kernel(const uint4* __restrict__ logits,
+                                                            const int64_t* __restrict__ targets,
+                                                            float* __restrict__ loss_rows, float* __restrict__ lse,
+                                                            int v8) {
+  __shared__ float sm[CE_THREADS / 32], ss[CE_THREADS / 32];
+  const int64_t base = (int64_t)blockIdx.x * v8;
+  float m = -INFINITY, sum = 0.f;
+  for (int v = threadIdx.x; v < v8; v += CE_THREADS) {
+    float f[8];
+    unpack8(logits[base + v], f);
+    float lm = f[0];
+#pragma unroll
+    for (int e = 1; e < 8; ++e) lm = fmaxf(lm, f[e]);
+    if (lm > m) {
+      sum *= __expf(m - lm);
+      m = lm;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sum += __expf(f[e] - m);
+  }
+  // combine (max, sum) pairs: warp, then block
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, sum, o);
+    const float nm = fmaxf(m, om);
+    sum = (m == -INFINITY ? 0.f : sum * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+    m = nm;
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    sm[w] = m;
+    ss[w] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = sm[0];
+    for (int i = 1; i < CE_THREADS / 32; ++i) M = fmaxf(M, sm[i]);
+    float S = 0.f;
+    for (int i = 0; i < CE_THREADS / 32; ++i) S += ss[i] * __expf(sm[i] - M);
+    const float L = M + __logf(S);
+    const int64_t t = targets[blockIdx.x];
+    const __nv_bfloat16* row = reinterpret_cast<const __nv_bfloat16*>(logits + base);
+    lse[blockIdx.x] = L;
+    loss_rows[blockIdx.x] = L - __bfloat162float(row[t]);
+  }
+}
+
+__global__ void __launch_bounds__(CE_THREADS) ce_bwd_kernel(const uint4* logits, const int64_t* __restrict__ targets,
+                                                            const float* __restrict__ lse,
+                                                            const float* __restrict__ grad_out, uint4* dlogits,
+                                                            int v8, float inv_n) {
+  const int64_t base = (int64_t)blockIdx.x * v8;
+  const float L = lse[blockIdx.x], g = grad_out[0] * inv_n;
+  const int64_t t = targets[blockIdx.x];
+  for (int v = threadIdx.x; v < v8; v += CE_THREADS) {
+    float f[8];
+    unpack8(logits[base + v], f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = (__expf(f[e] - L) - ((int64_t)v * 8 + e == t ? 1.f : 0.f)) * g;
+    dlogits[base + v] = pack8(f);
+  }
+}
+}  // namespace lors
+
+extern "C" int lors_cross_entropy(const void* logits, const int64_t* targets, float* loss_rows, float* lse,
+                                  int64_t N, int64_t V, void* stream) {
+  using namespace lors;
+  if (!logits || !targets || !loss_rows || !lse) {
+    set_error("lors_cross_entropy: null pointer");
+    return LORS_ERR_ARGUMENT;
+  }
+  if (N < 0 || V <= 0 || V % 8 != 0 || N > INT32_MAX || V / 8 > INT32_MAX) {
+    set_error("lors_cross_entropy: need V % 8 == 0");
+    return LORS_ERR_SHAPE;
+  }
+  if (N == 0) return LORS_OK;
+  ce_fwd_kernel<<<(unsigned)N, CE_THREADS, 0, (cudaStream_t)stream>>>((const uint4*)logits, targets, loss_rows, lse,
+                                                                      (int)(V / 8));
+  LORS_CHECK_LAUNCH("cross_entropy");
+  return LORS_OK;
+}
+
+extern "C" int lors_cross_entropy_bwd(const void* logits, const int64_t* targets, const float* lse,
+                                      const float* grad_out, void* dlogits, int64_t N, int64_t V, void* stream) {
+  using namespace lors;
+  if (!logits || !targets || !lse || !grad_out || !dlogits) {
+    set_error("lors_cross_entropy_bwd: null pointer");
+    return LORS_ERR_ARGUMENT;
+  }
+  if (N < 0 || V <= 0 || V % 8 != 0 || N > INT32_MAX || V / 8 > INT32_MAX) {
+    set_error("lors_cross_entropy_bwd: need V % 8 == 0");
+    return LORS_ERR_SHAPE;
+  }
+  if (N == 0) return LORS_OK;
+  ce_bwd_kernel<<<(unsigned)N, CE_THREADS, 0, (cudaStream_t)stream>>>((const uint4*)logits, targets, lse, grad_out,
+                                                                      (uint4*)dlogits, (int)(V / 8), 1.0f / (float)N);
+  LORS_CHECK_LAUNCH("cross_entropy_bwd");
+  return LORS_OK;
+}
+
 extern "C" int lors_add_rmsnorm(const void* h, const void* o, const void* gamma, void* hn, void* x, float* rstd,
                                 int64_t rows, int64_t D, float eps, void* stream) {
   using namespace lors;

@@ -216,6 +216,23 @@ class AddRMSNormFunction(torch.autograd.Function):
         return dh, dh, None, None
 
 
+class CrossEntropyFunction(torch.autograd.Function):
+    """Mean next-token cross-entropy of bf16 logits [N, V] (ops.cross_entropy: one pass per row, no fp32
+    copy of the logits); the backward writes the logits' gradient over the logits themselves (they are
+    this node's own input, consumed here only), scaled on the device by the incoming gradient."""
+
+    @staticmethod
+    def forward(ctx, logits, targets):
+        loss_rows, lse = ops.cross_entropy(logits, targets)
+        ctx.save_for_backward(logits, targets, lse)
+        return loss_rows.mean()
+
+    @staticmethod
+    def backward(ctx, g):
+        logits, targets, lse = ctx.saved_tensors
+        return ops.cross_entropy_bwd(logits, targets, lse, g, out=logits), None
+
+
 def fused_norms(h: torch.Tensor) -> bool:
     """Whether the decoder runs the fused residual-add + RMSNorm kernels: CUDA bf16 rows whose width
     the kernel takes (LORS_FUSED_NORM=0 turns them off for A/B runs)."""
@@ -344,7 +361,11 @@ class LoRSDecoder(nn.Module):
     def loss(self, tokens: torch.Tensor) -> torch.Tensor:
         """Next-token cross-entropy over tokens [B, S + 1] (mean over B*S predictions, fp32)."""
         logits = self(tokens[:, :-1])
-        return F.cross_entropy(logits.float().reshape(-1, self.cfg.vocab), tokens[:, 1:].reshape(-1))
+        targets = tokens[:, 1:].reshape(-1)
+        if logits.is_cuda and logits.dtype == torch.bfloat16 and self.cfg.vocab % 8 == 0 \
+                and os.environ.get("LORS_FUSED_CE", "1") != "0":
+            return CrossEntropyFunction.apply(logits.reshape(-1, self.cfg.vocab), targets)
+        return F.cross_entropy(logits.float().reshape(-1, self.cfg.vocab), targets)
 
     def adapter_parameters(self):
         return [p for p in self.parameters() if p.requires_grad]

@@ -355,6 +355,31 @@ def add_rmsnorm_bwd(dhn: Optional[torch.Tensor], dx: torch.Tensor, hn: torch.Ten
     return dh
 
 
+def cross_entropy(logits: torch.Tensor, targets: torch.Tensor):
+    """(per-row loss, logsumexp) of bf16 logits [N, V] against int64 targets [N], fp32."""
+    if logits.dtype != torch.bfloat16 or logits.dim() != 2 or targets.dtype != torch.int64:
+        raise ArgumentError("cross_entropy: bf16 logits [N, V] and int64 targets expected")
+    N_, V = logits.shape
+    if targets.shape != (N_,):
+        raise ShapeError(f"cross_entropy: targets must be [{N_}], got {tuple(targets.shape)}")
+    logits, targets = logits.contiguous(), targets.contiguous()
+    loss_rows = torch.empty(N_, dtype=torch.float32, device=logits.device)
+    lse = torch.empty(N_, dtype=torch.float32, device=logits.device)
+    N.check(N.load().lors_cross_entropy(_p(logits), _p(targets), _p(loss_rows), _p(lse), N_, V, _stream()))
+    return loss_rows, lse
+
+
+def cross_entropy_bwd(logits: torch.Tensor, targets: torch.Tensor, lse: torch.Tensor, grad_out: torch.Tensor,
+                      out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """d(mean loss)/d logits scaled by the device scalar grad_out; written into `out` (may be `logits`)."""
+    N_, V = logits.shape
+    out = torch.empty_like(logits) if out is None else out
+    g = grad_out.reshape(1).to(torch.float32).contiguous()
+    N.check(N.load().lors_cross_entropy_bwd(_p(logits), _p(targets.contiguous()), _p(lse), _p(g), _p(out), N_, V,
+                                            _stream()))
+    return out
+
+
 def swiglu_bwd(dh: torch.Tensor, g: torch.Tensor, u: torch.Tensor):
     """(dg, du) of h = silu(g) * u, bf16, one kernel."""
     dh, g, u = dh.contiguous(), g.contiguous(), u.contiguous()

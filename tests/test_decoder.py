@@ -318,3 +318,23 @@ def test_fused_add_rmsnorm_matches_torch(D, rows):
     ref = hnr.grad
     for got in (h.grad, o.grad):
         assert float((got.float() - ref).norm() / ref.norm()) < 5e-3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,V", [(300, 1000), (64, 128256), (7, 32000)])
+def test_fused_cross_entropy_matches_torch(N, V):
+    """CrossEntropyFunction (one-pass logsumexp, in-place gradient) against F.cross_entropy on the fp32
+    upcast of the same bf16 logits: loss and logits gradient, incl. a non-unit incoming gradient."""
+    from paper_2501_08582_b200.decoder import CrossEntropyFunction
+    g = torch.Generator(device="cuda").manual_seed(N + V)
+    base = (3 * torch.randn(N, V, device="cuda", generator=g)).bfloat16()
+    t = torch.randint(0, V, (N,), device="cuda", generator=g)
+    lr = base.float().requires_grad_(True)
+    ref = F.cross_entropy(lr, t)
+    (2.5 * ref).backward()
+    logits = base.clone().requires_grad_(True)
+    x = logits * 1          # a non-leaf input, as the LM head output is
+    loss = CrossEntropyFunction.apply(x, t)
+    (2.5 * loss).backward()
+    assert abs(float(loss) - float(ref)) < 1e-3 * max(1.0, abs(float(ref)))
+    assert float((logits.grad.float() - lr.grad).norm() / lr.grad.norm()) < 1e-2
