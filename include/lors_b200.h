@@ -133,7 +133,9 @@ typedef struct lors_bwd_args {
 int lors_fwd(const lors_fwd_args* args, void* stream);
 /* Bytes of device workspace lors_fwd can use (0 = none): fp32 partials and
  * counters of the persistent walk's tail split along K.  A call given less
- * (or NULL) runs without the split; results differ only in fp32 summation order. */
+ * (or NULL) runs without the split; results differ only in fp32 summation order.
+ * A workspace (forward or backward) belongs to one call at a time: calls that
+ * may run concurrently (different streams) need separate workspaces. */
 size_t lors_fwd_workspace(const lors_fwd_args* args);
 
 /* Backward: dX_t = dY_t . W_eff (recomputed tiles); STE: dA = alpha dY^T P,
