@@ -589,8 +589,9 @@ class _nullenv:
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("with_bias", [False, True])
-def test_group_node_matches_separate_layers(P, with_bias):
+@pytest.mark.parametrize("with_bias,grad_mode,mask_mode", [(False, "ste", "from_w"), (True, "ste", "from_w"),
+                                                           (False, "masked", "bits")])
+def test_group_node_matches_separate_layers(P, with_bias, grad_mode, mask_mode):
     """LoRSGroupFunction (projections of one input on concurrent streams, one summed
     dX) against the same LoRSLinear layers called one by one: outputs bit-identical,
     adapter / bias / input gradients equal up to fp32 / bf16 summation order."""
@@ -604,7 +605,7 @@ def test_group_node_matches_separate_layers(P, with_bias):
         a = torch.randn(R, r, device="cuda", generator=g) * 0.05
         b = torch.randn(r, C, device="cuda", generator=g) * 0.2
         bias = torch.randn(R, device="cuda", generator=g) * 0.1 if with_bias else None
-        layers.append(LoRSLinear(w, a=a, b=b, alpha=2.0, bias=bias))
+        layers.append(LoRSLinear(w, a=a, b=b, alpha=2.0, bias=bias, grad_mode=grad_mode, mask_mode=mask_mode))
     x = torch.randn(3, L // 3, C, device="cuda", generator=g).bfloat16()
     dys = [torch.randn(3, L // 3, m.out_features, device="cuda", generator=g).bfloat16() for m in layers]
 
