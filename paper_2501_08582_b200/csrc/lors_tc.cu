@@ -1869,26 +1869,26 @@ __global__ void __launch_bounds__(mg::THREADS, 1)
     const int t = q * 32 + lane;             // TMEM lane = G row inside the tile
     const int gm_row = m0 + t;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    mbar_wait(gfull, 0);
-    tc_fence_after();
-    const uint32_t gmb = smem_u32(sGM);
-#pragma unroll 1
-    for (int cb = 0; cb < BN; cb += 32) {
-      uint32_t v[32];
-      tmem_ld_x32(tmem + lane_addr + G_COL + cb, v);
-      tmem_ld_wait();
-      uint32_t keepw = 0;   // keep bits for columns cb .. cb+31
-      const int gc = c0 + cb;
+    // The row's keep bits (M = W != 0, or the packed mask) for all 256 columns of
+    // the tile, gathered while the mainloop runs: the masking after it then only
+    // touches TMEM and shared memory.
+    uint32_t keep[BN / 32];
+#pragma unroll
+    for (int j = 0; j < BN / 32; ++j) {
+      uint32_t keepw = 0;   // keep bits for columns 32 j .. 32 j + 31
+      const int gc = c0 + 32 * j;
       if (gm_row < R) {
         if (BITS) {
-          keepw = __ldg(bits + (int64_t)gm_row * words_per_row + (gc >> 5));
-          if (gc + 32 > C) keepw &= (C - gc) >= 32 ? 0xFFFFFFFFu : ((1u << max(C - gc, 0)) - 1u);
+          if (gc < C) {
+            keepw = __ldg(bits + (int64_t)gm_row * words_per_row + (gc >> 5));
+            if (gc + 32 > C) keepw &= (1u << (C - gc)) - 1u;
+          }
         } else {
           const bf16* wr = w + (int64_t)gm_row * C + gc;
 #pragma unroll
           for (int u = 0; u < 32; u += 8) {
             if (gc + u + 8 <= C) {
-              const uint4 raw = *reinterpret_cast<const uint4*>(wr + u);
+              const uint4 raw = __ldg(reinterpret_cast<const uint4*>(wr + u));
               const uint32_t ww[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
@@ -1899,6 +1899,17 @@ __global__ void __launch_bounds__(mg::THREADS, 1)
           }
         }
       }
+      keep[j] = keepw;
+    }
+    mbar_wait(gfull, 0);
+    tc_fence_after();
+    const uint32_t gmb = smem_u32(sGM);
+#pragma unroll
+    for (int cb = 0; cb < BN; cb += 32) {
+      uint32_t v[32];
+      tmem_ld_x32(tmem + lane_addr + G_COL + cb, v);
+      tmem_ld_wait();
+      const uint32_t keepw = keep[cb / 32];
       uint32_t pk[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
