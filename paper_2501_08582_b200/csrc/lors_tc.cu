@@ -1783,8 +1783,10 @@ __global__ void __launch_bounds__(mg::THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + STAGES + 4);
 
   const int warp = warp_id(), lane = lane_id();
-  const int m0 = blockIdx.x * BM;   // R rows
-  const int c0 = blockIdx.y * BN;   // C cols
+  // consecutive CTAs walk the C tiles of one R panel: a wave covers a few dY_t column
+  // panels and all of X_t, which stays L2-resident across waves
+  const int m0 = blockIdx.y * BM;   // R rows
+  const int c0 = blockIdx.x * BN;   // C cols
   const int nk = (L + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
@@ -1988,7 +1990,7 @@ static int launch_masked_grad(const bf16* dy, const bf16* x, const bf16* w, cons
   const size_t smem = smem_bytes<RP>();
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "masked_grad smem attribute");
-  dim3 grid((unsigned)ceil_div(R, BM), (unsigned)ceil_div(C, BN));
+  dim3 grid((unsigned)ceil_div(C, BN), (unsigned)ceil_div(R, BM));
   kern<<<grid, THREADS, smem, s>>>(tDY, tX, tB, tA, w, bits, (int)ceil_div(C, 32), da, db, L, R, C, r, alpha);
   LORS_CHECK_LAUNCH("tc_masked_grad");
   return LORS_OK;
