@@ -1761,8 +1761,9 @@ template <int RP, bool BITS>
 __global__ void __launch_bounds__(mg::THREADS, 1)
     tc_masked_grad_kernel(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmX,
                           const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmA,
+                          const __grid_constant__ CUtensorMap tmDAo, const __grid_constant__ CUtensorMap tmDBo,
                           const bf16* __restrict__ w, const uint32_t* __restrict__ bits, int words_per_row,
-                          float* __restrict__ da, float* __restrict__ db, int L, int R, int C, int r, float alpha) {
+                          int L, int R, int C, int r, float alpha) {
   using namespace mg;
   constexpr uint32_t BT = bt_bytes<RP>(), AT = at_bytes<RP>();
   constexpr uint32_t SWR = RP * 2;
@@ -1933,38 +1934,46 @@ __global__ void __launch_bounds__(mg::THREADS, 1)
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(gmready);
-    // reduce the partials
+    // reduce the partials: alpha-scaled fp32 tiles staged in the drained pipeline's shared
+    // memory, added into dA / dB with TMA bulk reduce-adds (full-line L2 reductions):
+    //   dA  [128 R rows][RP]: SW128 boxes of [128 rows][32 floats], row t at lane t
+    //   dB  [RP rows][128 C] per C half (dB is [r, C]; TMEM lane t = C index): plain rows
     mbar_wait(cfull, 0);
     tc_fence_after();
     {
+      uint8_t* st_da = smem;                     // 16 / 16 / 32 KB
+      uint8_t* st_db = smem + 32768;             // 2 x RP x 512 B
       uint32_t v[32];
 #pragma unroll
-      for (int half = 0; half < RP / 32 + (RP < 32 ? 1 : 0); ++half) {
-        if (half * 32 >= RP) break;
-        tmem_ld_x32(tmem + lane_addr + DA_COL + half * 32, v);
+      for (int half = 0; half * 32 < RP; ++half) {
+        tmem_ld_x32(tmem + lane_addr + DA_COL + half * 32, v);   // (RP 16: 16 spare columns, skipped by the map)
         tmem_ld_wait();
-        if (gm_row < R) {
-          float* dst = da + (int64_t)gm_row * r + half * 32;
+        uint8_t* box = st_da + half * 16384 + t * 128;
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            if (half * 32 + j < r)
-              red_add_v4(dst + j, alpha * __uint_as_float(v[j]), alpha * __uint_as_float(v[j + 1]),
-                         alpha * __uint_as_float(v[j + 2]), alpha * __uint_as_float(v[j + 3]));
-        }
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(box + ((j ^ (t & 7)) << 4)) =
+              make_float4(alpha * __uint_as_float(v[4 * j]), alpha * __uint_as_float(v[4 * j + 1]),
+                          alpha * __uint_as_float(v[4 * j + 2]), alpha * __uint_as_float(v[4 * j + 3]));
       }
 #pragma unroll
       for (int hc = 0; hc < 2; ++hc) {
-        const int gc = c0 + hc * 128 + t;   // dB^T row = C index
+        float* rows = reinterpret_cast<float*>(st_db + hc * RP * 512);
 #pragma unroll
         for (int half = 0; half * 32 < RP; ++half) {
           tmem_ld_x32(tmem + lane_addr + DB_COL + hc * 64 + half * 32, v);
           tmem_ld_wait();
-          if (gc < C) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (half * 32 + j < r) atomicAdd(db + (int64_t)(half * 32 + j) * C + gc, alpha * __uint_as_float(v[j]));
-          }
+          for (int j = 0; j < 32; ++j)
+            if (half * 32 + j < RP) rows[(half * 32 + j) * 128 + t] = alpha * __uint_as_float(v[j]);
         }
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (warp == 2 && lane == 0) {
+        for (int half = 0; half * 32 < RP; ++half) tma_reduce_add_2d(&tmDAo, st_da + half * 16384, 32 * half, m0);
+        for (int hc = 0; hc < 2; ++hc) tma_reduce_add_2d(&tmDBo, st_db + hc * RP * 512, c0 + 128 * hc, 0);
+        tma_store_commit();
+        tma_store_wait_done();
       }
     }
   }
@@ -1984,6 +1993,9 @@ static int launch_masked_grad(const bf16* dy, const bf16* x, const bf16* w, cons
   if ((st = make_map(&tX, x, C, L, 64, 64, 128, "X (MN)"))) return st;
   if ((st = make_map(&tB, b, C, r, 64, RP, 128, "b tile (K-major, K = C)"))) return st;
   if ((st = make_map(&tA, a, r, R, RP, 128, RP * 2, "a tile (MN-major)"))) return st;
+  CUtensorMap tDAo, tDBo;   // fp32 outputs, reduce-added per tile
+  if ((st = make_map(&tDAo, da, r, R, 32, 128, 128, "dA fp32 (masked-G)", true))) return st;
+  if ((st = make_map(&tDBo, db, C, r, 128, RP, 0, "dB fp32 (masked-G)", true))) return st;
   LORS_CUDA_TRY(cudaMemsetAsync(da, 0, sizeof(float) * (size_t)R * r, s), "zero dA");
   LORS_CUDA_TRY(cudaMemsetAsync(db, 0, sizeof(float) * (size_t)r * C, s), "zero dB");
   auto kern = bits ? tc_masked_grad_kernel<RP, true> : tc_masked_grad_kernel<RP, false>;
@@ -1991,7 +2003,7 @@ static int launch_masked_grad(const bf16* dy, const bf16* x, const bf16* w, cons
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "masked_grad smem attribute");
   dim3 grid((unsigned)ceil_div(C, BN), (unsigned)ceil_div(R, BM));
-  kern<<<grid, THREADS, smem, s>>>(tDY, tX, tB, tA, w, bits, (int)ceil_div(C, 32), da, db, L, R, C, r, alpha);
+  kern<<<grid, THREADS, smem, s>>>(tDY, tX, tB, tA, tDAo, tDBo, w, bits, (int)ceil_div(C, 32), L, R, C, r, alpha);
   LORS_CHECK_LAUNCH("tc_masked_grad");
   return LORS_OK;
 }
