@@ -664,6 +664,9 @@ constexpr int BM = 128, BN = 256, BK = 64;
 #ifndef LORS_N2
 #define LORS_N2 128
 #endif
+#ifndef LORS_NW_DENSE
+#define LORS_NW_DENSE 4
+#endif
 #ifndef LORS_PERSIST
 #define LORS_PERSIST 1
 #endif
@@ -692,7 +695,7 @@ constexpr int bnt() { return 256 + n2<SP>(); }            // tokens per pair til
 template <bool SP>
 constexpr int ne() { return SP ? 3 : (512 - 256 - n2<SP>()) / 64; }
 template <bool SP>
-constexpr int nw() { return SP ? 6 : 4; }  // W ring
+constexpr int nw() { return SP ? 6 : LORS_NW_DENSE; }  // W ring
 template <bool SP>
 constexpr int na() { return SP ? 4 : 3; }  // activation ring = W_eff buffers
 template <bool SP>
