@@ -2011,9 +2011,337 @@ static int launch_masked_grad(const bf16* dy, const bf16* x, const bf16* w, cons
   return LORS_OK;
 }
 
+// ===========================================================================
+// K5 on CTA pairs: the masked-G adapter gradient with the G mainloop as
+// tcgen05 cta_group::2 MMAs (M = 256 rows of R over the pair, each CTA staging
+// its 128 dY columns and half of the 256 X columns: 32 KB per SM per k-step
+// instead of 48), and the two small contractions as warp-level mma.sync on
+// each CTA's own masked rows:
+//   dA[own 128 R x r]   = (G.M)_own [128 x 256 C] . b^T[256 C x r]
+//   dB^T[256 C x r]    += (G.M)_own^T [256 C x 128 R] . a[own 128 R x r]
+// so no CTA needs its peer's G.M; both partials leave through TMA reduce-adds.
+// warps: 0 TMA producer, 1 MMA issuer (leader) / TMA relay (peer), 2..5 mask,
+// contract, reduce.
+// ===========================================================================
+namespace mgp {
+constexpr int BK = 64, STAGES = 4, THREADS = 192;
+constexpr uint32_t A_BYTES = 128 * BK * 2;      // 16 KB  dY_t [64 tokens][128 R]  (2 MN atoms)
+constexpr uint32_t B_BYTES = 128 * BK * 2;      // 16 KB  X_t  [64 tokens][128 C]  (this CTA's half of N)
+constexpr uint32_t PIPE = STAGES * (A_BYTES + B_BYTES);   // 128 KB, reused after the mainloop:
+constexpr uint32_t GM_OFF = 0, DA_OFF = 65536, DB_OFF = 98304;   // G.M 64 KB, dA 32 KB, dB 64 KB (+32 KB past PIPE)
+constexpr uint32_t EXTRA = 32768;
+template <int RP>
+constexpr uint32_t bt_bytes() { return RP * 256 * 2; }   // b [RP rows][256 C], 4 SW128 atoms of [RP][64]
+template <int RP>
+constexpr uint32_t at_bytes() { return 128 * RP * 2; }   // a [128 R][RP], swizzle span RP * 2
+template <int RP>
+constexpr size_t smem_bytes() { return 1024 + PIPE + EXTRA + bt_bytes<RP>() + at_bytes<RP>() + 256; }
+}  // namespace mgp
+
+template <int RP, bool BITS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(mgp::THREADS, 1)
+    tc_masked_grad_pair_kernel(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmX,
+                               const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmA,
+                               const __grid_constant__ CUtensorMap tmDAo, const __grid_constant__ CUtensorMap tmDBo,
+                               const bf16* __restrict__ w, const uint32_t* __restrict__ bits, int words_per_row,
+                               int L, int R, int C, float alpha) {
+  using namespace mgp;
+  constexpr uint32_t BT = bt_bytes<RP>(), AT = at_bytes<RP>();
+  constexpr uint32_t SWA = RP * 2;              // a tile swizzle span (bytes)
+  constexpr int NT = RP / 8;                    // n8 tiles of the contractions
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                            // [STAGES] dY tiles
+  uint8_t* sB = sA + STAGES * A_BYTES;           // [STAGES] X half tiles
+  uint8_t* sBt = smem + PIPE + EXTRA;            // b tile
+  uint8_t* sAt = sBt + BT;                       // a tile (own rows)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sAt + AT);
+  uint64_t* full = bars;                         // [STAGES] (leader: own producer + peer relay)
+  uint64_t* empty = full + STAGES;               // [STAGES] (leader's commit, multicast)
+  uint64_t* gfull = empty + STAGES;              // G accumulated (multicast)
+  uint64_t* abfull = gfull + 1;                  // a / b tiles landed (own)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(abfull + 1);
+
+  const int warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int m0 = (int)blockIdx.z * 256 + (int)rank * 128;   // this CTA's R rows
+  const int c0 = (int)blockIdx.y * 256;                       // the pair's C columns
+  const int nk = (L + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], leader ? 2 : 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(gfull, 1);
+    mbar_init(abfull, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tmDY);
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmA);
+  }
+  if (warp == 1) tmem_alloc_pair<256>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();                                // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t full_l = mapa_shared(smem_u32(full), 0);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(abfull, BT + AT);
+      for (int q = 0; q < 4; ++q) tma_load_2d(sBt + q * (RP * 128), &tmB, abfull, c0 + 64 * q, 0);
+      tma_load_2d(sAt, &tmA, abfull, 0, m0);
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % STAGES;
+        mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
+        const int l0 = i * BK;
+        uint8_t* a = sA + s * A_BYTES;
+        uint8_t* b = sB + s * B_BYTES;
+        tma_load_2d(a, &tmDY, &full[s], m0, l0);
+        tma_load_2d(a + A_BYTES / 2, &tmDY, &full[s], m0 + 64, l0);
+        tma_load_2d(b, &tmX, &full[s], c0 + 128 * (int)rank, l0);
+        tma_load_2d(b + B_BYTES / 2, &tmX, &full[s], c0 + 128 * (int)rank + 64, l0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      if (!leader) {
+        // relay: this CTA's tiles landed -> one arrival on the leader's barrier
+        for (int i = 0; i < nk; ++i) {
+          const int s = i % STAGES;
+          mbar_wait(&full[s], (i / STAGES) & 1);
+          mbar_arrive_cluster(full_l + s * 8);
+        }
+      } else {
+        constexpr uint32_t idesc_g = make_idesc_bf16(256, 256, true, true);
+        for (int i = 0; i < nk; ++i) {
+          const int s = i % STAGES;
+          mbar_wait(&full[s], (i / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + s * A_BYTES), b_base = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            mma_bf16_pair(tmem, make_sdesc(a_base + kk * 2048, A_BYTES / 2, 1024, SW_128),
+                          make_sdesc(b_base + kk * 2048, B_BYTES / 2, 1024, SW_128), idesc_g,
+                          (i > 0 || kk > 0) ? 1u : 0u);
+          mma_commit_pair(&empty[s], 0x3);
+        }
+        mma_commit_pair(gfull, 0x3);
+      }
+    }
+  } else {
+    const int q = warp & 3, ew = warp - 2;       // TMEM lane quarter; epilogue warp 0..3
+    const int t = q * 32 + lane;                 // G row (TMEM lane) inside this CTA's tile
+    const int gm_row = m0 + t;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    // keep bits of this row's 256 columns, gathered while the mainloop runs
+    uint32_t keep[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t keepw = 0;
+      const int gc = c0 + 32 * j;
+      if (gm_row < R) {
+        if (BITS) {
+          if (gc < C) {
+            keepw = __ldg(bits + (int64_t)gm_row * words_per_row + (gc >> 5));
+            if (gc + 32 > C) keepw &= (1u << (C - gc)) - 1u;
+          }
+        } else {
+          const bf16* wr = w + (int64_t)gm_row * C + gc;
+#pragma unroll
+          for (int u = 0; u < 32; u += 8) {
+            if (gc + u + 8 <= C) {
+              const uint4 raw = __ldg(reinterpret_cast<const uint4*>(wr + u));
+              const uint32_t ww[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const uint32_t nz = nonzero_mask_bf16x2(ww[e]);
+                keepw |= ((nz & 1u) | ((nz >> 15) & 2u)) << (u + 2 * e);
+              }
+            }
+          }
+        }
+      }
+      keep[j] = keepw;
+    }
+    mbar_wait(gfull, 0);
+    tc_fence_after();
+    // 1. mask G into bf16 G.M: 4 K-major SW128 atoms [128 R][64 C] at GM_OFF
+    const uint32_t gmb = smem_u32(smem + GM_OFF);
+#pragma unroll
+    for (int cb = 0; cb < 256; cb += 32) {
+      uint32_t v[32];
+      tmem_ld_x32(tmem + lane_addr + cb, v);
+      tmem_ld_wait();
+      const uint32_t keepw = keep[cb / 32];
+      uint32_t pk[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const float g0 = ((keepw >> (2 * e)) & 1u) ? __uint_as_float(v[2 * e]) : 0.0f;
+        const float g1 = ((keepw >> (2 * e + 1)) & 1u) ? __uint_as_float(v[2 * e + 1]) : 0.0f;
+        pk[e] = pack_bf16x2(g0, g1);
+      }
+      const uint32_t atom = gmb + (cb >> 6) * 16384 + t * 128;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const uint32_t chunk = ((((cb & 63) >> 3) + cc) ^ (t & 7)) << 4;
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(atom + chunk), "r"(pk[4 * cc]),
+                     "r"(pk[4 * cc + 1]), "r"(pk[4 * cc + 2]), "r"(pk[4 * cc + 3])
+                     : "memory");
+      }
+    }
+    mbar_wait(abfull, 0);
+    named_bar_sync(1, 128);                      // every row of G.M parked
+    const int g = lane >> 2, qd = lane & 3;
+    const uint32_t bt = smem_u32(sBt), at = smem_u32(sAt);
+    // 2. dA rows 32 ew .. +31 (two m16 tiles), K = 256 C
+    {
+      float acc[2][NT][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.f;
+#pragma unroll 4
+      for (int ks = 0; ks < 16; ++ks) {
+        uint32_t af[2][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int row = 32 * ew + 16 * mt + (lane & 7) + 8 * ((lane >> 3) & 1);
+          const int k = 16 * ks + 8 * (lane >> 4);
+          ldsm_x4(gmb + (k >> 6) * 16384 + row * 128 + ((((k & 63) >> 3) ^ (row & 7)) << 4), af[mt]);
+        }
+#pragma unroll
+        for (int np = 0; np < NT / 2; ++np) {
+          uint32_t bf[4];
+          const int n = 16 * np + (lane & 7) + 8 * (lane >> 4);
+          const int k = 16 * ks + 8 * ((lane >> 3) & 1);
+          ldsm_x4(bt + (k >> 6) * (RP * 128) + n * 128 + ((((k & 63) >> 3) ^ (n & 7)) << 4), bf);
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            mma_16816(acc[mt][2 * np], af[mt], bf[0], bf[1]);
+            mma_16816(acc[mt][2 * np + 1], af[mt], bf[2], bf[3]);
+          }
+        }
+      }
+      // stage alpha dA into SW128 boxes [128 rows][32 floats] (box = column / 32)
+      uint8_t* st = smem + DA_OFF;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int hr = 0; hr < 2; ++hr) {
+            const int row = 32 * ew + 16 * mt + g + 8 * hr, n = 8 * nt + 2 * qd;
+            const int chunk = (n & 31) >> 2;
+            *reinterpret_cast<float2*>(st + (n >> 5) * 16384 + row * 128 + ((chunk ^ (row & 7)) << 4) + (n & 3) * 4) =
+                make_float2(alpha * acc[mt][nt][2 * hr], alpha * acc[mt][nt][2 * hr + 1]);
+          }
+    }
+    // 3. dB^T rows (C) 64 ew .. +63 in two halves of 32, K = 128 own R rows
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      float acc[2][NT][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.f;
+#pragma unroll 2
+      for (int ks = 0; ks < 8; ++ks) {
+        uint32_t af[2][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int j = lane >> 3;               // matrix: (k 0-7 | 8-15) x (m 0-7 | 8-15)
+          const int k = 16 * ks + (lane & 7) + 8 * (j >> 1);
+          const int m = 64 * ew + 32 * h + 16 * mt + 8 * (j & 1);
+          ldsm_x4_trans(gmb + (m >> 6) * 16384 + k * 128 + ((((m & 63) >> 3) ^ (k & 7)) << 4), af[mt]);
+        }
+#pragma unroll
+        for (int np = 0; np < NT / 2; ++np) {
+          uint32_t bf[4];
+          const int j = lane >> 3;
+          const int k = 16 * ks + (lane & 7) + 8 * (j & 1);
+          const int n = 16 * np + 8 * (j >> 1);
+          const uint32_t off = (uint32_t)(k * SWA + n * 2);
+          ldsm_x4_trans(at + (off ^ (((off >> 7) & (SWA / 16 - 1)) << 4)), bf);
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            mma_16816(acc[mt][2 * np], af[mt], bf[0], bf[1]);
+            mma_16816(acc[mt][2 * np + 1], af[mt], bf[2], bf[3]);
+          }
+        }
+      }
+      // stage alpha dB^T into [RP rows][128 C] plain boxes per C half (dB is [r, C])
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int hr = 0; hr < 2; ++hr) {
+            const int c = 64 * ew + 32 * h + 16 * mt + g + 8 * hr, n = 8 * nt + 2 * qd;
+            float* rows = reinterpret_cast<float*>(smem + DB_OFF + (c >> 7) * (RP * 512));
+            rows[n * 128 + (c & 127)] = alpha * acc[mt][nt][2 * hr];
+            rows[(n + 1) * 128 + (c & 127)] = alpha * acc[mt][nt][2 * hr + 1];
+          }
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (ew == 0 && lane == 0) {
+      for (int hf = 0; hf * 32 < RP; ++hf) tma_reduce_add_2d(&tmDAo, smem + DA_OFF + hf * 16384, 32 * hf, m0);
+      for (int hc = 0; hc < 2; ++hc) tma_reduce_add_2d(&tmDBo, smem + DB_OFF + hc * RP * 512, c0 + 128 * hc, 0);
+      tma_store_commit();
+      tma_store_wait_done();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) tmem_dealloc_pair<256>(tmem);
+}
+
+template <int RP>
+static int launch_masked_grad_pair(const bf16* dy, const bf16* x, const bf16* w, const uint32_t* bits, const bf16* a,
+                                   const bf16* b, float* da, float* db, int L, int R, int C, int r, float alpha,
+                                   cudaStream_t s) {
+  using namespace mgp;
+  CUtensorMap tDY, tX, tB, tA, tDAo, tDBo;
+  int st;
+  if ((st = make_map(&tDY, dy, R, L, 64, 64, 128, "dY (MN)"))) return st;
+  if ((st = make_map(&tX, x, C, L, 64, 64, 128, "X (MN)"))) return st;
+  if ((st = make_map(&tB, b, C, r, 64, RP, 128, "b tile (K-major, K = C)"))) return st;
+  if ((st = make_map(&tA, a, r, R, RP, 128, RP * 2, "a tile"))) return st;
+  if ((st = make_map(&tDAo, da, r, R, 32, 128, 128, "dA fp32 (masked-G)", true))) return st;
+  if ((st = make_map(&tDBo, db, C, r, 128, RP, 0, "dB fp32 (masked-G)", true))) return st;
+  LORS_CUDA_TRY(cudaMemsetAsync(da, 0, sizeof(float) * (size_t)R * r, s), "zero dA");
+  LORS_CUDA_TRY(cudaMemsetAsync(db, 0, sizeof(float) * (size_t)r * C, s), "zero dB");
+  auto kern = bits ? tc_masked_grad_pair_kernel<RP, true> : tc_masked_grad_pair_kernel<RP, false>;
+  const size_t smem = smem_bytes<RP>();
+  LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                "masked_grad_pair smem attribute");
+  dim3 grid(2, (unsigned)ceil_div(C, 256), (unsigned)ceil_div(R, 256));
+  kern<<<grid, THREADS, smem, s>>>(tDY, tX, tB, tA, tDAo, tDBo, w, bits, (int)ceil_div(C, 32), L, R, C, alpha);
+  LORS_CHECK_LAUNCH("tc_masked_grad_pair");
+  return LORS_OK;
+}
+
 static int masked_grad_tc(int rp, const bf16* dy, const bf16* x, const bf16* w, const uint32_t* bits, const bf16* a,
                           const bf16* b, float* da, float* db, int L, int R, int C, int r, float alpha,
                           cudaStream_t s) {
+  static const bool single = getenv("LORS_K5_SINGLE") != nullptr;   // the one-CTA kernel, for A/B runs
+  if (!single) {
+    switch (rp) {
+      case 16: return launch_masked_grad_pair<16>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s);
+      case 32: return launch_masked_grad_pair<32>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s);
+      default: return launch_masked_grad_pair<64>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s);
+    }
+  }
   switch (rp) {
     case 16: return launch_masked_grad<16>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s);
     case 32: return launch_masked_grad<32>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s);

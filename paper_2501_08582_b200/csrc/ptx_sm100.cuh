@@ -408,6 +408,21 @@ __device__ __forceinline__ void ldsm_x4_trans(uint32_t saddr, uint32_t (&v)[4]) 
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
                : "r"(saddr));
 }
+// four 8x8 b16 matrices: thread l gets, per matrix i, (stored row l/4 ; columns 2(l%4), +1)
+__device__ __forceinline__ void ldsm_x4(uint32_t saddr, uint32_t (&v)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(saddr));
+}
+// warp-level D[16x8] += A[16x16] . B[16x8], bf16 in, fp32 accumulate (the small contractions
+// of the pair masked-G kernel, whose tensor-core MMAs are cta_group::2)
+__device__ __forceinline__ void mma_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
 __device__ __forceinline__ void lds128(uint32_t saddr, uint32_t (&v)[4]) {
   asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(saddr));
 }
