@@ -225,6 +225,12 @@ def _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, 
         da = buf[:R * r * 4].view(torch.float32).view(R, r)
         db = buf[da_b:da_b + r * C * 4].view(torch.float32).view(r, C)
         args.flags |= N.FLAG_ZEROED
+        if launch_stream is not None:
+            # the fill ran on the current stream, after the caller's fork: order it
+            # before the kernels on the launch stream
+            filled = torch.cuda.Event()
+            filled.record(torch.cuda.current_stream(dev))
+            launch_stream.wait_event(filled)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev) if ws_bytes else None
     args.dy, args.p, args.dx, args.da, args.db, args.dbias = _p(dy_t), _p(p), _p(dx), _p(da), _p(db), _p(dbias)
     args.workspace, args.workspace_bytes = _p(ws), ws_bytes
