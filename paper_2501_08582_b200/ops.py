@@ -164,8 +164,9 @@ def lors_bwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
         fork.record(main)
         hi.wait_event(fork)
         side.wait_event(fork)
-        dx = _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, True, False, fault_da_sign,
-                            dx_only=True, launch_stream=hi)[0]
+        # (the dX call's workspace -- tail-split partials -- is held until the joins below)
+        dx, _, _, _, ws_dx = _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, True, False,
+                                            fault_da_sign, dx_only=True, launch_stream=hi)
         # Every buffer comes from the current stream's pool, and the current stream
         # waits for both side streams before this call returns, so any later reuse
         # of these blocks is ordered after the side work: no record_stream (whose
