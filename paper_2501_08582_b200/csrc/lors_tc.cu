@@ -9,13 +9,16 @@
 //        rounds to bf16 and writes the swizzled operand tile to shared memory,
 //        which the main MMA consumes.  W_eff never touches HBM.
 //        Dense kernels: 256 features x 384 tokens per CTA pair (two accumulators),
-//        persistent over the tile raster; the 2:4 kernel (tcgen05.mma.sp) keeps
-//        256-token tiles, one per launch.  DESIGN.md section 3 has the pipeline.
-//   K4 tc_skinny            the rank-r products P = X b^T, Q = dY a,
-//        dA = alpha dY^T P, dB = alpha Q^T X (adapters.py:396-399), N = r,
-//        split-K into fp32 accumulators.
-//   K5 tc_masked_grad       G = (dY^T X) . M in TMEM, contracted into dA / dB
-//        (the sqft_gc comparator's masked gradient, adapters.py:303-312).
+//        persistent over the tile raster, the last wave's tiles optionally cut
+//        along K (tail split); the 2:4 kernel (tcgen05.mma.sp) keeps 256-token
+//        tiles, one per launch.  DESIGN.md section 3 has the pipeline.
+//   K4 tc_skinny            rank-r products P = X b^T and dB = alpha Q^T X
+//        (adapters.py:396, 399), N = r, split-K into fp32 accumulators.
+//   K4b tc_q_da             Q = dY a and dA = alpha dY^T P from one pass over dY
+//        (adapters.py:397-398), partials by TMA bulk reduce-add.
+//   K5 tc_masked_grad_pair  G = (dY^T X) . M in TMEM on CTA pairs, contracted into
+//        dA / dB (the sqft_gc masked gradient, adapters.py:303-312); the one-CTA
+//        tc_masked_grad is kept for A/B runs (LORS_K5_SINGLE).
 //
 // Timing-experiment switches (tools/exp_variants.sh, never set in the product
 // build): LORS_EXP_NO_RECOMPUTE / _NO_XFORM / _NO_W_TMA / _NO_ACT_TMA skip one
