@@ -658,3 +658,68 @@ def test_overlapped_backward_with_tail_split_is_deterministic(P):
         assert torch.equal(o[0], ref[0])
         for u, v in zip(o[1:3], ref[1:3]):
             assert float((u - v).norm() / v.norm()) < 1e-3
+
+
+def test_central_finite_differences_fp32(P):
+    """Central finite differences through the GPU path (fp32 FFMA mode), the reference's own check
+    (test_adapters.py:138-187, bench.py:97-111): loss = <Y, G>; dX against FD of the masked function,
+    dA / dB against FD of the unmasked surrogate W + alpha a b (STE).  The loss is linear in each of
+    X, a, b, so central differences are exact up to fp32 rounding."""
+    from paper_2501_08582_b200 import ops
+    rng = np.random.default_rng(7)
+    R, C, L, r, alpha, eps = 6, 5, 4, 2, 2.0, 0.25
+    w = rng.normal(size=(R, C)) * 0.5
+    w[rng.random((R, C)) < 0.4] = 0.0
+    a, b = rng.normal(size=(R, r)) * 0.3, rng.normal(size=(r, C)) * 0.3
+    x, gy = rng.normal(size=(L, C)), rng.normal(size=(L, R))
+    d = lambda t: _dev(t, torch.float32)  # noqa: E731
+
+    def loss(wm, am, bm, xm):
+        y, _ = ops.lors_fwd(d(xm), d(wm), d(am), d(bm), alpha)
+        return float((y.double().cpu().numpy() * gy).sum())
+
+    dx, da, db, _ = ops.lors_bwd(d(x), d(w), d(a), d(b), d(gy), alpha)
+    fd_x = np.zeros_like(x)
+    for i in range(L):
+        for j in range(C):
+            e = np.zeros_like(x)
+            e[i, j] = eps
+            fd_x[i, j] = (loss(w, a, b, x + e) - loss(w, a, b, x - e)) / (2 * eps)
+    # the unmasked surrogate: every entry of W treated as kept (a dense W with the same values where
+    # kept and a tiny nonzero elsewhere keeps all positions "on" without changing the kept values)
+    w_dense = np.where(w == 0.0, 1e-30, w)
+    fd_a, fd_b = np.zeros_like(a), np.zeros_like(b)
+    for i in range(R):
+        for j in range(r):
+            e = np.zeros_like(a)
+            e[i, j] = eps
+            fd_a[i, j] = (loss(w_dense, a + e, b, x) - loss(w_dense, a - e, b, x)) / (2 * eps)
+    for i in range(r):
+        for j in range(C):
+            e = np.zeros_like(b)
+            e[i, j] = eps
+            fd_b[i, j] = (loss(w_dense, a, b + e, x) - loss(w_dense, a, b - e, x)) / (2 * eps)
+    assert _rel(dx, fd_x) <= 1e-5
+    assert _rel(da, fd_a) <= 1e-5
+    assert _rel(db, fd_b) <= 1e-5
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
+def test_all_ones_mask_collapses_masked_onto_ste(P, dt):
+    """With no pruned entries, the masked-G gradients (sqft_gc) equal the STE ones (lors) -- the
+    reference's acceptance criterion (1) collapse (test_acceptance.py:90-148), on both kernels' paths."""
+    from paper_2501_08582_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(9)
+    L, R, C, r = 700, 512, 768, 16
+    w = (torch.randn(R, C, device="cuda", generator=g) * 0.02 + 0.05).to(dt)     # no zeros
+    assert bool((w != 0).all())
+    a = (torch.randn(R, r, device="cuda", generator=g) * 0.05).to(dt)
+    b = (torch.randn(r, C, device="cuda", generator=g) * 0.2).to(dt)
+    x = torch.randn(L, C, device="cuda", generator=g).to(dt)
+    dy = torch.randn(L, R, device="cuda", generator=g).to(dt)
+    s = ops.lors_bwd(x, w, a, b, dy, 2.0, grad_mode="ste", overlap=False)
+    m = ops.lors_bwd(x, w, a, b, dy, 2.0, grad_mode="masked", overlap=False)
+    tol = 1e-5 if dt == torch.float32 else 2e-2
+    assert torch.equal(s[0], m[0])
+    for u, v in zip(s[1:3], m[1:3]):
+        assert float((u - v).norm() / v.norm()) <= tol
