@@ -723,3 +723,28 @@ def test_all_ones_mask_collapses_masked_onto_ste(P, dt):
     assert torch.equal(s[0], m[0])
     for u, v in zip(s[1:3], m[1:3]):
         assert float((u - v).norm() / v.norm()) <= tol
+
+
+@pytest.mark.parametrize("L", [1, 3, 17, 129])
+@pytest.mark.parametrize("grad_mode", ["ste", "masked"])
+def test_tiny_token_counts_bf16(P, L, grad_mode):
+    """A handful of tokens through every tensor-core kernel (persistent GEMMs, Q/dA pass, K5 pairs):
+    forward, dX and adapter gradients against the float64 oracle on the bf16-rounded inputs."""
+    from paper_2501_08582_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(L)
+    R, C, r = 520, 264, 24
+    w = torch.randn(R, C, device="cuda", generator=g) * 0.02
+    w = torch.where(w.abs() < 0.012, torch.zeros_like(w), w).bfloat16()
+    a = (torch.randn(R, r, device="cuda", generator=g) * 0.05).bfloat16()
+    b = (torch.randn(r, C, device="cuda", generator=g) * 0.2).bfloat16()
+    x = torch.randn(L, C, device="cuda", generator=g).bfloat16()
+    dy = torch.randn(L, R, device="cuda", generator=g).bfloat16()
+    y, _ = ops.lors_fwd(x, w, a, b, 2.0)
+    dx, da, db, _ = ops.lors_bwd(x, w, a, b, dy, 2.0, grad_mode=grad_mode)
+    wn, an, bn, xn, dyn = (t.double().cpu().numpy() for t in (w, a, b, x, dy))
+    assert _rel(y, orc.lors_forward(wn, an, bn, xn.T, 2.0).T) <= 2e-2
+    ref = (orc.lors_backward(wn, an, bn, xn.T, dyn.T, 2.0) if grad_mode == "ste"
+           else orc.sqft_gc_backward(wn, an, bn, xn.T, dyn.T, 2.0))
+    assert _rel(dx, ref.dx.T) <= 2e-2
+    assert _rel(da, ref.da) <= 2e-2
+    assert _rel(db, ref.db) <= 2e-2
