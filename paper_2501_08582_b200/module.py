@@ -165,10 +165,15 @@ class LoRSGroupFunction(torch.autograd.Function):
         ab = [(compute_copy(As[i], dt), compute_copy(Bs[i], dt)) for i in range(n)]   # read at backward time
         need_dx = ctx.needs_input_grad[0]
         main = torch.cuda.current_stream(dev)
-        streams, side = ops.group_streams(dev, n)
+        # rank-r products of each projection on their own normal-priority stream (LORS_GROUP_SIDE=1:
+        # one shared stream), so the small HBM-bound kernels of different projections overlap
+        n_side = 1 if os.environ.get("LORS_GROUP_SIDE", "n") == "1" else n
+        streams, sides = ops.group_streams(dev, n, n_side)
+        sides = sides if isinstance(sides, list) else [sides]
         fork = torch.cuda.Event()
         fork.record(main)
-        side.wait_event(fork)
+        for sd in sides:
+            sd.wait_event(fork)
         dxs, res, keep = [], [], []
         for i, prm in enumerate(params_list):
             if need_dx:
@@ -180,10 +185,10 @@ class LoRSGroupFunction(torch.autograd.Function):
                 keep.append(ws)
             _, da, db, dbias, ws = ops._lors_bwd_call(x2, weights[i], ab[i][0], ab[i][1], dys[i], prm.alpha, None,
                                                       prm.mask_bits, prm.grad_mode, False, has_bias[i],
-                                                      prm.fault_da_sign, launch_stream=side)
+                                                      prm.fault_da_sign, launch_stream=sides[i % len(sides)])
             res.append((da, db, dbias))
             keep.append(ws)
-        for st in (streams if need_dx else []) + [side]:
+        for st in (streams if need_dx else []) + sides:
             ev = torch.cuda.Event()
             ev.record(st)
             main.wait_event(ev)

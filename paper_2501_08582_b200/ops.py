@@ -113,15 +113,16 @@ def lors_fwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
 _GROUP_STREAMS = {}
 
 
-def group_streams(dev: torch.device, n: int):
-    """n high-priority streams (one per concurrent LoRS GEMM) and one normal-priority
-    stream for the rank-r products, created once per device and reused."""
+def group_streams(dev: torch.device, n: int, n_side: int = 1):
+    """n high-priority streams (one per concurrent LoRS GEMM) and `n_side` normal-priority
+    streams for the rank-r products (a list when n_side > 1), created once per device."""
     pool = _GROUP_STREAMS.get(dev.index)
-    if pool is None or len(pool[0]) < n:
+    if pool is None or len(pool[0]) < n or len(pool[1]) < n_side:
         lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
-        pool = ([torch.cuda.Stream(device=dev, priority=hi) for _ in range(max(n, 3))], torch.cuda.Stream(device=dev))
+        pool = ([torch.cuda.Stream(device=dev, priority=hi) for _ in range(max(n, 3))],
+                [torch.cuda.Stream(device=dev) for _ in range(max(n_side, 3))])
         _GROUP_STREAMS[dev.index] = pool
-    return pool[0][:n], pool[1]
+    return pool[0][:n], (pool[1][:n_side] if n_side > 1 else pool[1][0])
 
 
 _SIDE_STREAMS = {}
