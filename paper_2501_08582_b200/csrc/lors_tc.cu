@@ -752,7 +752,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
                         const __grid_constant__ CUtensorMap tmOut, const bf16* __restrict__ bias,
                         const uint32_t* __restrict__ bits, const uint8_t* __restrict__ meta24, int words_per_row,
                         int Mout, int Kred, int n_t, int n_f, int split, float* __restrict__ partials,
-                        unsigned int* __restrict__ counters, float alpha) {
+                        unsigned int* __restrict__ counters, float alpha, int n_tok) {
   using namespace rg;
   static_assert(!(SP && DX), "2:4 sparse tensor cores apply to the forward only (SURVEY C6)");
   constexpr int XW = xw<SP>(), XFORM_THREADS = 32 * XW;
@@ -1049,8 +1049,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         }
         __syncwarp();
       };
+      bool main_n2 = true;   // the second MMA's tokens (l0 + 256 ..) hold valid rows in this unit
       auto do_main = [&](const int jm, const int mk, const int mn, const int mlen) {
         if (PERSIST && mk == 0 && mn > 0) mbar_wait(acc_empty, (mn - 1) & 1);  // previous tile drained
+        if (N2 && mk == 0) {   // a ragged last token tile: skip the all-padding N2 MMA (a third of it)
+          int m_, l_, kb_, ke_, ut_, pt_;
+          unit(mn, m_, l_, kb_, ke_, ut_, pt_);
+          main_n2 = l_ + 256 < n_tok;
+        }
         const int a = jm % NA;
         mbar_wait(&mready[a].b, (jm / NA) & 1);
         tc_fence_after();
@@ -1067,7 +1073,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk)
               mma_bf16_pair(tmem, ad + kk * 2, bd + kk * 2, idesc_main, (mk > 0 || kk > 0) ? 1u : 0u);
-            if (N2) {  // tokens 256 .. 256 + N2 into the second accumulator
+            if (N2 && main_n2) {  // tokens 256 .. 256 + N2 into the second accumulator
               const uint64_t bd2 = bd + (ACT1_BYTES >> 4);
 #pragma unroll
               for (int kk = 0; kk < BK / 16; ++kk)
@@ -1704,7 +1710,7 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
   }
   kern<<<grid, threads<SP>(), smem, s>>>(tAct, tAct2, tW, tS, tF, tOut, bias, bits, SP ? meta24 : nullptr,
                                          (int)ceil_div(C, 32), Mout, Kred, n_t, n_f, split, partials, counters,
-                                         alpha);
+                                         alpha, L);
   LORS_CHECK_LAUNCH(DX ? "tc_lors_gemm<dx>" : "tc_lors_gemm<fwd>");
   return LORS_OK;
 }
