@@ -296,7 +296,7 @@ def test_flat_adamw_matches_torch_adamw():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("D,rows", [(4096, 700), (256, 33), (5120, 64), (2056, 5)])
+@pytest.mark.parametrize("D,rows", [(4096, 700), (256, 33), (5120, 64), (2056, 5), (8192, 3), (8, 2)])
 def test_fused_add_rmsnorm_matches_torch(D, rows):
     """lors_add_rmsnorm / _bwd against the torch formula (h + o, F.rms_norm) in fp32: forward outputs
     and the gradient that reaches h and o (residual + norm paths)."""
