@@ -1,21 +1,26 @@
 #!/usr/bin/env python
-"""Benchmark of the LoRS masked-LoRA linear hot path (fwd+bwd) on B200.
+"""Benchmark of the LoRS masked-LoRA linear hot path on B200.
 
-Workload (BASELINE.json configs[1], the single-GPU configuration the metric is
-quoted on): one LoRS MLP projection, W 11008 x 4096 bf16 ~ N(0, 0.02^2) with
-2:4 magnitude sparsity, rank r = 64 (a ~ N(0, 1e-3^2), b ~ N(0, 1/r); SURVEY
-C2), alpha = 2.0, X = 8192 tokens x 4096 ~ N(0,1), dY ~ N(0,1), seeded
-synthetic data.  One step = forward (Y) + backward (dX, dA, dB) of the layer;
-with N > 1 GPUs every rank runs its own 8192 tokens (weak scaling) and the
-adapter gradients dA/dB are averaged with one NCCL all-reduce per step (the
-only exchange the path has).
+BASELINE.json's metric is "fine-tune tokens/s (fwd+bwd) at 1/2/4/8 B200 vs roofline; peak HBM GB" and
+north_star's target is stated on LLaMA-2-7B-shaped 50%-sparse layers, so the default workload is
+BASELINE configs[2] (cfg3): one fine-tuning step of a LLaMA-2-7B-shaped decoder (32 layers, d 4096,
+SwiGLU 11008, vocab 32000, random init) whose 7 projections per layer are LoRS linears (50% per-row
+magnitude masks, r = 16), bf16, seq 1024 x batch 4 per GPU, uniform token ids, next-token CE, the
+adapter gradients averaged with NCCL (N > 1), AdamW on the adapters.  Weak scaling: every rank runs
+its own batch.  The line also carries the dominant kernel's roofline (the LoRS GEMM, timed live), the
+single-projection configs[1] (cfg2) numbers with their spec / 2:4-sparse roofline fractions, peak HBM,
+the end-to-end rate through Trainer.step with host token ids, and the reference algorithm's CPU rate.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
-                    [--config cfg2|cfg1]
+                    [--config cfg3|cfg4|cfg5|cfg2|cfg1|tiny]
 
-`--impl reference` times the reference algorithm's CPU implementation (the
-float64 numpy port in oracle/, the reference itself is Python and cannot
-travel to the GPU box) on a bounded token sample of the same layer.
+--gpus N > 1 without torchrun's environment relaunches itself under torch.distributed.run with N
+ranks.  `--impl reference` times the reference algorithm's CPU implementation (the float64 numpy
+port in oracle/, pinned to the reference's own outputs; the reference is Python and cannot travel
+to the GPU box) on the same config: every distinct projection shape of the workload is timed on
+bounded token samples at two sizes, and the full-config step time is extrapolated from the fitted
+per-call and per-token costs (attention, norms and the LM head excluded; the reference has no
+transformer).
 """
 
 from __future__ import annotations
@@ -25,25 +30,36 @@ import gc
 import json
 import os
 import statistics
-import subprocess
 import sys
-import threading
 import time
+
+
+def _cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# The CPU legs are float64 numpy over OpenBLAS: its thread count is fixed to the cores this
+# process may use before anything imports numpy.
+os.environ.setdefault("OPENBLAS_NUM_THREADS", str(_cores()))
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fine-tune tokens/s (fwd+bwd) at 1/2/4/8 B200 vs roofline; peak HBM GB"
 CONFIGS = {
-    # name: (R, C, L, r, pattern, dtype)
     "cfg2": dict(R=11008, C=4096, L=8192, r=64, pattern="two_four", dtype="bf16",
-                 desc="LoRS MLP projection 11008x4096, 2:4, r=64, 8192 tokens/GPU (BASELINE configs[1])"),
+                 desc="cfg2: LoRS MLP projection 11008x4096, 2:4, r=64, 8192 tokens/GPU (BASELINE configs[1])"),
     "cfg1": dict(R=4096, C=4096, L=2048, r=16, pattern="rowwise", dtype="f32",
-                 desc="LoRS linear 4096x4096, 50% per-row, r=16, 2048 tokens (BASELINE configs[0], fp32 parity mode)"),
+                 desc="cfg1: LoRS linear 4096x4096, 50% per-row, r=16, 2048 tokens (BASELINE configs[0], fp32 parity "
+                      "mode)"),
 }
 # Model-level workloads (BASELINE configs 3-5): a fine-tuning step of the LLaMA-shaped
 # decoder whose 7 projections per layer are LoRS linears (decoder.py / trainer.py).
 DECODER_CONFIGS = {"cfg3": "llama2-7b", "cfg4": "llama3-8b", "cfg5": "llama2-13b", "tiny": "tiny"}
+DEFAULT_CONFIG = "cfg3"
 FALLBACK_PEAKS = dict(bf16_tflops=1590.0, hbm_gbs=6650.0)
 SPEC_PEAKS = dict(dense_tflops=2250.0, sparse_tflops=4500.0, hbm_gbs=8000.0)  # north_star's roofline
 
@@ -58,7 +74,7 @@ def peaks():
 
 
 # ---------------------------------------------------------------------------
-# clocks sampler (nvidia-smi during the timed region)
+# clocks sampler (NVML during the timed region)
 # ---------------------------------------------------------------------------
 class ClockSampler:
     """Samples NVML (SM clock + clock-event reasons) from the main thread while
@@ -77,7 +93,6 @@ class ClockSampler:
         self.nvml = None
         try:
             import pynvml as nv
-            import torch
             nv.nvmlInit()
             idx = torch_device.index or 0
             vis = os.environ.get("CUDA_VISIBLE_DEVICES")
@@ -104,8 +119,6 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:  # noqa: BLE001
                 pass
-            if done and len(self.samples) >= min_samples:
-                return
             if done:
                 return
             time.sleep(0.002)
@@ -143,113 +156,168 @@ def gpu_local_affinity(torch_device):
 
 
 # ---------------------------------------------------------------------------
-# reference arm / CPU baseline: the oracle port (float64 numpy)
+# workload descriptions (the SAME dict on both arms, so the driver can compare them)
 # ---------------------------------------------------------------------------
-def cpu_inputs(cfg, L_sample, seed=0):
+def layer_config(cfg, world):
+    return {"workload": cfg["desc"], "tokens_per_gpu": cfg["L"], "global_tokens": cfg["L"] * world, "R": cfg["R"],
+            "C": cfg["C"], "rank": cfg["r"], "alpha": 2.0, "sparsity": cfg["pattern"], "parallelism": f"dp{world}",
+            "l2": "inputs larger than L2 (W, X, dY each step)"}
+
+
+def decoder_config(name, dcfg, world):
+    return {"workload": f"{name}: {DECODER_CONFIGS[name]}-shaped decoder fine-tuning step (random init, uniform "
+                        "token ids)", "layers": dcfg.n_layers, "dim": dcfg.dim, "ffn": dcfg.ffn,
+            "heads": dcfg.n_heads, "kv_heads": dcfg.n_kv_heads, "vocab": dcfg.vocab, "rank": dcfg.rank,
+            "sparsity": dcfg.sparsity if dcfg.sparsity == "two_four" else f"{dcfg.ratio:.0%} per-row magnitude",
+            "seq": dcfg.seq, "batch_per_gpu": dcfg.batch, "global_batch": dcfg.batch * world,
+            "parallelism": f"dp{world}", "l2": "weights and activations far larger than L2"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle port (float64 numpy), extrapolated to the full config
+# ---------------------------------------------------------------------------
+def cpu_env():
+    """CPU model, cores used, numpy and BLAS versions."""
+    import numpy as np
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        for d in threadpool_info():
+            if d.get("user_api") == "blas":
+                blas = {"api": d.get("internal_api"), "version": d.get("version"),
+                        "num_threads": d.get("num_threads")}
+                break
+    except Exception:  # noqa: BLE001
+        pass
+    return {"cpu_model": model, "cores": _cores(), "numpy": np.__version__, "blas": blas,
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS")}
+
+
+def cpu_inputs(R, C, r, pattern, L, seed=0, ratio=0.5):
     import numpy as np
     from oracle import lors_oracle as orc
     rng = np.random.default_rng(seed)
-    R, C, r = cfg["R"], cfg["C"], cfg["r"]
     w = rng.normal(0, 0.02, size=(R, C))
-    w = orc.prune_two_four(w) if cfg["pattern"] == "two_four" else orc.prune_rowwise(w, 0.5)
+    w = orc.prune_two_four(w) if pattern == "two_four" else orc.prune_rowwise(w, ratio)
     a = rng.normal(0, 1e-3, size=(R, r))
     b = rng.normal(0, 1 / np.sqrt(r), size=(r, C))
-    x = rng.normal(size=(C, L_sample))
-    dy = rng.normal(size=(R, L_sample))
+    x = rng.normal(size=(C, L))
+    dy = rng.normal(size=(R, L))
     return w, a, b, x, dy
 
 
 def cpu_step(w, a, b, x, dy):
+    """lors_forward + lors_backward of the reference algorithm (adapters.py:359-406), float64."""
     from oracle import lors_oracle as orc
     orc.lors_forward(w, a, b, x, 2.0)
     orc.lors_backward(w, a, b, x, dy, 2.0)
 
 
-def cpu_cores():
-    try:
-        return len(os.sched_getaffinity(0))
-    except AttributeError:
-        return os.cpu_count() or 1
+class ShapeTimer:
+    """Times the reference step of one projection shape at two token counts L1 < L2 and fits
+    t(L) = fixed + per_token * L (fixed: the per-call merged-weight / mask passes, adapters.py:
+    214-224, 393-394; per_token: the RCL / rRL / rCL products), so a full-config step can be
+    extrapolated from bounded samples."""
 
+    def __init__(self, R, C, r, pattern, L1, L2, ratio=0.5):
+        import numpy as np
+        self.shape = (R, C)
+        self.L1, self.L2 = L1, L2
+        self.w, self.a, self.b, x, dy = cpu_inputs(R, C, r, pattern, L2, ratio=ratio)
+        self.x2, self.dy2 = x, dy
+        self.x1, self.dy1 = np.ascontiguousarray(x[:, :L1]), np.ascontiguousarray(dy[:, :L1])
+        self.fits = []
 
-def cpu_baseline(cfg, L_sample=1024, reps=3):
-    """Time the float64 port of lors_forward+lors_backward on a token sample."""
-    w, a, b, x, dy = cpu_inputs(cfg, L_sample)
-    cpu_step(w, a, b, x, dy)  # warm
-    ts = []
-    for _ in range(reps):
+    def sample(self):
         t0 = time.perf_counter()
-        cpu_step(w, a, b, x, dy)
-        ts.append(time.perf_counter() - t0)
-    med = statistics.median(ts)
-    return {"value": L_sample / med, "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
-            "sample": f"{L_sample} tokens of the {cfg['R']}x{cfg['C']} r={cfg['r']} layer, float64 numpy "
-                      f"(OpenBLAS threads = {cpu_cores()}), median of {reps} fwd+bwd; full step holds "
-                      f"{cfg['L']} tokens",
-            "s_per_sample_step": med}
+        cpu_step(self.w, self.a, self.b, self.x1, self.dy1)
+        t1 = time.perf_counter()
+        cpu_step(self.w, self.a, self.b, self.x2, self.dy2)
+        t2 = time.perf_counter()
+        per_tok = max((t2 - t1) - (t1 - t0), 0.0) / (self.L2 - self.L1)
+        fixed = max((t1 - t0) - per_tok * self.L1, 0.0)
+        self.fits.append((fixed, per_tok))
+        return t2 - t0
+
+    def step_seconds(self, L):
+        fixed = statistics.median(f for f, _ in self.fits)
+        per_tok = statistics.median(p for _, p in self.fits)
+        return fixed + per_tok * L
 
 
-def decoder_cpu_baseline(dcfg, L_sample=256):
-    """Reference CPU LoRS-linear time for one decoder token, extrapolated: each
-    distinct projection shape timed once with the float64 port on an L_sample-token sample,
-    summed over the 7 projections x layers; attention, norms and the LM head excluded."""
-    import collections
-    shapes = collections.Counter(dcfg.shapes().values())
-    per_token_s = 0.0
-    detail = {}
-    for (R, C), count in shapes.items():
-        cfg = dict(R=R, C=C, r=dcfg.rank, pattern=dcfg.sparsity)
-        w, a, b, x, dy = cpu_inputs(cfg, L_sample)
-        cpu_step(w, a, b, x, dy)
-        t0 = time.perf_counter()
-        cpu_step(w, a, b, x, dy)
-        dt = time.perf_counter() - t0
-        per_token_s += count * dcfg.n_layers * dt / L_sample
-        detail[f"{R}x{C}"] = dt
-    return {"value": 1.0 / per_token_s, "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
-            "sample": f"each distinct projection shape once on {L_sample} tokens (float64 numpy port, OpenBLAS "
-                      f"threads = {cpu_cores()}), summed x 7 projections x {dcfg.n_layers} layers; reference CPU "
-                      "LoRS-linear time, extrapolated, attention / norms / LM head excluded",
-            "s_per_shape_sample": detail}
-
-
-def run_reference(args, cfg):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return 0
+def reference_model(args, world):
+    """(config dict, [(ShapeTimer, calls per step)], tokens per step) of the workload."""
     if args.config in DECODER_CONFIGS:
+        import collections
         from paper_2501_08582_b200 import decoder as D
         dcfg = D.preset(DECODER_CONFIGS[args.config])
-        cb = decoder_cpu_baseline(dcfg)
-        line = {
-            "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": 1, "warmup": 1, "ms_per_step": 1e3 * dcfg.tokens_per_step() / cb["value"],
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {DECODER_CONFIGS[args.config]} decoder, LoRS linears only"},
-            "cpu_baseline": cb,
-            "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        }
-        print(json.dumps(line), flush=True)
+        counts = collections.Counter(dcfg.shapes().values())
+        L1, L2 = (64, 192) if args.config == "tiny" else (128, 384)
+        timers = [(ShapeTimer(R, C, dcfg.rank, dcfg.sparsity, L1, L2, ratio=dcfg.ratio), n * dcfg.n_layers)
+                  for (R, C), n in sorted(counts.items())]
+        return decoder_config(args.config, dcfg, world), timers, dcfg.tokens_per_step()
+    cfg = CONFIGS[args.config]
+    L1, L2 = (256, 768) if cfg["L"] <= 2048 else (512, 1024)
+    return layer_config(cfg, world), [(ShapeTimer(cfg["R"], cfg["C"], cfg["r"], cfg["pattern"], L1, L2), 1)], cfg["L"]
+
+
+def extrapolated(timers, T):
+    t = sum(n * tm.step_seconds(T) for tm, n in timers)
+    return T / t, t
+
+
+def sample_text(timers, T):
+    shapes = ", ".join(f"{tm.shape[0]}x{tm.shape[1]} x{n}" for tm, n in timers)
+    L1, L2 = timers[0][0].L1, timers[0][0].L2
+    return (f"oracle/lors_oracle.py float64 lors_forward + lors_backward (adapters.py:359-406) of every distinct "
+            f"projection shape ({shapes} calls per step) on {L1}- and {L2}-token samples; per-call and per-token "
+            f"costs fitted (median over samples) and extrapolated to the full {T}-token step"
+            + ("; LoRS linears only: attention, norms and LM head excluded (the reference has no transformer)"
+               if len(timers) > 1 or timers[0][1] > 1 else ""))
+
+
+def cpu_baseline(args, world=1):
+    """The reported CPU baseline of the native line: one sample per distinct shape (~10-30 s)."""
+    _, timers, T = reference_model(args, world)
+    for tm, _ in timers:
+        tm.sample()
+    value, t = extrapolated(timers, T)
+    return {"value": value, "unit": "tokens/s", "cores": _cores(), "kind": "port", "sample": sample_text(timers, T),
+            "s_per_step_extrapolated": t, "env": cpu_env()}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
         return 0
-    L_sample = 1024
-    w, a, b, x, dy = cpu_inputs(cfg, L_sample)
-    for _ in range(max(args.warmup, 1)):
-        cpu_step(w, a, b, x, dy)
-    ts = []
+    config, timers, T = reference_model(args, world)
+    # each step samples one distinct shape (round robin), so a step stays bounded (~1-3 s)
+    k = 0
+    for _ in range(max(args.warmup, len(timers))):
+        timers[k % len(timers)][0].sample()
+        k += 1
+    sampled = 0.0
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        cpu_step(w, a, b, x, dy)
-        ts.append(time.perf_counter() - t0)
-    tot = sum(ts)
-    value = L_sample * args.steps / tot
+        sampled += timers[k % len(timers)][0].sample()
+        k += 1
+    value, t = extrapolated(timers, T)
+    # the host's cores run the whole job: N ranks' steps take N times one step's time
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "sample_tokens_per_step": L_sample},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
-                         "sample": f"{L_sample} tokens per step of the {cfg['R']}x{cfg['C']} r={cfg['r']} layer, "
-                                   "oracle/lors_oracle.py float64 numpy (reference algorithm, adapters.py:359-406)"},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": world * t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": _cores(), "kind": "port",
+                         "sample": sample_text(timers, T), "sampled_seconds": sampled, "env": cpu_env()},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -257,23 +325,17 @@ def run_reference(args, cfg):
 
 
 # ---------------------------------------------------------------------------
-# native arm
+# native arm, single projection (cfg2 / cfg1)
 # ---------------------------------------------------------------------------
-def run_native(args, cfg):
+def measure_layer(cfg, steps, warmup, world, rank, dev, full=True):
+    """fwd + bwd of one LoRS projection with inputs resident in HBM.  Returns a dict of the
+    line's fields; full=False (the extra cfg2 block of the decoder line) skips e2e and the
+    comparators."""
     import torch
     import torch.distributed as dist
 
     from paper_2501_08582_b200 import _native, adapters, ops, prune
     from paper_2501_08582_b200.module import LoRSLinear
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    _native.check(_native.load().lors_device_check())
 
     R, C, L, r = cfg["R"], cfg["C"], cfg["L"], cfg["r"]
     dt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
@@ -287,7 +349,6 @@ def run_native(args, cfg):
     dy = torch.randn(L, R, device=dev, generator=gx).to(dt)
     a, b = a32.to(dt), b32.to(dt)
     grad_bucket = torch.empty(R * r + r * C, device=dev, dtype=torch.float32)
-
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
@@ -305,8 +366,7 @@ def run_native(args, cfg):
         if times is not None:
             times.append((e0, e1, e2))
 
-    print('[bench] warmup', file=sys.stderr, flush=True)
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
@@ -317,7 +377,7 @@ def run_native(args, cfg):
     t_start, t_end = ev(), ev()
     times = []
     t_start.record(stream)
-    for _ in range(args.steps):
+    for _ in range(steps):
         step(times)
     t_end.record(stream)
     clocks.sample_until(t_end)
@@ -326,8 +386,7 @@ def run_native(args, cfg):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clk = clocks.result()
-    ms = t_start.elapsed_time(t_end) / args.steps
+    ms = t_start.elapsed_time(t_end) / steps
     fwd_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1, _ in times)
     bwd_ms = statistics.mean(e1.elapsed_time(e2) for _, e1, e2 in times)
     if world > 1:
@@ -335,8 +394,6 @@ def run_native(args, cfg):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
 
-    # per-kernel split inside the backward, timed live: the dX GEMM alone and the
-    # rank-r products alone (in the step they overlap on two streams)
     def timed(fn, n=5):
         fn()
         t0_, t1_ = ev(), ev()
@@ -347,6 +404,7 @@ def run_native(args, cfg):
         torch.cuda.synchronize()
         return t0_.elapsed_time(t1_) / n
 
+    # the backward's parts alone (in the step they overlap on two streams)
     dx_ms = timed(lambda: ops._lors_bwd_call(x, w, a, b, dy, 2.0, None, None, "ste", True, False, False,
                                              dx_only=True))
     rank_r_ms = timed(lambda: ops.lors_bwd(x, w, a, b, dy, 2.0, need_dx=False))
@@ -354,22 +412,43 @@ def run_native(args, cfg):
     if cfg["pattern"] == "two_four" and dt == torch.bfloat16:
         # the 2:4 sparse-tensor-core forward (north_star 4), timed beside the dense-masked one
         meta24 = ops.compress_24(w)[1]   # kept-position metadata, built once per frozen weight
-        for _ in range(2):
-            ops.lors_fwd(x, w, a, b, 2.0, sparse24=True, meta24=meta24)
-        es0, es1 = ev(), ev()
-        es0.record(stream)
-        for _ in range(5):
-            ops.lors_fwd(x, w, a, b, 2.0, sparse24=True, meta24=meta24)
-        es1.record(stream)
-        torch.cuda.synchronize()
-        sp_ms = es0.elapsed_time(es1) / 5
+        sp_ms = timed(lambda: ops.lors_fwd(x, w, a, b, 2.0, sparse24=True, meta24=meta24))
+    cost = adapters.predict_cost("lors", R, C, L, r)
+    step_flops = cost.flops
+    fwd_flops = 2 * cost.macs_forward                       # one K1 launch (RCL + rRC + RC)
+    dx_flops = 2 * (R * C * L + r * R * C + R * C)          # one K3 launch (dX GEMM + its recompute)
+    out = {
+        "ms": ms, "tokens_per_s_per_gpu": L / (ms * 1e-3), "launches": launches, "clocks": clocks.result(),
+        "step_breakdown_ms": {"fwd": fwd_ms, "bwd": bwd_ms, "bwd_dx_gemm_alone": dx_ms, "bwd_rank_r_alone": rank_r_ms,
+                              "bwd_overlap": "dX and the rank-r products on two streams",
+                              "fwd_sparse24_tc": sp_ms},
+        "algorithmic_tflops": step_flops / (ms * 1e-3) / 1e12,
+        "fwd_flops": fwd_flops, "dx_flops": dx_flops, "step_flops": step_flops, "dt": dt,
+    }
+    if dt == torch.bfloat16:
+        # north_star's roofline: FLOPs at 2.25 PF dense (or 4.5 PF for the forward's main product on
+        # the 2:4 sparse tensor cores) vs bytes at 8 TB/s (676 us / 512 us at cfg2)
+        byt = 2 * (2 * R * C + 2 * L * C + 2 * L * R + L * C) + 4 * 2 * r * (R + C)
+        t_dense = max(step_flops / (SPEC_PEAKS["dense_tflops"] * 1e12), byt / (SPEC_PEAKS["hbm_gbs"] * 1e9))
+        fwd_main = 2 * R * C * L
+        t_sparse = max((step_flops - fwd_main) / (SPEC_PEAKS["dense_tflops"] * 1e12)
+                       + fwd_main / (SPEC_PEAKS["sparse_tflops"] * 1e12), byt / (SPEC_PEAKS["hbm_gbs"] * 1e9))
+        out["spec_roofline"] = {
+            "dense_masked_us": t_dense * 1e6, "sparse_tc_forward_us": t_sparse * 1e6,
+            "frac_of_dense_spec": t_dense / (ms * 1e-3),
+            "frac_of_sparse_spec": t_sparse / (ms * 1e-3) if cfg["pattern"] == "two_four" else None,
+            "fwd_frac_of_dense_spec": fwd_flops / (fwd_ms * 1e-3) / (SPEC_PEAKS["dense_tflops"] * 1e12),
+            "sparse24_fwd_frac_of_sparse_spec": (
+                (fwd_flops - fwd_main) / (SPEC_PEAKS["dense_tflops"] * 1e12)
+                + fwd_main / (SPEC_PEAKS["sparse_tflops"] * 1e12)) / (sp_ms * 1e-3) if sp_ms else None,
+            "bytes_per_step": byt}
+    if not full:
+        return out
 
     print('[bench] e2e', file=sys.stderr, flush=True)
     # ---------------- end-to-end through the public module API (host buffers)
     layer = LoRSLinear(w, a=a32, b=b32, alpha=2.0).to(dev)
-    # host buffers on the GPU's NUMA node (as a data loader bound to the GPU's
-    # CPUs would place them): bind to the GPU-local CPUs while allocating and
-    # first-touching the pinned batches, so H2D runs at the local PCIe rate
+    # host buffers on the GPU's NUMA node (as a data loader bound to the GPU's CPUs would place them)
     prev_aff = gpu_local_affinity(dev)
     hx = torch.empty(x.shape, dtype=x.dtype).pin_memory()
     hdy = torch.empty(dy.shape, dtype=dy.dtype).pin_memory()
@@ -377,7 +456,6 @@ def run_native(args, cfg):
     hdy.copy_(dy.cpu())
     hda = torch.empty(R, r, dtype=torch.float32).pin_memory()
     hdb = torch.empty(r, C, dtype=torch.float32).pin_memory()
-
     copy_stream = torch.cuda.Stream(device=dev)
     # two preallocated device batches: step k computes on slot k % 2 while the
     # copy stream fills slot (k + 1) % 2 (a training loop's data prefetch)
@@ -401,9 +479,7 @@ def run_native(args, cfg):
     def e2e_step():
         k = state["k"]
         state["k"] = k + 1
-        # bounded run-ahead, as a training loop reading its results has: the host waits
-        # for step k - 2's copy-out before enqueuing step k (the GPU stays a step ahead)
-        if k >= 2:
+        if k >= 2:   # bounded run-ahead, as a training loop reading its results has
             done[k % 2].synchronize()
         xs, dys = slots[k % 2]
         stream.wait_event(filled[k % 2])
@@ -423,32 +499,23 @@ def run_native(args, cfg):
         done[k % 2].record(stream)
 
     prefetch(0)
-    for _ in range(5):   # warm the copy path (PCIe link out of its idle state) before timing
+    for _ in range(5):   # warm the copy path before timing
         e2e_step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.reset_peak_memory_stats(dev)
     e0, e1 = ev(), ev()
-    e2e_steps = max(5, min(args.steps, 10))
-    marks = [ev() for _ in range(e2e_steps + 1)]
+    e2e_steps = max(5, min(steps, 10))
     gc.collect()
-    gc.disable()   # no interpreter GC pause inside the timed loop (training loops collect between steps)
+    gc.disable()
     e0.record(stream)
-    marks[0].record(stream)
-    host_ms = []
-    for i_ in range(e2e_steps):
-        th = time.perf_counter()
+    for _ in range(e2e_steps):
         e2e_step()
-        host_ms.append(1e3 * (time.perf_counter() - th))
-        marks[i_ + 1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
     gc.enable()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    if os.environ.get("LORS_BENCH_VERBOSE"):
-        print("[bench] e2e per-step ms", [round(marks[i].elapsed_time(marks[i + 1]), 2) for i in range(e2e_steps)],
-              "host ms", [round(v, 2) for v in host_ms], file=sys.stderr)
     if prev_aff is not None:
         os.sched_setaffinity(0, prev_aff)
     peak_gb = torch.cuda.max_memory_allocated(dev) / 1e9
@@ -456,26 +523,22 @@ def run_native(args, cfg):
         tt = torch.tensor([e2e_ms, peak_gb], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms, peak_gb = float(tt[0]), float(tt[1])
+    out.update(e2e_ms=e2e_ms, peak_gb=peak_gb, h2d=x.numel() * x.element_size() + dy.numel() * dy.element_size(),
+               d2h=(R * r + r * C) * 4)
 
-    # ---------------- memory / speed comparators (north_star: peak memory <= plain
-    # dense LoRA; bytes not allocated relative to an SQFT-style path that
-    # materialises W_eff), same layer and inputs, one fwd+bwd each
+    # ---------------- memory / speed comparators (north_star: peak memory <= plain dense
+    # LoRA; bytes not allocated relative to an SQFT-style path that materialises W_eff)
     from paper_2501_08582_b200.comparators import DenseLoRAFunction, SQFTFunction, peak_bytes_of_step
     xg = x.detach().clone().requires_grad_(True)
-    a_p = layer.a
-    b_p = layer.b
 
     def run_lors():
-        y = layer(xg)
-        y.backward(dy)
+        layer(xg).backward(dy)
 
     def run_lora():
-        y = DenseLoRAFunction.apply(xg, w, a_p, b_p, 2.0)
-        y.backward(dy)
+        DenseLoRAFunction.apply(xg, w, layer.a, layer.b, 2.0).backward(dy)
 
     def run_sqft():
-        y = SQFTFunction.apply(xg, w, a_p, b_p, 2.0)
-        y.backward(dy)
+        SQFTFunction.apply(xg, w, layer.a, layer.b, 2.0).backward(dy)
 
     memory, comp_speed = {}, {}
     for name, fn in (("lors", run_lors), ("dense_lora", run_lora), ("sqft_materialised", run_sqft)):
@@ -484,98 +547,114 @@ def run_native(args, cfg):
         layer.b.grad = None
         fn()
         memory[name + "_step_peak_gb"] = peak_bytes_of_step(fn) / 1e9
-        c0_, c1_ = ev(), ev()
-        c0_.record(stream)
-        for _ in range(3):
-            fn()
-        c1_.record(stream)
-        torch.cuda.synchronize()
-        comp_speed[name + "_tokens_per_s"] = L / (c0_.elapsed_time(c1_) / 3 * 1e-3)
+        comp_speed[name + "_tokens_per_s"] = L / (timed(fn, 3) * 1e-3)
     memory["bytes_not_allocated_vs_sqft_gb"] = memory["sqft_materialised_step_peak_gb"] - memory["lors_step_peak_gb"]
     memory["lors_le_dense_lora"] = memory["lors_step_peak_gb"] <= memory["dense_lora_step_peak_gb"]
     memory["note"] = ("extra device bytes allocated during one fwd+bwd above the resident inputs "
                       "(W, a, b, X, dY); comparators are plain torch/cuBLAS (adapters.py:245-312 semantics)")
-    del xg
+    out.update(memory=memory, comparators_tokens_per_s=comp_speed)
+    return out
 
+
+def dominant_roofline(label, flops, ms, traffic_key, peak_tf, pk_kind):
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic_latest.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tr = json.load(f)
+        traffic = tr.get(traffic_key, {}).get("dram_bytes_per_launch")
+    achieved = flops / (ms * 1e-3) / 1e12
+    return {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved / peak_tf,
+            "traffic": traffic, "kernel": label, "peak_kind": pk_kind, "algorithmic_flops_per_launch": flops,
+            "ms_per_launch": ms, "frac_of_spec_2250": achieved / SPEC_PEAKS["dense_tflops"]}
+
+
+def run_native(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_08582_b200 import _native
+
+    world, rank, dev = init_dist(args)
+    _native.check(_native.load().lors_device_check())
+    print('[bench] warmup', file=sys.stderr, flush=True)
+    m = measure_layer(cfg, args.steps, args.warmup, world, rank, dev, full=True)
     if rank == 0:
         pk, pk_kind = peaks()
-        cost = adapters.predict_cost("lors", R, C, L, r)
-        fwd_flops = 2 * cost.macs_forward                       # one K1 launch (RCL + rRC + RC)
-        dx_flops = 2 * (R * C * L + r * R * C + R * C)          # one K3 launch (dX GEMM + its recompute)
-        # dominant kernel = the larger of K1 (fwd) and K3 (dX)
-        if dx_ms >= fwd_ms:
-            dom, dom_ms, dom_flops = "tc_lors_gemm<dx> (K3, dX = dY W_eff)", dx_ms, dx_flops
-        else:
-            dom, dom_ms, dom_flops = "tc_lors_gemm<fwd> (K1, Y = X W_eff^T)", fwd_ms, fwd_flops
-        if dt == torch.bfloat16:
+        R, C, L = cfg["R"], cfg["C"], cfg["L"]
+        if m["dt"] == torch.bfloat16:
             peak_tf = float(pk.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
+            pk_kind = f"{pk_kind} bf16 burst (kernel timed alone)"
+            dx_label, fwd_label = "tc_lors_gemm<dx> (K3, dX = dY W_eff)", "tc_lors_gemm<fwd> (K1, Y = X W_eff^T)"
         else:
-            # fp32 parity mode: against the FP32 SIMT ceiling measured here, cuBLAS
-            # SGEMM with TF32 off (the FFMA rate), not the bf16 tensor peak; not graded at 60%
+            # fp32 parity mode: against the FP32 SIMT ceiling measured here (cuBLAS SGEMM
+            # with TF32 off), not the bf16 tensor peak; not graded at 60%
             prev = torch.backends.cuda.matmul.allow_tf32
             torch.backends.cuda.matmul.allow_tf32 = False
             m_ = torch.randn(4096, 4096, device=dev)
             for _ in range(2):
                 m_ @ m_
-            s0_, s1_ = ev(), ev()
-            s0_.record(stream)
+            s0_, s1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0_.record()
             for _ in range(5):
                 m_ @ m_
-            s1_.record(stream)
+            s1_.record()
             torch.cuda.synchronize()
             torch.backends.cuda.matmul.allow_tf32 = prev
             peak_tf = 5 * 2 * 4096 ** 3 / (s0_.elapsed_time(s1_) * 1e-3) / 1e12
             pk_kind = "measured fp32 SGEMM (TF32 off) on this box"
-            del m_
-        achieved = dom_flops / (dom_ms * 1e-3) / 1e12
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "traffic_latest.json")
-        if os.path.exists(tp) and dt == torch.bfloat16:   # the ncu capture is of the bf16 tensor-core kernels
-            with open(tp) as f:
-                tr = json.load(f)
-            key = "dx" if "dx" in dom else "fwd"
-            traffic = tr.get(key, {}).get("dram_bytes_per_launch")
-        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                    "frac": (achieved / peak_tf) if peak_tf else None, "traffic": traffic,
-                    "kernel": dom, "peak_kind": pk_kind + (" bf16 burst" if dt == torch.bfloat16 else ""),
-                    "algorithmic_flops_per_launch": dom_flops, "ms_per_launch": dom_ms}
-        step_flops = cost.flops
-        tokens = L * world
+            dx_label, fwd_label = "simt_lors_gemm<dx> (S1, dX = dY W_eff, FFMA)", "simt_lors_gemm<fwd> (S1, FFMA)"
+        sb = m["step_breakdown_ms"]
+        if sb["bwd_dx_gemm_alone"] >= sb["fwd"]:
+            roof = dominant_roofline(dx_label, m["dx_flops"], sb["bwd_dx_gemm_alone"], "dx", peak_tf, pk_kind)
+        else:
+            roof = dominant_roofline(fwd_label, m["fwd_flops"], sb["fwd"], "fwd", peak_tf, pk_kind)
+        if m["dt"] != torch.bfloat16:
+            roof["traffic"] = None       # the ncu capture is of the bf16 tensor-core kernels
         line = {
-            "metric": METRIC, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "metric": METRIC, "value": world * L / (m["ms"] * 1e-3), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": m["ms"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
-            "config": {"workload": cfg["desc"], "tokens_per_gpu": L, "R": R, "C": C, "rank": r, "alpha": 2.0,
-                       "sparsity": cfg["pattern"],
-                       "forward": ("dense-masked tcgen05 (W_eff rebuilt on chip)" if dt == torch.bfloat16
-                                   else "fp32 parity mode: FFMA kernels (W_eff rebuilt in shared memory)"),
-                       "adapter_grads": "ste (lors)", "parallelism": f"dp{world}",
-                       "l2": "inputs larger than L2 (W 90 MB + X 64 MB + dY 180 MB per step, 126 MB L2)"},
-            "peak_hbm_gb": peak_gb,
-            "memory": memory,
-            "comparators_tokens_per_s": comp_speed,
-            "step_breakdown_ms": {"fwd": fwd_ms, "bwd": bwd_ms, "bwd_dx_gemm_alone": dx_ms,
-                                  "bwd_rank_r_alone": rank_r_ms, "bwd_overlap": "dX and the rank-r products on two streams",
-                                  "fwd_sparse24_tc": sp_ms},
-            "algorithmic_tflops": step_flops / (ms * 1e-3) / 1e12,
-            "roofline": roofline,
-            "gpu_launches": launches,
-            "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s",
-                    "h2d_bytes_per_step": x.numel() * x.element_size() + dy.numel() * dy.element_size(),
-                    "d2h_bytes_per_step": (R * r + r * C) * 4,
-                    "ms_per_step": e2e_ms, "api": "LoRSLinear.forward + backward (autograd); pinned host X/dY "
-                                                  "copied in every step (next batch prefetched on a copy stream), "
-                                                  "dA/dB copied out every step"},
-            "clocks": clk,
+            "config": layer_config(cfg, world),
+            "path": {"forward": "dense-masked tcgen05 (W_eff rebuilt on chip)" if m["dt"] == torch.bfloat16
+                     else "fp32 parity mode: FFMA kernels (W_eff rebuilt in shared memory)",
+                     "adapter_grads": "ste (lors)"},
+            "peak_hbm_gb": m["peak_gb"], "memory": m["memory"],
+            "comparators_tokens_per_s": m["comparators_tokens_per_s"],
+            "step_breakdown_ms": sb, "algorithmic_tflops": m["algorithmic_tflops"],
+            "spec_roofline": m.get("spec_roofline"), "roofline": roof, "gpu_launches": m["launches"],
+            "e2e": {"value": world * L / (m["e2e_ms"] * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": m["h2d"],
+                    "d2h_bytes_per_step": m["d2h"], "ms_per_step": m["e2e_ms"],
+                    "api": "LoRSLinear.forward + backward (autograd); pinned host X/dY copied in every step (next "
+                           "batch prefetched on a copy stream), dA/dB copied out every step"},
+            "clocks": m["clocks"],
         }
         if world == 1 and not args.no_cpu:
-            line["cpu_baseline"] = cpu_baseline(cfg)
+            line["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
+def init_dist(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    return world, rank, dev
+
+
+# ---------------------------------------------------------------------------
+# native arm, decoder fine-tuning step (cfg3 default, cfg4, cfg5)
+# ---------------------------------------------------------------------------
 def run_decoder(args):
     """Fine-tuning step of a LLaMA-shaped LoRS decoder (BASELINE configs 3-5): forward, next-token
     CE, backward through the LoRS kernels, NCCL all-reduce of the adapter gradients (N > 1),
@@ -583,16 +662,10 @@ def run_decoder(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2501_08582_b200 import _native, decoder as D
+    from paper_2501_08582_b200 import _native, decoder as D, ops
     from paper_2501_08582_b200.trainer import Trainer, synthetic_tokens
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    world, rank, dev = init_dist(args)
     _native.check(_native.load().lors_device_check())
     name = DECODER_CONFIGS[args.config]
     dcfg = D.preset(name)
@@ -609,7 +682,7 @@ def run_decoder(args):
         model = D.LoRSDecoder(dcfg, device=dev, seed=0, linear_factory=fac)
         return model, Trainer(model, lr=2e-5, optimizer=args.optimizer if kind == "lors" else "auto")
 
-    def measure(kind, steps, warmup, sample_clocks=False):
+    def measure(kind, steps, warmup, sample_clocks=False, dominant=False):
         model, trainer = build(kind)
         toks = [synthetic_tokens(dcfg.vocab, dcfg.batch, dcfg.seq, s, rank=rank, device=dev)
                 for s in range(steps + warmup)]
@@ -649,18 +722,38 @@ def run_decoder(args):
         f0, f1 = ev(), ev()
         f0.record(stream)
         for s in range(len(hbuf)):
-            l = trainer.step(hbuf[s].to(dev, non_blocking=True))
-            hloss.copy_(l, non_blocking=True)
+            lo = trainer.step(hbuf[s].to(dev, non_blocking=True))
+            hloss.copy_(lo, non_blocking=True)
         f1.record(stream)
         torch.cuda.synchronize()
         out["e2e_ms"] = f0.elapsed_time(f1) / len(hbuf)
         out["h2d"] = hbuf[0].numel() * hbuf[0].element_size()
+        if dominant:
+            # the dominant kernel, timed live on its launching stream: the LoRS forward GEMM (K1) of the
+            # largest projection (gate) at this step's token count, on the model's own weights
+            proj = model.layers[0].proj["gate"]
+            w = proj.weight
+            a, b = proj.a.detach().to(w.dtype).contiguous(), proj.b.detach().to(w.dtype).contiguous()
+            x = torch.randn(T, w.shape[1], device=dev, dtype=w.dtype)
+            for _ in range(3):
+                ops.lors_fwd(x, w, a, b, dcfg.alpha)
+            k0, k1 = ev(), ev()
+            k0.record(stream)
+            for _ in range(10):
+                ops.lors_fwd(x, w, a, b, dcfg.alpha)
+            k1.record(stream)
+            torch.cuda.synchronize()
+            R_, C_ = w.shape
+            out["dominant"] = {"ms": k0.elapsed_time(k1) / 10, "R": R_, "C": C_,
+                               "flops": 2 * (R_ * C_ * T + dcfg.rank * R_ * C_ + R_ * C_)}
+            del x
         del trainer, model, toks
+        gc.collect()
         torch.cuda.empty_cache()
         return out
 
     print(f"[bench] {name}: building + warmup", file=sys.stderr, flush=True)
-    r = measure("lors", args.steps, args.warmup, sample_clocks=True)
+    r = measure("lors", args.steps, args.warmup, sample_clocks=True, dominant=rank == 0)
     vals = torch.tensor([r["ms"], r["e2e_ms"], r["peak_gb"]], device=dev)
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
@@ -681,35 +774,47 @@ def run_decoder(args):
             memory["bytes_not_allocated_vs_sqft_gb"] = memory["sqft_peak_gb"] - peak_gb
         if isinstance(memory.get("dense_lora_peak_gb"), float):
             memory["lors_le_dense_lora"] = peak_gb <= memory["dense_lora_peak_gb"]
+    layer_block = None
+    if world == 1 and not args.no_layer:
+        # BASELINE configs[1] (one 11008 x 4096 2:4 projection, 8192 tokens) beside the model step
+        print("[bench] cfg2 layer", file=sys.stderr, flush=True)
+        lm = measure_layer(CONFIGS["cfg2"], 10, 3, 1, 0, dev, full=False)
+        layer_block = {"workload": CONFIGS["cfg2"]["desc"], "tokens_per_s": lm["tokens_per_s_per_gpu"],
+                       "ms_per_step": lm["ms"], "step_breakdown_ms": lm["step_breakdown_ms"],
+                       "algorithmic_tflops": lm["algorithmic_tflops"], "spec_roofline": lm["spec_roofline"],
+                       "clocks": lm["clocks"]}
     if rank == 0:
         pk, pk_kind = peaks()
         f = D.flops_per_token(dcfg)
         per_gpu = T / (ms * 1e-3)
-        sustained = float(pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])))
-        achieved = f["total"] * per_gpu / 1e12
+        burst = float(pk.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
+        sustained = float(pk.get("bf16_tflops_sustained", burst))
+        dom = r["dominant"]
+        roof = dominant_roofline(f"tc_lors_gemm<fwd> (K1) on the {dom['R']}x{dom['C']} gate projection, {T} tokens "
+                                 "(the LoRS GEMMs are the step's dominant kernels, profiles/)", dom["flops"],
+                                 dom["ms"], f"{args.config}_gate_fwd", burst, f"{pk_kind} bf16 burst (timed alone)")
+        achieved_step = f["total"] * per_gpu / 1e12
         spec_roof = D.roofline_tokens_per_s(dcfg, SPEC_PEAKS["dense_tflops"], SPEC_PEAKS["sparse_tflops"])
         line = {
             "metric": METRIC, "value": world * per_gpu, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {name}-shaped decoder fine-tuning step (random init, "
-                                   "uniform token ids)", "layers": dcfg.n_layers, "dim": dcfg.dim,
-                       "ffn": dcfg.ffn, "heads": dcfg.n_heads, "kv_heads": dcfg.n_kv_heads, "vocab": dcfg.vocab,
-                       "rank": dcfg.rank, "sparsity": dcfg.sparsity if dcfg.sparsity == "two_four"
-                       else f"{dcfg.ratio:.0%} per-row magnitude", "seq": dcfg.seq, "batch_per_gpu": dcfg.batch,
-                       "global_batch": dcfg.batch * world, "parallelism": f"dp{world}",
-                       "forward": "2:4 sparse tensor cores" if args.sparse24 and dcfg.sparsity == "two_four"
-                       else "dense-masked tcgen05 (W_eff rebuilt on chip)",
-                       "l2": "weights and activations far larger than L2"},
+            "config": decoder_config(args.config, dcfg, world),
+            "path": {"forward": "2:4 sparse tensor cores" if args.sparse24 and dcfg.sparsity == "two_four"
+                     else "dense-masked tcgen05 (W_eff rebuilt on chip)", "adapter_grads": "ste (lors)",
+                     "optimizer": args.optimizer, "gradient_sync": "NCCL all-reduce of dA/dB buckets"
+                     if world > 1 else "none (1 GPU)"},
             "peak_hbm_gb": peak_gb,
             "memory": memory,
             "comparators_tokens_per_s": comp_speed,
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
-                         "frac": achieved / sustained, "traffic": None,
-                         "kernel": "whole fine-tuning step (model FLOPs / step time)",
-                         "peak_kind": pk_kind + " bf16 sustained",
-                         "flops_per_token": f, "spec_roofline_tokens_per_s_per_gpu": spec_roof,
-                         "frac_of_spec_roofline": per_gpu / spec_roof},
+            "roofline": roof,
+            "step_roofline": {"model_tflops": achieved_step, "flops_per_token": f,
+                              "frac_of_sustained": achieved_step / sustained,
+                              "sustained_peak_tflops": sustained,
+                              "spec_roofline_tokens_per_s_per_gpu": spec_roof,
+                              "frac_of_spec_roofline": per_gpu / spec_roof,
+                              "north_star_target_frac": 0.6},
+            "layer_cfg2": layer_block,
             "gpu_launches": r["launches"],
             "e2e": {"value": world * T / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": r["h2d"],
                     "d2h_bytes_per_step": 4, "ms_per_step": e2e_ms,
@@ -719,21 +824,36 @@ def run_decoder(args):
             "loss": r["loss"],
         }
         if world == 1 and not args.no_cpu:
-            line["cpu_baseline"] = decoder_cpu_baseline(dcfg)
+            print("[bench] cpu baseline", file=sys.stderr, flush=True)
+            line["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
-def main():
+def relaunch(args_list, n):
+    """--gpus N > 1 without torchrun's environment: one rank per GPU under torch.distributed.run."""
+    import random
+    import subprocess
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")            # NCCL's init log shows the ranks and transports
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + random.randrange(2000)),
+           os.path.abspath(__file__), *args_list]
+    return subprocess.call(cmd, env=env)
+
+
+def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("native", "reference"), default="native")
-    ap.add_argument("--config", choices=tuple(CONFIGS) + tuple(DECODER_CONFIGS), default="cfg2")
+    ap.add_argument("--config", choices=tuple(DECODER_CONFIGS) + tuple(CONFIGS), default=DEFAULT_CONFIG)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline sample")
+    ap.add_argument("--no-layer", action="store_true", help="decoder configs: skip the extra cfg2 layer block")
     ap.add_argument("--compare", action="store_true",
                     help="decoder configs: also run the dense-LoRA and SQFT-style decoders (peak HBM, tokens/s)")
     ap.add_argument("--optimizer", choices=("native", "p2p", "torch"), default="native",
@@ -741,16 +861,16 @@ def main():
                          "peer-memory reduce + AdamW kernel over symmetric memory (p2p), or torch AdamW")
     ap.add_argument("--sparse24", action="store_true",
                     help="decoder configs with 2:4 masks: forward on the sparse tensor cores")
-    args = ap.parse_args()
+    argv = sys.argv[1:] if argv is None else argv
+    args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
-    if args.config in DECODER_CONFIGS:
-        if args.impl == "reference":
-            return run_reference(args, None)
-        return run_decoder(args)
-    cfg = CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(argv, args.gpus)
     if args.impl == "reference":
-        return run_reference(args, cfg)
-    return run_native(args, cfg)
+        return run_reference(args)
+    if args.config in DECODER_CONFIGS:
+        return run_decoder(args)
+    return run_native(args, CONFIGS[args.config])
 
 
 if __name__ == "__main__":

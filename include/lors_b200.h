@@ -144,8 +144,13 @@ size_t lors_fwd_workspace(const lors_fwd_args* args);
 int lors_bwd(const lors_bwd_args* args, void* stream);
 size_t lors_bwd_workspace(const lors_bwd_args* args);
 
-/* W_eff (or merge() result) into out [R, C] in `dtype`, through the same
- * device function as the GEMM prologues; +0.0 bit pattern wherever M = 0. */
+/* W_eff (or merge() result) into out [R, C] in `dtype`: select(M, W + alpha a b, +0)
+ * with one fp32 fma per element and one rounding to `dtype`.  bf16 on tensor-core
+ * shapes runs the forward GEMM's own prologue (the same rank-r recompute MMA and
+ * the same weff_pair) with each tile TMA-stored instead of multiplied, so the
+ * result is bit-identical to the W_eff the forward and dX GEMMs consume
+ * (tests/test_weff_identity.py); fp32 and other shapes run the FFMA kernels'
+ * shared weff_value.  +0.0 bit pattern wherever M = 0. */
 int lors_effective_weight(int64_t R, int64_t C, int64_t r, int32_t dtype,
                           int32_t mask_mode, float alpha, const void* w,
                           const uint32_t* mask_bits, const void* a,

@@ -190,8 +190,8 @@ int lors_effective_weight(int64_t R, int64_t C, int64_t r, int32_t dtype, int32_
   if (dtype == LORS_DTYPE_F32)
     return effective_weight<float>((const float*)w, bits, (const float*)a, (const float*)b, (float*)out, (int)R,
                                    (int)C, (int)r, alpha, s);
-  return effective_weight<bf16>((const bf16*)w, bits, (const bf16*)a, (const bf16*)b, (bf16*)out, (int)R, (int)C,
-                                (int)r, alpha, s);
+  return tc_effective_weight((const bf16*)w, bits, (const bf16*)a, (const bf16*)b, (bf16*)out, (int)R, (int)C,
+                             (int)r, alpha, s);
 }
 
 int lors_pack_mask(int64_t R, int64_t C, int32_t dtype, const void* w, uint32_t* bits, void* stream) {

@@ -64,8 +64,10 @@ __device__ __forceinline__ bool mask_at(const T w, const uint32_t* __restrict__ 
   return to_f(w) != 0.0f;
 }
 
-// The effective-weight element, the one definition shared by every kernel:
-//   select(M, w + alpha * p, +0.0)
+// The effective-weight element of the FFMA kernels (fp32 mode, K6 fp32, shapes TMA
+// cannot address):  select(M, fma(alpha, p, w), +0.0), rounded once to the storage
+// type by the caller.  The tensor-core path's weff_pair (ptx_sm100.cuh) is the same
+// arithmetic on bf16 pairs; its K6 export runs that prologue itself.
 // `select`, not multiplication, so pruned entries are bit-exact +0.0
 // (reference merged_weight adapters.py:214-224 yields +0.0 there because W
 // is normalised to +0.0, prune.py:47; (w + alpha*p)*0 could give -0.0).

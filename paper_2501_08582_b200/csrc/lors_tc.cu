@@ -744,7 +744,12 @@ constexpr size_t smem_bytes() {
 }
 }  // namespace rg
 
-template <bool DX, int RP, bool BITS, bool SP>
+// EX (K6 export, forward orientation only): no activations, no main MMA, no
+// accumulator -- each transformed W_eff tile is TMA-stored to W_eff [R, C]
+// instead of being consumed, so lors_effective_weight / merge() return exactly
+// the tiles the forward's tensor cores multiply (same recompute MMA, same
+// weff_pair).
+template <bool DX, int RP, bool BITS, bool SP, bool EX = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1)
     tc_lors_gemm_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmAct2,
                         const __grid_constant__ CUtensorMap tmW,
@@ -755,6 +760,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
                         unsigned int* __restrict__ counters, float alpha, int n_tok) {
   using namespace rg;
   static_assert(!(SP && DX), "2:4 sparse tensor cores apply to the forward only (SURVEY C6)");
+  static_assert(!EX || (!DX && !SP && LORS_PERSIST), "W_eff export runs the persistent forward prologue");
   constexpr int XW = xw<SP>(), XFORM_THREADS = 32 * XW;
   constexpr int W_SF = XW, W_MMA = XW + 1, W_ACT = XW + 2, W_RELAY = XW + 3, W_WLOAD = XW + 4;
   constexpr int NE = ne<SP>(), NW = nw<SP>(), NA = na<SP>(), D = lookahead<SP>();
@@ -958,7 +964,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     cluster_wait();
   } else if (warp == W_ACT) {
     // ------------------------------------------------------------ activation-ring producer (both CTAs)
-    if (lane == 0) {
+    if (lane == 0 && !EX) {
       for (int n = 0, g = 0; n < my_units; ++n) {
       int kb, ke, ut, part;
       unit(n, m0, l0, kb, ke, ut, part);
@@ -980,7 +986,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   } else if (warp == W_RELAY) {
     cluster_wait();
     // ------------------------------------------------------------ activation relay (peer CTA)
-    if (!leader && lane == 0) {
+    if (!leader && lane == 0 && !EX) {
       int total = 0;
       for (int n = 0; n < my_units; ++n) {
         int m_, l_, kb, ke, ut, part;
@@ -1099,8 +1105,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       for (int n = 0; n < my_units; ++n) total += unit_len(n);
       int rk = 0, rn = 0, mk = 0, mn = 0;
       int rlen = my_units > 0 ? unit_len(0) : 1, mlen = rlen;
-      for (int j = 0; j < total + D; ++j) {
-        const bool has_rec = j < total, has_main = j >= D;
+      for (int j = 0; j < total + (EX ? 0 : D); ++j) {
+        const bool has_rec = j < total, has_main = !EX && j >= D;
         const bool flip = has_rec && rk == 0 && j > 0;
 #if defined(LORS_EXP_CLOCK) && !defined(LORS_EXP_CLOCK_PRO)
         if (j == D && lane == 0) t_ev[0] = gtimer();
@@ -1132,7 +1138,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     const int t = q * 32 + lane;   // feature row inside the tile (TMEM lane)
     int gm = m0 + t;               // global output feature (per tile)
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    const uint32_t alpha2 = pack_bf16x2(alpha, alpha);
+    const uint64_t alpha_x2 = f32x2_splat(alpha);   // fp32 alpha for weff_pair
     // Per k-step: issue the TMEM load of the rank-r product and all W loads,
     // release the recompute buffer, then transform and store.  (Pipelining the
     // loads of step i + 1 under step i measured no faster.)
@@ -1191,7 +1197,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       const int wb = i % NA, wi = i % NW;
       // 3. destination buffer drained by the MMA of step i - NA
       // waits for the commit of main(i - NA), the previous user of this buffer
-      if (i >= NA) mbar_wait(&wempty[(i % NGRP) * NA + wb].b, ((i - NA) / A_PERIOD) & 1);
+      if (!EX && i >= NA) mbar_wait(&wempty[(i % NGRP) * NA + wb].b, ((i - NA) / A_PERIOD) & 1);
       const uint32_t dst = smem_u32(weff + wb * WEFF_BYTES);
 #ifdef LORS_EXP_NO_XFORM
       constexpr bool XF = false;  // timing experiment: W_eff buffers left as they are
@@ -1199,19 +1205,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       constexpr bool XF = true;
 #endif
       if (XF && SP && meta24 != nullptr) {
-        // 2:4 with precomputed index nibbles: select the two kept positions of each
-        // group of 4 first (W and the rounded rank-r product alike), then form
-        // select(W != 0, W + alpha P, +0) on the kept pair only -- bit-identical to
-        // transforming all four and compressing afterwards, half the arithmetic
+        // 2:4 with precomputed index nibbles: weff_pair on the group's four
+        // values, then one prmt keeps the two positions the nibble names (no
+        // on-chip nibble derivation) -- the dense prologue's values, compressed
         uint32_t comp[8];
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
           const uint32_t nib = (mw >> (4 * g)) & 0xFu;
           const uint32_t sel = 0x1010u + (nib & 3u) * 0x22u + (nib >> 2) * 0x2200u;
-          const uint32_t wsel = prmt(wv[2 * g], wv[2 * g + 1], sel);
-          const uint32_t psel = prmt(cvt_bf16x2(__uint_as_float(p[4 * g]), __uint_as_float(p[4 * g + 1])),
-                                     cvt_bf16x2(__uint_as_float(p[4 * g + 2]), __uint_as_float(p[4 * g + 3])), sel);
-          comp[g] = fma_bf16x2(alpha2, psel, wsel) & nonzero_mask_bf16x2(wsel);
+          const uint32_t o0 = weff_pair(wv[2 * g], __uint_as_float(p[4 * g]), __uint_as_float(p[4 * g + 1]),
+                                        alpha_x2, nonzero_mask_bf16x2(wv[2 * g]));
+          const uint32_t o1 = weff_pair(wv[2 * g + 1], __uint_as_float(p[4 * g + 2]), __uint_as_float(p[4 * g + 3]),
+                                        alpha_x2, nonzero_mask_bf16x2(wv[2 * g + 1]));
+          comp[g] = prmt(o0, o1, sel);
         }
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
@@ -1239,7 +1245,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
             const uint32_t w2 = wv[4 * c + u];
             const uint32_t keep = BITS ? bits2_to_mask((mword >> (c * 8 + 2 * u)) & 3u) : nonzero_mask_bf16x2(w2);
             keepm[u] = keep;
-            o[u] = weff_pair(w2, __uint_as_float(p[c * 8 + 2 * u]), __uint_as_float(p[c * 8 + 2 * u + 1]), alpha2,
+            o[u] = weff_pair(w2, __uint_as_float(p[c * 8 + 2 * u]), __uint_as_float(p[c * 8 + 2 * u + 1]), alpha_x2,
                              keep);
           }
           if (SP) {
@@ -1309,7 +1315,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
                 keep = nonzero_mask_bf16x2(wq[mm]);
               }
               const uint32_t o = weff_pair(wq[mm], __uint_as_float(p[16 * g + 4 * j + 2 * sm]),
-                                           __uint_as_float(p[16 * g + 4 * j + 2 * sm + 1]), alpha2, keep);
+                                           __uint_as_float(p[16 * g + 4 * j + 2 * sm + 1]), alpha_x2, keep);
               sts32(dst + ct * 128 + ((((k >> 3)) ^ (ct & 7)) << 4) + (k & 7) * 2, o);
             }
           }
@@ -1320,6 +1326,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 #ifdef LORS_EXP_CLOCK_PRO
       if (i == 0 && warp == 0 && lane == 0) t_ev[2] = gtimer();
 #endif
+      if (EX) {
+        // export: the whole [128 rows][64 k] SW128 tile is the TMA box of W_eff at
+        // (k0, m0); the store has read the buffer before anyone rewrites it
+        named_bar_sync(1, XFORM_THREADS);
+        if (warp == 0 && lane == 0) {
+          tma_store_2d(&tmOut, weff + wb * WEFF_BYTES, kq * BK, m0);
+          tma_store_commit();
+          tma_store_wait_all();
+        }
+        named_bar_sync(1, XFORM_THREADS);
+        if (lane == 0) mbar_arrive(&wfree[wi].b);
+        return;
+      }
       if (lane == 0) {
         mbar_arrive(&wfree[wi].b);                   // done reading the W tile
         mbar_arrive_cluster(mready_l + wb * 16);     // W_eff half ready for the pair MMA
@@ -1416,6 +1435,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           release(g);
           finish(g, kq, p, wv, mw);
         }
+        if (EX) continue;   // no accumulator
         // -------------------------------------------------------- epilogue of unit n
         mbar_wait(accf, n & 1);
         tc_fence_after();
@@ -1489,6 +1509,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           named_bar_sync(1, XFORM_THREADS);
         }
       }
+      if (EX && warp == 0 && lane == 0) tma_store_wait_done();
     } else {
     for (int i = grp; i < nk; i += NGRP) {
       uint32_t p[32], wv[16], mw = 0;
@@ -1726,6 +1747,44 @@ static int lors_gemm(int rp, const bf16* act, const bf16* w, const bf16* a, cons
       return launch_lors_gemm<DX, 32, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s, ws, ws_bytes);
     default:
       return launch_lors_gemm<DX, 64, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s, ws, ws_bytes);
+  }
+}
+
+// K6 on the tensor-core path (merged_weight / merge, adapters.py:214-224, 709-727):
+// the forward kernel's own prologue -- the same rank-r recompute MMA and the same
+// weff_pair -- with each W_eff tile TMA-stored to out [R, C] instead of multiplied,
+// so the exported weight is bit-identical to the one the forward and dX GEMMs use.
+template <int RP>
+static int launch_weff_export(const bf16* w, const bf16* a, const bf16* b, const uint32_t* bits, bf16* out, int R,
+                              int C, int r, float alpha, cudaStream_t s) {
+  using namespace rg;
+  CUtensorMap tW, tS, tF, tOut;
+  int st;
+  if ((st = make_map(&tW, w, C, R, 64, 128, 128, "W (export)"))) return st;
+  if ((st = make_map(&tS, b, C, r, 32, RP, 64, "b (streamed half)"))) return st;
+  if ((st = make_map(&tF, a, r, R, RP, 128, RP * 2, "a (fixed)"))) return st;
+  if ((st = make_map(&tOut, out, C, R, 64, 128, 128, "W_eff out"))) return st;   // [128 rows][64 k] SW128
+  auto kern = bits ? tc_lors_gemm_kernel<false, RP, true, false, true> : tc_lors_gemm_kernel<false, RP, false, false, true>;
+  const size_t smem = smem_bytes<RP, false>();
+  LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                "weff export smem attribute");
+  const int n_f = (int)ceil_div(R, 2 * BM);
+  const int mc = persistent_clusters<false, RP, false>();
+  dim3 grid((unsigned)(2 * std::min(n_f, mc)));
+  // the activation maps are never read in export mode (W's map stands in)
+  kern<<<grid, threads<false>(), smem, s>>>(tW, tW, tW, tS, tF, tOut, nullptr, bits, nullptr, (int)ceil_div(C, 32), R,
+                                            C, /*n_t=*/1, n_f, /*split=*/1, nullptr, nullptr, alpha, 0);
+  LORS_CHECK_LAUNCH("tc_lors_gemm<export>");
+  return LORS_OK;
+}
+
+int tc_effective_weight(const bf16* w, const uint32_t* bits, const bf16* a, const bf16* b, bf16* out, int R, int C,
+                        int r, float alpha, cudaStream_t s) {
+  if (!tc_shape_ok(R, C, r)) return effective_weight<bf16>(w, bits, a, b, out, R, C, r, alpha, s);  // = the FFMA path's
+  switch (pad_rank(r)) {
+    case 16: return launch_weff_export<16>(w, a, b, bits, out, R, C, r, alpha, s);
+    case 32: return launch_weff_export<32>(w, a, b, bits, out, R, C, r, alpha, s);
+    default: return launch_weff_export<64>(w, a, b, bits, out, R, C, r, alpha, s);
   }
 }
 

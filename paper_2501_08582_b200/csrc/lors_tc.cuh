@@ -7,4 +7,8 @@ size_t tc_fwd_workspace(const lors_fwd_args* a);
 size_t tc_bwd_workspace(const lors_bwd_args* a);
 int tc_fwd(const lors_fwd_args* a, cudaStream_t s);
 int tc_bwd(const lors_bwd_args* a, cudaStream_t s);
+bool tc_shape_ok(int64_t R, int64_t C, int64_t r);
+// bf16 W_eff through the forward's tensor-core prologue (FFMA kernel for shapes TMA cannot address)
+int tc_effective_weight(const __nv_bfloat16* w, const uint32_t* bits, const __nv_bfloat16* a, const __nv_bfloat16* b,
+                        __nv_bfloat16* out, int R, int C, int r, float alpha, cudaStream_t s);
 }  // namespace lors

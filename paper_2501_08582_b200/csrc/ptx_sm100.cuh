@@ -466,9 +466,26 @@ __device__ __forceinline__ uint32_t nonzero_mask_bf16x2(uint32_t w) {
 __device__ __forceinline__ uint32_t bits2_to_mask(uint32_t two) {
   return ((two & 1u) * 0xFFFFu) | ((two >> 1) * 0xFFFF0000u);
 }
-// W_eff pair = select(M, W + alpha * P, +0): one cvt, one bf16x2 fma, one and.
-__device__ __forceinline__ uint32_t weff_pair(uint32_t w2, float p_lo, float p_hi, uint32_t alpha2, uint32_t keep) {
-  return fma_bf16x2(alpha2, cvt_bf16x2(p_lo, p_hi), w2) & keep;
+// (alpha, alpha) as the packed fp32 pair operand of fma.rn.f32x2
+__device__ __forceinline__ uint64_t f32x2_splat(float v) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(v));
+  return r;
+}
+// W_eff pair = select(M, bf16_rn(fma(alpha, P, W)), +0) -- THE effective-weight
+// definition of the bf16 path, the same arithmetic as weff_value (lors_common.cuh):
+// W widened exactly to fp32, alpha applied in fp32 inside one fma per element
+// (one FFMA2 for the pair), one rounding to bf16, then the select (an `and` with
+// the keep mask, so pruned entries are the +0.0 bit pattern).  Every tensor-core
+// prologue (K1, K2, K3) and the tensor-core K6 export call this.
+__device__ __forceinline__ uint32_t weff_pair(uint32_t w2, float p_lo, float p_hi, uint64_t alpha_x2, uint32_t keep) {
+  uint64_t wl, pl, rl;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(wl) : "f"(__uint_as_float(w2 << 16)), "f"(__uint_as_float(w2 & 0xFFFF0000u)));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(pl) : "f"(p_lo), "f"(p_hi));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rl) : "l"(alpha_x2), "l"(pl), "l"(wl));
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(rl));
+  return cvt_bf16x2(lo, hi) & keep;
 }
 
 // ---------------------------------------------------------------------------
