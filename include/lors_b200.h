@@ -79,6 +79,13 @@ typedef enum { LORS_GRAD_STE = 0, LORS_GRAD_MASKED = 1 } lors_grad_mode_t;
                                      /* (one fill of a joint buffer by the      */
                                      /* caller replaces the library's two       */
                                      /* zeroing launches); ignored elsewhere    */
+#define LORS_FLAG_DETERMINISTIC (1u << 5) /* backward: dA / dB (and P, Q) through split
+                                        partials summed in a fixed order -- no
+                                        atomics or TMA reduce-adds -- so they are
+                                        bitwise reproducible run to run (the
+                                        reference replays training bitwise,
+                                        test_train.py:169-178); needs the larger
+                                        workspace lors_bwd_workspace reports */
 #define LORS_FLAG_FAULT_DA_SIGN (1u << 30) /* negative control: flip dA sign,
                                               mirrors FAULT_INJECTION
                                               "lors_backward_sign_flip"

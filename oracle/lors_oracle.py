@@ -100,6 +100,24 @@ def sqft_gc_backward(w, a, b, x, dy, alpha=ALPHA_DEFAULT, with_bias=False):
     return Grads(da=da, db=db, dx=dx, dbias=dbias)
 
 
+def lors_adapter_grads(w, a, b, x, dy, alpha=ALPHA_DEFAULT):
+    """(da, db) of lors_backward alone -- adapters.py:396-399 in the pinned order
+    (xt_bt, at_dy, da, db); dx is token-local and is checked on token subsets."""
+    xt_bt = x.T.copy() @ b.T.copy()           # :396
+    at_dy = a.T.copy() @ dy                   # :397
+    da = (dy @ xt_bt) * alpha                 # :398
+    db = (at_dy @ x.T.copy()) * alpha         # :399
+    return da, db
+
+
+def sqft_gc_adapter_grads(w, a, b, x, dy, alpha=ALPHA_DEFAULT):
+    """(da, db) of sqft_gc_backward alone -- _sqft_grads, adapters.py:303-312."""
+    masked = (dy @ x.T.copy()) * mask_matrix(w)
+    da = (masked @ b.T.copy()) * alpha
+    db = (a.T.copy() @ masked) * alpha
+    return da, db
+
+
 def merge(w, a, b, alpha=ALPHA_DEFAULT, original_mask=None):
     """Finalize into a sparse weight -- adapters.py:709-727."""
     if original_mask is None:

@@ -17,8 +17,10 @@
 //   K4b tc_q_da             Q = dY a and dA = alpha dY^T P from one pass over dY
 //        (adapters.py:397-398), partials by TMA bulk reduce-add.
 //   K5 tc_masked_grad_pair  G = (dY^T X) . M in TMEM on CTA pairs, contracted into
-//        dA / dB (the sqft_gc masked gradient, adapters.py:303-312); the one-CTA
-//        tc_masked_grad is kept for A/B runs (LORS_K5_SINGLE).
+//        dA / dB (the sqft_gc masked gradient, adapters.py:303-312).
+//   LORS_FLAG_DETERMINISTIC: the rank-r products and K5 write split partials to
+//        workspace slabs that one kernel sums in a fixed order (no atomics, no TMA
+//        reduce-adds), so dA / dB are bitwise reproducible run to run.
 //
 // Timing-experiment switches (tools/exp_variants.sh, never set in the product
 // build): LORS_EXP_NO_RECOMPUTE / _NO_XFORM / _NO_W_TMA / _NO_ACT_TMA skip one
@@ -148,7 +150,9 @@ static inline uint32_t pad_rank(int r) { return r <= 16 ? 16 : r <= 32 ? 32 : 64
 // K4: skinny GEMM  D[M, BN] = sum_k A[m, k] B[n, k]   (M tile 128, BN = padded r)
 //   A_MN / B_MN: operand stored MN-major (m resp. n contiguous) instead of K-major.
 //   OUT 0: bf16 out[m*ldo + n]; 1: fp32 alpha*out[m*ldo + n]; 2: fp32 alpha*out[n*ldo + m]
-//   (1/2 accumulate atomically when the grid splits K).
+//   out_mode 0: plain stores; 1: the grid splits K and 1/2 accumulate atomically (OUT 0:
+//   fp32 red.add into a caller-zeroed accumulator); 2 (deterministic): split s stores its raw
+//   fp32 partial to out[s][M][BN], summed in split order by skinny_reduce_kernel.
 // warps: 0 TMA producer, 1 MMA issuer + TMEM owner, 2..5 epilogue.
 // ===========================================================================
 namespace sk {
@@ -163,7 +167,7 @@ constexpr size_t smem_bytes() { return 1024 + STAGES * (A_BYTES + b_bytes<BN>())
 template <int BN, bool A_MN, bool B_MN, int OUT>
 __global__ void __launch_bounds__(sk::THREADS, 1)
     tc_skinny_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, void* out,
-                     int M, int N, int K, int k_per_split, int ldo, float alpha, int atomic_out) {
+                     int M, int N, int K, int k_per_split, int ldo, float alpha, int out_mode) {
   using namespace sk;
   constexpr uint32_t B_BYTES = b_bytes<BN>();
   constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
@@ -255,7 +259,14 @@ __global__ void __launch_bounds__(sk::THREADS, 1)
       tmem_ld_x16(taddr + c0, v);
       tmem_ld_wait();
       if (m < M) {
-        if (OUT == 0 && atomic_out) {  // split-K partial: fp32 sums, converted to bf16 afterwards
+        if (out_mode == 2) {   // deterministic split: this split's partial row, plain stores
+          float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) +
+                                                ((int64_t)blockIdx.y * M + m) * BN + c0);
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+            o[h] = make_float4(__uint_as_float(v[h * 4]), __uint_as_float(v[h * 4 + 1]), __uint_as_float(v[h * 4 + 2]),
+                               __uint_as_float(v[h * 4 + 3]));
+        } else if (OUT == 0 && out_mode) {  // split-K partial: fp32 sums, converted to bf16 afterwards
           float* o = reinterpret_cast<float*>(out) + (int64_t)m * ldo + c0;
 #pragma unroll
           for (int h = 0; h < 4; ++h)
@@ -283,7 +294,7 @@ __global__ void __launch_bounds__(sk::THREADS, 1)
             if (n < N) {
               const float val = alpha * __uint_as_float(v[j]);
               float* dst = OUT == 1 ? o + (int64_t)m * ldo + n : o + (int64_t)n * ldo + m;
-              if (atomic_out) atomicAdd(dst, val);
+              if (out_mode) atomicAdd(dst, val);
               else *dst = val;
             }
           }
@@ -299,9 +310,39 @@ __global__ void __launch_bounds__(sk::THREADS, 1)
 // host launcher for one skinny product.
 //   A: K-major tensor [M, K] (A_MN=false) or MN-major [K, M] (A_MN=true), bf16
 //   B: K-major [N, K] or MN-major [K, N]
+// deterministic split: out[m, n] (OUT's layout) = alpha * sum over s in order of part[s][m][n]
+template <int OUT>
+__global__ void skinny_reduce_kernel(const float* __restrict__ part, int split, int M, int N, int BN, void* out,
+                                     int ldo, float alpha) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)M * N) return;
+  const int m = OUT == 2 ? (int)(i % M) : (int)(i / N);   // OUT 2 writes along m (coalesced)
+  const int n = OUT == 2 ? (int)(i / M) : (int)(i % N);
+  float acc = 0.f;
+  for (int k = 0; k < split; ++k) acc += part[((int64_t)k * M + m) * BN + n];
+  if (OUT == 0) reinterpret_cast<bf16*>(out)[(int64_t)m * ldo + n] = __float2bfloat16_rn(acc);
+  else if (OUT == 1) reinterpret_cast<float*>(out)[(int64_t)m * ldo + n] = alpha * acc;
+  else reinterpret_cast<float*>(out)[(int64_t)n * ldo + m] = alpha * acc;
+}
+
+// K split of a skinny product: the CTAs fill one wave at two resident per SM (never a
+// second, mostly empty wave) and every split keeps >= 4 k-blocks
+static int skinny_split(int M, int K) {
+  const int mt = (int)ceil_div(M, sk::BM), kblocks = (int)ceil_div(K, sk::BK);
+  const int split = (int)std::max<int64_t>(1, std::min<int64_t>((2 * num_sms()) / mt, kblocks / 4));
+  const int kps = (int)ceil_div(kblocks, split) * sk::BK;
+  return (int)ceil_div(K, kps);
+}
+// bytes of the deterministic partials of one skinny product (0 = no split)
+static size_t skinny_partial_bytes(int M, int K, int bn) {
+  const int split = skinny_split(M, K);
+  return split > 1 ? (size_t)split * (size_t)M * (size_t)bn * sizeof(float) : 0;
+}
+
 template <int BN, bool A_MN, bool B_MN, int OUT>
 static int launch_skinny(const bf16* A, const bf16* B, void* out, int M, int N, int K, int ldo, float alpha,
-                         bool allow_split, cudaStream_t s, float* acc32 = nullptr, bool zeroed = false) {
+                         bool allow_split, cudaStream_t s, float* acc32 = nullptr, bool zeroed = false,
+                         float* det_part = nullptr) {
   CUtensorMap tA, tB;
   int st;
   if (A_MN) st = make_map(&tA, A, M, K, 64, 64, 128, "skinny A (MN)");
@@ -316,20 +357,27 @@ static int launch_skinny(const bf16* A, const bf16* B, void* out, int M, int N, 
   // second, mostly empty wave); OUT 0 splits only into a caller-zeroed fp32
   // accumulator (acc32)
   int split = 1;
-  const bool can_split = allow_split && (OUT != 0 || acc32 != nullptr);
-  if (can_split) split = (int)std::max<int64_t>(1, std::min<int64_t>((2 * num_sms()) / mt, kblocks / 4));
+  const bool can_split = allow_split && (OUT != 0 || acc32 != nullptr || det_part != nullptr);
+  if (can_split) split = skinny_split(M, K);
   const int kps = (int)ceil_div(kblocks, split) * sk::BK;
-  split = (int)ceil_div(K, kps);
-  if (split > 1 && OUT != 0 && !zeroed) {
-    const size_t elems = OUT == 2 ? (size_t)N * ldo : (size_t)M * ldo;
-    LORS_CUDA_TRY(cudaMemsetAsync(out, 0, elems * sizeof(float), s), "zero split-K output");
-  }
-  if (OUT == 0 && acc32 != nullptr) out = acc32;  // fp32 sums; the caller converts to bf16
   auto kern = tc_skinny_kernel<BN, A_MN, B_MN, OUT>;
   const size_t smem = sk::smem_bytes<BN>();
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "skinny smem attribute");
-  const int atomic_out = (split > 1 || (OUT == 0 && acc32 != nullptr)) ? 1 : 0;
+  if (det_part != nullptr && split > 1) {   // deterministic: partials, then one ordered sum
+    kern<<<dim3(mt, split), sk::THREADS, smem, s>>>(tA, tB, det_part, M, N, K, kps, ldo, alpha, 2);
+    LORS_CHECK_LAUNCH("tc_skinny (partials)");
+    const int64_t n = (int64_t)M * N;
+    skinny_reduce_kernel<OUT><<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(det_part, split, M, N, BN, out, ldo, alpha);
+    LORS_CHECK_LAUNCH("skinny_reduce");
+    return LORS_OK;
+  }
+  if (split > 1 && OUT != 0 && !zeroed) {
+    const size_t elems = OUT == 2 ? (size_t)N * ldo : (size_t)M * ldo;
+    LORS_CUDA_TRY(cudaMemsetAsync(out, 0, elems * sizeof(float), s), "zero split-K output");
+  }
+  if (OUT == 0 && acc32 != nullptr && det_part == nullptr) out = acc32;  // fp32 sums; the caller converts to bf16
+  const int atomic_out = (split > 1 || (OUT == 0 && acc32 != nullptr && det_part == nullptr)) ? 1 : 0;
   kern<<<dim3(mt, split), sk::THREADS, smem, s>>>(tA, tB, out, M, N, K, kps, ldo, alpha, atomic_out);
   LORS_CHECK_LAUNCH("tc_skinny");
   return LORS_OK;
@@ -338,11 +386,15 @@ static int launch_skinny(const bf16* A, const bf16* B, void* out, int M, int N, 
 // dispatch on the padded rank
 template <bool A_MN, bool B_MN, int OUT>
 static int skinny(int rp, const bf16* A, const bf16* B, void* out, int M, int N, int K, int ldo, float alpha,
-                  bool allow_split, cudaStream_t s, float* acc32 = nullptr, bool zeroed = false) {
+                  bool allow_split, cudaStream_t s, float* acc32 = nullptr, bool zeroed = false,
+                  float* det_part = nullptr) {
   switch (rp) {
-    case 16: return launch_skinny<16, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32, zeroed);
-    case 32: return launch_skinny<32, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32, zeroed);
-    default: return launch_skinny<64, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32, zeroed);
+    case 16:
+      return launch_skinny<16, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32, zeroed, det_part);
+    case 32:
+      return launch_skinny<32, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32, zeroed, det_part);
+    default:
+      return launch_skinny<64, A_MN, B_MN, OUT>(A, B, out, M, N, K, ldo, alpha, allow_split, s, acc32, zeroed, det_part);
   }
 }
 
@@ -1800,287 +1852,8 @@ static size_t lors_gemm_workspace(int rp, int L, int R, int C) {
 
 // ===========================================================================
 // K5: masked-G fused adapter gradient (north_star 3; oracle _sqft_grads,
-// adapters.py:303-312).
-//
-// One CTA owns G[128 rows of R x 256 cols of C] = sum_l dY_t[l, R] X_t[l, C]:
-//   mainloop : tcgen05 M=128 N=256 over all L tokens (A = dY_t tile, B = X_t
-//              tile, both MN-major via TMA), fp32 accumulator in TMEM;
-//   mask     : 4 epilogue warps read G rows from TMEM, select on W != 0 (or the
-//              packed bits), round to bf16 and park G.M as a K-major SW128 tile
-//              in shared memory -- G never reaches HBM;
-//   contract : dA_part[128 x r]  = (G.M) . b[:, C-tile]^T   (M=128, K=256)
-//              dB_part^T[256 x r] = (G.M)^T . a[R-tile]      (2 x M=128, K=128)
-//              with the same shared-memory bytes read K-major and MN-major;
-//   reduce   : alpha * partials added into dA / dB with red.global.add.v4.f32.
-// warps: 0 TMA producer, 1 MMA issuer + TMEM owner, 2..5 mask / reduce.
-// ===========================================================================
-namespace mg {
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 3, THREADS = 192;
-constexpr uint32_t A_BYTES = BM * BK * 2;   // 16 KB  dY tile [64 tokens][128 R]  (2 MN atoms)
-constexpr uint32_t B_BYTES = BN * BK * 2;   // 32 KB  X tile  [64 tokens][256 C]  (4 MN atoms)
-constexpr uint32_t GM_BYTES = BM * BN * 2;  // 64 KB  masked G tile, 4 K-atoms of [128 R][64 C]
-constexpr uint32_t G_COL = 0, DA_COL = 256, DB_COL = 320;
-template <int RP>
-constexpr uint32_t bt_bytes() { return RP * BN * 2; }   // b[:, C-tile] as 4 K-atoms of [RP][64 C]
-template <int RP>
-constexpr uint32_t at_bytes() { return BM * RP * 2; }   // a[R-tile, :] MN-major [128 R][RP]
-template <int RP>
-constexpr size_t smem_bytes() { return 1024 + STAGES * (A_BYTES + B_BYTES) + bt_bytes<RP>() + at_bytes<RP>() + 256; }
-}  // namespace mg
-
-template <int RP, bool BITS>
-__global__ void __launch_bounds__(mg::THREADS, 1)
-    tc_masked_grad_kernel(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmX,
-                          const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmA,
-                          const __grid_constant__ CUtensorMap tmDAo, const __grid_constant__ CUtensorMap tmDBo,
-                          const bf16* __restrict__ w, const uint32_t* __restrict__ bits, int words_per_row,
-                          int L, int R, int C, int r, float alpha) {
-  using namespace mg;
-  constexpr uint32_t BT = bt_bytes<RP>(), AT = at_bytes<RP>();
-  constexpr uint32_t SWR = RP * 2;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;                          // [STAGES] dY tiles
-  uint8_t* sB = sA + STAGES * A_BYTES;         // [STAGES] X tiles
-  uint8_t* sBt = sB + STAGES * B_BYTES;        // b tile (dA contraction, B operand)
-  uint8_t* sAt = sBt + BT;                     // a tile (dB contraction, B operand)
-  uint8_t* sGM = smem;                         // masked G (reuses the drained pipeline)
-  Bar16* bars = reinterpret_cast<Bar16*>(sAt + AT);
-  Bar16* full = bars;                          // [STAGES]
-  Bar16* empty = full + STAGES;                // [STAGES]
-  uint64_t* gfull = &(empty + STAGES)->b;      // G accumulated
-  uint64_t* abfull = &(empty + STAGES + 1)->b; // a / b tiles landed
-  uint64_t* gmready = &(empty + STAGES + 2)->b;  // 4 mask warps parked G.M
-  uint64_t* cfull = &(empty + STAGES + 3)->b;  // contractions done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + STAGES + 4);
-
-  const int warp = warp_id(), lane = lane_id();
-  // consecutive CTAs walk the C tiles of one R panel: a wave covers a few dY_t column
-  // panels and all of X_t, which stays L2-resident across waves
-  const int m0 = blockIdx.y * BM;   // R rows
-  const int c0 = blockIdx.x * BN;   // C cols
-  const int nk = (L + BK - 1) / BK;
-
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s].b, 1);
-      mbar_init(&empty[s].b, 1);
-    }
-    mbar_init(gfull, 1);
-    mbar_init(abfull, 1);
-    mbar_init(gmready, 4);
-    mbar_init(cfull, 1);
-    fence_barrier_init();
-    tma_prefetch_desc(&tmDY);
-    tma_prefetch_desc(&tmX);
-    tma_prefetch_desc(&tmB);
-    tma_prefetch_desc(&tmA);
-  }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_arrive_expect_tx(abfull, BT + AT);
-      for (int q = 0; q < 4; ++q) tma_load_2d(sBt + q * (RP * 128), &tmB, abfull, c0 + 64 * q, 0);
-      tma_load_2d(sAt, &tmA, abfull, 0, m0);
-      for (int i = 0; i < nk; ++i) {
-        const int s = i % STAGES;
-        mbar_wait(&empty[s].b, ((i / STAGES) & 1) ^ 1);
-        mbar_arrive_expect_tx(&full[s].b, A_BYTES + B_BYTES);
-        const int l0 = i * BK;
-        uint8_t* a = sA + s * A_BYTES;
-        uint8_t* b = sB + s * B_BYTES;
-        tma_load_2d(a, &tmDY, &full[s].b, m0, l0);
-        tma_load_2d(a + A_BYTES / 2, &tmDY, &full[s].b, m0 + 64, l0);
-        for (int q = 0; q < 4; ++q) tma_load_2d(b + q * (B_BYTES / 4), &tmX, &full[s].b, c0 + 64 * q, l0);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc_g = make_idesc_bf16(128, 256, true, true);
-      for (int i = 0; i < nk; ++i) {
-        const int s = i % STAGES;
-        mbar_wait(&full[s].b, (i / STAGES) & 1);
-        tc_fence_after();
-        const uint32_t a_base = smem_u32(sA + s * A_BYTES), b_base = smem_u32(sB + s * B_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk)
-          mma_bf16(tmem + G_COL, make_sdesc(a_base + kk * 2048, A_BYTES / 2, 1024, SW_128),
-                   make_sdesc(b_base + kk * 2048, B_BYTES / 4, 1024, SW_128), idesc_g, (i > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&empty[s].b);
-      }
-      mma_commit(gfull);
-      // contractions once the mask warps parked G.M
-      mbar_wait(gmready, 0);
-      mbar_wait(abfull, 0);
-      tc_fence_after();
-      const uint32_t gm = smem_u32(sGM), bt = smem_u32(sBt), at = smem_u32(sAt);
-      constexpr uint32_t idesc_da = make_idesc_bf16(128, RP, false, false);   // G.M K-major, b K-major
-      constexpr uint32_t idesc_db = make_idesc_bf16(128, RP, true, true);     // (G.M)^T MN-major, a MN-major
-#pragma unroll
-      for (int kk = 0; kk < BN / 16; ++kk) {   // K = 256 columns of C, 4 per 64-wide atom
-        const uint32_t q = kk >> 2, o = (kk & 3) * 32;
-        mma_bf16(tmem + DA_COL, make_sdesc(gm + q * 16384 + o, 16, 1024, SW_128),
-                 make_sdesc(bt + q * (RP * 128) + o, 16, 1024, SW_128), idesc_da, kk > 0 ? 1u : 0u);
-      }
-#pragma unroll
-      for (int hc = 0; hc < 2; ++hc) {         // C halves of 128 (M), K = 128 rows of R
-#pragma unroll
-        for (int kk = 0; kk < BM / 16; ++kk) {
-          mma_bf16(tmem + DB_COL + hc * 64, make_sdesc(gm + hc * 32768 + kk * 2048, 16384, 1024, SW_128),
-                   make_sdesc(at + kk * 16 * SWR, 0, 8 * SWR, sw_layout(SWR)), idesc_db, kk > 0 ? 1u : 0u);
-        }
-      }
-      mma_commit(cfull);
-    }
-  } else {
-    // ---------------------------------------------------------------- mask / reduce warps 2..5
-    const int q = warp & 3;
-    const int t = q * 32 + lane;             // TMEM lane = G row inside the tile
-    const int gm_row = m0 + t;
-    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    // The row's keep bits (M = W != 0, or the packed mask) for all 256 columns of
-    // the tile, gathered while the mainloop runs: the masking after it then only
-    // touches TMEM and shared memory.
-    uint32_t keep[BN / 32];
-#pragma unroll
-    for (int j = 0; j < BN / 32; ++j) {
-      uint32_t keepw = 0;   // keep bits for columns 32 j .. 32 j + 31
-      const int gc = c0 + 32 * j;
-      if (gm_row < R) {
-        if (BITS) {
-          if (gc < C) {
-            keepw = __ldg(bits + (int64_t)gm_row * words_per_row + (gc >> 5));
-            if (gc + 32 > C) keepw &= (1u << (C - gc)) - 1u;
-          }
-        } else {
-          const bf16* wr = w + (int64_t)gm_row * C + gc;
-#pragma unroll
-          for (int u = 0; u < 32; u += 8) {
-            if (gc + u + 8 <= C) {
-              const uint4 raw = __ldg(reinterpret_cast<const uint4*>(wr + u));
-              const uint32_t ww[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const uint32_t nz = nonzero_mask_bf16x2(ww[e]);
-                keepw |= ((nz & 1u) | ((nz >> 15) & 2u)) << (u + 2 * e);
-              }
-            }
-          }
-        }
-      }
-      keep[j] = keepw;
-    }
-    mbar_wait(gfull, 0);
-    tc_fence_after();
-    const uint32_t gmb = smem_u32(sGM);
-#pragma unroll
-    for (int cb = 0; cb < BN; cb += 32) {
-      uint32_t v[32];
-      tmem_ld_x32(tmem + lane_addr + G_COL + cb, v);
-      tmem_ld_wait();
-      const uint32_t keepw = keep[cb / 32];
-      uint32_t pk[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const float g0 = ((keepw >> (2 * e)) & 1u) ? __uint_as_float(v[2 * e]) : 0.0f;
-        const float g1 = ((keepw >> (2 * e + 1)) & 1u) ? __uint_as_float(v[2 * e + 1]) : 0.0f;
-        pk[e] = pack_bf16x2(g0, g1);
-      }
-      // K-major SW128 atom cb/64 [128 rows][64 cols]: row t, chunks (cb%64)/8 .. +3
-      const uint32_t atom = gmb + (cb >> 6) * 16384 + t * 128;
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        const uint32_t chunk = ((((cb & 63) >> 3) + cc) ^ (t & 7)) << 4;
-        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(atom + chunk), "r"(pk[4 * cc]),
-                     "r"(pk[4 * cc + 1]), "r"(pk[4 * cc + 2]), "r"(pk[4 * cc + 3])
-                     : "memory");
-      }
-    }
-    fence_proxy_async_smem();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(gmready);
-    // reduce the partials: alpha-scaled fp32 tiles staged in the drained pipeline's shared
-    // memory, added into dA / dB with TMA bulk reduce-adds (full-line L2 reductions):
-    //   dA  [128 R rows][RP]: SW128 boxes of [128 rows][32 floats], row t at lane t
-    //   dB  [RP rows][128 C] per C half (dB is [r, C]; TMEM lane t = C index): plain rows
-    mbar_wait(cfull, 0);
-    tc_fence_after();
-    {
-      uint8_t* st_da = smem;                     // 16 / 16 / 32 KB
-      uint8_t* st_db = smem + 32768;             // 2 x RP x 512 B
-      uint32_t v[32];
-#pragma unroll
-      for (int half = 0; half * 32 < RP; ++half) {
-        tmem_ld_x32(tmem + lane_addr + DA_COL + half * 32, v);   // (RP 16: 16 spare columns, skipped by the map)
-        tmem_ld_wait();
-        uint8_t* box = st_da + half * 16384 + t * 128;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          *reinterpret_cast<float4*>(box + ((j ^ (t & 7)) << 4)) =
-              make_float4(alpha * __uint_as_float(v[4 * j]), alpha * __uint_as_float(v[4 * j + 1]),
-                          alpha * __uint_as_float(v[4 * j + 2]), alpha * __uint_as_float(v[4 * j + 3]));
-      }
-#pragma unroll
-      for (int hc = 0; hc < 2; ++hc) {
-        float* rows = reinterpret_cast<float*>(st_db + hc * RP * 512);
-#pragma unroll
-        for (int half = 0; half * 32 < RP; ++half) {
-          tmem_ld_x32(tmem + lane_addr + DB_COL + hc * 64 + half * 32, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (half * 32 + j < RP) rows[(half * 32 + j) * 128 + t] = alpha * __uint_as_float(v[j]);
-        }
-      }
-      fence_proxy_async_smem();
-      named_bar_sync(1, 128);
-      if (warp == 2 && lane == 0) {
-        for (int half = 0; half * 32 < RP; ++half) tma_reduce_add_2d(&tmDAo, st_da + half * 16384, 32 * half, m0);
-        for (int hc = 0; hc < 2; ++hc) tma_reduce_add_2d(&tmDBo, st_db + hc * RP * 512, c0 + 128 * hc, 0);
-        tma_store_commit();
-        tma_store_wait_done();
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc<512>(tmem);
-}
-
-template <int RP>
-static int launch_masked_grad(const bf16* dy, const bf16* x, const bf16* w, const uint32_t* bits, const bf16* a,
-                              const bf16* b, float* da, float* db, int L, int R, int C, int r, float alpha,
-                              cudaStream_t s) {
-  using namespace mg;
-  CUtensorMap tDY, tX, tB, tA;
-  int st;
-  if ((st = make_map(&tDY, dy, R, L, 64, 64, 128, "dY (MN)"))) return st;
-  if ((st = make_map(&tX, x, C, L, 64, 64, 128, "X (MN)"))) return st;
-  if ((st = make_map(&tB, b, C, r, 64, RP, 128, "b tile (K-major, K = C)"))) return st;
-  if ((st = make_map(&tA, a, r, R, RP, 128, RP * 2, "a tile (MN-major)"))) return st;
-  CUtensorMap tDAo, tDBo;   // fp32 outputs, reduce-added per tile
-  if ((st = make_map(&tDAo, da, r, R, 32, 128, 128, "dA fp32 (masked-G)", true))) return st;
-  if ((st = make_map(&tDBo, db, C, r, 128, RP, 0, "dB fp32 (masked-G)", true))) return st;
-  LORS_CUDA_TRY(cudaMemsetAsync(da, 0, sizeof(float) * (size_t)R * r, s), "zero dA");
-  LORS_CUDA_TRY(cudaMemsetAsync(db, 0, sizeof(float) * (size_t)r * C, s), "zero dB");
-  auto kern = bits ? tc_masked_grad_kernel<RP, true> : tc_masked_grad_kernel<RP, false>;
-  const size_t smem = smem_bytes<RP>();
-  LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                "masked_grad smem attribute");
-  dim3 grid((unsigned)ceil_div(C, BN), (unsigned)ceil_div(R, BM));
-  kern<<<grid, THREADS, smem, s>>>(tDY, tX, tB, tA, tDAo, tDBo, w, bits, (int)ceil_div(C, 32), L, R, C, r, alpha);
-  LORS_CHECK_LAUNCH("tc_masked_grad");
-  return LORS_OK;
-}
-
-// ===========================================================================
-// K5 on CTA pairs: the masked-G adapter gradient with the G mainloop as
+// adapters.py:303-312): G = (dY^T X) . M is accumulated in TMEM, masked in
+// registers and contracted in place -- G never reaches HBM.  On CTA pairs, the G mainloop as
 // tcgen05 cta_group::2 MMAs (M = 256 rows of R over the pair, each CTA staging
 // its 128 dY columns and half of the 256 X columns: 32 KB per SM per k-step
 // instead of 48), and the two small contractions as warp-level mma.sync on
@@ -2112,7 +1885,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(mgp::THREADS, 1)
                                const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmA,
                                const __grid_constant__ CUtensorMap tmDAo, const __grid_constant__ CUtensorMap tmDBo,
                                const bf16* __restrict__ w, const uint32_t* __restrict__ bits, int words_per_row,
-                               int L, int R, int C, float alpha) {
+                               int L, int R, int C, float alpha, int det, int r_pad) {
   using namespace mgp;
   constexpr uint32_t BT = bt_bytes<RP>(), AT = at_bytes<RP>();
   constexpr uint32_t SWA = RP * 2;              // a tile swizzle span (bytes)
@@ -2362,8 +2135,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(mgp::THREADS, 1)
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
     if (ew == 0 && lane == 0) {
-      for (int hf = 0; hf * 32 < RP; ++hf) tma_reduce_add_2d(&tmDAo, smem + DA_OFF + hf * 16384, 32 * hf, m0);
-      for (int hc = 0; hc < 2; ++hc) tma_reduce_add_2d(&tmDBo, smem + DB_OFF + hc * RP * 512, c0 + 128 * hc, 0);
+      if (det) {
+        // deterministic: this CTA's partials to their own slabs (dA: slab of the C tile,
+        // dB: slab of the 128-row R tile), summed in slab order by slab_sum_kernel
+        const int da_row = (int)blockIdx.y * r_pad + m0, db_row = ((int)blockIdx.z * 2 + (int)rank) * RP;
+        for (int hf = 0; hf * 32 < RP; ++hf) tma_store_2d(&tmDAo, smem + DA_OFF + hf * 16384, 32 * hf, da_row);
+        for (int hc = 0; hc < 2; ++hc) tma_store_2d(&tmDBo, smem + DB_OFF + hc * RP * 512, c0 + 128 * hc, db_row);
+      } else {
+        for (int hf = 0; hf * 32 < RP; ++hf) tma_reduce_add_2d(&tmDAo, smem + DA_OFF + hf * 16384, 32 * hf, m0);
+        for (int hc = 0; hc < 2; ++hc) tma_reduce_add_2d(&tmDBo, smem + DB_OFF + hc * RP * 512, c0 + 128 * hc, 0);
+      }
       tma_store_commit();
       tma_store_wait_done();
     }
@@ -2374,10 +2155,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(mgp::THREADS, 1)
   if (warp == 1) tmem_dealloc_pair<256>(tmem);
 }
 
+// out[i] = sum over s in order of part[s * slab + i]  (deterministic slab reduction)
+__global__ void slab_sum_kernel(const float* __restrict__ part, int n_slabs, int64_t slab, float* __restrict__ out,
+                                int64_t n_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_out) return;
+  float acc = 0.f;
+  for (int k = 0; k < n_slabs; ++k) acc += part[k * slab + i];
+  out[i] = acc;
+}
+
+// deterministic masked-G partial slabs: dA [C tiles][R padded to 256][r], dB [128-row R tiles][RP][C]
+static size_t masked_grad_det_bytes(int R, int C, int rp) {
+  const size_t r_pad = (size_t)ceil_div(R, 256) * 256;
+  return (size_t)ceil_div(C, 256) * r_pad * rp * sizeof(float) + 256 +
+         (size_t)ceil_div(R, 256) * 2 * rp * (size_t)C * sizeof(float);
+}
+
 template <int RP>
 static int launch_masked_grad_pair(const bf16* dy, const bf16* x, const bf16* w, const uint32_t* bits, const bf16* a,
                                    const bf16* b, float* da, float* db, int L, int R, int C, int r, float alpha,
-                                   cudaStream_t s) {
+                                   cudaStream_t s, float* det_ws = nullptr) {
   using namespace mgp;
   CUtensorMap tDY, tX, tB, tA, tDAo, tDBo;
   int st;
@@ -2385,35 +2183,44 @@ static int launch_masked_grad_pair(const bf16* dy, const bf16* x, const bf16* w,
   if ((st = make_map(&tX, x, C, L, 64, 64, 128, "X (MN)"))) return st;
   if ((st = make_map(&tB, b, C, r, 64, RP, 128, "b tile (K-major, K = C)"))) return st;
   if ((st = make_map(&tA, a, r, R, RP, 128, RP * 2, "a tile"))) return st;
-  if ((st = make_map(&tDAo, da, r, R, 32, 128, 128, "dA fp32 (masked-G)", true))) return st;
-  if ((st = make_map(&tDBo, db, C, r, 128, RP, 0, "dB fp32 (masked-G)", true))) return st;
-  LORS_CUDA_TRY(cudaMemsetAsync(da, 0, sizeof(float) * (size_t)R * r, s), "zero dA");
-  LORS_CUDA_TRY(cudaMemsetAsync(db, 0, sizeof(float) * (size_t)r * C, s), "zero dB");
+  const int n_ct = (int)ceil_div(C, 256), n_rt2 = (int)ceil_div(R, 256) * 2, r_pad = (int)ceil_div(R, 256) * 256;
+  float* da_part = det_ws;
+  float* db_part = det_ws ? (float*)((char*)det_ws + ((size_t)n_ct * r_pad * r * sizeof(float) + 255) / 256 * 256)
+                          : nullptr;
+  if (det_ws) {
+    if ((st = make_map(&tDAo, da_part, r, (uint64_t)n_ct * r_pad, 32, 128, 128, "dA partial slabs", true))) return st;
+    if ((st = make_map(&tDBo, db_part, C, (uint64_t)n_rt2 * RP, 128, RP, 0, "dB partial slabs", true))) return st;
+  } else {
+    if ((st = make_map(&tDAo, da, r, R, 32, 128, 128, "dA fp32 (masked-G)", true))) return st;
+    if ((st = make_map(&tDBo, db, C, r, 128, RP, 0, "dB fp32 (masked-G)", true))) return st;
+    LORS_CUDA_TRY(cudaMemsetAsync(da, 0, sizeof(float) * (size_t)R * r, s), "zero dA");
+    LORS_CUDA_TRY(cudaMemsetAsync(db, 0, sizeof(float) * (size_t)r * C, s), "zero dB");
+  }
   auto kern = bits ? tc_masked_grad_pair_kernel<RP, true> : tc_masked_grad_pair_kernel<RP, false>;
   const size_t smem = smem_bytes<RP>();
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "masked_grad_pair smem attribute");
-  dim3 grid(2, (unsigned)ceil_div(C, 256), (unsigned)ceil_div(R, 256));
-  kern<<<grid, THREADS, smem, s>>>(tDY, tX, tB, tA, tDAo, tDBo, w, bits, (int)ceil_div(C, 32), L, R, C, alpha);
+  dim3 grid(2, (unsigned)n_ct, (unsigned)ceil_div(R, 256));
+  kern<<<grid, THREADS, smem, s>>>(tDY, tX, tB, tA, tDAo, tDBo, w, bits, (int)ceil_div(C, 32), L, R, C, alpha,
+                                   det_ws ? 1 : 0, r_pad);
   LORS_CHECK_LAUNCH("tc_masked_grad_pair");
+  if (det_ws) {
+    const int64_t na = (int64_t)R * r, nb = (int64_t)r * C;
+    slab_sum_kernel<<<(unsigned)ceil_div(na, 256), 256, 0, s>>>(da_part, n_ct, (int64_t)r_pad * r, da, na);
+    LORS_CHECK_LAUNCH("slab_sum dA");
+    slab_sum_kernel<<<(unsigned)ceil_div(nb, 256), 256, 0, s>>>(db_part, n_rt2, (int64_t)RP * C, db, nb);
+    LORS_CHECK_LAUNCH("slab_sum dB");
+  }
   return LORS_OK;
 }
 
 static int masked_grad_tc(int rp, const bf16* dy, const bf16* x, const bf16* w, const uint32_t* bits, const bf16* a,
                           const bf16* b, float* da, float* db, int L, int R, int C, int r, float alpha,
-                          cudaStream_t s) {
-  static const bool single = getenv("LORS_K5_SINGLE") != nullptr;   // the one-CTA kernel, for A/B runs
-  if (!single) {
-    switch (rp) {
-      case 16: return launch_masked_grad_pair<16>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s);
-      case 32: return launch_masked_grad_pair<32>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s);
-      default: return launch_masked_grad_pair<64>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s);
-    }
-  }
+                          cudaStream_t s, float* det_ws) {
   switch (rp) {
-    case 16: return launch_masked_grad<16>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s);
-    case 32: return launch_masked_grad<32>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s);
-    default: return launch_masked_grad<64>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s);
+    case 16: return launch_masked_grad_pair<16>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s, det_ws);
+    case 32: return launch_masked_grad_pair<32>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s, det_ws);
+    default: return launch_masked_grad_pair<64>(dy, x, w, bits, a, b, da, db, L, R, C, r, alpha, s, det_ws);
   }
 }
 
@@ -2435,11 +2242,32 @@ static size_t dx_workspace(const lors_bwd_args* a) {
     return 0;
   return lors_gemm_workspace<true>((int)pad_rank(a->r), (int)a->L, (int)a->R, (int)a->C);
 }
+static size_t rank_slot(const lors_bwd_args* a) {
+  return ((size_t)a->L * (size_t)a->r * sizeof(float) + 255) / 256 * 256;
+}
+// the region after the capi's two bf16 P / Q slots: P / Q's fp32 split-K accumulators, or
+// (LORS_FLAG_DETERMINISTIC) the partial slabs of the ordered reductions
+static size_t rank_r_region(const lors_bwd_args* a) {
+  const size_t slot = rank_slot(a);
+  if (!(a->flags & LORS_FLAG_DETERMINISTIC) || a->dtype != LORS_DTYPE_BF16 || a->L <= 0 ||
+      !tc_shape_ok(a->R, a->C, a->r))
+    return 2 * slot;
+  const int L = (int)a->L, R = (int)a->R, C = (int)a->C, rp = (int)pad_rank((int)a->r);
+  size_t need = 0;
+  if (a->grad_mode == LORS_GRAD_MASKED) {
+    need = masked_grad_det_bytes(R, C, rp);
+  } else {
+    for (size_t v : {skinny_partial_bytes(L, C, rp), skinny_partial_bytes(L, R, rp), skinny_partial_bytes(R, L, rp),
+                     skinny_partial_bytes(C, L, rp)})
+      need = std::max(need, v);
+  }
+  return (need + 255) / 256 * 256;
+}
 // DX_ONLY: the dX GEMM's tail split alone; otherwise, beyond the capi's two bf16
-// P / Q slots: their fp32 split-K accumulators, then the dX tail split
+// P / Q slots: the rank-r region, then the dX tail split
 size_t tc_bwd_workspace(const lors_bwd_args* a) {
   if (a->flags & LORS_FLAG_DX_ONLY) return dx_workspace(a);
-  return 2 * (((size_t)a->L * (size_t)a->r * sizeof(float) + 255) / 256 * 256) + dx_workspace(a);
+  return rank_r_region(a) + dx_workspace(a);
 }
 
 int tc_fwd(const lors_fwd_args* A, cudaStream_t s) {
@@ -2478,11 +2306,12 @@ int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {
   const bf16 *x = (const bf16*)A->x, *w = (const bf16*)A->w, *a = (const bf16*)A->a, *b = (const bf16*)A->b,
              *dy = (const bf16*)A->dy;
   const bool tc = tc_shape_ok(R, C, r);
+  const bool det = (A->flags & LORS_FLAG_DETERMINISTIC) != 0;
   const int rp = (int)pad_rank(r);
   int st;
   if (!(A->flags & LORS_FLAG_NO_DX)) {
-    // the dX tail split's workspace: all of it (DX_ONLY) or after the four rank-r slots
-    const size_t off = (A->flags & LORS_FLAG_DX_ONLY) ? 0 : 4 * (((size_t)L * r * sizeof(float) + 255) / 256 * 256);
+    // the dX tail split's workspace: all of it (DX_ONLY) or after the P / Q slots and the rank-r region
+    const size_t off = (A->flags & LORS_FLAG_DX_ONLY) ? 0 : 2 * rank_slot(A) + rank_r_region(A);
     const size_t dxw = dx_workspace(A);
     void* ws = dxw && A->workspace && A->workspace_bytes >= off + dxw ? (char*)A->workspace + off : nullptr;
     st = tc ? lors_gemm<true>(rp, dy, w, a, b, nullptr, bits, (bf16*)A->dx, L, R, C, r, A->alpha, s, ws, dxw)
@@ -2494,7 +2323,20 @@ int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {
     const size_t slot = ((size_t)L * r * sizeof(float) + 255) / 256 * 256;
     bf16* P = (bf16*)A->p;
     bf16* Q = (bf16*)((char*)A->workspace + slot);
-    if (tc) {
+    if (tc && det) {
+      // deterministic: every split-K product writes per-split partials that one kernel
+      // sums in split order (P / Q rounded to bf16 there); adapters.py:396-399 order
+      float* part = (float*)((char*)A->workspace + 2 * slot);
+      if (P == nullptr) {  // P = X_t b^T
+        P = (bf16*)A->workspace;
+        if ((st = skinny<false, false, 0>(rp, x, b, P, L, r, C, r, 1.0f, true, s, nullptr, false, part))) return st;
+      }
+      if ((st = skinny<false, true, 0>(rp, dy, a, Q, L, r, R, r, 1.0f, true, s, nullptr, false, part))) return st;
+      if ((st = skinny<true, true, 1>(rp, dy, P, A->da, R, r, L, r, A->alpha, true, s, nullptr, false, part)))
+        return st;
+      if ((st = skinny<true, true, 2>(rp, x, Q, A->db, C, r, L, C, A->alpha, true, s, nullptr, false, part)))
+        return st;
+    } else if (tc) {
       // P = X_t b^T and Q = dY_t a are split over their reductions (C, R) into fp32
       // accumulators so that L / 128 token tiles still fill the SMs, then rounded to bf16
       float* P32 = (float*)((char*)A->workspace + 2 * slot);
@@ -2552,7 +2394,8 @@ int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {
       if (st) return st;
     }
   } else {
-    st = tc ? masked_grad_tc(rp, dy, x, w, bits, a, b, A->da, A->db, L, R, C, r, A->alpha, s)
+    float* det_ws = det ? (float*)((char*)A->workspace + 2 * rank_slot(A)) : nullptr;
+    st = tc ? masked_grad_tc(rp, dy, x, w, bits, a, b, A->da, A->db, L, R, C, r, A->alpha, s, det_ws)
             : simt_masked_grad<bf16>(dy, x, w, bits, a, b, A->da, A->db, L, R, C, r, A->alpha, s);
     if (st) return st;
   }

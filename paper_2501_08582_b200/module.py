@@ -185,7 +185,8 @@ class LoRSGroupFunction(torch.autograd.Function):
                 keep.append(ws)
             _, da, db, dbias, ws = ops._lors_bwd_call(x2, weights[i], ab[i][0], ab[i][1], dys[i], prm.alpha, None,
                                                       prm.mask_bits, prm.grad_mode, False, has_bias[i],
-                                                      prm.fault_da_sign, launch_stream=sides[i % len(sides)])
+                                                      prm.fault_da_sign, launch_stream=sides[i % len(sides)],
+                                                      deterministic=ops.deterministic_default())
             res.append((da, db, dbias))
             keep.append(ws)
         for st in (streams if need_dx else []) + sides:

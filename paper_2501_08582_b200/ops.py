@@ -142,11 +142,20 @@ def _side_stream(dev: torch.device):
     return s
 
 
+def deterministic_default() -> bool:
+    """Default of lors_bwd's `deterministic` (LORS_DETERMINISTIC=1 turns it on process-wide)."""
+    return os.environ.get("LORS_DETERMINISTIC", "0") == "1"
+
+
 def lors_bwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tensor, dy_t: torch.Tensor,
              alpha: float = 2.0, p: Optional[torch.Tensor] = None, mask_bits: Optional[torch.Tensor] = None,
              grad_mode: str = "ste", need_dx: bool = True, with_bias: bool = False,
-             fault_da_sign: bool = False, overlap: Optional[bool] = None):
+             fault_da_sign: bool = False, overlap: Optional[bool] = None, deterministic: Optional[bool] = None):
     """(dX_t [L, C] | None, dA [R, r] fp32, dB [r, C] fp32, dbias [R] fp32 | None).
+
+    deterministic=True (LORS_FLAG_DETERMINISTIC): the adapter gradients' split-K
+    partials are summed in a fixed order instead of by atomics / TMA reduce-adds,
+    so dA and dB are bitwise reproducible run to run (default: LORS_DETERMINISTIC).
 
     overlap=True (bf16 tensor-core shapes): the dX GEMM is enqueued on the
     current stream and the rank-r products (P, Q, dA, dB) on a side stream, two
@@ -155,6 +164,8 @@ def lors_bwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
     round.  The current stream waits for both before returning."""
     if overlap is None:
         overlap = os.environ.get("LORS_BWD_OVERLAP", "1") != "0"
+    if deterministic is None:
+        deterministic = deterministic_default()
     R_, C_ = w.shape
     r_ = a.shape[1] if a.dim() == 2 else 0
     if (overlap and need_dx and w.is_cuda and w.dtype == torch.bfloat16 and R_ % 8 == 0 and C_ % 8 == 0
@@ -173,18 +184,18 @@ def lors_bwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
         # of these blocks is ordered after the side work: no record_stream (whose
         # deferred frees made the caching allocator grow with cudaMalloc stalls).
         _, da, db, dbias, ws = _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, False, with_bias,
-                                              fault_da_sign, launch_stream=side)
+                                              fault_da_sign, launch_stream=side, deterministic=deterministic)
         join_hi.record(hi)
         join.record(side)
         main.wait_event(join_hi)
         main.wait_event(join)
         return dx, da, db, dbias
     return _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, with_bias,
-                          fault_da_sign)[:4]
+                          fault_da_sign, deterministic=deterministic)[:4]
 
 
 def _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, with_bias, fault_da_sign,
-                   dx_only: bool = False, launch_stream=None):
+                   dx_only: bool = False, launch_stream=None, deterministic: bool = False):
     """One lors_bwd C-ABI call: outputs and workspace allocated on the current
     stream, the kernels launched on `launch_stream` (default: the current stream).
     Returns (dx, da, db, dbias, workspace)."""
@@ -217,7 +228,8 @@ def _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, 
     args.mask_mode = N.MASK_BITS if mask_bits is not None else N.MASK_FROM_W
     args.grad_mode = N.GRAD_STE if grad_mode == "ste" else N.GRAD_MASKED
     args.flags = ((0 if need_dx else N.FLAG_NO_DX) | (N.FLAG_DX_ONLY if dx_only else 0)
-                  | (N.FLAG_FAULT_DA_SIGN if fault_da_sign and not dx_only else 0))
+                  | (N.FLAG_FAULT_DA_SIGN if fault_da_sign and not dx_only else 0)
+                  | (N.FLAG_DETERMINISTIC if deterministic and not dx_only else 0))
     args.alpha = float(alpha)
     args.x, args.w, args.mask_bits, args.a, args.b = _p(x_t), _p(w), _p(mask_bits), _p(a), _p(b)
     lib = N.load()
