@@ -201,6 +201,7 @@ def lors_forward(layer: AdaptedLayer, x: torch.Tensor, counters=None):
     x_t = _as_rows(x.to(dt))
     bias = None if layer.bias is None else layer.bias.detach().reshape(-1).to(dt).contiguous()
     y_t, _ = ops.lors_fwd(x_t, layer.base.values, a, b, layer.adapter.alpha, bias)
+    ops.require_finite("lors_forward output", y_t)      # the reference's NumericError (matrix.py:53-54)
     if counters is not None:
         counters.add_forward(layer, x_t.shape[0])
     return y_t.t(), _Context(layer, x=x_t)
@@ -217,6 +218,7 @@ def _backward(grad_y: torch.Tensor, ctx: _Context, grad_mode: str, counters=None
                                      grad_mode=grad_mode, with_bias=layer.bias is not None,
                                      fault_da_sign=(grad_mode == "ste"
                                                     and FAULT_INJECTION["lors_backward_sign_flip"]))
+    ops.require_finite("lors_backward gradients", dx, da, db, dbias)
     if counters is not None:
         counters.add_backward(layer, x_t.shape[0])
     return VariantGrads(da=da, db=db, dx=dx.t(), dbias=None if dbias is None else dbias.reshape(-1, 1))

@@ -54,6 +54,7 @@ class AdapterGradReducer:
                      for b in self.buckets]
         self._pending = []
         self._ready = [0] * len(self.buckets)
+        self._stale = set()   # buckets launched, then accumulated into again (gradient accumulation)
         self._hooks = []
         if overlap:
             where = {}
@@ -67,8 +68,13 @@ class AdapterGradReducer:
     # -- overlap path -------------------------------------------------------
     def _grad_ready(self, bi: int) -> None:
         self._ready[bi] += 1
-        if self._ready[bi] == len(self.buckets[bi]):
+        n = len(self.buckets[bi])
+        if self._ready[bi] == n:
             self._launch(bi, async_op=True)
+        elif self._ready[bi] > n:
+            # a further backward (gradient accumulation) added to grads this bucket already
+            # sent: its reduction is redone from the accumulated .grad in finish()
+            self._stale.add(bi)
 
     def _launch(self, bi: int, async_op: bool):
         bucket, flat = self.buckets[bi], self.flat[bi]
@@ -107,10 +113,11 @@ class AdapterGradReducer:
         for bi, work in self._pending:
             work.wait()
         for bi in range(len(self.buckets)):
-            if bi not in launched:
+            if bi not in launched or bi in self._stale:
                 self._launch(bi, async_op=False)
             self._scatter_back(bi)
         self._pending.clear()
+        self._stale.clear()
         self._ready = [0] * len(self.buckets)
 
     __call__ = finish

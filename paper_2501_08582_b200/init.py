@@ -89,8 +89,10 @@ def init_gradient_svd(layers: Iterable[nn.Module], probe: Callable[[], None], ma
             m.a.zero_()  # initialization.py:196
     for m in layers:
         hooks.append(m.register_forward_hook(fwd_hook))
+    from .module import no_grouping
     try:
-        probe()
+        with no_grouping():    # grouped q/k/v and gate/up nodes would bypass the per-layer hooks
+            probe()
     finally:
         for h in hooks:
             h.remove()

@@ -12,6 +12,7 @@ adapters.py:372).
 
 from __future__ import annotations
 
+import contextlib
 import math
 import os
 from dataclasses import dataclass
@@ -33,6 +34,7 @@ class LoRSParams:
     fault_da_sign: bool = False   # negative control (adapters.py:57-60)
     sparse24: bool = False        # forward on 2:4 sparse tensor cores (north_star 4)
     meta24: Optional[torch.Tensor] = None  # kept-position metadata of the frozen 2:4 weight
+    check_finite: bool = False    # raise NumericError on NaN / inf outputs (one host sync per call)
 
 
 def compute_copy(t: torch.Tensor, dt: torch.dtype) -> torch.Tensor:
@@ -66,17 +68,20 @@ class LoRSFunction(torch.autograd.Function):
         bias_c = None if bias is None else bias.detach().to(dt).contiguous()
         y, p = ops.lors_fwd(x2, weight, a, b, params.alpha, bias_c, params.mask_bits, emit_p=params.save_p,
                             sparse24=params.sparse24, meta24=params.meta24 if params.sparse24 else None)
+        if params.check_finite:
+            ops.require_finite("LoRS forward output", y)
         if params.save_p:
             ctx.save_for_backward(x2, p)
         else:
             ctx.save_for_backward(x2)
         # adapter read at backward time (reference b2, adapters.py:387-394)
-        ctx.lors = (weight, lora_A, lora_B, bias is not None, params, shape, x.dtype)
+        ctx.lors = (weight, lora_A, lora_B, None if bias is None else bias.dtype, params, shape, x.dtype)
         return y.view(*shape[:-1], out_f)
 
     @staticmethod
     def backward(ctx, grad_y):
-        weight, lora_A, lora_B, has_bias, params, x_shape, x_dtype = ctx.lors
+        weight, lora_A, lora_B, bias_dtype, params, x_shape, x_dtype = ctx.lors
+        has_bias = bias_dtype is not None
         saved = ctx.saved_tensors
         x2 = saved[0]
         p = saved[1] if len(saved) > 1 else None
@@ -95,8 +100,10 @@ class LoRSFunction(torch.autograd.Function):
         dx, da, db, dbias = ops.lors_bwd(x2, weight, a, b, dy, params.alpha, p=p, mask_bits=params.mask_bits,
                                          grad_mode=params.grad_mode, need_dx=need_dx, with_bias=has_bias,
                                          fault_da_sign=params.fault_da_sign)
+        if params.check_finite:
+            ops.require_finite("LoRS backward gradients", dx, da, db, dbias)
         grad_x = dx.view(x_shape).to(x_dtype) if need_dx else None
-        grad_bias = dbias.to(dt) if has_bias and ctx.needs_input_grad[2] else None
+        grad_bias = dbias.to(bias_dtype) if has_bias and ctx.needs_input_grad[2] else None
         grad_a = da.to(lora_A.dtype) if ctx.needs_input_grad[3] else None
         grad_b = db.to(lora_B.dtype) if ctx.needs_input_grad[4] else None
         return grad_x, None, grad_bias, grad_a, grad_b, None
@@ -148,12 +155,16 @@ class LoRSGroupFunction(torch.autograd.Function):
         # keep / ab / bc were allocated on the main stream and are released after the
         # joins are enqueued there, so no later main-stream reuse can overtake the GEMMs
         ctx.save_for_backward(x2)
-        ctx.lors = (weights, As, Bs, tuple(b is not None for b in biases), params_list, shape, x.dtype)
+        if any(prm.check_finite for prm in params_list):
+            ops.require_finite("LoRS forward outputs", *outs)
+        ctx.lors = (weights, As, Bs, tuple(None if b is None else b.dtype for b in biases), params_list, shape,
+                    x.dtype)
         return tuple(outs)
 
     @staticmethod
     def backward(ctx, *grads):
-        weights, As, Bs, has_bias, params_list, x_shape, x_dtype = ctx.lors
+        weights, As, Bs, bias_dtypes, params_list, x_shape, x_dtype = ctx.lors
+        has_bias = tuple(d is not None for d in bias_dtypes)
         (x2,) = ctx.saved_tensors
         n = len(params_list)
         dt = weights[0].dtype
@@ -199,22 +210,39 @@ class LoRSGroupFunction(torch.autograd.Function):
             for d in dxs[1:]:
                 dx.add_(d)
             grad_x = dx.view(x_shape).to(x_dtype)
+        if any(prm.check_finite for prm in params_list):
+            ops.require_finite("LoRS backward gradients", grad_x, *[t for r3 in res for t in r3])
         out = [grad_x, None]
         for i in range(n):
             da, db, dbias = res[i]
             k = 2 + 4 * i
             out += [None,
-                    dbias.to(dt) if has_bias[i] and ctx.needs_input_grad[k + 1] else None,
+                    dbias.to(bias_dtypes[i]) if has_bias[i] and ctx.needs_input_grad[k + 1] else None,
                     da.to(As[i].dtype) if ctx.needs_input_grad[k + 2] else None,
                     db.to(Bs[i].dtype) if ctx.needs_input_grad[k + 3] else None]
         return tuple(out)
+
+
+_GROUPING = [True]
+
+
+@contextlib.contextmanager
+def no_grouping():
+    """Run every projection as its own LoRSLinear call (init_gradient_svd's probe needs each
+    layer's forward hook to fire)."""
+    prev = _GROUPING[0]
+    _GROUPING[0] = False
+    try:
+        yield
+    finally:
+        _GROUPING[0] = prev
 
 
 def groupable(layers) -> bool:
     """Whether `layers` can run as one LoRSGroupFunction node: LoRSLinear projections
     of the same input on a CUDA device in bf16 (the tensor-core path), without the
     options that change the saved set (save_p)."""
-    if len(layers) < 2 or os.environ.get("LORS_GROUP", "1") == "0":
+    if len(layers) < 2 or not _GROUPING[0] or os.environ.get("LORS_GROUP", "1") == "0":
         return False
     w0 = getattr(layers[0], "weight", None)
     return all(isinstance(m, LoRSLinear) and m.weight.is_cuda and m.weight.dtype == torch.bfloat16
@@ -244,7 +272,7 @@ class LoRSLinear(nn.Module):
     def __init__(self, weight: torch.Tensor, rank: Optional[int] = None, a: Optional[torch.Tensor] = None,
                  b: Optional[torch.Tensor] = None, alpha: float = 2.0, bias: Optional[torch.Tensor] = None,
                  name: str = "", grad_mode: str = "ste", mask_mode: str = "from_w", save_p: bool = False,
-                 param_dtype: torch.dtype = torch.float32, sparse24: bool = False):
+                 param_dtype: torch.dtype = torch.float32, sparse24: bool = False, check_finite: bool = False):
         super().__init__()
         if weight.dim() != 2:
             raise ShapeError("weight must be 2-D [out, in]")
@@ -294,6 +322,7 @@ class LoRSLinear(nn.Module):
         self.grad_mode = grad_mode
         self.save_p = save_p
         self.fault_da_sign = False
+        self.check_finite = check_finite   # NumericError on NaN / inf (matrix.py:53-54), one host sync per call
 
     @property
     def in_features(self) -> int:
@@ -310,7 +339,7 @@ class LoRSLinear(nn.Module):
     def params(self) -> LoRSParams:
         return LoRSParams(alpha=self.alpha, grad_mode=self.grad_mode, mask_bits=self.mask,
                           save_p=self.save_p, fault_da_sign=self.fault_da_sign, sparse24=self.sparse24,
-                          meta24=self.meta24)
+                          meta24=self.meta24, check_finite=self.check_finite)
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         return LoRSFunction.apply(x, self.weight, self.bias, self.a, self.b, self.params())

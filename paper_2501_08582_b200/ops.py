@@ -15,7 +15,7 @@ from typing import Optional
 import torch
 
 from . import _native as N
-from .errors import ArgumentError, ShapeError
+from .errors import ArgumentError, NumericError, ShapeError
 
 _DTYPES = {torch.float32: N.DTYPE_F32, torch.bfloat16: N.DTYPE_BF16}
 
@@ -58,6 +58,17 @@ def _check_layer(x_t, w, a, b):
     if x_t.shape[1] != C:
         raise ShapeError(f"layer expects {C} input rows, got {x_t.shape[1]}x{x_t.shape[0]}")
     return x_t.shape[0], R, C, a.shape[1]
+
+
+def require_finite(what: str, *tensors: Optional[torch.Tensor]) -> None:
+    """Raise NumericError when any given tensor holds NaN or +-inf -- the reference checks
+    every matrix result (matrix.py:44-45, 53-54).  One device reduction and one host read."""
+    ts = [t for t in tensors if t is not None and t.numel()]
+    if not ts:
+        return
+    ok = torch.stack([torch.isfinite(t).all() for t in ts]).all()
+    if not bool(ok):
+        raise NumericError(f"non-finite values in {what}")
 
 
 def lors_fwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tensor, alpha: float = 2.0,

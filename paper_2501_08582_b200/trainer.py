@@ -95,8 +95,9 @@ class Trainer:
     def __init__(self, model: nn.Module, lr: float = 2e-5, betas=(0.9, 0.999), eps: float = 1e-8,
                  weight_decay: float = 0.0, process_group=None, overlap: bool = True,
                  bucket_bytes: int = 64 << 20, params: Optional[Sequence[nn.Parameter]] = None,
-                 optimizer: str = "auto"):
+                 optimizer: str = "auto", check_finite: bool = False):
         self.model = model
+        self.check_every_step = check_finite   # NumericError on a non-finite loss (train.py:215-217); syncs
         self.params = list(params) if params is not None else [p for p in model.parameters() if p.requires_grad]
         if not self.params:
             raise ArgumentError("model has no trainable adapter parameters")
@@ -124,6 +125,8 @@ class Trainer:
         """One fine-tuning step on this rank's tokens [B, S + 1]; returns the (local) loss
         as a device scalar -- no host synchronisation."""
         loss = self.model.loss(tokens)
+        if self.check_every_step:
+            self.check_finite(loss, self.steps)
         loss.backward()
         if self.reducer is not None:
             self.reducer.finish()

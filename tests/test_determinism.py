@@ -66,13 +66,15 @@ def test_adapter_grads_bitwise_reproducible(ops, R, C, L, r, grad_mode):
 
 
 def test_fast_and_deterministic_modes_agree(ops):
-    """Same sums in another order: the two modes differ only by fp32 rounding."""
+    """Same sums in another order: the two modes differ only by fp32 summation order, which can
+    flip the bf16 rounding of a few intermediate P / Q entries (adapters.py:396-397 products are
+    rounded to the compute dtype before dA / dB): relative differences ~1e-4."""
     w, a, b, x, dy = _inputs(11008, 4096, 8192, 64, seed=7)
     _, da0, db0, _ = ops.lors_bwd(x, w, a, b, dy, 2.0, need_dx=False, deterministic=False)
     _, da1, db1, _ = ops.lors_bwd(x, w, a, b, dy, 2.0, need_dx=False, deterministic=True)
     torch.cuda.synchronize()
     for u, v in ((da0, da1), (db0, db1)):
-        assert float((u - v).norm() / v.norm()) < 1e-5
+        assert float((u - v).norm() / v.norm()) < 1e-3
 
 
 def test_training_replays_bitwise(ops, monkeypatch):
