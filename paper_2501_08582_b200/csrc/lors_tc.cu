@@ -22,10 +22,6 @@
 //        workspace slabs that one kernel sums in a fixed order (no atomics, no TMA
 //        reduce-adds), so dA / dB are bitwise reproducible run to run.
 //
-// Timing-experiment switches (tools/exp_variants.sh, never set in the product
-// build): LORS_EXP_NO_RECOMPUTE / _NO_XFORM / _NO_W_TMA / _NO_ACT_TMA skip one
-// pipeline stage; LORS_EXP_CLOCK / _CLOCK_PRO record an in-kernel timeline.
-//
 // Shapes that the TMA path cannot address (rows not 16-byte multiples, or
 // r > 64) run the FFMA kernels of lors_simt.cu instead.
 #include <cuda.h>
@@ -40,22 +36,6 @@
 #include "lors_tc.cuh"
 #include "ptx_sm100.cuh"
 
-#ifdef LORS_EXP_CLOCK
-// timing experiment: per-CTA (clock64, globaltimer) at start and end of the LoRS GEMM
-__device__ unsigned long long g_lors_clk[4096 * 8];
-__device__ unsigned int g_lors_clk_n;
-extern "C" int lors_exp_clock_read(unsigned long long* out, unsigned int* n) {
-  cudaMemcpyFromSymbol(n, g_lors_clk_n, sizeof(unsigned int));
-  unsigned int z = 0;
-  cudaMemcpyToSymbol(g_lors_clk_n, &z, sizeof(unsigned int));
-  return (int)cudaMemcpyFromSymbol(out, g_lors_clk, sizeof(unsigned long long) * 4096 * 8);
-}
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#endif
 #ifdef LORS_DEBUG_HANG
 extern "C" int lors_debug_hang_info(unsigned int* out) {
   return (int)cudaMemcpyFromSymbol(out, lors::ptx::g_lors_hang, sizeof(unsigned int) * 64);
@@ -865,10 +845,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   const int warp = warp_id(), lane = lane_id();
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
-#ifdef LORS_EXP_CLOCK
-  const unsigned long long clk0 = clock64(), gt0 = gtimer();
-  __shared__ unsigned long long t_ev[4];  // first main MMA issued, accumulator done, staged, stored
-#endif
   // grouped raster over (token tile, feature pair): GROUP_T token tiles x all
   // feature pairs per group, token tile fastest, so the ~74 clusters of a wave
   // read ~9 W panels and <= 8 activation panels and both stay L2-resident.
@@ -949,9 +925,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   __syncthreads();
   tc_fence_after();
   cluster_arrive();
-#ifdef LORS_EXP_CLOCK_PRO
-  if (threadIdx.x == 0) t_ev[0] = gtimer();
-#endif
   const uint32_t tmem = *tmem_slot;
   // Every TMA completes on a barrier of the CTA that issued it; the peer
   // relays its landings to the leader, and the transform warps of both CTAs
@@ -999,9 +972,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         uint8_t* st = wring + wi * W_BYTES;
         const int k0 = i * BK;
         uint64_t* wf = &wfull[(g % NGRP) * NW + wi].b;   // the set of the group that reads step g
-#ifdef LORS_EXP_NO_W_TMA
-        mbar_arrive(wf);
-#else
         mbar_arrive_expect_tx(wf, W_BYTES);
         if (DX) {  // W[k0:k0+64, m0:m0+128] as two SW128 boxes of 64 columns
           tma_load_2d(st, &tmW, wf, m0, k0);
@@ -1009,7 +979,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         } else {   // W[m0:m0+128, k0:k0+64], SW128
           tma_load_2d(st, &tmW, wf, k0, m0);
         }
-#endif
       }
       }
     }
@@ -1024,13 +993,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       for (int i = kb; i < ke; ++i, ++g) {
         const int a = g % NA;
         mbar_wait(&a_empty[a].b, ((g / NA) & 1) ^ 1);
-#ifdef LORS_EXP_NO_ACT_TMA
-        mbar_arrive(&mready[a].b);
-#else
         mbar_arrive_expect_tx(&mready[a].b, ACT_BYTES);
         tma_load_2d(actb + a * ACT_BYTES, &tmAct, &mready[a].b, i * BK, lh);
         if (N2) tma_load_2d(actb + a * ACT_BYTES + ACT1_BYTES, &tmAct2, &mready[a].b, i * BK, lh2);
-#endif
       }
       }
     }
@@ -1095,12 +1060,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         tc_fence_after();
         if (elect_one()) {
           const uint64_t sfd = sf_desc + (uint64_t)(e * (SF >> 4));
-#ifndef LORS_EXP_NO_RECOMPUTE
 #pragma unroll
           for (int kk = 0; kk < RP / 16; ++kk)
             mma_bf16_pair(tmem + RE_COL + e * 64, ff_desc + kk * FF_KSTEP, sfd + kk * SF_KSTEP, idesc_re,
                           kk > 0 ? 1u : 0u);
-#endif
           mma_commit_pair(&refull[(j % NGRP) * NE + e].b, 0x3);
           mma_commit_pair(&e_empty[e].b, 0x3);
           if (PERSIST && rk == rlen - 1) mma_commit_pair(ff_empty, 0x3);   // fixed factor may be replaced
@@ -1160,13 +1123,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       for (int j = 0; j < total + (EX ? 0 : D); ++j) {
         const bool has_rec = j < total, has_main = !EX && j >= D;
         const bool flip = has_rec && rk == 0 && j > 0;
-#if defined(LORS_EXP_CLOCK) && !defined(LORS_EXP_CLOCK_PRO)
-        if (j == D && lane == 0) t_ev[0] = gtimer();
-#endif
-#ifdef LORS_EXP_CLOCK_PRO
-        if (j == D && lane == 0) t_ev[3] = gtimer();
-        if (j == 0 && lane == 0) t_ev[1] = gtimer();
-#endif
         if (flip && has_main) {
           do_main(j - D, mk, mn, mlen);
           if (++mk == mlen) { mk = 0; if (++mn < my_units) mlen = unit_len(mn); }
@@ -1251,12 +1207,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       // waits for the commit of main(i - NA), the previous user of this buffer
       if (!EX && i >= NA) mbar_wait(&wempty[(i % NGRP) * NA + wb].b, ((i - NA) / A_PERIOD) & 1);
       const uint32_t dst = smem_u32(weff + wb * WEFF_BYTES);
-#ifdef LORS_EXP_NO_XFORM
-      constexpr bool XF = false;  // timing experiment: W_eff buffers left as they are
-#else
-      constexpr bool XF = true;
-#endif
-      if (XF && SP && meta24 != nullptr) {
+      if (SP && meta24 != nullptr) {
         // 2:4 with precomputed index nibbles: weff_pair on the group's four
         // values, then one prmt keeps the two positions the nibble names (no
         // on-chip nibble derivation) -- the dense prologue's values, compressed
@@ -1283,7 +1234,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         tmem_st_x1(tmem + lane_addr + E_COL + wb * 8 + h * 4, word);
         tmem_st_wait();
         tc_fence_before();
-      } else if (XF && !DX) {
+      } else if (!DX) {
         // thread = W row; 4 chunks of 8 k-values, same swizzled position in and out
         uint32_t mword = 0;
         uint32_t comp[8], meta = 0;  // 2:4: compressed pairs and index nibbles of this half
@@ -1335,7 +1286,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           tmem_st_wait();
           tc_fence_before();
         }
-      } else if (XF && DX) {
+      } else {
         // ldmatrix.trans handed thread l the pair (k = 32h + 8j + 2(l%4) + {0,1},
         // c = 32q + 16g + 8s + l/4), the positions p[16g + 4j + 2s + {0,1}] hold;
         // results go to the K-major W_eff^T tile (row c) as 32-bit pairs.
@@ -1375,9 +1326,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       }
       fence_proxy_async_smem();
       __syncwarp();
-#ifdef LORS_EXP_CLOCK_PRO
-      if (i == 0 && warp == 0 && lane == 0) t_ev[2] = gtimer();
-#endif
       if (EX) {
         // export: the whole [128 rows][64 k] SW128 tile is the TMA box of W_eff at
         // (k0, m0); the store has read the buffer before anyone rewrites it
@@ -1572,9 +1520,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     // ------------------------------------------------------------ epilogue
     mbar_wait(accf, 0);
     tc_fence_after();
-#if defined(LORS_EXP_CLOCK) && !defined(LORS_EXP_CLOCK_PRO)
-    if (warp == 0 && lane == 0) t_ev[1] = gtimer();
-#endif
     // Per 128-token chunk: the accumulator is read in the MMA fragment layout
     // (tcgen05.ld.16x256b: a thread holds two adjacent tokens of a feature),
     // rounded to bf16 pairs and written transposed by stmatrix.trans into
@@ -1630,9 +1575,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       fence_proxy_async_smem();
       named_bar_sync(1, XFORM_THREADS);
       if (warp == 0 && lane == 0) {
-#if defined(LORS_EXP_CLOCK) && !defined(LORS_EXP_CLOCK_PRO)
-        if (c == 0) t_ev[2] = gtimer();
-#endif
         tma_store_2d(&tmOut, stg + (c * 2) * 16384, m0, l0 + 128 * c);
         tma_store_2d(&tmOut, stg + (c * 2 + 1) * 16384, m0 + 64, l0 + 128 * c);
         tma_store_commit();
@@ -1640,31 +1582,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     }
     if (warp == 0 && lane == 0) {
       tma_store_wait_all();
-#if defined(LORS_EXP_CLOCK) && !defined(LORS_EXP_CLOCK_PRO)
-      t_ev[3] = gtimer();
-#endif
     }
     }
   }
   tc_fence_before();
   cluster_sync();
   if (warp == W_MMA) tmem_dealloc_pair<TMEM_COLS>(tmem);
-#ifdef LORS_EXP_CLOCK
-  if (threadIdx.x == 0) {
-    const unsigned int slot = atomicAdd(&g_lors_clk_n, 1u);
-    if (slot < 4096) {
-      g_lors_clk[slot * 8 + 0] = clk0;
-      g_lors_clk[slot * 8 + 1] = clock64();
-      g_lors_clk[slot * 8 + 2] = gt0;
-      g_lors_clk[slot * 8 + 3] = gtimer();
-#ifdef LORS_EXP_CLOCK_PRO
-      for (int e = 0; e < 4; ++e) g_lors_clk[slot * 8 + 4 + e] = leader ? t_ev[e] : 0ull;
-#else
-      for (int e = 0; e < 4; ++e) g_lors_clk[slot * 8 + 4 + e] = leader || e > 0 ? t_ev[e] : 0ull;
-#endif
-    }
-  }
-#endif
 }
 
 // Co-resident clusters of the persistent kernel (cached per kernel once it is known;
