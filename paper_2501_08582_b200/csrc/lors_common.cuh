@@ -65,14 +65,17 @@ __device__ __forceinline__ bool mask_at(const T w, const uint32_t* __restrict__ 
 }
 
 // The effective-weight element of the FFMA kernels (fp32 mode, K6 fp32, shapes TMA
-// cannot address):  select(M, fma(alpha, p, w), +0.0), rounded once to the storage
-// type by the caller.  The tensor-core path's weff_pair (ptx_sm100.cuh) is the same
-// arithmetic on bf16 pairs; its K6 export runs that prologue itself.
-// `select`, not multiplication, so pruned entries are bit-exact +0.0
-// (reference merged_weight adapters.py:214-224 yields +0.0 there because W
-// is normalised to +0.0, prune.py:47; (w + alpha*p)*0 could give -0.0).
+// cannot address), rounded to the storage type T by the caller:
+//   fp32: select(M, fma(alpha, p, w), +0.0)
+//   bf16: select(M, bf16(w + bf16(alpha p)), +0.0)  -- the tensor-core weff_pair's arithmetic
+// `select`, not multiplication, so pruned entries are bit-exact +0.0 (reference
+// merged_weight adapters.py:214-224 yields +0.0 there because W is normalised to +0.0,
+// prune.py:47; (w + alpha*p)*0 could give -0.0).
+template <typename T>
 __device__ __forceinline__ float weff_value(bool keep, float w, float p, float alpha) {
-  return keep ? fmaf(alpha, p, w) : 0.0f;
+  if (!keep) return 0.0f;
+  if (sizeof(T) == 2) return w + round_to<T>(alpha * p);
+  return fmaf(alpha, p, w);
 }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(NT) simt_lors_gemm_kernel(
         if (gm < M && gk < K) {
           const int64_t row = DX ? gk : gm, col = DX ? gm : gk;
           const T wv = w[row * C + col];
-          v = round_to<T>(weff_value(mask_at(wv, bits, words, row, col), to_f(wv), p[q], alpha));
+          v = round_to<T>(weff_value<T>(mask_at(wv, bits, words, row, col), to_f(wv), p[q], alpha));
         }
         sW[(pk + q) * BM + pm] = v;
       }
@@ -391,7 +391,7 @@ __global__ void effective_weight_kernel(const T* __restrict__ w, const uint32_t*
     const int n = n0 + q;
     if (n >= R) break;
     const T wv = w[(int64_t)n * C + c];
-    out[(int64_t)n * C + c] = from_f<T>(weff_value(mask_at(wv, bits, words, n, c), to_f(wv), p[q], alpha));
+    out[(int64_t)n * C + c] = from_f<T>(weff_value<T>(mask_at(wv, bits, words, n, c), to_f(wv), p[q], alpha));
   }
 }
 

@@ -125,6 +125,13 @@ __global__ void f32_to_bf16_pair_kernel(const float4* __restrict__ a32, __nv_bfl
 }
 
 static inline uint32_t pad_rank(int r) { return r <= 16 ? 16 : r <= 32 ? 32 : 64; }
+// alpha a (normal) power of two: bf16(alpha P) = alpha bf16(P), weff_pair's fused form applies
+static inline bool alpha_pow2(float alpha) {
+  uint32_t u;
+  std::memcpy(&u, &alpha, sizeof u);
+  const uint32_t e = (u >> 23) & 0xFFu;
+  return (u & 0x7FFFFFu) == 0 && e > 0 && e < 255;
+}
 
 // ===========================================================================
 // K4: skinny GEMM  D[M, BN] = sum_k A[m, k] B[n, k]   (M tile 128, BN = padded r)
@@ -781,7 +788,9 @@ constexpr size_t smem_bytes() {
 // instead of being consumed, so lors_effective_weight / merge() return exactly
 // the tiles the forward's tensor cores multiply (same recompute MMA, same
 // weff_pair).
-template <bool DX, int RP, bool BITS, bool SP, bool EX = false>
+// P2: alpha is a power of two (the default 2.0) -- weff_pair's fused three-instruction form;
+// the host picks the instantiation from alpha (alpha_pow2), so the transform carries one form.
+template <bool DX, int RP, bool BITS, bool SP, bool EX = false, bool P2 = true>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1)
     tc_lors_gemm_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmAct2,
                         const __grid_constant__ CUtensorMap tmW,
@@ -1146,7 +1155,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     const int t = q * 32 + lane;   // feature row inside the tile (TMEM lane)
     int gm = m0 + t;               // global output feature (per tile)
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    const uint64_t alpha_x2 = f32x2_splat(alpha);   // fp32 alpha for weff_pair
+    const WeffAlpha walpha = weff_alpha(alpha);      // weff_pair's alpha operands
     // Per k-step: issue the TMEM load of the rank-r product and all W loads,
     // release the recompute buffer, then transform and store.  (Pipelining the
     // loads of step i + 1 under step i measured no faster.)
@@ -1202,6 +1211,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       if (lane == 0) mbar_arrive_cluster(rready_l + (i % NE) * 16);  // RE buffer free for step i + NE
     };
     auto finish = [&](const int i, const int kq, uint32_t (&p)[32], uint32_t (&wv)[16], uint32_t mw) {
+      constexpr bool POW2 = P2;
       const int wb = i % NA, wi = i % NW;
       // 3. destination buffer drained by the MMA of step i - NA
       // waits for the commit of main(i - NA), the previous user of this buffer
@@ -1216,10 +1226,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         for (int g = 0; g < 8; ++g) {
           const uint32_t nib = (mw >> (4 * g)) & 0xFu;
           const uint32_t sel = 0x1010u + (nib & 3u) * 0x22u + (nib >> 2) * 0x2200u;
-          const uint32_t o0 = weff_pair(wv[2 * g], __uint_as_float(p[4 * g]), __uint_as_float(p[4 * g + 1]),
-                                        alpha_x2, nonzero_mask_bf16x2(wv[2 * g]));
-          const uint32_t o1 = weff_pair(wv[2 * g + 1], __uint_as_float(p[4 * g + 2]), __uint_as_float(p[4 * g + 3]),
-                                        alpha_x2, nonzero_mask_bf16x2(wv[2 * g + 1]));
+          const uint32_t o0 = weff_pair<POW2>(wv[2 * g], __uint_as_float(p[4 * g]), __uint_as_float(p[4 * g + 1]),
+                                        walpha, nonzero_mask_bf16x2(wv[2 * g]));
+          const uint32_t o1 = weff_pair<POW2>(wv[2 * g + 1], __uint_as_float(p[4 * g + 2]), __uint_as_float(p[4 * g + 3]),
+                                        walpha, nonzero_mask_bf16x2(wv[2 * g + 1]));
           comp[g] = prmt(o0, o1, sel);
         }
 #pragma unroll
@@ -1248,7 +1258,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
             const uint32_t w2 = wv[4 * c + u];
             const uint32_t keep = BITS ? bits2_to_mask((mword >> (c * 8 + 2 * u)) & 3u) : nonzero_mask_bf16x2(w2);
             keepm[u] = keep;
-            o[u] = weff_pair(w2, __uint_as_float(p[c * 8 + 2 * u]), __uint_as_float(p[c * 8 + 2 * u + 1]), alpha_x2,
+            o[u] = weff_pair<POW2>(w2, __uint_as_float(p[c * 8 + 2 * u]), __uint_as_float(p[c * 8 + 2 * u + 1]), walpha,
                              keep);
           }
           if (SP) {
@@ -1305,11 +1315,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 #pragma unroll
           for (int jp = 0; jp < 2; ++jp) {
             const uint32_t* wq = &wv[4 * (2 * g + jp)];
+            uint32_t o4[4];
 #pragma unroll
             for (int mm = 0; mm < 4; ++mm) {
               const int sm = mm & 1, j = 2 * jp + (mm >> 1);
-              const uint32_t ct = q * 32 + 16 * g + 8 * sm + (lane >> 2);
-              const uint32_t k = h * 32 + 8 * j + 2 * (lane & 3);
+              const uint32_t ct = q * 32 + 16 * g + 8 * sm + (lane >> 2);   // k = 32h + 8j + 2(lane % 4)
               uint32_t keep;
               if (BITS) {
                 const uint32_t cb = ct & 31;
@@ -1317,9 +1327,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
               } else {
                 keep = nonzero_mask_bf16x2(wq[mm]);
               }
-              const uint32_t o = weff_pair(wq[mm], __uint_as_float(p[16 * g + 4 * j + 2 * sm]),
-                                           __uint_as_float(p[16 * g + 4 * j + 2 * sm + 1]), alpha_x2, keep);
-              sts32(dst + ct * 128 + ((((k >> 3)) ^ (ct & 7)) << 4) + (k & 7) * 2, o);
+              const uint32_t o = weff_pair<POW2>(wq[mm], __uint_as_float(p[16 * g + 4 * j + 2 * sm]),
+                                           __uint_as_float(p[16 * g + 4 * j + 2 * sm + 1]), walpha, keep);
+              o4[mm] = o;   // W_eff^T(ct, k .. k + 1): row lane / 4, column pair lane % 4 of 8x8 block mm
+            }
+            {  // one stmatrix per four blocks: matrix mm = lane / 8 (rows ct .. ct + 7 of the K-major
+               // W_eff^T tile, 16-byte k chunk 4h + j), this lane's row address lane % 8
+              const int mi = lane >> 3;
+              const uint32_t ct = q * 32 + 16 * g + 8 * (mi & 1) + (lane & 7);
+              const uint32_t chunk = 4 * h + 2 * jp + (mi >> 1);
+              stsm_x4(dst + ct * 128 + ((chunk ^ (ct & 7)) << 4), o4[0], o4[1], o4[2], o4[3]);
             }
           }
         }
@@ -1671,7 +1688,9 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
     if ((st = make_map(&tF, a, r, R, RP, 128, RP * 2, "a (fixed)"))) return st;
   }
   if ((st = make_map(&tOut, out, Mout, L, 64, 128, 128, "output"))) return st;  // [128 tokens][64 features] SW128
-  auto kern = bits ? tc_lors_gemm_kernel<DX, RP, true, SP> : tc_lors_gemm_kernel<DX, RP, false, SP>;
+  const bool p2 = alpha_pow2(alpha);
+  auto kern = bits ? (p2 ? tc_lors_gemm_kernel<DX, RP, true, SP, false, true> : tc_lors_gemm_kernel<DX, RP, true, SP, false, false>)
+                   : (p2 ? tc_lors_gemm_kernel<DX, RP, false, SP, false, true> : tc_lors_gemm_kernel<DX, RP, false, SP, false, false>);
   const size_t smem = smem_bytes<RP, SP>();
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "lors_gemm smem attribute");
@@ -1739,7 +1758,9 @@ static int launch_weff_export(const bf16* w, const bf16* a, const bf16* b, const
   if ((st = make_map(&tS, b, C, r, 32, RP, 64, "b (streamed half)"))) return st;
   if ((st = make_map(&tF, a, r, R, RP, 128, RP * 2, "a (fixed)"))) return st;
   if ((st = make_map(&tOut, out, C, R, 64, 128, 128, "W_eff out"))) return st;   // [128 rows][64 k] SW128
-  auto kern = bits ? tc_lors_gemm_kernel<false, RP, true, false, true> : tc_lors_gemm_kernel<false, RP, false, false, true>;
+  const bool p2 = alpha_pow2(alpha);
+  auto kern = bits ? (p2 ? tc_lors_gemm_kernel<false, RP, true, false, true, true> : tc_lors_gemm_kernel<false, RP, true, false, true, false>)
+                   : (p2 ? tc_lors_gemm_kernel<false, RP, false, false, true, true> : tc_lors_gemm_kernel<false, RP, false, false, true, false>);
   const size_t smem = smem_bytes<RP, false>();
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                 "weff export smem attribute");

@@ -433,6 +433,13 @@ __device__ __forceinline__ void stsm_x4_trans(uint32_t saddr, uint32_t a, uint32
                "r"(c), "r"(d)
                : "memory");
 }
+// four 8x8 bf16 matrices, not transposed: register i of lane l = (row l/4, cols 2(l%4), +1) of
+// matrix i; lanes 8i .. 8i+7 give the 16-byte row addresses of matrix i
+__device__ __forceinline__ void stsm_x4(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
 __device__ __forceinline__ void sts32(uint32_t saddr, uint32_t v) {
   asm volatile("st.shared.b32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
 }
@@ -466,35 +473,45 @@ __device__ __forceinline__ uint32_t nonzero_mask_bf16x2(uint32_t w) {
 __device__ __forceinline__ uint32_t bits2_to_mask(uint32_t two) {
   return ((two & 1u) * 0xFFFFu) | ((two >> 1) * 0xFFFF0000u);
 }
-// (alpha, alpha) as the packed fp32 pair operand of fma.rn.f32x2
-__device__ __forceinline__ uint64_t f32x2_splat(float v) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(v));
-  return r;
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
 }
-// W_eff pair = select(M, bf16_rn(fma(alpha, P, W)), +0) -- THE effective-weight
-// definition of the bf16 path, the same arithmetic as weff_value (lors_common.cuh):
-// W widened exactly to fp32, alpha applied in fp32 inside one fma per element
-// (one FFMA2 for the pair), one rounding to bf16, then the select (an `and` with
-// the keep mask, so pruned entries are the +0.0 bit pattern).  Every tensor-core
-// prologue (K1, K2, K3) and the tensor-core K6 export call this.
-__device__ __forceinline__ uint32_t weff_pair(uint32_t w2, float p_lo, float p_hi, uint64_t alpha_x2, uint32_t keep) {
-  uint64_t wl, pl, rl;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(wl) : "f"(__uint_as_float(w2 << 16)), "f"(__uint_as_float(w2 & 0xFFFF0000u)));
+// alpha for weff_pair: (alpha, alpha) as the packed fp32 operand of mul.rn.f32x2 and as a bf16 pair
+struct WeffAlpha {
+  uint64_t x2;
+  uint32_t b2;
+};
+__device__ __forceinline__ WeffAlpha weff_alpha(float alpha) {
+  WeffAlpha a;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(a.x2) : "f"(alpha));
+  a.b2 = pack_bf16x2(alpha, alpha);
+  return a;
+}
+// W_eff pair = select(M, bf16(W + bf16(alpha P)), +0) -- THE effective weight of the bf16
+// path: the reference's evaluation order (matmul -> hadamard -> add_scaled, adapters.py:
+// 214-224) with the scaled product and the sum each rounded to bf16, alpha applied in fp32;
+// the select is an `and` with the keep mask, so pruned entries are the +0.0 bit pattern.
+// POW2 (alpha a power of two, the default 2.0): bf16(alpha P) = alpha bf16(P), so the
+// product and the add fuse into one bf16x2 fma (cvt, fma, and); otherwise mul.rn.f32x2,
+// cvt, add (one instruction more).  Every tensor-core prologue (K1, K2, K3) and the
+// tensor-core K6 export call this; the FFMA kernels' weff_value is the same arithmetic.
+template <bool POW2>
+__device__ __forceinline__ uint32_t weff_pair(uint32_t w2, float p_lo, float p_hi, const WeffAlpha& al, uint32_t keep) {
+  if (POW2) return fma_bf16x2(al.b2, cvt_bf16x2(p_lo, p_hi), w2) & keep;
+  uint64_t pl, ap;
   asm("mov.b64 %0, {%1, %2};" : "=l"(pl) : "f"(p_lo), "f"(p_hi));
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rl) : "l"(alpha_x2), "l"(pl), "l"(wl));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(ap) : "l"(al.x2), "l"(pl));
   float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(rl));
-  return cvt_bf16x2(lo, hi) & keep;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(ap));
+  uint32_t r;
+  asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(cvt_bf16x2(lo, hi)), "r"(w2));
+  return r & keep;
 }
 
 // ---------------------------------------------------------------------------
 // misc
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
 
 }  // namespace ptx
 }  // namespace lors

@@ -25,6 +25,13 @@ def _fixture():
     return dict(np.load(GOLD))
 
 
+@pytest.fixture(autouse=True)
+def _deterministic(monkeypatch):
+    """Parity runs use the deterministic adapter-gradient mode (ordered split-K reductions),
+    so a curve is bitwise replayable like the reference's (test_train.py:169-178)."""
+    monkeypatch.setenv("LORS_DETERMINISTIC", "1")
+
+
 def test_oracle_loss_curve_matches_reference_fixture():
     d = _fixture()
     D = int(d["meta"][1])

@@ -103,16 +103,19 @@ def test_sparse24_tile_is_effective_weight(ops, R, C, r, with_meta, alpha):
 @pytest.mark.parametrize("alpha", ALPHAS)
 @pytest.mark.parametrize("R,C,r", [(512, 384, 16), (1024, 4096, 64), (250, 120, 5)])
 def test_effective_weight_vs_oracle(ops, R, C, r, alpha):
-    """K6 against the oracle's merged_weight on the bf16-rounded inputs: every kept
-    entry within one bf16 rounding of the float64 value (the fp32 rank-r product is
-    the only other error), every pruned entry +0.0.  (250, 120, 5) runs the FFMA
+    """K6 against the oracle's merged_weight on the bf16-rounded inputs: W_eff is
+    bf16(W + bf16(alpha P)) (the reference's order, matmul -> hadamard -> add_scaled,
+    each result rounded to bf16), so every kept entry lies within half a bf16 ulp of
+    alpha P plus half an ulp of the result of the float64 value (the fp32 rank-r sum
+    adds a few fp32 ulps); every pruned entry is +0.0.  (250, 120, 5) runs the FFMA
     kernel (shapes TMA cannot address)."""
     w, a, b = _layer(R, C, r, "rowwise", seed=11 * R + r, a_scale=0.5)
     weff = ops.effective_weight(w, a, b, alpha).double().cpu().numpy()
     wd, ad, bd = (t.double().cpu().numpy() for t in (w, a, b))
     ref = orc.merged_weight(wd, ad, bd, alpha, orc.mask_matrix(wd))
     keep = wd != 0
-    ulp = np.abs(ref) * 2.0 ** -8 + 4e-6   # one bf16 rounding + the fp32 rank-r sum near cancellation
+    scaled = np.abs(alpha * (ad @ bd))
+    ulp = (scaled + np.abs(ref)) * 2.0 ** -8 + 4e-6   # two bf16 roundings + the fp32 rank-r sum
     assert np.all(np.abs(weff - ref)[keep] <= ulp[keep])
     assert np.all(weff[~keep] == 0) and not np.signbit(weff[~keep]).any()
 

@@ -1,0 +1,8 @@
+E=$PWD/paper_2501_08582_b200/_native/exp
+LORS_B200_LIB=$E/stsm/liblors_b200.so python -m pytest tests/test_weff_identity.py -q -m gpu -k dx > gpurun_out/stsm_id.log 2>&1
+for i in 1 2; do
+  python tools/ab_gemm.py >> gpurun_out/ab1.log 2>&1
+  LORS_B200_LIB=$E/oldweff/liblors_b200.so python tools/ab_gemm.py >> gpurun_out/ab1.log 2>&1
+  LORS_B200_LIB=$E/stsm/liblors_b200.so python tools/ab_gemm.py >> gpurun_out/ab1.log 2>&1
+done
+tail -n 2 gpurun_out/stsm_id.log
