@@ -695,11 +695,10 @@ struct alignas(16) Bar16 {
 
 namespace rg {
 constexpr int BM = 128, BN = 256, BK = 64;
-// warps 0 .. XW-1: transform + epilogue.  The 2:4 forward runs two groups of 8
-// taking alternate k-steps, so one step's transform may span two (twice as
-// fast) sparse MMA steps; the dense kernels measured faster with one group.
-// Then the roles: factor-ring producer, MMA issuer / relay, activation
-// producer, activation relay, W-ring producer.
+// warps 0 .. XW-1: transform + epilogue (one group of 8; the non-persistent build,
+// LORS_PERSIST=0, can run two groups on alternate k-steps).  Then the roles:
+// factor-ring producer, MMA issuer / relay, activation producer, activation
+// relay, W-ring producer.
 #ifndef LORS_XW_DENSE
 #define LORS_XW_DENSE 8
 #endif
@@ -712,36 +711,41 @@ constexpr int BM = 128, BN = 256, BK = 64;
 #ifndef LORS_PERSIST
 #define LORS_PERSIST 1
 #endif
-// Persistent dense kernels: one CTA pair per SM pair walks its tiles; the
-// producers and the recompute run ahead into the next tile while the
+// Persistent kernels (dense-masked and 2:4): one CTA pair per SM pair walks its
+// tiles; the producers and the recompute run ahead into the next tile while the
 // epilogue drains the accumulator through the (then idle) W_eff ring.
 template <bool SP>
-constexpr bool persist() { return !SP && LORS_PERSIST; }
+constexpr bool persist() { return LORS_PERSIST; }
 template <bool SP>
-constexpr int xw() { return SP ? 16 : LORS_XW_DENSE; }
+constexpr int xw() { return LORS_PERSIST ? LORS_XW_DENSE : (SP ? 16 : LORS_XW_DENSE); }
 template <bool SP>
 constexpr int threads() { return 32 * (xw<SP>() + 5); }
-// Token tile of a CTA pair.  The dense kernels take 256 + N2 tokens per W_eff
-// tile -- one N = 256 MMA and one N = N2 MMA per k-step into two accumulators
-// -- so each on-chip W_eff tile (its rank-r recompute, transform and W load)
-// serves 1.5x the tokens; TMEM is then acc 256 + N2 columns plus NE = 2
-// recompute buffers of 64.  The 2:4 kernel keeps 256 tokens: its TMEM holds
-// the sparse metadata next to three recompute buffers.
+// Token tile of a CTA pair: 256 + N2 tokens per W_eff tile -- one N = 256 MMA and
+// one N = N2 MMA per k-step into two accumulators -- so each on-chip W_eff tile (its
+// rank-r recompute, transform and W load) serves 1.5x the tokens.  TMEM: acc 256 + N2
+// columns, then NE recompute buffers of 64 (dense: 2; 2:4: 1, next to the sparse
+// metadata of the NA W_eff buffers at E_COL).
 template <bool SP>
-constexpr int n2() { return SP ? 0 : LORS_N2; }
+constexpr int n2() { return (SP && !LORS_PERSIST) ? 0 : LORS_N2; }
 template <bool SP>
 constexpr int bnt() { return 256 + n2<SP>(); }            // tokens per pair tile
-// factor ring (streamed adapter-factor half) = TMEM recompute buffers.  The W
-// ring is separate: the recompute of step j needs only its factor slice, W(j)
-// is first read by the transform, D steps later, so W loads are not exposed.
+// TMEM recompute buffers, and the factor ring (streamed adapter-factor half) with its
+// own depth NS: a factor slot is free once its recompute committed, a recompute
+// buffer once the transform has read it.  The W ring is separate too: the recompute
+// of step j needs only its factor slice, W(j) is first read by the transform.
 template <bool SP>
-constexpr int ne() { return SP ? 3 : (512 - 256 - n2<SP>()) / 64; }
+constexpr int ne() { return SP ? (LORS_PERSIST ? 1 : 3) : (512 - 256 - n2<SP>()) / 64; }
 template <bool SP>
-constexpr int nw() { return SP ? 6 : LORS_NW_DENSE; }  // W ring
+constexpr int ns() { return SP ? 3 : 2; }
 template <bool SP>
-constexpr int na() { return SP ? 4 : 3; }  // activation ring = W_eff buffers
+constexpr int nw() { return SP ? (LORS_PERSIST ? 4 : 6) : LORS_NW_DENSE; }  // W ring
 template <bool SP>
-constexpr int lookahead() { return ne<SP>() - 1; }  // recompute lookahead (steps)
+constexpr int na() { return SP ? (LORS_PERSIST ? 3 : 4) : 3; }  // activation ring = W_eff buffers
+// recompute lookahead: recompute(j) is issued before main(j - 1), so the transform of
+// step j overlaps the tensor-core work of step j - 1 (one buffer suffices: the
+// transform releases it right after its TMEM load)
+template <bool SP>
+constexpr int lookahead() { return 1; }
 // 2:4 index nibble (idx0 | idx1 << 2, idx0 < idx1) for each 4-bit keep mask;
 // groups with fewer than two kept entries are padded with zero-valued slots,
 // masks with more than two are not 2:4 (prune.py:72-77) and never reach here.
@@ -767,8 +771,10 @@ constexpr int GROUP_T = LORS_GROUP_T;  // raster: token tiles per group (cluster
 template <bool SP>
 constexpr uint32_t act_bytes() { return (bnt<SP>() / 2) * BK * 2; }   // this CTA's tokens: 24 KB / 16 KB
 constexpr uint32_t W_BYTES = BM * BK * 2;           // 16 KB
+// W_eff buffer stride: 16 KB (the 2:4 kernel's compressed tile uses the first half; the
+// persistent epilogue stages 16 KB output blocks through these buffers)
 template <bool SP>
-constexpr uint32_t weff_bytes() { return SP ? BM * BK : BM * BK * 2; }  // 2:4 keeps half (compressed)
+constexpr uint32_t weff_bytes() { return (SP && !LORS_PERSIST) ? BM * BK : BM * BK * 2; }
 constexpr uint32_t TMEM_COLS = 512;
 template <bool SP>
 constexpr uint32_t re_col() { return 256 + n2<SP>(); }  // recompute buffers at TMEM cols re_col + 64 e
@@ -778,7 +784,7 @@ template <int RP>
 constexpr uint32_t ff_bytes() { return 128 * RP * 2; }  // fixed factor tile (128 m x RP)
 template <int RP, bool SP>
 constexpr size_t smem_bytes() {
-  return 1024 + ne<SP>() * sf_bytes<RP>() + nw<SP>() * W_BYTES + na<SP>() * act_bytes<SP>() +
+  return 1024 + ns<SP>() * sf_bytes<RP>() + nw<SP>() * W_BYTES + na<SP>() * act_bytes<SP>() +
          na<SP>() * weff_bytes<SP>() + ff_bytes<RP>() + 1024;
 }
 }  // namespace rg
@@ -804,10 +810,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   static_assert(!EX || (!DX && !SP && LORS_PERSIST), "W_eff export runs the persistent forward prologue");
   constexpr int XW = xw<SP>(), XFORM_THREADS = 32 * XW;
   constexpr int W_SF = XW, W_MMA = XW + 1, W_ACT = XW + 2, W_RELAY = XW + 3, W_WLOAD = XW + 4;
-  constexpr int NE = ne<SP>(), NW = nw<SP>(), NA = na<SP>(), D = lookahead<SP>();
+  constexpr int NE = ne<SP>(), NS = ns<SP>(), NW = nw<SP>(), NA = na<SP>(), D = lookahead<SP>();
   constexpr int NGRP = XW / 8;          // transform groups (alternate k-steps)
   constexpr bool PERSIST = persist<SP>();
   static_assert(!PERSIST || NGRP == 1, "persistent schedule assumes one transform group");
+  static_assert(re_col<SP>() + NE * 64 <= (SP ? E_COL : TMEM_COLS) && (!SP || E_COL + NA * 8 <= TMEM_COLS),
+                "TMEM: accumulators, recompute buffers and 2:4 metadata must fit 512 columns");
   constexpr int N2 = n2<SP>(), BNT = bnt<SP>();
   constexpr uint32_t ACT_BYTES = act_bytes<SP>(), ACT1_BYTES = 128 * BK * 2;
   constexpr uint32_t RE_COL = re_col<SP>();
@@ -822,19 +830,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   constexpr uint32_t SWR = RP * 2;  // swizzle span of the K-major rank-r tiles
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sfr = smem;                       // [NE] streamed factor halves
-  uint8_t* wring = sfr + NE * SF;            // [NW] W tiles
+  uint8_t* sfr = smem;                       // [NS] streamed factor halves
+  uint8_t* wring = sfr + NS * SF;            // [NW] W tiles
   uint8_t* actb = wring + NW * W_BYTES;      // [NA] activation halves
   uint8_t* weff = actb + NA * ACT_BYTES;     // [NA] W_eff tiles
   uint8_t* ffac = weff + NA * WEFF_BYTES;    // fixed factor
-  // mbarriers, one per 16 bytes.  rready / mready are the merged "may issue"
-  // barriers of the leader: count 18 = own producer (with its TMA bytes) +
-  // the peer's relayed landing + 16 transform warps of both CTAs.  In the
-  // peer they only track the peer's own TMA landing (count 1).
+  // mbarriers, one per 16 bytes.  mready is the merged "may issue" barrier of the
+  // leader: count 18 = own producer (with its TMA bytes) + the peer's relayed
+  // landing + 16 transform warps of both CTAs; sready counts 2 in the leader (own
+  // factor load + the peer's relayed one).  In the peer they only track the
+  // peer's own TMA landing (count 1).
   Bar16* bars = reinterpret_cast<Bar16*>(ffac + FF);
-  Bar16* rready = bars;                 // [NE] recompute(j) may issue / factor landed
-  Bar16* e_empty = rready + NE;         // [NE] local: recompute committed (factor slot free)
-  Bar16* mready = e_empty + NE;         // [NA] main(j) may issue / activation landed
+  Bar16* sready = bars;                 // [NS] factor slot landed (both CTAs, in the leader)
+  Bar16* s_empty = sready + NS;         // [NS] local: recompute committed (factor slot free)
+  Bar16* refree = s_empty + NS;         // [NE] leader: 16 transform warps read the recompute buffer
+  Bar16* mready = refree + NE;          // [NA] main(j) may issue / activation landed
   Bar16* a_empty = mready + NA;         // [NA] local: pair MMA done with the activation half
   // [2][NE] local: recompute landed in TMEM, one set per transform group so that
   // with an odd NE (buffers alternate between the groups) no waiter runs two
@@ -901,13 +911,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 
   if (warp == W_SF) {
     // lane-parallel barrier initialisation over the flat Bar16 array (layout above):
-    // rready / mready count the merged arrivals in the leader, wfree the 8
-    // transform warps, everything else one arrival
-    constexpr int NBARS = 4 * NE + 4 * NA + 3 + 3 * NW + 2;
-    const uint32_t merged = leader ? 18u : 1u;
+    // sready / mready count the merged arrivals in the leader, refree and acc_empty
+    // the 16 transform warps of the pair, wfree the 8 of the CTA, the rest one arrival
+    constexpr int NBARS = 2 * NS + 3 * NE + 4 * NA + 3 + 3 * NW + 2;
+    constexpr int MREADY0 = 2 * NS + NE;
     for (int k = lane; k < NBARS; k += 32) {
       uint32_t cnt = 1;
-      if (k < NE || (k >= 2 * NE && k < 2 * NE + NA)) cnt = merged;
+      if (k < NS) cnt = leader ? 2u : 1u;                              // sready
+      if (k >= 2 * NS && k < MREADY0) cnt = 16;                        // refree
+      if (k >= MREADY0 && k < MREADY0 + NA) cnt = leader ? 18u : 1u;   // mready
       if (k >= NBARS - 2 - NW && k < NBARS - 2) cnt = 8;   // wfree
       if (k == NBARS - 1) cnt = 16;                       // acc_empty
       mbar_init(&bars[k].b, cnt);
@@ -915,7 +927,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     fence_barrier_init();
     __syncwarp();
     // first use of every recompute buffer: nobody has read it yet
-    if (leader && lane < NE) mbar_arrive_count(&rready[lane].b, 16);
+    if (leader && lane < NE) mbar_arrive_count(&refree[lane].b, 16);
     if (lane == 0) {
       tma_prefetch_desc(&tmAct);
       if (N2) tma_prefetch_desc(&tmAct2);
@@ -938,7 +950,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   // Every TMA completes on a barrier of the CTA that issued it; the peer
   // relays its landings to the leader, and the transform warps of both CTAs
   // arrive on the leader's merged barriers.  Remote arrives go through mapa.
-  const uint32_t rready_l = mapa_shared(smem_u32(rready), 0);
+  const uint32_t sready_l = mapa_shared(smem_u32(sready), 0);
+  const uint32_t refree_l = mapa_shared(smem_u32(refree), 0);
   const uint32_t mready_l = mapa_shared(smem_u32(mready), 0);
   const uint32_t pffull_l = mapa_shared(smem_u32(pffull), 0);
   const uint32_t acc_empty_l = mapa_shared(smem_u32(acc_empty), 0);
@@ -958,13 +971,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         tma_load_2d(ffac, &tmF, ffull, 0, m0);
       }
       for (int i = kb; i < ke; ++i, ++g) {
-        const int e = g % NE;
-        mbar_wait(&e_empty[e].b, ((g / NE) & 1) ^ 1);
-        uint8_t* st = sfr + e * SF;
+        const int sl = g % NS;
+        mbar_wait(&s_empty[sl].b, ((g / NS) & 1) ^ 1);
+        uint8_t* st = sfr + sl * SF;
         const int k0 = i * BK;
-        mbar_arrive_expect_tx(&rready[e].b, SF);
-        if (DX) tma_load_2d(st, &tmS, &rready[e].b, 0, k0 + 32 * rank);   // a rows, K-major
-        else tma_load_2d(st, &tmS, &rready[e].b, k0 + 32 * rank, 0);      // b cols, MN-major
+        mbar_arrive_expect_tx(&sready[sl].b, SF);
+        if (DX) tma_load_2d(st, &tmS, &sready[sl].b, 0, k0 + 32 * rank);   // a rows, K-major
+        else tma_load_2d(st, &tmS, &sready[sl].b, k0 + 32 * rank, 0);      // b cols, MN-major
       }
       }
     }
@@ -1036,9 +1049,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           mbar_wait(ffull, n & 1);
           mbar_arrive_cluster(pffull_l);
           for (int i = kb; i < ke; ++i, ++g) {
-            const int e = g % NE;
-            mbar_wait(&rready[e].b, (g / NE) & 1);
-            mbar_arrive_cluster(rready_l + e * 16);
+            const int sl = g % NS;
+            mbar_wait(&sready[sl].b, (g / NS) & 1);
+            mbar_arrive_cluster(sready_l + sl * 16);
           }
         }
       }
@@ -1048,6 +1061,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       constexpr uint32_t idesc_main = make_idesc_bf16(256, 256, false, false);
       constexpr uint32_t idesc_n2 = make_idesc_bf16(256, N2 ? N2 : 256, false, false);
       constexpr uint32_t idesc_sp = make_idesc_bf16(256, 256, false, false, true);
+      constexpr uint32_t idesc_sp_n2 = make_idesc_bf16(256, N2 ? N2 : 256, false, false, true);
       // descriptor bases; a descriptor's start-address field is addr >> 4, so
       // byte offsets inside shared memory are added as (offset >> 4)
       const uint64_t ff_desc = DX ? make_sdesc(smem_u32(ffac), FF / 2, 1024, SW_128)
@@ -1064,17 +1078,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           mbar_wait(ffull, rn & 1);
           mbar_wait(pffull, rn & 1);
         }
-        const int e = j % NE;
-        mbar_wait(&rready[e].b, (j / NE) & 1);
+        const int e = j % NE, sl = j % NS;
+        mbar_wait(&sready[sl].b, (j / NS) & 1);      // factor slice of step j landed in both CTAs
+        mbar_wait(&refree[e].b, (j / NE) & 1);       // recompute buffer e read by the transform of j - NE
         tc_fence_after();
         if (elect_one()) {
-          const uint64_t sfd = sf_desc + (uint64_t)(e * (SF >> 4));
+          const uint64_t sfd = sf_desc + (uint64_t)(sl * (SF >> 4));
 #pragma unroll
           for (int kk = 0; kk < RP / 16; ++kk)
             mma_bf16_pair(tmem + RE_COL + e * 64, ff_desc + kk * FF_KSTEP, sfd + kk * SF_KSTEP, idesc_re,
                           kk > 0 ? 1u : 0u);
           mma_commit_pair(&refull[(j % NGRP) * NE + e].b, 0x3);
-          mma_commit_pair(&e_empty[e].b, 0x3);
+          mma_commit_pair(&s_empty[sl].b, 0x3);
           if (PERSIST && rk == rlen - 1) mma_commit_pair(ff_empty, 0x3);   // fixed factor may be replaced
         }
         __syncwarp();
@@ -1099,6 +1114,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
             for (int hh = 0; hh < 2; ++hh)
               mma_bf16_pair_sp(tmem, ad + hh * 2, bd + hh * 4, tmem + E_COL + a * 8 + hh * 4, idesc_sp,
                                (mk > 0 || hh > 0) ? 1u : 0u);
+            if (N2 && main_n2) {  // tokens 256 .. 256 + N2 into the second accumulator, same A and metadata
+              const uint64_t bd2 = bd + (ACT1_BYTES >> 4);
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh)
+                mma_bf16_pair_sp(tmem + 256, ad + hh * 2, bd2 + hh * 4, tmem + E_COL + a * 8 + hh * 4, idesc_sp_n2,
+                                 (mk > 0 || hh > 0) ? 1u : 0u);
+            }
           } else {
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk)
@@ -1208,7 +1230,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(rready_l + (i % NE) * 16);  // RE buffer free for step i + NE
+      if (lane == 0) mbar_arrive_cluster(refree_l + (i % NE) * 16);  // RE buffer free for step i + NE
     };
     auto finish = [&](const int i, const int kq, uint32_t (&p)[32], uint32_t (&wv)[16], uint32_t mw) {
       constexpr bool POW2 = P2;

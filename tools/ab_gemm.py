@@ -71,6 +71,9 @@ for name, L, R, C, r, pat in SHAPES:
     fwd = lambda: ops.lors_fwd(x, w, a, b, 2.0)  # noqa: E731
     dx = lambda: ops._lors_bwd_call(x, w, a, b, dy, 2.0, None, None, "ste", True, False, False, dx_only=True)  # noqa
     res = {"fwd": (iso(fwd), sus(fwd)), "dx": (iso(dx), sus(dx))}
+    if os.environ.get("AB_CUBLAS"):
+        mm = lambda: x @ w.t()  # noqa: E731
+        res["cublas"] = (iso(mm), sus(mm))
     if pat == "two_four":
         meta = ops.compress_24(w)[1]
         sp = lambda: ops.lors_fwd(x, w, a, b, 2.0, sparse24=True, meta24=meta)  # noqa: E731
