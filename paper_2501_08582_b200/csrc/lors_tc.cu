@@ -1007,7 +1007,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     cluster_wait();
   } else if (warp == W_ACT) {
     // ------------------------------------------------------------ activation-ring producer (both CTAs)
+#ifdef LORS_ACT_2LANE
+    // two issuing lanes: lane 0 the N = 256 half (with the byte count), lane 1 the N2 half
+    if (lane < (N2 ? 2 : 1) && !EX) {
+#else
     if (lane == 0 && !EX) {
+#endif
       for (int n = 0, g = 0; n < my_units; ++n) {
       int kb, ke, ut, part;
       unit(n, m0, l0, kb, ke, ut, part);
@@ -1015,9 +1020,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       for (int i = kb; i < ke; ++i, ++g) {
         const int a = g % NA;
         mbar_wait(&a_empty[a].b, ((g / NA) & 1) ^ 1);
+#ifdef LORS_ACT_2LANE
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&mready[a].b, ACT_BYTES);
+          tma_load_2d(actb + a * ACT_BYTES, &tmAct, &mready[a].b, i * BK, lh);
+        } else {
+          tma_load_2d(actb + a * ACT_BYTES + ACT1_BYTES, &tmAct2, &mready[a].b, i * BK, lh2);
+        }
+#else
         mbar_arrive_expect_tx(&mready[a].b, ACT_BYTES);
         tma_load_2d(actb + a * ACT_BYTES, &tmAct, &mready[a].b, i * BK, lh);
         if (N2) tma_load_2d(actb + a * ACT_BYTES + ACT1_BYTES, &tmAct2, &mready[a].b, i * BK, lh2);
+#endif
       }
       }
     }

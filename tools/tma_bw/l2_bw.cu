@@ -23,10 +23,12 @@ __global__ void l2_kernel(const __grid_constant__ CUtensorMap m, int n_boxes, in
     fence_barrier_init();
   }
   __syncthreads();
-  if (threadIdx.x != 0) return;
+  // `issuers` threads (one per warp) each own every issuers-th stage of the ring
+  const int issuers = blockDim.x / 32, me = threadIdx.x / 32;
+  if (threadIdx.x % 32 != 0) return;
   unsigned long long acc = 0;
   const int total = n_boxes * reps, start = stagger ? (int)(blockIdx.x * 7919) % n_boxes : 0;
-  for (int i = 0; i < total; ++i) {
+  for (int i = me; i < total; i += issuers) {
     const int s = i % stages;
     if (i >= stages) {
       mbar_wait(&full[s], ((i / stages) - 1) & 1);
@@ -36,7 +38,8 @@ __global__ void l2_kernel(const __grid_constant__ CUtensorMap m, int n_boxes, in
     mbar_arrive_expect_tx(&full[s], box_bytes);
     tma_load_2d(smem + s * box_bytes, &m, &full[s], (b % col_boxes) * 64, (b / col_boxes) * box_rows);
   }
-  for (int j = (total > stages ? total - stages : 0); j < total; ++j) mbar_wait(&full[j % stages], (j / stages) & 1);
+  for (int j = (total > stages ? total - stages : 0); j < total; ++j)
+    if (j % issuers == me) mbar_wait(&full[j % stages], (j / stages) & 1);
   if (acc == 12345) *sink = acc;
 }
 
@@ -44,7 +47,8 @@ typedef CUresult (*PFN_encode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, vo
                                const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 int main(int argc, char** argv) {
-  if (argc < 8) { printf("usage: l2_bw rows cols box_rows stages ctas_per_sm reps stagger\n"); return 1; }
+  if (argc < 8) { printf("usage: l2_bw rows cols box_rows stages ctas_per_sm reps stagger [issuers]\n"); return 1; }
+  const int issuers = argc > 8 ? atoi(argv[8]) : 1;
   const int rows = atoi(argv[1]), cols = atoi(argv[2]), box_rows = atoi(argv[3]), stages = atoi(argv[4]),
             cps = atoi(argv[5]), reps = atoi(argv[6]), stagger = atoi(argv[7]);
   void* d; cudaMalloc(&d, (size_t)rows * cols * 2); cudaMemset(d, 1, (size_t)rows * cols * 2);
@@ -66,7 +70,7 @@ int main(int argc, char** argv) {
   float best = 1e9;
   for (int it = 0; it < 5; ++it) {
     cudaEventRecord(e0);
-    l2_kernel<<<nsm * cps, 32, smem>>>(m, n_boxes, col_boxes, box_rows, stages, reps, stagger, sink);
+    l2_kernel<<<nsm * cps, 32 * issuers, smem>>>(m, n_boxes, col_boxes, box_rows, stages, reps, stagger, sink);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -74,8 +78,8 @@ int main(int argc, char** argv) {
   }
   cudaError_t err = cudaGetLastError();
   const double bytes = (double)nsm * cps * rows * cols * 2 * reps;
-  printf("l2 rows %d cols %d box %dx64 stages %d ctas/sm %d reps %d stagger %d: %.1f us, %.0f GB/s delivered, %.1f B/clk/SM at 1.965 GHz (%s)\n",
-         rows, cols, box_rows, stages, cps, reps, stagger, best * 1e3, bytes / (best * 1e-3) / 1e9,
+  printf("l2 issuers %d rows %d cols %d box %dx64 stages %d ctas/sm %d reps %d stagger %d: %.1f us, %.0f GB/s delivered, %.1f B/clk/SM at 1.965 GHz (%s)\n",
+         issuers, rows, cols, box_rows, stages, cps, reps, stagger, best * 1e3, bytes / (best * 1e-3) / 1e9,
          bytes / (best * 1e-3) / nsm / 1.965e9, cudaGetErrorString(err));
   return 0;
 }
