@@ -708,6 +708,9 @@ constexpr int BM = 128, BN = 256, BK = 64;
 #ifndef LORS_NW_DENSE
 #define LORS_NW_DENSE 4
 #endif
+#ifndef LORS_NW_SP
+#define LORS_NW_SP 4
+#endif
 #ifndef LORS_PERSIST
 #define LORS_PERSIST 1
 #endif
@@ -738,9 +741,17 @@ constexpr int ne() { return SP ? (LORS_PERSIST ? 1 : 3) : (512 - 256 - n2<SP>())
 template <bool SP>
 constexpr int ns() { return SP ? 3 : 2; }
 template <bool SP>
-constexpr int nw() { return SP ? (LORS_PERSIST ? 4 : 6) : LORS_NW_DENSE; }  // W ring
+constexpr int nw() { return SP ? (LORS_PERSIST ? LORS_NW_SP : 6) : LORS_NW_DENSE; }  // W ring
 template <bool SP>
-constexpr int na() { return SP ? (LORS_PERSIST ? 3 : 4) : 3; }  // activation ring = W_eff buffers
+constexpr int na() { return SP ? (LORS_PERSIST ? 3 : 4) : 3; }  // W_eff buffers
+#ifndef LORS_NACT
+#define LORS_NACT 3
+#endif
+// activation ring, its own depth (barriers afull / a_empty) apart from the W_eff ring: an
+// activation half is requested when the MMA of the step NACT earlier has finished with its
+// slot.  4 slots (with a 3-deep W ring to fit 227 KB) measured no faster than 3 (tools/ab_gemm.py)
+template <bool SP>
+constexpr int nact() { return LORS_PERSIST ? LORS_NACT : na<SP>(); }
 // recompute lookahead: recompute(j) is issued before main(j - 1), so the transform of
 // step j overlaps the tensor-core work of step j - 1 (one buffer suffices: the
 // transform releases it right after its TMEM load)
@@ -784,7 +795,7 @@ template <int RP>
 constexpr uint32_t ff_bytes() { return 128 * RP * 2; }  // fixed factor tile (128 m x RP)
 template <int RP, bool SP>
 constexpr size_t smem_bytes() {
-  return 1024 + ns<SP>() * sf_bytes<RP>() + nw<SP>() * W_BYTES + na<SP>() * act_bytes<SP>() +
+  return 1024 + ns<SP>() * sf_bytes<RP>() + nw<SP>() * W_BYTES + nact<SP>() * act_bytes<SP>() +
          na<SP>() * weff_bytes<SP>() + ff_bytes<RP>() + 1024;
 }
 }  // namespace rg
@@ -810,10 +821,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   static_assert(!EX || (!DX && !SP && LORS_PERSIST), "W_eff export runs the persistent forward prologue");
   constexpr int XW = xw<SP>(), XFORM_THREADS = 32 * XW;
   constexpr int W_SF = XW, W_MMA = XW + 1, W_ACT = XW + 2, W_RELAY = XW + 3, W_WLOAD = XW + 4;
-  constexpr int NE = ne<SP>(), NS = ns<SP>(), NW = nw<SP>(), NA = na<SP>(), D = lookahead<SP>();
+  constexpr int NE = ne<SP>(), NS = ns<SP>(), NW = nw<SP>(), NA = na<SP>(), NACT = nact<SP>(), D = lookahead<SP>();
   constexpr int NGRP = XW / 8;          // transform groups (alternate k-steps)
   constexpr bool PERSIST = persist<SP>();
   static_assert(!PERSIST || NGRP == 1, "persistent schedule assumes one transform group");
+  static_assert(smem_bytes<RP, SP>() <= 232448, "shared memory: rings exceed 227 KB");
   static_assert(re_col<SP>() + NE * 64 <= (SP ? E_COL : TMEM_COLS) && (!SP || E_COL + NA * 8 <= TMEM_COLS),
                 "TMEM: accumulators, recompute buffers and 2:4 metadata must fit 512 columns");
   constexpr int N2 = n2<SP>(), BNT = bnt<SP>();
@@ -832,24 +844,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sfr = smem;                       // [NS] streamed factor halves
   uint8_t* wring = sfr + NS * SF;            // [NW] W tiles
-  uint8_t* actb = wring + NW * W_BYTES;      // [NA] activation halves
-  uint8_t* weff = actb + NA * ACT_BYTES;     // [NA] W_eff tiles
+  uint8_t* actb = wring + NW * W_BYTES;      // [NACT] activation halves
+  uint8_t* weff = actb + NACT * ACT_BYTES;   // [NA] W_eff tiles
   uint8_t* ffac = weff + NA * WEFF_BYTES;    // fixed factor
-  // mbarriers, one per 16 bytes.  mready is the merged "may issue" barrier of the
-  // leader: count 18 = own producer (with its TMA bytes) + the peer's relayed
-  // landing + 16 transform warps of both CTAs; sready counts 2 in the leader (own
-  // factor load + the peer's relayed one).  In the peer they only track the
-  // peer's own TMA landing (count 1).
+  // mbarriers, one per 16 bytes.  sready / afull count 2 in the leader (own TMA
+  // load with its bytes + the peer's relayed landing), 1 in the peer (its own
+  // landing); refree / wready count the 16 transform warps of both CTAs.
   Bar16* bars = reinterpret_cast<Bar16*>(ffac + FF);
   Bar16* sready = bars;                 // [NS] factor slot landed (both CTAs, in the leader)
   Bar16* s_empty = sready + NS;         // [NS] local: recompute committed (factor slot free)
   Bar16* refree = s_empty + NS;         // [NE] leader: 16 transform warps read the recompute buffer
-  Bar16* mready = refree + NE;          // [NA] main(j) may issue / activation landed
-  Bar16* a_empty = mready + NA;         // [NA] local: pair MMA done with the activation half
+  Bar16* afull = refree + NE;           // [NACT] activation half landed (both CTAs, in the leader)
+  Bar16* wready = afull + NACT;         // [NA] leader: W_eff buffer written by the 16 transform warps
+  Bar16* a_empty = wready + NA;         // [NACT] local: pair MMA done with the activation half
   // [2][NE] local: recompute landed in TMEM, one set per transform group so that
   // with an odd NE (buffers alternate between the groups) no waiter runs two
   // phases ahead of a barrier
-  Bar16* refull = a_empty + NA;
+  Bar16* refull = a_empty + NACT;
   // [2][NA] local: pair MMA done with the W_eff buffer, set = group of the next writer
   Bar16* wempty = refull + 2 * NE;
   uint64_t* ffull = &(wempty + 2 * NA)->b;      // local: own fixed factor landed
@@ -911,15 +922,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 
   if (warp == W_SF) {
     // lane-parallel barrier initialisation over the flat Bar16 array (layout above):
-    // sready / mready count the merged arrivals in the leader, refree and acc_empty
-    // the 16 transform warps of the pair, wfree the 8 of the CTA, the rest one arrival
-    constexpr int NBARS = 2 * NS + 3 * NE + 4 * NA + 3 + 3 * NW + 2;
-    constexpr int MREADY0 = 2 * NS + NE;
+    // sready / afull count the merged arrivals in the leader, refree / wready and
+    // acc_empty the 16 transform warps of the pair, wfree the 8 of the CTA, the rest one
+    constexpr int NBARS = 2 * NS + 3 * NE + 2 * NACT + 3 * NA + 3 + 3 * NW + 2;
+    constexpr int AFULL0 = 2 * NS + NE, WREADY0 = AFULL0 + NACT;
     for (int k = lane; k < NBARS; k += 32) {
       uint32_t cnt = 1;
       if (k < NS) cnt = leader ? 2u : 1u;                              // sready
-      if (k >= 2 * NS && k < MREADY0) cnt = 16;                        // refree
-      if (k >= MREADY0 && k < MREADY0 + NA) cnt = leader ? 18u : 1u;   // mready
+      if (k >= 2 * NS && k < AFULL0) cnt = 16;                         // refree
+      if (k >= AFULL0 && k < WREADY0) cnt = leader ? 2u : 1u;          // afull
+      if (k >= WREADY0 && k < WREADY0 + NA) cnt = 16;                  // wready
       if (k >= NBARS - 2 - NW && k < NBARS - 2) cnt = 8;   // wfree
       if (k == NBARS - 1) cnt = 16;                       // acc_empty
       mbar_init(&bars[k].b, cnt);
@@ -952,7 +964,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   // arrive on the leader's merged barriers.  Remote arrives go through mapa.
   const uint32_t sready_l = mapa_shared(smem_u32(sready), 0);
   const uint32_t refree_l = mapa_shared(smem_u32(refree), 0);
-  const uint32_t mready_l = mapa_shared(smem_u32(mready), 0);
+  const uint32_t afull_l = mapa_shared(smem_u32(afull), 0);
+  const uint32_t wready_l = mapa_shared(smem_u32(wready), 0);
   const uint32_t pffull_l = mapa_shared(smem_u32(pffull), 0);
   const uint32_t acc_empty_l = mapa_shared(smem_u32(acc_empty), 0);
 
@@ -1007,31 +1020,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     cluster_wait();
   } else if (warp == W_ACT) {
     // ------------------------------------------------------------ activation-ring producer (both CTAs)
-#ifdef LORS_ACT_2LANE
-    // two issuing lanes: lane 0 the N = 256 half (with the byte count), lane 1 the N2 half
-    if (lane < (N2 ? 2 : 1) && !EX) {
-#else
     if (lane == 0 && !EX) {
-#endif
       for (int n = 0, g = 0; n < my_units; ++n) {
       int kb, ke, ut, part;
       unit(n, m0, l0, kb, ke, ut, part);
       const int lh = l0 + rank * 128, lh2 = l0 + 256 + rank * (N2 / 2);
       for (int i = kb; i < ke; ++i, ++g) {
-        const int a = g % NA;
-        mbar_wait(&a_empty[a].b, ((g / NA) & 1) ^ 1);
-#ifdef LORS_ACT_2LANE
-        if (lane == 0) {
-          mbar_arrive_expect_tx(&mready[a].b, ACT_BYTES);
-          tma_load_2d(actb + a * ACT_BYTES, &tmAct, &mready[a].b, i * BK, lh);
-        } else {
-          tma_load_2d(actb + a * ACT_BYTES + ACT1_BYTES, &tmAct2, &mready[a].b, i * BK, lh2);
-        }
-#else
-        mbar_arrive_expect_tx(&mready[a].b, ACT_BYTES);
-        tma_load_2d(actb + a * ACT_BYTES, &tmAct, &mready[a].b, i * BK, lh);
-        if (N2) tma_load_2d(actb + a * ACT_BYTES + ACT1_BYTES, &tmAct2, &mready[a].b, i * BK, lh2);
-#endif
+        const int a = g % NACT;
+        mbar_wait(&a_empty[a].b, ((g / NACT) & 1) ^ 1);
+        mbar_arrive_expect_tx(&afull[a].b, ACT_BYTES);
+        tma_load_2d(actb + a * ACT_BYTES, &tmAct, &afull[a].b, i * BK, lh);
+        if (N2) tma_load_2d(actb + a * ACT_BYTES + ACT1_BYTES, &tmAct2, &afull[a].b, i * BK, lh2);
       }
       }
     }
@@ -1047,9 +1046,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         total += ke - kb;
       }
       for (int g = 0; g < total; ++g) {
-        const int a = g % NA;
-        mbar_wait(&mready[a].b, (g / NA) & 1);
-        mbar_arrive_cluster(mready_l + a * 16);
+        const int a = g % NACT;
+        mbar_wait(&afull[a].b, (g / NACT) & 1);
+        mbar_arrive_cluster(afull_l + a * 16);
       }
     }
   } else if (warp == W_MMA) {
@@ -1116,23 +1115,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           unit(mn, m_, l_, kb_, ke_, ut_, pt_);
           main_n2 = l_ + 256 < n_tok;
         }
-        const int a = jm % NA;
-        mbar_wait(&mready[a].b, (jm / NA) & 1);
+        const int a = jm % NACT, wb = jm % NA;
+        mbar_wait(&afull[a].b, (jm / NACT) & 1);     // activation halves of both CTAs landed
+        mbar_wait(&wready[wb].b, (jm / NA) & 1);     // W_eff tiles of both CTAs written
         tc_fence_after();
         if (elect_one()) {
-          const uint64_t ad = weff_desc + (uint64_t)(a * (WEFF_BYTES >> 4));
+          const uint64_t ad = weff_desc + (uint64_t)(wb * (WEFF_BYTES >> 4));
           const uint64_t bd = act_desc + (uint64_t)(a * (ACT_BYTES >> 4));
           if (SP) {
             // two K = 32 sparse MMAs: compressed A advances 32 B, B 64 B, metadata one column each
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh)
-              mma_bf16_pair_sp(tmem, ad + hh * 2, bd + hh * 4, tmem + E_COL + a * 8 + hh * 4, idesc_sp,
+              mma_bf16_pair_sp(tmem, ad + hh * 2, bd + hh * 4, tmem + E_COL + wb * 8 + hh * 4, idesc_sp,
                                (mk > 0 || hh > 0) ? 1u : 0u);
             if (N2 && main_n2) {  // tokens 256 .. 256 + N2 into the second accumulator, same A and metadata
               const uint64_t bd2 = bd + (ACT1_BYTES >> 4);
 #pragma unroll
               for (int hh = 0; hh < 2; ++hh)
-                mma_bf16_pair_sp(tmem + 256, ad + hh * 2, bd2 + hh * 4, tmem + E_COL + a * 8 + hh * 4, idesc_sp_n2,
+                mma_bf16_pair_sp(tmem + 256, ad + hh * 2, bd2 + hh * 4, tmem + E_COL + wb * 8 + hh * 4, idesc_sp_n2,
                                  (mk > 0 || hh > 0) ? 1u : 0u);
             }
           } else {
@@ -1147,7 +1147,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
             }
           }
           mma_commit_pair(&a_empty[a].b, 0x3);
-          mma_commit_pair(&wempty[((jm + NA) % NGRP) * NA + a].b, 0x3);   // next writer's group
+          mma_commit_pair(&wempty[((jm + NA) % NGRP) * NA + wb].b, 0x3);   // next writer's group
           if (mk == mlen - 1) mma_commit_pair(accf, 0x3);
         }
         __syncwarp();
@@ -1394,7 +1394,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       }
       if (lane == 0) {
         mbar_arrive(&wfree[wi].b);                   // done reading the W tile
-        mbar_arrive_cluster(mready_l + wb * 16);     // W_eff half ready for the pair MMA
+        mbar_arrive_cluster(wready_l + wb * 16);     // W_eff half ready for the pair MMA
       }
     };
     // Accumulator -> bf16 -> transposed staging: the accumulator is read in the MMA
