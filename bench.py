@@ -104,21 +104,27 @@ class ClockSampler:
         except Exception as exc:  # noqa: BLE001
             print(f"[bench] NVML unavailable: {exc}", file=sys.stderr)
 
+    def sample(self):
+        """One NVML sample (SM clock + active clock-event reasons)."""
+        if self.nvml is None:
+            return
+        nv, h = self.nvml
+        try:
+            self.samples.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+            mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            for name, attr in self.REASONS:
+                if mask & getattr(nv, attr, 0):
+                    self.reasons.add(name)
+        except Exception:  # noqa: BLE001
+            pass
+
     def sample_until(self, event, min_samples=3):
         """Poll every ~2 ms until `event` (recorded after the timed region) completes."""
         if self.nvml is None:
             return
-        nv, h = self.nvml
         while True:
             done = event.query()
-            try:
-                self.samples.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
-                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                for name, attr in self.REASONS:
-                    if mask & getattr(nv, attr, 0):
-                        self.reasons.add(name)
-            except Exception:  # noqa: BLE001
-                pass
+            self.sample()
             if done:
                 return
             time.sleep(0.002)
@@ -701,6 +707,8 @@ def run_decoder(args):
         for s in range(steps):
             if s >= 2:   # bounded run-ahead: the host waits for step s - 2 (as a loop logging its loss would)
                 done[s % 2].synchronize()
+                if clocks:
+                    clocks.sample()   # the GPU is one to two steps ahead here: a sample under load
             loss = trainer.step(toks[warmup + s])
             done[s % 2].record(stream)
         e1.record(stream)
