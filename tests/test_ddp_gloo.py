@@ -62,3 +62,43 @@ def test_adapter_grad_average_world2(overlap, bucket_bytes):
     # broadcast made the adapters identical
     for a, b in zip(res[0][2], res[1][2]):
         assert torch.equal(torch.tensor(a), torch.tensor(b))
+
+
+def _accum_worker(rank, world, port, overlap, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2501_08582_b200.ddp import AdapterGradReducer
+        params = [nn.Parameter(torch.zeros(37, 5)), nn.Parameter(torch.zeros(5, 29)), nn.Parameter(torch.zeros(37))]
+        red = AdapterGradReducer(params, bucket_bytes=64, overlap=overlap)
+        for micro in range(2):   # gradient accumulation: two backward passes, one finish()
+            loss = sum(((rank + 1) * (micro + 1) * (i + 1) * p).sum() for i, p in enumerate(params))
+            loss.backward()
+        red.finish()
+        q.put((rank, [p.grad.clone().tolist() for p in params]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+def test_reducer_gradient_accumulation_world2(overlap):
+    """Two backward passes before finish(): the buckets the first pass launched from its hooks are
+    reduced again from the accumulated .grad, so every rank ends with the average over ranks of
+    the summed micro-batch gradients (ddp.py, AdapterGradReducer._stale)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_accum_worker, args=(r, world, port, overlap, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # grad of param i = mean_r (r+1) * (1 + 2) * (i+1) = 1.5 * 3 * (i+1)
+    for _, grads in res:
+        for i, g in enumerate(grads):
+            t = torch.tensor(g)
+            assert torch.allclose(t, torch.full_like(t, 4.5 * (i + 1)))

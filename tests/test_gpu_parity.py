@@ -365,6 +365,32 @@ def test_init_gradient_svd_two_layer_probe(P, masked):
         assert abs(d["projection_residual"] - d["singular_tail"]) <= 1e-3 * max(1.0, d["grad_norm"])
 
 
+def test_init_gradient_svd_on_grouped_decoder(P):
+    """The decoder runs q/k/v and gate/up as grouped autograd nodes (module.lors_group), which bypass
+    the per-layer forward hooks; init_gradient_svd turns grouping off for its probe, so every one of
+    the 7 projections per layer gets b = its top-r right singular vectors (orthonormal rows, first
+    nonzero entry >= 0, svd.py:155-161) and a = 0 (initialization.py:171-232)."""
+    from paper_2501_08582_b200 import decoder as D
+    from paper_2501_08582_b200.init import init_gradient_svd
+    from paper_2501_08582_b200.module import groupable
+    from paper_2501_08582_b200.trainer import synthetic_tokens
+    cfg = D.preset("tiny")
+    model = D.LoRSDecoder(cfg, device="cuda", seed=0)
+    layer0 = model.layers[0].proj
+    assert groupable([layer0["q"], layer0["k"], layer0["v"]])
+    toks = synthetic_tokens(cfg.vocab, cfg.batch, cfg.seq, 0, device="cuda")
+    before = [p.b.detach().clone() for p in model.projections()]
+    init_gradient_svd(list(model.projections()), lambda: model.loss(toks).backward())
+    for proj, b0 in zip(model.projections(), before):
+        b = proj.b.detach().double()
+        assert not torch.equal(proj.b.detach(), b0)
+        assert float(proj.a.abs().sum()) == 0.0
+        gram = b @ b.t()
+        assert torch.allclose(gram, torch.eye(cfg.rank, dtype=torch.float64, device="cuda"), atol=1e-4)
+        first = b.gather(1, (b != 0).to(torch.int8).argmax(dim=1, keepdim=True))
+        assert bool((first >= 0).all())
+
+
 # ---------------------------------------------------------------------------
 # 2:4 sparse-tensor-core forward (north_star 4)
 # ---------------------------------------------------------------------------
