@@ -36,6 +36,22 @@
 #include "lors_tc.cuh"
 #include "ptx_sm100.cuh"
 
+#ifdef LORS_TRACE
+// timeline experiment (tools/trace_k1.py): globaltimer stamps of pipeline events of the first CTA
+// pair, per flat k-step g < 512: g_lors_trace[(cta * 16 + event) * 512 + g]
+__device__ unsigned long long g_lors_trace[2 * 24 * 512];
+extern "C" int lors_trace_read(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_lors_trace, sizeof(unsigned long long) * 2 * 24 * 512);
+}
+#define LORS_TR(ev, g)                                                                          \
+  do {                                                                                         \
+    if (blockIdx.x < 2 && (g) < 512) g_lors_trace[(blockIdx.x * 24 + (ev)) * 512 + (g)] = clock64(); \
+  } while (0)
+#else
+#define LORS_TR(ev, g) \
+  do {                 \
+  } while (0)
+#endif
 #ifdef LORS_DEBUG_HANG
 extern "C" int lors_debug_hang_info(unsigned int* out) {
   return (int)cudaMemcpyFromSymbol(out, lors::ptx::g_lors_hang, sizeof(unsigned int) * 64);
@@ -714,6 +730,7 @@ constexpr int BM = 128, BN = 256, BK = 64;
 #ifndef LORS_PERSIST
 #define LORS_PERSIST 1
 #endif
+
 // Persistent kernels (dense-masked and 2:4): one CTA pair per SM pair walks its
 // tiles; the producers and the recompute run ahead into the next tile while the
 // epilogue drains the accumulator through the (then idle) W_eff ring.
@@ -752,11 +769,20 @@ constexpr int na() { return SP ? (LORS_PERSIST ? 3 : 4) : 3; }  // W_eff buffers
 // slot.  4 slots (with a 3-deep W ring to fit 227 KB) measured no faster than 3 (tools/ab_gemm.py)
 template <bool SP>
 constexpr int nact() { return LORS_PERSIST ? LORS_NACT : na<SP>(); }
-// recompute lookahead: recompute(j) is issued before main(j - 1), so the transform of
-// step j overlaps the tensor-core work of step j - 1 (one buffer suffices: the
-// transform releases it right after its TMEM load)
+// recompute lookahead D: recompute(j) is issued with main(j - D), so (tcgen05 ops run in
+// issue order) it completes right after main(j - D - 1) and the transform of step j has D
+// main MMAs to finish before main(j) is due.  tools/trace_k1.py measured the chain
+// main(j - 2) done -> recompute(j) -> transform(j) -> issuer sees it -> main(j) at ~1200
+// cycles against ~900 for one step's MMAs, so D = 1 left the tensor pipe idle ~25% of the
+// time; D = 2 (dense: NE = 2) hides it.
+#ifndef LORS_LOOKAHEAD
+#define LORS_LOOKAHEAD 2
+#endif
+// (at most NE: recompute(j) waits for the transform of j - NE to release its buffer; with a
+// larger lookahead that transform could sit behind the previous tile's epilogue, whose
+// accumulator waits for a main MMA the issuer has not issued yet)
 template <bool SP>
-constexpr int lookahead() { return 1; }
+constexpr int lookahead() { return LORS_LOOKAHEAD < ne<SP>() ? LORS_LOOKAHEAD : ne<SP>(); }
 // 2:4 index nibble (idx0 | idx1 << 2, idx0 < idx1) for each 4-bit keep mask;
 // groups with fewer than two kept entries are padded with zero-valued slots,
 // masks with more than two are not 2:4 (prune.py:72-77) and never reach here.
@@ -1004,6 +1030,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       for (int i = kb; i < ke; ++i, ++g) {
         const int wi = g % NW;
         mbar_wait(&wfree[wi].b, ((g / NW) & 1) ^ 1);
+        LORS_TR(8, g);
         uint8_t* st = wring + wi * W_BYTES;
         const int k0 = i * BK;
         uint64_t* wf = &wfull[(g % NGRP) * NW + wi].b;   // the set of the group that reads step g
@@ -1028,7 +1055,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       for (int i = kb; i < ke; ++i, ++g) {
         const int a = g % NACT;
         mbar_wait(&a_empty[a].b, ((g / NACT) & 1) ^ 1);
-        mbar_arrive_expect_tx(&afull[a].b, ACT_BYTES);
+        LORS_TR(7, g);
+        mbar_arrive_expect_tx(&afull[a].b, ACT_BYTES);   // both halves' bytes
         tma_load_2d(actb + a * ACT_BYTES, &tmAct, &afull[a].b, i * BK, lh);
         if (N2) tma_load_2d(actb + a * ACT_BYTES + ACT1_BYTES, &tmAct2, &afull[a].b, i * BK, lh2);
       }
@@ -1092,8 +1120,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           mbar_wait(pffull, rn & 1);
         }
         const int e = j % NE, sl = j % NS;
+        LORS_TR(0, j);
         mbar_wait(&sready[sl].b, (j / NS) & 1);      // factor slice of step j landed in both CTAs
+        LORS_TR(1, j);
         mbar_wait(&refree[e].b, (j / NE) & 1);       // recompute buffer e read by the transform of j - NE
+        LORS_TR(2, j);
         tc_fence_after();
         if (elect_one()) {
           const uint64_t sfd = sf_desc + (uint64_t)(sl * (SF >> 4));
@@ -1101,13 +1132,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           for (int kk = 0; kk < RP / 16; ++kk)
             mma_bf16_pair(tmem + RE_COL + e * 64, ff_desc + kk * FF_KSTEP, sfd + kk * SF_KSTEP, idesc_re,
                           kk > 0 ? 1u : 0u);
+          LORS_TR(14, j);
           mma_commit_pair(&refull[(j % NGRP) * NE + e].b, 0x3);
           mma_commit_pair(&s_empty[sl].b, 0x3);
           if (PERSIST && rk == rlen - 1) mma_commit_pair(ff_empty, 0x3);   // fixed factor may be replaced
+          LORS_TR(15, j);
         }
         __syncwarp();
+        LORS_TR(16, j);
       };
       bool main_n2 = true;   // the second MMA's tokens (l0 + 256 ..) hold valid rows in this unit
+      // the main MMAs of step jm (activation slot a, W_eff buffer wb) and the commits that free
+      // both slots; called from the elected lane
+      auto main_mmas = [&](const int jm, const int mk, const int a, const int wb) {
+        const uint64_t ad = weff_desc + (uint64_t)(wb * (WEFF_BYTES >> 4));
+        const uint64_t bd = act_desc + (uint64_t)(a * (ACT_BYTES >> 4));
+        if (SP) {
+          // two K = 32 sparse MMAs: compressed A advances 32 B, B 64 B, metadata one column each
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+            mma_bf16_pair_sp(tmem, ad + hh * 2, bd + hh * 4, tmem + E_COL + wb * 8 + hh * 4, idesc_sp,
+                             (mk > 0 || hh > 0) ? 1u : 0u);
+          if (N2 && main_n2) {  // tokens 256 .. 256 + N2 into the second accumulator, same A and metadata
+            const uint64_t bd2 = bd + (ACT1_BYTES >> 4);
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+              mma_bf16_pair_sp(tmem + 256, ad + hh * 2, bd2 + hh * 4, tmem + E_COL + wb * 8 + hh * 4, idesc_sp_n2,
+                               (mk > 0 || hh > 0) ? 1u : 0u);
+          }
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            mma_bf16_pair(tmem, ad + kk * 2, bd + kk * 2, idesc_main, (mk > 0 || kk > 0) ? 1u : 0u);
+          if (N2 && main_n2) {  // tokens 256 .. 256 + N2 into the second accumulator
+            const uint64_t bd2 = bd + (ACT1_BYTES >> 4);
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              mma_bf16_pair(tmem + 256, ad + kk * 2, bd2 + kk * 2, idesc_n2, (mk > 0 || kk > 0) ? 1u : 0u);
+          }
+        }
+        mma_commit_pair(&a_empty[a].b, 0x3);
+        mma_commit_pair(&wempty[((jm + NA) % NGRP) * NA + wb].b, 0x3);   // next writer's group
+      };
       auto do_main = [&](const int jm, const int mk, const int mn, const int mlen) {
         if (PERSIST && mk == 0 && mn > 0) mbar_wait(acc_empty, (mn - 1) & 1);  // previous tile drained
         if (N2 && mk == 0) {   // a ragged last token tile: skip the all-padding N2 MMA (a third of it)
@@ -1116,41 +1182,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           main_n2 = l_ + 256 < n_tok;
         }
         const int a = jm % NACT, wb = jm % NA;
+        LORS_TR(3, jm);
         mbar_wait(&afull[a].b, (jm / NACT) & 1);     // activation halves of both CTAs landed
+        LORS_TR(4, jm);
         mbar_wait(&wready[wb].b, (jm / NA) & 1);     // W_eff tiles of both CTAs written
+        LORS_TR(5, jm);
         tc_fence_after();
         if (elect_one()) {
-          const uint64_t ad = weff_desc + (uint64_t)(wb * (WEFF_BYTES >> 4));
-          const uint64_t bd = act_desc + (uint64_t)(a * (ACT_BYTES >> 4));
-          if (SP) {
-            // two K = 32 sparse MMAs: compressed A advances 32 B, B 64 B, metadata one column each
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh)
-              mma_bf16_pair_sp(tmem, ad + hh * 2, bd + hh * 4, tmem + E_COL + wb * 8 + hh * 4, idesc_sp,
-                               (mk > 0 || hh > 0) ? 1u : 0u);
-            if (N2 && main_n2) {  // tokens 256 .. 256 + N2 into the second accumulator, same A and metadata
-              const uint64_t bd2 = bd + (ACT1_BYTES >> 4);
-#pragma unroll
-              for (int hh = 0; hh < 2; ++hh)
-                mma_bf16_pair_sp(tmem + 256, ad + hh * 2, bd2 + hh * 4, tmem + E_COL + wb * 8 + hh * 4, idesc_sp_n2,
-                                 (mk > 0 || hh > 0) ? 1u : 0u);
-            }
-          } else {
-#pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk)
-              mma_bf16_pair(tmem, ad + kk * 2, bd + kk * 2, idesc_main, (mk > 0 || kk > 0) ? 1u : 0u);
-            if (N2 && main_n2) {  // tokens 256 .. 256 + N2 into the second accumulator
-              const uint64_t bd2 = bd + (ACT1_BYTES >> 4);
-#pragma unroll
-              for (int kk = 0; kk < BK / 16; ++kk)
-                mma_bf16_pair(tmem + 256, ad + kk * 2, bd2 + kk * 2, idesc_n2, (mk > 0 || kk > 0) ? 1u : 0u);
-            }
-          }
-          mma_commit_pair(&a_empty[a].b, 0x3);
-          mma_commit_pair(&wempty[((jm + NA) % NGRP) * NA + wb].b, 0x3);   // next writer's group
+          main_mmas(jm, mk, a, wb);
           if (mk == mlen - 1) mma_commit_pair(accf, 0x3);
         }
         __syncwarp();
+        LORS_TR(6, jm);
       };
       // Flat schedule over this CTA pair's tiles: the recompute of step j runs D
       // steps ahead of its main MMA and into the next tile.  At a tile boundary
@@ -1168,6 +1211,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       for (int j = 0; j < total + (EX ? 0 : D); ++j) {
         const bool has_rec = j < total, has_main = !EX && j >= D;
         const bool flip = has_rec && rk == 0 && j > 0;
+        if (!SP && has_rec && has_main && rk != 0 && mk != 0) {
+          // steady state (no tile boundary on either side): all four barriers of rec(j) and
+          // main(j - D) probed at once, then both issued from one elected lane -- each barrier
+          // probe costs ~100 cycles and each elect / __syncwarp region ~150, and this loop paces
+          // the pipeline (tools/trace_k1.py: 1570 -> ~1030 cycles a k-step at cfg3).  (The 2:4
+          // kernel, one recompute buffer and D = 1, keeps the two-phase path below: there the
+          // recompute must not wait for the main MMA's barriers.)
+          const int jm = j - D, e = j % NE, sl = j % NS, a = jm % NACT, wb = jm % NA;
+          LORS_TR(0, j);
+          mbar_wait4(&sready[sl].b, (j / NS) & 1, &refree[e].b, (j / NE) & 1, &afull[a].b, (jm / NACT) & 1,
+                     &wready[wb].b, (jm / NA) & 1);
+          LORS_TR(5, jm);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t sfd = sf_desc + (uint64_t)(sl * (SF >> 4));
+#pragma unroll
+            for (int kk = 0; kk < RP / 16; ++kk)
+              mma_bf16_pair(tmem + RE_COL + e * 64, ff_desc + kk * FF_KSTEP, sfd + kk * SF_KSTEP, idesc_re,
+                            kk > 0 ? 1u : 0u);
+            mma_commit_pair(&refull[(j % NGRP) * NE + e].b, 0x3);
+            mma_commit_pair(&s_empty[sl].b, 0x3);
+            if (PERSIST && rk == rlen - 1) mma_commit_pair(ff_empty, 0x3);   // fixed factor may be replaced
+            main_mmas(jm, mk, a, wb);
+            if (mk == mlen - 1) mma_commit_pair(accf, 0x3);
+          }
+          __syncwarp();
+          LORS_TR(6, jm);
+          if (++rk == rlen) { rk = 0; if (++rn < my_units) rlen = unit_len(rn); }
+          if (++mk == mlen) { mk = 0; if (++mn < my_units) mlen = unit_len(mn); }
+          continue;
+        }
         if (flip && has_main) {
           do_main(j - D, mk, mn, mlen);
           if (++mk == mlen) { mk = 0; if (++mn < my_units) mlen = unit_len(mn); }
@@ -1203,7 +1277,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
                        : 0x44444444u;
       // 1. rank-r product of this k-step (TMEM -> registers), then release the buffer
       const int rb = i % NE;
+      if (warp == 0 && lane == 0) LORS_TR(9, i);
       mbar_wait(&refull[(i % NGRP) * NE + rb].b, (i / RE_PERIOD) & 1);
+      if (warp == 0 && lane == 0) LORS_TR(10, i);
       tc_fence_after();
       const uint32_t re_col = RE_COL + rb * 64 + h * 32;
       if (!DX) {
@@ -1218,6 +1294,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       //    result is needed, so their latency overlaps the TMEM load's
       const int wi = i % NW;
       mbar_wait(&wfull[(i % NGRP) * NW + wi].b, (i / W_PERIOD) & 1);
+      if (warp == 0 && lane == 0) LORS_TR(11, i);
       const uint32_t wt = smem_u32(wring + wi * W_BYTES);
       if (!DX) {
         // thread = W row t; chunks 4h .. 4h+3 of 8 k-values (SW128)
@@ -1252,6 +1329,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       // 3. destination buffer drained by the MMA of step i - NA
       // waits for the commit of main(i - NA), the previous user of this buffer
       if (!EX && i >= NA) mbar_wait(&wempty[(i % NGRP) * NA + wb].b, ((i - NA) / A_PERIOD) & 1);
+      if (warp == 0 && lane == 0) LORS_TR(12, i);
       const uint32_t dst = smem_u32(weff + wb * WEFF_BYTES);
       if (SP && meta24 != nullptr) {
         // 2:4 with precomputed index nibbles: weff_pair on the group's four
@@ -1395,6 +1473,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       if (lane == 0) {
         mbar_arrive(&wfree[wi].b);                   // done reading the W tile
         mbar_arrive_cluster(wready_l + wb * 16);     // W_eff half ready for the pair MMA
+        if (warp == 0) LORS_TR(13, i);
       }
     };
     // Accumulator -> bf16 -> transposed staging: the accumulator is read in the MMA

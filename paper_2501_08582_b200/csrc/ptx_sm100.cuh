@@ -108,6 +108,32 @@ __device__ __forceinline__ void mbar_wait_impl(uint64_t* bar, uint32_t parity) {
   }
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_wait_impl<false>(bar, parity); }
+// Four barriers at once: one non-blocking test of each, issued back to back so their
+// latencies overlap (a probe costs ~100 cycles, tools/trace_k1.py); the barriers not yet
+// complete are then waited for one by one.
+__device__ __forceinline__ void mbar_wait4(uint64_t* b0, uint32_t p0, uint64_t* b1, uint32_t p1, uint64_t* b2,
+                                           uint32_t p2, uint64_t* b3, uint32_t p3) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred q0, q1, q2, q3;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 q0, [%1], %2;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 q1, [%3], %4;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 q2, [%5], %6;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 q3, [%7], %8;\n\t"
+      "and.pred q0, q0, q1;\n\t"
+      "and.pred q2, q2, q3;\n\t"
+      "and.pred q0, q0, q2;\n\t"
+      "selp.u32 %0, 1, 0, q0;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(b0)), "r"(p0), "r"(smem_u32(b1)), "r"(p1), "r"(smem_u32(b2)), "r"(p2), "r"(smem_u32(b3)),
+        "r"(p3)
+      : "memory");
+  if (ok) return;
+  mbar_wait(b0, p0);
+  mbar_wait(b1, p1);
+  mbar_wait(b2, p2);
+  mbar_wait(b3, p3);
+}
 // wait on a barrier that receives arrives from the peer CTA (cluster-scope acquire)
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) { mbar_wait_impl<true>(bar, parity); }
 

@@ -1,0 +1,10 @@
+E=$PWD/paper_2501_08582_b200/_native/exp
+LORS_B200_LIB=$E/la2f/liblors_b200.so timeout 600 python -m pytest tests/test_weff_identity.py -q -m gpu -x > gpurun_out/la2f_id.log 2>&1; tail -n 1 gpurun_out/la2f_id.log
+LORS_B200_LIB=$E/trace2/liblors_b200.so python tools/trace_k1.py > gpurun_out/trace7.log 2>&1; head -4 gpurun_out/trace7.log; grep -A4 "CTA 0 trans" gpurun_out/trace7.log
+LORS_B200_LIB=$E/trace2/liblors_b200.so python tools/trace_k1.py 8192 11008 4096 64 > gpurun_out/trace8.log 2>&1; head -4 gpurun_out/trace8.log
+for i in 1 2; do
+  for v in default la2f roles5; do
+    if [ $v = default ]; then python tools/ab_gemm.py "cfg" >> gpurun_out/ab14.log 2>&1; else LORS_B200_LIB=$E/$v/liblors_b200.so timeout 300 python tools/ab_gemm.py "cfg" >> gpurun_out/ab14.log 2>&1; fi
+  done
+done
+python tools/ab_table.py gpurun_out/ab14.log

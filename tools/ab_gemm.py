@@ -8,6 +8,8 @@ back-to-back launches for ~0.3 s (power-capped clocks, as inside a training step
 import os
 import statistics
 import sys
+import threading
+import time
 
 import torch
 
@@ -39,6 +41,21 @@ def iso(fn, n=15):
     return statistics.median(ts)
 
 
+CLK = []
+
+
+def _clock_thread(stop, out):
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(0)
+        while not stop.is_set():
+            out.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+            time.sleep(0.005)
+    except Exception:  # noqa: BLE001
+        pass
+
+
 def sus(fn, seconds=0.3):
     fn()
     torch.cuda.synchronize()
@@ -48,11 +65,17 @@ def sus(fn, seconds=0.3):
     e1.record()
     torch.cuda.synchronize()
     n = max(5, int(seconds / (e0.elapsed_time(e1) * 1e-3)))
+    clk, stop = [], threading.Event()
+    th = threading.Thread(target=_clock_thread, args=(stop, clk))
     e0.record()
     for _ in range(n):
         fn()
     e1.record()
+    th.start()
     torch.cuda.synchronize()
+    stop.set()
+    th.join()
+    CLK.append(statistics.median(clk) if clk else 0)
     return e0.elapsed_time(e1) * 1e3 / n
 
 
@@ -79,5 +102,8 @@ for name, L, R, C, r, pat in SHAPES:
         sp = lambda: ops.lors_fwd(x, w, a, b, 2.0, sparse24=True, meta24=meta)  # noqa: E731
         res["sp24"] = (iso(sp), sus(sp))
     fl = 2 * L * R * C
+    if os.environ.get("AB_CLOCKS"):
+        print(f"[{lib}] {name:13s} clocks (MHz, median while the sus loops ran): " +
+              " ".join(f"{k} {c:.0f}" for k, c in zip(res, CLK[-len(res):])), flush=True)
     print(f"[{lib}] {name:13s} " + "  ".join(f"{k} iso {v[0]:7.1f} sus {v[1]:7.1f} us ({fl / v[1] / 1e6:5.0f} TF/s)"
                                             for k, v in res.items()), flush=True)

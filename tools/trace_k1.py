@@ -1,0 +1,59 @@
+"""Timeline of the K1 pipeline (library built with -DLORS_TRACE, tools/build_variant.py trace):
+globaltimer stamps per flat k-step of the first CTA pair, summarised as mean nanoseconds per k-step.
+    LORS_B200_LIB=.../exp/trace/liblors_b200.so python tools/trace_k1.py [L R C r]"""
+import ctypes as ct
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2501_08582_b200 import _native, ops, prune  # noqa: E402
+
+L, R, C, r = (int(v) for v in sys.argv[1:5]) if len(sys.argv) > 4 else (4096, 11008, 4096, 16)
+g = torch.Generator(device="cuda").manual_seed(0)
+w = prune.prune_rowwise(torch.randn(R, C, device="cuda", generator=g) * 0.02, 0.5).bfloat16()
+a = (torch.randn(R, r, device="cuda", generator=g) * 1e-3).bfloat16()
+b = (torch.randn(r, C, device="cuda", generator=g) / r ** 0.5).bfloat16()
+x = torch.randn(L, C, device="cuda", generator=g).bfloat16()
+for _ in range(3):
+    ops.lors_fwd(x, w, a, b, 2.0)
+torch.cuda.synchronize()
+buf = (ct.c_ulonglong * (2 * 24 * 512))()
+lib = _native.load()
+lib.lors_trace_read(buf)
+t = np.frombuffer(buf, dtype=np.uint64).reshape(2, 24, 512).astype(np.int64)
+names = {0: "iss: rec start", 1: "iss: sready ok", 2: "iss: refree ok", 3: "iss: main start", 4: "iss: afull ok",
+         5: "iss: wready ok", 6: "iss: main issued", 7: "act: slot free", 8: "W: slot free", 9: "xf: start",
+         10: "xf: refull ok", 11: "xf: W landed", 12: "xf: wempty ok", 13: "xf: arrived"}
+lo, hi = 70, 300
+print("(SM cycles, clock64)")
+j = np.arange(lo, hi)
+T = lambda cta, ev, idx: t[cta, ev, idx]  # noqa: E731
+it = T(0, 0, j + 1) - T(0, 0, j)
+print(f"issuer iteration (rec(j) + main(j-1)): mean {it.mean():.0f} median {np.median(it):.0f}")
+d = T(0, 5, j - 1) - T(0, 0, j)
+print(f"  fast path: 4 barriers (rec j, main j-1) mean {d.mean():.0f} median {np.median(d):.0f}")
+d = T(0, 6, j - 1) - T(0, 5, j - 1)
+print(f"  fast path: issue rec + main + commits   mean {d.mean():.0f} median {np.median(d):.0f}")
+parts = [("wait sready", T(0, 1, j) - T(0, 0, j)), ("wait refree", T(0, 2, j) - T(0, 1, j)),
+         ("issue rec MMA", T(0, 14, j) - T(0, 2, j)), ("rec commits", T(0, 15, j) - T(0, 14, j)),
+         ("syncwarp", T(0, 16, j) - T(0, 15, j)), ("gap -> main", T(0, 3, j - 1) - T(0, 16, j)),
+         ("wait afull", T(0, 4, j - 1) - T(0, 3, j - 1)), ("wait wready", T(0, 5, j - 1) - T(0, 4, j - 1)),
+         ("issue 8 MMAs + commits", T(0, 6, j - 1) - T(0, 5, j - 1)), ("gap -> next rec", T(0, 0, j + 1) - T(0, 6, j - 1))]
+for lbl, d in parts:
+    print(f"  {lbl:24s} mean {d.mean():7.0f}  median {np.median(d):7.0f}")
+for cta in (0, 1):
+    per = np.diff(t[cta, 13, lo:hi])
+    print(f"CTA {cta} transform period mean {per.mean():.0f}")
+    for a_, b_, lbl in ((9, 10, "xf wait refull"), (10, 11, "xf tmem ld + W wait"), (11, 12, "xf wait wempty"),
+                        (12, 13, "xf compute + store + arrive")):
+        d = t[cta, b_, lo:hi] - t[cta, a_, lo:hi]
+        print(f"  {lbl:28s} mean {d.mean():7.0f}  median {np.median(d):7.0f}")
+d = T(0, 5, j) - T(0, 13, j)
+print(f"issuer wready ok - CTA0 warp0 arrived: mean {d.mean():.0f}")
+d = T(0, 10, j) - T(0, 2, j)
+print(f"xf refull ok - rec issue (rec queue + exec + signal): mean {d.mean():.0f}")
+d = T(0, 4, j) - T(0, 7, j)
+print(f"afull ok - act slot free: mean {d.mean():.0f}")
