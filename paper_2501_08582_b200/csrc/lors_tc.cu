@@ -759,8 +759,11 @@ template <bool SP>
 constexpr int ns() { return SP ? 3 : 2; }
 template <bool SP>
 constexpr int nw() { return SP ? (LORS_PERSIST ? LORS_NW_SP : 6) : LORS_NW_DENSE; }  // W ring
+#ifndef LORS_NA_SP
+#define LORS_NA_SP 3
+#endif
 template <bool SP>
-constexpr int na() { return SP ? (LORS_PERSIST ? 3 : 4) : 3; }  // W_eff buffers
+constexpr int na() { return SP ? (LORS_PERSIST ? LORS_NA_SP : 4) : 3; }  // W_eff buffers
 #ifndef LORS_NACT
 #define LORS_NACT 3
 #endif
@@ -778,11 +781,11 @@ constexpr int nact() { return LORS_PERSIST ? LORS_NACT : na<SP>(); }
 #ifndef LORS_LOOKAHEAD
 #define LORS_LOOKAHEAD 2
 #endif
-// (at most NE: recompute(j) waits for the transform of j - NE to release its buffer; with a
-// larger lookahead that transform could sit behind the previous tile's epilogue, whose
-// accumulator waits for a main MMA the issuer has not issued yet)
+// (recompute(j) waits for the transform of j - NE to release its buffer; in the first D
+// steps of a tile that transform may sit behind the previous tile's epilogue, so there the
+// issuer puts the previous tile's pending main MMAs first, see `flip`)
 template <bool SP>
-constexpr int lookahead() { return LORS_LOOKAHEAD < ne<SP>() ? LORS_LOOKAHEAD : ne<SP>(); }
+constexpr int lookahead() { return LORS_LOOKAHEAD; }
 // 2:4 index nibble (idx0 | idx1 << 2, idx0 < idx1) for each 4-bit keep mask;
 // groups with fewer than two kept entries are padded with zero-valued slots,
 // masks with more than two are not 2:4 (prune.py:72-77) and never reach here.
@@ -1121,9 +1124,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         }
         const int e = j % NE, sl = j % NS;
         LORS_TR(0, j);
-        mbar_wait(&sready[sl].b, (j / NS) & 1);      // factor slice of step j landed in both CTAs
-        LORS_TR(1, j);
-        mbar_wait(&refree[e].b, (j / NE) & 1);       // recompute buffer e read by the transform of j - NE
+        // factor slice of step j landed in both CTAs; recompute buffer e read by the transform of j - NE
+        mbar_wait2(&sready[sl].b, (j / NS) & 1, &refree[e].b, (j / NE) & 1);
         LORS_TR(2, j);
         tc_fence_after();
         if (elect_one()) {
@@ -1183,9 +1185,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         }
         const int a = jm % NACT, wb = jm % NA;
         LORS_TR(3, jm);
-        mbar_wait(&afull[a].b, (jm / NACT) & 1);     // activation halves of both CTAs landed
-        LORS_TR(4, jm);
-        mbar_wait(&wready[wb].b, (jm / NA) & 1);     // W_eff tiles of both CTAs written
+        // activation halves of both CTAs landed; W_eff tiles of both CTAs written
+        mbar_wait2(&afull[a].b, (jm / NACT) & 1, &wready[wb].b, (jm / NA) & 1);
         LORS_TR(5, jm);
         tc_fence_after();
         if (elect_one()) {
@@ -1210,14 +1211,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       int rlen = my_units > 0 ? unit_len(0) : 1, mlen = rlen;
       for (int j = 0; j < total + (EX ? 0 : D); ++j) {
         const bool has_rec = j < total, has_main = !EX && j >= D;
-        const bool flip = has_rec && rk == 0 && j > 0;
-        if (!SP && has_rec && has_main && rk != 0 && mk != 0) {
+        // the first D steps of a tile: the previous tile's main MMA goes first (its accumulator
+        // must be complete before the transform warps, after their epilogue, release the
+        // recompute buffers of the new tile; and the new tile's first recompute waits for its
+        // fixed factor)
+        const bool flip = has_rec && rk < D && j > 0;
+        if (has_rec && has_main && rk >= D && mk != 0) {
           // steady state (no tile boundary on either side): all four barriers of rec(j) and
           // main(j - D) probed at once, then both issued from one elected lane -- each barrier
           // probe costs ~100 cycles and each elect / __syncwarp region ~150, and this loop paces
-          // the pipeline (tools/trace_k1.py: 1570 -> ~1030 cycles a k-step at cfg3).  (The 2:4
-          // kernel, one recompute buffer and D = 1, keeps the two-phase path below: there the
-          // recompute must not wait for the main MMA's barriers.)
+          // the pipeline (tools/trace_k1.py: 1570 -> ~1030 cycles a k-step at cfg3)
           const int jm = j - D, e = j % NE, sl = j % NS, a = jm % NACT, wb = jm % NA;
           LORS_TR(0, j);
           mbar_wait4(&sready[sl].b, (j / NS) & 1, &refree[e].b, (j / NE) & 1, &afull[a].b, (jm / NACT) & 1,

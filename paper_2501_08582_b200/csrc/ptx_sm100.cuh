@@ -108,6 +108,22 @@ __device__ __forceinline__ void mbar_wait_impl(uint64_t* bar, uint32_t parity) {
   }
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_wait_impl<false>(bar, parity); }
+// Two barriers at once (see mbar_wait4)
+__device__ __forceinline__ void mbar_wait2(uint64_t* b0, uint32_t p0, uint64_t* b1, uint32_t p1) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred q0, q1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 q0, [%1], %2;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 q1, [%3], %4;\n\t"
+      "and.pred q0, q0, q1;\n\t"
+      "selp.u32 %0, 1, 0, q0;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(b0)), "r"(p0), "r"(smem_u32(b1)), "r"(p1)
+      : "memory");
+  if (ok) return;
+  mbar_wait(b0, p0);
+  mbar_wait(b1, p1);
+}
 // Four barriers at once: one non-blocking test of each, issued back to back so their
 // latencies overlap (a probe costs ~100 cycles, tools/trace_k1.py); the barriers not yet
 // complete are then waited for one by one.

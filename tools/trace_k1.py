@@ -12,13 +12,16 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2501_08582_b200 import _native, ops, prune  # noqa: E402
 
 L, R, C, r = (int(v) for v in sys.argv[1:5]) if len(sys.argv) > 4 else (4096, 11008, 4096, 16)
+SP = len(sys.argv) > 5 and sys.argv[5] == "sp24"   # the 2:4 sparse-tensor-core forward (2:4 weight)
 g = torch.Generator(device="cuda").manual_seed(0)
-w = prune.prune_rowwise(torch.randn(R, C, device="cuda", generator=g) * 0.02, 0.5).bfloat16()
+w = torch.randn(R, C, device="cuda", generator=g) * 0.02
+w = (prune.prune_two_four(w) if SP else prune.prune_rowwise(w, 0.5)).bfloat16()
 a = (torch.randn(R, r, device="cuda", generator=g) * 1e-3).bfloat16()
 b = (torch.randn(r, C, device="cuda", generator=g) / r ** 0.5).bfloat16()
 x = torch.randn(L, C, device="cuda", generator=g).bfloat16()
+meta = ops.compress_24(w)[1] if SP else None
 for _ in range(3):
-    ops.lors_fwd(x, w, a, b, 2.0)
+    ops.lors_fwd(x, w, a, b, 2.0, sparse24=SP, meta24=meta)
 torch.cuda.synchronize()
 buf = (ct.c_ulonglong * (2 * 24 * 512))()
 lib = _native.load()
