@@ -11,7 +11,7 @@
 using namespace lors::ptx;
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
-    mma_kernel(int n, int count, int mix, unsigned long long* out) {
+    mma_kernel(int n, int count, int mix, int sp, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* A = smem;            // [128 rows][64 k] SW128, 16 KB
@@ -31,6 +31,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *slot;
+  if (sp) {   // valid 2:4 metadata (kept positions 0 and 1 of every group) in columns 448..455
+    const uint32_t lane_base = (uint32_t)((threadIdx.x / 32) * 32) << 16;
+    for (int c = 0; c < 8; ++c) tmem_st_x1(tmem + lane_base + 448 + c, 0x44444444u);
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
   if (rank == 0 && threadIdx.x / 32 == 0) {
     const uint64_t ad = make_sdesc(smem_u32(A), 16, 1024, SW_128), bd = make_sdesc(smem_u32(B), 16, 1024, SW_128);
     const uint32_t i256 = make_idesc_bf16(256, 256, false, false), i128 = make_idesc_bf16(256, 128, false, false),
@@ -40,7 +49,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     if (elect_one()) {
       for (int c = 0; c < count; ++c) {
         const int kk = c & 3;
-        if (mix) {
+        if (sp) {
+          const uint32_t isp = make_idesc_bf16(256, n, false, false, true);
+          mma_bf16_pair_sp(tmem + (c & 1) * (n == 256 ? 256 : 0), ad + (c & 1) * 2, bd + (c & 1) * 4, tmem + 448 + (c & 1) * 4,
+                           isp, 1u);
+        } else if (mix) {
           mma_bf16_pair(tmem, ad + kk * 2, bd + kk * 2, i256, 1u);
           mma_bf16_pair(tmem + 256, ad + kk * 2, bd + kk * 2, i128, 1u);
         } else {
@@ -64,6 +77,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
 
 int main(int argc, char** argv) {
   const int n = argc > 1 ? atoi(argv[1]) : 256, count = argc > 2 ? atoi(argv[2]) : 4096, mix = argc > 3 ? atoi(argv[3]) : 0;
+  const int sp = argc > 4 ? atoi(argv[4]) : 0;   // 2:4 sparse MMAs (K = 32 logical each)
   int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   unsigned long long* out; cudaMalloc(&out, 8 * nsm);
   const size_t smem = 1024 + 32768 + 64;
@@ -72,15 +86,15 @@ int main(int argc, char** argv) {
   float best = 1e9;
   for (int it = 0; it < 4; ++it) {
     cudaEventRecord(e0);
-    mma_kernel<<<nsm / 2 * 2, 128, smem>>>(n, count, mix, out);
+    mma_kernel<<<nsm / 2 * 2, 128, smem>>>(n, count, mix, sp, out);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     if (it > 0 && ms < best) best = ms;
   }
   unsigned long long cyc; cudaMemcpy(&cyc, out, 8, cudaMemcpyDeviceToHost);
-  const double macs = (double)count * 256.0 * (mix ? 384.0 : (double)n) * 16.0 * (nsm / 2);
-  printf("N %d%s count %d: %.1f us, %.1f cycles per MMA%s (SM 0 pair), %.0f TFLOP/s (%s)\n", n, mix ? " (256+128 mix)" : "",
+  const double macs = (double)count * 256.0 * (mix ? 384.0 : (double)n) * (sp ? 32.0 : 16.0) * (nsm / 2);
+  printf("%sN %d%s count %d: %.1f us, %.1f cycles per MMA%s (SM 0 pair), %.0f TFLOP/s (%s)\n", sp ? "sparse " : "", n, mix ? " (256+128 mix)" : "",
          count, best * 1e3, (double)cyc / count / (mix ? 2 : 1), mix ? " instr" : "", 2 * macs / (best * 1e-3) / 1e12,
          cudaGetErrorString(cudaGetLastError()));
   return 0;

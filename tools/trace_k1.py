@@ -58,5 +58,11 @@ d = T(0, 5, j) - T(0, 13, j)
 print(f"issuer wready ok - CTA0 warp0 arrived: mean {d.mean():.0f}")
 d = T(0, 10, j) - T(0, 2, j)
 print(f"xf refull ok - rec issue (rec queue + exec + signal): mean {d.mean():.0f}")
-d = T(0, 4, j) - T(0, 7, j)
-print(f"afull ok - act slot free: mean {d.mean():.0f}")
+# main(g) completion as seen by the activation producer (slot of step g + 3 freed by its commit)
+done_ = T(0, 7, j + 3)
+d = done_ - T(0, 6, j)
+print(f"main issued -> main complete (seen by producer): mean {d.mean():.0f} median {np.median(d):.0f}")
+d = np.diff(done_)
+print(f"main completion period: mean {d.mean():.0f} median {np.median(d):.0f}")
+d = T(0, 6, j) - done_[:0].sum() if False else T(0, 6, j + 1) - T(0, 7, j + 3)
+print(f"main(j+1) issued - main(j) complete (negative: queued ahead): mean {d.mean():.0f} median {np.median(d):.0f}")
