@@ -1177,7 +1177,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         mma_commit_pair(&wempty[((jm + NA) % NGRP) * NA + wb].b, 0x3);   // next writer's group
       };
       auto do_main = [&](const int jm, const int mk, const int mn, const int mlen) {
-        if (PERSIST && mk == 0 && mn > 0) mbar_wait(acc_empty, (mn - 1) & 1);  // previous tile drained
+        if (PERSIST && mk == 0 && mn > 0) {
+          LORS_TR(20, mn);
+          mbar_wait(acc_empty, (mn - 1) & 1);  // previous tile drained
+          LORS_TR(21, mn);
+        }
         if (N2 && mk == 0) {   // a ragged last token tile: skip the all-padding N2 MMA (a third of it)
           int m_, l_, kb_, ke_, ut_, pt_;
           unit(mn, m_, l_, kb_, ke_, ut_, pt_);
@@ -1326,7 +1330,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(refree_l + (i % NE) * 16);  // RE buffer free for step i + NE
     };
-    auto finish = [&](const int i, const int kq, uint32_t (&p)[32], uint32_t (&wv)[16], uint32_t mw) {
+    // hold_w: keep the W slot (no wfree arrival): the epilogue stages its output blocks there
+    auto finish = [&](const int i, const int kq, uint32_t (&p)[32], uint32_t (&wv)[16], uint32_t mw,
+                      const bool hold_w = false) {
       constexpr bool POW2 = P2;
       const int wb = i % NA, wi = i % NW;
       // 3. destination buffer drained by the MMA of step i - NA
@@ -1474,7 +1480,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         return;
       }
       if (lane == 0) {
-        mbar_arrive(&wfree[wi].b);                   // done reading the W tile
+        if (!hold_w) mbar_arrive(&wfree[wi].b);      // done reading the W tile
         mbar_arrive_cluster(wready_l + wb * 16);     // W_eff half ready for the pair MMA
         if (warp == 0) LORS_TR(13, i);
       }
@@ -1549,7 +1555,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         }
       }
     };
-    auto bias_of = [&](float (&bvals)[2][2]) {     // bias of features (16 g + l/4) and (+8)
+    auto bias_of = [&](float (&bvals)[2][2], const int m0) {   // bias of features (16 g + l/4) and (+8)
 #pragma unroll
       for (int g16 = 0; g16 < 2; ++g16)
 #pragma unroll
@@ -1559,27 +1565,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         }
     };
     if constexpr (PERSIST) {
+      // Per unit n: its remaining k-steps; then (when unit n + 1 has >= 3 k-steps) the first three
+      // k-steps of unit n + 1, whose W_eff buffers free up as unit n's last main MMAs complete and
+      // whose W slots, read and held, stage unit n's epilogue; then the epilogue.  The MMAs of unit
+      // n + 1 restart the moment the accumulator is handed back (tools/trace_k1.py: transforming
+      // after the epilogue left the tensor pipe idle ~5000 cycles a tile on top of the drain).
       __shared__ int last_flag;
-      for (int n = 0, g = 0; n < my_units; ++n) {
-        int kb, ke, ut, part;
-        unit(n, m0, l0, kb, ke, ut, part);
+      constexpr int PRE = 3;
+      int g = 0, pre = 0, kb = 0, ke = 0, ut = -1, part = 0;
+      if (my_units > 0) unit(0, m0, l0, kb, ke, ut, part);
+      auto step = [&](const int kq, const bool hold_w) {
+        uint32_t p[32], wv[16], mw = 0;
+        issue(g, kq, p, wv, mw);
+        release(g);
+        finish(g, kq, p, wv, mw, hold_w);
+        ++g;
+      };
+      for (int n = 0; n < my_units; ++n) {
         gm = m0 + t;
-        for (int kq = kb; kq < ke; ++kq, ++g) {
-          uint32_t p[32], wv[16], mw = 0;
-          issue(g, kq, p, wv, mw);
-          release(g);
-          finish(g, kq, p, wv, mw);
+        for (int kq = kb + pre; kq < ke; ++kq) step(kq, false);
+        const int em0 = m0, el0 = l0, eut = ut, epart = part;   // this unit, for its epilogue
+        int stage_g = -1;       // flat step of the first held W slot (-1: stage in the W_eff ring)
+        pre = 0;
+        if (n + 1 < my_units) {
+          unit(n + 1, m0, l0, kb, ke, ut, part);
+          if (!EX && ke - kb >= PRE) {
+            gm = m0 + t;
+            stage_g = g;
+            pre = PRE;
+            for (int i = 0; i < PRE; ++i) step(kb + i, true);
+          }
         }
         if (EX) continue;   // no accumulator
+        // staging block b of the epilogue: a held W slot, or the (then idle) W_eff ring
+        auto stage_buf = [&](const int b) {
+          return stage_g >= 0 ? wring + ((stage_g + b % 3) % NW) * W_BYTES : weff + (b % 3) * WEFF_BYTES;
+        };
+        if (stage_g >= 0) named_bar_sync(1, XFORM_THREADS);   // every warp done reading the held W tiles
         // -------------------------------------------------------- epilogue of unit n
+        if (warp == 0 && lane == 0) LORS_TR(17, n);
         mbar_wait(accf, n & 1);
+        if (warp == 0 && lane == 0) LORS_TR(18, n);
         tc_fence_after();
         const float* adds[2];
         int n_adds = 0;
-        if (ut >= 0) {
+        if (eut >= 0) {
           // part of a split tile: publish this part's fp32 accumulator, then the last
           // part to arrive (per CTA of the pair) adds the others and writes the tile
-          float* mine = partials + ((int64_t)(ut * split + part) * 2 + rank) * PSLOT;
+          float* mine = partials + ((int64_t)(eut * split + epart) * 2 + rank) * PSLOT;
 #pragma unroll 1
           for (int c = 0; c < BNT / 128; ++c)
 #pragma unroll 1
@@ -1602,47 +1635,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           __threadfence();
           named_bar_sync(1, XFORM_THREADS);
           if (threadIdx.x == 0) {
-            const unsigned int old = atomicAdd(&counters[ut * 2 + rank], 1u);
+            const unsigned int old = atomicAdd(&counters[eut * 2 + rank], 1u);
             last_flag = old == (unsigned int)(split - 1);
-            if (last_flag) counters[ut * 2 + rank] = 0u;   // reusable without a memset
+            if (last_flag) counters[eut * 2 + rank] = 0u;   // reusable without a memset
           }
           named_bar_sync(1, XFORM_THREADS);
           if (!last_flag) {                                  // done: hand the accumulator back
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(acc_empty_l);
+            if (stage_g >= 0 && lane == 0)             // the held W slots were not needed
+              for (int k = 0; k < PRE; ++k) mbar_arrive(&wfree[(stage_g + k) % NW].b);
             continue;
           }
           __threadfence();
-          for (int p2 = 0; p2 < split; ++p2) adds[n_adds++] = partials + ((int64_t)(ut * split + p2) * 2 + rank) * PSLOT;
+          for (int p2 = 0; p2 < split; ++p2) adds[n_adds++] = partials + ((int64_t)(eut * split + p2) * 2 + rank) * PSLOT;
         }
-        // Staged through the W_eff ring, idle until this unit's successor is
-        // transformed: six [128 tokens][64 features] blocks in two batches of three;
-        // the accumulator is handed back to the MMA issuer after the last TMEM read.
+        // Staged through three 16 KB buffers (held W slots or the W_eff ring): six
+        // [128 tokens][64 features] blocks in two batches of three; the accumulator is handed
+        // back to the MMA issuer after the last TMEM read.
         float bvals[2][2];
-        bias_of(bvals);
+        bias_of(bvals, em0);
 #pragma unroll 1
         for (int batch = 0; batch < 2; ++batch) {
 #pragma unroll 1
           for (int c = 0; c < BNT / 128; ++c) {
             const int b = 2 * c + (q >> 1);            // block (chunk c, feature half q >> 1)
-            if (b / 3 == batch) stage_chunk(c, weff + (b % 3) * WEFF_BYTES, bvals, adds, n_adds);
+            if (b / 3 == batch) stage_chunk(c, stage_buf(b), bvals, adds, n_adds);
           }
           if (batch == 1) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(acc_empty_l);
+            if (warp == 0 && lane == 0) LORS_TR(19, n);
           }
           fence_proxy_async_smem();
           named_bar_sync(1, XFORM_THREADS);
           if (warp == 0 && lane == 0) {
             for (int b = 3 * batch; b < 3 * batch + 3; ++b)
-              tma_store_2d(&tmOut, weff + (b % 3) * WEFF_BYTES, m0 + 64 * (b & 1), l0 + 128 * (b >> 1));
+              tma_store_2d(&tmOut, stage_buf(b), em0 + 64 * (b & 1), el0 + 128 * (b >> 1));
             tma_store_commit();
             tma_store_wait_all();                      // the blocks are rewritten next
           }
           named_bar_sync(1, XFORM_THREADS);
         }
+        if (stage_g >= 0 && lane == 0)                 // the stores have read the held W slots
+          for (int k = 0; k < PRE; ++k) mbar_arrive(&wfree[(stage_g + k) % NW].b);
       }
       if (EX && warp == 0 && lane == 0) tma_store_wait_done();
     } else {

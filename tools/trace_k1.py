@@ -66,3 +66,15 @@ d = np.diff(done_)
 print(f"main completion period: mean {d.mean():.0f} median {np.median(d):.0f}")
 d = T(0, 6, j) - done_[:0].sum() if False else T(0, 6, j + 1) - T(0, 7, j + 3)
 print(f"main(j+1) issued - main(j) complete (negative: queued ahead): mean {d.mean():.0f} median {np.median(d):.0f}")
+# tile boundaries (uniform tiles of nk k-steps): accumulator complete -> drained -> next tile's first main
+nk = (C + 63) // 64
+print(f"tile boundaries (nk = {nk} k-steps a tile), cycles:")
+for n in range(1, 6):
+    acc_done, acc_back = t[0, 18, n], t[0, 19, n]
+    xf_end = t[0, 17, n]
+    iss_wait0, iss_wait1 = t[0, 20, n + 1], t[0, 21, n + 1]
+    first_main = t[0, 6, (n + 1) * nk] if (n + 1) * nk < 512 else 0
+    last_main_issue = t[0, 6, (n + 1) * nk - 1] if (n + 1) * nk - 1 < 512 else 0
+    print(f"  tile {n}: last main issued -> acc complete {acc_done - last_main_issue:6d}; xf loop end -> acc complete "
+          f"{acc_done - xf_end:6d}; drain (acc complete -> handed back) {acc_back - acc_done:6d}; "
+          f"handed back -> next first main issued {first_main - acc_back:6d}; issuer waited acc_empty {iss_wait1 - iss_wait0:6d}")
