@@ -1,5 +1,6 @@
-"""One cfg3 (LLaMA-2-7B-shaped) fine-tuning step inside an NVTX range "step", after two warm-up steps:
-    ncu --nvtx --nvtx-include "step/" --metrics gpu__time_duration.sum --csv python tools/step_nvtx.py"""
+"""One cfg3 (LLaMA-2-7B-shaped) fine-tuning step inside a process-wide NVTX start/end range "step" (the
+backward runs on autograd's threads), after two warm-up steps:
+    ncu --nvtx --nvtx-include "step" --metrics gpu__time_duration.sum --csv python tools/step_nvtx.py"""
 import os
 import sys
 import torch
@@ -14,8 +15,8 @@ toks = [synthetic_tokens(cfg.vocab, cfg.batch, cfg.seq, s, device="cuda") for s 
 for s in range(2):
     tr.step(toks[s])
 torch.cuda.synchronize()
-torch.cuda.nvtx.range_push("step")
+rid = torch.cuda.nvtx.range_start("step")
 tr.step(toks[2])
 torch.cuda.synchronize()
-torch.cuda.nvtx.range_pop()
+torch.cuda.nvtx.range_end(rid)
 print("ok")
