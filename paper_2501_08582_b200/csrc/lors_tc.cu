@@ -113,6 +113,28 @@ static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
   return LORS_OK;
 }
 
+// 2-D byte tensor [outer][inner], no swizzle (the 2:4 metadata boxes)
+static int make_map_u8(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                       uint32_t box_outer, const char* what) {
+  PFN_encodeTiled_t fn = encode_fn();
+  if (fn == nullptr) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return LORS_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error(std::string("cuTensorMapEncodeTiled failed for ") + what + " (CUresult " + std::to_string((int)r) + ")");
+    return LORS_ERR_CUDA;
+  }
+  return LORS_OK;
+}
+
 static int num_sms() {
   static int n[64] = {0};
   int dev = 0;
@@ -822,10 +844,17 @@ template <int RP>
 constexpr uint32_t sf_bytes() { return 32 * RP * 2; }   // streamed factor half (32 k x RP)
 template <int RP>
 constexpr uint32_t ff_bytes() { return 128 * RP * 2; }  // fixed factor tile (128 m x RP)
+// 2:4 with precomputed metadata: each W slot carries the TMA box of meta24 rows m0 .. m0+127,
+// bytes [16 (kq / 2), +16) (the 16 index nibbles a row of k-steps kq & ~1 and kq | 1), and a
+// 256-entry table maps a metadata byte (two groups' nibbles) to the two groups' prmt selectors
+template <bool SP>
+constexpr uint32_t meta_bytes() { return SP ? 128 * 16 : 0; }
+template <bool SP>
+constexpr uint32_t sel_lut_bytes() { return SP ? 256 * 4 : 0; }
 template <int RP, bool SP>
 constexpr size_t smem_bytes() {
-  return 1024 + ns<SP>() * sf_bytes<RP>() + nw<SP>() * W_BYTES + nact<SP>() * act_bytes<SP>() +
-         na<SP>() * weff_bytes<SP>() + ff_bytes<RP>() + 1024;
+  return 1024 + ns<SP>() * sf_bytes<RP>() + nw<SP>() * (W_BYTES + meta_bytes<SP>()) + nact<SP>() * act_bytes<SP>() +
+         na<SP>() * weff_bytes<SP>() + ff_bytes<RP>() + sel_lut_bytes<SP>() + 1024;
 }
 }  // namespace rg
 
@@ -841,7 +870,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     tc_lors_gemm_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmAct2,
                         const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmF,
-                        const __grid_constant__ CUtensorMap tmOut, const bf16* __restrict__ bias,
+                        const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmMeta,
+                        const bf16* __restrict__ bias,
                         const uint32_t* __restrict__ bits, const uint8_t* __restrict__ meta24, int words_per_row,
                         int Mout, int Kred, int n_t, int n_f, int split, float* __restrict__ partials,
                         unsigned int* __restrict__ counters, float alpha, int n_tok) {
@@ -876,10 +906,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   uint8_t* actb = wring + NW * W_BYTES;      // [NACT] activation halves
   uint8_t* weff = actb + NACT * ACT_BYTES;   // [NA] W_eff tiles
   uint8_t* ffac = weff + NA * WEFF_BYTES;    // fixed factor
+  uint8_t* mring = ffac + FF;                // [NW] 2:4 metadata boxes (meta24 != nullptr), one per W slot
+  uint32_t* sel_lut = reinterpret_cast<uint32_t*>(mring + NW * meta_bytes<SP>());  // 2:4: byte -> 2 selectors
   // mbarriers, one per 16 bytes.  sready / afull count 2 in the leader (own TMA
   // load with its bytes + the peer's relayed landing), 1 in the peer (its own
   // landing); refree / wready count the 16 transform warps of both CTAs.
-  Bar16* bars = reinterpret_cast<Bar16*>(ffac + FF);
+  Bar16* bars = reinterpret_cast<Bar16*>(mring + NW * meta_bytes<SP>() + sel_lut_bytes<SP>());
   Bar16* sready = bars;                 // [NS] factor slot landed (both CTAs, in the leader)
   Bar16* s_empty = sready + NS;         // [NS] local: recompute committed (factor slot free)
   Bar16* refree = s_empty + NS;         // [NE] leader: 16 transform warps read the recompute buffer
@@ -976,9 +1008,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       tma_prefetch_desc(&tmS);
       tma_prefetch_desc(&tmF);
       tma_prefetch_desc(&tmOut);
+      if (SP && meta24 != nullptr) tma_prefetch_desc(&tmMeta);
     }
   }
   if (warp == W_MMA) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+  if (SP && threadIdx.x < 256) {
+    // prmt selector keeping entries i0 < i1 of a group of four bf16 (index nibble i0 | i1 << 2)
+    auto sel = [](uint32_t n) { return 0x1010u + (n & 3u) * 0x22u + (n >> 2) * 0x2200u; };
+    sel_lut[threadIdx.x] = sel(threadIdx.x & 0xFu) | (sel(threadIdx.x >> 4) << 16);
+  }
   tc_fence_before();
   // Local barrier only: the producers start their TMA loads (which complete on
   // this CTA's own barriers) at once; every role that touches the peer CTA
@@ -1037,7 +1075,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         uint8_t* st = wring + wi * W_BYTES;
         const int k0 = i * BK;
         uint64_t* wf = &wfull[(g % NGRP) * NW + wi].b;   // the set of the group that reads step g
-        mbar_arrive_expect_tx(wf, W_BYTES);
+        mbar_arrive_expect_tx(wf, W_BYTES + (SP && meta24 != nullptr ? meta_bytes<SP>() : 0u));
+        // (a box's first byte must be 16-byte aligned: the box of k-steps 2j, 2j + 1)
+        if (SP && meta24 != nullptr) tma_load_2d(mring + wi * meta_bytes<SP>(), &tmMeta, wf, (k0 / 8) & ~15, m0);
         if (DX) {  // W[k0:k0+64, m0:m0+128] as two SW128 boxes of 64 columns
           tma_load_2d(st, &tmW, wf, m0, k0);
           tma_load_2d(st + W_BYTES / 2, &tmW, wf, m0 + 64, k0);
@@ -1273,16 +1313,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     int gm = m0 + t;               // global output feature (per tile)
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const WeffAlpha walpha = weff_alpha(alpha);      // weff_pair's alpha operands
-    // Per k-step: issue the TMEM load of the rank-r product and all W loads,
-    // release the recompute buffer, then transform and store.  (Pipelining the
-    // loads of step i + 1 under step i measured no faster.)
-    auto issue = [&](const int i, const int kq, uint32_t (&p)[32], uint32_t (&wv)[16], uint32_t& mw) {
-      // 0. 2:4 with precomputed metadata: this row's 8 index nibbles of the half
-      //    (lors_compress_24 layout [R, C/8]); the load overlaps everything below
-      if (SP && meta24 != nullptr)
-        mw = gm < Mout ? __ldg(reinterpret_cast<const uint32_t*>(meta24 + (int64_t)gm * (Kred / 8) + kq * 8 + h * 4))
-                       : 0x44444444u;
-      // 1. rank-r product of this k-step (TMEM -> registers), then release the buffer
+    // Per k-step: the TMEM load of the rank-r product (load_p), the W loads (load_w),
+    // release of the recompute buffer, then transform and store (finish).  (Issuing the
+    // next step's TMEM load at the end of a step measured 0-2% slower, tools/ab_gemm.py.)
+    auto load_p = [&](const int i, uint32_t (&p)[32]) {
       const int rb = i % NE;
       if (warp == 0 && lane == 0) LORS_TR(9, i);
       mbar_wait(&refull[(i % NGRP) * NE + rb].b, (i / RE_PERIOD) & 1);
@@ -1297,12 +1331,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         tmem_ld_16x256b_x4(tmem + lane_addr + re_col, p0);
         tmem_ld_16x256b_x4(tmem + lane_addr + (16u << 16) + re_col, p1);
       }
-      // 2. W tile landed: all of this thread's W loads are issued before any
-      //    result is needed, so their latency overlaps the TMEM load's
+    };
+    auto load_w = [&](const int i, const int kq, uint32_t (&wv)[16], uint32_t& mw) {
+      // W tile landed: all of this thread's W loads are issued before any result is
+      // needed, so their latency overlaps the TMEM load's
       const int wi = i % NW;
       mbar_wait(&wfull[(i % NGRP) * NW + wi].b, (i / W_PERIOD) & 1);
       if (warp == 0 && lane == 0) LORS_TR(11, i);
       const uint32_t wt = smem_u32(wring + wi * W_BYTES);
+      // 2:4 with precomputed metadata: this row's 8 index nibbles of the half, from the
+      // slot's meta24 box (lors_compress_24 layout [R, C/8]; rows past R were zero-filled)
+      if (SP && meta24 != nullptr) {
+        mw = lds32(smem_u32(mring + wi * meta_bytes<SP>()) + (uint32_t)t * 16 + (kq & 1) * 8 + h * 4);
+        if (gm >= Mout) mw = 0x44444444u;   // rows past R: zero-filled box -> a valid (unused) pattern
+      }
       if (!DX) {
         // thread = W row t; chunks 4h .. 4h+3 of 8 k-values (SW128)
 #pragma unroll
@@ -1341,19 +1383,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       if (warp == 0 && lane == 0) LORS_TR(12, i);
       const uint32_t dst = smem_u32(weff + wb * WEFF_BYTES);
       if (SP && meta24 != nullptr) {
-        // 2:4 with precomputed index nibbles: weff_pair on the group's four
-        // values, then one prmt keeps the two positions the nibble names (no
-        // on-chip nibble derivation) -- the dense prologue's values, compressed
+        // 2:4 with precomputed index nibbles: the kept pair of each group of four is
+        // selected first (one prmt on W, one on the rounded product, the selectors from
+        // sel_lut), then weff_combine runs once per pair -- W_eff is elementwise, so this
+        // is the dense prologue's value at the kept positions, compressed
         uint32_t comp[8];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          const uint32_t nib = (mw >> (4 * g)) & 0xFu;
-          const uint32_t sel = 0x1010u + (nib & 3u) * 0x22u + (nib >> 2) * 0x2200u;
-          const uint32_t o0 = weff_pair<POW2>(wv[2 * g], __uint_as_float(p[4 * g]), __uint_as_float(p[4 * g + 1]),
-                                        walpha, nonzero_mask_bf16x2(wv[2 * g]));
-          const uint32_t o1 = weff_pair<POW2>(wv[2 * g + 1], __uint_as_float(p[4 * g + 2]), __uint_as_float(p[4 * g + 3]),
-                                        walpha, nonzero_mask_bf16x2(wv[2 * g + 1]));
-          comp[g] = prmt(o0, o1, sel);
+        for (int g2 = 0; g2 < 4; ++g2) {
+          const uint32_t sels = lds32_table(smem_u32(sel_lut) + ((mw >> (8 * g2)) & 0xFFu) * 4);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int g = 2 * g2 + e;
+            const uint32_t sel = e ? (sels >> 16) : sels;
+            const uint32_t w2 = prmt(wv[2 * g], wv[2 * g + 1], sel);
+            const uint32_t s2 = prmt(weff_scaled_p<POW2>(__uint_as_float(p[4 * g]), __uint_as_float(p[4 * g + 1]), walpha),
+                                     weff_scaled_p<POW2>(__uint_as_float(p[4 * g + 2]), __uint_as_float(p[4 * g + 3]), walpha),
+                                     sel);
+            comp[g] = weff_combine<POW2>(w2, s2, walpha, nonzero_mask_bf16x2(w2));
+          }
         }
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
@@ -1576,7 +1623,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       if (my_units > 0) unit(0, m0, l0, kb, ke, ut, part);
       auto step = [&](const int kq, const bool hold_w) {
         uint32_t p[32], wv[16], mw = 0;
-        issue(g, kq, p, wv, mw);
+        load_p(g, p);
+        load_w(g, kq, wv, mw);
         release(g);
         finish(g, kq, p, wv, mw, hold_w);
         ++g;
@@ -1686,7 +1734,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     } else {
     for (int i = grp; i < nk; i += NGRP) {
       uint32_t p[32], wv[16], mw = 0;
-      issue(i, i, p, wv, mw);
+      load_p(i, p);
+      load_w(i, i, wv, mw);
       release(i);
       finish(i, i, p, wv, mw);
     }
@@ -1844,6 +1893,16 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
     if ((st = make_map(&tF, a, r, R, RP, 128, RP * 2, "a (fixed)"))) return st;
   }
   if ((st = make_map(&tOut, out, Mout, L, 64, 128, 128, "output"))) return st;  // [128 tokens][64 features] SW128
+  // 2:4 metadata boxes ([R, C/8] bytes, 128 rows x 16 bytes): a TMA row pitch is a multiple of
+  // 16 bytes, so C % 128 == 0; other widths derive the nibbles on chip from W instead
+  CUtensorMap tMeta = tW;
+  if (SP && meta24 != nullptr) {
+    if (C % 128 == 0) {
+      if ((st = make_map_u8(&tMeta, meta24, (uint64_t)C / 8, R, 16, 128, "meta24"))) return st;
+    } else {
+      meta24 = nullptr;
+    }
+  }
   const bool p2 = alpha_pow2(alpha);
   auto kern = bits ? (p2 ? tc_lors_gemm_kernel<DX, RP, true, SP, false, true> : tc_lors_gemm_kernel<DX, RP, true, SP, false, false>)
                    : (p2 ? tc_lors_gemm_kernel<DX, RP, false, SP, false, true> : tc_lors_gemm_kernel<DX, RP, false, SP, false, false>);
@@ -1879,7 +1938,7 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
             RP, (int)SP, grid.x, grid.y, v, cudaGetErrorString(e));
     (void)cudaGetLastError();
   }
-  kern<<<grid, threads<SP>(), smem, s>>>(tAct, tAct2, tW, tS, tF, tOut, bias, bits, SP ? meta24 : nullptr,
+  kern<<<grid, threads<SP>(), smem, s>>>(tAct, tAct2, tW, tS, tF, tOut, tMeta, bias, bits, SP ? meta24 : nullptr,
                                          (int)ceil_div(C, 32), Mout, Kred, n_t, n_f, split, partials, counters,
                                          alpha, L);
   LORS_CHECK_LAUNCH(DX ? "tc_lors_gemm<dx>" : "tc_lors_gemm<fwd>");
@@ -1924,7 +1983,7 @@ static int launch_weff_export(const bf16* w, const bf16* a, const bf16* b, const
   const int mc = persistent_clusters<false, RP, false>();
   dim3 grid((unsigned)(2 * std::min(n_f, mc)));
   // the activation maps are never read in export mode (W's map stands in)
-  kern<<<grid, threads<false>(), smem, s>>>(tW, tW, tW, tS, tF, tOut, nullptr, bits, nullptr, (int)ceil_div(C, 32), R,
+  kern<<<grid, threads<false>(), smem, s>>>(tW, tW, tW, tS, tF, tOut, tW, nullptr, bits, nullptr, (int)ceil_div(C, 32), R,
                                             C, /*n_t=*/1, n_f, /*split=*/1, nullptr, nullptr, alpha, 0);
   LORS_CHECK_LAUNCH("tc_lors_gemm<export>");
   return LORS_OK;

@@ -465,6 +465,17 @@ __device__ __forceinline__ void mma_16816(float (&d)[4], const uint32_t (&a)[4],
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+__device__ __forceinline__ uint32_t lds32(uint32_t saddr) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(saddr));
+  return v;
+}
+// a shared-memory table written once before a block-wide barrier: free to schedule
+__device__ __forceinline__ uint32_t lds32_table(uint32_t saddr) {
+  uint32_t v;
+  asm("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(saddr));
+  return v;
+}
 __device__ __forceinline__ void lds128(uint32_t saddr, uint32_t (&v)[4]) {
   asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(saddr));
 }
@@ -538,17 +549,30 @@ __device__ __forceinline__ WeffAlpha weff_alpha(float alpha) {
 // product and the add fuse into one bf16x2 fma (cvt, fma, and); otherwise mul.rn.f32x2,
 // cvt, add (one instruction more).  Every tensor-core prologue (K1, K2, K3) and the
 // tensor-core K6 export call this; the FFMA kernels' weff_value is the same arithmetic.
+// The two halves of weff_pair, for callers that move the rounded product around in between
+// (the 2:4 prologue selects the kept pair first): weff_scaled_p is the bf16 pair the sum
+// adds -- bf16(P) for POW2 (alpha is applied exactly inside the fma), bf16(alpha P)
+// otherwise -- and weff_combine finishes the pair.  weff_pair = combine(scaled(P)).
 template <bool POW2>
-__device__ __forceinline__ uint32_t weff_pair(uint32_t w2, float p_lo, float p_hi, const WeffAlpha& al, uint32_t keep) {
-  if (POW2) return fma_bf16x2(al.b2, cvt_bf16x2(p_lo, p_hi), w2) & keep;
+__device__ __forceinline__ uint32_t weff_scaled_p(float p_lo, float p_hi, const WeffAlpha& al) {
+  if (POW2) return cvt_bf16x2(p_lo, p_hi);
   uint64_t pl, ap;
   asm("mov.b64 %0, {%1, %2};" : "=l"(pl) : "f"(p_lo), "f"(p_hi));
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(ap) : "l"(al.x2), "l"(pl));
   float lo, hi;
   asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(ap));
+  return cvt_bf16x2(lo, hi);
+}
+template <bool POW2>
+__device__ __forceinline__ uint32_t weff_combine(uint32_t w2, uint32_t sp2, const WeffAlpha& al, uint32_t keep) {
+  if (POW2) return fma_bf16x2(al.b2, sp2, w2) & keep;
   uint32_t r;
-  asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(cvt_bf16x2(lo, hi)), "r"(w2));
+  asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(sp2), "r"(w2));
   return r & keep;
+}
+template <bool POW2>
+__device__ __forceinline__ uint32_t weff_pair(uint32_t w2, float p_lo, float p_hi, const WeffAlpha& al, uint32_t keep) {
+  return weff_combine<POW2>(w2, weff_scaled_p<POW2>(p_lo, p_hi, al), al, keep);
 }
 
 // ---------------------------------------------------------------------------

@@ -1,6 +1,5 @@
 E=$PWD/paper_2501_08582_b200/_native/exp
-timeout 900 python -m pytest tests/test_weff_identity.py tests/test_shape_sweep.py tests/test_fullsize_parity.py -q -m gpu -x > gpurun_out/sp_tests.log 2>&1; tail -n 3 gpurun_out/sp_tests.log
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "sparse or 24" > gpurun_out/sp_tests2.log 2>&1; tail -n 2 gpurun_out/sp_tests2.log
+timeout 600 python -m pytest tests/test_weff_identity.py -q -m gpu -x -k sparse > gpurun_out/sp_tests.log 2>&1; tail -n 1 gpurun_out/sp_tests.log
 LORS_B200_LIB=$E/trace/liblors_b200.so timeout 300 python tools/trace_k1.py 8192 11008 4096 64 sp24 2>&1 | grep -E "issuer iteration|transform period|xf |main completion" > gpurun_out/trace_sp2.log; cat gpurun_out/trace_sp2.log
 for i in 1 2; do
   for v in base new; do
