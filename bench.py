@@ -676,6 +676,7 @@ def run_decoder(args):
     name = DECODER_CONFIGS[args.config]
     dcfg = D.preset(name)
     T = dcfg.tokens_per_step()
+    use_graph = world == 1 and args.optimizer == "native" and not args.no_graph
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
@@ -686,14 +687,22 @@ def run_decoder(args):
             from paper_2501_08582_b200.comparators import comparator_factory
             fac = comparator_factory(kind, dcfg, seed=0)
         model = D.LoRSDecoder(dcfg, device=dev, seed=0, linear_factory=fac)
-        return model, Trainer(model, lr=2e-5, optimizer=args.optimizer if kind == "lors" else "auto")
+        graph = kind == "lors" and use_graph
+        return model, Trainer(model, lr=2e-5, optimizer=args.optimizer if kind == "lors" else "auto",
+                              cuda_graph=graph)
 
     def measure(kind, steps, warmup, sample_clocks=False, dominant=False):
         model, trainer = build(kind)
         toks = [synthetic_tokens(dcfg.vocab, dcfg.batch, dcfg.seq, s, rank=rank, device=dev)
                 for s in range(steps + warmup)]
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats(dev)
         for s in range(warmup):
             trainer.step(toks[s])
+            if s == 0:
+                # peak HBM of an eager step (a graph replay allocates nothing, so its peak would
+                # hide the activations; the graph's pool holds the same bytes)
+                eager_peak = torch.cuda.max_memory_allocated(dev) / 1e9
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -716,11 +725,13 @@ def run_decoder(args):
             clocks.sample_until(e1)
         torch.cuda.synchronize()
         launches = _native.launch_count()
+        if trainer.cuda_graph:   # replays launch no kernel from the host: the captured step's count
+            launches = trainer.graph_launches * steps
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / steps
-        peak = torch.cuda.max_memory_allocated(dev) / 1e9
+        peak = max(eager_peak, torch.cuda.max_memory_allocated(dev) / 1e9)
         out = {"ms": ms, "peak_gb": peak, "launches": launches, "loss": float(loss),
                "clocks": clocks.result() if clocks else None}
         # end to end through the public API: host token ids copied in, loss copied out, every step
@@ -810,7 +821,8 @@ def run_decoder(args):
             "config": decoder_config(args.config, dcfg, world),
             "path": {"forward": "2:4 sparse tensor cores" if args.sparse24 and dcfg.sparsity == "two_four"
                      else "dense-masked tcgen05 (W_eff rebuilt on chip)", "adapter_grads": "ste (lors)",
-                     "optimizer": args.optimizer, "gradient_sync": "NCCL all-reduce of dA/dB buckets"
+                     "optimizer": args.optimizer, "cuda_graph": use_graph,
+                     "gradient_sync": "NCCL all-reduce of dA/dB buckets"
                      if world > 1 else "none (1 GPU)"},
             "peak_hbm_gb": peak_gb,
             "memory": memory,
@@ -869,6 +881,9 @@ def main(argv=None):
                          "peer-memory reduce + AdamW kernel over symmetric memory (p2p), or torch AdamW")
     ap.add_argument("--sparse24", action="store_true",
                     help="decoder configs with 2:4 masks: forward on the sparse tensor cores")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="decoder configs: launch every kernel from Python each step instead of replaying the "
+                         "captured step (CUDA graph; one process with the native optimizer only)")
     argv = sys.argv[1:] if argv is None else argv
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)

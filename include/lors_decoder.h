@@ -60,6 +60,13 @@ int lors_cross_entropy_bwd(const void* logits, const int64_t* targets, const flo
 int lors_adamw(float* p, const float* g, float* m, float* v, void* shadow, int64_t n, float lr, float beta1,
                float beta2, float eps, float weight_decay, int64_t step, void* stream);
 
+/* lors_adamw with the step count on the device, for CUDA-graph capture (trainer.Trainer(cuda_graph=True)):
+ * counter = int64[2] in device memory, zero-initialised; counter[0] = updates taken so far.  The call applies
+ * update t = counter[0] + 1 (bias corrections computed on the device from t, in double as lors_adamw does on
+ * the host) and leaves counter[0] = t when the launch completes; counter[1] is scratch. */
+int lors_adamw_dstep(float* p, const float* g, float* m, float* v, void* shadow, int64_t n, float lr, float beta1,
+                     float beta2, float eps, float weight_decay, int64_t* counter, void* stream);
+
 /* Fused gradient collective + AdamW over NVLink peer memory: every rank owns the shard
  * [rank n / world, (rank + 1) n / world) of the flat adapter buffers (n a multiple of 4 * world).  For each
  * element of its shard it sums the gradient over all ranks' gradient buffers (peer loads), divides by world,

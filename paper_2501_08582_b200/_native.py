@@ -38,7 +38,8 @@ EXPORTED_SYMBOLS = (
 )
 # include/lors_decoder.h: decoder-side helpers (not the LoRS drop-in boundary)
 DECODER_SYMBOLS = ("lors_rope", "lors_swiglu", "lors_swiglu_bwd", "lors_add_rmsnorm", "lors_add_rmsnorm_bwd",
-                   "lors_cross_entropy", "lors_cross_entropy_bwd", "lors_adamw", "lors_adamw_p2p")
+                   "lors_cross_entropy", "lors_cross_entropy_bwd", "lors_adamw", "lors_adamw_dstep",
+                   "lors_adamw_p2p")
 
 _vp = ct.c_void_p
 
@@ -120,6 +121,9 @@ def load(path: str = LIB_PATH) -> ct.CDLL:
         lib.lors_adamw.argtypes = [_vp, _vp, _vp, _vp, _vp, ct.c_int64, ct.c_float, ct.c_float, ct.c_float,
                                    ct.c_float, ct.c_float, ct.c_int64, _vp]
         lib.lors_adamw.restype = ct.c_int
+        lib.lors_adamw_dstep.argtypes = [_vp, _vp, _vp, _vp, _vp, ct.c_int64, ct.c_float, ct.c_float, ct.c_float,
+                                         ct.c_float, ct.c_float, _vp, _vp]
+        lib.lors_adamw_dstep.restype = ct.c_int
         lib.lors_adamw_p2p.argtypes = [_vp, _vp, _vp, _vp, _vp, ct.c_int64, ct.c_int32, ct.c_int32, ct.c_float,
                                        ct.c_float, ct.c_float, ct.c_float, ct.c_float, ct.c_int64, _vp]
         lib.lors_adamw_p2p.restype = ct.c_int

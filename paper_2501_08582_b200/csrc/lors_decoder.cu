@@ -110,6 +110,44 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
   if (shadow != nullptr) shadow[i] = __float2bfloat16_rn(pi);
 }
 
+// AdamW with the step counter on the device (a CUDA-graph replay reuses the launch, so the
+// bias correction cannot be a host argument): counter[0] = steps taken, counter[1] = block
+// ticket.  Every block reads t = counter[0] + 1 before taking a ticket; the last block to
+// finish stores t, so no block can see the new count.  Same element arithmetic as adamw_kernel.
+__global__ void adamw_dstep_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                                   float* __restrict__ v, __nv_bfloat16* __restrict__ shadow, int64_t n, float lr,
+                                   float decay, float b1, float b2, float eps, unsigned long long* counter) {
+  __shared__ float s_step_size, s_inv_sqrt_bc2;
+  __shared__ unsigned long long s_t;
+  if (threadIdx.x == 0) {
+    const unsigned long long t = *reinterpret_cast<volatile unsigned long long*>(counter) + 1ull;
+    const double bc1 = 1.0 - pow((double)b1, (double)t);
+    const double bc2 = 1.0 - pow((double)b2, (double)t);
+    s_step_size = (float)((double)lr / bc1);
+    s_inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
+    s_t = t;
+  }
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const float gi = g[i];
+    const float mi = fmaf(b1, m[i], (1.0f - b1) * gi);
+    const float vi = fmaf(b2, v[i], (1.0f - b2) * gi * gi);
+    const float pi = p[i] * decay - s_step_size * mi / (sqrtf(vi) * s_inv_sqrt_bc2 + eps);
+    m[i] = mi;
+    v[i] = vi;
+    p[i] = pi;
+    if (shadow != nullptr) shadow[i] = __float2bfloat16_rn(pi);
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&counter[1], 1ull) == (unsigned long long)gridDim.x - 1ull) {
+      counter[0] = s_t;
+      counter[1] = 0ull;
+    }
+  }
+}
+
 // Peer-memory AdamW over one shard: 4 elements per thread (16-byte peer loads and stores).
 // The rank's own master copy is read through params[rank] (all copies are identical).
 __global__ void adamw_p2p_kernel(const float* const* __restrict__ grads, float* const* __restrict__ params,
@@ -174,6 +212,26 @@ extern "C" int lors_adamw_p2p(const void* grads, const void* params, const void*
       (int64_t)rank * shard, shard4, rank, world, 1.0f - lr * weight_decay, beta1, beta2, (float)(lr / bc1),
       (float)(1.0 / std::sqrt(bc2)), eps, 1.0f / (float)world);
   LORS_CHECK_LAUNCH("adamw_p2p");
+  return LORS_OK;
+}
+
+extern "C" int lors_adamw_dstep(float* p, const float* g, float* m, float* v, void* shadow, int64_t n, float lr,
+                                float beta1, float beta2, float eps, float weight_decay, int64_t* counter,
+                                void* stream) {
+  using namespace lors;
+  if (!p || !g || !m || !v || !counter) {
+    set_error("lors_adamw_dstep: null pointer");
+    return LORS_ERR_ARGUMENT;
+  }
+  if (n < 0 || !(lr >= 0.0f) || !(beta1 >= 0.0f && beta1 < 1.0f) || !(beta2 >= 0.0f && beta2 < 1.0f)) {
+    set_error("lors_adamw_dstep: invalid hyper-parameters (n >= 0, lr >= 0, 0 <= beta < 1)");
+    return LORS_ERR_ARGUMENT;
+  }
+  if (n == 0) return LORS_OK;
+  adamw_dstep_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      p, g, m, v, (__nv_bfloat16*)shadow, n, lr, 1.0f - lr * weight_decay, beta1, beta2, eps,
+      reinterpret_cast<unsigned long long*>(counter));
+  LORS_CHECK_LAUNCH("adamw_dstep");
   return LORS_OK;
 }
 

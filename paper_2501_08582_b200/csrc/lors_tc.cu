@@ -765,10 +765,16 @@ constexpr int threads() { return 32 * (xw<SP>() + 5); }
 // Token tile of a CTA pair: 256 + N2 tokens per W_eff tile -- one N = 256 MMA and
 // one N = N2 MMA per k-step into two accumulators -- so each on-chip W_eff tile (its
 // rank-r recompute, transform and W load) serves 1.5x the tokens.  TMEM: acc 256 + N2
-// columns, then NE recompute buffers of 64 (dense: 2; 2:4: 1, next to the sparse
-// metadata of the NA W_eff buffers at E_COL).
+// columns, then NE recompute buffers of 64 (dense: two; 2:4: one), then for 2:4 the
+// sparse metadata of the NA W_eff buffers at e_col.  (A 352-token 2:4 tile, N2 = 96,
+// fits two recompute buffers next to the metadata; it measured slower, 684 vs 645 us at
+// cfg2: the 2:4 pipeline is paced by the transform warps' ~1300-cycle k-step, not by the
+// single recompute buffer, tools/trace_k1.py.)
+#ifndef LORS_N2_SP
+#define LORS_N2_SP 128
+#endif
 template <bool SP>
-constexpr int n2() { return (SP && !LORS_PERSIST) ? 0 : LORS_N2; }
+constexpr int n2() { return (SP && !LORS_PERSIST) ? 0 : (SP ? LORS_N2_SP : LORS_N2); }
 template <bool SP>
 constexpr int bnt() { return 256 + n2<SP>(); }            // tokens per pair tile
 // TMEM recompute buffers, and the factor ring (streamed adapter-factor half) with its
@@ -776,7 +782,7 @@ constexpr int bnt() { return 256 + n2<SP>(); }            // tokens per pair til
 // buffer once the transform has read it.  The W ring is separate too: the recompute
 // of step j needs only its factor slice, W(j) is first read by the transform.
 template <bool SP>
-constexpr int ne() { return SP ? (LORS_PERSIST ? 1 : 3) : (512 - 256 - n2<SP>()) / 64; }
+constexpr int ne() { return SP ? (LORS_PERSIST ? (512 - 256 - n2<SP>() - 32) / 64 : 3) : (512 - 256 - n2<SP>()) / 64; }
 template <bool SP>
 constexpr int ns() { return SP ? 3 : 2; }
 template <bool SP>
@@ -825,7 +831,7 @@ constexpr uint64_t nibble_lut() {
   return lut;
 }
 constexpr uint64_t kNibbleLut = nibble_lut();
-constexpr uint32_t E_COL = 448;  // 2:4 metadata: W_eff buffer b, MMA h at column 448 + 8 b + 4 h
+constexpr uint32_t E_COL_NP = 448;  // non-persistent 2:4 build: metadata columns
 #ifndef LORS_GROUP_T
 #define LORS_GROUP_T 8
 #endif
@@ -840,6 +846,15 @@ constexpr uint32_t weff_bytes() { return (SP && !LORS_PERSIST) ? BM * BK : BM * 
 constexpr uint32_t TMEM_COLS = 512;
 template <bool SP>
 constexpr uint32_t re_col() { return 256 + n2<SP>(); }  // recompute buffers at TMEM cols re_col + 64 e
+// 2:4 metadata: W_eff buffer b, MMA h at column e_col + 8 b + 4 h
+template <bool SP>
+constexpr uint32_t e_col() { return LORS_PERSIST ? re_col<SP>() + ne<SP>() * 64 : E_COL_NP; }
+// accumulator drain: chunks of 128 tokens (the last one BNT - 128 (nch - 1)), stored in
+// boxes of out_rows token rows (32 when a chunk is partial, so no store crosses the tile)
+template <bool SP>
+constexpr int nch() { return (bnt<SP>() + 127) / 128; }
+template <bool SP>
+constexpr int out_rows() { return bnt<SP>() % 128 ? 32 : 128; }
 template <int RP>
 constexpr uint32_t sf_bytes() { return 32 * RP * 2; }   // streamed factor half (32 k x RP)
 template <int RP>
@@ -885,6 +900,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   constexpr bool PERSIST = persist<SP>();
   static_assert(!PERSIST || NGRP == 1, "persistent schedule assumes one transform group");
   static_assert(smem_bytes<RP, SP>() <= 232448, "shared memory: rings exceed 227 KB");
+  constexpr uint32_t E_COL = e_col<SP>();
   static_assert(re_col<SP>() + NE * 64 <= (SP ? E_COL : TMEM_COLS) && (!SP || E_COL + NA * 8 <= TMEM_COLS),
                 "TMEM: accumulators, recompute buffers and 2:4 metadata must fit 512 columns");
   constexpr int N2 = n2<SP>(), BNT = bnt<SP>();
@@ -1371,6 +1387,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(refree_l + (i % NE) * 16);  // RE buffer free for step i + NE
+      if (warp == 0 && lane == 0) LORS_TR(22, i);
     };
     // hold_w: keep the W slot (no wfree arrival): the epilogue stages its output blocks there
     auto finish = [&](const int i, const int kq, uint32_t (&p)[32], uint32_t (&wv)[16], uint32_t mw,
@@ -1511,6 +1528,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           }
         }
       }
+      if (warp == 0 && lane == 0) LORS_TR(23, i);
       fence_proxy_async_smem();
       __syncwarp();
       if (EX) {
@@ -1542,7 +1560,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
     // split-K partials: fragment f = (chunk, 32-token slice, 16-lane group) of this thread,
     // 16 floats at ((f * XFORM_THREADS + tid) * 16) of the part's slot -- coalesced, and
     // read back by the same thread of the CTA that finishes the tile
-    constexpr int PSLOT = 128 * BNT;                 // floats per CTA and part
+    constexpr int NCH = nch<SP>(), OUT_ROWS = out_rows<SP>();
+    constexpr int PSLOT = 128 * 128 * NCH;           // floats per CTA and part
     const int tid_x = (int)threadIdx.x;
     auto frag_off = [&](int c, int tb, int g16) {
       return ((int64_t)((c * (TSL / 32) + tb / 32) * 2 + g16) * XFORM_THREADS + tid_x) * 16;
@@ -1552,6 +1571,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 #pragma unroll 1
       for (int tb = 0; tb < TSL; tb += 32) {
         const int tok = hh * TSL + tb;                // token offset inside the chunk
+        if (c * 128 + tok >= BNT) continue;           // past a partial last chunk
         uint32_t v[2][16];
 #pragma unroll
         for (int g16 = 0; g16 < 2; ++g16)
@@ -1662,11 +1682,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           // part to arrive (per CTA of the pair) adds the others and writes the tile
           float* mine = partials + ((int64_t)(eut * split + epart) * 2 + rank) * PSLOT;
 #pragma unroll 1
-          for (int c = 0; c < BNT / 128; ++c)
+          for (int c = 0; c < NCH; ++c)
 #pragma unroll 1
             for (int tb = 0; tb < TSL; tb += 32) {
               uint32_t v[2][16];
               const int tok = hh * TSL + tb;
+              if (c * 128 + tok >= BNT) continue;         // past a partial last chunk
 #pragma unroll
               for (int g16 = 0; g16 < 2; ++g16)
                 tmem_ld_16x256b_x4(tmem + ((uint32_t)(q * 32 + 16 * g16) << 16) + (uint32_t)(c * 128 + tok), v[g16]);
@@ -1707,7 +1728,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
 #pragma unroll 1
         for (int batch = 0; batch < 2; ++batch) {
 #pragma unroll 1
-          for (int c = 0; c < BNT / 128; ++c) {
+          for (int c = 0; c < NCH; ++c) {
             const int b = 2 * c + (q >> 1);            // block (chunk c, feature half q >> 1)
             if (b / 3 == batch) stage_chunk(c, stage_buf(b), bvals, adds, n_adds);
           }
@@ -1721,7 +1742,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           named_bar_sync(1, XFORM_THREADS);
           if (warp == 0 && lane == 0) {
             for (int b = 3 * batch; b < 3 * batch + 3; ++b)
-              tma_store_2d(&tmOut, stage_buf(b), em0 + 64 * (b & 1), el0 + 128 * (b >> 1));
+              for (int rr = 0; rr < 128 && (b >> 1) * 128 + rr < BNT; rr += OUT_ROWS)
+                tma_store_2d(&tmOut, stage_buf(b) + rr * 128, em0 + 64 * (b & 1), el0 + 128 * (b >> 1) + rr);
             tma_store_commit();
             tma_store_wait_all();                      // the blocks are rewritten next
           }
@@ -1867,7 +1889,7 @@ static TailSplit plan_tail_split(int L, int R, int C) {
   p.split = split;
   p.tail = tail;
   p.counter_bytes = ((size_t)tail * 2 * sizeof(unsigned int) + 255) / 256 * 256;
-  p.bytes = p.counter_bytes + (size_t)tail * split * 2 * 128 * BNT * sizeof(float);
+  p.bytes = p.counter_bytes + (size_t)tail * split * 2 * 128 * 128 * nch<SP>() * sizeof(float);
   return p;
 }
 
@@ -1892,7 +1914,7 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
     if ((st = make_map(&tS, b, C, r, 32, RP, 64, "b (streamed half)"))) return st;
     if ((st = make_map(&tF, a, r, R, RP, 128, RP * 2, "a (fixed)"))) return st;
   }
-  if ((st = make_map(&tOut, out, Mout, L, 64, 128, 128, "output"))) return st;  // [128 tokens][64 features] SW128
+  if ((st = make_map(&tOut, out, Mout, L, 64, out_rows<SP>(), 128, "output"))) return st;  // [tokens][64 features] SW128
   // 2:4 metadata boxes ([R, C/8] bytes, 128 rows x 16 bytes): a TMA row pitch is a multiple of
   // 16 bytes, so C % 128 == 0; other widths derive the nibbles on chip from W instead
   CUtensorMap tMeta = tW;

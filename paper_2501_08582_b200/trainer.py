@@ -36,7 +36,9 @@ class FlatAdamW:
     view would), the moments live in two more, and the same kernel writes the
     bf16 compute copies the LoRS kernels read (`_lors_shadow` views, see
     module.compute_copy), so a step casts no adapter.  Semantics of
-    torch.optim.AdamW (decoupled weight decay, bias-corrected moments)."""
+    torch.optim.AdamW (decoupled weight decay, bias-corrected moments).  The step
+    count lives on the device (lors_adamw_dstep), so the update can be replayed
+    from a CUDA graph; `steps` mirrors it on the host."""
 
     def __init__(self, params: Sequence[nn.Parameter], lr: float, betas=(0.9, 0.999), eps: float = 1e-8,
                  weight_decay: float = 0.0, shadow_dtype=torch.bfloat16):
@@ -54,6 +56,7 @@ class FlatAdamW:
         self.M = torch.zeros(n, dtype=torch.float32, device=dev)
         self.V = torch.zeros(n, dtype=torch.float32, device=dev)
         self.S = torch.empty(n, dtype=shadow_dtype, device=dev) if shadow_dtype is not None else None
+        self.counter = torch.zeros(2, dtype=torch.int64, device=dev)   # updates taken, block ticket
         off = 0
         with torch.no_grad():
             for p in self.params:
@@ -80,10 +83,10 @@ class FlatAdamW:
             self.S.copy_(self.P)             # a master was changed elsewhere: resync the compute copies
         self.steps += 1
         N = self.N
-        N.check(N.load().lors_adamw(self.P.data_ptr(), self.G.data_ptr(), self.M.data_ptr(), self.V.data_ptr(),
-                                    None if self.S is None else self.S.data_ptr(), self.n, self.lr, self.b1,
-                                    self.b2, self.eps, self.wd, self.steps,
-                                    torch.cuda.current_stream(self.P.device).cuda_stream))
+        N.check(N.load().lors_adamw_dstep(self.P.data_ptr(), self.G.data_ptr(), self.M.data_ptr(),
+                                          self.V.data_ptr(), None if self.S is None else self.S.data_ptr(), self.n,
+                                          self.lr, self.b1, self.b2, self.eps, self.wd, self.counter.data_ptr(),
+                                          torch.cuda.current_stream(self.P.device).cuda_stream))
         self._mark()
 
     def zero_grad(self, set_to_none: bool = True) -> None:
@@ -95,7 +98,7 @@ class Trainer:
     def __init__(self, model: nn.Module, lr: float = 2e-5, betas=(0.9, 0.999), eps: float = 1e-8,
                  weight_decay: float = 0.0, process_group=None, overlap: bool = True,
                  bucket_bytes: int = 64 << 20, params: Optional[Sequence[nn.Parameter]] = None,
-                 optimizer: str = "auto", check_finite: bool = False):
+                 optimizer: str = "auto", check_finite: bool = False, cuda_graph: bool = False):
         self.model = model
         self.check_every_step = check_finite   # NumericError on a non-finite loss (train.py:215-217); syncs
         self.params = list(params) if params is not None else [p for p in model.parameters() if p.requires_grad]
@@ -120,10 +123,68 @@ class Trainer:
             self.opt = torch.optim.AdamW(self.params, lr=lr, betas=betas, eps=eps, weight_decay=weight_decay,
                                          fused=all(p.is_cuda for p in self.params))
         self.steps = 0
+        # cuda_graph: after one eager step, the whole step (forward, CE, backward, AdamW) is captured
+        # once per token shape and replayed -- one graph launch instead of ~2300 kernel launches
+        # from Python (tools/graph_probe.py).  One process, the native optimizer; the adapters must
+        # change only through this trainer (call invalidate_graph() after loading weights).
+        self.cuda_graph = bool(cuda_graph)
+        if self.cuda_graph and (self.world > 1 or not isinstance(self.opt, FlatAdamW)):
+            raise ArgumentError("cuda_graph needs one process and the native optimizer (FlatAdamW)")
+        self._graph = None
+        self._static_tokens = None
+        self._static_loss = None
+        self.graph_launches = 0      # native kernel launches recorded into the graph (one step)
 
     def step(self, tokens: torch.Tensor) -> torch.Tensor:
         """One fine-tuning step on this rank's tokens [B, S + 1]; returns the (local) loss
         as a device scalar -- no host synchronisation."""
+        if self.cuda_graph:
+            return self._step_graphed(tokens)
+        return self._step_eager(tokens)
+
+    def invalidate_graph(self) -> None:
+        """Drop the captured step (the next step runs eagerly and captures again)."""
+        self._graph = None
+        self._static_tokens = None
+        self._static_loss = None
+
+    def _step_graphed(self, tokens: torch.Tensor) -> torch.Tensor:
+        st = self._static_tokens
+        same = st is not None and st.shape == tokens.shape and st.dtype == tokens.dtype
+        if self._graph is not None and not same:
+            self.invalidate_graph()                    # a new token shape: warm up and capture again
+        if self._graph is None:
+            if not same:
+                loss = self._step_eager(tokens)        # warm-up: lazy handles and workspaces exist
+                self._static_tokens = torch.empty_like(tokens, device=self.opt.P.device)
+                return loss
+            self._capture()
+        self._static_tokens.copy_(tokens, non_blocking=True)
+        self._graph.replay()
+        self.opt.steps += 1
+        self.steps += 1
+        if self.check_every_step:
+            self.check_finite(self._static_loss, self.steps - 1)
+        return self._static_loss.clone()
+
+    def _capture(self) -> None:
+        from . import _native as N
+        torch.cuda.synchronize()
+        self.opt.zero_grad(set_to_none=True)
+        torch.cuda.empty_cache()     # the warm-up step's cached blocks: the graph gets its own pool
+        g = torch.cuda.CUDAGraph()
+        n0 = N.launch_count()
+        with torch.cuda.graph(g):
+            loss = self.model.loss(self._static_tokens)
+            loss.backward()
+            self.opt.step()
+            self.opt.zero_grad(set_to_none=True)
+        self.graph_launches = N.launch_count() - n0
+        self.opt.steps -= 1          # capture recorded the update without applying it
+        self._static_loss = loss.detach()
+        self._graph = g
+
+    def _step_eager(self, tokens: torch.Tensor) -> torch.Tensor:
         loss = self.model.loss(tokens)
         if self.check_every_step:
             self.check_finite(loss, self.steps)

@@ -290,9 +290,38 @@ def test_flat_adamw_matches_torch_adamw():
             assert torch.allclose(a, b, rtol=1e-5, atol=1e-7)
             assert compute_copy(a, torch.bfloat16) is a._lors_shadow
             assert torch.equal(compute_copy(a, torch.bfloat16), a.detach().bfloat16())
+    assert int(o1.counter[0]) == 6 and o1.steps == 6   # the device step count (lors_adamw_dstep)
     with torch.no_grad():                              # an outside in-place change: the cast path takes over
         p1[0].mul_(2.0)
     assert torch.equal(compute_copy(p1[0], torch.bfloat16), p1[0].detach().bfloat16())
+
+
+@pytest.mark.gpu
+def test_cuda_graph_trainer_matches_eager():
+    """Trainer(cuda_graph=True): one eager warm-up step, then the whole step (forward, CE, backward
+    through the LoRS kernels, AdamW with the device step count) captured once and replayed.  Same
+    losses and adapters as the eager trainer from the same initialisation and tokens, step by step
+    (tolerance: the eager and replayed runs may sum the split-K partials in a different order); a
+    new token shape re-captures; the captured step records the native launches it replays."""
+    from paper_2501_08582_b200 import decoder as D
+    from paper_2501_08582_b200.trainer import Trainer, synthetic_tokens
+    cfg = D.preset("tiny")
+    runs = []
+    for graph in (False, True):
+        model = D.LoRSDecoder(cfg, device="cuda", seed=3)
+        tr = Trainer(model, lr=1e-3, cuda_graph=graph)
+        losses = []
+        for s in range(5):
+            seq = cfg.seq if s < 4 else cfg.seq // 2          # the last step changes the shape
+            losses.append(float(tr.step(synthetic_tokens(cfg.vocab, cfg.batch, seq, s, device="cuda"))))
+        runs.append((losses, [p.detach().clone() for p in model.adapter_parameters()], tr))
+    (l0, p0, t0), (l1, p1, t1) = runs
+    assert t1._graph is None and t1.steps == t0.steps == 5 and t1.opt.steps == 5 and int(t1.opt.counter[0]) == 5
+    assert t1.graph_launches > 0
+    for a, b in zip(l0, l1):
+        assert abs(a - b) <= 1e-3 * abs(a), (l0, l1)
+    for a, b in zip(p0, p1):
+        assert torch.allclose(a, b, rtol=1e-3, atol=1e-6)
 
 
 @pytest.mark.gpu

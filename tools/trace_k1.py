@@ -49,9 +49,11 @@ for lbl, d in parts:
     print(f"  {lbl:24s} mean {d.mean():7.0f}  median {np.median(d):7.0f}")
 for cta in (0, 1):
     per = np.diff(t[cta, 13, lo:hi])
+    d = t[cta, 9, lo + 1:hi] - t[cta, 13, lo:hi - 1]
+    print(f"  xf arrive(j) -> start(j+1)     mean {d.mean():7.0f}  median {np.median(d):7.0f}")
     print(f"CTA {cta} transform period mean {per.mean():.0f}")
-    for a_, b_, lbl in ((9, 10, "xf wait refull"), (10, 11, "xf tmem ld + W wait"), (11, 12, "xf wait wempty"),
-                        (12, 13, "xf compute + store + arrive")):
+    for a_, b_, lbl in ((9, 10, "xf wait refull"), (10, 11, "xf tmem ld + W wait"), (11, 22, "xf W lds + tmem ld wait + release"),
+                        (22, 12, "xf wait wempty"), (12, 23, "xf compute + stores"), (23, 13, "xf fences + arrive")):
         d = t[cta, b_, lo:hi] - t[cta, a_, lo:hi]
         print(f"  {lbl:28s} mean {d.mean():7.0f}  median {np.median(d):7.0f}")
 d = T(0, 5, j) - T(0, 13, j)
