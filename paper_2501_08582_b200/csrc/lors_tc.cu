@@ -1190,14 +1190,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           for (int kk = 0; kk < RP / 16; ++kk)
             mma_bf16_pair(tmem + RE_COL + e * 64, ff_desc + kk * FF_KSTEP, sfd + kk * SF_KSTEP, idesc_re,
                           kk > 0 ? 1u : 0u);
-          LORS_TR(14, j);
           mma_commit_pair(&refull[(j % NGRP) * NE + e].b, 0x3);
           mma_commit_pair(&s_empty[sl].b, 0x3);
           if (PERSIST && rk == rlen - 1) mma_commit_pair(ff_empty, 0x3);   // fixed factor may be replaced
-          LORS_TR(15, j);
         }
         __syncwarp();
-        LORS_TR(16, j);
       };
       bool main_n2 = true;   // the second MMA's tokens (l0 + 256 ..) hold valid rows in this unit
       // the main MMAs of step jm (activation slot a, W_eff buffer wb) and the commits that free
@@ -1283,8 +1280,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           // the pipeline (tools/trace_k1.py: 1570 -> ~1030 cycles a k-step at cfg3)
           const int jm = j - D, e = j % NE, sl = j % NS, a = jm % NACT, wb = jm % NA;
           LORS_TR(0, j);
+#ifdef LORS_TRACE
+          // which barrier the issue loop waits for: one at a time, in the order they usually complete
+          mbar_wait(&wready[wb].b, (jm / NA) & 1);
+          LORS_TR(1, jm);
+          mbar_wait(&afull[a].b, (jm / NACT) & 1);
+          LORS_TR(2, jm);
+          mbar_wait(&sready[sl].b, (j / NS) & 1);
+          LORS_TR(4, jm);
+          mbar_wait(&refree[e].b, (j / NE) & 1);
+#else
           mbar_wait4(&sready[sl].b, (j / NS) & 1, &refree[e].b, (j / NE) & 1, &afull[a].b, (jm / NACT) & 1,
                      &wready[wb].b, (jm / NA) & 1);
+#endif
           LORS_TR(5, jm);
           tc_fence_after();
           if (elect_one()) {
@@ -1548,6 +1556,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         if (!hold_w) mbar_arrive(&wfree[wi].b);      // done reading the W tile
         mbar_arrive_cluster(wready_l + wb * 16);     // W_eff half ready for the pair MMA
         if (warp == 0) LORS_TR(13, i);
+        if (warp == 3) LORS_TR(14, i);   // arrival skew across the transform warps
+        if (warp == 5) LORS_TR(15, i);
+        if (warp == 7) LORS_TR(16, i);
       }
     };
     // Accumulator -> bf16 -> transposed staging: the accumulator is read in the MMA

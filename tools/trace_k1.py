@@ -40,13 +40,6 @@ d = T(0, 5, j - 1) - T(0, 0, j)
 print(f"  fast path: 4 barriers (rec j, main j-1) mean {d.mean():.0f} median {np.median(d):.0f}")
 d = T(0, 6, j - 1) - T(0, 5, j - 1)
 print(f"  fast path: issue rec + main + commits   mean {d.mean():.0f} median {np.median(d):.0f}")
-parts = [("wait sready", T(0, 1, j) - T(0, 0, j)), ("wait refree", T(0, 2, j) - T(0, 1, j)),
-         ("issue rec MMA", T(0, 14, j) - T(0, 2, j)), ("rec commits", T(0, 15, j) - T(0, 14, j)),
-         ("syncwarp", T(0, 16, j) - T(0, 15, j)), ("gap -> main", T(0, 3, j - 1) - T(0, 16, j)),
-         ("wait afull", T(0, 4, j - 1) - T(0, 3, j - 1)), ("wait wready", T(0, 5, j - 1) - T(0, 4, j - 1)),
-         ("issue 8 MMAs + commits", T(0, 6, j - 1) - T(0, 5, j - 1)), ("gap -> next rec", T(0, 0, j + 1) - T(0, 6, j - 1))]
-for lbl, d in parts:
-    print(f"  {lbl:24s} mean {d.mean():7.0f}  median {np.median(d):7.0f}")
 for cta in (0, 1):
     per = np.diff(t[cta, 13, lo:hi])
     d = t[cta, 9, lo + 1:hi] - t[cta, 13, lo:hi - 1]
@@ -58,6 +51,15 @@ for cta in (0, 1):
         print(f"  {lbl:28s} mean {d.mean():7.0f}  median {np.median(d):7.0f}")
 d = T(0, 5, j) - T(0, 13, j)
 print(f"issuer wready ok - CTA0 warp0 arrived: mean {d.mean():.0f}")
+for ev, w in ((14, 3), (15, 5), (16, 7)):
+    d = T(0, ev, j) - T(0, 13, j)
+    print(f"  CTA0 warp {w} arrived - warp 0 arrived: mean {d.mean():.0f} median {np.median(d):.0f}")
+last = np.max(np.stack([T(0, ev, j) for ev in (13, 14, 15, 16)]), axis=0)
+for ev, lbl in ((1, "wready(jm)"), (2, "afull(jm)"), (4, "sready(jm+D)"), (5, "refree(jm+D)")):
+    d = T(0, ev, j) - last
+    print(f"  issuer passed {lbl:14s} - last CTA0 warp arrived: mean {d.mean():6.0f} median {np.median(d):6.0f}")
+d = T(0, 5, j) - last
+print(f"issuer wready ok - last of CTA0 warps 0/3/5/7 arrived: mean {d.mean():.0f} median {np.median(d):.0f}")
 d = T(0, 10, j) - T(0, 2, j)
 print(f"xf refull ok - rec issue (rec queue + exec + signal): mean {d.mean():.0f}")
 # main(g) completion as seen by the activation producer (slot of step g + 3 freed by its commit)
