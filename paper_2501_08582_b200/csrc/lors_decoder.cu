@@ -1,7 +1,8 @@
 // Decoder-side helpers (include/lors_decoder.h): fused RoPE + head transpose.
-// Memory-bound elementwise work: one thread per 8 consecutive elements of a
-// head's first half (16-byte loads and stores of both halves), so a warp reads
-// and writes 512 contiguous bytes.
+// Memory-bound elementwise work: one thread per 8 consecutive elements of a head's
+// first half and their partners in the second half (16-byte loads and stores), for
+// four heads at once when H % 4 == 0.
+#include <type_traits>
 #include "../../include/lors_decoder.h"
 #include "lors_common.cuh"
 
@@ -26,41 +27,60 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   return v;
 }
 
-template <int LAYOUT>
+// One thread: 8 + 8 elements (both halves) of HPT consecutive heads at one (b, s) -- the
+// cos / sin rows are loaded once for the HPT heads and all x loads are issued before any
+// arithmetic.  IDX: the index type of the thread -> (b, s, head group, c) decomposition,
+// 32-bit whenever the thread count allows (64-bit division made the kernel issue-bound).
+template <int LAYOUT, int HPT, typename IDX>
 __global__ void rope_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
-                            const __nv_bfloat16* __restrict__ cs, const __nv_bfloat16* __restrict__ sn, int64_t B,
-                            int64_t S, int64_t H, int hd, float sgn) {
+                            const __nv_bfloat16* __restrict__ cs, const __nv_bfloat16* __restrict__ sn, IDX B,
+                            IDX S, IDX H, int hd, float sgn) {
   const int half = hd / 2, per_head = half / 8;
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t total = B * S * H * per_head;
+  const IDX HG = H / HPT;
+  const IDX idx = (IDX)blockIdx.x * (IDX)blockDim.x + (IDX)threadIdx.x;
+  const IDX total = B * S * HG * (IDX)per_head;
   if (idx >= total) return;
-  const int c = (int)(idx % per_head) * 8;
-  int64_t rest = idx / per_head;
+  const int c = (int)(idx % (IDX)per_head) * 8;
+  IDX rest = idx / (IDX)per_head;
   // LAYOUT 0 / 2 walk the input [B, S, H] order, LAYOUT 1 the input [B, H, S] order
-  int64_t b, s, h;
+  IDX b, s, hg;
   if (LAYOUT != 1) {
-    h = rest % H; rest /= H; s = rest % S; b = rest / S;
+    hg = rest % HG; rest /= HG; s = rest % S; b = rest / S;
   } else {
-    s = rest % S; rest /= S; h = rest % H; b = rest / H;
+    s = rest % S; rest /= S; hg = rest % HG; b = rest / HG;
   }
-  const int64_t bsh = ((b * S + s) * H + h) * hd;   // [B, S, H, hd]
-  const int64_t bhs = ((b * H + h) * S + s) * hd;   // [B, H, S, hd]
-  const int64_t in = LAYOUT == 1 ? bhs : bsh, out = LAYOUT == 0 ? bhs : bsh;   // 2: [B, S, H, hd] in place order
-  float x1[8], x2[8], c1[8], c2[8], s1[8], s2[8], o1[8], o2[8];
-  unpack8(*reinterpret_cast<const uint4*>(x + in + c), x1);
-  unpack8(*reinterpret_cast<const uint4*>(x + in + half + c), x2);
-  unpack8(__ldg(reinterpret_cast<const uint4*>(cs + s * hd + c)), c1);
-  unpack8(__ldg(reinterpret_cast<const uint4*>(cs + s * hd + half + c)), c2);
-  unpack8(__ldg(reinterpret_cast<const uint4*>(sn + s * hd + c)), s1);
-  unpack8(__ldg(reinterpret_cast<const uint4*>(sn + s * hd + half + c)), s2);
+  uint4 xa[HPT], xb[HPT];
+  int64_t outo[HPT];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    // rotate_half(x) = (-x2, x1)
-    o1[i] = fmaf(x1[i], c1[i], -sgn * x2[i] * s1[i]);
-    o2[i] = fmaf(x2[i], c2[i], sgn * x1[i] * s2[i]);
+  for (int k = 0; k < HPT; ++k) {
+    const IDX h = hg * HPT + k;
+    const int64_t bsh = (((int64_t)b * S + s) * H + h) * hd;   // [B, S, H, hd]
+    const int64_t bhs = (((int64_t)b * H + h) * S + s) * hd;   // [B, H, S, hd]
+    const int64_t in = LAYOUT == 1 ? bhs : bsh;
+    outo[k] = LAYOUT == 0 ? bhs : bsh;                         // 2: [B, S, H, hd] in place order
+    xa[k] = *reinterpret_cast<const uint4*>(x + in + c);
+    xb[k] = *reinterpret_cast<const uint4*>(x + in + half + c);
   }
-  *reinterpret_cast<uint4*>(y + out + c) = pack8(o1);
-  *reinterpret_cast<uint4*>(y + out + half + c) = pack8(o2);
+  float c1[8], c2[8], s1[8], s2[8];
+  const int64_t sr = (int64_t)s * hd;
+  unpack8(__ldg(reinterpret_cast<const uint4*>(cs + sr + c)), c1);
+  unpack8(__ldg(reinterpret_cast<const uint4*>(cs + sr + half + c)), c2);
+  unpack8(__ldg(reinterpret_cast<const uint4*>(sn + sr + c)), s1);
+  unpack8(__ldg(reinterpret_cast<const uint4*>(sn + sr + half + c)), s2);
+#pragma unroll
+  for (int k = 0; k < HPT; ++k) {
+    float x1[8], x2[8], o1[8], o2[8];
+    unpack8(xa[k], x1);
+    unpack8(xb[k], x2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      // rotate_half(x) = (-x2, x1)
+      o1[i] = fmaf(x1[i], c1[i], -sgn * x2[i] * s1[i]);
+      o2[i] = fmaf(x2[i], c2[i], sgn * x1[i] * s2[i]);
+    }
+    *reinterpret_cast<uint4*>(y + outo[k] + c) = pack8(o1);
+    *reinterpret_cast<uint4*>(y + outo[k] + half + c) = pack8(o2);
+  }
 }
 
 __global__ void swiglu_kernel(const uint4* __restrict__ g, const uint4* __restrict__ u, uint4* __restrict__ h,
@@ -584,7 +604,8 @@ extern "C" int lors_rope(const void* x, void* y, const void* cos_t, const void* 
     set_error("lors_rope: layout must be 0 ([B,S,H,hd] -> [B,H,S,hd]), 1 (the reverse) or 2 (no transpose)");
     return LORS_ERR_ARGUMENT;
   }
-  const int64_t total = B * S * H * (hd / 16);
+  const int hpt = H % 4 == 0 ? 4 : 1;
+  const int64_t total = B * S * (H / hpt) * (hd / 16);
   if (total == 0) return LORS_OK;
   const cudaStream_t s = (cudaStream_t)stream;
   const unsigned grid = (unsigned)ceil_div(total, 256);
@@ -593,9 +614,22 @@ extern "C" int lors_rope(const void* x, void* y, const void* cos_t, const void* 
   auto yp = (__nv_bfloat16*)y;
   auto cp = (const __nv_bfloat16*)cos_t;
   auto sp = (const __nv_bfloat16*)sin_t;
-  if (layout == 0) rope_kernel<0><<<grid, 256, 0, s>>>(xp, yp, cp, sp, B, S, H, (int)hd, sgn);
-  else if (layout == 1) rope_kernel<1><<<grid, 256, 0, s>>>(xp, yp, cp, sp, B, S, H, (int)hd, sgn);
-  else rope_kernel<2><<<grid, 256, 0, s>>>(xp, yp, cp, sp, B, S, H, (int)hd, sgn);
+  auto launch = [&](auto layout_c, auto hpt_c, auto idx_zero) {
+    using IDX = decltype(idx_zero);
+    rope_kernel<decltype(layout_c)::value, decltype(hpt_c)::value, IDX><<<grid, 256, 0, s>>>(
+        xp, yp, cp, sp, (IDX)B, (IDX)S, (IDX)H, (int)hd, sgn);
+  };
+  auto by_layout = [&](auto hpt_c, auto idx_zero) {
+    if (layout == 0) launch(std::integral_constant<int, 0>(), hpt_c, idx_zero);
+    else if (layout == 1) launch(std::integral_constant<int, 1>(), hpt_c, idx_zero);
+    else launch(std::integral_constant<int, 2>(), hpt_c, idx_zero);
+  };
+  auto by_hpt = [&](auto idx_zero) {
+    if (hpt == 4) by_layout(std::integral_constant<int, 4>(), idx_zero);
+    else by_layout(std::integral_constant<int, 1>(), idx_zero);
+  };
+  if (total < ((int64_t)1 << 31)) by_hpt(uint32_t(0));
+  else by_hpt(int64_t(0));
   LORS_CHECK_LAUNCH("rope");
   return LORS_OK;
 }
