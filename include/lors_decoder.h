@@ -29,6 +29,10 @@ int lors_rope(const void* x, void* y, const void* cos_t, const void* sin_t, int6
 int lors_swiglu(const void* g, const void* u, void* h, int64_t n, void* stream);
 int lors_swiglu_bwd(const void* dh, const void* g, const void* u, void* dg, void* du, int64_t n, void* stream);
 
+/* out = a + b (+ c when c != NULL), bf16, n elements (n % 8 == 0, 16-byte aligned), summed in fp32 and
+ * rounded once; out may alias a.  The input gradient of projections sharing one input (q/k/v, gate/up). */
+int lors_add3(const void* a, const void* b, const void* c, void* out, int64_t n, void* stream);
+
 /* Residual add fused with the RMSNorm that follows it (pre-norm decoder), bf16 rows of D elements
  * (D % 8 == 0, D <= 8192), gamma [D] bf16, fp32 arithmetic:
  *   forward   hn = bf16(h + o)            (o may be NULL: hn = h and `hn` may be NULL)
@@ -63,7 +67,8 @@ int lors_adamw(float* p, const float* g, float* m, float* v, void* shadow, int64
 /* lors_adamw with the step count on the device, for CUDA-graph capture (trainer.Trainer(cuda_graph=True)):
  * counter = int64[2] in device memory, zero-initialised; counter[0] = updates taken so far.  The call applies
  * update t = counter[0] + 1 (bias corrections computed on the device from t, in double as lors_adamw does on
- * the host) and leaves counter[0] = t when the launch completes; counter[1] is scratch. */
+ * the host, by a one-thread launch ahead of the elementwise one) and leaves counter[0] = t; counter[1] is
+ * scratch (the two corrections). */
 int lors_adamw_dstep(float* p, const float* g, float* m, float* v, void* shadow, int64_t n, float lr, float beta1,
                      float beta2, float eps, float weight_decay, int64_t* counter, void* stream);
 

@@ -37,7 +37,7 @@ EXPORTED_SYMBOLS = (
     "lors_launch_count", "lors_reset_launch_count",
 )
 # include/lors_decoder.h: decoder-side helpers (not the LoRS drop-in boundary)
-DECODER_SYMBOLS = ("lors_rope", "lors_swiglu", "lors_swiglu_bwd", "lors_add_rmsnorm", "lors_add_rmsnorm_bwd",
+DECODER_SYMBOLS = ("lors_rope", "lors_swiglu", "lors_swiglu_bwd", "lors_add3", "lors_add_rmsnorm", "lors_add_rmsnorm_bwd",
                    "lors_cross_entropy", "lors_cross_entropy_bwd", "lors_adamw", "lors_adamw_dstep",
                    "lors_adamw_p2p")
 
@@ -110,6 +110,8 @@ def load(path: str = LIB_PATH) -> ct.CDLL:
         lib.lors_swiglu.restype = ct.c_int
         lib.lors_swiglu_bwd.argtypes = [_vp, _vp, _vp, _vp, _vp, ct.c_int64, _vp]
         lib.lors_swiglu_bwd.restype = ct.c_int
+        lib.lors_add3.argtypes = [_vp, _vp, _vp, _vp, ct.c_int64, _vp]
+        lib.lors_add3.restype = ct.c_int
         lib.lors_add_rmsnorm.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, ct.c_int64, ct.c_int64, ct.c_float, _vp]
         lib.lors_add_rmsnorm.restype = ct.c_int
         lib.lors_add_rmsnorm_bwd.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, ct.c_int64, ct.c_int64, _vp]

@@ -95,6 +95,26 @@ __global__ void swiglu_kernel(const uint4* __restrict__ g, const uint4* __restri
   h[i] = pack8(o);
 }
 
+// out = bf16(a + b (+ c)), the sum in fp32 (the grouped projections' input gradient: one pass
+// over the two or three dX instead of one bf16 add per extra projection)
+__global__ void add3_kernel(const uint4* __restrict__ a, const uint4* __restrict__ b, const uint4* __restrict__ c,
+                            uint4* __restrict__ out, int64_t n8) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n8) return;
+  float af[8], bf[8], cf[8];
+  unpack8(a[i], af);
+  unpack8(b[i], bf);
+  if (c != nullptr) {
+    unpack8(c[i], cf);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) af[k] = af[k] + bf[k] + cf[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) af[k] += bf[k];
+  }
+  out[i] = pack8(af);
+}
+
 __global__ void swiglu_bwd_kernel(const uint4* __restrict__ dh, const uint4* __restrict__ g,
                                   const uint4* __restrict__ u, uint4* __restrict__ dg, uint4* __restrict__ du,
                                   int64_t n8) {
@@ -131,41 +151,34 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
 }
 
 // AdamW with the step counter on the device (a CUDA-graph replay reuses the launch, so the
-// bias correction cannot be a host argument): counter[0] = steps taken, counter[1] = block
-// ticket.  Every block reads t = counter[0] + 1 before taking a ticket; the last block to
-// finish stores t, so no block can see the new count.  Same element arithmetic as adamw_kernel.
+// bias correction cannot be a host argument): counter[0] = updates taken, counter[1] = scratch.
+// One thread advances the count and computes the two bias-correction scalars in double, as
+// lors_adamw does on the host; the elementwise update (adamw_kernel's arithmetic) reads them.
+__global__ void adamw_advance_kernel(unsigned long long* counter, float lr, float b1, float b2) {
+  const unsigned long long t = counter[0] + 1ull;
+  counter[0] = t;
+  const double bc1 = 1.0 - pow((double)b1, (double)t);
+  const double bc2 = 1.0 - pow((double)b2, (double)t);
+  float* sc = reinterpret_cast<float*>(&counter[1]);
+  sc[0] = (float)((double)lr / bc1);
+  sc[1] = (float)(1.0 / sqrt(bc2));
+}
+
 __global__ void adamw_dstep_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
-                                   float* __restrict__ v, __nv_bfloat16* __restrict__ shadow, int64_t n, float lr,
-                                   float decay, float b1, float b2, float eps, unsigned long long* counter) {
-  __shared__ float s_step_size, s_inv_sqrt_bc2;
-  __shared__ unsigned long long s_t;
-  if (threadIdx.x == 0) {
-    const unsigned long long t = *reinterpret_cast<volatile unsigned long long*>(counter) + 1ull;
-    const double bc1 = 1.0 - pow((double)b1, (double)t);
-    const double bc2 = 1.0 - pow((double)b2, (double)t);
-    s_step_size = (float)((double)lr / bc1);
-    s_inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
-    s_t = t;
-  }
-  __syncthreads();
+                                   float* __restrict__ v, __nv_bfloat16* __restrict__ shadow, int64_t n, float decay,
+                                   float b1, float b2, float eps, const unsigned long long* __restrict__ counter) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    const float gi = g[i];
-    const float mi = fmaf(b1, m[i], (1.0f - b1) * gi);
-    const float vi = fmaf(b2, v[i], (1.0f - b2) * gi * gi);
-    const float pi = p[i] * decay - s_step_size * mi / (sqrtf(vi) * s_inv_sqrt_bc2 + eps);
-    m[i] = mi;
-    v[i] = vi;
-    p[i] = pi;
-    if (shadow != nullptr) shadow[i] = __float2bfloat16_rn(pi);
-  }
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&counter[1], 1ull) == (unsigned long long)gridDim.x - 1ull) {
-      counter[0] = s_t;
-      counter[1] = 0ull;
-    }
-  }
+  if (i >= n) return;
+  const float* sc = reinterpret_cast<const float*>(&counter[1]);
+  const float step_size = sc[0], inv_sqrt_bc2 = sc[1];
+  const float gi = g[i];
+  const float mi = fmaf(b1, m[i], (1.0f - b1) * gi);
+  const float vi = fmaf(b2, v[i], (1.0f - b2) * gi * gi);
+  const float pi = p[i] * decay - step_size * mi / (sqrtf(vi) * inv_sqrt_bc2 + eps);
+  m[i] = mi;
+  v[i] = vi;
+  p[i] = pi;
+  if (shadow != nullptr) shadow[i] = __float2bfloat16_rn(pi);
 }
 
 // Peer-memory AdamW over one shard: 4 elements per thread (16-byte peer loads and stores).
@@ -248,9 +261,11 @@ extern "C" int lors_adamw_dstep(float* p, const float* g, float* m, float* v, vo
     return LORS_ERR_ARGUMENT;
   }
   if (n == 0) return LORS_OK;
+  auto* cnt = reinterpret_cast<unsigned long long*>(counter);
+  adamw_advance_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(cnt, lr, beta1, beta2);
+  LORS_CHECK_LAUNCH("adamw_advance");
   adamw_dstep_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(
-      p, g, m, v, (__nv_bfloat16*)shadow, n, lr, 1.0f - lr * weight_decay, beta1, beta2, eps,
-      reinterpret_cast<unsigned long long*>(counter));
+      p, g, m, v, (__nv_bfloat16*)shadow, n, 1.0f - lr * weight_decay, beta1, beta2, eps, cnt);
   LORS_CHECK_LAUNCH("adamw_dstep");
   return LORS_OK;
 }
@@ -549,6 +564,24 @@ extern "C" int lors_add_rmsnorm_bwd(const void* dhn, const void* dx, const void*
   else if (nv <= 2) go(add_rmsnorm_bwd_kernel<2>);
   else go(add_rmsnorm_bwd_kernel<4>);
   LORS_CHECK_LAUNCH("add_rmsnorm_bwd");
+  return LORS_OK;
+}
+
+extern "C" int lors_add3(const void* a, const void* b, const void* c, void* out, int64_t n, void* stream) {
+  using namespace lors;
+  if (!a || !b || !out) {
+    set_error("lors_add3: null pointer");
+    return LORS_ERR_ARGUMENT;
+  }
+  if (n < 0 || n % 8 != 0) {
+    set_error("lors_add3: element count must be a non-negative multiple of 8");
+    return LORS_ERR_SHAPE;
+  }
+  if (n == 0) return LORS_OK;
+  const int64_t n8 = n / 8;
+  add3_kernel<<<(unsigned)ceil_div(n8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)a, (const uint4*)b, (const uint4*)c, (uint4*)out, n8);
+  LORS_CHECK_LAUNCH("add3");
   return LORS_OK;
 }
 

@@ -206,9 +206,12 @@ class LoRSGroupFunction(torch.autograd.Function):
             main.wait_event(ev)
         grad_x = None
         if need_dx:
-            dx = dxs[0]
-            for d in dxs[1:]:
-                dx.add_(d)
+            if len(dxs) > 1 and dxs[0].dtype == torch.bfloat16 and dxs[0].numel() % 8 == 0:
+                dx = ops.sum_into(dxs)            # one fp32 pass over the projections' dX
+            else:
+                dx = dxs[0]
+                for d in dxs[1:]:
+                    dx.add_(d)
             grad_x = dx.view(x_shape).to(x_dtype)
         if any(prm.check_finite for prm in params_list):
             ops.require_finite("LoRS backward gradients", grad_x, *[t for r3 in res for t in r3])

@@ -345,6 +345,21 @@ def rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor, layout: int = 0,
     return y
 
 
+def sum_into(tensors) -> torch.Tensor:
+    """tensors[0] <- the sum of 2+ same-shape bf16 tensors, three at a time in fp32 (lors_add3);
+    returns tensors[0]."""
+    out = tensors[0]
+    if any(t.shape != out.shape or t.dtype != torch.bfloat16 or not t.is_contiguous() for t in tensors) \
+            or out.numel() % 8:
+        raise ShapeError("sum_into: contiguous bf16 tensors of one shape, a multiple of 8 elements")
+    rest = list(tensors[1:])
+    while rest:
+        b = rest.pop(0)
+        c = rest.pop(0) if rest else None
+        N.check(N.load().lors_add3(_p(out), _p(b), None if c is None else _p(c), _p(out), out.numel(), _stream()))
+    return out
+
+
 def swiglu(g: torch.Tensor, u: torch.Tensor) -> torch.Tensor:
     """h = silu(g) * u, bf16, one kernel (include/lors_decoder.h)."""
     if g.shape != u.shape or g.dtype != torch.bfloat16 or u.dtype != torch.bfloat16:

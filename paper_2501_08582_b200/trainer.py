@@ -56,7 +56,7 @@ class FlatAdamW:
         self.M = torch.zeros(n, dtype=torch.float32, device=dev)
         self.V = torch.zeros(n, dtype=torch.float32, device=dev)
         self.S = torch.empty(n, dtype=shadow_dtype, device=dev) if shadow_dtype is not None else None
-        self.counter = torch.zeros(2, dtype=torch.int64, device=dev)   # updates taken, block ticket
+        self.counter = torch.zeros(2, dtype=torch.int64, device=dev)   # updates taken, scratch
         off = 0
         with torch.no_grad():
             for p in self.params:

@@ -297,6 +297,22 @@ def test_flat_adamw_matches_torch_adamw():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 3, 4])
+def test_sum_into_matches_fp32_sum(n):
+    """ops.sum_into (lors_add3): the grouped projections' input gradient, summed in fp32 and
+    rounded once -- bit-equal to torch's fp32 sum rounded to bf16 for two or three terms."""
+    from paper_2501_08582_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(n)
+    ts = [torch.randn(513, 136, device="cuda", generator=g).bfloat16() for _ in range(n)]
+    ref = sum(t.float() for t in ts)
+    out = ops.sum_into([t.clone() for t in ts])
+    if n <= 3:
+        assert torch.equal(out, ref.bfloat16())
+    else:
+        assert torch.allclose(out.float(), ref, rtol=1e-2, atol=1e-2)
+
+
+@pytest.mark.gpu
 def test_cuda_graph_trainer_matches_eager():
     """Trainer(cuda_graph=True): one eager warm-up step, then the whole step (forward, CE, backward
     through the LoRS kernels, AdamW with the device step count) captured once and replayed.  Same

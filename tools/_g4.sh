@@ -1,0 +1,4 @@
+timeout 1200 python -m pytest tests/test_decoder.py tests/test_module_api.py -q -m gpu -x > gpurun_out/g4_tests.log 2>&1; tail -n 1 gpurun_out/g4_tests.log
+timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu --no-layer > gpurun_out/g4_bench.json 2> gpurun_out/g4_bench.err
+python -c "import json; d=json.loads(open('gpurun_out/g4_bench.json').read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['e2e']['value'], d['clocks']['sm_mhz'], d['gpu_launches'])"
+ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches_r02c.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-layer > gpurun_out/ncu_bench.log 2>&1; tail -2 gpurun_out/ncu_bench.log; wc -l gpurun_out/launches_r02c.csv
