@@ -761,7 +761,7 @@ constexpr bool persist() { return LORS_PERSIST; }
 template <bool SP>
 constexpr int xw() { return LORS_PERSIST ? LORS_XW_DENSE : (SP ? 16 : LORS_XW_DENSE); }
 template <bool SP>
-constexpr int threads() { return 32 * (xw<SP>() + 5); }
+constexpr int threads() { return 32 * (xw<SP>() + 4); }
 // Token tile of a CTA pair: 256 + N2 tokens per W_eff tile -- one N = 256 MMA and
 // one N = N2 MMA per k-step into two accumulators -- so each on-chip W_eff tile (its
 // rank-r recompute, transform and W load) serves 1.5x the tokens.  TMEM: acc 256 + N2
@@ -894,7 +894,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
   static_assert(!(SP && DX), "2:4 sparse tensor cores apply to the forward only (SURVEY C6)");
   static_assert(!EX || (!DX && !SP && LORS_PERSIST), "W_eff export runs the persistent forward prologue");
   constexpr int XW = xw<SP>(), XFORM_THREADS = 32 * XW;
-  constexpr int W_SF = XW, W_MMA = XW + 1, W_ACT = XW + 2, W_RELAY = XW + 3, W_WLOAD = XW + 4;
+  constexpr int W_SF = XW, W_MMA = XW + 1, W_ACT = XW + 2, W_RELAY = XW + 3;   // W ring: lane 1 of W_SF
   constexpr int NE = ne<SP>(), NS = ns<SP>(), NW = nw<SP>(), NA = na<SP>(), NACT = nact<SP>(), D = lookahead<SP>();
   constexpr int NGRP = XW / 8;          // transform groups (alternate k-steps)
   constexpr bool PERSIST = persist<SP>();
@@ -1076,11 +1076,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         else tma_load_2d(st, &tmS, &sready[sl].b, k0 + 32 * rank, 0);      // b cols, MN-major
       }
       }
-    }
-    cluster_wait();
-  } else if (warp == W_WLOAD) {
-    // ------------------------------------------------------------ W-ring producer (both CTAs)
-    if (lane == 0) {
+    } else if (lane == 1) {
+      // ---------------------------------------------------------- W-ring producer (both CTAs), a
+      // second lane of this warp: one fewer warp keeps the kernel at 12 warps, whose register
+      // budget is 168 a thread instead of 128 at 13
       for (int n = 0, g = 0; n < my_units; ++n) {
       int kb, ke, ut, part;
       unit(n, m0, l0, kb, ke, ut, part);
