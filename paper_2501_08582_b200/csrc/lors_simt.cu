@@ -150,11 +150,201 @@ __global__ void __launch_bounds__(NT) simt_lors_gemm_kernel(
   }
 }
 
+// S1v: the fp32 kernel when R and C are multiples of 4 (16-byte rows): 128 x 128 tiles, BK = 16,
+// the next k-tile's activation and W fragments fetched into registers (float4) while the current
+// one is multiplied, W_eff of the next tile built from those registers, two barriers a k-tile.
+// Same arithmetic and summation order as S1 (p over j, then the k-ascending fma chain), so the
+// two kernels agree bit for bit.
+namespace {
+constexpr int VBK = 16;
+}
+template <bool DX>
+__global__ void __launch_bounds__(NT, 2) simt_lors_gemm_v4_kernel(
+    const float* __restrict__ act, const float* __restrict__ w, const uint32_t* __restrict__ bits,
+    const float* __restrict__ a, const float* __restrict__ b, const float* __restrict__ bias,
+    float* __restrict__ out, int L, int R, int C, int r, float alpha) {
+  extern __shared__ float smem[];
+  float* sF = smem;                              // [r][BM] fixed factor
+  float* sS = sF + (size_t)r * BM;               // [2][VBK][r] streamed factor
+  float* sA = sS + (size_t)2 * VBK * r;          // [2][VBK][BL] activation, k-major
+  float* sW = sA + 2 * VBK * BL;                 // [2][VBK][BM] W_eff, k-major
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.x * BM, l0 = blockIdx.y * BL;
+  const int M = DX ? C : R, K = DX ? R : C;
+  const int64_t words = (C + 31) / 32;
+  for (int i = tid; i < r * BM; i += NT) {
+    int j, m;
+    float v = 0.f;
+    if (DX) {
+      j = i / BM; m = i % BM;
+      if (m0 + m < M) v = b[(int64_t)j * C + m0 + m];
+    } else {
+      m = i / r; j = i % r;
+      if (m0 + m < M) v = a[(int64_t)(m0 + m) * r + j];
+    }
+    sF[j * BM + m] = v;
+  }
+  // fragment ownership: activation row al (8 k from ak); W: FWD row wm (8 k from wk), DX row wk
+  // (m = wm .. wm+3 and wm+64 .. wm+67) -- a warp covers 32 rows (FWD / activation) or 2 rows of
+  // 128 m (DX W), every shared-memory access 16 bytes apart across the lanes
+  const int al = tid % BL, ak = (tid / BL) * 8;
+  const int wm = DX ? (tid % 16) * 4 : tid % BM;
+  const int wk = DX ? tid / 16 : (tid / BM) * 8;
+  float ra[8], rw[8];
+  auto fetch = [&](const int k0, const int buf) {
+    const int gl = l0 + al;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int gk = k0 + ak + 4 * h;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gl < L && gk < K) v = __ldg(reinterpret_cast<const float4*>(act + (int64_t)gl * K + gk));
+      ra[4 * h] = v.x; ra[4 * h + 1] = v.y; ra[4 * h + 2] = v.z; ra[4 * h + 3] = v.w;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (DX) {
+        const int gk = k0 + wk, gm = m0 + wm + 64 * h;
+        if (gk < K && gm < M) v = __ldg(reinterpret_cast<const float4*>(w + (int64_t)gk * C + gm));
+      } else {
+        const int gm = m0 + wm, gk = k0 + wk + 4 * h;
+        if (gm < M && gk < K) v = __ldg(reinterpret_cast<const float4*>(w + (int64_t)gm * C + gk));
+      }
+      rw[4 * h] = v.x; rw[4 * h + 1] = v.y; rw[4 * h + 2] = v.z; rw[4 * h + 3] = v.w;
+    }
+    // streamed factor, laid out for stage(): DX [k][j] (a rows), FWD [j][k] (b rows)
+    float* ss = sS + (size_t)buf * VBK * r;
+    for (int i = tid; i < VBK * r; i += NT) {
+      int k, j;
+      float v = 0.f;
+      if (DX) {
+        k = i / r; j = i % r;
+        if (k0 + k < K) v = a[(int64_t)(k0 + k) * r + j];
+        ss[k * r + j] = v;
+      } else {
+        j = i / VBK; k = i % VBK;
+        if (k0 + k < K) v = b[(int64_t)j * C + k0 + k];
+        ss[j * VBK + k] = v;
+      }
+    }
+  };
+  // W_eff of the fetched fragment (needs sS[buf]) and both fragments into shared memory
+  auto stage = [&](const int k0, const int buf) {
+    const float* ss = sS + (size_t)buf * VBK * r;
+    float* sa = sA + (size_t)buf * VBK * BL;
+    float* sw = sW + (size_t)buf * VBK * BM;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sa[(ak + e) * BL + al] = ra[e];
+    // rank-r product of the thread's 8 elements, p[e] = sum_j F[j][m_e] S[k_e][j] in j order (S1's
+    // fma chain); FWD: one m, 8 k (S row j as two float4); DX: one k, 8 m (F row j as two float4)
+    float p[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) p[e] = 0.f;
+    for (int j = 0; j < r; ++j) {
+      float f[8], sv[8];
+      if (DX) {
+        const float4 f0 = *reinterpret_cast<const float4*>(sF + j * BM + wm);
+        const float4 f1 = *reinterpret_cast<const float4*>(sF + j * BM + wm + 64);
+        f[0] = f0.x; f[1] = f0.y; f[2] = f0.z; f[3] = f0.w; f[4] = f1.x; f[5] = f1.y; f[6] = f1.z; f[7] = f1.w;
+        const float sk = ss[wk * r + j];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sv[e] = sk;
+      } else {
+        const float fm = sF[j * BM + wm];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] = fm;
+        const float4 s0 = *reinterpret_cast<const float4*>(ss + j * VBK + wk);
+        const float4 s1 = *reinterpret_cast<const float4*>(ss + j * VBK + wk + 4);
+        sv[0] = s0.x; sv[1] = s0.y; sv[2] = s0.z; sv[3] = s0.w; sv[4] = s1.x; sv[5] = s1.y; sv[6] = s1.z; sv[7] = s1.w;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) p[e] = fmaf(f[e], sv[e], p[e]);
+    }
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int km = DX ? wk : wk + e;           // k of element e (tile-local)
+      const int mm = DX ? wm + (e & 3) + 64 * (e >> 2) : wm;   // m of element e (tile-local)
+      const int gk = k0 + km, gm = m0 + mm;
+      v[e] = 0.f;
+      if (gm < M && gk < K) {
+        const int64_t row = DX ? gk : gm, col = DX ? gm : gk;
+        v[e] = weff_value<float>(mask_at(rw[e], bits, words, row, col), rw[e], p[e], alpha);
+      }
+      if (!DX) sw[km * BM + mm] = v[e];          // a warp: 32 consecutive m of one k row
+    }
+    if (DX) {                                    // the thread's two runs of 4 m in row wk
+      *reinterpret_cast<float4*>(sw + wk * BM + wm) = make_float4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<float4*>(sw + wk * BM + wm + 64) = make_float4(v[4], v[5], v[6], v[7]);
+    }
+  };
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  const int tx = tid % 16, ty = tid / 16;
+  fetch(0, 0);
+  __syncthreads();          // sF, sS[0]
+  stage(0, 0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < K; k0 += VBK, buf ^= 1) {
+    const bool more = k0 + VBK < K;
+    if (more) fetch(k0 + VBK, buf ^ 1);
+    const float* sa = sA + (size_t)buf * VBK * BL;
+    const float* sw = sW + (size_t)buf * VBK * BM;
+#pragma unroll
+    for (int k = 0; k < VBK; ++k) {
+      const float4 a0 = *reinterpret_cast<const float4*>(sa + k * BL + ty * 4);
+      const float4 a1 = *reinterpret_cast<const float4*>(sa + k * BL + 64 + ty * 4);
+      const float4 w0 = *reinterpret_cast<const float4*>(sw + k * BM + tx * 4);
+      const float4 w1 = *reinterpret_cast<const float4*>(sw + k * BM + 64 + tx * 4);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], wv[j], acc[i][j]);
+    }
+    if (more) {
+      __syncthreads();      // sS[buf ^ 1] written; everyone done with the other buffers' last use
+      stage(k0 + VBK, buf ^ 1);
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int l = l0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+    if (l >= L) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int m = m0 + h * 64 + tx * 4;
+      if (m >= M) continue;                     // M % 4 == 0: all four or none
+      float4 v = make_float4(acc[i][4 * h], acc[i][4 * h + 1], acc[i][4 * h + 2], acc[i][4 * h + 3]);
+      if (!DX && bias != nullptr) {
+        v.x += bias[m]; v.y += bias[m + 1]; v.z += bias[m + 2]; v.w += bias[m + 3];
+      }
+      *reinterpret_cast<float4*>(out + (int64_t)l * M + m) = v;
+    }
+  }
+}
+
 template <typename T>
 int simt_lors_gemm(bool dx, const T* act, const T* w, const uint32_t* bits, const T* a, const T* b,
                    const T* bias, T* out, int L, int R, int C, int r, float alpha, cudaStream_t s) {
   const int M = dx ? C : R;
   dim3 grid((unsigned)ceil_div(M, BM), (unsigned)ceil_div(L, BL));
+  if (sizeof(T) == 4 && R % 4 == 0 && C % 4 == 0) {   // 16-byte rows: the vectorised, pipelined kernel
+    const size_t sm = sizeof(float) * ((size_t)r * BM + (size_t)2 * VBK * r + 2 * VBK * BL + 2 * VBK * BM);
+    auto kv = dx ? simt_lors_gemm_v4_kernel<true> : simt_lors_gemm_v4_kernel<false>;
+    LORS_CUDA_TRY(cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+                  "simt_lors_gemm smem attribute");
+    kv<<<grid, NT, sm, s>>>((const float*)act, (const float*)w, bits, (const float*)a, (const float*)b,
+                            (const float*)bias, (float*)out, L, R, C, r, alpha);
+    LORS_CHECK_LAUNCH("simt_lors_gemm");
+    return LORS_OK;
+  }
   size_t smem = sizeof(float) * ((size_t)r * BM + (size_t)BK * r + BK * BL + BK * BM);
   auto kern = dx ? simt_lors_gemm_kernel<T, true> : simt_lors_gemm_kernel<T, false>;
   LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
