@@ -147,22 +147,26 @@ int lors_bwd(const lors_bwd_args* A, void* stream) {
     }
     if (dx_only) return LORS_OK;
     if (A->grad_mode == LORS_GRAD_STE) {
+      // fast mode splits every product along its reduction (fp32 atomics into a zeroed output;
+      // P and Q have only L / 64 row tiles); LORS_FLAG_DETERMINISTIC keeps one CTA per output
+      // tile, summed in k order, so dA / dB are bitwise reproducible
+      const bool split = (A->flags & LORS_FLAG_DETERMINISTIC) == 0;
       const size_t slot = ((size_t)L * r * sizeof(float) + 255) / 256 * 256;
       float* P = (float*)A->p;
       float* Q = (float*)((char*)A->workspace + slot);
       if (P == nullptr) {  // xt_bt = X^T b^T  (adapters.py:396)
         P = (float*)A->workspace;
-        st = simt_strided_gemm<float, float, float>(x, C, 1, b, C, 1, P, r, 1, L, r, C, 1.0f, false, s);
+        st = simt_strided_gemm<float, float, float>(x, C, 1, b, C, 1, P, r, 1, L, r, C, 1.0f, split, s);
         if (st) return st;
       }
       // at_dy = a^T dY (adapters.py:397): Q[l, j] = sum_n dY_t[l, n] a[n, j]
-      st = simt_strided_gemm<float, float, float>(dy, R, 1, a, 1, r, Q, r, 1, L, r, R, 1.0f, false, s);
+      st = simt_strided_gemm<float, float, float>(dy, R, 1, a, 1, r, Q, r, 1, L, r, R, 1.0f, split, s);
       if (st) return st;
       // da = alpha dY xt_bt (adapters.py:398): dA[n, j] = alpha sum_l dY_t[l, n] P[l, j]
-      st = simt_strided_gemm<float, float, float>(dy, 1, R, P, 1, r, A->da, r, 1, R, r, L, A->alpha, true, s);
+      st = simt_strided_gemm<float, float, float>(dy, 1, R, P, 1, r, A->da, r, 1, R, r, L, A->alpha, split, s);
       if (st) return st;
       // db = alpha at_dy X^T (adapters.py:399): dB[j, c] = alpha sum_l Q[l, j] X_t[l, c]
-      st = simt_strided_gemm<float, float, float>(Q, 1, r, x, 1, C, A->db, C, 1, r, C, L, A->alpha, true, s);
+      st = simt_strided_gemm<float, float, float>(Q, 1, r, x, 1, C, A->db, C, 1, r, C, L, A->alpha, split, s);
       if (st) return st;
     } else {
       st = simt_masked_grad<float>(dy, x, w, bits, a, b, A->da, A->db, L, R, C, r, A->alpha, s);

@@ -65,6 +65,29 @@ def test_adapter_grads_bitwise_reproducible(ops, R, C, L, r, grad_mode):
     assert orc.rel_l2(db.double().cpu().numpy(), db_ref) <= 2e-2
 
 
+def test_fp32_adapter_grads_bitwise_reproducible(ops):
+    """The fp32 parity mode under LORS_FLAG_DETERMINISTIC: P, Q, dA, dB each from one CTA per output
+    tile in k order (the fast mode splits them along the reduction with fp32 atomics)."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    R, C, L, r = 2048, 1024, 2048, 16
+    w = (torch.randn(R, C, device="cuda", generator=g) * 0.02) * (torch.rand(R, C, device="cuda", generator=g) > 0.5)
+    a = torch.randn(R, r, device="cuda", generator=g) * 0.05
+    b = torch.randn(r, C, device="cuda", generator=g) / r ** 0.5
+    x = torch.randn(L, C, device="cuda", generator=g)
+    dy = torch.randn(L, R, device="cuda", generator=g)
+    runs = []
+    for _ in range(3):
+        _, da, db, _ = ops.lors_bwd(x, w, a, b, dy, 2.0, need_dx=False, deterministic=True)
+        torch.cuda.synchronize()
+        runs.append((_bits(da), _bits(db)))
+    for other in runs[1:]:
+        for u, v in zip(runs[0], other):
+            assert torch.equal(u, v)
+    _, da_f, db_f, _ = ops.lors_bwd(x, w, a, b, dy, 2.0, need_dx=False, deterministic=False)
+    for u, v in ((da_f, da), (db_f, db)):
+        assert float((u - v).norm() / v.norm()) < 1e-5
+
+
 def test_fast_and_deterministic_modes_agree(ops):
     """Same sums in another order: the two modes differ only by fp32 summation order, which can
     flip the bf16 rounding of a few intermediate P / Q entries (adapters.py:396-397 products are
