@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(NT, 2) simt_lors_gemm_v4_kernel(
   const int wm = DX ? (tid % 16) * 4 : tid % BM;
   const int wk = DX ? tid / 16 : (tid / BM) * 8;
   float ra[8], rw[8];
+  uint32_t rb[2] = {0u, 0u};   // packed-mask words of the W fragment (FWD: one; DX: one per run of 4)
   auto fetch = [&](const int k0, const int buf) {
     const int gl = l0 + al;
 #pragma unroll
@@ -211,6 +212,14 @@ __global__ void __launch_bounds__(NT, 2) simt_lors_gemm_v4_kernel(
         if (gm < M && gk < K) v = __ldg(reinterpret_cast<const float4*>(w + (int64_t)gm * C + gk));
       }
       rw[4 * h] = v.x; rw[4 * h + 1] = v.y; rw[4 * h + 2] = v.z; rw[4 * h + 3] = v.w;
+    }
+    if (bits != nullptr) {   // the fragment's mask bits, fetched with it (8 k / 4 m share a word)
+#pragma unroll
+      for (int h = 0; h < (DX ? 2 : 1); ++h) {
+        const int gk = DX ? k0 + wk : k0 + wk, gm = DX ? m0 + wm + 64 * h : m0 + wm;
+        const int64_t row = DX ? gk : gm, col = DX ? gm : gk;
+        rb[h] = (gk < K && gm < M) ? __ldg(bits + row * words + (col >> 5)) : 0u;
+      }
     }
     // streamed factor, laid out for stage(): DX [k][j] (a rows), FWD [j][k] (b rows)
     float* ss = sS + (size_t)buf * VBK * r;
@@ -268,8 +277,9 @@ __global__ void __launch_bounds__(NT, 2) simt_lors_gemm_v4_kernel(
       const int gk = k0 + km, gm = m0 + mm;
       v[e] = 0.f;
       if (gm < M && gk < K) {
-        const int64_t row = DX ? gk : gm, col = DX ? gm : gk;
-        v[e] = weff_value<float>(mask_at(rw[e], bits, words, row, col), rw[e], p[e], alpha);
+        const int col = DX ? gm : gk;
+        const bool keep = bits != nullptr ? ((rb[DX ? (e >> 2) : 0] >> (col & 31)) & 1u) != 0u : rw[e] != 0.0f;
+        v[e] = weff_value<float>(keep, rw[e], p[e], alpha);
       }
       if (!DX) sw[km * BM + mm] = v[e];          // a warp: 32 consecutive m of one k row
     }
