@@ -157,6 +157,21 @@ __global__ void __launch_bounds__(NT) simt_lors_gemm_kernel(
 // two kernels agree bit for bit.
 namespace {
 constexpr int VBK = 16;
+// two independent fp32 fmas in one instruction (fma.rn.f32x2, sm_100): a 3-register FFMA issues
+// at half rate per SMSP, so the packed form doubles the FMA throughput; each lane rounds like fmaf
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void fma2(uint64_t& d, uint64_t a, uint64_t b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ float2 unpack2(uint64_t v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return make_float2(lo, hi);
+}
 }
 template <bool DX>
 __global__ void __launch_bounds__(NT, 2) simt_lors_gemm_v4_kernel(
@@ -246,28 +261,34 @@ __global__ void __launch_bounds__(NT, 2) simt_lors_gemm_v4_kernel(
     for (int e = 0; e < 8; ++e) sa[(ak + e) * BL + al] = ra[e];
     // rank-r product of the thread's 8 elements, p[e] = sum_j F[j][m_e] S[k_e][j] in j order (S1's
     // fma chain); FWD: one m, 8 k (S row j as two float4); DX: one k, 8 m (F row j as two float4)
-    float p[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) p[e] = 0.f;
+    uint64_t p2[4] = {0ull, 0ull, 0ull, 0ull};   // (p[2q], p[2q + 1]), packed fmas
     for (int j = 0; j < r; ++j) {
-      float f[8], sv[8];
       if (DX) {
         const float4 f0 = *reinterpret_cast<const float4*>(sF + j * BM + wm);
         const float4 f1 = *reinterpret_cast<const float4*>(sF + j * BM + wm + 64);
-        f[0] = f0.x; f[1] = f0.y; f[2] = f0.z; f[3] = f0.w; f[4] = f1.x; f[5] = f1.y; f[6] = f1.z; f[7] = f1.w;
         const float sk = ss[wk * r + j];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) sv[e] = sk;
+        const uint64_t sk2 = pack2(sk, sk);
+        fma2(p2[0], pack2(f0.x, f0.y), sk2);
+        fma2(p2[1], pack2(f0.z, f0.w), sk2);
+        fma2(p2[2], pack2(f1.x, f1.y), sk2);
+        fma2(p2[3], pack2(f1.z, f1.w), sk2);
       } else {
         const float fm = sF[j * BM + wm];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] = fm;
+        const uint64_t fm2 = pack2(fm, fm);
         const float4 s0 = *reinterpret_cast<const float4*>(ss + j * VBK + wk);
         const float4 s1 = *reinterpret_cast<const float4*>(ss + j * VBK + wk + 4);
-        sv[0] = s0.x; sv[1] = s0.y; sv[2] = s0.z; sv[3] = s0.w; sv[4] = s1.x; sv[5] = s1.y; sv[6] = s1.z; sv[7] = s1.w;
+        fma2(p2[0], fm2, pack2(s0.x, s0.y));
+        fma2(p2[1], fm2, pack2(s0.z, s0.w));
+        fma2(p2[2], fm2, pack2(s1.x, s1.y));
+        fma2(p2[3], fm2, pack2(s1.z, s1.w));
       }
+    }
+    float p[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) p[e] = fmaf(f[e], sv[e], p[e]);
+    for (int q = 0; q < 4; ++q) {
+      const float2 v = unpack2(p2[q]);
+      p[2 * q] = v.x;
+      p[2 * q + 1] = v.y;
     }
     float v[8];
 #pragma unroll
@@ -288,11 +309,11 @@ __global__ void __launch_bounds__(NT, 2) simt_lors_gemm_v4_kernel(
       *reinterpret_cast<float4*>(sw + wk * BM + wm + 64) = make_float4(v[4], v[5], v[6], v[7]);
     }
   };
-  float acc[8][8];
+  uint64_t acc2[4][8];   // (acc[2 ip][j], acc[2 ip + 1][j])
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < 8; ++j) acc2[i][j] = 0ull;
   const int tx = tid % 16, ty = tid / 16;
   fetch(0, 0);
   __syncthreads();          // sF, sS[0]
@@ -310,12 +331,14 @@ __global__ void __launch_bounds__(NT, 2) simt_lors_gemm_v4_kernel(
       const float4 a1 = *reinterpret_cast<const float4*>(sa + k * BL + 64 + ty * 4);
       const float4 w0 = *reinterpret_cast<const float4*>(sw + k * BM + tx * 4);
       const float4 w1 = *reinterpret_cast<const float4*>(sw + k * BM + 64 + tx * 4);
-      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const uint64_t ap[4] = {pack2(a0.x, a0.y), pack2(a0.z, a0.w), pack2(a1.x, a1.y), pack2(a1.z, a1.w)};
       const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < 8; ++j) {
+        const uint64_t wj = pack2(wv[j], wv[j]);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], wv[j], acc[i][j]);
+        for (int ip = 0; ip < 4; ++ip) fma2(acc2[ip][j], ap[ip], wj);
+      }
     }
     if (more) {
       __syncthreads();      // sS[buf ^ 1] written; everyone done with the other buffers' last use
@@ -323,6 +346,15 @@ __global__ void __launch_bounds__(NT, 2) simt_lors_gemm_v4_kernel(
       __syncthreads();
     }
   }
+  float acc[8][8];
+#pragma unroll
+  for (int ip = 0; ip < 4; ++ip)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float2 v = unpack2(acc2[ip][j]);
+      acc[2 * ip][j] = v.x;
+      acc[2 * ip + 1][j] = v.y;
+    }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int l = l0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
