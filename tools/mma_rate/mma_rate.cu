@@ -1,7 +1,8 @@
 // Experiment (tools only): tcgen05.mma issue-to-completion rate of back-to-back pair MMAs
 // (cta_group::2, M = 256, K = 16, bf16 -> fp32) for N = 256 / 128 / 64, operands resident in
 // shared memory (zeros), one CTA pair per SM pair -- is a small-N MMA as long as a large one?
-//   mma_rate <N> <count> [mix]   mix = 1: alternate N = 256 and N = 128 (the LoRS K1 k-step)
+//   mma_rate <N> <count> [mix]   mix = 1: alternate N = 256 and N = 128 (the LoRS K1 k-step);
+//   mix = 2 / 3: a whole K2 (2:4, r = 64) / K1 (dense, r = 16) k-step's MMAs, recompute included
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdio>
@@ -49,7 +50,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     if (elect_one()) {
       for (int c = 0; c < count; ++c) {
         const int kk = c & 3;
-        if (sp) {
+        if (mix >= 2) {
+          // one K2 k-step (mix 2: 2:4, r = 64) or K1 k-step (mix 3: dense, r = 16): the main MMAs into
+          // the two accumulators, then the recompute's N = 64 MMAs into column 384
+          const int nrec = mix == 2 ? 4 : 1;
+          if (mix == 2) {
+            const uint32_t s256 = make_idesc_bf16(256, 256, false, false, true), s128 = make_idesc_bf16(256, 128, false, false, true);
+            for (int h = 0; h < 2; ++h) mma_bf16_pair_sp(tmem, ad + h * 2, bd + h * 4, tmem + 448 + h * 4, s256, 1u);
+            for (int h = 0; h < 2; ++h) mma_bf16_pair_sp(tmem + 256, ad + h * 2, bd + h * 4, tmem + 448 + h * 4, s128, 1u);
+          } else {
+            for (int q = 0; q < 4; ++q) mma_bf16_pair(tmem, ad + q * 2, bd + q * 2, i256, 1u);
+            for (int q = 0; q < 4; ++q) mma_bf16_pair(tmem + 256, ad + q * 2, bd + q * 2, i128, 1u);
+          }
+          for (int q = 0; q < nrec; ++q) mma_bf16_pair(tmem + 384, ad + q * 2, bd + q * 2, i64, 1u);
+        } else if (sp) {
           const uint32_t isp = make_idesc_bf16(256, n, false, false, true);
           mma_bf16_pair_sp(tmem + (c & 1) * (n == 256 ? 256 : 0), ad + (c & 1) * 2, bd + (c & 1) * 4, tmem + 448 + (c & 1) * 4,
                            isp, 1u);
@@ -94,6 +108,11 @@ int main(int argc, char** argv) {
   }
   unsigned long long cyc; cudaMemcpy(&cyc, out, 8, cudaMemcpyDeviceToHost);
   const double macs = (double)count * 256.0 * (mix ? 384.0 : (double)n) * (sp ? 32.0 : 16.0) * (nsm / 2);
+  if (mix >= 2) {
+    printf("%s k-step pattern count %d: %.1f cycles per k-step (SM 0 pair) (%s)\n", mix == 2 ? "K2 2:4 r=64" : "K1 dense r=16",
+           count, (double)cyc / count, cudaGetErrorString(cudaGetLastError()));
+    return 0;
+  }
   printf("%sN %d%s count %d: %.1f us, %.1f cycles per MMA%s (SM 0 pair), %.0f TFLOP/s (%s)\n", sp ? "sparse " : "", n, mix ? " (256+128 mix)" : "",
          count, best * 1e3, (double)cyc / count / (mix ? 2 : 1), mix ? " instr" : "", 2 * macs / (best * 1e-3) / 1e12,
          cudaGetErrorString(cudaGetLastError()));
