@@ -1,8 +1,8 @@
 E=$PWD/paper_2501_08582_b200/_native/exp
-timeout 1200 python -m pytest tests/test_weff_identity.py tests/test_shape_sweep.py -q -m gpu -x > gpurun_out/la_tests.log 2>&1; tail -n 1 gpurun_out/la_tests.log
+LORS_B200_LIB=$E/na4/liblors_b200.so timeout 1200 python -m pytest tests/test_weff_identity.py tests/test_shape_sweep.py -q -m gpu -x > gpurun_out/la_tests.log 2>&1; tail -n 1 gpurun_out/la_tests.log
 for i in 1 2; do
-  for v in prev new; do
-    if [ $v = new ]; then timeout 300 python tools/ab_gemm.py >> gpurun_out/abla.log 2>&1; else LORS_B200_LIB=$E/$v/liblors_b200.so timeout 300 python tools/ab_gemm.py >> gpurun_out/abla.log 2>&1; fi
+  for v in prev na4; do
+    if false; then true; else LORS_B200_LIB=$E/$v/liblors_b200.so timeout 300 python tools/ab_gemm.py >> gpurun_out/abla.log 2>&1; fi
   done
 done
 python tools/ab_table.py gpurun_out/abla.log
