@@ -110,3 +110,42 @@ def test_model_projection_shapes(ops, name):
     _check_step(ops, R, C, 4096, r, pattern, ratio, seed=seed)
     if pattern == "two_four":   # cfg4's forwards can run on the sparse tensor cores (bench --sparse24)
         _check_step(ops, R, C, 4096, r, pattern, ratio, seed=seed + 1, sparse24=True)
+
+
+def _check_fp32(ops, R, C, L, r, seed, a_std, b_std, bits=False):
+    """The fp32 parity mode (FFMA kernels) against the oracle on the same fp32 inputs, rel-L2 <= 1e-4."""
+    from paper_2501_08582_b200 import prune
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    w = prune.prune_rowwise(torch.randn(R, C, device="cuda", generator=g) * 0.02, 0.5).contiguous()
+    a = (torch.randn(R, r, device="cuda", generator=g) * a_std).contiguous()
+    b = (torch.randn(r, C, device="cuda", generator=g) * b_std).contiguous()
+    x = torch.randn(L, C, device="cuda", generator=g)
+    dy = torch.randn(L, R, device="cuda", generator=g)
+    mb = ops.pack_mask(w) if bits else None
+    y, _ = ops.lors_fwd(x, w, a, b, 2.0, mask_bits=mb)
+    dx, da, db, _ = ops.lors_bwd(x, w, a, b, dy, 2.0, mask_bits=mb)
+    torch.cuda.synchronize()
+    sub = np.sort(np.random.default_rng(seed).choice(L, size=min(N_SUB, L), replace=False))
+    wd, ad, bd = _f64(w), _f64(a), _f64(b)
+    xs, dys = _f64(x[sub]).T, _f64(dy[sub]).T
+    y_ref = orc.lors_forward(wd, ad, bd, xs, 2.0)
+    dx_ref = orc.lors_backward(wd, ad, bd, xs, dys, 2.0).dx
+    da_ref, db_ref = orc.lors_adapter_grads(wd, ad, bd, _f64(x).T, _f64(dy).T, 2.0)
+    errs = {"y": _rel(_f64(y[sub]).T, y_ref), "dx": _rel(_f64(dx[sub]).T, dx_ref),
+            "da": _rel(_f64(da), da_ref), "db": _rel(_f64(db), db_ref)}
+    print(f"fp32 {R}x{C} L={L} r={r} bits={bits}: " + ", ".join(f"{k} {v:.2e}" for k, v in errs.items()))
+    assert max(errs.values()) <= 1e-4, errs
+
+
+def test_cfg1_fp32_full(ops):
+    """BASELINE configs[0] at full size in the fp32 parity mode: 4096 x 4096, 50% per-row mask, r = 16,
+    A ~ N(0, 1/r), B ~ N(0, 1e-3^2), 2048 tokens (the vectorised FFMA GEMM, R and C multiples of 4)."""
+    _check_fp32(ops, 4096, 4096, 2048, 16, seed=11, a_std=16 ** -0.5, b_std=1e-3)
+
+
+@pytest.mark.parametrize("R,C,L,r,bits", [(1028, 516, 300, 12, False), (1028, 516, 300, 12, True),
+                                          (1030, 518, 77, 5, False)])
+def test_fp32_ragged_shapes(ops, R, C, L, r, bits):
+    """Ragged fp32 shapes: tile edges of the vectorised kernel (R, C multiples of 4), its packed-mask
+    path, and the scalar kernel (R, C not multiples of 4)."""
+    _check_fp32(ops, R, C, L, r, seed=R + L, a_std=0.05, b_std=r ** -0.5, bits=bits)
