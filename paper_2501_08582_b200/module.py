@@ -49,6 +49,20 @@ def compute_copy(t: torch.Tensor, dt: torch.dtype) -> torch.Tensor:
     return src if src.dtype == dt and src.is_contiguous() else src.to(dt).contiguous()
 
 
+def grad_slots(lora_A, lora_B):
+    """(dA, dB) destinations inside the optimizer's flat fp32 gradient buffer (trainer.FlatAdamW sets
+    `_lors_grad_base` = (buffer, offset) on each adapter and keeps the buffer zeroed between steps), or
+    (None, None).  Used only while both adapters hold no gradient: the views become .grad as they are
+    (fresh view objects, so autograd takes them without a copy), which saves the per-layer fp32
+    gradient buffers, their zero fills and the optimizer's concatenation."""
+    ga, gb = getattr(lora_A, "_lors_grad_base", None), getattr(lora_B, "_lors_grad_base", None)
+    if ga is None or gb is None or lora_A.grad is not None or lora_B.grad is not None:
+        return None, None
+    (buf_a, off_a), (buf_b, off_b) = ga, gb
+    return (buf_a[off_a:off_a + lora_A.numel()].view(lora_A.shape),
+            buf_b[off_b:off_b + lora_B.numel()].view(lora_B.shape))
+
+
 class LoRSFunction(torch.autograd.Function):
     """y = x (W + alpha a b . M)^T + bias over x [..., in]."""
 
@@ -97,9 +111,12 @@ class LoRSFunction(torch.autograd.Function):
         a = compute_copy(lora_A, dt)
         b = compute_copy(lora_B, dt)
         need_dx = ctx.needs_input_grad[0]
+        da_out, db_out = grad_slots(lora_A, lora_B) if ctx.needs_input_grad[3] and ctx.needs_input_grad[4] \
+            else (None, None)
         dx, da, db, dbias = ops.lors_bwd(x2, weight, a, b, dy, params.alpha, p=p, mask_bits=params.mask_bits,
                                          grad_mode=params.grad_mode, need_dx=need_dx, with_bias=has_bias,
-                                         fault_da_sign=params.fault_da_sign)
+                                         fault_da_sign=params.fault_da_sign, da_out=da_out, db_out=db_out)
+        del da_out, db_out
         if params.check_finite:
             ops.require_finite("LoRS backward gradients", dx, da, db, dbias)
         grad_x = dx.view(x_shape).to(x_dtype) if need_dx else None
@@ -194,10 +211,15 @@ class LoRSGroupFunction(torch.autograd.Function):
                                                      dx_only=True, launch_stream=streams[i])
                 dxs.append(dx)
                 keep.append(ws)
+            k = 2 + 4 * i
+            da_out, db_out = grad_slots(As[i], Bs[i]) if ctx.needs_input_grad[k + 2] and ctx.needs_input_grad[k + 3] \
+                else (None, None)
             _, da, db, dbias, ws = ops._lors_bwd_call(x2, weights[i], ab[i][0], ab[i][1], dys[i], prm.alpha, None,
                                                       prm.mask_bits, prm.grad_mode, False, has_bias[i],
                                                       prm.fault_da_sign, launch_stream=sides[i % len(sides)],
-                                                      deterministic=ops.deterministic_default())
+                                                      deterministic=ops.deterministic_default(),
+                                                      da_out=da_out, db_out=db_out)
+            del da_out, db_out
             res.append((da, db, dbias))
             keep.append(ws)
         for st in (streams if need_dx else []) + sides:

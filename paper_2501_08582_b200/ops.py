@@ -161,7 +161,8 @@ def deterministic_default() -> bool:
 def lors_bwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tensor, dy_t: torch.Tensor,
              alpha: float = 2.0, p: Optional[torch.Tensor] = None, mask_bits: Optional[torch.Tensor] = None,
              grad_mode: str = "ste", need_dx: bool = True, with_bias: bool = False,
-             fault_da_sign: bool = False, overlap: Optional[bool] = None, deterministic: Optional[bool] = None):
+             fault_da_sign: bool = False, overlap: Optional[bool] = None, deterministic: Optional[bool] = None,
+             da_out: Optional[torch.Tensor] = None, db_out: Optional[torch.Tensor] = None):
     """(dX_t [L, C] | None, dA [R, r] fp32, dB [r, C] fp32, dbias [R] fp32 | None).
 
     deterministic=True (LORS_FLAG_DETERMINISTIC): the adapter gradients' split-K
@@ -195,21 +196,25 @@ def lors_bwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
         # of these blocks is ordered after the side work: no record_stream (whose
         # deferred frees made the caching allocator grow with cudaMalloc stalls).
         _, da, db, dbias, ws = _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, False, with_bias,
-                                              fault_da_sign, launch_stream=side, deterministic=deterministic)
+                                              fault_da_sign, launch_stream=side, deterministic=deterministic,
+                                              da_out=da_out, db_out=db_out)
         join_hi.record(hi)
         join.record(side)
         main.wait_event(join_hi)
         main.wait_event(join)
         return dx, da, db, dbias
     return _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, with_bias,
-                          fault_da_sign, deterministic=deterministic)[:4]
+                          fault_da_sign, deterministic=deterministic, da_out=da_out, db_out=db_out)[:4]
 
 
 def _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, with_bias, fault_da_sign,
-                   dx_only: bool = False, launch_stream=None, deterministic: bool = False):
+                   dx_only: bool = False, launch_stream=None, deterministic: bool = False,
+                   da_out: Optional[torch.Tensor] = None, db_out: Optional[torch.Tensor] = None):
     """One lors_bwd C-ABI call: outputs and workspace allocated on the current
     stream, the kernels launched on `launch_stream` (default: the current stream).
-    Returns (dx, da, db, dbias, workspace)."""
+    da_out / db_out: zero-filled fp32 [R, r] / [r, C] destinations (views into an
+    optimizer's flat gradient buffer) used by the tensor-core STE path instead of a
+    fresh zeroed buffer.  Returns (dx, da, db, dbias, workspace)."""
     L, R, C, r = _check_layer(x_t, w, a, b)
     dt = w.dtype
     code = dtype_code(dt)
@@ -246,9 +251,14 @@ def _lors_bwd_call(x_t, w, a, b, dy_t, alpha, p, mask_bits, grad_mode, need_dx, 
     lib = N.load()
     ws_bytes = lib.lors_bwd_workspace(ct.byref(args))
     if zeroed:
-        buf = torch.zeros(da_b + db_b, dtype=torch.uint8, device=dev)
-        da = buf[:R * r * 4].view(torch.float32).view(R, r)
-        db = buf[da_b:da_b + r * C * 4].view(torch.float32).view(r, C)
+        if (da_out is not None and db_out is not None and tuple(da_out.shape) == (R, r)
+                and tuple(db_out.shape) == (r, C) and da_out.dtype == torch.float32
+                and db_out.dtype == torch.float32 and da_out.is_contiguous() and db_out.is_contiguous()):
+            da, db = da_out, db_out          # zero-filled by their owner (trainer.FlatAdamW.zero_grad)
+        else:
+            buf = torch.zeros(da_b + db_b, dtype=torch.uint8, device=dev)
+            da = buf[:R * r * 4].view(torch.float32).view(R, r)
+            db = buf[da_b:da_b + r * C * 4].view(torch.float32).view(r, C)
         args.flags |= N.FLAG_ZEROED
         if launch_stream is not None:
             # the fill ran on the current stream, after the caller's fork: order it

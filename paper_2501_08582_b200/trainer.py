@@ -58,11 +58,14 @@ class FlatAdamW:
         self.S = torch.empty(n, dtype=shadow_dtype, device=dev) if shadow_dtype is not None else None
         self.counter = torch.zeros(2, dtype=torch.int64, device=dev)   # updates taken, scratch
         off = 0
+        self._offs = []
         with torch.no_grad():
             for p in self.params:
                 k = p.numel()
                 self.P[off:off + k].copy_(p.detach().reshape(-1))
                 p.data = self.P[off:off + k].view_as(p)
+                p._lors_grad_base = (self.G, off)   # the LoRS backward may write dA / dB here (module.grad_slots)
+                self._offs.append(off)
                 if self.S is not None:
                     p._lors_shadow = self.S[off:off + k].view_as(p)
                 off += k
@@ -76,9 +79,23 @@ class FlatAdamW:
             p._lors_shadow_version = p._version
 
     def step(self) -> None:
-        grads = [p.grad.reshape(-1) if p.grad is not None else torch.zeros(p.numel(), device=self.P.device)
-                 for p in self.params]
-        torch.cat(grads, out=self.G)
+        # gradients the LoRS backward wrote straight into their slot of G stay there; the others
+        # (other layer types, accumulated micro-batches) are copied in
+        g0 = self.G.data_ptr()
+        in_place = [p.grad is not None and p.grad.data_ptr() == g0 + 4 * off and p.grad.is_contiguous()
+                    for p, off in zip(self.params, self._offs)]
+        if not any(in_place):
+            grads = [p.grad.reshape(-1) if p.grad is not None else torch.zeros(p.numel(), device=self.P.device)
+                     for p in self.params]
+            torch.cat(grads, out=self.G)
+        elif not all(in_place):
+            for p, off, ok in zip(self.params, self._offs, in_place):
+                if not ok:
+                    dst = self.G[off:off + p.numel()]
+                    if p.grad is None:
+                        dst.zero_()
+                    else:
+                        dst.copy_(p.grad.reshape(-1))
         if self.S is not None and any(p._version != p._lors_shadow_version for p in self.params):
             self.S.copy_(self.P)             # a master was changed elsewhere: resync the compute copies
         self.steps += 1
@@ -92,6 +109,7 @@ class FlatAdamW:
     def zero_grad(self, set_to_none: bool = True) -> None:
         for p in self.params:
             p.grad = None
+        self.G.zero_()    # the slots the next backward accumulates into start at zero
 
 
 class Trainer:

@@ -297,6 +297,30 @@ def test_flat_adamw_matches_torch_adamw():
 
 
 @pytest.mark.gpu
+def test_backward_writes_adapter_grads_into_the_flat_buffer():
+    """With FlatAdamW, the LoRS backward (grouped and single projections) writes dA / dB straight into
+    the optimizer's zeroed flat gradient buffer and autograd keeps those views as .grad (no per-layer
+    fp32 gradient buffers, no concatenation); a second backward before the step accumulates on top."""
+    from paper_2501_08582_b200 import decoder as D
+    from paper_2501_08582_b200.trainer import FlatAdamW, synthetic_tokens
+    cfg = D.preset("tiny")
+    model = D.LoRSDecoder(cfg, device="cuda", seed=5)
+    params = model.adapter_parameters()
+    opt = FlatAdamW(params, lr=1e-3)
+    toks = synthetic_tokens(cfg.vocab, cfg.batch, cfg.seq, 0, device="cuda")
+    model.loss(toks).backward()
+    g0 = opt.G.data_ptr()
+    in_place = [p.grad.data_ptr() == g0 + 4 * off for p, off in zip(params, opt._offs)]
+    assert all(in_place), sum(in_place)
+    first = [p.grad.clone() for p in params]
+    model.loss(toks).backward()                 # accumulation: same tokens, twice the gradient
+    for p, f in zip(params, first):
+        assert torch.allclose(p.grad, 2 * f, rtol=1e-3, atol=1e-7)
+    opt.zero_grad()
+    assert float(opt.G.abs().sum()) == 0.0
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("n", [2, 3, 4])
 def test_sum_into_matches_fp32_sum(n):
     """ops.sum_into (lors_add3): the grouped projections' input gradient, summed in fp32 and
