@@ -104,7 +104,10 @@ int lors_fwd(const lors_fwd_args* A, void* stream) {
   if (A->dtype == LORS_DTYPE_F32) {
     if (A->flags & LORS_FLAG_SPARSE24) return fail(LORS_ERR_ARGUMENT, "2:4 sparse tensor cores need bf16");
     const float *x = (const float*)A->x, *w = (const float*)A->w, *a = (const float*)A->a, *b = (const float*)A->b;
-    st = simt_lors_gemm<float>(false, x, w, bits, a, b, (const float*)A->bias, (float*)A->y, L, R, C, r, A->alpha, s);
+    // tensor cores (3xTF32) where TMA can address the fp32 rows, else the FFMA kernels
+    st = tf32x3_lors_gemm(false, x, w, a, b, bits, (const float*)A->bias, (float*)A->y, L, R, C, r, A->alpha, s);
+    if (st == LORS_ERR_SHAPE)
+      st = simt_lors_gemm<float>(false, x, w, bits, a, b, (const float*)A->bias, (float*)A->y, L, R, C, r, A->alpha, s);
     if (st) return st;
     if (A->flags & LORS_FLAG_EMIT_P)  // P[l, j] = sum_c X_t[l, c] b[j, c]
       st = simt_strided_gemm<float, float, float>(x, C, 1, b, C, 1, (float*)A->p, r, 1, L, r, C, 1.0f, false, s);
@@ -142,7 +145,9 @@ int lors_bwd(const lors_bwd_args* A, void* stream) {
     const float *x = (const float*)A->x, *w = (const float*)A->w, *a = (const float*)A->a,
                 *b = (const float*)A->b, *dy = (const float*)A->dy;
     if (!(A->flags & LORS_FLAG_NO_DX)) {  // dX_t = dY_t W_eff  (adapters.py:395)
-      st = simt_lors_gemm<float>(true, dy, w, bits, a, b, nullptr, (float*)A->dx, L, R, C, r, A->alpha, s);
+      st = tf32x3_lors_gemm(true, dy, w, a, b, bits, nullptr, (float*)A->dx, L, R, C, r, A->alpha, s);
+      if (st == LORS_ERR_SHAPE)
+        st = simt_lors_gemm<float>(true, dy, w, bits, a, b, nullptr, (float*)A->dx, L, R, C, r, A->alpha, s);
       if (st) return st;
     }
     if (dx_only) return LORS_OK;

@@ -2598,4 +2598,295 @@ int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {
   return LORS_OK;
 }
 
+
+// ===========================================================================
+// K8: the fp32 parity mode's forward / dX on the tensor cores, 3xTF32:
+//   out[t, m] = sum_k act[t, k] * Weff(m, k)
+//   (FWD: act = X_t, Weff(m, k) = W_eff[m, k]; DX: act = dY_t, Weff(m, k) = W_eff[k, m])
+// Each fp32 operand is split x = hi + lo (hi: the top 19 bits, what a TF32 MMA reads; lo = x - hi,
+// exact), and D = A_hi B_hi + A_hi B_lo + A_lo B_hi in fp32 (TMEM) -- rel-L2 ~1e-6, inside the
+// fp32 bar (1e-4) that plain TF32 misses.  W_eff is built by the FFMA kernels'
+// weff_value (same p = sum_j fixed_j * streamed_j order), so the effective weight is the same
+// fp32 value; only the GEMM's summation differs.  One CTA per [128 tokens x 128 features]
+// tile, BK = 32 (one 128-byte SW128 row of fp32), two stages:
+//   warp 8: TMA (activation tile, W tile, the streamed factor slice) into stage s
+//   warps 0-7: split the activation tile in place (hi) + lo copy; W_eff of the W tile, split,
+//              written K-major into two B tiles
+//   warp 9: 12 MMAs per k-step (4 x K8, three products), M = N = 128, kind::tf32
+//   warps 0-3: epilogue, TMEM -> registers -> out (+bias)
+// ===========================================================================
+namespace t3 {
+constexpr int BT = 128, BF = 128, BK = 32, NR = 2, NS = 2, THREADS = 320;
+constexpr uint32_t TILE = 128 * 128;                       // one [128][32] fp32 tile, bytes
+template <int RP>
+constexpr uint32_t fac_bytes() { return 32 * RP * 4; }     // streamed factor slice, fp32
+// raw ring (TMA): activation, W, factor slice; split ring (transform -> MMA): act hi, act lo, B hi, B lo.
+// The raw slot is released once the transform has read it, so the next TMA does not wait for the MMAs.
+template <int RP>
+constexpr uint32_t raw_bytes() { return 2 * TILE + fac_bytes<RP>(); }
+constexpr uint32_t SPLIT_BYTES = 4 * TILE;
+template <int RP>
+constexpr size_t smem_bytes() { return 1024 + NR * raw_bytes<RP>() + NS * SPLIT_BYTES + 256; }
+__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+}  // namespace t3
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+template <bool DX, int RP>
+__global__ void __launch_bounds__(t3::THREADS, 1)
+    tf32x3_lors_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant__ CUtensorMap tmW,
+                       const __grid_constant__ CUtensorMap tmS, const float* __restrict__ a,
+                       const float* __restrict__ b, const uint32_t* __restrict__ bits,
+                       const float* __restrict__ bias, float* __restrict__ out, int L, int R, int C, int r,
+                       float alpha) {
+  using namespace t3;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* split = smem;                                   // [NS] x (act hi, act lo, B hi, B lo)
+  uint8_t* raw = smem + NS * SPLIT_BYTES;                  // [NR] x (act, W, factor)
+  uint64_t* rfull = reinterpret_cast<uint64_t*>(raw + NR * raw_bytes<RP>());
+  uint64_t* rempty = rfull + NR;
+  uint64_t* sfull = rempty + NR;
+  uint64_t* sempty = sfull + NS;
+  uint64_t* accf = sempty + NS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  const int warp = warp_id(), lane = lane_id();
+  const int M = DX ? C : R, K = DX ? R : C;
+  const int m0 = blockIdx.x * BF, t0 = blockIdx.y * BT;
+  const int nk = (K + BK - 1) / BK;
+  const int64_t words = (C + 31) / 32;
+  auto ract = [&](int s) { return raw + s * raw_bytes<RP>(); };
+  auto rw = [&](int s) { return raw + s * raw_bytes<RP>() + TILE; };
+  auto rfac = [&](int s) { return raw + s * raw_bytes<RP>() + 2 * TILE; };
+  auto ahi = [&](int s) { return split + s * SPLIT_BYTES; };
+  auto alo = [&](int s) { return split + s * SPLIT_BYTES + TILE; };
+  auto bhi = [&](int s) { return split + s * SPLIT_BYTES + 2 * TILE; };
+  auto blo = [&](int s) { return split + s * SPLIT_BYTES + 3 * TILE; };
+  if (warp == 8 && lane == 0) {
+    for (int i = 0; i < NR; ++i) {
+      mbar_init(&rfull[i], 1);
+      mbar_init(&rempty[i], 8);
+    }
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&sfull[i], 8);
+      mbar_init(&sempty[i], 1);
+    }
+    mbar_init(accf, 1);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc<128>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 8) {
+    if (lane == 0) {
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % NR;
+        mbar_wait(&rempty[s], ((i / NR) & 1) ^ 1);
+        const int k0 = i * BK;
+        mbar_arrive_expect_tx(&rfull[s], 2 * TILE + fac_bytes<RP>());
+        tma_load_2d(ract(s), &tmAct, &rfull[s], k0, t0);                        // [128 t][32 k] SW128
+        if (DX) tma_load_2d(rw(s), &tmW, &rfull[s], m0, k0);                    // [32 k][128 m] plain
+        else tma_load_2d(rw(s), &tmW, &rfull[s], k0, m0);                       // [128 m][32 k] SW128
+        if (DX) tma_load_2d(rfac(s), &tmS, &rfull[s], 0, k0);                   // a [32 k][RP]
+        else tma_load_2d(rfac(s), &tmS, &rfull[s], k0, 0);                      // b [RP][32 k]
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(128, 128);
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % NS;
+        mbar_wait(&sfull[s], (i / NS) & 1);
+        tc_fence_after();
+        const uint64_t ah = make_sdesc(smem_u32(ahi(s)), 16, 1024, SW_128);
+        const uint64_t al = make_sdesc(smem_u32(alo(s)), 16, 1024, SW_128);
+        const uint64_t bh = make_sdesc(smem_u32(bhi(s)), 16, 1024, SW_128);
+        const uint64_t bl = make_sdesc(smem_u32(blo(s)), 16, 1024, SW_128);
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {   // K = 8 tf32 = 32 bytes of the 128-byte row
+          mma_tf32(tmem, ah + kk * 2, bh + kk * 2, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_tf32(tmem, ah + kk * 2, bl + kk * 2, idesc, 1u);
+          mma_tf32(tmem, al + kk * 2, bh + kk * 2, idesc, 1u);
+        }
+        mma_commit(&sempty[s]);
+      }
+      mma_commit(accf);
+    }
+  } else {
+    // ---------------------------------------------------------------- transform warps 0-7
+    const int tid = threadIdx.x;            // 0 .. 255
+    const int row = tid % 128, half = tid / 128;   // activation row / W_eff feature; k half (16 k)
+    const int gm = m0 + row;
+    float fix[RP];                          // fixed factor of this feature: FWD a[m][j], DX b[j][m]
+#pragma unroll
+    for (int j = 0; j < RP; ++j) fix[j] = (j < r && gm < M) ? (DX ? b[(int64_t)j * C + gm] : a[(int64_t)gm * r + j]) : 0.f;
+    for (int i = 0; i < nk; ++i) {
+      const int sr = i % NR, ss = i % NS;
+      const int k0 = i * BK;
+      mbar_wait(&rfull[sr], (i / NR) & 1);
+      // this thread's raw values: activation row chunks, W row / column, into registers
+      uint32_t av[16];
+      const uint32_t arow = smem_u32(ract(sr)) + row * 128;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        lds128(arow + (uint32_t)(((half * 4 + c) ^ (row & 7)) << 4), *reinterpret_cast<uint32_t(*)[4]>(&av[4 * c]));
+      float wv[16];
+      if (DX) {
+        const float* wr = reinterpret_cast<const float*>(rw(sr));   // [32 k][128 m]
+#pragma unroll
+        for (int e = 0; e < 16; ++e) wv[e] = wr[(half * 16 + e) * 128 + row];
+      } else {
+        const uint32_t wrow = smem_u32(rw(sr)) + row * 128;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t v[4];
+          lds128(wrow + (uint32_t)(((half * 4 + c) ^ (row & 7)) << 4), v);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) wv[4 * c + e] = __uint_as_float(v[e]);
+        }
+      }
+      // packed-mask words, fetched before the rank-r sums so their latency overlaps them:
+      // FWD one word (16 consecutive k of row gm), DX one per k row (column gm)
+      uint32_t mwd[DX ? 16 : 1];
+      if (bits != nullptr) {
+#pragma unroll
+        for (int e = 0; e < (DX ? 16 : 1); ++e) {
+          const int gk = k0 + half * 16 + e;
+          mwd[e] = (gm < M && gk < K) ? __ldg(bits + (int64_t)(DX ? gk : gm) * words + ((DX ? gm : gk) >> 5)) : 0u;
+        }
+      }
+      float pv[16];
+      const float* fac = reinterpret_cast<const float*>(rfac(sr));
+#pragma unroll
+      for (int e = 0; e < 16; ++e) pv[e] = 0.f;
+#pragma unroll
+      for (int j = 0; j < RP; ++j) {   // streamed factor: FWD b[j][k] ([RP][32]); DX a[k][j] ([32][RP])
+        if (j < r) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            pv[e] = fmaf(fix[j], DX ? fac[(half * 16 + e) * RP + j] : fac[j * BK + half * 16 + e], pv[e]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&rempty[sr]);   // raw slot read: the next TMA may overwrite it
+      float hv[16], lv[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int gk = k0 + half * 16 + e;
+        float v = 0.f;
+        if (gm < M && gk < K) {
+          const int wcol = DX ? gm : gk;
+          const bool keep = bits != nullptr ? ((mwd[DX ? e : 0] >> (wcol & 31)) & 1u) != 0u : wv[e] != 0.0f;
+          v = weff_value<float>(keep, wv[e], pv[e], alpha);
+        }
+        hv[e] = tf32_hi(v);
+        lv[e] = v - hv[e];
+      }
+      mbar_wait(&sempty[ss], ((i / NS) & 1) ^ 1);   // the MMAs of step i - NS are done with the split slot
+      const uint32_t hrow = smem_u32(ahi(ss)) + row * 128, lrow = smem_u32(alo(ss)) + row * 128;
+      const uint32_t bhrow = smem_u32(bhi(ss)) + row * 128, blrow = smem_u32(blo(ss)) + row * 128;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t off = (uint32_t)(((half * 4 + c) ^ (row & 7)) << 4);
+        float h[4], l[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          h[e] = tf32_hi(__uint_as_float(av[4 * c + e]));
+          l[e] = __uint_as_float(av[4 * c + e]) - h[e];
+        }
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(hrow + off), "f"(h[0]), "f"(h[1]), "f"(h[2]),
+                     "f"(h[3]) : "memory");
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lrow + off), "f"(l[0]), "f"(l[1]), "f"(l[2]),
+                     "f"(l[3]) : "memory");
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(bhrow + off), "f"(hv[4 * c]), "f"(hv[4 * c + 1]),
+                     "f"(hv[4 * c + 2]), "f"(hv[4 * c + 3]) : "memory");
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(blrow + off), "f"(lv[4 * c]), "f"(lv[4 * c + 1]),
+                     "f"(lv[4 * c + 2]), "f"(lv[4 * c + 3]) : "memory");
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sfull[ss]);
+    }
+    // ---------------------------------------------------------------- epilogue (warps 0-3: TMEM lanes)
+    if (warp < 4) {
+      mbar_wait(accf, 0);
+      tc_fence_after();
+      const int t = t0 + warp * 32 + lane;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BF; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld_x32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+        tmem_ld_wait();
+        if (t < L) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int m = m0 + c0 + 4 * q;
+            if (m < M) {   // M % 4 == 0
+              float4 o = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                     __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+              if (!DX && bias != nullptr) {
+                o.x += bias[m]; o.y += bias[m + 1]; o.z += bias[m + 2]; o.w += bias[m + 3];
+              }
+              *reinterpret_cast<float4*>(out + (int64_t)t * M + m) = o;
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) tmem_dealloc<128>(tmem);
+}
+
+template <bool DX, int RP>
+static int launch_tf32x3(const float* act, const float* w, const float* a, const float* b, const uint32_t* bits,
+                         const float* bias, float* out, int L, int R, int C, int r, float alpha, cudaStream_t s) {
+  using namespace t3;
+  const int M = DX ? C : R, K = DX ? R : C;
+  CUtensorMap tAct, tW, tS;
+  int st;
+  if ((st = make_map(&tAct, act, K, L, 32, 128, 128, "tf32 activation", true))) return st;
+  if (DX) st = make_map(&tW, w, C, R, 128, 32, 0, "tf32 W (dX)", true);     // [32 k rows][128 m], plain
+  else st = make_map(&tW, w, C, R, 32, 128, 128, "tf32 W", true);           // [128 m][32 k], SW128
+  if (st) return st;
+  if (DX) st = make_map(&tS, a, r, R, RP, 32, 0, "tf32 a slice", true);     // a [32 k][RP]
+  else st = make_map(&tS, b, C, r, 32, RP, 0, "tf32 b slice", true);        // b [RP][32 k]
+  if (st) return st;
+  auto kern = tf32x3_lors_kernel<DX, RP>;
+  const size_t smem = smem_bytes<RP>();
+  LORS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                "tf32x3 smem attribute");
+  dim3 grid((unsigned)ceil_div(M, BF), (unsigned)ceil_div(L, BT));
+  kern<<<grid, THREADS, smem, s>>>(tAct, tW, tS, a, b, bits, bias, out, L, R, C, r, alpha);
+  LORS_CHECK_LAUNCH(DX ? "tf32x3_lors<dx>" : "tf32x3_lors<fwd>");
+  (void)K;
+  return LORS_OK;
+}
+
+// fp32 forward / dX on the tensor cores when the shapes allow 16-byte TMA rows (R, C, r multiples of 4,
+// r <= 32); returns LORS_ERR_SHAPE otherwise (the caller runs the FFMA kernels)
+int tf32x3_lors_gemm(bool dx, const float* act, const float* w, const float* a, const float* b, const uint32_t* bits,
+                     const float* bias, float* out, int L, int R, int C, int r, float alpha, cudaStream_t s) {
+  if (R % 4 || C % 4 || r % 4 || r > 32 || r < 1 || L < 1) return LORS_ERR_SHAPE;
+  if (r <= 16)
+    return dx ? launch_tf32x3<true, 16>(act, w, a, b, bits, bias, out, L, R, C, r, alpha, s)
+              : launch_tf32x3<false, 16>(act, w, a, b, bits, bias, out, L, R, C, r, alpha, s);
+  return dx ? launch_tf32x3<true, 32>(act, w, a, b, bits, bias, out, L, R, C, r, alpha, s)
+            : launch_tf32x3<false, 32>(act, w, a, b, bits, bias, out, L, R, C, r, alpha, s);
+}
+
 }  // namespace lors
