@@ -2772,12 +2772,26 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
       const float* fac = reinterpret_cast<const float*>(rfac(sr));
 #pragma unroll
       for (int e = 0; e < 16; ++e) pv[e] = 0.f;
+      if (DX) {   // a[k][j] ([32][RP]): row k's factors as float4, the chain over j in order
 #pragma unroll
-      for (int j = 0; j < RP; ++j) {   // streamed factor: FWD b[j][k] ([RP][32]); DX a[k][j] ([32][RP])
-        if (j < r) {
+        for (int e = 0; e < 16; ++e) {
+          const float4* fr = reinterpret_cast<const float4*>(fac + (half * 16 + e) * RP);
 #pragma unroll
-          for (int e = 0; e < 16; ++e)
-            pv[e] = fmaf(fix[j], DX ? fac[(half * 16 + e) * RP + j] : fac[j * BK + half * 16 + e], pv[e]);
+          for (int j4 = 0; j4 < RP / 4; ++j4) {
+            const float4 f = fr[j4];
+            const float fj[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (4 * j4 + u < r) pv[e] = fmaf(fix[4 * j4 + u], fj[u], pv[e]);
+          }
+        }
+      } else {    // b[j][k] ([RP][32]): 16 consecutive k of row j
+#pragma unroll
+        for (int j = 0; j < RP; ++j) {
+          if (j < r) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pv[e] = fmaf(fix[j], fac[j * BK + half * 16 + e], pv[e]);
+          }
         }
       }
       __syncwarp();
