@@ -402,29 +402,33 @@ int simt_lors_gemm(bool dx, const T* act, const T* w, const uint32_t* bits, cons
 // 64x64 tiles, BK = 16, 256 threads, 4x4 per thread; gridDim.z splits K and
 // accumulates with atomicAdd into a zeroed fp32 output.
 // ===========================================================================
-template <typename TA, typename TB, typename TO>
+template <typename TA, typename TB, typename TO, int TM, int TN>
 __global__ void __launch_bounds__(256) simt_strided_gemm_kernel(
     const TA* __restrict__ A, int64_t sam, int64_t sak, const TB* __restrict__ B, int64_t sbn,
     int64_t sbk, TO* __restrict__ out, int64_t som, int64_t son, int M, int N, int K,
     int k_per_split, float alpha, int atomic_out) {
-  __shared__ float sA[16][64 + 4];
-  __shared__ float sB[16][64 + 4];
+  // TM x TN tile (64 x 64, or 256 x 16 / 16 x 256 when one side is the rank), 4 x 4 per thread
+  __shared__ float sA[16][TM + 4];
+  __shared__ float sB[16][TN + 4];
   const int tid = threadIdx.x;
-  const int m0 = blockIdx.x * 64, n0 = blockIdx.y * 64;
+  const int m0 = blockIdx.x * TM, n0 = blockIdx.y * TN;
   const int kbeg = blockIdx.z * k_per_split;
   const int kend = min(K, kbeg + k_per_split);
-  const int tx = tid % 16, ty = tid / 16;
-  float acc[4][4] = {};
+  constexpr int TXN = TN / 4;
+  const int tx = tid % TXN, ty = tid / TXN;
+  uint64_t acc2[2][4] = {};   // (acc[2 ip][j], acc[2 ip + 1][j]): packed fmas, each lane rounds like fmaf
   for (int k0 = kbeg; k0 < kend; k0 += 16) {
-    for (int i = tid; i < 16 * 64; i += 256) {
+    for (int i = tid; i < 16 * TM; i += 256) {
       int m, k;
-      if (sak == 1) { k = i % 16; m = i / 16; } else { m = i % 64; k = i / 64; }
+      if (sak == 1) { k = i % 16; m = i / 16; } else { m = i % TM; k = i / TM; }
       float v = 0.f;
       if (m0 + m < M && k0 + k < kend) v = to_f(A[(int64_t)(m0 + m) * sam + (int64_t)(k0 + k) * sak]);
       sA[k][m] = v;
-      int n;
-      if (sbk == 1) { k = i % 16; n = i / 16; } else { n = i % 64; k = i / 64; }
-      v = 0.f;
+    }
+    for (int i = tid; i < 16 * TN; i += 256) {
+      int n, k;
+      if (sbk == 1) { k = i % 16; n = i / 16; } else { n = i % TN; k = i / TN; }
+      float v = 0.f;
       if (n0 + n < N && k0 + k < kend) v = to_f(B[(int64_t)(n0 + n) * sbn + (int64_t)(k0 + k) * sbk]);
       sB[k][n] = v;
     }
@@ -434,13 +438,25 @@ __global__ void __launch_bounds__(256) simt_strided_gemm_kernel(
       float av[4], bv[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) { av[i] = sA[k][ty * 4 + i]; bv[i] = sB[k][tx * 4 + i]; }
+      const uint64_t ap[2] = {pack2(av[0], av[1]), pack2(av[2], av[3])};
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t bj = pack2(bv[j], bv[j]);
+        fma2(acc2[0][j], ap[0], bj);
+        fma2(acc2[1][j], ap[1], bj);
+      }
     }
     __syncthreads();
   }
+  float acc[4][4];
+#pragma unroll
+  for (int ip = 0; ip < 2; ++ip)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 v = unpack2(acc2[ip][j]);
+      acc[2 * ip][j] = v.x;
+      acc[2 * ip + 1][j] = v.y;
+    }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int m = m0 + ty * 4 + i;
@@ -461,7 +477,10 @@ template <typename TA, typename TB, typename TO>
 int simt_strided_gemm(const TA* A, int64_t sam, int64_t sak, const TB* B, int64_t sbn, int64_t sbk,
                       TO* out, int64_t som, int64_t son, int M, int N, int K, float alpha,
                       bool allow_split, cudaStream_t s) {
-  const int tiles = (int)(ceil_div(M, 64) * ceil_div(N, 64));
+  // tile shape: the rank side (N or M <= 16) gets a 16-wide tile, no 64-wide padding
+  const int shape = N <= 16 ? 1 : M <= 16 ? 2 : 0;   // 0: 64 x 64, 1: 256 x 16, 2: 16 x 256
+  const int TMh = shape == 1 ? 256 : shape == 2 ? 16 : 64, TNh = shape == 1 ? 16 : shape == 2 ? 256 : 64;
+  const int tiles = (int)(ceil_div(M, TMh) * ceil_div(N, TNh));
   int split = 1;
   if (allow_split && sizeof(TO) == sizeof(float)) {
     split = (int)ceil_div(296, tiles);
@@ -473,9 +492,16 @@ int simt_strided_gemm(const TA* A, int64_t sam, int64_t sak, const TB* B, int64_
     // atomic accumulation requires a zeroed fp32, densely addressed output
     LORS_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)M * N, s), "zero split-K output");
   }
-  dim3 grid((unsigned)ceil_div(M, 64), (unsigned)ceil_div(N, 64), (unsigned)split);
-  simt_strided_gemm_kernel<TA, TB, TO><<<grid, 256, 0, s>>>(A, sam, sak, B, sbn, sbk, out, som, son, M, N, K,
-                                                            kps, alpha, split > 1 ? 1 : 0);
+  dim3 grid((unsigned)ceil_div(M, TMh), (unsigned)ceil_div(N, TNh), (unsigned)split);
+  if (shape == 1)
+    simt_strided_gemm_kernel<TA, TB, TO, 256, 16><<<grid, 256, 0, s>>>(A, sam, sak, B, sbn, sbk, out, som, son, M,
+                                                                       N, K, kps, alpha, split > 1 ? 1 : 0);
+  else if (shape == 2)
+    simt_strided_gemm_kernel<TA, TB, TO, 16, 256><<<grid, 256, 0, s>>>(A, sam, sak, B, sbn, sbk, out, som, son, M,
+                                                                       N, K, kps, alpha, split > 1 ? 1 : 0);
+  else
+    simt_strided_gemm_kernel<TA, TB, TO, 64, 64><<<grid, 256, 0, s>>>(A, sam, sak, B, sbn, sbk, out, som, son, M, N,
+                                                                      K, kps, alpha, split > 1 ? 1 : 0);
   LORS_CHECK_LAUNCH("simt_strided_gemm");
   return LORS_OK;
 }
