@@ -2733,6 +2733,17 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
     float fix[RP];                          // fixed factor of this feature: FWD a[m][j], DX b[j][m]
 #pragma unroll
     for (int j = 0; j < RP; ++j) fix[j] = (j < r && gm < M) ? (DX ? b[(int64_t)j * C + gm] : a[(int64_t)gm * r + j]) : 0.f;
+    // packed-mask words of a step: FWD one word (16 consecutive k of row gm), DX one per k row (column gm);
+    // fetched a step ahead so the load latency hides behind a whole transform
+    auto fetch_bits = [&](const int k0n, uint32_t (&dst)[DX ? 16 : 1]) {
+#pragma unroll
+      for (int e = 0; e < (DX ? 16 : 1); ++e) {
+        const int gk = k0n + half * 16 + e;
+        dst[e] = (gm < M && gk < K) ? __ldg(bits + (int64_t)(DX ? gk : gm) * words + ((DX ? gm : gk) >> 5)) : 0u;
+      }
+    };
+    uint32_t mwn[DX ? 16 : 1] = {};
+    if (bits != nullptr) fetch_bits(0, mwn);
     for (int i = 0; i < nk; ++i) {
       const int sr = i % NR, ss = i % NS;
       const int k0 = i * BK;
@@ -2758,16 +2769,11 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
           for (int e = 0; e < 4; ++e) wv[4 * c + e] = __uint_as_float(v[e]);
         }
       }
-      // packed-mask words, fetched before the rank-r sums so their latency overlaps them:
-      // FWD one word (16 consecutive k of row gm), DX one per k row (column gm)
+      // packed-mask words of this step (fetched during the previous one) and the next step's
       uint32_t mwd[DX ? 16 : 1];
-      if (bits != nullptr) {
 #pragma unroll
-        for (int e = 0; e < (DX ? 16 : 1); ++e) {
-          const int gk = k0 + half * 16 + e;
-          mwd[e] = (gm < M && gk < K) ? __ldg(bits + (int64_t)(DX ? gk : gm) * words + ((DX ? gm : gk) >> 5)) : 0u;
-        }
-      }
+      for (int e = 0; e < (DX ? 16 : 1); ++e) mwd[e] = mwn[e];
+      if (bits != nullptr) fetch_bits(k0 + BK, mwn);
       float pv[16];
       const float* fac = reinterpret_cast<const float*>(rfac(sr));
 #pragma unroll
