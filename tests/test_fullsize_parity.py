@@ -144,8 +144,26 @@ def test_cfg1_fp32_full(ops):
 
 
 @pytest.mark.parametrize("R,C,L,r,bits", [(1028, 516, 300, 12, False), (1028, 516, 300, 12, True),
-                                          (1030, 518, 77, 5, False)])
+                                          (1030, 518, 77, 5, False), (772, 1540, 257, 28, True),
+                                          (640, 384, 129, 40, False)])
 def test_fp32_ragged_shapes(ops, R, C, L, r, bits):
-    """Ragged fp32 shapes: tile edges of the vectorised kernel (R, C multiples of 4), its packed-mask
-    path, and the scalar kernel (R, C not multiples of 4)."""
+    """Ragged fp32 shapes: tile edges of the 3xTF32 kernels (R, C, r multiples of 4; r <= 16 and <= 32
+    instantiations), their packed-mask path, and the FFMA kernels (R, C not multiples of 4; r > 32)."""
     _check_fp32(ops, R, C, L, r, seed=R + L, a_std=0.05, b_std=r ** -0.5, bits=bits)
+
+
+def test_fp32_bias_forward(ops):
+    """The 3xTF32 forward's epilogue adds the bias (lors_forward with a bias, adapters.py:359-373)."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    R, C, L, r = 516, 260, 200, 8
+    w = (torch.randn(R, C, device="cuda", generator=g) * 0.02) * (torch.rand(R, C, device="cuda", generator=g) > 0.5)
+    a = torch.randn(R, r, device="cuda", generator=g) * 0.05
+    b = torch.randn(r, C, device="cuda", generator=g) / r ** 0.5
+    x = torch.randn(L, C, device="cuda", generator=g)
+    bias = torch.randn(R, device="cuda", generator=g)
+    y, _ = ops.lors_fwd(x, w, a, b, 2.0, bias)
+    y0, _ = ops.lors_fwd(x, w, a, b, 2.0)
+    torch.cuda.synchronize()
+    ref = orc.lors_forward(_f64(w), _f64(a), _f64(b), _f64(x).T, 2.0).T + _f64(bias)[None, :]
+    assert _rel(_f64(y), ref) <= 1e-4
+    assert torch.allclose(y - y0, bias.expand_as(y), rtol=0, atol=1e-5)
