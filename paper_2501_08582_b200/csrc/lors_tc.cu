@@ -2616,17 +2616,17 @@ int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {
 //   warps 0-3: epilogue, TMEM -> registers -> out (+bias)
 // ===========================================================================
 namespace t3 {
-constexpr int BT = 128, BF = 128, BK = 32, NR = 2, NS = 2, THREADS = 320;
-constexpr uint32_t TILE = 128 * 128;                       // one [128][32] fp32 tile, bytes
+// One CTA: 128 output features x 256 tokens; the W_eff tile of a k-step (built once) feeds all 256.
+// D[feature][token] in TMEM (256 columns); A = W_eff (M = 128), B = activations (N = 256).
+constexpr int BF = 128, BT = 256, BK = 32, NSTAGE = 2, THREADS = 320;
+constexpr uint32_t WTILE = 128 * 128, ATILE = 256 * 128;   // [128][32] / [256][32] fp32, bytes
 template <int RP>
 constexpr uint32_t fac_bytes() { return 32 * RP * 4; }     // streamed factor slice, fp32
-// raw ring (TMA): activation, W, factor slice; split ring (transform -> MMA): act hi, act lo, B hi, B lo.
-// The raw slot is released once the transform has read it, so the next TMA does not wait for the MMAs.
+// stage: activation (raw -> hi in place), activation lo, W (raw -> W_eff hi in place), W_eff lo, factor
 template <int RP>
-constexpr uint32_t raw_bytes() { return 2 * TILE + fac_bytes<RP>(); }
-constexpr uint32_t SPLIT_BYTES = 4 * TILE;
+constexpr uint32_t stage_bytes() { return 2 * ATILE + 2 * WTILE + fac_bytes<RP>(); }
 template <int RP>
-constexpr size_t smem_bytes() { return 1024 + NR * raw_bytes<RP>() + NS * SPLIT_BYTES + 256; }
+constexpr size_t smem_bytes() { return 1024 + NSTAGE * stage_bytes<RP>() + 256; }
 __host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
@@ -2653,39 +2653,31 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
   using namespace t3;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* split = smem;                                   // [NS] x (act hi, act lo, B hi, B lo)
-  uint8_t* raw = smem + NS * SPLIT_BYTES;                  // [NR] x (act, W, factor)
-  uint64_t* rfull = reinterpret_cast<uint64_t*>(raw + NR * raw_bytes<RP>());
-  uint64_t* rempty = rfull + NR;
-  uint64_t* sfull = rempty + NR;
-  uint64_t* sempty = sfull + NS;
-  uint64_t* accf = sempty + NS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * stage_bytes<RP>());
+  uint64_t* xf = full + NSTAGE;
+  uint64_t* empty = xf + NSTAGE;
+  uint64_t* accf = empty + NSTAGE;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
   const int warp = warp_id(), lane = lane_id();
   const int M = DX ? C : R, K = DX ? R : C;
   const int m0 = blockIdx.x * BF, t0 = blockIdx.y * BT;
   const int nk = (K + BK - 1) / BK;
   const int64_t words = (C + 31) / 32;
-  auto ract = [&](int s) { return raw + s * raw_bytes<RP>(); };
-  auto rw = [&](int s) { return raw + s * raw_bytes<RP>() + TILE; };
-  auto rfac = [&](int s) { return raw + s * raw_bytes<RP>() + 2 * TILE; };
-  auto ahi = [&](int s) { return split + s * SPLIT_BYTES; };
-  auto alo = [&](int s) { return split + s * SPLIT_BYTES + TILE; };
-  auto bhi = [&](int s) { return split + s * SPLIT_BYTES + 2 * TILE; };
-  auto blo = [&](int s) { return split + s * SPLIT_BYTES + 3 * TILE; };
+  auto act_t = [&](int s) { return smem + s * stage_bytes<RP>(); };
+  auto alo_t = [&](int s) { return smem + s * stage_bytes<RP>() + ATILE; };
+  auto w_t = [&](int s) { return smem + s * stage_bytes<RP>() + 2 * ATILE; };
+  auto wlo_t = [&](int s) { return smem + s * stage_bytes<RP>() + 2 * ATILE + WTILE; };
+  auto fac_t = [&](int s) { return smem + s * stage_bytes<RP>() + 2 * ATILE + 2 * WTILE; };
   if (warp == 8 && lane == 0) {
-    for (int i = 0; i < NR; ++i) {
-      mbar_init(&rfull[i], 1);
-      mbar_init(&rempty[i], 8);
-    }
-    for (int i = 0; i < NS; ++i) {
-      mbar_init(&sfull[i], 8);
-      mbar_init(&sempty[i], 1);
+    for (int i = 0; i < NSTAGE; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&xf[i], 8);
+      mbar_init(&empty[i], 1);
     }
     mbar_init(accf, 1);
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<128>(tmem_slot);
+  if (warp == 9) tmem_alloc<256>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -2693,48 +2685,48 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
   if (warp == 8) {
     if (lane == 0) {
       for (int i = 0; i < nk; ++i) {
-        const int s = i % NR;
-        mbar_wait(&rempty[s], ((i / NR) & 1) ^ 1);
+        const int s = i % NSTAGE;
+        mbar_wait(&empty[s], ((i / NSTAGE) & 1) ^ 1);
         const int k0 = i * BK;
-        mbar_arrive_expect_tx(&rfull[s], 2 * TILE + fac_bytes<RP>());
-        tma_load_2d(ract(s), &tmAct, &rfull[s], k0, t0);                        // [128 t][32 k] SW128
-        if (DX) tma_load_2d(rw(s), &tmW, &rfull[s], m0, k0);                    // [32 k][128 m] plain
-        else tma_load_2d(rw(s), &tmW, &rfull[s], k0, m0);                       // [128 m][32 k] SW128
-        if (DX) tma_load_2d(rfac(s), &tmS, &rfull[s], 0, k0);                   // a [32 k][RP]
-        else tma_load_2d(rfac(s), &tmS, &rfull[s], k0, 0);                      // b [RP][32 k]
+        mbar_arrive_expect_tx(&full[s], ATILE + WTILE + fac_bytes<RP>());
+        tma_load_2d(act_t(s), &tmAct, &full[s], k0, t0);                        // tokens t0 .. t0+127
+        tma_load_2d(act_t(s) + ATILE / 2, &tmAct, &full[s], k0, t0 + 128);     // tokens t0+128 .. +255
+        if (DX) tma_load_2d(w_t(s), &tmW, &full[s], m0, k0);                    // [32 k][128 m] plain
+        else tma_load_2d(w_t(s), &tmW, &full[s], k0, m0);                       // [128 m][32 k] SW128
+        if (DX) tma_load_2d(fac_t(s), &tmS, &full[s], 0, k0);                   // a [32 k][RP]
+        else tma_load_2d(fac_t(s), &tmS, &full[s], k0, 0);                      // b [RP][32 k]
       }
     }
   } else if (warp == 9) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_tf32(128, 128);
+      constexpr uint32_t idesc = idesc_tf32(128, 256);
       for (int i = 0; i < nk; ++i) {
-        const int s = i % NS;
-        mbar_wait(&sfull[s], (i / NS) & 1);
+        const int s = i % NSTAGE;
+        mbar_wait(&xf[s], (i / NSTAGE) & 1);
         tc_fence_after();
-        const uint64_t ah = make_sdesc(smem_u32(ahi(s)), 16, 1024, SW_128);
-        const uint64_t al = make_sdesc(smem_u32(alo(s)), 16, 1024, SW_128);
-        const uint64_t bh = make_sdesc(smem_u32(bhi(s)), 16, 1024, SW_128);
-        const uint64_t bl = make_sdesc(smem_u32(blo(s)), 16, 1024, SW_128);
+        const uint64_t wh = make_sdesc(smem_u32(w_t(s)), 16, 1024, SW_128);
+        const uint64_t wl = make_sdesc(smem_u32(wlo_t(s)), 16, 1024, SW_128);
+        const uint64_t ah = make_sdesc(smem_u32(act_t(s)), 16, 1024, SW_128);
+        const uint64_t al = make_sdesc(smem_u32(alo_t(s)), 16, 1024, SW_128);
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {   // K = 8 tf32 = 32 bytes of the 128-byte row
-          mma_tf32(tmem, ah + kk * 2, bh + kk * 2, idesc, (i > 0 || kk > 0) ? 1u : 0u);
-          mma_tf32(tmem, ah + kk * 2, bl + kk * 2, idesc, 1u);
-          mma_tf32(tmem, al + kk * 2, bh + kk * 2, idesc, 1u);
+          mma_tf32(tmem, wh + kk * 2, ah + kk * 2, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_tf32(tmem, wh + kk * 2, al + kk * 2, idesc, 1u);
+          mma_tf32(tmem, wl + kk * 2, ah + kk * 2, idesc, 1u);
         }
-        mma_commit(&sempty[s]);
+        mma_commit(&empty[s]);
       }
       mma_commit(accf);
     }
   } else {
     // ---------------------------------------------------------------- transform warps 0-7
     const int tid = threadIdx.x;            // 0 .. 255
-    const int row = tid % 128, half = tid / 128;   // activation row / W_eff feature; k half (16 k)
+    const int row = tid % 128, half = tid / 128;   // W_eff feature row; k half (16 k)
     const int gm = m0 + row;
     float fix[RP];                          // fixed factor of this feature: FWD a[m][j], DX b[j][m]
 #pragma unroll
     for (int j = 0; j < RP; ++j) fix[j] = (j < r && gm < M) ? (DX ? b[(int64_t)j * C + gm] : a[(int64_t)gm * r + j]) : 0.f;
-    // packed-mask words of a step: FWD one word (16 consecutive k of row gm), DX one per k row (column gm);
-    // fetched a step ahead so the load latency hides behind a whole transform
+    // packed-mask words of a step (FWD one word, DX one per k row), fetched a step ahead
     auto fetch_bits = [&](const int k0n, uint32_t (&dst)[DX ? 16 : 1]) {
 #pragma unroll
       for (int e = 0; e < (DX ? 16 : 1); ++e) {
@@ -2745,22 +2737,41 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
     uint32_t mwn[DX ? 16 : 1] = {};
     if (bits != nullptr) fetch_bits(0, mwn);
     for (int i = 0; i < nk; ++i) {
-      const int sr = i % NR, ss = i % NS;
+      const int s = i % NSTAGE;
       const int k0 = i * BK;
-      mbar_wait(&rfull[sr], (i / NR) & 1);
-      // this thread's raw values: activation row chunks, W row / column, into registers
-      uint32_t av[16];
-      const uint32_t arow = smem_u32(ract(sr)) + row * 128;
+      mbar_wait(&full[s], (i / NSTAGE) & 1);
+      uint32_t mwd[DX ? 16 : 1];
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        lds128(arow + (uint32_t)(((half * 4 + c) ^ (row & 7)) << 4), *reinterpret_cast<uint32_t(*)[4]>(&av[4 * c]));
+      for (int e = 0; e < (DX ? 16 : 1); ++e) mwd[e] = mwn[e];
+      if (bits != nullptr) fetch_bits(k0 + BK, mwn);
+      // 1. activation row tid (256 tokens): hi in place, lo beside it
+      {
+        const uint32_t arow = smem_u32(act_t(s)) + tid * 128, lrow = smem_u32(alo_t(s)) + tid * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t off = (uint32_t)((c ^ (tid & 7)) << 4);
+          uint32_t v[4];
+          lds128(arow + off, v);
+          float h[4], l[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            h[e] = tf32_hi(__uint_as_float(v[e]));
+            l[e] = __uint_as_float(v[e]) - h[e];
+          }
+          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(arow + off), "f"(h[0]), "f"(h[1]), "f"(h[2]),
+                       "f"(h[3]) : "memory");
+          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lrow + off), "f"(l[0]), "f"(l[1]), "f"(l[2]),
+                       "f"(l[3]) : "memory");
+        }
+      }
+      // 2. W_eff(m = row, k = k0 + 16 half + e)
       float wv[16];
       if (DX) {
-        const float* wr = reinterpret_cast<const float*>(rw(sr));   // [32 k][128 m]
+        const float* wr = reinterpret_cast<const float*>(w_t(s));   // [32 k][128 m]
 #pragma unroll
         for (int e = 0; e < 16; ++e) wv[e] = wr[(half * 16 + e) * 128 + row];
       } else {
-        const uint32_t wrow = smem_u32(rw(sr)) + row * 128;
+        const uint32_t wrow = smem_u32(w_t(s)) + row * 128;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t v[4];
@@ -2769,13 +2780,8 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
           for (int e = 0; e < 4; ++e) wv[4 * c + e] = __uint_as_float(v[e]);
         }
       }
-      // packed-mask words of this step (fetched during the previous one) and the next step's
-      uint32_t mwd[DX ? 16 : 1];
-#pragma unroll
-      for (int e = 0; e < (DX ? 16 : 1); ++e) mwd[e] = mwn[e];
-      if (bits != nullptr) fetch_bits(k0 + BK, mwn);
       float pv[16];
-      const float* fac = reinterpret_cast<const float*>(rfac(sr));
+      const float* fac = reinterpret_cast<const float*>(fac_t(s));
 #pragma unroll
       for (int e = 0; e < 16; ++e) pv[e] = 0.f;
       if (DX) {   // a[k][j] ([32][RP]): row k's factors as float4, the chain over j in order
@@ -2800,8 +2806,6 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&rempty[sr]);   // raw slot read: the next TMA may overwrite it
       float hv[16], lv[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
@@ -2815,53 +2819,37 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
         hv[e] = tf32_hi(v);
         lv[e] = v - hv[e];
       }
-      mbar_wait(&sempty[ss], ((i / NS) & 1) ^ 1);   // the MMAs of step i - NS are done with the split slot
-      const uint32_t hrow = smem_u32(ahi(ss)) + row * 128, lrow = smem_u32(alo(ss)) + row * 128;
-      const uint32_t bhrow = smem_u32(bhi(ss)) + row * 128, blrow = smem_u32(blo(ss)) + row * 128;
+      // (dX: the W tile's [k][m] layout is rewritten as [m][k], so every thread reads first)
+      if (DX) named_bar_sync(1, 256);
+      const uint32_t hrow = smem_u32(w_t(s)) + row * 128, lrow = smem_u32(wlo_t(s)) + row * 128;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const uint32_t off = (uint32_t)(((half * 4 + c) ^ (row & 7)) << 4);
-        float h[4], l[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          h[e] = tf32_hi(__uint_as_float(av[4 * c + e]));
-          l[e] = __uint_as_float(av[4 * c + e]) - h[e];
-        }
-        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(hrow + off), "f"(h[0]), "f"(h[1]), "f"(h[2]),
-                     "f"(h[3]) : "memory");
-        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lrow + off), "f"(l[0]), "f"(l[1]), "f"(l[2]),
-                     "f"(l[3]) : "memory");
-        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(bhrow + off), "f"(hv[4 * c]), "f"(hv[4 * c + 1]),
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(hrow + off), "f"(hv[4 * c]), "f"(hv[4 * c + 1]),
                      "f"(hv[4 * c + 2]), "f"(hv[4 * c + 3]) : "memory");
-        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(blrow + off), "f"(lv[4 * c]), "f"(lv[4 * c + 1]),
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lrow + off), "f"(lv[4 * c]), "f"(lv[4 * c + 1]),
                      "f"(lv[4 * c + 2]), "f"(lv[4 * c + 3]) : "memory");
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sfull[ss]);
+      if (lane == 0) mbar_arrive(&xf[s]);
     }
-    // ---------------------------------------------------------------- epilogue (warps 0-3: TMEM lanes)
+    // ---------------------------------------------------------------- epilogue (warps 0-3: TMEM lanes = features)
     if (warp < 4) {
       mbar_wait(accf, 0);
       tc_fence_after();
-      const int t = t0 + warp * 32 + lane;
+      const int m = m0 + warp * 32 + lane;
+      const float bv = (!DX && bias != nullptr && m < M) ? bias[m] : 0.f;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BF; c0 += 32) {
+      for (int c0 = 0; c0 < BT; c0 += 32) {
         uint32_t v[32];
         tmem_ld_x32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
         tmem_ld_wait();
-        if (t < L) {
+        if (m < M) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int m = m0 + c0 + 4 * q;
-            if (m < M) {   // M % 4 == 0
-              float4 o = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                     __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
-              if (!DX && bias != nullptr) {
-                o.x += bias[m]; o.y += bias[m + 1]; o.z += bias[m + 2]; o.w += bias[m + 3];
-              }
-              *reinterpret_cast<float4*>(out + (int64_t)t * M + m) = o;
-            }
+          for (int q = 0; q < 32; ++q) {
+            const int t = t0 + c0 + q;
+            if (t < L) out[(int64_t)t * M + m] = __uint_as_float(v[q]) + bv;   // a warp: 32 consecutive m
           }
         }
       }
@@ -2869,7 +2857,7 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) tmem_dealloc<128>(tmem);
+  if (warp == 9) tmem_dealloc<256>(tmem);
 }
 
 template <bool DX, int RP>
