@@ -357,11 +357,15 @@ def measure_layer(cfg, steps, warmup, world, rank, dev, full=True):
     grad_bucket = torch.empty(R * r + r * C, device=dev, dtype=torch.float32)
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    # 2:4 weights: the forward on the sparse tensor cores (K2, faster than the dense-masked K1), its
+    # kept-position metadata built once per frozen weight as LoRSLinear(sparse24=True) does
+    sp_step = cfg["pattern"] == "two_four" and dt == torch.bfloat16 and C % 64 == 0
+    meta_step = ops.compress_24(w)[1] if sp_step else None
 
     def step(times=None):
         e0, e1, e2 = (ev(), ev(), ev()) if times is not None else (None, None, None)
         if e0: e0.record(stream)
-        ops.lors_fwd(x, w, a, b, 2.0)
+        ops.lors_fwd(x, w, a, b, 2.0, sparse24=sp_step, meta24=meta_step)
         if e1: e1.record(stream)
         dxo, da, db, _ = ops.lors_bwd(x, w, a, b, dy, 2.0)
         if e2: e2.record(stream)
@@ -419,6 +423,7 @@ def measure_layer(cfg, steps, warmup, world, rank, dev, full=True):
         # the 2:4 sparse-tensor-core forward (north_star 4), timed beside the dense-masked one
         meta24 = ops.compress_24(w)[1]   # kept-position metadata, built once per frozen weight
         sp_ms = timed(lambda: ops.lors_fwd(x, w, a, b, 2.0, sparse24=True, meta24=meta24))
+    dense_fwd_ms = timed(lambda: ops.lors_fwd(x, w, a, b, 2.0)) if sp_step else fwd_ms
     cost = adapters.predict_cost("lors", R, C, L, r)
     step_flops = cost.flops
     fwd_flops = 2 * cost.macs_forward                       # one K1 launch (RCL + rRC + RC)
@@ -427,9 +432,10 @@ def measure_layer(cfg, steps, warmup, world, rank, dev, full=True):
         "ms": ms, "tokens_per_s_per_gpu": L / (ms * 1e-3), "launches": launches, "clocks": clocks.result(),
         "step_breakdown_ms": {"fwd": fwd_ms, "bwd": bwd_ms, "bwd_dx_gemm_alone": dx_ms, "bwd_rank_r_alone": rank_r_ms,
                               "bwd_overlap": "dX and the rank-r products on two streams",
-                              "fwd_sparse24_tc": sp_ms},
+                              "fwd_sparse24_tc": sp_ms, "fwd_dense_masked": dense_fwd_ms,
+                              "fwd_path": "2:4 sparse tensor cores (K2)" if sp_step else "dense-masked (K1)"},
         "algorithmic_tflops": step_flops / (ms * 1e-3) / 1e12,
-        "fwd_flops": fwd_flops, "dx_flops": dx_flops, "step_flops": step_flops, "dt": dt,
+        "fwd_flops": fwd_flops, "dx_flops": dx_flops, "step_flops": step_flops, "dt": dt, "sp_step": sp_step,
     }
     if dt == torch.bfloat16:
         # north_star's roofline: FLOPs at 2.25 PF dense (or 4.5 PF for the forward's main product on
@@ -443,7 +449,7 @@ def measure_layer(cfg, steps, warmup, world, rank, dev, full=True):
             "dense_masked_us": t_dense * 1e6, "sparse_tc_forward_us": t_sparse * 1e6,
             "frac_of_dense_spec": t_dense / (ms * 1e-3),
             "frac_of_sparse_spec": t_sparse / (ms * 1e-3) if cfg["pattern"] == "two_four" else None,
-            "fwd_frac_of_dense_spec": fwd_flops / (fwd_ms * 1e-3) / (SPEC_PEAKS["dense_tflops"] * 1e12),
+            "fwd_frac_of_dense_spec": fwd_flops / (dense_fwd_ms * 1e-3) / (SPEC_PEAKS["dense_tflops"] * 1e12),
             "sparse24_fwd_frac_of_sparse_spec": (
                 (fwd_flops - fwd_main) / (SPEC_PEAKS["dense_tflops"] * 1e12)
                 + fwd_main / (SPEC_PEAKS["sparse_tflops"] * 1e12)) / (sp_ms * 1e-3) if sp_ms else None,
@@ -453,7 +459,7 @@ def measure_layer(cfg, steps, warmup, world, rank, dev, full=True):
 
     print('[bench] e2e', file=sys.stderr, flush=True)
     # ---------------- end-to-end through the public module API (host buffers)
-    layer = LoRSLinear(w, a=a32, b=b32, alpha=2.0).to(dev)
+    layer = LoRSLinear(w, a=a32, b=b32, alpha=2.0, sparse24=sp_step).to(dev)
     # host buffers on the GPU's NUMA node (as a data loader bound to the GPU's CPUs would place them)
     prev_aff = gpu_local_affinity(dev)
     hx = torch.empty(x.shape, dtype=x.dtype).pin_memory()
@@ -612,7 +618,8 @@ def run_native(args, cfg):
             pk_kind = "measured cuBLAS TF32 GEMM on this box / 3 (3xTF32: three TF32 products per fp32 product)"
             dx_label, fwd_label = "tf32x3_lors<dx> (K8, 3xTF32 tensor cores)", "tf32x3_lors<fwd> (K8, 3xTF32)"
         sb = m["step_breakdown_ms"]
-        if sb["bwd_dx_gemm_alone"] >= sb["fwd"]:
+        if sb["bwd_dx_gemm_alone"] >= sb["fwd"] or m.get("sp_step"):
+            # (a 2:4 step's forward is K2 on the sparse tensor cores: the dense peak is not its roofline)
             roof = dominant_roofline(dx_label, m["dx_flops"], sb["bwd_dx_gemm_alone"], "dx", peak_tf, pk_kind)
         else:
             roof = dominant_roofline(fwd_label, m["fwd_flops"], sb["fwd"], "fwd", peak_tf, pk_kind)
@@ -623,7 +630,8 @@ def run_native(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": m["ms"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
             "config": layer_config(cfg, world),
-            "path": {"forward": "dense-masked tcgen05 (W_eff rebuilt on chip)" if m["dt"] == torch.bfloat16
+            "path": {"forward": ("2:4 sparse tensor cores (K2, W_eff rebuilt and compressed on chip)" if m.get("sp_step")
+                                 else "dense-masked tcgen05 (W_eff rebuilt on chip)") if m["dt"] == torch.bfloat16
                      else "fp32 parity mode: 3xTF32 tensor cores (W_eff rebuilt on chip, split hi + lo)",
                      "adapter_grads": "ste (lors)"},
             "peak_hbm_gb": m["peak_gb"], "memory": m["memory"],
