@@ -433,7 +433,9 @@ def measure_layer(cfg, steps, warmup, world, rank, dev, full=True):
         "step_breakdown_ms": {"fwd": fwd_ms, "bwd": bwd_ms, "bwd_dx_gemm_alone": dx_ms, "bwd_rank_r_alone": rank_r_ms,
                               "bwd_overlap": "dX and the rank-r products on two streams",
                               "fwd_sparse24_tc": sp_ms, "fwd_dense_masked": dense_fwd_ms,
-                              "fwd_path": "2:4 sparse tensor cores (K2)" if sp_step else "dense-masked (K1)"},
+                              "fwd_path": ("2:4 sparse tensor cores (K2)" if sp_step else
+                                           "dense-masked (K1)" if dt == torch.bfloat16 else
+                                           "dense-masked 3xTF32 (K8)")},
         "algorithmic_tflops": step_flops / (ms * 1e-3) / 1e12,
         "fwd_flops": fwd_flops, "dx_flops": dx_flops, "step_flops": step_flops, "dt": dt, "sp_step": sp_step,
     }

@@ -2618,7 +2618,10 @@ int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {
 namespace t3 {
 // One CTA: 128 output features x 256 tokens; the W_eff tile of a k-step (built once) feeds all 256.
 // D[feature][token] in TMEM (256 columns); A = W_eff (M = 128), B = activations (N = 256).
-constexpr int BF = 128, BT = 256, BK = 32, NSTAGE = 2, THREADS = 320;
+// TW transform warps (latency hiding: the split and the W_eff build are short dependent chains), then the
+// TMA warp and the MMA warp; NQ k-groups of KQ k per W_eff row, APT threads per activation row
+constexpr int BF = 128, BT = 256, BK = 32, NSTAGE = 2, TW = 16, THREADS = 32 * (TW + 2);
+constexpr int NQ = TW * 32 / 128, KQ = BK / NQ, APT = TW * 32 / 256;
 constexpr uint32_t WTILE = 128 * 128, ATILE = 256 * 128;   // [128][32] / [256][32] fp32, bytes
 template <int RP>
 constexpr uint32_t fac_bytes() { return 32 * RP * 4; }     // streamed factor slice, fp32
@@ -2668,21 +2671,21 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
   auto w_t = [&](int s) { return smem + s * stage_bytes<RP>() + 2 * ATILE; };
   auto wlo_t = [&](int s) { return smem + s * stage_bytes<RP>() + 2 * ATILE + WTILE; };
   auto fac_t = [&](int s) { return smem + s * stage_bytes<RP>() + 2 * ATILE + 2 * WTILE; };
-  if (warp == 8 && lane == 0) {
+  if (warp == TW && lane == 0) {
     for (int i = 0; i < NSTAGE; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&xf[i], 8);
+      mbar_init(&xf[i], TW);
       mbar_init(&empty[i], 1);
     }
     mbar_init(accf, 1);
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<256>(tmem_slot);
+  if (warp == TW + 1) tmem_alloc<256>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (warp == 8) {
+  if (warp == TW) {
     if (lane == 0) {
       for (int i = 0; i < nk; ++i) {
         const int s = i % NSTAGE;
@@ -2697,7 +2700,7 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
         else tma_load_2d(fac_t(s), &tmS, &full[s], k0, 0);                      // b [RP][32 k]
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == TW + 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_tf32(128, 256);
       for (int i = 0; i < nk; ++i) {
@@ -2719,37 +2722,38 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
       mma_commit(accf);
     }
   } else {
-    // ---------------------------------------------------------------- transform warps 0-7
-    const int tid = threadIdx.x;            // 0 .. 255
-    const int row = tid % 128, half = tid / 128;   // W_eff feature row; k half (16 k)
+    // ---------------------------------------------------------------- transform warps 0 .. TW-1
+    const int tid = threadIdx.x;            // 0 .. 32 TW - 1
+    const int row = tid % 128, half = tid / 128;   // W_eff feature row; k group (KQ k)
     const int gm = m0 + row;
     float fix[RP];                          // fixed factor of this feature: FWD a[m][j], DX b[j][m]
 #pragma unroll
     for (int j = 0; j < RP; ++j) fix[j] = (j < r && gm < M) ? (DX ? b[(int64_t)j * C + gm] : a[(int64_t)gm * r + j]) : 0.f;
     // packed-mask words of a step (FWD one word, DX one per k row), fetched a step ahead
-    auto fetch_bits = [&](const int k0n, uint32_t (&dst)[DX ? 16 : 1]) {
+    auto fetch_bits = [&](const int k0n, uint32_t (&dst)[DX ? KQ : 1]) {
 #pragma unroll
-      for (int e = 0; e < (DX ? 16 : 1); ++e) {
-        const int gk = k0n + half * 16 + e;
+      for (int e = 0; e < (DX ? KQ : 1); ++e) {
+        const int gk = k0n + half * KQ + e;
         dst[e] = (gm < M && gk < K) ? __ldg(bits + (int64_t)(DX ? gk : gm) * words + ((DX ? gm : gk) >> 5)) : 0u;
       }
     };
-    uint32_t mwn[DX ? 16 : 1] = {};
+    uint32_t mwn[DX ? KQ : 1] = {};
     if (bits != nullptr) fetch_bits(0, mwn);
     for (int i = 0; i < nk; ++i) {
       const int s = i % NSTAGE;
       const int k0 = i * BK;
       mbar_wait(&full[s], (i / NSTAGE) & 1);
-      uint32_t mwd[DX ? 16 : 1];
+      uint32_t mwd[DX ? KQ : 1];
 #pragma unroll
-      for (int e = 0; e < (DX ? 16 : 1); ++e) mwd[e] = mwn[e];
+      for (int e = 0; e < (DX ? KQ : 1); ++e) mwd[e] = mwn[e];
       if (bits != nullptr) fetch_bits(k0 + BK, mwn);
-      // 1. activation row tid (256 tokens): hi in place, lo beside it
+      // 1. activation row tid / APT (256 tokens): hi in place, lo beside it
       {
-        const uint32_t arow = smem_u32(act_t(s)) + tid * 128, lrow = smem_u32(alo_t(s)) + tid * 128;
+        const int ar = tid / APT, ac = (tid % APT) * (8 / APT);
+        const uint32_t arow = smem_u32(act_t(s)) + ar * 128, lrow = smem_u32(alo_t(s)) + ar * 128;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t off = (uint32_t)((c ^ (tid & 7)) << 4);
+        for (int c = ac; c < ac + 8 / APT; ++c) {
+          const uint32_t off = (uint32_t)((c ^ (ar & 7)) << 4);
           uint32_t v[4];
           lds128(arow + off, v);
           float h[4], l[4];
@@ -2764,30 +2768,30 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
                        "f"(l[3]) : "memory");
         }
       }
-      // 2. W_eff(m = row, k = k0 + 16 half + e)
-      float wv[16];
+      // 2. W_eff(m = row, k = k0 + KQ half + e)
+      float wv[KQ];
       if (DX) {
         const float* wr = reinterpret_cast<const float*>(w_t(s));   // [32 k][128 m]
 #pragma unroll
-        for (int e = 0; e < 16; ++e) wv[e] = wr[(half * 16 + e) * 128 + row];
+        for (int e = 0; e < KQ; ++e) wv[e] = wr[(half * KQ + e) * 128 + row];
       } else {
         const uint32_t wrow = smem_u32(w_t(s)) + row * 128;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < KQ / 4; ++c) {
           uint32_t v[4];
-          lds128(wrow + (uint32_t)(((half * 4 + c) ^ (row & 7)) << 4), v);
+          lds128(wrow + (uint32_t)(((half * (KQ / 4) + c) ^ (row & 7)) << 4), v);
 #pragma unroll
           for (int e = 0; e < 4; ++e) wv[4 * c + e] = __uint_as_float(v[e]);
         }
       }
-      float pv[16];
+      float pv[KQ];
       const float* fac = reinterpret_cast<const float*>(fac_t(s));
 #pragma unroll
-      for (int e = 0; e < 16; ++e) pv[e] = 0.f;
+      for (int e = 0; e < KQ; ++e) pv[e] = 0.f;
       if (DX) {   // a[k][j] ([32][RP]): row k's factors as float4, the chain over j in order
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const float4* fr = reinterpret_cast<const float4*>(fac + (half * 16 + e) * RP);
+        for (int e = 0; e < KQ; ++e) {
+          const float4* fr = reinterpret_cast<const float4*>(fac + (half * KQ + e) * RP);
 #pragma unroll
           for (int j4 = 0; j4 < RP / 4; ++j4) {
             const float4 f = fr[j4];
@@ -2797,19 +2801,19 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
               if (4 * j4 + u < r) pv[e] = fmaf(fix[4 * j4 + u], fj[u], pv[e]);
           }
         }
-      } else {    // b[j][k] ([RP][32]): 16 consecutive k of row j
+      } else {    // b[j][k] ([RP][32]): KQ consecutive k of row j
 #pragma unroll
         for (int j = 0; j < RP; ++j) {
           if (j < r) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) pv[e] = fmaf(fix[j], fac[j * BK + half * 16 + e], pv[e]);
+            for (int e = 0; e < KQ; ++e) pv[e] = fmaf(fix[j], fac[j * BK + half * KQ + e], pv[e]);
           }
         }
       }
-      float hv[16], lv[16];
+      float hv[KQ], lv[KQ];
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int gk = k0 + half * 16 + e;
+      for (int e = 0; e < KQ; ++e) {
+        const int gk = k0 + half * KQ + e;
         float v = 0.f;
         if (gm < M && gk < K) {
           const int wcol = DX ? gm : gk;
@@ -2820,11 +2824,11 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
         lv[e] = v - hv[e];
       }
       // (dX: the W tile's [k][m] layout is rewritten as [m][k], so every thread reads first)
-      if (DX) named_bar_sync(1, 256);
+      if (DX) named_bar_sync(1, TW * 32);
       const uint32_t hrow = smem_u32(w_t(s)) + row * 128, lrow = smem_u32(wlo_t(s)) + row * 128;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const uint32_t off = (uint32_t)(((half * 4 + c) ^ (row & 7)) << 4);
+      for (int c = 0; c < KQ / 4; ++c) {
+        const uint32_t off = (uint32_t)(((half * (KQ / 4) + c) ^ (row & 7)) << 4);
         asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(hrow + off), "f"(hv[4 * c]), "f"(hv[4 * c + 1]),
                      "f"(hv[4 * c + 2]), "f"(hv[4 * c + 3]) : "memory");
         asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lrow + off), "f"(lv[4 * c]), "f"(lv[4 * c + 1]),
@@ -2834,16 +2838,17 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&xf[s]);
     }
-    // ---------------------------------------------------------------- epilogue (warps 0-3: TMEM lanes = features)
-    if (warp < 4) {
+    // ---------------------------------------------------------------- epilogue (warps 0-7: TMEM lanes = features,
+    // warp / 4 picks the token half)
+    if (warp < 8) {
       mbar_wait(accf, 0);
       tc_fence_after();
-      const int m = m0 + warp * 32 + lane;
+      const int m = m0 + (warp & 3) * 32 + lane;
       const float bv = (!DX && bias != nullptr && m < M) ? bias[m] : 0.f;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BT; c0 += 32) {
+      for (int c0 = (warp >> 2) * (BT / 2); c0 < (warp >> 2) * (BT / 2) + BT / 2; c0 += 32) {
         uint32_t v[32];
-        tmem_ld_x32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+        tmem_ld_x32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, v);
         tmem_ld_wait();
         if (m < M) {
 #pragma unroll
@@ -2857,7 +2862,7 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) tmem_dealloc<256>(tmem);
+  if (warp == TW + 1) tmem_dealloc<256>(tmem);
 }
 
 template <bool DX, int RP>
