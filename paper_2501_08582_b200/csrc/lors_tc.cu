@@ -2762,8 +2762,7 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
             h[e] = tf32_hi(__uint_as_float(v[e]));
             l[e] = __uint_as_float(v[e]) - h[e];
           }
-          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(arow + off), "f"(h[0]), "f"(h[1]), "f"(h[2]),
-                       "f"(h[3]) : "memory");
+          // (hi stays as the raw value: kind::tf32 reads only the top 19 bits of each fp32 operand)
           asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lrow + off), "f"(l[0]), "f"(l[1]), "f"(l[2]),
                        "f"(l[3]) : "memory");
         }
@@ -2785,17 +2784,18 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
         }
       }
       float pv[KQ];
-      const float* fac = reinterpret_cast<const float*>(fac_t(s));
+      const uint32_t fbase = smem_u32(fac_t(s));
 #pragma unroll
       for (int e = 0; e < KQ; ++e) pv[e] = 0.f;
       if (DX) {   // a[k][j] ([32][RP]): row k's factors as float4, the chain over j in order
 #pragma unroll
         for (int e = 0; e < KQ; ++e) {
-          const float4* fr = reinterpret_cast<const float4*>(fac + (half * KQ + e) * RP);
 #pragma unroll
           for (int j4 = 0; j4 < RP / 4; ++j4) {
-            const float4 f = fr[j4];
-            const float fj[4] = {f.x, f.y, f.z, f.w};
+            uint32_t f[4];
+            lds128(fbase + (uint32_t)(((half * KQ + e) * RP + 4 * j4) * 4), f);
+            const float fj[4] = {__uint_as_float(f[0]), __uint_as_float(f[1]), __uint_as_float(f[2]),
+                                 __uint_as_float(f[3])};
 #pragma unroll
             for (int u = 0; u < 4; ++u)
               if (4 * j4 + u < r) pv[e] = fmaf(fix[4 * j4 + u], fj[u], pv[e]);
@@ -2806,7 +2806,12 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
         for (int j = 0; j < RP; ++j) {
           if (j < r) {
 #pragma unroll
-            for (int e = 0; e < KQ; ++e) pv[e] = fmaf(fix[j], fac[j * BK + half * KQ + e], pv[e]);
+            for (int c = 0; c < KQ / 4; ++c) {
+              uint32_t f[4];
+              lds128(fbase + (uint32_t)((j * BK + half * KQ + 4 * c) * 4), f);   // warp-uniform: a broadcast
+#pragma unroll
+              for (int u = 0; u < 4; ++u) pv[4 * c + u] = fmaf(fix[j], __uint_as_float(f[u]), pv[4 * c + u]);
+            }
           }
         }
       }
