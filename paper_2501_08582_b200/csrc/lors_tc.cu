@@ -2619,9 +2619,9 @@ namespace t3 {
 // One CTA: 128 output features x 256 tokens; the W_eff tile of a k-step (built once) feeds all 256.
 // D[feature][token] in TMEM (256 columns); A = W_eff (M = 128), B = activations (N = 256).
 // TW transform warps (latency hiding: the split and the W_eff build are short dependent chains), then the
-// TMA warp and the MMA warp; NQ k-groups of KQ k per W_eff row, APT threads per activation row
+// TMA warp and the MMA warp; APT threads per activation row
 constexpr int BF = 128, BT = 256, BK = 32, NSTAGE = 2, TW = 16, THREADS = 32 * (TW + 2);
-constexpr int NQ = TW * 32 / 128, KQ = BK / NQ, APT = TW * 32 / 256;
+constexpr int APT = TW * 32 / 256;
 constexpr uint32_t WTILE = 128 * 128, ATILE = 256 * 128;   // [128][32] / [256][32] fp32, bytes
 template <int RP>
 constexpr uint32_t fac_bytes() { return 32 * RP * 4; }     // streamed factor slice, fp32
@@ -2724,28 +2724,41 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
   } else {
     // ---------------------------------------------------------------- transform warps 0 .. TW-1
     const int tid = threadIdx.x;            // 0 .. 32 TW - 1
-    const int row = tid % 128, half = tid / 128;   // W_eff feature row; k group (KQ k)
-    const int gm = m0 + row;
-    float fix[RP];                          // fixed factor of this feature: FWD a[m][j], DX b[j][m]
+    // W_eff: RPT rows (row0, row0 + 128 / RPT) x KQ k a thread; a warp shares its k group, so the factor
+    // slice reads are broadcasts (two rows a thread halve them; r <= 16 keeps both rows' factors in registers)
+    constexpr int RPT = RP <= 16 ? 2 : 1, RSTEP = 128 / RPT, KQ = BK * RSTEP / (TW * 32);
+    const int row0 = tid % RSTEP, half = tid / RSTEP;
+    float fix[RPT][RP];                     // fixed factor of each row: FWD a[m][j], DX b[j][m]
 #pragma unroll
-    for (int j = 0; j < RP; ++j) fix[j] = (j < r && gm < M) ? (DX ? b[(int64_t)j * C + gm] : a[(int64_t)gm * r + j]) : 0.f;
-    // packed-mask words of a step (FWD one word, DX one per k row), fetched a step ahead
-    auto fetch_bits = [&](const int k0n, uint32_t (&dst)[DX ? KQ : 1]) {
+    for (int rr = 0; rr < RPT; ++rr) {
+      const int gm = m0 + row0 + rr * RSTEP;
 #pragma unroll
-      for (int e = 0; e < (DX ? KQ : 1); ++e) {
-        const int gk = k0n + half * KQ + e;
-        dst[e] = (gm < M && gk < K) ? __ldg(bits + (int64_t)(DX ? gk : gm) * words + ((DX ? gm : gk) >> 5)) : 0u;
+      for (int j = 0; j < RP; ++j)
+        fix[rr][j] = (j < r && gm < M) ? (DX ? b[(int64_t)j * C + gm] : a[(int64_t)gm * r + j]) : 0.f;
+    }
+    // packed-mask words of a step (FWD one a row, DX one a row and k), fetched a step ahead
+    constexpr int NWB = RPT * (DX ? KQ : 1);
+    auto fetch_bits = [&](const int k0n, uint32_t (&dst)[NWB]) {
+#pragma unroll
+      for (int rr = 0; rr < RPT; ++rr) {
+        const int gm = m0 + row0 + rr * RSTEP;
+#pragma unroll
+        for (int e = 0; e < (DX ? KQ : 1); ++e) {
+          const int gk = k0n + half * KQ + e;
+          dst[rr * (DX ? KQ : 1) + e] =
+              (gm < M && gk < K) ? __ldg(bits + (int64_t)(DX ? gk : gm) * words + ((DX ? gm : gk) >> 5)) : 0u;
+        }
       }
     };
-    uint32_t mwn[DX ? KQ : 1] = {};
+    uint32_t mwn[NWB] = {};
     if (bits != nullptr) fetch_bits(0, mwn);
     for (int i = 0; i < nk; ++i) {
       const int s = i % NSTAGE;
       const int k0 = i * BK;
       mbar_wait(&full[s], (i / NSTAGE) & 1);
-      uint32_t mwd[DX ? KQ : 1];
+      uint32_t mwd[NWB];
 #pragma unroll
-      for (int e = 0; e < (DX ? KQ : 1); ++e) mwd[e] = mwn[e];
+      for (int e = 0; e < NWB; ++e) mwd[e] = mwn[e];
       if (bits != nullptr) fetch_bits(k0 + BK, mwn);
       // 1. activation row tid / APT (256 tokens): hi in place, lo beside it
       {
@@ -2767,38 +2780,46 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
                        "f"(l[3]) : "memory");
         }
       }
-      // 2. W_eff(m = row, k = k0 + KQ half + e)
-      float wv[KQ];
-      if (DX) {
-        const float* wr = reinterpret_cast<const float*>(w_t(s));   // [32 k][128 m]
+      // 2. W_eff(m = row0 + RSTEP rr, k = k0 + KQ half + e)
+      float wv[RPT][KQ];
 #pragma unroll
-        for (int e = 0; e < KQ; ++e) wv[e] = wr[(half * KQ + e) * 128 + row];
-      } else {
-        const uint32_t wrow = smem_u32(w_t(s)) + row * 128;
+      for (int rr = 0; rr < RPT; ++rr) {
+        const int row = row0 + rr * RSTEP;
+        if (DX) {
+          const float* wr = reinterpret_cast<const float*>(w_t(s));   // [32 k][128 m]
 #pragma unroll
-        for (int c = 0; c < KQ / 4; ++c) {
-          uint32_t v[4];
-          lds128(wrow + (uint32_t)(((half * (KQ / 4) + c) ^ (row & 7)) << 4), v);
+          for (int e = 0; e < KQ; ++e) wv[rr][e] = wr[(half * KQ + e) * 128 + row];
+        } else {
+          const uint32_t wrow = smem_u32(w_t(s)) + row * 128;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) wv[4 * c + e] = __uint_as_float(v[e]);
+          for (int c = 0; c < KQ / 4; ++c) {
+            uint32_t v[4];
+            lds128(wrow + (uint32_t)(((half * (KQ / 4) + c) ^ (row & 7)) << 4), v);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) wv[rr][4 * c + e] = __uint_as_float(v[e]);
+          }
         }
       }
-      float pv[KQ];
+      float pv[RPT][KQ];
       const uint32_t fbase = smem_u32(fac_t(s));
 #pragma unroll
-      for (int e = 0; e < KQ; ++e) pv[e] = 0.f;
+      for (int rr = 0; rr < RPT; ++rr)
+#pragma unroll
+        for (int e = 0; e < KQ; ++e) pv[rr][e] = 0.f;
       if (DX) {   // a[k][j] ([32][RP]): row k's factors as float4, the chain over j in order
 #pragma unroll
         for (int e = 0; e < KQ; ++e) {
 #pragma unroll
           for (int j4 = 0; j4 < RP / 4; ++j4) {
             uint32_t f[4];
-            lds128(fbase + (uint32_t)(((half * KQ + e) * RP + 4 * j4) * 4), f);
-            const float fj[4] = {__uint_as_float(f[0]), __uint_as_float(f[1]), __uint_as_float(f[2]),
-                                 __uint_as_float(f[3])};
+            lds128(fbase + (uint32_t)(((half * KQ + e) * RP + 4 * j4) * 4), f);   // warp-uniform: a broadcast
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-              if (4 * j4 + u < r) pv[e] = fmaf(fix[4 * j4 + u], fj[u], pv[e]);
+              if (4 * j4 + u < r) {
+#pragma unroll
+                for (int rr = 0; rr < RPT; ++rr)
+                  pv[rr][e] = fmaf(fix[rr][4 * j4 + u], __uint_as_float(f[u]), pv[rr][e]);
+              }
           }
         }
       } else {    // b[j][k] ([RP][32]): KQ consecutive k of row j
@@ -2810,34 +2831,47 @@ __global__ void __launch_bounds__(t3::THREADS, 1)
               uint32_t f[4];
               lds128(fbase + (uint32_t)((j * BK + half * KQ + 4 * c) * 4), f);   // warp-uniform: a broadcast
 #pragma unroll
-              for (int u = 0; u < 4; ++u) pv[4 * c + u] = fmaf(fix[j], __uint_as_float(f[u]), pv[4 * c + u]);
+              for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int rr = 0; rr < RPT; ++rr)
+                  pv[rr][4 * c + u] = fmaf(fix[rr][j], __uint_as_float(f[u]), pv[rr][4 * c + u]);
             }
           }
         }
       }
-      float hv[KQ], lv[KQ];
+      float hv[RPT][KQ], lv[RPT][KQ];
 #pragma unroll
-      for (int e = 0; e < KQ; ++e) {
-        const int gk = k0 + half * KQ + e;
-        float v = 0.f;
-        if (gm < M && gk < K) {
-          const int wcol = DX ? gm : gk;
-          const bool keep = bits != nullptr ? ((mwd[DX ? e : 0] >> (wcol & 31)) & 1u) != 0u : wv[e] != 0.0f;
-          v = weff_value<float>(keep, wv[e], pv[e], alpha);
+      for (int rr = 0; rr < RPT; ++rr) {
+        const int gm = m0 + row0 + rr * RSTEP;
+#pragma unroll
+        for (int e = 0; e < KQ; ++e) {
+          const int gk = k0 + half * KQ + e;
+          float v = 0.f;
+          if (gm < M && gk < K) {
+            const int wcol = DX ? gm : gk;
+            const bool keep = bits != nullptr
+                                  ? ((mwd[rr * (DX ? KQ : 1) + (DX ? e : 0)] >> (wcol & 31)) & 1u) != 0u
+                                  : wv[rr][e] != 0.0f;
+            v = weff_value<float>(keep, wv[rr][e], pv[rr][e], alpha);
+          }
+          hv[rr][e] = tf32_hi(v);
+          lv[rr][e] = v - hv[rr][e];
         }
-        hv[e] = tf32_hi(v);
-        lv[e] = v - hv[e];
       }
       // (dX: the W tile's [k][m] layout is rewritten as [m][k], so every thread reads first)
       if (DX) named_bar_sync(1, TW * 32);
-      const uint32_t hrow = smem_u32(w_t(s)) + row * 128, lrow = smem_u32(wlo_t(s)) + row * 128;
 #pragma unroll
-      for (int c = 0; c < KQ / 4; ++c) {
-        const uint32_t off = (uint32_t)(((half * (KQ / 4) + c) ^ (row & 7)) << 4);
-        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(hrow + off), "f"(hv[4 * c]), "f"(hv[4 * c + 1]),
-                     "f"(hv[4 * c + 2]), "f"(hv[4 * c + 3]) : "memory");
-        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lrow + off), "f"(lv[4 * c]), "f"(lv[4 * c + 1]),
-                     "f"(lv[4 * c + 2]), "f"(lv[4 * c + 3]) : "memory");
+      for (int rr = 0; rr < RPT; ++rr) {
+        const int row = row0 + rr * RSTEP;
+        const uint32_t hrow = smem_u32(w_t(s)) + row * 128, lrow = smem_u32(wlo_t(s)) + row * 128;
+#pragma unroll
+        for (int c = 0; c < KQ / 4; ++c) {
+          const uint32_t off = (uint32_t)(((half * (KQ / 4) + c) ^ (row & 7)) << 4);
+          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(hrow + off), "f"(hv[rr][4 * c]),
+                       "f"(hv[rr][4 * c + 1]), "f"(hv[rr][4 * c + 2]), "f"(hv[rr][4 * c + 3]) : "memory");
+          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(lrow + off), "f"(lv[rr][4 * c]),
+                       "f"(lv[rr][4 * c + 1]), "f"(lv[rr][4 * c + 2]), "f"(lv[rr][4 * c + 3]) : "memory");
+        }
       }
       fence_proxy_async_smem();
       __syncwarp();
