@@ -109,8 +109,11 @@ int lors_fwd(const lors_fwd_args* A, void* stream) {
     if (st == LORS_ERR_SHAPE)
       st = simt_lors_gemm<float>(false, x, w, bits, a, b, (const float*)A->bias, (float*)A->y, L, R, C, r, A->alpha, s);
     if (st) return st;
-    if (A->flags & LORS_FLAG_EMIT_P)  // P[l, j] = sum_c X_t[l, c] b[j, c]
-      st = simt_strided_gemm<float, float, float>(x, C, 1, b, C, 1, (float*)A->p, r, 1, L, r, C, 1.0f, false, s);
+    if (A->flags & LORS_FLAG_EMIT_P) {  // P[l, j] = sum_c X_t[l, c] b[j, c], one warp a row (deterministic)
+      st = s4_rank_project(x, C, b, C, 1, (float*)A->p, L, C, r, true, s);
+      if (st == LORS_ERR_SHAPE)
+        st = simt_strided_gemm<float, float, float>(x, C, 1, b, C, 1, (float*)A->p, r, 1, L, r, C, 1.0f, false, s);
+    }
     return st;
   }
   return tc_fwd(A, s);
@@ -159,19 +162,29 @@ int lors_bwd(const lors_bwd_args* A, void* stream) {
       const size_t slot = ((size_t)L * r * sizeof(float) + 255) / 256 * 256;
       float* P = (float*)A->p;
       float* Q = (float*)((char*)A->workspace + slot);
+      // S4 streams X / dY once per product (P and Q: one warp a row, no atomics when deterministic;
+      // dA and dB: L split with fp32 atomics, fast mode only); S2 covers the rest
       if (P == nullptr) {  // xt_bt = X^T b^T  (adapters.py:396)
         P = (float*)A->workspace;
-        st = simt_strided_gemm<float, float, float>(x, C, 1, b, C, 1, P, r, 1, L, r, C, 1.0f, split, s);
+        st = s4_rank_project(x, C, b, C, 1, P, L, C, r, !split, s);
+        if (st == LORS_ERR_SHAPE)
+          st = simt_strided_gemm<float, float, float>(x, C, 1, b, C, 1, P, r, 1, L, r, C, 1.0f, split, s);
         if (st) return st;
       }
       // at_dy = a^T dY (adapters.py:397): Q[l, j] = sum_n dY_t[l, n] a[n, j]
-      st = simt_strided_gemm<float, float, float>(dy, R, 1, a, 1, r, Q, r, 1, L, r, R, 1.0f, split, s);
+      st = s4_rank_project(dy, R, a, 1, r, Q, L, R, r, !split, s);
+      if (st == LORS_ERR_SHAPE)
+        st = simt_strided_gemm<float, float, float>(dy, R, 1, a, 1, r, Q, r, 1, L, r, R, 1.0f, split, s);
       if (st) return st;
       // da = alpha dY xt_bt (adapters.py:398): dA[n, j] = alpha sum_l dY_t[l, n] P[l, j]
-      st = simt_strided_gemm<float, float, float>(dy, 1, R, P, 1, r, A->da, r, 1, R, r, L, A->alpha, split, s);
+      st = split ? s4_rank_accumulate(dy, R, P, A->da, r, 1, L, R, r, A->alpha, s) : LORS_ERR_SHAPE;
+      if (st == LORS_ERR_SHAPE)
+        st = simt_strided_gemm<float, float, float>(dy, 1, R, P, 1, r, A->da, r, 1, R, r, L, A->alpha, split, s);
       if (st) return st;
       // db = alpha at_dy X^T (adapters.py:399): dB[j, c] = alpha sum_l Q[l, j] X_t[l, c]
-      st = simt_strided_gemm<float, float, float>(Q, 1, r, x, 1, C, A->db, C, 1, r, C, L, A->alpha, split, s);
+      st = split ? s4_rank_accumulate(x, C, Q, A->db, 1, C, L, C, r, A->alpha, s) : LORS_ERR_SHAPE;
+      if (st == LORS_ERR_SHAPE)
+        st = simt_strided_gemm<float, float, float>(Q, 1, r, x, 1, C, A->db, C, 1, r, C, L, A->alpha, split, s);
       if (st) return st;
     } else {
       st = simt_masked_grad<float>(dy, x, w, bits, a, b, A->da, A->db, L, R, C, r, A->alpha, s);

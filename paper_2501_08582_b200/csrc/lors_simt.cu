@@ -10,6 +10,7 @@
 
 #include "lors_common.cuh"
 #include "lors_simt.cuh"
+#include <algorithm>
 
 namespace lors {
 
@@ -503,6 +504,234 @@ int simt_strided_gemm(const TA* A, int64_t sam, int64_t sak, const TB* B, int64_
     simt_strided_gemm_kernel<TA, TB, TO, 64, 64><<<grid, 256, 0, s>>>(A, sam, sak, B, sbn, sbk, out, som, son, M, N,
                                                                       K, kps, alpha, split > 1 ? 1 : 0);
   LORS_CHECK_LAUNCH("simt_strided_gemm");
+  return LORS_OK;
+}
+
+// ===========================================================================
+// S4: the fp32 rank-r products at the HBM rate (P = X b^T, Q = dY a, dA = dY^T P, dB = Q^T X).
+// Each reads one L x N activation matrix once against an r-wide factor; S2's tiles stage the big
+// operand through shared memory a 16-k slice at a time, S4 streams it with float4 loads straight into
+// packed fmas and keeps the factor on chip.
+//   project:    out[l, j]  = sum_n Y[l, n] F(j, n)            F(j, n) = Fm[j sfj + n sfn]
+//   accumulate: out[n, j] += alpha sum_l Y[l, n] S[l, j]     written at out[n son + j soj]
+// Requires N % 4 == 0, ldy % 4 == 0 and a 16-byte aligned Y (the caller falls back to S2 otherwise).
+// project splits N over gridDim.y with fp32 atomics into a zeroed out, or (deterministic) runs each
+// row's whole reduction in one warp; accumulate always splits L (atomics: fast mode only).
+// ===========================================================================
+namespace {
+constexpr int S4_THREADS = 256;
+template <int RP>
+struct s4 {
+  static constexpr int PR = 64 / RP;            // project: rows a warp (PR x RP accumulators)
+  static constexpr int ROWS = 8 * PR;           // project: rows a CTA
+  static constexpr int NCH = RP <= 16 ? 1024 : 512;   // project: factor rows staged a chunk (80 / 72 KB)
+  static constexpr size_t SMEM = (size_t)NCH * (RP + 4) * sizeof(float);
+};
+
+// reduce-scatter of NV values over the warp: afterwards lane l holds NV / 32 fully reduced values,
+// value t of lane l being index ((l >> 4 & 1) NV/2 + (l >> 3 & 1) NV/4 + ... ) + t
+template <int NV>
+__device__ __forceinline__ void warp_reduce_scatter(float (&v)[NV], int lane) {
+#pragma unroll
+  for (int off = 16, n = NV; off >= 1; off >>= 1, n >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const float keep = up ? v[n / 2 + i] : v[i];
+      const float give = up ? v[i] : v[n / 2 + i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, give, off);
+    }
+  }
+}
+__device__ __forceinline__ int scatter_index(int lane, int nv) {
+  int idx = 0;
+#pragma unroll
+  for (int off = 16, h = nv / 2; off >= 1; off >>= 1, h >>= 1)
+    if (lane & off) idx += h;
+  return idx;
+}
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+}  // namespace
+
+template <int RP>
+__global__ void __launch_bounds__(S4_THREADS, 2) s4_project_kernel(const float* __restrict__ Y, int64_t ldy,
+                                                                   const float* __restrict__ Fm, int64_t sfj,
+                                                                   int64_t sfn, float* __restrict__ out, int L,
+                                                                   int N, int r, int n_per_cta, int atomic_out) {
+  // factor slice as sF[n][RP + 4]: lane l reads row n = l + 32 t, the 4-float pad makes the 16-byte
+  // reads of 8 consecutive rows hit 8 distinct bank groups
+  using S = s4<RP>;
+  constexpr int FS = RP + 4;
+  extern __shared__ __align__(16) float sF[];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int row0 = blockIdx.x * S::ROWS + warp * S::PR;
+  const int nbeg = blockIdx.y * n_per_cta, nend = min(N, nbeg + n_per_cta);
+  uint64_t acc[S::PR][RP / 2] = {};   // (rank 2 jp, 2 jp + 1) of row p
+  for (int c0 = nbeg; c0 < nend; c0 += S::NCH) {
+    const int cn = min(S::NCH, nend - c0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < RP * S::NCH; i += S4_THREADS) {
+      int j, c;
+      if (sfn == 1) { j = i / S::NCH; c = i % S::NCH; } else { c = i / RP; j = i % RP; }
+      sF[c * FS + j] = (j < r && c < cn) ? Fm[(int64_t)j * sfj + (int64_t)(c0 + c) * sfn] : 0.f;
+    }
+    __syncthreads();
+    const float* yr[S::PR];
+#pragma unroll
+    for (int p = 0; p < S::PR; ++p) yr[p] = Y + (int64_t)min(row0 + p, L - 1) * ldy + c0;
+#pragma unroll 4
+    for (int c = lane; c < cn; c += 32) {
+      float y[S::PR];
+#pragma unroll
+      for (int p = 0; p < S::PR; ++p) y[p] = __ldg(yr[p] + c);
+#pragma unroll
+      for (int j4 = 0; j4 < RP / 4; ++j4) {
+        const float4 f = *reinterpret_cast<const float4*>(&sF[c * FS + 4 * j4]);
+        const uint64_t f01 = pack2(f.x, f.y), f23 = pack2(f.z, f.w);
+#pragma unroll
+        for (int p = 0; p < S::PR; ++p) {
+          const uint64_t y2 = pack2(y[p], y[p]);
+          fma2(acc[p][2 * j4], y2, f01);
+          fma2(acc[p][2 * j4 + 1], y2, f23);
+        }
+      }
+    }
+  }
+  float v[S::PR * RP];
+#pragma unroll
+  for (int p = 0; p < S::PR; ++p)
+#pragma unroll
+    for (int jp = 0; jp < RP / 2; ++jp) {
+      const float2 h = unpack2(acc[p][jp]);
+      v[p * RP + 2 * jp] = h.x;
+      v[p * RP + 2 * jp + 1] = h.y;
+    }
+  warp_reduce_scatter<S::PR * RP>(v, lane);
+  const int idx = scatter_index(lane, S::PR * RP);
+#pragma unroll
+  for (int t = 0; t < S::PR * RP / 32; ++t) {
+    const int p = (idx + t) / RP, j = (idx + t) % RP;
+    if (j < r && row0 + p < L) {
+      float* dst = out + (int64_t)(row0 + p) * r + j;
+      if (atomic_out) atomicAdd(dst, v[t]);
+      else *dst = v[t];
+    }
+  }
+}
+
+// mode 0: scalar atomics; 1: v4 over j (soj == 1, r % 4 == 0); 2: v4 over n (son == 1, soj % 4 == 0)
+template <int RP>
+__global__ void __launch_bounds__(S4_THREADS) s4_accumulate_kernel(const float* __restrict__ Y, int64_t ldy,
+                                                                   const float* __restrict__ Sm,
+                                                                   float* __restrict__ out, int64_t son,
+                                                                   int64_t soj, int L, int N, int r, int l_per_cta,
+                                                                   float alpha, int mode) {
+  constexpr int LMAX = 128;
+  __shared__ __align__(16) float sS[LMAX][RP];
+  const int n = (blockIdx.x * S4_THREADS + threadIdx.x) * 4;
+  const int l0 = blockIdx.y * l_per_cta, ln = min(l_per_cta, L - l0);
+  for (int i = threadIdx.x; i < ln * RP; i += S4_THREADS) {
+    const int l = i / RP, j = i % RP;
+    sS[l][j] = j < r ? Sm[(int64_t)(l0 + l) * r + j] : 0.f;
+  }
+  __syncthreads();
+  if (n >= N) return;
+  uint64_t acc[4][RP / 2] = {};   // (n + q; ranks 2 jp, 2 jp + 1)
+  const float* yp = Y + (int64_t)l0 * ldy + n;
+#pragma unroll 4
+  for (int l = 0; l < ln; ++l) {
+    const float4 y = __ldg(reinterpret_cast<const float4*>(yp + (int64_t)l * ldy));
+    const float yq[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+    for (int j4 = 0; j4 < RP / 4; ++j4) {
+      const float4 sv = *reinterpret_cast<const float4*>(&sS[l][4 * j4]);   // broadcast
+      const uint64_t s01 = pack2(sv.x, sv.y), s23 = pack2(sv.z, sv.w);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t y2 = pack2(yq[q], yq[q]);
+        fma2(acc[q][2 * j4], y2, s01);
+        fma2(acc[q][2 * j4 + 1], y2, s23);
+      }
+    }
+  }
+  float o[4][RP];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int jp = 0; jp < RP / 2; ++jp) {
+      const float2 h = unpack2(acc[q][jp]);
+      o[q][2 * jp] = alpha * h.x;
+      o[q][2 * jp + 1] = alpha * h.y;
+    }
+  if (mode == 1) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int j4 = 0; j4 < RP / 4; ++j4)
+        if (4 * j4 < r)
+          red_add_v4(out + (int64_t)(n + q) * son + 4 * j4, o[q][4 * j4], o[q][4 * j4 + 1], o[q][4 * j4 + 2],
+                     o[q][4 * j4 + 3]);
+  } else if (mode == 2) {
+#pragma unroll
+    for (int j = 0; j < RP; ++j)
+      if (j < r) red_add_v4(out + (int64_t)j * soj + n, o[0][j], o[1][j], o[2][j], o[3][j]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int j = 0; j < RP; ++j)
+        if (j < r) atomicAdd(out + (int64_t)(n + q) * son + (int64_t)j * soj, o[q][j]);
+  }
+}
+
+static bool s4_ok(const float* Y, int64_t ldy, int N, int r) {
+  return r >= 1 && r <= 32 && N % 4 == 0 && ldy % 4 == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
+}
+
+int s4_rank_project(const float* Y, int64_t ldy, const float* Fm, int64_t sfj, int64_t sfn, float* out, int L,
+                    int N, int r, bool deterministic, cudaStream_t s) {
+  if (!s4_ok(Y, ldy, N, r)) return LORS_ERR_SHAPE;
+  const int rows = r <= 16 ? s4<16>::ROWS : s4<32>::ROWS, nch = r <= 16 ? s4<16>::NCH : s4<32>::NCH;
+  const int rtiles = (int)ceil_div(L, rows);
+  // fast mode: one staged factor chunk a CTA (N split over gridDim.y, atomics); deterministic: whole rows
+  int splits = deterministic ? 1 : (int)ceil_div(N, nch);
+  const int npc = (int)(ceil_div(ceil_div(N, splits), 4) * 4);
+  splits = (int)ceil_div(N, npc);
+  if (splits > 1) LORS_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)L * r, s), "zero S4 output");
+  dim3 grid((unsigned)rtiles, (unsigned)splits);
+  if (r <= 16) {
+    LORS_CUDA_TRY(cudaFuncSetAttribute(s4_project_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)s4<16>::SMEM), "S4 smem attribute");
+    s4_project_kernel<16><<<grid, S4_THREADS, s4<16>::SMEM, s>>>(Y, ldy, Fm, sfj, sfn, out, L, N, r, npc,
+                                                                  splits > 1);
+  } else {
+    LORS_CUDA_TRY(cudaFuncSetAttribute(s4_project_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)s4<32>::SMEM), "S4 smem attribute");
+    s4_project_kernel<32><<<grid, S4_THREADS, s4<32>::SMEM, s>>>(Y, ldy, Fm, sfj, sfn, out, L, N, r, npc,
+                                                                  splits > 1);
+  }
+  LORS_CHECK_LAUNCH("s4_project");
+  return LORS_OK;
+}
+
+int s4_rank_accumulate(const float* Y, int64_t ldy, const float* Sm, float* out, int64_t son, int64_t soj, int L,
+                       int N, int r, float alpha, cudaStream_t s) {
+  if (!s4_ok(Y, ldy, N, r)) return LORS_ERR_SHAPE;
+  const int ntiles = (int)ceil_div(N, 4 * S4_THREADS);
+  int lpc = (int)std::min<int64_t>(128, std::max<int64_t>(8, ceil_div(ceil_div((int64_t)L * ntiles, 296), 4) * 4));
+  const int ltiles = (int)ceil_div(L, lpc);
+  const bool aligned = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  const int mode = !aligned ? 0 : (soj == 1 && r % 4 == 0 && son % 4 == 0) ? 1 : (son == 1 && soj % 4 == 0) ? 2 : 0;
+  // out is a dense N x r (or r x N) block here: zero it, then every L slice adds its share
+  LORS_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)N * r, s), "zero S4 output");
+  dim3 grid((unsigned)ntiles, (unsigned)ltiles);
+  if (r <= 16)
+    s4_accumulate_kernel<16><<<grid, S4_THREADS, 0, s>>>(Y, ldy, Sm, out, son, soj, L, N, r, lpc, alpha, mode);
+  else
+    s4_accumulate_kernel<32><<<grid, S4_THREADS, 0, s>>>(Y, ldy, Sm, out, son, soj, L, N, r, lpc, alpha, mode);
+  LORS_CHECK_LAUNCH("s4_accumulate");
   return LORS_OK;
 }
 

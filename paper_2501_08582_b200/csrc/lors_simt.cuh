@@ -13,6 +13,12 @@ int simt_strided_gemm(const TA* A, int64_t sam, int64_t sak, const TB* B, int64_
                       TO* out, int64_t som, int64_t son, int M, int N, int K, float alpha,
                       bool allow_split, cudaStream_t s);
 
+// S4: fp32 rank-r products streamed at the HBM rate (LORS_ERR_SHAPE when N, ldy or Y are not float4-aligned)
+int s4_rank_project(const float* Y, int64_t ldy, const float* Fm, int64_t sfj, int64_t sfn, float* out, int L,
+                    int N, int r, bool deterministic, cudaStream_t s);
+int s4_rank_accumulate(const float* Y, int64_t ldy, const float* Sm, float* out, int64_t son, int64_t soj, int L,
+                       int N, int r, float alpha, cudaStream_t s);
+
 template <typename T>
 int simt_masked_grad(const T* dy, const T* x, const T* w, const uint32_t* bits, const T* a,
                      const T* b, float* da, float* db, int L, int R, int C, int r, float alpha,
