@@ -145,6 +145,17 @@ int lors_fwd(const lors_fwd_args* args, void* stream);
  * may run concurrently (different streams) need separate workspaces. */
 size_t lors_fwd_workspace(const lors_fwd_args* args);
 
+/* Grouped forward (beyond the reference's per-layer call, which a host loops over
+ * its projections, adapters.py:359-373): `groups` projections of the same input x
+ * -- q / k / v, gate / up -- as ONE persistent tensor-core launch.  args describes
+ * one projection (R rows each) and points at consecutive storage for all of them:
+ * w [groups * R, C], a [groups * R, r], b [groups * r, C], y [groups][L][R].
+ * Needs bf16, mask_mode FROM_W, no bias, no SPARSE24 / EMIT_P, R % 256 == 0,
+ * C % 8 == 0 and r in {16, 32, 64} (LORS_ERR_ARGUMENT otherwise).  Each y[g] is
+ * bit-identical to lors_fwd of projection g. */
+int lors_fwd_group(const lors_fwd_args* args, int32_t groups, void* stream);
+size_t lors_fwd_group_workspace(const lors_fwd_args* args, int32_t groups);
+
 /* Backward: dX_t = dY_t . W_eff (recomputed tiles); STE: dA = alpha dY^T P,
  * dB = alpha Q^T X (P = X b^T, Q = dY a); MASKED: G = (dY^T X) (.) M never
  * materialised, dA = alpha G b^T, dB = alpha a^T G; dbias = sum_L dY. */

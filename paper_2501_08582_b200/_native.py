@@ -31,7 +31,7 @@ FLAG_FAULT_DA_SIGN = 1 << 30
 
 # Every symbol include/lors_b200.h declares (checked by tests/test_capi_symbols.py).
 EXPORTED_SYMBOLS = (
-    "lors_fwd", "lors_fwd_workspace", "lors_bwd", "lors_bwd_workspace",
+    "lors_fwd", "lors_fwd_workspace", "lors_fwd_group", "lors_fwd_group_workspace", "lors_bwd", "lors_bwd_workspace",
     "lors_effective_weight", "lors_pack_mask", "lors_compress_24", "lors_grad_outer",
     "lors_last_error", "lors_abi_version", "lors_device_check",
     "lors_launch_count", "lors_reset_launch_count",
@@ -85,6 +85,10 @@ def load(path: str = LIB_PATH) -> ct.CDLL:
         lib.lors_fwd.restype = ct.c_int
         lib.lors_fwd_workspace.argtypes = [ct.POINTER(FwdArgs)]
         lib.lors_fwd_workspace.restype = ct.c_size_t
+        lib.lors_fwd_group.argtypes = [ct.POINTER(FwdArgs), ct.c_int32, _vp]
+        lib.lors_fwd_group.restype = ct.c_int
+        lib.lors_fwd_group_workspace.argtypes = [ct.POINTER(FwdArgs), ct.c_int32]
+        lib.lors_fwd_group_workspace.restype = ct.c_size_t
         lib.lors_bwd.argtypes = [ct.POINTER(BwdArgs), _vp]
         lib.lors_bwd.restype = ct.c_int
         lib.lors_bwd_workspace.argtypes = [ct.POINTER(BwdArgs)]

@@ -119,6 +119,25 @@ int lors_fwd(const lors_fwd_args* A, void* stream) {
   return tc_fwd(A, s);
 }
 
+size_t lors_fwd_group_workspace(const lors_fwd_args* a, int32_t groups) {
+  if (a == nullptr) return 0;
+  return tc_fwd_group_workspace(a, groups);
+}
+
+int lors_fwd_group(const lors_fwd_args* A, int32_t groups, void* stream) {
+  if (A == nullptr) return fail(LORS_ERR_ARGUMENT, "null args");
+  int st = check_common(A->L, A->R, A->C, A->r, A->dtype, A->mask_mode, A->alpha, A->mask_bits);
+  if (st) return st;
+  if (!tc_fwd_group_ok(A, groups))
+    return fail(LORS_ERR_ARGUMENT, "grouped forward needs bf16, FROM_W, no bias / SPARSE24 / EMIT_P, R % 256 == 0, "
+                                   "C % 8 == 0, r in {16, 32, 64} and groups >= 1");
+  if (!A->w || !A->a || !A->b) return fail(LORS_ERR_ARGUMENT, "null tensor pointer");
+  if (A->L > 0 && (!A->x || !A->y)) return fail(LORS_ERR_ARGUMENT, "null tensor pointer");
+  if ((st = require_sm100())) return st;
+  if (A->L == 0) return LORS_OK;
+  return tc_fwd_group(A, groups, (cudaStream_t)stream);
+}
+
 int lors_bwd(const lors_bwd_args* A, void* stream) {
   if (A == nullptr) return fail(LORS_ERR_ARGUMENT, "null args");
   int st = check_common(A->L, A->R, A->C, A->r, A->dtype, A->mask_mode, A->alpha, A->mask_bits);

@@ -113,6 +113,30 @@ static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
   return LORS_OK;
 }
 
+// 3-D bf16 tensor [depth][outer][inner] with a dense [outer][inner] plane per depth index (the
+// grouped forward's [G][L][R] outputs), box depth 1
+static int make_map_3d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t depth,
+                       uint32_t box_inner, uint32_t box_outer, uint32_t swizzle_bytes, const char* what) {
+  PFN_encodeTiled_t fn = encode_fn();
+  if (fn == nullptr) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return LORS_ERR_CUDA;
+  }
+  cuuint64_t dims[3] = {inner, outer, depth};
+  cuuint64_t strides[2] = {inner * sizeof(bf16), inner * outer * sizeof(bf16)};
+  cuuint32_t box[3] = {box_inner, box_outer, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, to_swizzle(swizzle_bytes), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error(std::string("cuTensorMapEncodeTiled failed for ") + what + " (CUresult " + std::to_string((int)r) +
+              ")");
+    return LORS_ERR_CUDA;
+  }
+  return LORS_OK;
+}
+
 // 2-D byte tensor [outer][inner], no swizzle (the 2:4 metadata boxes)
 static int make_map_u8(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
                        uint32_t box_outer, const char* what) {
@@ -889,9 +913,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
                         const bf16* __restrict__ bias,
                         const uint32_t* __restrict__ bits, const uint8_t* __restrict__ meta24, int words_per_row,
                         int Mout, int Kred, int n_t, int n_f, int split, float* __restrict__ partials,
-                        unsigned int* __restrict__ counters, float alpha, int n_tok) {
+                        unsigned int* __restrict__ counters, float alpha, int n_tok, int grp_rows, int grp_r) {
   using namespace rg;
   static_assert(!(SP && DX), "2:4 sparse tensor cores apply to the forward only (SURVEY C6)");
+  // Grouped forward (lors_fwd_group; grp_rows < Mout): G projections of one input whose W [G R, C],
+  // a [G R, r] and b [G r, C] are consecutive and whose outputs are the 3-D [G][L][R] tmOut; a pair
+  // tile never straddles two projections (R % 256 == 0).  grp_rows = Mout: one projection.
+  const bool grouped = grp_rows < Mout;
+  auto store_out = [&](const void* src, int m, int l) {
+    if (grouped) tma_store_3d(&tmOut, src, m % grp_rows, l, m / grp_rows);
+    else tma_store_2d(&tmOut, src, m, l);
+  };
   static_assert(!EX || (!DX && !SP && LORS_PERSIST), "W_eff export runs the persistent forward prologue");
   constexpr int XW = xw<SP>(), XFORM_THREADS = 32 * XW;
   constexpr int W_SF = XW, W_MMA = XW + 1, W_ACT = XW + 2, W_RELAY = XW + 3;   // W ring: lane 1 of W_SF
@@ -1073,7 +1105,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
         const int k0 = i * BK;
         mbar_arrive_expect_tx(&sready[sl].b, SF);
         if (DX) tma_load_2d(st, &tmS, &sready[sl].b, 0, k0 + 32 * rank);   // a rows, K-major
-        else tma_load_2d(st, &tmS, &sready[sl].b, k0 + 32 * rank, 0);      // b cols, MN-major
+        else tma_load_2d(st, &tmS, &sready[sl].b, k0 + 32 * rank, (m0 / grp_rows) * grp_r);  // b cols, MN-major
       }
       }
     } else if (lane == 1) {
@@ -1753,7 +1785,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
           if (warp == 0 && lane == 0) {
             for (int b = 3 * batch; b < 3 * batch + 3; ++b)
               for (int rr = 0; rr < 128 && (b >> 1) * 128 + rr < BNT; rr += OUT_ROWS)
-                tma_store_2d(&tmOut, stage_buf(b) + rr * 128, em0 + 64 * (b & 1), el0 + 128 * (b >> 1) + rr);
+                store_out(stage_buf(b) + rr * 128, em0 + 64 * (b & 1), el0 + 128 * (b >> 1) + rr);
             tma_store_commit();
             tma_store_wait_all();                      // the blocks are rewritten next
           }
@@ -1829,8 +1861,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(rg::threads<SP>(), 1
       fence_proxy_async_smem();
       named_bar_sync(1, XFORM_THREADS);
       if (warp == 0 && lane == 0) {
-        tma_store_2d(&tmOut, stg + (c * 2) * 16384, m0, l0 + 128 * c);
-        tma_store_2d(&tmOut, stg + (c * 2 + 1) * 16384, m0 + 64, l0 + 128 * c);
+        store_out(stg + (c * 2) * 16384, m0, l0 + 128 * c);
+        store_out(stg + (c * 2 + 1) * 16384, m0 + 64, l0 + 128 * c);
         tma_store_commit();
       }
     }
@@ -1906,25 +1938,29 @@ static TailSplit plan_tail_split(int L, int R, int C) {
 template <bool DX, int RP, bool SP>
 static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const bf16* b, const bf16* bias,
                             const uint32_t* bits, const uint8_t* meta24, bf16* out, int L, int R, int C, int r,
-                            float alpha, cudaStream_t s, void* ws, size_t ws_bytes) {
+                            float alpha, cudaStream_t s, void* ws, size_t ws_bytes, int groups = 1) {
   using namespace rg;
-  const int Mout = DX ? C : R, Kred = DX ? R : C;
+  // groups > 1 (forward only): R rows per projection, W / a / b / out of the G projections consecutive
+  const int G = DX ? 1 : groups, Rt = R * G;
+  const int Mout = DX ? C : Rt, Kred = DX ? R : C;
   constexpr int N2 = n2<SP>(), BNT = bnt<SP>();
   CUtensorMap tAct, tAct2, tW, tS, tF, tOut;
   int st;
   if ((st = make_map(&tAct, act, Kred, L, 64, 128, 128, "activation"))) return st;
   if ((st = make_map(&tAct2, act, Kred, L, 64, N2 ? N2 / 2 : 128, 128, "activation (second MMA)"))) return st;
   if (DX) st = make_map(&tW, w, C, R, 64, 64, 128, "W (dX)");
-  else st = make_map(&tW, w, C, R, 64, 128, 128, "W (fwd)");
+  else st = make_map(&tW, w, C, Rt, 64, 128, 128, "W (fwd)");
   if (st) return st;
   if (DX) {
     if ((st = make_map(&tS, a, r, R, RP, 32, RP * 2, "a (streamed half)"))) return st;
     if ((st = make_map(&tF, b, C, r, 64, RP, 128, "b (fixed)"))) return st;
   } else {
-    if ((st = make_map(&tS, b, C, r, 32, RP, 64, "b (streamed half)"))) return st;
-    if ((st = make_map(&tF, a, r, R, RP, 128, RP * 2, "a (fixed)"))) return st;
+    if ((st = make_map(&tS, b, C, (uint64_t)r * G, 32, RP, 64, "b (streamed half)"))) return st;
+    if ((st = make_map(&tF, a, r, Rt, RP, 128, RP * 2, "a (fixed)"))) return st;
   }
-  if ((st = make_map(&tOut, out, Mout, L, 64, out_rows<SP>(), 128, "output"))) return st;  // [tokens][64 features] SW128
+  if (G > 1) st = make_map_3d(&tOut, out, R, L, G, 64, out_rows<SP>(), 128, "grouped output");
+  else st = make_map(&tOut, out, Mout, L, 64, out_rows<SP>(), 128, "output");  // [tokens][64 features] SW128
+  if (st) return st;
   // 2:4 metadata boxes ([R, C/8] bytes, 128 rows x 16 bytes): a TMA row pitch is a multiple of
   // 16 bytes, so C % 128 == 0; other widths derive the nibbles on chip from W instead
   CUtensorMap tMeta = tW;
@@ -1949,7 +1985,7 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
   if (persist<SP>()) {  // one CTA pair per co-resident cluster slot, tiles walked in the raster order
     const int mc = persistent_clusters<DX, RP, SP>();
     int units = n_f * n_t;
-    const TailSplit ts = plan_tail_split<DX, RP, SP>(L, R, C);
+    const TailSplit ts = plan_tail_split<DX, RP, SP>(L, Rt, C);
     if (ts.split > 1 && ts.clusters == mc && ws != nullptr && ws_bytes >= ts.bytes) {
       split = ts.split;
       counters = (unsigned int*)ws;
@@ -1972,7 +2008,7 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
   }
   kern<<<grid, threads<SP>(), smem, s>>>(tAct, tAct2, tW, tS, tF, tOut, tMeta, bias, bits, SP ? meta24 : nullptr,
                                          (int)ceil_div(C, 32), Mout, Kred, n_t, n_f, split, partials, counters,
-                                         alpha, L);
+                                         alpha, L, DX ? Mout : R, G > 1 ? r : 0);
   LORS_CHECK_LAUNCH(DX ? "tc_lors_gemm<dx>" : "tc_lors_gemm<fwd>");
   return LORS_OK;
 }
@@ -1980,14 +2016,17 @@ static int launch_lors_gemm(const bf16* act, const bf16* w, const bf16* a, const
 template <bool DX, bool SP = false>
 static int lors_gemm(int rp, const bf16* act, const bf16* w, const bf16* a, const bf16* b, const bf16* bias,
                      const uint32_t* bits, bf16* out, int L, int R, int C, int r, float alpha, cudaStream_t s,
-                     void* ws, size_t ws_bytes, const uint8_t* meta24 = nullptr) {
+                     void* ws, size_t ws_bytes, const uint8_t* meta24 = nullptr, int groups = 1) {
   switch (rp) {
     case 16:
-      return launch_lors_gemm<DX, 16, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s, ws, ws_bytes);
+      return launch_lors_gemm<DX, 16, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s, ws, ws_bytes,
+                                          groups);
     case 32:
-      return launch_lors_gemm<DX, 32, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s, ws, ws_bytes);
+      return launch_lors_gemm<DX, 32, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s, ws, ws_bytes,
+                                          groups);
     default:
-      return launch_lors_gemm<DX, 64, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s, ws, ws_bytes);
+      return launch_lors_gemm<DX, 64, SP>(act, w, a, b, bias, bits, meta24, out, L, R, C, r, alpha, s, ws, ws_bytes,
+                                          groups);
   }
 }
 
@@ -2016,7 +2055,7 @@ static int launch_weff_export(const bf16* w, const bf16* a, const bf16* b, const
   dim3 grid((unsigned)(2 * std::min(n_f, mc)));
   // the activation maps are never read in export mode (W's map stands in)
   kern<<<grid, threads<false>(), smem, s>>>(tW, tW, tW, tS, tF, tOut, tW, nullptr, bits, nullptr, (int)ceil_div(C, 32), R,
-                                            C, /*n_t=*/1, n_f, /*split=*/1, nullptr, nullptr, alpha, 0);
+                                            C, /*n_t=*/1, n_f, /*split=*/1, nullptr, nullptr, alpha, 0, R, 0);
   LORS_CHECK_LAUNCH("tc_lors_gemm<export>");
   return LORS_OK;
 }
@@ -2489,6 +2528,26 @@ int tc_fwd(const lors_fwd_args* A, cudaStream_t s) {
   if (A->flags & LORS_FLAG_EMIT_P)  // P = X_t b^T: A = X_t K-major, B = b [r, C] K-major
     st = skinny<false, false, 0>(rp, x, b, A->p, L, r, C, r, 1.0f, false, s);
   return st;
+}
+
+// Grouped forward: G projections of one input X as ONE persistent launch over their G * R / 256
+// pair tiles (the tiles of all projections share the rounds, instead of each projection's
+// partial last round).  Same per-tile arithmetic as tc_fwd, so every Y_g is bit-identical to
+// its own lors_fwd.  Shapes: tc_fwd_group_ok.
+bool tc_fwd_group_ok(const lors_fwd_args* A, int groups) {
+  return groups >= 1 && A->dtype == LORS_DTYPE_BF16 && A->mask_mode == LORS_MASK_FROM_W && A->bias == nullptr &&
+         !(A->flags & (LORS_FLAG_SPARSE24 | LORS_FLAG_EMIT_P)) && tc_shape_ok(A->R, A->C, A->r) &&
+         A->R % 256 == 0 && pad_rank((int)A->r) == A->r;
+}
+size_t tc_fwd_group_workspace(const lors_fwd_args* A, int groups) {
+  if (A->L <= 0 || !tc_fwd_group_ok(A, groups)) return 0;
+  return lors_gemm_workspace<false>((int)A->r, (int)A->L, (int)(A->R * groups), (int)A->C);
+}
+int tc_fwd_group(const lors_fwd_args* A, int groups, cudaStream_t s) {
+  const int L = (int)A->L, R = (int)A->R, C = (int)A->C, r = (int)A->r;
+  return lors_gemm<false>(r, (const bf16*)A->x, (const bf16*)A->w, (const bf16*)A->a, (const bf16*)A->b, nullptr,
+                          nullptr, (bf16*)A->y, L, R, C, r, A->alpha, s, A->workspace, A->workspace_bytes, nullptr,
+                          groups);
 }
 
 int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {

@@ -6,6 +6,9 @@ namespace lors {
 size_t tc_fwd_workspace(const lors_fwd_args* a);
 size_t tc_bwd_workspace(const lors_bwd_args* a);
 int tc_fwd(const lors_fwd_args* a, cudaStream_t s);
+bool tc_fwd_group_ok(const lors_fwd_args* a, int groups);
+size_t tc_fwd_group_workspace(const lors_fwd_args* a, int groups);
+int tc_fwd_group(const lors_fwd_args* a, int groups, cudaStream_t s);
 int tc_bwd(const lors_bwd_args* a, cudaStream_t s);
 bool tc_shape_ok(int64_t R, int64_t C, int64_t r);
 // fp32 parity mode on the tensor cores (3xTF32): forward (dx = false, act = X_t) or dX (act = dY_t);

@@ -28,7 +28,7 @@ from torch import nn
 
 from . import ops
 from .errors import ArgumentError
-from .module import LoRSLinear, groupable, lors_group
+from .module import LoRSLinear, groupable, lors_group, pack_group_weights
 from .prune import prune_rowwise, prune_two_four
 
 PROJECTIONS = ("q", "k", "v", "o", "gate", "up", "down")
@@ -266,6 +266,10 @@ class DecoderLayer(nn.Module):
         qo, ko, vo = lors_group(qkv, x) if groupable(qkv) else (m(x) for m in qkv)
         q = rope_heads(qo.view(B, S, cfg.n_heads, cfg.head_dim), cos, sin)
         k = rope_heads(ko.view(B, S, cfg.n_kv_heads, cfg.head_dim), cos, sin)
+        if vo._base is not None:
+            # a grouped launch's outputs share one buffer: attention saves v, so v gets its own
+            # storage and the buffer is freed with q / k once they are rotated (peak HBM unchanged)
+            vo = vo.clone()
         v = vo.view(B, S, cfg.n_kv_heads, cfg.head_dim).transpose(1, 2)
         att = F.scaled_dot_product_attention(q, k, v, is_causal=True,
                                              enable_gqa=cfg.n_kv_heads != cfg.n_heads)
@@ -333,6 +337,12 @@ class LoRSDecoder(nn.Module):
                 w = prune_two_four(w) if cfg.sparsity == "two_four" else prune_rowwise(w, cfg.ratio)
                 linears[name] = factory(w, cfg.rank, f"layers.{i}.{name}")
                 del w
+            for grp in (("q", "k", "v"), ("gate", "up")):
+                # one [G R, C] buffer per group of equal-shape projections, so their forward can run
+                # as one grouped launch (module.packed_weights)
+                ms = [linears[n] for n in grp]
+                if all(isinstance(m, LoRSLinear) and m.weight.is_cuda for m in ms):
+                    pack_group_weights(ms)
             layers.append(DecoderLayer(cfg, linears, dev))
         self.layers = nn.ModuleList(layers)
         self.norm = RMSNorm(cfg.dim, cfg.eps, cfg.dtype, dev)

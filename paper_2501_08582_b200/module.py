@@ -155,19 +155,29 @@ class LoRSGroupFunction(torch.autograd.Function):
         ab = [(compute_copy(As[i], dt), compute_copy(Bs[i], dt)) for i in range(n)]
         bc = [None if biases[i] is None else biases[i].detach().to(dt).contiguous() for i in range(n)]
         main = torch.cuda.current_stream(dev)
-        streams, _ = ops.group_streams(dev, n)
-        fork = torch.cuda.Event()
-        fork.record(main)
-        keep, outs = [], []
-        for i, prm in enumerate(params_list):
-            streams[i].wait_event(fork)
-            y, _ = ops.lors_fwd(x2, weights[i], ab[i][0], ab[i][1], prm.alpha, bc[i], prm.mask_bits,
-                                sparse24=prm.sparse24, meta24=prm.meta24 if prm.sparse24 else None,
-                                launch_stream=streams[i], keep=keep)
-            outs.append(y.view(*shape[:-1], weights[i].shape[0]))
-        for i in range(n):
+        w_cat = packed_weights(weights, biases, As, params_list)
+        keep, outs, streams = [], [], ()
+        if w_cat is not None:
+            # one persistent launch over every projection's tiles (lors_fwd_group), on the main
+            # stream; outputs bit-identical to the per-projection launches
+            a_cat = torch.cat([ab[i][0] for i in range(n)])
+            b_cat = torch.cat([ab[i][1] for i in range(n)])
+            y = ops.lors_fwd_group(x2, w_cat, a_cat, b_cat, n, params_list[0].alpha)
+            outs = [y[i].view(*shape[:-1], weights[i].shape[0]) for i in range(n)]
+        else:
+            streams, _ = ops.group_streams(dev, n)
+            streams = streams[:n]
+            fork = torch.cuda.Event()
+            fork.record(main)
+            for i, prm in enumerate(params_list):
+                streams[i].wait_event(fork)
+                y, _ = ops.lors_fwd(x2, weights[i], ab[i][0], ab[i][1], prm.alpha, bc[i], prm.mask_bits,
+                                    sparse24=prm.sparse24, meta24=prm.meta24 if prm.sparse24 else None,
+                                    launch_stream=streams[i], keep=keep)
+                outs.append(y.view(*shape[:-1], weights[i].shape[0]))
+        for st in streams:
             ev = torch.cuda.Event()
-            ev.record(streams[i])
+            ev.record(st)
             main.wait_event(ev)
         # keep / ab / bc were allocated on the main stream and are released after the
         # joins are enqueued there, so no later main-stream reuse can overtake the GEMMs
@@ -261,6 +271,43 @@ def no_grouping():
         yield
     finally:
         _GROUPING[0] = prev
+
+
+def packed_weights(weights, biases, As, params_list) -> Optional[torch.Tensor]:
+    """[G R, C] storage holding `weights` back to back (pack_group_weights) when the projections
+    can run as one grouped launch (lors_fwd_group: bf16, masks from W, no bias / 2:4, equal alpha,
+    R % 256 == 0, r in {16, 32, 64}), else None."""
+    if os.environ.get("LORS_GROUP_FWD", "1") == "0":
+        return None
+    w0 = weights[0]
+    base = w0._base
+    n = len(weights)
+    R, C = w0.shape
+    r = As[0].shape[1]
+    if (base is None or w0.dtype != torch.bfloat16 or R % 256 or r not in (16, 32, 64) or C % 8
+            or tuple(base.shape) != (n * R, C) or not base.is_contiguous()):
+        return None
+    for i, (w, bias, a, prm) in enumerate(zip(weights, biases, As, params_list)):
+        if (w._base is not base or tuple(w.shape) != (R, C) or w.data_ptr() != base.data_ptr() + i * R * C * 2
+                or bias is not None or a.shape[1] != r or prm.mask_bits is not None or prm.sparse24
+                or prm.alpha != params_list[0].alpha):
+            return None
+    return base
+
+
+def pack_group_weights(layers) -> bool:
+    """Move the frozen weights of `layers` (projections of one input with equal shapes) into one
+    [G R, C] buffer, each layer's `weight` becoming its row slice, so LoRSGroupFunction can run
+    them as one grouped launch.  Values, shapes and state_dict names are unchanged."""
+    ws = [m.weight for m in layers]
+    if len(ws) < 2 or any(tuple(w.shape) != tuple(ws[0].shape) or w.dtype != ws[0].dtype or w.device != ws[0].device
+                          for w in ws):
+        return False
+    buf = torch.cat(ws)
+    R = ws[0].shape[0]
+    for i, m in enumerate(layers):
+        m._buffers["weight"] = buf[i * R:(i + 1) * R]
+    return True
 
 
 def groupable(layers) -> bool:

@@ -121,6 +121,38 @@ def lors_fwd(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tenso
     return y, p
 
 
+def lors_fwd_group(x_t: torch.Tensor, w: torch.Tensor, a: torch.Tensor, b: torch.Tensor, groups: int,
+                   alpha: float = 2.0, launch_stream=None, keep: Optional[list] = None) -> torch.Tensor:
+    """Y [G, L, R] of G projections of the same X_t in one launch (lors_fwd_group): w [G R, C],
+    a [G R, r], b [G r, C] hold the projections consecutively (bf16, masks from W, no bias).
+    Y[g] is bit-identical to lors_fwd(x_t, w[g R:(g+1) R], a[g R:(g+1) R], b[g r:(g+1) r])."""
+    G = int(groups)
+    if G < 1 or w.dim() != 2 or w.shape[0] % G or b.shape[0] % G:
+        raise ShapeError(f"w {tuple(w.shape)} / b {tuple(b.shape)} do not split into {groups} projections")
+    R, C, r = w.shape[0] // G, w.shape[1], b.shape[0] // G
+    L = x_t.shape[0]
+    dt = w.dtype
+    for t, nm, sh in ((x_t, "x", (L, C)), (w, "w", (G * R, C)), (a, "a", (G * R, r)), (b, "b", (G * r, C))):
+        _need(t, nm, sh, dt)
+    y = torch.empty((G, L, R), dtype=dt, device=w.device)
+    args = N.FwdArgs()
+    args.L, args.R, args.C, args.r = L, R, C, r
+    args.dtype = dtype_code(dt)
+    args.mask_mode = N.MASK_FROM_W
+    args.flags = 0
+    args.alpha = float(alpha)
+    args.x, args.w, args.a, args.b, args.y = _p(x_t), _p(w), _p(a), _p(b), _p(y)
+    lib = N.load()
+    ws_bytes = lib.lors_fwd_group_workspace(ct.byref(args), G)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=w.device) if ws_bytes else None
+    args.workspace, args.workspace_bytes = _p(ws), ws_bytes
+    if keep is not None and ws is not None:
+        keep.append(ws)
+    st = _stream() if launch_stream is None else ct.c_void_p(launch_stream.cuda_stream)
+    N.check(lib.lors_fwd_group(ct.byref(args), G, st))
+    return y
+
+
 _GROUP_STREAMS = {}
 
 

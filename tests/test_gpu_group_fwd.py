@@ -1,0 +1,79 @@
+"""GPU: the grouped forward (lors_fwd_group) -- G projections of one input in one persistent launch --
+gives every projection's output bit for bit as its own lors_fwd (the same tiles, recompute and
+weff_pair), masks stay exact, and the argument checks of the C ABI hold.  Per projection the
+arithmetic is lors_forward (adapters.py:359-373), checked against the float64 oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import lors_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ops():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2501_08582_b200 import ops
+    return ops
+
+
+def _group(G, R, C, r, seed):
+    from paper_2501_08582_b200 import prune
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    w = prune.prune_rowwise(torch.randn(G * R, C, device="cuda", generator=g) * 0.05, 0.5).bfloat16()
+    a = (torch.randn(G * R, r, device="cuda", generator=g) * 0.05).bfloat16()
+    b = (torch.randn(G * r, C, device="cuda", generator=g) / r ** 0.5).bfloat16()
+    return w, a, b
+
+
+@pytest.mark.parametrize("G,R,C,r,L", [(3, 256, 128, 16, 300), (2, 512, 320, 32, 384), (3, 256, 256, 64, 1000),
+                                       (2, 768, 192, 16, 1), (4, 256, 64, 16, 130)])
+@pytest.mark.parametrize("alpha", [2.0, 1.0 / 3.0])
+def test_group_matches_per_projection_bitwise(ops, G, R, C, r, L, alpha):
+    w, a, b = _group(G, R, C, r, seed=G * 1000 + R + C + r + L)
+    x = torch.randn(L, C, device="cuda").bfloat16()
+    y = ops.lors_fwd_group(x, w, a, b, G, alpha)
+    assert y.shape == (G, L, R)
+    for i in range(G):
+        yi, _ = ops.lors_fwd(x, w[i * R:(i + 1) * R].contiguous(), a[i * R:(i + 1) * R].contiguous(),
+                             b[i * r:(i + 1) * r].contiguous(), alpha)
+        assert torch.equal(y[i], yi), f"projection {i} differs from its own lors_fwd"
+
+
+def test_group_against_oracle_and_mask(ops):
+    G, R, C, r, L = 3, 256, 192, 16, 200
+    w, a, b = _group(G, R, C, r, seed=7)
+    x = torch.randn(L, C, device="cuda").bfloat16()
+    y = ops.lors_fwd_group(x, w, a, b, G, 2.0).float().cpu().numpy()
+    xf = x.float().cpu().numpy().astype(np.float64)
+    for i in range(G):
+        wi = w[i * R:(i + 1) * R].float().cpu().numpy().astype(np.float64)
+        ai = a[i * R:(i + 1) * R].float().cpu().numpy().astype(np.float64)
+        bi = b[i * r:(i + 1) * r].float().cpu().numpy().astype(np.float64)
+        ref = orc.lors_forward(wi, ai, bi, xf.T, 2.0).T
+        err = np.linalg.norm(y[i] - ref) / np.linalg.norm(ref)
+        assert err <= 2e-2, f"projection {i}: rel-L2 {err}"
+    # identity input: Y = W_eff^T rows -> exactly +0 wherever W == 0
+    eye = torch.eye(C, device="cuda").bfloat16()
+    ye = ops.lors_fwd_group(eye, w, a, b, G, 2.0)
+    for i in range(G):
+        weff_t = ye[i]                                   # [C, R] = W_eff^T
+        zero = (w[i * R:(i + 1) * R] == 0).T
+        assert torch.all(weff_t[zero].view(torch.int16) == 0)
+
+
+def test_group_argument_checks(ops):
+    from paper_2501_08582_b200.errors import ArgumentError, ShapeError
+    w, a, b = _group(2, 200, 128, 16, seed=1)            # R % 256 != 0
+    x = torch.randn(64, 128, device="cuda").bfloat16()
+    with pytest.raises(ArgumentError):
+        ops.lors_fwd_group(x, w, a, b, 2, 2.0)
+    w, a, b = _group(2, 256, 128, 24, seed=2)            # r not 16 / 32 / 64
+    with pytest.raises(ArgumentError):
+        ops.lors_fwd_group(x, w, a, b, 2, 2.0)
+    w, a, b = _group(2, 256, 128, 16, seed=3)
+    with pytest.raises(ShapeError):
+        ops.lors_fwd_group(x, w, a, b[:-1], 2, 2.0)
