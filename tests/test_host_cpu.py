@@ -106,3 +106,28 @@ def test_fit_rank_r_rows_matches_reference_svd_fixtures():
             b = fit_rank_r_rows(dw, r, exact_limit=lim)
             np.testing.assert_allclose(b.double().numpy(), d[f"s{i}_b"], atol=2e-5)
         assert abs(singular_tail(dw, r) - float(d[f"s{i}_tail"])) < 1e-9
+
+
+def test_pack_group_weights_host_logic():
+    """pack_group_weights moves equal-shape frozen weights into one [G R, C] buffer (values, shapes and
+    state_dict names unchanged); packed_weights accepts exactly the layouts lors_fwd_group can run."""
+    import torch
+    from paper_2501_08582_b200.module import LoRSLinear, pack_group_weights, packed_weights
+    g = torch.Generator().manual_seed(0)
+    ws = [torch.randn(256, 64, generator=g).bfloat16() for _ in range(3)]
+    ls = [LoRSLinear(w, rank=16) for w in ws]
+    before = [m.weight.clone() for m in ls]
+    keys = [sorted(m.state_dict()) for m in ls]
+    assert pack_group_weights(ls)
+    base = ls[0].weight._base
+    assert base is not None and tuple(base.shape) == (768, 64)
+    assert all(m.weight._base is base for m in ls)
+    assert all(torch.equal(m.weight, w) for m, w in zip(ls, before))
+    assert [sorted(m.state_dict()) for m in ls] == keys
+    args = ([m.weight for m in ls], [None] * 3, [m.a for m in ls], [m.params() for m in ls])
+    assert packed_weights(*args) is base
+    assert packed_weights(args[0][:2], args[1][:2], args[2][:2], args[3][:2]) is None      # not the whole buffer
+    assert packed_weights(args[0], [None, torch.zeros(256), None], args[2], args[3]) is None   # bias
+    # unequal shapes are left alone
+    assert not pack_group_weights([LoRSLinear(torch.randn(256, 64).bfloat16(), rank=16),
+                                   LoRSLinear(torch.randn(512, 64).bfloat16(), rank=16)])
