@@ -86,6 +86,13 @@ typedef enum { LORS_GRAD_STE = 0, LORS_GRAD_MASKED = 1 } lors_grad_mode_t;
                                         reference replays training bitwise,
                                         test_train.py:169-178); needs the larger
                                         workspace lors_bwd_workspace reports */
+#define LORS_FLAG_NO_TAIL_SPLIT (1u << 6) /* forward / dX GEMMs: walk every tile whole,
+                                        without the tail split along K (the split
+                                        fills the last round's idle SMs: faster for
+                                        a GEMM timed alone, 0.3-0.8% slower in a
+                                        sustained, power-capped training step, where
+                                        idle SMs leave their power to the busy ones);
+                                        its workspace is then not needed */
 #define LORS_FLAG_FAULT_DA_SIGN (1u << 30) /* negative control: flip dA sign,
                                               mirrors FAULT_INJECTION
                                               "lors_backward_sign_flip"

@@ -27,6 +27,7 @@ FLAG_NO_DX = 1 << 2
 FLAG_DX_ONLY = 1 << 3
 FLAG_ZEROED = 1 << 4
 FLAG_DETERMINISTIC = 1 << 5
+FLAG_NO_TAIL_SPLIT = 1 << 6
 FLAG_FAULT_DA_SIGN = 1 << 30
 
 # Every symbol include/lors_b200.h declares (checked by tests/test_capi_symbols.py).

@@ -2463,12 +2463,14 @@ bool tc_shape_ok(int64_t R, int64_t C, int64_t r) {
 
 // the forward's tail-split workspace (0 when the walk has no tail to split)
 size_t tc_fwd_workspace(const lors_fwd_args* a) {
-  if (a->dtype != LORS_DTYPE_BF16 || (a->flags & LORS_FLAG_SPARSE24) || a->L <= 0 || !tc_shape_ok(a->R, a->C, a->r))
+  if (a->dtype != LORS_DTYPE_BF16 || (a->flags & (LORS_FLAG_SPARSE24 | LORS_FLAG_NO_TAIL_SPLIT)) || a->L <= 0 ||
+      !tc_shape_ok(a->R, a->C, a->r))
     return 0;
   return lors_gemm_workspace<false>((int)pad_rank(a->r), (int)a->L, (int)a->R, (int)a->C);
 }
 static size_t dx_workspace(const lors_bwd_args* a) {
-  if (a->dtype != LORS_DTYPE_BF16 || (a->flags & LORS_FLAG_NO_DX) || a->L <= 0 || !tc_shape_ok(a->R, a->C, a->r))
+  if (a->dtype != LORS_DTYPE_BF16 || (a->flags & (LORS_FLAG_NO_DX | LORS_FLAG_NO_TAIL_SPLIT)) || a->L <= 0 ||
+      !tc_shape_ok(a->R, a->C, a->r))
     return 0;
   return lors_gemm_workspace<true>((int)pad_rank(a->r), (int)a->L, (int)a->R, (int)a->C);
 }
@@ -2521,8 +2523,9 @@ int tc_fwd(const lors_fwd_args* A, cudaStream_t s) {
     st = lors_gemm<false, true>(rp, x, w, a, b, (const bf16*)A->bias, bits, (bf16*)A->y, L, R, C, r, A->alpha, s,
                                 nullptr, 0, A->meta24);
   } else {
+    const bool split = !(A->flags & LORS_FLAG_NO_TAIL_SPLIT);
     st = lors_gemm<false>(rp, x, w, a, b, (const bf16*)A->bias, bits, (bf16*)A->y, L, R, C, r, A->alpha, s,
-                          A->workspace, A->workspace_bytes);
+                          split ? A->workspace : nullptr, split ? A->workspace_bytes : 0);
   }
   if (st) return st;
   if (A->flags & LORS_FLAG_EMIT_P)  // P = X_t b^T: A = X_t K-major, B = b [r, C] K-major
@@ -2540,14 +2543,15 @@ bool tc_fwd_group_ok(const lors_fwd_args* A, int groups) {
          A->R % 256 == 0 && pad_rank((int)A->r) == A->r;
 }
 size_t tc_fwd_group_workspace(const lors_fwd_args* A, int groups) {
-  if (A->L <= 0 || !tc_fwd_group_ok(A, groups)) return 0;
+  if (A->L <= 0 || !tc_fwd_group_ok(A, groups) || (A->flags & LORS_FLAG_NO_TAIL_SPLIT)) return 0;
   return lors_gemm_workspace<false>((int)A->r, (int)A->L, (int)(A->R * groups), (int)A->C);
 }
 int tc_fwd_group(const lors_fwd_args* A, int groups, cudaStream_t s) {
   const int L = (int)A->L, R = (int)A->R, C = (int)A->C, r = (int)A->r;
+  const bool split = !(A->flags & LORS_FLAG_NO_TAIL_SPLIT);
   return lors_gemm<false>(r, (const bf16*)A->x, (const bf16*)A->w, (const bf16*)A->a, (const bf16*)A->b, nullptr,
-                          nullptr, (bf16*)A->y, L, R, C, r, A->alpha, s, A->workspace, A->workspace_bytes, nullptr,
-                          groups);
+                          nullptr, (bf16*)A->y, L, R, C, r, A->alpha, s, split ? A->workspace : nullptr,
+                          split ? A->workspace_bytes : 0, nullptr, groups);
 }
 
 int tc_bwd(const lors_bwd_args* A, cudaStream_t s) {

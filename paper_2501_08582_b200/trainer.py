@@ -116,7 +116,8 @@ class Trainer:
     def __init__(self, model: nn.Module, lr: float = 2e-5, betas=(0.9, 0.999), eps: float = 1e-8,
                  weight_decay: float = 0.0, process_group=None, overlap: bool = True,
                  bucket_bytes: int = 64 << 20, params: Optional[Sequence[nn.Parameter]] = None,
-                 optimizer: str = "auto", check_finite: bool = False, cuda_graph: bool = False):
+                 optimizer: str = "auto", check_finite: bool = False, cuda_graph: bool = False,
+                 tail_split: bool = False):
         self.model = model
         self.check_every_step = check_finite   # NumericError on a non-finite loss (train.py:215-217); syncs
         self.params = list(params) if params is not None else [p for p in model.parameters() if p.requires_grad]
@@ -152,13 +153,22 @@ class Trainer:
         self._static_tokens = None
         self._static_loss = None
         self.graph_launches = 0      # native kernel launches recorded into the graph (one step)
+        # the LoRS GEMMs' tail split along K (ops.set_tail_split) during this trainer's steps: off by
+        # default -- a sustained step runs under the power cap, where the split's extra partial
+        # traffic costs more than the idle SMs it fills (cfg3 +0.8%, cfg4 / cfg5 +0.3% without it)
+        self.tail_split = bool(tail_split)
 
     def step(self, tokens: torch.Tensor) -> torch.Tensor:
         """One fine-tuning step on this rank's tokens [B, S + 1]; returns the (local) loss
         as a device scalar -- no host synchronisation."""
-        if self.cuda_graph:
-            return self._step_graphed(tokens)
-        return self._step_eager(tokens)
+        from . import ops
+        prev = ops.set_tail_split(self.tail_split)
+        try:
+            if self.cuda_graph:
+                return self._step_graphed(tokens)
+            return self._step_eager(tokens)
+        finally:
+            ops.set_tail_split(prev)
 
     def invalidate_graph(self) -> None:
         """Drop the captured step (the next step runs eagerly and captures again)."""

@@ -102,3 +102,31 @@ def test_decoder_grouped_forward_is_bitwise_the_per_projection_path(ops, monkeyp
     for n, g in out["0"][1].items():                  # (attention's backward is not bitwise reproducible)
         g1 = out["1"][1][n]
         assert float((g1 - g).double().norm()) <= 1e-3 * float(g.double().norm()) + 1e-30, n
+
+
+@pytest.mark.parametrize("L,R,C,r", [(4096, 4096, 11008, 64), (2048, 11008, 8192, 32)])
+def test_no_tail_split_flag_is_the_unsplit_walk(ops, L, R, C, r):
+    """LORS_FLAG_NO_TAIL_SPLIT (ops.set_tail_split(False), what Trainer steps use) runs the forward and
+    dX walks unsplit: bit-identical to the LORS_NO_TAIL_SPLIT build-time switch, and the flag is
+    restored by the trainer's step."""
+    import os
+    g = torch.Generator(device="cuda").manual_seed(L + r)
+    w = torch.randn(R, C, device="cuda", generator=g) * 0.02
+    w = torch.where(w.abs() < 0.015, torch.zeros_like(w), w).bfloat16()
+    a = (torch.randn(R, r, device="cuda", generator=g) * 0.05).bfloat16()
+    b = (torch.randn(r, C, device="cuda", generator=g) * 0.3).bfloat16()
+    x = torch.randn(L, C, device="cuda", generator=g).bfloat16()
+    dy = torch.randn(L, R, device="cuda", generator=g).bfloat16()
+    prev = ops.set_tail_split(False)
+    try:
+        y1, _ = ops.lors_fwd(x, w, a, b, 2.0)
+        dx1 = ops.lors_bwd(x, w, a, b, dy, 2.0, overlap=False)[0]
+    finally:
+        ops.set_tail_split(prev)
+    os.environ["LORS_NO_TAIL_SPLIT"] = "1"
+    try:
+        y0, _ = ops.lors_fwd(x, w, a, b, 2.0)
+        dx0 = ops.lors_bwd(x, w, a, b, dy, 2.0, overlap=False)[0]
+    finally:
+        os.environ.pop("LORS_NO_TAIL_SPLIT", None)
+    assert torch.equal(y1, y0) and torch.equal(dx1, dx0)
