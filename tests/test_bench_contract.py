@@ -25,6 +25,22 @@ def test_reference_arm_json_line():
     assert "workload" in d["config"]
 
 
+
+def test_reference_arm_two_ranks_self_launch():
+    """`--gpus 2` without torchrun's environment relaunches itself as two ranks (torch.distributed.run on
+    127.0.0.1); rank 0 alone prints the line with n_gpus 2, rank 1 exits 0 -- the launcher path the
+    driver's scaling run uses, exercised on the CPU arm."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "cfg1",
+                          "--gpus", "2", "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["config"]["parallelism"] == "dp2"
+
+
 import pytest  # noqa: E402
 
 
