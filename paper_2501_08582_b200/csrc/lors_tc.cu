@@ -10,8 +10,10 @@
 //        which the main MMA consumes.  W_eff never touches HBM.
 //        Dense kernels: 256 features x 384 tokens per CTA pair (two accumulators),
 //        persistent over the tile raster, the last wave's tiles optionally cut
-//        along K (tail split); the 2:4 kernel (tcgen05.mma.sp) keeps 256-token
-//        tiles, one per launch.  DESIGN.md section 3 has the pipeline.
+//        along K (tail split, off under LORS_FLAG_NO_TAIL_SPLIT); the 2:4 kernel
+//        (tcgen05.mma.sp) runs the same persistent 384-token walk.  Grouped forward
+//        (lors_fwd_group): the pair tiles of G projections of one X in one walk, the
+//        outputs through a 3-D [G][L][R] TMA map.  DESIGN.md section 4 has the pipeline.
 //   K4 tc_skinny            rank-r products P = X b^T and dB = alpha Q^T X
 //        (adapters.py:396, 399), N = r, split-K into fp32 accumulators.
 //   K4b tc_q_da             Q = dY a and dA = alpha dY^T P from one pass over dY
